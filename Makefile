@@ -1,0 +1,49 @@
+# Builds the product library (sm_100a CUDA + host C++) in-tree, plus the
+# parity checker under oracle/ (test infrastructure).
+NVCC     ?= nvcc
+CXX      ?= g++
+ARCH     := -gencode arch=compute_100a,code=sm_100a
+PKG      := paper_2604_08374_b200
+CSRC     := $(PKG)/csrc
+BUILD    := build
+CUDA_INC := $(dir $(shell which $(NVCC)))../include
+NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v --fmad=false
+CXXFLAGS := -O3 -std=c++17 -fPIC -Wall -ffp-contract=off -I$(CUDA_INC)
+LIB      := $(PKG)/libsieveball_cuda.so
+TOOL     := tools/sb_hyperball
+
+OBJS := $(BUILD)/sb_kernels.o $(BUILD)/sb_runtime.o $(BUILD)/sb_csr.o $(BUILD)/sb_error.o
+HDRS := $(CSRC)/sb_device.cuh $(CSRC)/sb_internal.h $(CSRC)/sb_error.h include/sieveball_cuda.h
+
+all: $(LIB) $(TOOL) oracle
+
+$(BUILD):
+	mkdir -p $(BUILD)
+
+$(BUILD)/sb_kernels.o: $(CSRC)/sb_kernels.cu $(HDRS) | $(BUILD)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(BUILD)/ptxas_kernels.txt || (cat $(BUILD)/ptxas_kernels.txt; false)
+
+$(BUILD)/sb_runtime.o: $(CSRC)/sb_runtime.cu $(HDRS) | $(BUILD)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(BUILD)/ptxas_runtime.txt || (cat $(BUILD)/ptxas_runtime.txt; false)
+
+$(BUILD)/sb_csr.o: $(CSRC)/sb_csr.cpp $(HDRS) | $(BUILD)
+	$(CXX) $(CXXFLAGS) -c $< -o $@
+
+$(BUILD)/sb_error.o: $(CSRC)/sb_error.cpp $(CSRC)/sb_error.h | $(BUILD)
+	$(CXX) $(CXXFLAGS) -c $< -o $@
+
+# cudart is linked statically (nvcc default); NCCL and zlib from the system.
+$(LIB): $(OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lnccl -lz -lpthread
+
+$(TOOL): tools/sb_hyperball.cpp include/sieveball/hyperball_cuda.hpp $(LIB)
+	$(CXX) -O2 -std=c++17 -Wall -Iinclude -o $@ $< -L$(PKG) -lsieveball_cuda -Wl,-rpath,'$$ORIGIN/../$(PKG)'
+
+oracle:
+	$(MAKE) -s -C oracle
+
+clean:
+	rm -rf $(BUILD) $(LIB) $(TOOL)
+	$(MAKE) -C oracle clean
+
+.PHONY: all oracle clean

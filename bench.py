@@ -1,0 +1,415 @@
+#!/usr/bin/env python
+"""bench.py -- HyperBall hot path on B200 (driver contract in the task spec).
+
+A step = one full HyperBall run (init -> iterate until max increase <= 0.5,
+or the depth limit) over the synthetic C3 graph (open 486x486 grid, radius 87
+cells: 236,196 cells, 4.79e9 directed edges, 4.83 GB LEB128 stream), p=10.
+
+  value    edge-register updates/s = iterations * |E| * 2^p / time, CSR and
+           counters resident in HBM, device time (CUDA events on the
+           library's stream), max over ranks.
+  e2e      same metric through the public C-ABI with HOST buffers: CSR upload
+           (pinned H2D) + validation + run + read-back of c / sum_d / sum_d2.
+  roofline the fused decode-union kernel: SURVEY §8(d) algorithmic bytes per
+           launch / its CUDA-event time, against MEASURED_PEAKS.json hbm_gbs.
+  cpu_baseline  the reference's compiled primitives + SPEC loop
+           (oracle/_ref) on this host's cores, bounded sample.
+
+`--impl reference` times only the reference CPU path (rank 0) on the same
+config and prints its own line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (rows, cols, n_rects, rect_min, rect_max, seed, radius2, description)
+    "c1": (64, 64, 20, 2, 9, 20261017, 0, "C1 64x64 grid, 20 rectangles, unlimited radius"),
+    "c2": (215, 215, 60, 3, 10, 20261017, 38 * 38, "C2 215x215 grid, 60 rectangles, radius 38 cells"),
+    "c3": (486, 486, 0, 1, 1, 20261017, 87 * 87, "C3 open 486x486 grid, radius 87 cells"),
+}
+METRIC = "HyperBall edge-register updates/s"
+UNIT = "edge-register updates/s"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy bandwidth)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def build_graph(cfg, threads=0):
+    from paper_2604_08374_b200 import CompressedCsr
+    r, c, k, a, b, seed, rad2, _ = CONFIGS[cfg]
+    t0 = time.perf_counter()
+    g = CompressedCsr.synth_grid(r, c, k, a, b, seed, rad2, threads)
+    log(f"[bench] generated {cfg}: {g} in {time.perf_counter() - t0:.1f} s")
+    return g
+
+
+def alg_bytes_per_iter(n, edges, stream_len, p):
+    """CSR (stream + 8(N+1) + 4N) + |E| m/2 + N m/2 (own) + N m/2 (write)."""
+    row = (1 << p) // 2
+    return stream_len + 8 * (n + 1) + 4 * n + edges * row + 2 * n * row
+
+
+def traffic_from_profile(cfg, p):
+    path = os.path.join(ROOT, "profiles", "union_ncu_summary.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        e = d.get(f"{cfg}_p{p}")
+        return e["dram_bytes_per_launch"] if e else None
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------ CPU (reference) arm
+def cpu_sample(g, p, target_s, threads):
+    """Times iterate_once (t=1) of the reference CPU path over a node sample."""
+    import oracle
+    O = oracle.reference() if oracle.reference_available() else oracle.port()
+    n = g.n
+    cur, c0 = O.hb_init(n, p)
+    nxt = np.zeros_like(cur)
+    c1, sd, sd2 = np.zeros(n), np.zeros(n), np.zeros(n)
+    mid = n // 2
+    k = max(threads, 64)
+    while True:  # calibrate
+        v0, v1 = mid, min(n, mid + k)
+        t0 = time.perf_counter()
+        O.hb_iterate(g, p, 1, cur, nxt, c0, c1, sd, sd2, v0=v0, v1=v1, threads=threads)
+        dt = time.perf_counter() - t0
+        if dt > target_s / 8 or v1 == n:
+            break
+        k *= 4
+    k = min(n - mid, max(1, int(k * target_s / max(dt, 1e-6))))
+    v0, v1 = mid, mid + k
+    edges = int(g.degrees[v0:v1].sum(dtype=np.uint64))
+    return O, (v0, v1), edges, (cur, nxt, c0, c1, sd, sd2)
+
+
+def run_cpu(g, p, target_s, threads, reps=1):
+    O, (v0, v1), edges, bufs = cpu_sample(g, p, target_s, threads)
+    cur, nxt, c0, c1, sd, sd2 = bufs
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        O.hb_iterate(g, p, 1, cur, nxt, c0, c1, sd, sd2, v0=v0, v1=v1, threads=threads)
+        times.append(time.perf_counter() - t0)
+    m = 1 << p
+    return {
+        "value": edges * m / statistics.median(times), "unit": UNIT, "cores": threads, "kind": O.kind,
+        "sample": f"iterate_once (t=1) over nodes [{v0},{v1}) = {v1 - v0} nodes / {edges} edges of the same "
+                  f"graph, p={p}, {threads} threads, median of {reps} ({statistics.median(times):.2f} s)",
+        "seconds": times,
+    }
+
+
+def reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    g = build_graph(args.config)
+    threads = os.cpu_count() or 1
+    import oracle
+    O, (v0, v1), edges, bufs = cpu_sample(g, args.p, args.cpu_step_s, threads)
+    cur, nxt, c0, c1, sd, sd2 = bufs
+    for _ in range(args.warmup):
+        O.hb_iterate(g, args.p, 1, cur, nxt, c0, c1, sd, sd2, v0=v0, v1=v1, threads=threads)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        O.hb_iterate(g, args.p, 1, cur, nxt, c0, c1, sd, sd2, v0=v0, v1=v1, threads=threads)
+        times.append(time.perf_counter() - t0)
+    m = 1 << args.p
+    v = edges * m / statistics.mean(times)
+    cb = {"value": v, "unit": UNIT, "cores": threads, "kind": O.kind,
+          "sample": f"iterate_once (t=1) over nodes [{v0},{v1}) ({v1 - v0} nodes, {edges} edges) of {args.config}"}
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(times),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic", "config": workload_config(args, g, None),
+        "cpu_baseline": cb, "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(args, g, iters):
+    return {
+        "workload": CONFIGS[args.config][7] + f", p={args.p}, depth {'unbounded' if not args.depth else args.depth}",
+        "config": args.config, "nodes": g.n, "edges": g.edges, "stream_bytes": g.stream_len, "p": args.p,
+        "depth_limit": args.depth or None, "iterations": iters,
+        "register_layout": "4-bit bit-sliced (reference density m/2 B per row)",
+        "l2": "inputs larger than L2 (4.8 GB CSR stream read every iteration; 121 MB plane)" if args.config == "c3"
+        else "small graph", "parallelism": f"node-range shards x{args.gpus}",
+    }
+
+
+# ------------------------------------------------------------------ GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--p", type=int, default=10)
+    ap.add_argument("--depth", type=int, default=0)
+    ap.add_argument("--cpu-sample-s", type=float, default=15.0)
+    ap.add_argument("--cpu-step-s", type=float, default=6.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-variants", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (1 run, no extras)")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return reference_arm(args)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2604_08374_b200 import Comm, DeviceGraph, HllParams, HyperBall
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    g = build_graph(args.config, threads=max(1, (os.cpu_count() or 1) // max(world, 1)))
+    P = HllParams(args.p)
+    m = P.m
+    bounds = g.partition(world)
+    v0, v1 = int(bounds[rank]), int(bounds[rank + 1])
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    comm = None
+    if world > 1:
+        uid = [Comm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = Comm(world, rank, uid[0], local)
+
+    def make_hb(skip=False):
+        dg = DeviceGraph(g, local, (v0, v1))
+        hb = HyperBall(dg, P, args.depth or None, skip_unchanged=skip)
+        if comm is not None:
+            hb.attach_comm(comm, bounds)
+        return hb
+
+    t0 = time.perf_counter()
+    hb = make_hb()
+    log(f"[bench] rank {rank}: upload+validate+init {time.perf_counter() - t0:.2f} s, items={hb.graph.n_items} "
+        f"chunk={hb.graph.chunk}")
+    stream = torch.cuda.ExternalStream(hb.stream_handle())
+
+    def one_run(h):
+        h.reset()
+        return h.run()
+
+    for _ in range(args.warmup if not args.profile else 1):
+        iters = one_run(hb)
+    if args.profile:
+        log(f"[bench] profile run done: {iters} iterations")
+        return 0
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    union_ms = []
+    ev0.record(stream)
+    for _ in range(args.steps):
+        iters = one_run(hb)
+        union_ms += [s["union_ms"] for s in hb.stats()]
+    ev1.record(stream)
+    ev1.synchronize()
+    barrier()
+    clock_info = clocks.stop()
+    dev_s = max_over_ranks(ev0.elapsed_time(ev1) / 1e3)
+    st = hb.stats()
+    total_updates = args.steps * iters * g.edges * m
+    value = total_updates / dev_s
+    bytes_iter = alg_bytes_per_iter(g.n, g.edges, g.stream_len, args.p)
+    # roofline of the dominant kernel (rank-local work / rank-local launch time)
+    el = hb.graph.edges_local
+    nl = hb.graph.n_local
+    bytes_launch = hb.graph.stream_bytes_local + 8 * (nl + 1) + 4 * nl + el * P.row_bytes + 2 * nl * P.row_bytes
+    avg_union_s = statistics.mean(union_ms) / 1e3
+    pk, pk_src = peaks()
+    achieved = bytes_launch / avg_union_s / 1e9
+    log(f"[bench] {args.steps} runs x {iters} iterations in {dev_s:.3f} s; union avg {avg_union_s * 1e3:.2f} ms "
+        f"-> {achieved:.0f} GB/s algorithmic")
+    for s in st:
+        log(f"[bench]   t={s['t']} union={s['union_ms']:.2f} ms est={s['estimate_ms']:.3f} ms "
+            f"xchg={s['exchange_ms']:.3f} ms changed={s['changed_nodes']} max_inc={s['max_increase']:.3f}")
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * dev_s / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": workload_config(args, g, iters),
+        "hbm_gbs_algorithmic": bytes_iter * iters * args.steps / dev_s / 1e9,
+        "end_to_end_s_device": dev_s / args.steps,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk, "unit": "GB/s", "frac": achieved / pk,
+                     "traffic": traffic_from_profile(args.config, args.p),
+                     "kernel": f"sb::union_kernel<{args.p},false>",
+                     "bytes_per_launch": bytes_launch, "launch_ms": avg_union_s * 1e3, "peak_source": pk_src,
+                     "note": "algorithmic bytes (SURVEY 8d, packed m/2 rows); most row gathers hit L2"},
+        "per_iteration_ms": [round(s["step_ms"], 3) for s in st],
+        "exchange_ms": [round(s["exchange_ms"], 4) for s in st] if world > 1 else None,
+        "clocks": clock_info,
+        "gpu_launches": args.steps * (2 + 2 * iters),
+    }
+
+    # ---- end to end through the public API with host buffers
+    if not args.no_e2e:
+        g.pin(True)
+        h2d = g.stream_len + 8 * (g.n + 1) + 4 * g.n
+        d2h = 3 * 8 * nl
+        def e2e_once():
+            t = time.perf_counter()
+            dg = DeviceGraph(g, local, (v0, v1))
+            h = HyperBall(dg, P, args.depth or None)
+            if comm is not None:
+                h.attach_comm(comm, bounds)
+            it = h.run()
+            s = h.state()  # D2H c_t, c_(t-1), sum_d, sum_d2, changed
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t
+            del h, dg, s
+            return dt, it
+        e2e_once()
+        barrier()
+        e2e_t = []
+        for _ in range(args.steps):
+            dt, it = e2e_once()
+            e2e_t.append(dt)
+        barrier()
+        e2e_s = max_over_ranks(statistics.mean(e2e_t))
+        line["e2e"] = {"value": iters * g.edges * m / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                       "d2h_bytes_per_step": d2h, "seconds_per_step": e2e_s,
+                       "path": "sb_graph_create(host CSR, pinned) + sb_hb_create + sb_hb_run + sb_hb_read_state"}
+        line["end_to_end_s"] = e2e_s
+        g.pin(False)
+
+    # ---- variant: skip unchanged neighbours (bit-exact; reported separately)
+    if not args.no_variants:
+        hs = make_hb(skip=True)
+        one_run(hs)
+        barrier()
+        t = time.perf_counter()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s2 = torch.cuda.ExternalStream(hs.stream_handle())
+        e0.record(s2)
+        its = one_run(hs)
+        e1.record(s2)
+        e1.synchronize()
+        sk = max_over_ranks(e0.elapsed_time(e1) / 1e3)
+        same = bool(np.array_equal(hs.state().sum_d, hb.state().sum_d))
+        line["variants"] = {"skip_unchanged": {
+            "seconds_per_run": sk, "iterations": its, "dense_equivalent_updates_per_s": its * g.edges * m / sk,
+            "sum_d_identical_to_dense": same,
+            "per_iteration_union_ms": [round(s["union_ms"], 3) for s in hs.stats()],
+            "note": "gathers only neighbours whose registers changed last iteration; not used for value/roofline"}}
+        del hs
+
+    # ---- CPU baseline (rank 0, N=1)
+    if not args.no_cpu and world == 1 and rank == 0:
+        try:
+            line["cpu_baseline"] = run_cpu(g, args.p, args.cpu_sample_s, os.cpu_count() or 1)
+            line["cpu_baseline"].pop("seconds", None)
+        except Exception as e:  # the baseline is reported, never required
+            line["cpu_baseline"] = {"value": None, "error": repr(e)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,187 @@
+/*
+ * sieveball_cuda.h -- C-ABI of the B200 HyperBall library (libsieveball_cuda.so).
+ *
+ * Drop-in boundary for the reference's HyperBall path.  The
+ * reference exposes it as C++ (SPEC.md signatures; hyperball.cpp / cgraph.cpp
+ * are unshipped, CMakeLists.txt:20,25); this header is the plain-C seam a
+ * host in any language binds, and include/sieveball/hyperball_cuda.hpp wraps
+ * it back into the reference's C++ shapes and exceptions.
+ *
+ *   reference interface                                   replaced by
+ *   -----------------------------------------------------  ---------------------------
+ *   CompressedCsr arrays + load_vgacsr   sb_csr_* / sb_vgacsr_* (host)
+ *     (layout :253)                       sb_graph_create (-> HBM)
+ *   hyperball::run(graph, HllParams, depth)  sb_hb_create + sb_hb_run
+ *   hyperball::iterate_once              sb_hb_step
+ *   hyperball::check_convergence         sb_check_convergence
+ *   HllParams(p) (hll.cpp:9-19), invalid_argument          SB_EINVAL from sb_hb_create
+ *   kernels::Ops nibble_max_inplace / harmonic_sum         fused into the device kernels
+ *     (kernels.hpp:21-37)                                  (bit-exact by contract)
+ *   metrics: mean_depth, integration_* , moments           sb_hb_metrics
+ *
+ *   parallel_ranges (parallel.hpp:20-47)                   sb_partition_edges + sb_comm
+ *
+ * Conventions: every function returns SB_OK (0) or an error code; the message
+ * of the last error on the calling thread is in sb_last_error().  Host arrays
+ * are owned by the caller and copied; handles own all device memory.  One host
+ * thread per handle at a time.  No CPU fallback: without a CUDA device every
+ * device entry point fails with SB_ECUDA.
+ */
+#ifndef SIEVEBALL_CUDA_H
+#define SIEVEBALL_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  SB_OK = 0,
+  SB_EINVAL = 1,   /* std::invalid_argument (hll.cpp:10) */
+  SB_ERUNTIME = 2, /* std::runtime_error (leb128.hpp:32,38) */
+  SB_ECUDA = 3,
+  SB_ENCCL = 4,
+  SB_ENOMEM = 5
+};
+
+/* sb_hb_create flags */
+#define SB_HB_SKIP_UNCHANGED 1u /* gather only neighbours whose registers changed last iteration (bit-exact) */
+
+/* sb_hb_read_registers `which` */
+#define SB_REGS_LATEST 0   /* registers after the last executed iteration (c_t) */
+#define SB_REGS_PREVIOUS 1 /* registers before it (c_{t-1}) */
+
+typedef struct sb_csr sb_csr;     /* host CompressedCsr */
+typedef struct sb_graph sb_graph; /* device-resident CSR slice on one GPU */
+typedef struct sb_hb sb_hb;       /* HyperBallState on one GPU */
+typedef struct sb_comm sb_comm;   /* NCCL communicator for node-range sharding */
+
+const char* sb_last_error(void);
+const char* sb_version(void);
+int sb_device_count(int* n);
+
+/* ---------------- host CompressedCsr ---------------- */
+typedef struct {
+  uint64_t n;            /* node count N */
+  uint64_t edges;        /* |E| = sum of degrees (directed) */
+  uint64_t stream_len;   /* offsets[N] */
+  const uint64_t* offsets;        /* N+1 byte offsets */
+  const uint32_t* degrees;        /* N */
+  const uint8_t* stream;          /* stream_len bytes (+64 zero bytes of padding) */
+  uint64_t n_components;
+  const uint32_t* component_id;   /* N */
+  const uint32_t* component_sizes;/* n_components */
+  const uint32_t* cell_of_node;   /* N (grid cell index), may be NULL */
+  const uint32_t* hilbert_inverse;/* N original id per node, NULL if not reordered */
+  double origin_x, origin_y, spacing;
+  uint32_t rows, cols;
+} sb_csr_desc;
+
+/* Synthetic grid visibility graph: rows x cols cells, n_rects random
+ * axis-aligned rectangular obstacles with side in [rect_min, rect_max] cells
+ * (seeded), visibility radius^2 in cells^2 (0 = unlimited).  Line of sight is
+ * exact in integer arithmetic: the open centre-to-centre segment may not
+ * intersect the interior of an obstacle cell.  Ids are raster order. */
+int sb_csr_synth_grid(uint32_t rows, uint32_t cols, uint32_t n_rects, uint32_t rect_min,
+                      uint32_t rect_max, uint64_t seed, uint64_t radius2, unsigned threads,
+                      sb_csr** out);
+/* Builds from an uncompressed sorted adjacency (adj_offsets[n+1], adj_ids);
+ * rows must be strictly increasing ("non-increasing input -> error"). */
+int sb_csr_from_adjacency(uint64_t n, const uint64_t* adj_offsets, const uint32_t* adj_ids,
+                          sb_csr** out);
+/* Wraps caller arrays (copied); components computed with UnionFind if NULL. */
+int sb_csr_from_arrays(uint64_t n, const uint64_t* offsets, const uint32_t* degrees,
+                       const uint8_t* stream, uint64_t stream_len, sb_csr** out);
+int sb_csr_describe(const sb_csr* c, sb_csr_desc* out);
+/* Decodes row v into ids (capacity >= degrees[v]); returns SB_ERUNTIME on a malformed row. */
+int sb_csr_neighbors(const sb_csr* c, uint64_t v, uint32_t* ids);
+/* Hilbert renumbering: new graph, hilbert_inverse set. */
+int sb_csr_hilbert_reorder(const sb_csr* c, sb_csr** out);
+int sb_vgacsr_save(const sb_csr* c, const char* path);
+int sb_vgacsr_load(const char* path, sb_csr** out);
+void sb_csr_destroy(sb_csr* c);
+/* Page-locks (pin=1) or releases the stream buffer for full-speed H2D upload. */
+int sb_csr_pin(sb_csr* c, int pin);
+
+/* Edge-balanced contiguous node ranges: bounds[0]=0 <= ... <= bounds[parts]=n. */
+int sb_partition_edges(uint64_t n, const uint64_t* offsets, const uint32_t* degrees, int parts,
+                       uint64_t* bounds);
+
+/* ---------------- device graph + HyperBall ---------------- */
+/* Uploads rows [node_begin, node_end) of the CSR (stream slice, offsets,
+ * degrees) to HBM of `device`, validates every row (LEB128 well-formed,
+ * strictly increasing ids < n, exactly degrees[v] ids) and cuts rows into work
+ * items.  orig_id (N entries, NULL = identity) is the hash key per node
+ * (SPEC.md:454).  Errors: SB_EINVAL (bad range / empty graph), SB_ERUNTIME
+ * (malformed stream), SB_ECUDA / SB_ENOMEM. */
+int sb_graph_create(uint64_t n, const uint64_t* offsets, const uint32_t* degrees,
+                    const uint8_t* stream, uint64_t stream_len, const uint32_t* orig_id,
+                    uint64_t node_begin, uint64_t node_end, int device, sb_graph** out);
+int sb_graph_stats(const sb_graph* g, uint64_t* n_local, uint64_t* edges_local,
+                   uint64_t* stream_bytes_local, uint64_t* n_items, uint32_t* chunk);
+void sb_graph_destroy(sb_graph* g);
+
+/* HyperBallState on the device; init (insert orig_id, estimate c_0).
+ * p in [4,16] else SB_EINVAL; depth_limit 0 = unlimited. */
+int sb_hb_create(sb_graph* g, unsigned p, uint32_t depth_limit, uint32_t flags, sb_hb** out);
+/* iterate_once + check_convergence + (if not finished) swap, exactly Alg. 1
+ * order.  With an attached communicator the shard exchange
+ * and the global max run inside.  *finished = converged || t == depth_limit. */
+int sb_hb_step(sb_hb* h, double* max_increase, int* converged, int* finished);
+/* Loops sb_hb_step until finished (== hyperball::run). */
+int sb_hb_run(sb_hb* h, uint32_t* iterations, int* converged);
+/* Split step for same-process shards (tests / single-GPU logical sharding):
+ * compute -> exchange_local(all shards) -> finish(global max). */
+int sb_hb_step_compute(sb_hb* h, double* local_max_increase);
+int sb_hb_exchange_local(sb_hb* const* hs, int count);
+int sb_hb_step_finish(sb_hb* h, double global_max_increase, int* converged, int* finished);
+
+/* Registers in the REFERENCE packed layout (m/2 bytes per row, low nibble =
+ * even register, hll.hpp:31-32), rows [v0, v1) of the replica. */
+int sb_hb_read_registers(const sb_hb* h, int which, uint64_t v0, uint64_t v1, uint8_t* dst);
+/* Overwrites the latest registers of ALL rows (packed layout) and re-estimates
+ * c for the local range (treated as c_t; t unchanged).  Test hook. */
+int sb_hb_set_registers(sb_hb* h, const uint8_t* packed_all_rows);
+/* Local-range state (any pointer may be NULL).  c_latest = c_t, c_previous = c_{t-1}. */
+int sb_hb_read_state(const sb_hb* h, double* c_latest, double* c_previous, double* sum_d,
+                     double* sum_d2, uint8_t* changed, uint32_t* t, int* converged,
+                     int* finished);
+/* Metrics for the local range: nv = component size per local
+ * node, deg = degree per local node.  Outputs may be NULL. */
+int sb_hb_metrics(const sb_hb* h, const uint32_t* nv, const uint32_t* deg, double* md,
+                  double* ihh, double* tekl, double* pv, double* m1, double* m2);
+
+typedef struct {
+  uint32_t t;              /* iteration number */
+  float union_ms;          /* fused decode-union kernel (CUDA events) */
+  float estimate_ms;       /* estimate + accumulate kernel */
+  float exchange_ms;       /* shard exchange (NCCL / local copies) */
+  float step_ms;           /* whole step incl. host sync */
+  double max_increase;
+  uint64_t changed_nodes;  /* local nodes whose registers changed */
+} sb_iter_stats;
+/* Copies up to `cap` per-iteration records since create/reset; *count = total. */
+int sb_hb_stats(const sb_hb* h, sb_iter_stats* out, uint32_t cap, uint32_t* count);
+/* Re-initialises the state (t = 0, registers from orig_id, sums zeroed). */
+int sb_hb_reset(sb_hb* h);
+/* Raw CUDA stream the handle launches on (cudaStream_t as void*). */
+void* sb_hb_stream(const sb_hb* h);
+void sb_hb_destroy(sb_hb* h);
+
+int sb_check_convergence(double max_increase); /* 1 iff max_increase <= 0.5 */
+
+/* ---------------- multi-GPU (one process per GPU) ---------------- */
+#define SB_COMM_ID_BYTES 128
+int sb_comm_unique_id(void* id_out /* SB_COMM_ID_BYTES */);
+int sb_comm_create(int nranks, int rank, const void* id, int device, sb_comm** out);
+/* Attaches the communicator; bounds[nranks+1] = node ranges of all ranks
+ * (this rank's graph must cover [bounds[rank], bounds[rank+1])). */
+int sb_hb_attach_comm(sb_hb* h, sb_comm* c, const uint64_t* bounds);
+void sb_comm_destroy(sb_comm* c);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SIEVEBALL_CUDA_H */

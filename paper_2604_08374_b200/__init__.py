@@ -1,0 +1,15 @@
+"""sieveball-b200: B200-native HyperBall hot path of arxiv 2604.08374.
+
+Drop-in for the reference's HyperBall path (compressed-CSR loader, HyperBall
+runner, VGA metrics).  Host API mirrors SPEC.md's hyperball / cgraph / hll /
+metrics modules; compute runs in libsieveball_cuda.so (sm_100a).
+"""
+from ._lib import CudaError, NcclError, lib  # noqa: F401
+from .cgraph import CompressedCsr, encode_neighbor_row, leb128_decode, leb128_encode  # noqa: F401
+from .hyperball import (Comm, DeviceGraph, HllParams, HyperBall, HyperBallState,  # noqa: F401
+                        check_convergence, run)
+from . import metrics  # noqa: F401
+
+__all__ = ["CompressedCsr", "DeviceGraph", "HllParams", "HyperBall", "HyperBallState", "Comm",
+           "check_convergence", "run", "metrics", "leb128_encode", "leb128_decode",
+           "encode_neighbor_row", "lib"]

@@ -1,0 +1,196 @@
+// sb_device.cuh -- device building blocks of the B200 HyperBall path.
+//
+// Register layout in HBM ("bit-sliced 4-bit"): a counter row keeps the
+// reference density of m/2 bytes (hll.hpp:31-32) but stores each group of 32
+// registers (16 for p=4) as four bit-planes: plane b holds bit b of every
+// register of the group, bit i of a plane <-> register 32*g+i.  A register-wise
+// max (kernels.hpp:21-25, nibble_max_inplace) is then a 4-stage ripple
+// comparator over whole 32-bit words: 8 LOP3 per 32 registers, instead of the
+// masked byte-max a packed layout needs.  The reference packed layout (low
+// nibble = even register, hll.hpp:50-60) is produced on export by
+// bits_to_packed(); parity is always checked in the reference layout.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace sb {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+template <int P>
+struct Geo {
+  static constexpr int M = 1 << P;
+  static constexpr int ROW = M / 2;                     // bytes per counter row (m/2)
+  static constexpr int GB = P >= 5 ? 16 : 8;            // bytes per bit-sliced group
+  static constexpr int GROUPS = ROW / GB;               // groups per row
+  static constexpr int LPR = GROUPS >= 32 ? 32 : GROUPS;  // lanes spanning one row slice
+  static constexpr int SLICES = GROUPS >= 32 ? GROUPS / 32 : 1;
+  static constexpr int SUB = 32 / LPR;                  // neighbour rows per warp step
+  static constexpr int SLICE_BYTES = LPR * GB;          // 512 B for p >= 10
+  static constexpr uint32_t VALID = P >= 5 ? 0xffffffffu : 0x0000ffffu;
+};
+
+struct Grp {
+  uint32_t b0, b1, b2, b3;
+};
+
+__device__ __forceinline__ Grp grp_zero() { return Grp{0u, 0u, 0u, 0u}; }
+
+__device__ __forceinline__ uint32_t lop3_0c(uint32_t a, uint32_t b) {  // ~a & b
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0x0c;" : "=r"(r) : "r"(a), "r"(b), "r"(0u));
+  return r;
+}
+__device__ __forceinline__ uint32_t lop3_8e(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t r;  // (~a & b) | (~(a ^ b) & c)
+  asm("lop3.b32 %0, %1, %2, %3, 0x8e;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+  return r;
+}
+__device__ __forceinline__ uint32_t lop3_d8(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t r;  // (a & ~c) | (b & c)
+  asm("lop3.b32 %0, %1, %2, %3, 0xd8;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+  return r;
+}
+
+// a <- register-wise max(a, b).  g = positions where b > a, computed LSB-first
+// as a ripple comparator g_k = (b_k & ~a_k) | (~(a_k ^ b_k) & g_{k-1}) -- one
+// LOP3 per bit-plane -- then a 4-LOP3 select: 8 LOP3 per 32 registers.
+__device__ __forceinline__ void bsmax(Grp& a, const Grp& b) {
+  uint32_t g = lop3_0c(a.b0, b.b0);
+  g = lop3_8e(a.b1, b.b1, g);
+  g = lop3_8e(a.b2, b.b2, g);
+  g = lop3_8e(a.b3, b.b3, g);
+  a.b0 = lop3_d8(a.b0, b.b0, g);
+  a.b1 = lop3_d8(a.b1, b.b1, g);
+  a.b2 = lop3_d8(a.b2, b.b2, g);
+  a.b3 = lop3_d8(a.b3, b.b3, g);
+}
+
+__device__ __forceinline__ bool grp_ne(const Grp& a, const Grp& b) {
+  return ((a.b0 ^ b.b0) | (a.b1 ^ b.b1) | (a.b2 ^ b.b2) | (a.b3 ^ b.b3)) != 0u;
+}
+
+__device__ __forceinline__ Grp grp_shfl_xor(const Grp& a, int m) {
+  return Grp{__shfl_xor_sync(FULL, a.b0, m), __shfl_xor_sync(FULL, a.b1, m),
+             __shfl_xor_sync(FULL, a.b2, m), __shfl_xor_sync(FULL, a.b3, m)};
+}
+
+// ---- group loads / stores (16 B groups; p=4 uses 8 B groups of 16-bit planes)
+template <int GB>
+struct GrpIO;
+
+template <>
+struct GrpIO<16> {
+  __device__ __forceinline__ static Grp ld(const uint8_t* p) {
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(p));
+    return Grp{v.x, v.y, v.z, v.w};
+  }
+  __device__ __forceinline__ static Grp ld_cg(const uint8_t* p) {
+    const uint4 v = __ldcg(reinterpret_cast<const uint4*>(p));
+    return Grp{v.x, v.y, v.z, v.w};
+  }
+  __device__ __forceinline__ static void st(uint8_t* p, const Grp& g) {
+    *reinterpret_cast<uint4*>(p) = make_uint4(g.b0, g.b1, g.b2, g.b3);
+  }
+};
+
+template <>
+struct GrpIO<8> {
+  __device__ __forceinline__ static Grp unpack(uint2 v) {
+    return Grp{v.x & 0xffffu, v.x >> 16, v.y & 0xffffu, v.y >> 16};
+  }
+  __device__ __forceinline__ static Grp ld(const uint8_t* p) {
+    return unpack(__ldg(reinterpret_cast<const uint2*>(p)));
+  }
+  __device__ __forceinline__ static Grp ld_cg(const uint8_t* p) {
+    return unpack(__ldcg(reinterpret_cast<const uint2*>(p)));
+  }
+  __device__ __forceinline__ static void st(uint8_t* p, const Grp& g) {
+    *reinterpret_cast<uint2*>(p) = make_uint2(g.b0 | (g.b1 << 16), g.b2 | (g.b3 << 16));
+  }
+};
+
+// ---- packed <-> bit-sliced conversion of one group (nwords = GB/4 packed words)
+// Packed word w (little endian) holds registers 8w..8w+7, nibble k = register 8w+k.
+__device__ __host__ __forceinline__ uint32_t gather_every4(uint32_t x) {
+  x &= 0x11111111u;
+  x = (x | (x >> 3)) & 0x03030303u;
+  x = (x | (x >> 6)) & 0x000f000fu;
+  x = (x | (x >> 12)) & 0x000000ffu;
+  return x;
+}
+__device__ __host__ __forceinline__ uint32_t spread_every4(uint32_t y) {
+  y &= 0xffu;
+  y = (y | (y << 12)) & 0x000f000fu;
+  y = (y | (y << 6)) & 0x03030303u;
+  y = (y | (y << 3)) & 0x11111111u;
+  return y;
+}
+
+// ---- ordered encoding of doubles for atomicMax
+__device__ __host__ __forceinline__ unsigned long long dbl_to_ord(double x) {
+#ifdef __CUDA_ARCH__
+  const unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(x));
+#else
+  unsigned long long u;
+  memcpy(&u, &x, 8);
+#endif
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+
+// ---- warp-cooperative LEB128 decode -----------------------------------
+// One step consumes the 32-byte window at `pos` up to its last wanted varint
+// terminator (bit 7 clear).  Each terminator lane assembles its varint from
+// itself and up to four preceding bytes (shfl_up), a warp inclusive scan turns
+// deltas into absolute ids (first id of a row is absolute: base 0), and the
+// window always starts on a varint boundary so no carry crosses steps.
+// Returns the ballot of lanes holding a decoded id in *idmask and the id in *id.
+struct DecodeOut {
+  uint32_t mask;  // lanes holding a wanted id
+  uint32_t id;    // this lane's absolute id (valid iff mask bit set); for other
+                  // lanes the id of the closest wanted lane below (or base)
+  int count;      // popc(mask)
+  int last;       // lane of the last wanted id (-1 if none)
+  bool bad;       // (CHECK only) this lane's varint is > 5 bytes or exceeds 32 bits
+};
+
+template <bool CHECK>
+__device__ __forceinline__ DecodeOut decode_step(const uint8_t* __restrict__ stream, uint64_t pos,
+                                                 uint64_t end, uint32_t remaining, uint32_t base,
+                                                 int lane) {
+  const uint64_t at = pos + static_cast<uint64_t>(lane);
+  const uint32_t b = at < end ? static_cast<uint32_t>(__ldg(stream + at)) : 0x80u;
+  const bool term = (b & 0x80u) == 0;
+  const uint32_t T = __ballot_sync(FULL, term);
+  const uint32_t lt = (1u << lane) - 1u;
+  const uint32_t rank = __popc(T & lt);
+  const bool want = term && rank < remaining;
+  const uint32_t W = __ballot_sync(FULL, want);
+  const uint32_t b1 = __shfl_up_sync(FULL, b, 1);
+  const uint32_t b2 = __shfl_up_sync(FULL, b, 2);
+  const uint32_t b3 = __shfl_up_sync(FULL, b, 3);
+  const uint32_t b4 = __shfl_up_sync(FULL, b, 4);
+  const uint32_t below = T & lt;
+  const int start = below ? 32 - __clz(below) : 0;
+  const int k = lane - start;  // continuation bytes preceding this terminator
+  uint32_t v = b & 0x7fu;
+  if (k >= 1) v = (v << 7) | (b1 & 0x7fu);
+  if (k >= 2) v = (v << 7) | (b2 & 0x7fu);
+  if (k >= 3) v = (v << 7) | (b3 & 0x7fu);
+  if (k >= 4) v = (v << 7) | (b4 & 0x7fu);
+  if (!want) v = 0;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(FULL, v, d);
+    if (lane >= d) v += y;
+  }
+  DecodeOut o;
+  o.mask = W;
+  o.id = base + v;
+  o.count = __popc(W);
+  o.last = W ? 31 - __clz(W) : -1;
+  o.bad = CHECK ? (want && (k > 4 || (k == 4 && (b & 0x7fu) > 0x0fu))) : false;
+  return o;
+}
+
+}  // namespace sb

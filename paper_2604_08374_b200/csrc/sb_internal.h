@@ -1,0 +1,76 @@
+// sb_internal.h -- argument blocks and launchers shared by the runtime and kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace sb {
+
+struct BuildArgs {
+  const uint8_t* stream;       // local stream slice (padded)
+  const uint64_t* row_off;     // local byte offsets, n_local + 1
+  const uint32_t* degrees;     // local degrees
+  uint64_t n_local;
+  uint64_t n_global;
+  uint32_t chunk;              // neighbours per work item
+  const uint32_t* node_item;   // local node -> first item (n_local + 1)
+  uint64_t* item_off;
+  uint32_t* item_base;
+  uint32_t* item_count;
+  uint32_t* item_node;
+  unsigned long long* err_node;  // min local node with a malformed row (~0 = none)
+};
+
+struct UnionArgs {
+  const uint8_t* stream;
+  const uint64_t* item_off;
+  const uint32_t* item_base;
+  const uint32_t* item_count;
+  const uint32_t* item_node;   // local node index
+  const uint32_t* node_item;   // local node -> first item (n_local + 1)
+  uint64_t n_items;
+  uint64_t node_begin;         // global id of local node 0
+  const uint8_t* cur;          // full replica, global rows
+  uint8_t* next;               // global rows (own range written)
+  uint8_t* scratch;            // per work unit partial rows
+  uint32_t* node_counter;      // n_local * slices arrival counters (self-resetting)
+  uint8_t* changed_out;        // global-indexed, 1 = registers changed this iteration
+  const uint8_t* changed_in;   // global-indexed, previous iteration (skip mode)
+  unsigned long long* work;    // dynamic work counter (zeroed per launch)
+};
+
+struct EstArgs {
+  const uint8_t* plane;        // registers to estimate (global rows)
+  uint64_t node_begin;
+  uint64_t n_local;
+  const double* lc;            // lc[z] = m * log(m / z), host-built (hll.cpp:35)
+  double alpha;
+  double m;
+  const double* c_prev;        // local
+  double* c_cur;               // local
+  double* sum_d;               // local
+  double* sum_d2;              // local
+  const uint8_t* changed;      // global-indexed
+  uint32_t t;
+  unsigned long long* max_ord; // ordered-encoded max increase
+  unsigned long long* changed_count;
+};
+
+struct MetricArgs {
+  uint64_t n;
+  const double* sum_d;
+  const double* sum_d2;
+  const uint32_t* nv;
+  const uint32_t* deg;
+  double *md, *ihh, *tekl, *pv, *m1, *m2;
+};
+
+cudaError_t launch_build_items(const BuildArgs& a, cudaStream_t s);
+cudaError_t launch_init(int p, uint8_t* plane, uint64_t n, const uint32_t* orig, cudaStream_t s);
+cudaError_t launch_union(int p, bool skip, const UnionArgs& a, cudaStream_t s);
+cudaError_t launch_estimate(int p, int mode, const EstArgs& a, cudaStream_t s);
+cudaError_t launch_to_packed(int p, const uint8_t* bits, uint8_t* packed, uint64_t rows, cudaStream_t s);
+cudaError_t launch_from_packed(int p, const uint8_t* packed, uint8_t* bits, uint64_t rows, cudaStream_t s);
+cudaError_t launch_metrics(const MetricArgs& a, cudaStream_t s);
+int union_slices(int p);
+
+}  // namespace sb

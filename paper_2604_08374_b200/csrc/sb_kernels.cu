@@ -1,0 +1,522 @@
+// sb_kernels.cu -- sm_100a kernels of the HyperBall hot path.
+//
+//   sb_build_items   : validates the LEB128 delta-CSR once at upload and cuts
+//                      every row into work items of <= `chunk` neighbours
+//   sb_init          : hll_init: insert orig_id[v]
+//   sb_union   <P>   : fused decode-union (PAPER.md:469-475 replaced): warp per
+//                      work item, warp-cooperative LEB128 decode, 16-B coalesced
+//                      row gathers, bit-sliced register max, per-node changed flag
+//   sb_estimate<P>   : hll_cardinality + hll_accumulate:
+//                      integer harmonic sum -> bit-exact estimate (hll.cpp:31-37),
+//                      sum_d/sum_d2 accumulation, global max increase
+//   sb_to_packed / sb_from_packed : export/import in the reference packed layout
+//   sb_metrics       : MD / IHH / Tekl / PV / moments
+#include <cstdio>
+
+#include "sb_device.cuh"
+#include "sb_internal.h"
+
+namespace sb {
+
+// ------------------------------------------------------------------ build
+__global__ void __launch_bounds__(256) build_items_kernel(BuildArgs a) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = (gridDim.x * (uint64_t)blockDim.x) >> 5;
+  for (uint64_t node = gw; node < a.n_local; node += nw) {
+    uint64_t pos = a.row_off[node];
+    const uint64_t end = a.row_off[node + 1];
+    const uint32_t deg = a.degrees[node];
+    const uint32_t i0 = a.node_item[node];
+    if (lane == 0) {
+      a.item_off[i0] = pos;
+      a.item_base[i0] = 0;
+      a.item_count[i0] = deg < a.chunk ? deg : a.chunk;
+      a.item_node[i0] = static_cast<uint32_t>(node);
+    }
+    uint32_t rem = deg, base = 0, k0 = 0;
+    bool bad = false;
+    while (rem > 0) {
+      const DecodeOut d = decode_step<true>(a.stream, pos, end, rem, base, lane);
+      if (d.count == 0) {  // truncated row or varint longer than the window
+        bad = true;
+        break;
+      }
+      const bool want = (d.mask >> lane) & 1u;
+      const uint32_t up = __shfl_up_sync(FULL, d.id, 1);  // every lane must execute the shuffle
+      const uint32_t prev = lane > 0 ? up : base;
+      const uint32_t rank = __popc(d.mask & ((1u << lane) - 1u));
+      const uint32_t j = k0 + rank;  // neighbour index within the row
+      bool lane_bad = d.bad;
+      if (want) {
+        if (d.id >= a.n_global) lane_bad = true;
+        if (j > 0 && !(d.id > prev)) lane_bad = true;  // strictly increasing
+        if ((j + 1) % a.chunk == 0 && j + 1 < deg) {
+          const uint32_t it = i0 + (j + 1) / a.chunk;
+          a.item_off[it] = pos + lane + 1;
+          a.item_base[it] = d.id;
+          a.item_count[it] = (deg - (j + 1)) < a.chunk ? deg - (j + 1) : a.chunk;
+          a.item_node[it] = static_cast<uint32_t>(node);
+        }
+      }
+      if (__any_sync(FULL, lane_bad)) {
+        bad = true;
+        break;
+      }
+      pos += d.last + 1;
+      rem -= d.count;
+      base = __shfl_sync(FULL, d.id, d.last);
+      k0 += d.count;
+    }
+    if (!bad && pos != end) bad = true;  // trailing bytes in the row
+    if (bad && lane == 0) atomicMin(a.err_node, static_cast<unsigned long long>(node));
+  }
+}
+
+// ------------------------------------------------------------------ init
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {  // hll.hpp:13-20
+  x ^= x >> 30;
+  x *= 0xBF58476D1CE4E5B9ull;
+  x ^= x >> 27;
+  x *= 0x94D049BB133111EBull;
+  x ^= x >> 31;
+  return x;
+}
+
+template <int P>
+__global__ void __launch_bounds__(256) init_kernel(uint8_t* plane, uint64_t n, const uint32_t* orig) {
+  using G = Geo<P>;
+  using IO = GrpIO<G::GB>;
+  constexpr int RPG = G::GB * 2;  // registers per group
+  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const uint64_t total = n * G::GROUPS;
+  for (uint64_t i = tid; i < total; i += gridDim.x * (uint64_t)blockDim.x) {
+    const uint64_t v = i / G::GROUPS;
+    const int g = static_cast<int>(i % G::GROUPS);
+    // hll_insert (hll.cpp:21-29)
+    const uint64_t h = splitmix64(orig ? static_cast<uint64_t>(orig[v]) : v);
+    const uint32_t idx = static_cast<uint32_t>(h >> (64 - P));
+    const uint64_t w = h << P;
+    const unsigned lz = w == 0 ? (64 - P) : static_cast<unsigned>(__clzll(static_cast<long long>(w)));
+    const uint32_t rho = lz + 1 < 15u ? lz + 1 : 15u;
+    Grp x = grp_zero();
+    if (static_cast<int>(idx / RPG) == g) {
+      const uint32_t bit = 1u << (idx % RPG);
+      x.b0 = (rho & 1u) ? bit : 0u;
+      x.b1 = (rho & 2u) ? bit : 0u;
+      x.b2 = (rho & 4u) ? bit : 0u;
+      x.b3 = (rho & 8u) ? bit : 0u;
+    }
+    IO::st(plane + v * G::ROW + static_cast<uint64_t>(g) * G::GB, x);
+  }
+}
+
+// ------------------------------------------------------------------ union
+// Per-warp id feeder: decodes one 32-byte window of the item's LEB128 stream
+// at a time into a 32-entry shared buffer (compacted; tail lanes padded with
+// the last id, harmless because max is idempotent) and hands out batches of
+// BATCH = U * SUB ids.
+template <int P, bool SKIP>
+struct Feeder {
+  using G = Geo<P>;
+  static constexpr int U = (32 / G::SUB) < 8 ? (32 / G::SUB) : 8;  // row loads in flight per lane
+  static constexpr int BATCH = U * G::SUB;
+  uint32_t* buf;
+  uint64_t pos;
+  uint32_t rem, base;
+  int n, i;
+
+  // Returns false when the item is exhausted.
+  __device__ __forceinline__ bool next(const UnionArgs& a, int lane) {
+    while (i >= n) {
+      if (rem == 0) return false;
+      const DecodeOut d = decode_step<false>(a.stream, pos, ~0ull, rem, base, lane);
+      if (d.count == 0) {  // unreachable on a validated stream
+        rem = 0;
+        return false;
+      }
+      pos += d.last + 1;
+      rem -= d.count;
+      base = __shfl_sync(FULL, d.id, d.last);
+      uint32_t keep = d.mask;
+      if (SKIP) {
+        // Only neighbours whose registers changed in the previous iteration can
+        // raise next[v]: an unchanged w was already folded into cur[v].
+        const bool c = ((d.mask >> lane) & 1u) && a.changed_in[d.id];
+        keep = __ballot_sync(FULL, c);
+      }
+      n = __popc(keep);
+      i = 0;
+      if (n == 0) continue;
+      const int lastk = 31 - __clz(keep);
+      const uint32_t lastid = __shfl_sync(FULL, d.id, lastk);
+      __syncwarp();
+      if ((keep >> lane) & 1u) buf[__popc(keep & ((1u << lane) - 1u))] = d.id;
+      if (lane >= n) buf[lane] = lastid;
+      __syncwarp();
+    }
+    return true;
+  }
+};
+
+template <int P, int U>
+__device__ __forceinline__ void load_batch(Grp (&x)[U], const uint8_t* __restrict__ curb,
+                                           const uint32_t* buf, int i, int sub) {
+  using G = Geo<P>;
+  using IO = GrpIO<G::GB>;
+#pragma unroll
+  for (int q = 0; q < U; ++q) x[q] = IO::ld(curb + static_cast<uint64_t>(buf[i + q * G::SUB + sub]) * G::ROW);
+}
+
+// One warp per work unit u = item * SLICES + slice.  Item = <= chunk consecutive
+// neighbours of one node.  next[v] = max(cur[v], max_w cur[w])
+// register-wise; a node split over several items is merged by the last item
+// to finish (partials in `scratch`, arrival counter per node-slice).
+// Gathers are software-pipelined: batch k+1's row loads (and, when needed, the
+// next window decode) are issued before batch k's max, so U..2U 16-byte loads
+// per lane stay in flight.
+template <int P, bool SKIP>
+__global__ void __launch_bounds__(256) union_kernel(UnionArgs a) {
+  using G = Geo<P>;
+  using IO = GrpIO<G::GB>;
+  using F = Feeder<P, SKIP>;
+  constexpr int U = F::U;
+  __shared__ uint32_t ids_s[8][32];
+  const int lane = threadIdx.x & 31;
+  const uint64_t total = a.n_items * G::SLICES;
+  const int sub = lane / G::LPR;
+  const int gl = lane % G::LPR;
+  for (;;) {
+    unsigned long long u = 0;
+    if (lane == 0) u = atomicAdd(a.work, 1ull);
+    u = __shfl_sync(FULL, u, 0);
+    if (u >= total) break;
+    const uint64_t item = u / G::SLICES;
+    const int slice = static_cast<int>(u % G::SLICES);
+    const uint32_t node = a.item_node[item];
+    const uint64_t v = a.node_begin + node;
+    const uint32_t first = a.node_item[node];
+    const uint32_t nit = a.node_item[node + 1] - first;
+    const uint64_t goff = static_cast<uint64_t>(slice) * G::SLICE_BYTES + static_cast<uint64_t>(gl) * G::GB;
+    const uint8_t* __restrict__ curb = a.cur + goff;
+    Grp acc = (item == first) ? IO::ld(curb + v * G::ROW) : grp_zero();  // next[v] <- cur[v]
+    F f;
+    f.buf = ids_s[threadIdx.x >> 5];
+    f.pos = a.item_off[item];
+    f.rem = a.item_count[item];
+    f.base = a.item_base[item];
+    f.n = 0;
+    f.i = 0;
+    Grp xa[U], xb[U];
+    bool ha = f.next(a, lane);
+    if (ha) {
+      load_batch<P, U>(xa, curb, f.buf, f.i, sub);
+      f.i += F::BATCH;
+    }
+    while (ha) {
+      const bool hb = f.next(a, lane);
+      if (hb) {
+        load_batch<P, U>(xb, curb, f.buf, f.i, sub);
+        f.i += F::BATCH;
+      }
+#pragma unroll
+      for (int q = 0; q < U; ++q) bsmax(acc, xa[q]);
+      if (!hb) break;
+      ha = f.next(a, lane);
+      if (ha) {
+        load_batch<P, U>(xa, curb, f.buf, f.i, sub);
+        f.i += F::BATCH;
+      }
+#pragma unroll
+      for (int q = 0; q < U; ++q) bsmax(acc, xb[q]);
+    }
+    if (G::SUB > 1) {
+#pragma unroll
+      for (int m = G::LPR; m < 32; m <<= 1) bsmax(acc, grp_shfl_xor(acc, m));
+    }
+    uint8_t* nextb = a.next + goff + v * G::ROW;
+    bool finish = nit == 1;
+    if (!finish) {
+      if (lane < G::LPR) IO::st(a.scratch + u * G::SLICE_BYTES + static_cast<uint64_t>(gl) * G::GB, acc);
+      __threadfence();
+      uint32_t prev = 0;
+      if (lane == 0) prev = atomicAdd(&a.node_counter[static_cast<uint64_t>(node) * G::SLICES + slice], 1u);
+      prev = __shfl_sync(FULL, prev, 0);
+      finish = prev == nit - 1;
+      if (finish) {
+        __threadfence();
+        for (uint32_t i = first; i < first + nit; ++i) {
+          if (i == item) continue;
+          const uint64_t uu = static_cast<uint64_t>(i) * G::SLICES + slice;
+          bsmax(acc, IO::ld_cg(a.scratch + uu * G::SLICE_BYTES + static_cast<uint64_t>(gl) * G::GB));
+        }
+        if (lane == 0) a.node_counter[static_cast<uint64_t>(node) * G::SLICES + slice] = 0u;
+      }
+    }
+    if (finish) {
+      const Grp own = IO::ld(curb + v * G::ROW);
+      const bool ch = lane < G::LPR && grp_ne(acc, own);
+      if (lane < G::LPR) IO::st(nextb, acc);
+      if (__any_sync(FULL, ch) && lane == 0) a.changed_out[v] = 1;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ estimate
+// MODE 0: init (c -> c_cur only); 1: dense accumulate; 2: skip unchanged rows.
+template <int P, int MODE>
+__global__ void __launch_bounds__(256) estimate_kernel(EstArgs a) {
+  using G = Geo<P>;
+  using IO = GrpIO<G::GB>;
+  __shared__ unsigned long long red[8];
+  const int lane = threadIdx.x & 31;
+  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = (gridDim.x * (uint64_t)blockDim.x) >> 5;
+  unsigned long long wmax = 0ull;  // ordered encoding; 0 < every encoded value
+  unsigned long long nchanged = 0ull;
+  const double m = a.m;
+  const double td = static_cast<double>(a.t);
+  const double tt = static_cast<double>(static_cast<uint64_t>(a.t) * a.t);
+  for (uint64_t node = gw; node < a.n_local; node += nw) {
+    const uint64_t v = a.node_begin + node;
+    if (MODE == 2 && !a.changed[v]) {
+      if (lane == 0) {
+        a.c_cur[node] = a.c_prev[node];
+        wmax = max(wmax, dbl_to_ord(0.0));
+      }
+      continue;
+    }
+    if (MODE != 0 && lane == 0 && a.changed[v]) ++nchanged;
+    uint64_t num = 0;
+    uint32_t zeros = 0;
+    const uint8_t* row = a.plane + v * G::ROW;
+    for (int g = lane; g < G::GROUPS; g += 32) {
+      const Grp x = IO::ld(row + static_cast<uint64_t>(g) * G::GB);
+      const uint32_t n0 = ~x.b0 & G::VALID, n1 = ~x.b1 & G::VALID, n2 = ~x.b2 & G::VALID, n3 = ~x.b3 & G::VALID;
+      const uint32_t lo[4] = {n1 & n0, n1 & x.b0, x.b1 & n0, x.b1 & x.b0};
+      const uint32_t hi[4] = {n3 & n2, n3 & x.b2, x.b3 & n2, x.b3 & x.b2};
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        const uint32_t c = __popc(hi[r >> 2] & lo[r & 3]);
+        num += static_cast<uint64_t>(c) << (15 - r);  // sum 2^(15-r) (kernels.hpp:11-16)
+        if (r == 0) zeros += c;
+      }
+    }
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) {
+      num += __shfl_xor_sync(FULL, num, d);
+      zeros += __shfl_xor_sync(FULL, zeros, d);
+    }
+    if (lane == 0) {
+      // hll_estimate_from_sum (hll.cpp:31-37), same operation order, no FMA.
+      const double harmonic = __ddiv_rn(static_cast<double>(num), 32768.0);
+      const double raw = __ddiv_rn(__dmul_rn(__dmul_rn(a.alpha, m), m), harmonic);
+      const double c = (raw <= 2.5 * m && zeros > 0) ? a.lc[zeros] : raw;
+      if (MODE == 0) {
+        a.c_cur[node] = c;
+      } else {
+        // sum_d += t * (c_t - c_{t-1}), sum_d2 += t^2 * (...)
+        const double delta = __dsub_rn(c, a.c_prev[node]);
+        a.c_cur[node] = c;
+        a.sum_d[node] = __dadd_rn(a.sum_d[node], __dmul_rn(td, delta));
+        a.sum_d2[node] = __dadd_rn(a.sum_d2[node], __dmul_rn(tt, delta));
+        wmax = max(wmax, dbl_to_ord(delta));
+      }
+    }
+  }
+  if (MODE == 0) return;
+  if (lane == 0) red[threadIdx.x >> 5] = wmax;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long b = red[0];
+    for (int i = 1; i < static_cast<int>(blockDim.x >> 5); ++i) b = max(b, red[i]);
+    if (b) atomicMax(a.max_ord, b);
+  }
+  if (lane == 0 && nchanged) atomicAdd(a.changed_count, nchanged);
+}
+
+// ------------------------------------------------------------------ layout conversion
+template <int P>
+__global__ void to_packed_kernel(const uint8_t* __restrict__ bits, uint8_t* __restrict__ packed,
+                                 uint64_t groups) {
+  using G = Geo<P>;
+  using IO = GrpIO<G::GB>;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < groups;
+       i += gridDim.x * (uint64_t)blockDim.x) {
+    const Grp x = IO::ld(bits + i * G::GB);
+    const uint32_t pl[4] = {x.b0, x.b1, x.b2, x.b3};
+    uint32_t* out = reinterpret_cast<uint32_t*>(packed + i * G::GB);
+#pragma unroll
+    for (int w = 0; w < G::GB / 4; ++w) {
+      uint32_t word = 0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) word |= spread_every4(pl[b] >> (8 * w)) << b;
+      out[w] = word;
+    }
+  }
+}
+
+template <int P>
+__global__ void from_packed_kernel(const uint8_t* __restrict__ packed, uint8_t* __restrict__ bits,
+                                   uint64_t groups) {
+  using G = Geo<P>;
+  using IO = GrpIO<G::GB>;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < groups;
+       i += gridDim.x * (uint64_t)blockDim.x) {
+    const uint32_t* in = reinterpret_cast<const uint32_t*>(packed + i * G::GB);
+    uint32_t pl[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int w = 0; w < G::GB / 4; ++w) {
+      const uint32_t word = in[w];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) pl[b] |= gather_every4(word >> b) << (8 * w);
+    }
+    IO::st(bits + i * G::GB, Grp{pl[0], pl[1], pl[2], pl[3]});
+  }
+}
+
+// ------------------------------------------------------------------ metrics
+__global__ void metrics_kernel(MetricArgs a) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < a.n;
+       i += gridDim.x * (uint64_t)blockDim.x) {
+    const uint32_t nv = a.nv[i];
+    const double N = static_cast<double>(nv);
+    const double nan = __longlong_as_double(0x7ff8000000000000ll);
+    double MD = nan, IHH = nan, TK = nan, PV = nan, M1 = nan, M2 = nan;
+    if (nv >= 2) {
+      MD = a.sum_d[i] / (N - 1.0);
+      TK = log2((MD + 2.0) / 3.0);
+      M1 = MD * static_cast<double>(a.deg[i]);
+      M2 = a.sum_d2[i] / (N - 1.0);
+      if (nv >= 3) {
+        const double RA = 2.0 * (MD - 1.0) / (N - 2.0);
+        const double pv = 1.0 - RA;
+        PV = pv > 0.0 ? pv : 0.0;
+        if (MD != 1.0) {
+          const double Dk = 2.0 * (N * (log2((N + 2.0) / 3.0) - 1.0) + 1.0) / ((N - 1.0) * (N - 2.0));
+          IHH = 1.0 / (RA / Dk);
+        }
+      }
+    }
+    a.md[i] = MD;
+    a.ihh[i] = IHH;
+    a.tekl[i] = TK;
+    a.pv[i] = PV;
+    a.m1[i] = M1;
+    a.m2[i] = M2;
+  }
+}
+
+// ------------------------------------------------------------------ launchers
+static int grid_for(const void* fn, int block, size_t smem = 0) {
+  int dev = 0, sms = 0, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, block, smem);
+  if (per < 1) per = 1;
+  return sms * per;
+}
+
+#define SB_DISPATCH_P(p, CALL)          \
+  switch (p) {                          \
+    case 4: CALL(4); break;             \
+    case 5: CALL(5); break;             \
+    case 6: CALL(6); break;             \
+    case 7: CALL(7); break;             \
+    case 8: CALL(8); break;             \
+    case 9: CALL(9); break;             \
+    case 10: CALL(10); break;           \
+    case 11: CALL(11); break;           \
+    case 12: CALL(12); break;           \
+    case 13: CALL(13); break;           \
+    case 14: CALL(14); break;           \
+    case 15: CALL(15); break;           \
+    case 16: CALL(16); break;           \
+    default: return cudaErrorInvalidValue; \
+  }
+
+cudaError_t launch_build_items(const BuildArgs& a, cudaStream_t s) {
+  const int g = grid_for(reinterpret_cast<const void*>(build_items_kernel), 256);
+  build_items_kernel<<<g, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_init(int p, uint8_t* plane, uint64_t n, const uint32_t* orig, cudaStream_t s) {
+#define SB_L(P)                                                                  \
+  {                                                                              \
+    const int g = grid_for(reinterpret_cast<const void*>(init_kernel<P>), 256); \
+    init_kernel<P><<<g, 256, 0, s>>>(plane, n, orig);                            \
+  }
+  SB_DISPATCH_P(p, SB_L)
+#undef SB_L
+  return cudaGetLastError();
+}
+
+int union_slices(int p) { return p > 10 ? 1 << (p - 10) : 1; }
+
+cudaError_t launch_union(int p, bool skip, const UnionArgs& a, cudaStream_t s) {
+#define SB_L(P)                                                                           \
+  {                                                                                       \
+    if (skip) {                                                                           \
+      static int g = grid_for(reinterpret_cast<const void*>(union_kernel<P, true>), 256);  \
+      union_kernel<P, true><<<g, 256, 0, s>>>(a);                                         \
+    } else {                                                                              \
+      static int g = grid_for(reinterpret_cast<const void*>(union_kernel<P, false>), 256); \
+      union_kernel<P, false><<<g, 256, 0, s>>>(a);                                        \
+    }                                                                                     \
+  }
+  SB_DISPATCH_P(p, SB_L)
+#undef SB_L
+  return cudaGetLastError();
+}
+
+cudaError_t launch_estimate(int p, int mode, const EstArgs& a, cudaStream_t s) {
+#define SB_L(P)                                                                                 \
+  {                                                                                             \
+    if (mode == 0) {                                                                            \
+      static int g = grid_for(reinterpret_cast<const void*>(estimate_kernel<P, 0>), 256);        \
+      estimate_kernel<P, 0><<<g, 256, 0, s>>>(a);                                               \
+    } else if (mode == 1) {                                                                     \
+      static int g = grid_for(reinterpret_cast<const void*>(estimate_kernel<P, 1>), 256);        \
+      estimate_kernel<P, 1><<<g, 256, 0, s>>>(a);                                               \
+    } else {                                                                                    \
+      static int g = grid_for(reinterpret_cast<const void*>(estimate_kernel<P, 2>), 256);        \
+      estimate_kernel<P, 2><<<g, 256, 0, s>>>(a);                                               \
+    }                                                                                           \
+  }
+  SB_DISPATCH_P(p, SB_L)
+#undef SB_L
+  return cudaGetLastError();
+}
+
+cudaError_t launch_to_packed(int p, const uint8_t* bits, uint8_t* packed, uint64_t rows, cudaStream_t s) {
+#define SB_L(P)                                                                            \
+  {                                                                                        \
+    const uint64_t groups = rows * Geo<P>::GROUPS;                                         \
+    const int g = static_cast<int>(groups / 256 + 1 < 65535 ? groups / 256 + 1 : 65535);  \
+    to_packed_kernel<P><<<g, 256, 0, s>>>(bits, packed, groups);                           \
+  }
+  SB_DISPATCH_P(p, SB_L)
+#undef SB_L
+  return cudaGetLastError();
+}
+
+cudaError_t launch_from_packed(int p, const uint8_t* packed, uint8_t* bits, uint64_t rows, cudaStream_t s) {
+#define SB_L(P)                                                                            \
+  {                                                                                        \
+    const uint64_t groups = rows * Geo<P>::GROUPS;                                         \
+    const int g = static_cast<int>(groups / 256 + 1 < 65535 ? groups / 256 + 1 : 65535);  \
+    from_packed_kernel<P><<<g, 256, 0, s>>>(packed, bits, groups);                         \
+  }
+  SB_DISPATCH_P(p, SB_L)
+#undef SB_L
+  return cudaGetLastError();
+}
+
+cudaError_t launch_metrics(const MetricArgs& a, cudaStream_t s) {
+  const int g = static_cast<int>(a.n / 256 + 1 < 65535 ? a.n / 256 + 1 : 65535);
+  metrics_kernel<<<g, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace sb

@@ -1,0 +1,721 @@
+// sb_runtime.cu -- host side of the C-ABI: device graph, HyperBall state,
+// Alg. 1 control loop, shard exchange (NCCL / same-process copies), stats.
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdlib>
+#include <thread>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/sieveball_cuda.h"
+#include "sb_device.cuh"
+#include "sb_error.h"
+#include "sb_internal.h"
+
+using sb::fail;
+
+namespace {
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(e == cudaErrorMemoryAllocation ? SB_ENOMEM : SB_ECUDA, "%s: %s", what,
+              cudaGetErrorString(e));
+}
+
+#define CK(x)                                          \
+  do {                                                 \
+    cudaError_t e_ = (x);                              \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #x);   \
+  } while (0)
+
+#define NK(x)                                                               \
+  do {                                                                      \
+    ncclResult_t r_ = (x);                                                  \
+    if (r_ != ncclSuccess) return fail(SB_ENCCL, "%s: %s", #x, ncclGetErrorString(r_)); \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+template <class T>
+void dfree(T*& p) {
+  if (p) cudaFree(p);
+  p = nullptr;
+}
+
+// Stream sync with an optional watchdog: SB_SYNC_TIMEOUT_S=<seconds> turns a
+// device hang into an SB_ECUDA error instead of a blocked host thread.
+cudaError_t sync_stream(cudaStream_t s) {
+  static const double limit = [] {
+    const char* e = getenv("SB_SYNC_TIMEOUT_S");
+    return e ? atof(e) : 0.0;
+  }();
+  if (limit <= 0.0) return cudaStreamSynchronize(s);
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    const cudaError_t e = cudaStreamQuery(s);
+    if (e != cudaErrorNotReady) return e;
+    if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > limit)
+      return cudaErrorLaunchTimeout;
+    std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+}
+
+double decode_ord(unsigned long long e) {
+  if (e == 0ull) return -INFINITY;  // no node contributed
+  unsigned long long u = (e >> 63) ? (e & 0x7fffffffffffffffull) : ~e;
+  double x;
+  memcpy(&x, &u, 8);
+  return x;
+}
+}  // namespace
+
+struct sb_graph {
+  int device = 0;
+  uint64_t n = 0, v0 = 0, v1 = 0, n_local = 0, edges_local = 0, stream_local = 0;
+  uint8_t* d_stream = nullptr;
+  uint64_t* d_rowoff = nullptr;
+  uint32_t* d_deg = nullptr;
+  uint32_t* d_orig = nullptr;
+  uint32_t chunk = 0;
+  uint64_t n_items = 0;
+  uint32_t* d_node_item = nullptr;
+  uint64_t* d_item_off = nullptr;
+  uint32_t* d_item_base = nullptr;
+  uint32_t* d_item_count = nullptr;
+  uint32_t* d_item_node = nullptr;
+  ~sb_graph() {
+    DeviceGuard dg(device);
+    dfree(d_stream); dfree(d_rowoff); dfree(d_deg); dfree(d_orig); dfree(d_node_item);
+    dfree(d_item_off); dfree(d_item_base); dfree(d_item_count); dfree(d_item_node);
+  }
+};
+
+struct sb_comm {
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0, device = 0;
+  ~sb_comm() {
+    if (comm) ncclCommDestroy(comm);
+  }
+};
+
+struct sb_hb {
+  sb_graph* g = nullptr;
+  unsigned p = 10;
+  uint32_t depth = 0, flags = 0;
+  uint64_t row = 0;
+  int slices = 1;
+  uint8_t* d_plane[2] = {nullptr, nullptr};
+  uint8_t* d_changed[2] = {nullptr, nullptr};
+  double* d_c[2] = {nullptr, nullptr};
+  double* d_sum_d = nullptr;
+  double* d_sum_d2 = nullptr;
+  double* d_lc = nullptr;
+  uint8_t* d_scratch = nullptr;
+  uint32_t* d_counter = nullptr;
+  unsigned long long* d_misc = nullptr;  // [0] work, [1] max_ord, [2] changed count
+  unsigned long long* h_misc = nullptr;  // pinned
+  uint8_t* d_tmp = nullptr;              // packed export buffer
+  uint64_t tmp_bytes = 0;
+  int latest = 0;     // plane / c / changed index holding iteration t
+  uint32_t t = 0;
+  bool converged = false, finished = false, computed = false;
+  double alpha = 0.0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  std::vector<sb_iter_stats> stats;
+  sb_iter_stats cur_stats{};
+  sb_comm* comm = nullptr;
+  std::vector<uint64_t> bounds;
+  ~sb_hb() {
+    DeviceGuard dg(g ? g->device : 0);
+    for (int i = 0; i < 2; ++i) { dfree(d_plane[i]); dfree(d_changed[i]); dfree(d_c[i]); }
+    dfree(d_sum_d); dfree(d_sum_d2); dfree(d_lc); dfree(d_scratch); dfree(d_counter);
+    dfree(d_misc); dfree(d_tmp);
+    if (h_misc) cudaFreeHost(h_misc);
+    for (auto& e : ev) if (e) cudaEventDestroy(e);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+extern "C" {
+
+const char* sb_last_error(void) { return sb::last_error(); }
+const char* sb_version(void) { return "sieveball-b200 0.1 (sm_100a)"; }
+
+int sb_device_count(int* n) {
+  int c = 0;
+  cudaError_t e = cudaGetDeviceCount(&c);
+  if (e != cudaSuccess) {
+    *n = 0;
+    return cuda_fail(e, "cudaGetDeviceCount");
+  }
+  *n = c;
+  return SB_OK;
+}
+
+int sb_check_convergence(double max_increase) { return max_increase <= 0.5 ? 1 : 0; }
+
+// ------------------------------------------------------------------ graph
+int sb_graph_create(uint64_t n, const uint64_t* offsets, const uint32_t* degrees,
+                    const uint8_t* stream, uint64_t stream_len, const uint32_t* orig_id,
+                    uint64_t node_begin, uint64_t node_end, int device, sb_graph** out) {
+  if (!out) return fail(SB_EINVAL, "sb_graph_create: out is NULL");
+  *out = nullptr;
+  if (n == 0) return fail(SB_EINVAL, "hyperball: graph empty");
+  if (n > 0xffffffffull) return fail(SB_EINVAL, "graph has more than 2^32 nodes");
+  if (!offsets || !degrees || (stream_len && !stream))
+    return fail(SB_EINVAL, "sb_graph_create: NULL array");
+  if (node_begin > node_end || node_end > n) return fail(SB_EINVAL, "sb_graph_create: bad node range");
+  if (offsets[n] != stream_len) return fail(SB_ERUNTIME, "cgraph: offsets[N] != stream length");
+  for (uint64_t v = node_begin; v < node_end; ++v)
+    if (offsets[v + 1] < offsets[v]) return fail(SB_ERUNTIME, "cgraph: offsets decrease at node %llu", (unsigned long long)v);
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(SB_ECUDA, "no CUDA device: the HyperBall path has no CPU fallback");
+  if (device < 0 || device >= ndev) return fail(SB_EINVAL, "bad device %d", device);
+  DeviceGuard dg(device);
+  auto* g = new sb_graph();
+  g->device = device;
+  g->n = n;
+  g->v0 = node_begin;
+  g->v1 = node_end;
+  g->n_local = node_end - node_begin;
+  const uint64_t b0 = offsets[node_begin], b1 = offsets[node_end];
+  g->stream_local = b1 - b0;
+  uint64_t edges = 0;
+  for (uint64_t v = node_begin; v < node_end; ++v) edges += degrees[v];
+  g->edges_local = edges;
+  auto bail = [&](int rc) { delete g; return rc; };
+#define GK(x)                                                 \
+  do {                                                        \
+    cudaError_t e_ = (x);                                     \
+    if (e_ != cudaSuccess) return bail(cuda_fail(e_, #x));    \
+  } while (0)
+  GK(cudaMalloc(&g->d_stream, g->stream_local + 64));
+  GK(cudaMemset(g->d_stream + g->stream_local, 0, 64));
+  if (g->stream_local) GK(cudaMemcpy(g->d_stream, stream + b0, g->stream_local, cudaMemcpyHostToDevice));
+  std::vector<uint64_t> ro(g->n_local + 1);
+  for (uint64_t i = 0; i <= g->n_local; ++i) ro[i] = offsets[node_begin + i] - b0;
+  GK(cudaMalloc(&g->d_rowoff, ro.size() * 8));
+  GK(cudaMemcpy(g->d_rowoff, ro.data(), ro.size() * 8, cudaMemcpyHostToDevice));
+  GK(cudaMalloc(&g->d_deg, std::max<uint64_t>(g->n_local, 1) * 4));
+  if (g->n_local) GK(cudaMemcpy(g->d_deg, degrees + node_begin, g->n_local * 4, cudaMemcpyHostToDevice));
+  if (orig_id) {
+    GK(cudaMalloc(&g->d_orig, n * 4));
+    GK(cudaMemcpy(g->d_orig, orig_id, n * 4, cudaMemcpyHostToDevice));
+  }
+  // Work items: <= chunk neighbours each, sized so the edge work splits into
+  // ~4 items per resident warp (load balance) but stays >= 512 ids (decode
+  // and merge amortisation).
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  const uint64_t target = edges / (static_cast<uint64_t>(sms) * 64 * 4);
+  g->chunk = static_cast<uint32_t>(std::min<uint64_t>(8192, std::max<uint64_t>(512, target)));
+  std::vector<uint32_t> node_item(g->n_local + 1);
+  uint64_t items = 0;
+  for (uint64_t i = 0; i < g->n_local; ++i) {
+    node_item[i] = static_cast<uint32_t>(items);
+    const uint32_t d = degrees[node_begin + i];
+    items += d ? (d + g->chunk - 1) / g->chunk : 1;
+  }
+  if (items > 0xffffffffull) return bail(fail(SB_EINVAL, "too many work items"));
+  node_item[g->n_local] = static_cast<uint32_t>(items);
+  g->n_items = items;
+  GK(cudaMalloc(&g->d_node_item, node_item.size() * 4));
+  GK(cudaMemcpy(g->d_node_item, node_item.data(), node_item.size() * 4, cudaMemcpyHostToDevice));
+  const uint64_t ni = std::max<uint64_t>(items, 1);
+  GK(cudaMalloc(&g->d_item_off, ni * 8));
+  GK(cudaMalloc(&g->d_item_base, ni * 4));
+  GK(cudaMalloc(&g->d_item_count, ni * 4));
+  GK(cudaMalloc(&g->d_item_node, ni * 4));
+  unsigned long long* d_err = nullptr;
+  GK(cudaMalloc(&d_err, 8));
+  GK(cudaMemset(d_err, 0xff, 8));
+  if (g->n_local) {
+    sb::BuildArgs a{};
+    a.stream = g->d_stream;
+    a.row_off = g->d_rowoff;
+    a.degrees = g->d_deg;
+    a.n_local = g->n_local;
+    a.n_global = n;
+    a.chunk = g->chunk;
+    a.node_item = g->d_node_item;
+    a.item_off = g->d_item_off;
+    a.item_base = g->d_item_base;
+    a.item_count = g->d_item_count;
+    a.item_node = g->d_item_node;
+    a.err_node = d_err;
+    GK(sb::launch_build_items(a, 0));
+  }
+  GK(sync_stream(0));
+  unsigned long long err = 0;
+  GK(cudaMemcpy(&err, d_err, 8, cudaMemcpyDeviceToHost));
+  cudaFree(d_err);
+  if (err != ~0ull)
+    return bail(fail(SB_ERUNTIME, "cgraph: malformed compressed row at node %llu (bad varint, "
+                                  "non-increasing or out-of-range id, or degree mismatch)",
+                     (unsigned long long)(err + node_begin)));
+#undef GK
+  *out = g;
+  return SB_OK;
+}
+
+int sb_graph_stats(const sb_graph* g, uint64_t* n_local, uint64_t* edges_local,
+                   uint64_t* stream_bytes_local, uint64_t* n_items, uint32_t* chunk) {
+  if (!g) return fail(SB_EINVAL, "NULL graph");
+  if (n_local) *n_local = g->n_local;
+  if (edges_local) *edges_local = g->edges_local;
+  if (stream_bytes_local) *stream_bytes_local = g->stream_local;
+  if (n_items) *n_items = g->n_items;
+  if (chunk) *chunk = g->chunk;
+  return SB_OK;
+}
+
+void sb_graph_destroy(sb_graph* g) { delete g; }
+
+// ------------------------------------------------------------------ HyperBall
+static int hb_init(sb_hb* h) {
+  sb_graph* g = h->g;
+  const int L = h->latest = 0;
+  h->t = 0;
+  h->converged = h->finished = h->computed = false;
+  h->stats.clear();
+  CK(sb::launch_init(static_cast<int>(h->p), h->d_plane[L], g->n, g->d_orig, h->stream));
+  CK(cudaMemsetAsync(h->d_changed[L], 1, g->n, h->stream));  // t=1 gathers every neighbour
+  CK(cudaMemsetAsync(h->d_changed[1 - L], 0, g->n, h->stream));
+  if (g->n_local) {
+    CK(cudaMemsetAsync(h->d_sum_d, 0, g->n_local * 8, h->stream));
+    CK(cudaMemsetAsync(h->d_sum_d2, 0, g->n_local * 8, h->stream));
+    sb::EstArgs e{};
+    e.plane = h->d_plane[L];
+    e.node_begin = g->v0;
+    e.n_local = g->n_local;
+    e.lc = h->d_lc;
+    e.alpha = h->alpha;
+    e.m = static_cast<double>(1u << h->p);
+    e.c_cur = h->d_c[L];
+    e.t = 0;
+    CK(sb::launch_estimate(static_cast<int>(h->p), 0, e, h->stream));
+  }
+  if (h->d_counter) CK(cudaMemsetAsync(h->d_counter, 0, std::max<uint64_t>(g->n_local, 1) * h->slices * 4, h->stream));
+  CK(sync_stream(h->stream));
+  return SB_OK;
+}
+
+int sb_hb_create(sb_graph* g, unsigned p, uint32_t depth_limit, uint32_t flags, sb_hb** out) {
+  if (!out) return fail(SB_EINVAL, "sb_hb_create: out is NULL");
+  *out = nullptr;
+  if (!g) return fail(SB_EINVAL, "sb_hb_create: NULL graph");
+  if (p < 4 || p > 16) return fail(SB_EINVAL, "hll: precision must be in [4, 16]");
+  DeviceGuard dg(g->device);
+  auto* h = new sb_hb();
+  h->g = g;
+  h->p = p;
+  h->depth = depth_limit;
+  h->flags = flags;
+  const uint32_t m = 1u << p;
+  h->row = m / 2;
+  h->slices = sb::union_slices(static_cast<int>(p));
+  // alpha_m exactly as hll.cpp:13-18
+  switch (m) {
+    case 16: h->alpha = 0.673; break;
+    case 32: h->alpha = 0.697; break;
+    case 64: h->alpha = 0.709; break;
+    default: h->alpha = 0.7213 / (1.0 + 1.079 / m); break;
+  }
+  auto bail = [&](int rc) { delete h; return rc; };
+#define HK(x)                                                 \
+  do {                                                        \
+    cudaError_t e_ = (x);                                     \
+    if (e_ != cudaSuccess) return bail(cuda_fail(e_, #x));    \
+  } while (0)
+  HK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  for (auto& e : h->ev) HK(cudaEventCreate(&e));
+  const uint64_t plane = g->n * h->row;
+  const uint64_t nl = std::max<uint64_t>(g->n_local, 1);
+  for (int i = 0; i < 2; ++i) {
+    HK(cudaMalloc(&h->d_plane[i], plane + 64));
+    HK(cudaMalloc(&h->d_changed[i], g->n));
+    HK(cudaMalloc(&h->d_c[i], nl * 8));
+  }
+  HK(cudaMalloc(&h->d_sum_d, nl * 8));
+  HK(cudaMalloc(&h->d_sum_d2, nl * 8));
+  // Linear-counting table lc[z] = m * log(m / z) built with the host libm, so
+  // the device never evaluates log (hll.cpp:35).
+  std::vector<double> lc(m + 1, 0.0);
+  const double md = static_cast<double>(m);
+  for (uint32_t z = 1; z <= m; ++z) lc[z] = md * std::log(md / static_cast<double>(z));
+  HK(cudaMalloc(&h->d_lc, lc.size() * 8));
+  HK(cudaMemcpy(h->d_lc, lc.data(), lc.size() * 8, cudaMemcpyHostToDevice));
+  const uint64_t slice_bytes = std::min<uint64_t>(h->row, 512);
+  HK(cudaMalloc(&h->d_scratch, std::max<uint64_t>(g->n_items, 1) * h->slices * slice_bytes));
+  HK(cudaMalloc(&h->d_counter, nl * h->slices * 4));
+  HK(cudaMalloc(&h->d_misc, 4 * 8));
+  HK(cudaMallocHost(&h->h_misc, 4 * 8));
+#undef HK
+  const int rc = hb_init(h);
+  if (rc != SB_OK) return bail(rc);
+  *out = h;
+  return SB_OK;
+}
+
+int sb_hb_reset(sb_hb* h) {
+  if (!h) return fail(SB_EINVAL, "NULL handle");
+  DeviceGuard dg(h->g->device);
+  return hb_init(h);
+}
+
+void* sb_hb_stream(const sb_hb* h) { return h ? static_cast<void*>(h->stream) : nullptr; }
+
+int sb_hb_step_compute(sb_hb* h, double* local_max) {
+  if (!h) return fail(SB_EINVAL, "NULL handle");
+  if (h->finished) return fail(SB_EINVAL, "hyperball: already finished (t=%u)", h->t);
+  if (h->computed) return fail(SB_EINVAL, "hyperball: step_compute called twice without finish");
+  sb_graph* g = h->g;
+  DeviceGuard dg(g->device);
+  h->t += 1;
+  const int L = h->latest, N = 1 - L;
+  const bool skip = (h->flags & SB_HB_SKIP_UNCHANGED) != 0;
+  h->cur_stats = sb_iter_stats{};
+  h->cur_stats.t = h->t;
+  CK(cudaMemsetAsync(h->d_misc, 0, 4 * 8, h->stream));
+  CK(cudaEventRecord(h->ev[0], h->stream));
+  if (g->n_local) {
+    CK(cudaMemsetAsync(h->d_changed[N] + g->v0, 0, g->n_local, h->stream));
+    sb::UnionArgs u{};
+    u.stream = g->d_stream;
+    u.item_off = g->d_item_off;
+    u.item_base = g->d_item_base;
+    u.item_count = g->d_item_count;
+    u.item_node = g->d_item_node;
+    u.node_item = g->d_node_item;
+    u.n_items = g->n_items;
+    u.node_begin = g->v0;
+    u.cur = h->d_plane[L];
+    u.next = h->d_plane[N];
+    u.scratch = h->d_scratch;
+    u.node_counter = h->d_counter;
+    u.changed_out = h->d_changed[N];
+    u.changed_in = h->d_changed[L];
+    u.work = h->d_misc;
+    CK(cudaEventRecord(h->ev[1], h->stream));
+    CK(sb::launch_union(static_cast<int>(h->p), skip, u, h->stream));
+    CK(cudaEventRecord(h->ev[2], h->stream));
+    sb::EstArgs e{};
+    e.plane = h->d_plane[N];
+    e.node_begin = g->v0;
+    e.n_local = g->n_local;
+    e.lc = h->d_lc;
+    e.alpha = h->alpha;
+    e.m = static_cast<double>(1u << h->p);
+    e.c_prev = h->d_c[L];
+    e.c_cur = h->d_c[N];
+    e.sum_d = h->d_sum_d;
+    e.sum_d2 = h->d_sum_d2;
+    e.changed = h->d_changed[N];
+    e.t = h->t;
+    e.max_ord = h->d_misc + 1;
+    e.changed_count = h->d_misc + 2;
+    CK(sb::launch_estimate(static_cast<int>(h->p), skip ? 2 : 1, e, h->stream));
+  } else {
+    CK(cudaEventRecord(h->ev[1], h->stream));
+    CK(cudaEventRecord(h->ev[2], h->stream));
+  }
+  CK(cudaEventRecord(h->ev[3], h->stream));
+  CK(cudaMemcpyAsync(h->h_misc, h->d_misc, 4 * 8, cudaMemcpyDeviceToHost, h->stream));
+  CK(sync_stream(h->stream));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, h->ev[1], h->ev[2]);
+  h->cur_stats.union_ms = ms;
+  cudaEventElapsedTime(&ms, h->ev[2], h->ev[3]);
+  h->cur_stats.estimate_ms = ms;
+  cudaEventElapsedTime(&ms, h->ev[0], h->ev[3]);
+  h->cur_stats.step_ms = ms;
+  h->cur_stats.changed_nodes = h->h_misc[2];
+  h->computed = true;
+  if (local_max) *local_max = decode_ord(h->h_misc[1]);
+  return SB_OK;
+}
+
+int sb_hb_step_finish(sb_hb* h, double global_max, int* converged, int* finished) {
+  if (!h) return fail(SB_EINVAL, "NULL handle");
+  if (!h->computed) return fail(SB_EINVAL, "hyperball: step_finish without step_compute");
+  h->computed = false;
+  // Alg. 1: converged -> break (no swap); t == d -> stop.
+  h->converged = sb_check_convergence(global_max) != 0;
+  h->finished = h->converged || (h->depth != 0 && h->t == h->depth);
+  h->latest = 1 - h->latest;  // registers / c of iteration t become "latest"
+  h->cur_stats.max_increase = global_max;
+  h->stats.push_back(h->cur_stats);
+  if (converged) *converged = h->converged;
+  if (finished) *finished = h->finished;
+  return SB_OK;
+}
+
+int sb_hb_exchange_local(sb_hb* const* hs, int count) {
+  if (!hs || count < 1) return fail(SB_EINVAL, "sb_hb_exchange_local: no handles");
+  for (int i = 0; i < count; ++i) {
+    if (!hs[i] || !hs[i]->computed) return fail(SB_EINVAL, "exchange: handle %d not computed", i);
+    if (hs[i]->g->n != hs[0]->g->n || hs[i]->p != hs[0]->p) return fail(SB_EINVAL, "exchange: shape mismatch");
+  }
+  for (int i = 0; i < count; ++i) {
+    const sb_hb* src = hs[i];
+    const sb_graph* gs = src->g;
+    if (!gs->n_local) continue;
+    const int sN = 1 - src->latest;
+    for (int j = 0; j < count; ++j) {
+      if (j == i) continue;
+      sb_hb* dst = hs[j];
+      const int dN = 1 - dst->latest;
+      DeviceGuard dg(dst->g->device);
+      CK(cudaMemcpyPeerAsync(dst->d_plane[dN] + gs->v0 * src->row, dst->g->device,
+                             src->d_plane[sN] + gs->v0 * src->row, gs->device,
+                             gs->n_local * src->row, dst->stream));
+      CK(cudaMemcpyPeerAsync(dst->d_changed[dN] + gs->v0, dst->g->device, src->d_changed[sN] + gs->v0,
+                             gs->device, gs->n_local, dst->stream));
+    }
+  }
+  for (int j = 0; j < count; ++j) {
+    DeviceGuard dg(hs[j]->g->device);
+    CK(sync_stream(hs[j]->stream));
+  }
+  return SB_OK;
+}
+
+static int exchange_nccl(sb_hb* h, double* gmax) {
+  sb_comm* c = h->comm;
+  sb_graph* g = h->g;
+  const int N = 1 - h->latest;
+  CK(cudaEventRecord(h->ev[0], h->stream));
+  NK(ncclGroupStart());
+  for (int r = 0; r < c->nranks; ++r) {
+    const uint64_t a = h->bounds[r], b = h->bounds[r + 1];
+    if (b == a) continue;
+    uint8_t* rows = h->d_plane[N] + a * h->row;
+    NK(ncclBroadcast(rows, rows, (b - a) * h->row, ncclUint8, r, c->comm, h->stream));
+    uint8_t* ch = h->d_changed[N] + a;
+    NK(ncclBroadcast(ch, ch, b - a, ncclUint8, r, c->comm, h->stream));
+  }
+  NK(ncclGroupEnd());
+  NK(ncclAllReduce(h->d_misc + 1, h->d_misc + 1, 1, ncclUint64, ncclMax, c->comm, h->stream));
+  CK(cudaEventRecord(h->ev[1], h->stream));
+  CK(cudaMemcpyAsync(h->h_misc + 1, h->d_misc + 1, 8, cudaMemcpyDeviceToHost, h->stream));
+  CK(sync_stream(h->stream));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]);
+  h->cur_stats.exchange_ms = ms;
+  *gmax = decode_ord(h->h_misc[1]);
+  (void)g;
+  return SB_OK;
+}
+
+int sb_hb_step(sb_hb* h, double* max_increase, int* converged, int* finished) {
+  double mx = 0.0;
+  int rc = sb_hb_step_compute(h, &mx);
+  if (rc) return rc;
+  if (h->comm && h->comm->nranks > 1) {
+    DeviceGuard dg(h->g->device);
+    rc = exchange_nccl(h, &mx);
+    if (rc) {
+      h->computed = false;
+      return rc;
+    }
+  }
+  if (max_increase) *max_increase = mx;
+  return sb_hb_step_finish(h, mx, converged, finished);
+}
+
+int sb_hb_run(sb_hb* h, uint32_t* iterations, int* converged) {
+  if (!h) return fail(SB_EINVAL, "NULL handle");
+  int conv = 0, fin = h->finished ? 1 : 0;
+  while (!fin) {
+    const int rc = sb_hb_step(h, nullptr, &conv, &fin);
+    if (rc) return rc;
+  }
+  if (iterations) *iterations = h->t;
+  if (converged) *converged = h->converged;
+  return SB_OK;
+}
+
+static int ensure_tmp(sb_hb* h, uint64_t bytes) {
+  if (h->tmp_bytes >= bytes) return SB_OK;
+  dfree(h->d_tmp);
+  h->tmp_bytes = 0;
+  CK(cudaMalloc(&h->d_tmp, bytes));
+  h->tmp_bytes = bytes;
+  return SB_OK;
+}
+
+int sb_hb_read_registers(const sb_hb* hc, int which, uint64_t v0, uint64_t v1, uint8_t* dst) {
+  sb_hb* h = const_cast<sb_hb*>(hc);
+  if (!h || !dst) return fail(SB_EINVAL, "NULL argument");
+  if (v0 > v1 || v1 > h->g->n) return fail(SB_EINVAL, "bad row range");
+  if (which != SB_REGS_LATEST && which != SB_REGS_PREVIOUS) return fail(SB_EINVAL, "bad plane selector");
+  if (v0 == v1) return SB_OK;
+  DeviceGuard dg(h->g->device);
+  const int idx = which == SB_REGS_LATEST ? h->latest : 1 - h->latest;
+  const uint64_t bytes = (v1 - v0) * h->row;
+  int rc = ensure_tmp(h, bytes);
+  if (rc) return rc;
+  CK(sb::launch_to_packed(static_cast<int>(h->p), h->d_plane[idx] + v0 * h->row, h->d_tmp, v1 - v0, h->stream));
+  CK(cudaMemcpyAsync(dst, h->d_tmp, bytes, cudaMemcpyDeviceToHost, h->stream));
+  CK(sync_stream(h->stream));
+  return SB_OK;
+}
+
+int sb_hb_set_registers(sb_hb* h, const uint8_t* packed) {
+  if (!h || !packed) return fail(SB_EINVAL, "NULL argument");
+  if (h->computed) return fail(SB_EINVAL, "set_registers during a step");
+  sb_graph* g = h->g;
+  DeviceGuard dg(g->device);
+  const uint64_t bytes = g->n * h->row;
+  int rc = ensure_tmp(h, bytes);
+  if (rc) return rc;
+  const int L = h->latest;
+  CK(cudaMemcpyAsync(h->d_tmp, packed, bytes, cudaMemcpyHostToDevice, h->stream));
+  CK(sb::launch_from_packed(static_cast<int>(h->p), h->d_tmp, h->d_plane[L], g->n, h->stream));
+  CK(cudaMemsetAsync(h->d_changed[L], 1, g->n, h->stream));
+  if (g->n_local) {
+    sb::EstArgs e{};
+    e.plane = h->d_plane[L];
+    e.node_begin = g->v0;
+    e.n_local = g->n_local;
+    e.lc = h->d_lc;
+    e.alpha = h->alpha;
+    e.m = static_cast<double>(1u << h->p);
+    e.c_cur = h->d_c[L];
+    CK(sb::launch_estimate(static_cast<int>(h->p), 0, e, h->stream));
+  }
+  CK(sync_stream(h->stream));
+  h->finished = h->converged = false;
+  return SB_OK;
+}
+
+int sb_hb_read_state(const sb_hb* h, double* c_latest, double* c_previous, double* sum_d,
+                     double* sum_d2, uint8_t* changed, uint32_t* t, int* converged, int* finished) {
+  if (!h) return fail(SB_EINVAL, "NULL handle");
+  const sb_graph* g = h->g;
+  DeviceGuard dg(g->device);
+  const uint64_t nb = g->n_local * 8;
+  if (g->n_local) {
+    if (c_latest) CK(cudaMemcpy(c_latest, h->d_c[h->latest], nb, cudaMemcpyDeviceToHost));
+    if (c_previous) CK(cudaMemcpy(c_previous, h->d_c[1 - h->latest], nb, cudaMemcpyDeviceToHost));
+    if (sum_d) CK(cudaMemcpy(sum_d, h->d_sum_d, nb, cudaMemcpyDeviceToHost));
+    if (sum_d2) CK(cudaMemcpy(sum_d2, h->d_sum_d2, nb, cudaMemcpyDeviceToHost));
+    if (changed) CK(cudaMemcpy(changed, h->d_changed[h->latest] + g->v0, g->n_local, cudaMemcpyDeviceToHost));
+  }
+  if (t) *t = h->t;
+  if (converged) *converged = h->converged;
+  if (finished) *finished = h->finished;
+  return SB_OK;
+}
+
+int sb_hb_metrics(const sb_hb* hc, const uint32_t* nv, const uint32_t* deg, double* md, double* ihh,
+                  double* tekl, double* pv, double* m1, double* m2) {
+  sb_hb* h = const_cast<sb_hb*>(hc);
+  if (!h || !nv || !deg) return fail(SB_EINVAL, "NULL argument");
+  const uint64_t n = h->g->n_local;
+  if (!n) return SB_OK;
+  DeviceGuard dg(h->g->device);
+  // one device block: [nv u32 | deg u32 | 6 x f64 outputs]
+  const uint64_t bytes = n * 8 + 6 * n * 8;
+  int rc = ensure_tmp(h, bytes);
+  if (rc) return rc;
+  uint32_t* d_nv = reinterpret_cast<uint32_t*>(h->d_tmp);
+  uint32_t* d_deg = d_nv + n;
+  double* o = reinterpret_cast<double*>(h->d_tmp + n * 8);
+  CK(cudaMemcpyAsync(d_nv, nv, n * 4, cudaMemcpyHostToDevice, h->stream));
+  CK(cudaMemcpyAsync(d_deg, deg, n * 4, cudaMemcpyHostToDevice, h->stream));
+  sb::MetricArgs a{};
+  a.n = n;
+  a.sum_d = h->d_sum_d;
+  a.sum_d2 = h->d_sum_d2;
+  a.nv = d_nv;
+  a.deg = d_deg;
+  a.md = o;
+  a.ihh = o + n;
+  a.tekl = o + 2 * n;
+  a.pv = o + 3 * n;
+  a.m1 = o + 4 * n;
+  a.m2 = o + 5 * n;
+  CK(sb::launch_metrics(a, h->stream));
+  double* outs[6] = {md, ihh, tekl, pv, m1, m2};
+  for (int i = 0; i < 6; ++i)
+    if (outs[i]) CK(cudaMemcpyAsync(outs[i], o + i * n, n * 8, cudaMemcpyDeviceToHost, h->stream));
+  CK(sync_stream(h->stream));
+  return SB_OK;
+}
+
+int sb_hb_stats(const sb_hb* h, sb_iter_stats* out, uint32_t cap, uint32_t* count) {
+  if (!h) return fail(SB_EINVAL, "NULL handle");
+  const uint32_t n = static_cast<uint32_t>(h->stats.size());
+  if (out)
+    for (uint32_t i = 0; i < n && i < cap; ++i) out[i] = h->stats[i];
+  if (count) *count = n;
+  return SB_OK;
+}
+
+void sb_hb_destroy(sb_hb* h) { delete h; }
+
+// ------------------------------------------------------------------ NCCL
+int sb_comm_unique_id(void* id_out) {
+  if (!id_out) return fail(SB_EINVAL, "NULL id");
+  static_assert(sizeof(ncclUniqueId) == SB_COMM_ID_BYTES, "ncclUniqueId size");
+  ncclUniqueId id;
+  NK(ncclGetUniqueId(&id));
+  memcpy(id_out, &id, sizeof(id));
+  return SB_OK;
+}
+
+int sb_comm_create(int nranks, int rank, const void* id, int device, sb_comm** out) {
+  if (!out || !id) return fail(SB_EINVAL, "NULL argument");
+  *out = nullptr;
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(SB_EINVAL, "bad rank/nranks");
+  DeviceGuard dg(device);
+  auto* c = new sb_comm();
+  c->nranks = nranks;
+  c->rank = rank;
+  c->device = device;
+  ncclUniqueId uid;
+  memcpy(&uid, id, sizeof(uid));
+  const ncclResult_t r = ncclCommInitRank(&c->comm, nranks, uid, rank);
+  if (r != ncclSuccess) {
+    c->comm = nullptr;
+    delete c;
+    return fail(SB_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+  }
+  *out = c;
+  return SB_OK;
+}
+
+int sb_hb_attach_comm(sb_hb* h, sb_comm* c, const uint64_t* bounds) {
+  if (!h || !c || !bounds) return fail(SB_EINVAL, "NULL argument");
+  if (bounds[0] != 0 || bounds[c->nranks] != h->g->n) return fail(SB_EINVAL, "bounds must cover [0, N)");
+  for (int r = 0; r < c->nranks; ++r)
+    if (bounds[r + 1] < bounds[r]) return fail(SB_EINVAL, "bounds not monotone");
+  if (bounds[c->rank] != h->g->v0 || bounds[c->rank + 1] != h->g->v1)
+    return fail(SB_EINVAL, "graph range does not match this rank's bounds");
+  if (c->device != h->g->device) return fail(SB_EINVAL, "communicator device != graph device");
+  h->comm = c;
+  h->bounds.assign(bounds, bounds + c->nranks + 1);
+  return SB_OK;
+}
+
+void sb_comm_destroy(sb_comm* c) { delete c; }
+
+}  // extern "C"

@@ -1,0 +1,246 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the CPU oracle.
+
+Bar (BASELINE.json north_star): HLL registers bit-exact after EVERY
+iteration; c, sum_d, sum_d2, max increase and the iteration count identical
+(stronger than the 1e-6 metric tolerance); metrics within 1e-6 relative.
+"""
+import hashlib
+import json
+import os
+import struct
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2604_08374_b200 import CompressedCsr, DeviceGraph, HllParams, HyperBall
+from tests.golden.make_golden import ArrCsr
+
+pytestmark = pytest.mark.gpu
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "reference_golden.json")))
+
+
+def f64(h):
+    return struct.unpack("<d", bytes.fromhex(h))[0]
+
+
+def csr_of(adj):
+    return CompressedCsr.from_adjacency(adj)
+
+
+def lockstep(csr, p, depth, O, skip=False, threads=0):
+    """Run GPU and oracle side by side; assert bit-exact state after every iteration."""
+    hb = HyperBall(csr, HllParams(p), depth, skip_unchanged=skip)
+    n = csr.n
+    cur, c_prev = O.hb_init(n, p)
+    assert np.array_equal(hb.registers(), cur), "init registers"
+    st = hb.state()
+    assert np.array_equal(st.c_curr, c_prev), "c_0"
+    nxt = np.zeros_like(cur)
+    c_cur = np.zeros(n)
+    sd, sd2 = np.zeros(n), np.zeros(n)
+    t = 0
+    while True:
+        t += 1
+        mg = hb.iterate_once()
+        mo = O.hb_iterate(csr, p, t, cur, nxt, c_prev, c_cur, sd, sd2, threads=threads)
+        regs = hb.registers()
+        if not np.array_equal(regs, nxt):
+            bad = np.nonzero(regs != nxt)[0]
+            raise AssertionError(f"registers differ at t={t}: {bad.size} bytes, first node {bad[0] // (1 << (p - 1))}")
+        s = hb.state()
+        assert s.t == t
+        assert np.array_equal(s.c_curr, c_cur), f"c_t at t={t}"
+        assert np.array_equal(s.c_prev, c_prev), f"c_(t-1) at t={t}"
+        assert np.array_equal(s.sum_d, sd), f"sum_d at t={t}"
+        assert np.array_equal(s.sum_d2, sd2), f"sum_d2 at t={t}"
+        assert mg == mo, f"max increase at t={t}: {mg} vs {mo}"
+        conv = mo <= 0.5
+        fin = conv or (depth is not None and t == depth)
+        assert s.converged == conv and s.finished == fin
+        if fin:
+            break
+        cur, nxt = nxt, cur
+        c_prev, c_cur = c_cur, c_prev
+    return t
+
+
+@pytest.fixture(scope="module")
+def c1():
+    # C1: 64x64 grid, 20 rectangles of 2..9 cells, unlimited radius
+    return CompressedCsr.synth_grid(64, 64, 20, 2, 9, 20261017, 0)
+
+
+# ---------------------------------------------------------------- golden (reference-generated) fixtures
+@pytest.mark.parametrize("case", range(len(GOLD["hyperball"])))
+def test_gpu_matches_reference_golden(case):
+    c = GOLD["hyperball"][case]
+    csr = csr_of(GOLD["graphs"][c["graph"]])
+    hb = HyperBall(csr, HllParams(c["p"]), c["depth"] or None)
+    hashes, maxes = [], []
+    while not hb.finished:
+        maxes.append(hb.iterate_once())
+        hashes.append(hashlib.sha256(hb.registers().tobytes()).hexdigest())
+    st = hb.state()
+    assert st.t == c["iterations"] and st.converged == c["converged"]
+    assert hashes == c["register_sha256_per_iteration"]
+    assert maxes == [f64(x) for x in c["max_increase"]]
+    if isinstance(c["sum_d"], list):
+        assert st.sum_d.tolist() == [f64(x) for x in c["sum_d"]]
+    else:
+        assert hashlib.sha256(st.sum_d.tobytes()).hexdigest() == c["sum_d"]
+    assert hashlib.sha256(st.sum_d2.tobytes()).hexdigest() == c["sum_d2_sha256"]
+    assert hashlib.sha256(st.c_curr.tobytes()).hexdigest() == c["c_sha256"]
+
+
+# ---------------------------------------------------------------- lockstep vs oracle
+@pytest.mark.parametrize("p", [4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14])
+def test_gpu_lockstep_c1_depth3(c1, oracle_best, p):
+    assert lockstep(c1, p, 3, oracle_best) == 3
+
+
+@pytest.mark.parametrize("depth", [1, 2, None])
+def test_gpu_lockstep_c1_p10(c1, oracle_best, depth):
+    lockstep(c1, 10, depth, oracle_best)
+
+
+@pytest.mark.parametrize("p", [8, 10, 12])
+def test_gpu_skip_unchanged_bit_exact(c1, oracle_best, p):
+    lockstep(c1, p, None, oracle_best, skip=True)
+
+
+@pytest.mark.parametrize("p", [15, 16])
+def test_gpu_lockstep_large_p(oracle_best, p):
+    g = CompressedCsr.synth_grid(24, 24, 6, 2, 5, 3, 0)
+    lockstep(g, p, 2, oracle_best)
+
+
+def test_gpu_lockstep_radius_and_obstacles(oracle_best):
+    g = CompressedCsr.synth_grid(90, 70, 40, 2, 8, 99, 15 * 15)
+    lockstep(g, 10, None, oracle_best)
+
+
+def test_gpu_edge_cases(oracle_best):
+    # isolated nodes, empty rows mixed with a clique, a star
+    adj = [[], [2, 3, 4], [1, 3, 4], [1, 2, 4], [1, 2, 3], [], [7], [6]]
+    for p in (4, 10, 16):
+        lockstep(csr_of(adj), p, None, oracle_best)
+    lockstep(csr_of([[]]), 10, None, oracle_best)
+
+
+# ---------------------------------------------------------------- random registers (all nibble values)
+@pytest.mark.parametrize("p", list(range(4, 17)))
+def test_gpu_random_registers_one_step(oracle_best, p):
+    g = CompressedCsr.synth_grid(20, 20, 4, 2, 4, p, 0)
+    n, rb = g.n, (1 << p) // 2
+    rng = np.random.default_rng(p)
+    regs = rng.integers(0, 256, n * rb, dtype=np.uint8)
+    regs[rng.random(regs.size) < 0.3] = 0
+    hb = HyperBall(g, p, None)
+    hb.set_registers(regs)
+    assert np.array_equal(hb.registers(), regs), "packed <-> bit-sliced round trip"
+    c_prev = np.array([oracle_best.estimate(regs[v * rb:(v + 1) * rb].copy(), p) for v in range(n)])
+    assert np.array_equal(hb.state().c_curr, c_prev)
+    nxt = np.zeros_like(regs)
+    c_cur, sd, sd2 = np.zeros(n), np.zeros(n), np.zeros(n)
+    mo = oracle_best.hb_iterate(g, p, 1, regs, nxt, c_prev, c_cur, sd, sd2)
+    mg = hb.iterate_once()
+    assert np.array_equal(hb.registers(), nxt)
+    s = hb.state()
+    assert np.array_equal(s.c_curr, c_cur) and np.array_equal(s.sum_d, sd) and mg == mo
+
+
+# ---------------------------------------------------------------- sharding (same process, one GPU)
+@pytest.mark.parametrize("parts", [2, 3, 5])
+def test_gpu_local_shards_identical(c1, parts):
+    p = 10
+    ref = HyperBall(c1, p, None)
+    ref.run()
+    bounds = c1.partition(parts)
+    shards = [HyperBall(c1, p, None, node_range=(int(bounds[i]), int(bounds[i + 1]))) for i in range(parts)]
+    while True:
+        mx = max(s.step_compute() for s in shards)
+        HyperBall.exchange_local(shards)
+        fins = [s.step_finish(mx)[1] for s in shards]
+        assert len(set(fins)) == 1
+        if fins[0]:
+            break
+    whole = ref.state(with_registers=True)
+    for i, s in enumerate(shards):
+        st = s.state()
+        a, b = int(bounds[i]), int(bounds[i + 1])
+        assert st.t == whole.t
+        assert np.array_equal(st.sum_d, whole.sum_d[a:b])
+        assert np.array_equal(st.c_curr, whole.c_curr[a:b])
+        assert np.array_equal(s.registers(), whole.registers)  # full replica everywhere
+
+
+# ---------------------------------------------------------------- metrics, errors, determinism
+def test_gpu_metrics(c1, oracle_port):
+    hb = HyperBall(c1, 10, None)
+    hb.run()
+    s = hb.state()
+    nv = c1.node_count_of_component()
+    m = hb.metrics(nv, c1.degrees)
+    o = oracle_port.metrics(s.sum_d, s.sum_d2, nv, c1.degrees)
+    for k in m:
+        a, b = m[k], o[k]
+        assert np.array_equal(np.isnan(a), np.isnan(b))
+        ok = ~np.isnan(a)
+        assert np.allclose(a[ok], b[ok], rtol=1e-6, atol=0), k
+
+
+def test_gpu_errors():
+    g = csr_of([[1], [0]])
+    with pytest.raises(ValueError):
+        HyperBall(g, 3)
+    with pytest.raises(ValueError):
+        HyperBall(g, 17)
+    # truncated varint
+    with pytest.raises(RuntimeError):
+        DeviceGraph.from_raw(2, [0, 1, 2], [1, 1], [0x81, 0x80])
+    # degree mismatch (row has 2 ids, degree says 1)
+    with pytest.raises(RuntimeError):
+        DeviceGraph.from_raw(3, [0, 2, 3, 4], [1, 1, 1], [1, 1, 0, 1])
+    # non-increasing (delta 0)
+    with pytest.raises(RuntimeError):
+        DeviceGraph.from_raw(3, [0, 2, 3, 4], [2, 1, 1], [1, 0, 0, 1])
+    # id out of range
+    with pytest.raises(RuntimeError):
+        DeviceGraph.from_raw(2, [0, 1, 2], [1, 1], [5, 0])
+    # varint longer than 5 bytes
+    with pytest.raises(RuntimeError):
+        DeviceGraph.from_raw(2, [0, 6, 7], [1, 1], [0x81, 0x80, 0x80, 0x80, 0x80, 0x00, 0x00])
+    hb = HyperBall(g, 10, 1)
+    hb.run()
+    with pytest.raises(ValueError):
+        hb.iterate_once()  # already finished
+
+
+def test_gpu_determinism_and_reset(c1):
+    hb = HyperBall(c1, 10, None)
+    hb.run()
+    a = hb.state(with_registers=True)
+    hb.reset()
+    assert hb.t == 0
+    hb.run()
+    b = hb.state(with_registers=True)
+    assert np.array_equal(a.registers, b.registers) and np.array_equal(a.sum_d, b.sum_d)
+
+
+def test_gpu_hilbert_permutation_equivariance(c1):
+    """Hashing original ids makes reordering layout-only."""
+    h = c1.hilbert_reorder()
+    a = HyperBall(c1, 10, None)
+    a.run()
+    b = HyperBall(h, 10, None)
+    b.run()
+    sa, sb_ = a.state(True), b.state(True)
+    inv = h.hilbert_inverse.astype(np.int64)
+    assert sa.t == sb_.t
+    assert np.array_equal(sb_.sum_d, sa.sum_d[inv])
+    rb = 512
+    ra = sa.registers.reshape(-1, rb)
+    rbm = sb_.registers.reshape(-1, rb)
+    assert np.array_equal(rbm, ra[inv])

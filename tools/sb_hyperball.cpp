@@ -1,0 +1,82 @@
+// sb_hyperball -- C++ host driver over the facade (the reference's analyze /
+// bench shapes): builds or loads a graph, runs HyperBall on
+// one GPU, prints per-iteration timings and a metrics summary.
+//
+//   sb_hyperball synth ROWS COLS RECTS RMIN RMAX SEED RADIUS2 P DEPTH [--skip]
+//   sb_hyperball load  FILE.vgacsr P DEPTH [--skip]
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+#include "sieveball/hyperball_cuda.hpp"
+
+using namespace sieveball::cuda;
+
+int main(int argc, char** argv) {
+  try {
+    if (argc < 2) {
+      std::fprintf(stderr, "usage: %s synth ROWS COLS RECTS RMIN RMAX SEED RADIUS2 P DEPTH [--skip]\n"
+                           "       %s load FILE P DEPTH [--skip]\n", argv[0], argv[0]);
+      return 2;
+    }
+    const std::string mode = argv[1];
+    bool skip = std::strcmp(argv[argc - 1], "--skip") == 0;
+    auto t0 = std::chrono::steady_clock::now();
+    std::optional<CompressedCsr> g;
+    unsigned p = 10;
+    uint32_t depth = 0;
+    if (mode == "synth" && argc >= 11) {
+      g = CompressedCsr::synth_grid(std::atoi(argv[2]), std::atoi(argv[3]), std::atoi(argv[4]), std::atoi(argv[5]),
+                                    std::atoi(argv[6]), std::strtoull(argv[7], nullptr, 10),
+                                    std::strtoull(argv[8], nullptr, 10));
+      p = std::atoi(argv[9]);
+      depth = std::atoi(argv[10]);
+    } else if (mode == "load" && argc >= 5) {
+      g = CompressedCsr::load_vgacsr(argv[2]);
+      p = std::atoi(argv[3]);
+      depth = std::atoi(argv[4]);
+    } else {
+      std::fprintf(stderr, "bad arguments\n");
+      return 2;
+    }
+    auto t1 = std::chrono::steady_clock::now();
+    HllParams P(p);
+    HyperBall hb(*g, P, depth ? std::optional<uint32_t>(depth) : std::nullopt, 0, skip);
+    auto t2 = std::chrono::steady_clock::now();
+    const uint32_t it = hb.run();
+    auto t3 = std::chrono::steady_clock::now();
+    const auto st = hb.stats();
+    const double ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); }(t2, t3);
+    std::printf("graph: N=%llu |E|=%llu stream=%llu B (build %.1f ms, upload+init %.1f ms)\n",
+                (unsigned long long)g->node_count(), (unsigned long long)g->edge_count(),
+                (unsigned long long)g->desc().stream_len,
+                std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                std::chrono::duration<double, std::milli>(t2 - t1).count());
+    for (const auto& s : st)
+      std::printf("t=%u union=%.3f ms estimate=%.3f ms changed=%llu max_inc=%.4f\n", s.t, s.union_ms, s.estimate_ms,
+                  (unsigned long long)s.changed_nodes, s.max_increase);
+    const double upd = static_cast<double>(g->edge_count()) * P.m * it;
+    std::printf("iterations=%u hyperball=%.3f ms  edge-register updates/s=%.3e\n", it, ms, upd / (ms * 1e-3));
+    const HyperBallState s = hb.state(false);
+    const auto& d = g->desc();
+    double md_sum = 0;
+    uint64_t cnt = 0;
+    for (uint64_t v = 0; v < d.n; ++v) {
+      const double md = metrics::mean_depth(s.sum_d[v], d.component_sizes[d.component_id[v]]);
+      if (!std::isnan(md)) {
+        md_sum += md;
+        ++cnt;
+      }
+    }
+    std::printf("mean MD over %llu nodes = %.6f\n", (unsigned long long)cnt, cnt ? md_sum / cnt : NAN);
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    std::fprintf(stderr, "invalid argument: %s\n", e.what());
+    return 2;
+  } catch (const std::exception& e) {
+    std::fprintf(stderr, "error: %s\n", e.what());
+    return 1;
+  }
+}
