@@ -193,4 +193,127 @@ __device__ __forceinline__ DecodeOut decode_step(const uint8_t* __restrict__ str
   return o;
 }
 
+// ---- 4-bytes-per-lane LEB128 decode (hot path) ------------------------
+// A 128-byte window at `pos` (a varint boundary); lane L holds bytes
+// 4L..4L+3.  Because every byte's payload lands in exactly one delta, the
+// absolute id at a terminator j is
+//     base + sum_{k <= j} (b_k & 0x7f) << (7 * d_k),
+// d_k = number of continuation bytes immediately preceding byte k -- a plain
+// prefix sum over bytes, no segmented reduction.  d_k needs at most 4 bytes
+// of look-back (ids < 2^32 -> varints <= 5 bytes), i.e. the previous lane's
+// word.  Only the first `remaining` terminators are taken; the window's
+// trailing partial varint is re-read by the next step.
+struct Decode4 {
+  int wanted;     // terminators consumed from the item in this window
+  int count;      // ids written to buf (== wanted unless SKIP filtered some)
+  int advance;    // bytes consumed (through the last wanted terminator)
+  uint32_t last;  // id of the last wanted terminator (next base)
+};
+
+__device__ __forceinline__ uint32_t ld_stream_word(const uint8_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
+// Writes the kept ids (compacted, in order) to buf[0..count) and pads
+// buf[count..count+PAD) with the last one.  Needs the stream padded by >= 136 B.
+__device__ __forceinline__ uint32_t sel4(const uint32_t (&v)[4], int k) {
+  return k <= 0 ? v[0] : k == 1 ? v[1] : k == 2 ? v[2] : v[3];
+}
+
+// buf must hold 128 + PAD entries.
+template <bool SKIP, int PAD>
+__device__ __forceinline__ Decode4 decode_step4(const uint8_t* __restrict__ stream, uint64_t pos,
+                                                uint32_t remaining, uint32_t base, const uint8_t* changed,
+                                                uint32_t* buf, int lane) {
+  const uint8_t* al = stream + (pos & ~3ull) + 4 * lane;
+  const uint32_t w0 = ld_stream_word(al);
+  const uint32_t w1 = ld_stream_word(al + 4);
+  const uint32_t w = __funnelshift_r(w0, w1, static_cast<uint32_t>(pos & 3) * 8);
+  uint32_t wp = __shfl_up_sync(FULL, w, 1);
+  if (lane == 0) wp = 0;  // the window starts on a varint boundary
+  const uint32_t F = w & 0x80808080u, Fp = wp & 0x80808080u;
+  // run of continuation flags before each byte of w (1..4 bytes back)
+  const uint32_t m1 = __funnelshift_l(Fp, F, 8);
+  const uint32_t m2 = m1 & __funnelshift_l(Fp, F, 16);
+  const uint32_t m3 = m2 & __funnelshift_l(Fp, F, 24);
+  const uint32_t m4 = m3 & Fp;
+  const uint32_t D = (m1 >> 7) + (m2 >> 7) + (m3 >> 7) + (m4 >> 7);  // per-byte d_k in 0..4
+  uint32_t c[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) c[k] = ((w >> (8 * k)) & 0x7fu) << (7 * ((D >> (8 * k)) & 0xffu));
+  const uint32_t p1 = c[0] + c[1], p2 = p1 + c[2], lane_sum = p2 + c[3];
+  uint32_t incl = lane_sum;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(FULL, incl, d);
+    if (lane >= d) incl += y;
+  }
+  const uint32_t excl = base + incl - lane_sum;
+  const uint32_t id[4] = {excl + c[0], excl + p1, excl + p2, excl + lane_sum};
+  const uint32_t T = ~w & 0x80808080u;  // terminator flags
+  const uint32_t ltm = (1u << lane) - 1u;
+  // global rank of each terminator = terminators in lower lanes + earlier bytes of this lane
+  uint32_t below = 0, tot = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint32_t B = __ballot_sync(FULL, (T >> (8 * k + 7)) & 1u);
+    below += __popc(B & ltm);
+    tot += __popc(B);
+  }
+  bool want[4];
+  uint32_t r = below;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const bool t = (T >> (8 * k + 7)) & 1u;
+    want[k] = t && r < remaining;
+    r += t;
+  }
+  // position of the last wanted terminator
+  int lastk = -1;
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (want[k]) lastk = k;
+  const uint32_t anyw = __ballot_sync(FULL, lastk >= 0);
+  Decode4 o;
+  o.wanted = static_cast<int>(tot < remaining ? tot : remaining);
+  o.count = 0;
+  o.advance = 0;
+  o.last = base;
+  if (anyw == 0) return o;
+  const int L = 31 - __clz(anyw);
+  const int lk = __shfl_sync(FULL, lastk, L);
+  o.advance = 4 * L + lk + 1;
+  o.last = __shfl_sync(FULL, sel4(id, lk), L);  // lk is warp-uniform
+  bool keep[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) keep[k] = want[k] && (!SKIP || changed[id[k]]);
+  uint32_t kb = 0, kn = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint32_t B = __ballot_sync(FULL, keep[k]);
+    kb += __popc(B & ltm);
+    kn += __popc(B);
+  }
+  uint32_t slot = kb;
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (keep[k]) buf[slot++] = id[k];
+  o.count = static_cast<int>(kn);
+  if (kn) {
+    // last kept id: highest lane with a kept id, its highest kept byte
+    int hk = -1;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (keep[k]) hk = k;
+    const uint32_t anyk = __ballot_sync(FULL, hk >= 0);
+    const int KL = 31 - __clz(anyk);
+    const int kk = __shfl_sync(FULL, hk, KL);
+    const uint32_t lastkept = __shfl_sync(FULL, sel4(id, kk), KL);
+    if (lane < PAD) buf[kn + lane] = lastkept;
+  }
+  return o;
+}
+
 }  // namespace sb

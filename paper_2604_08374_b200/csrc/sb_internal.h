@@ -36,6 +36,11 @@ struct UnionArgs {
   uint8_t* changed_out;        // global-indexed, 1 = registers changed this iteration
   const uint8_t* changed_in;   // global-indexed, previous iteration (skip mode)
   unsigned long long* work;    // dynamic work counter (zeroed per launch)
+  // CTA tile schedule (n_tiles == 0 -> per-warp item schedule)
+  uint64_t n_tiles;
+  uint64_t n_local;
+  const uint32_t* tile_node0;  // first local node of the 8-node group
+  const uint32_t* tile_q;      // chunk index within each node of the group
 };
 
 struct EstArgs {

@@ -112,8 +112,8 @@ __global__ void __launch_bounds__(256) init_kernel(uint8_t* plane, uint64_t n, c
 }
 
 // ------------------------------------------------------------------ union
-// Per-warp id feeder: decodes one 32-byte window of the item's LEB128 stream
-// at a time into a 32-entry shared buffer (compacted; tail lanes padded with
+// Per-warp id feeder: decodes one 128-byte window of the item's LEB128 stream
+// at a time (decode_step4) into a shared buffer (compacted; tail padded with
 // the last id, harmless because max is idempotent) and hands out batches of
 // BATCH = U * SUB ids.
 template <int P, bool SKIP>
@@ -121,6 +121,7 @@ struct Feeder {
   using G = Geo<P>;
   static constexpr int U = (32 / G::SUB) < 8 ? (32 / G::SUB) : 8;  // row loads in flight per lane
   static constexpr int BATCH = U * G::SUB;
+  static constexpr int BUF = 128 + BATCH;  // one 128-byte window of ids + padding
   uint32_t* buf;
   uint64_t pos;
   uint32_t rem, base;
@@ -130,134 +131,174 @@ struct Feeder {
   __device__ __forceinline__ bool next(const UnionArgs& a, int lane) {
     while (i >= n) {
       if (rem == 0) return false;
-      const DecodeOut d = decode_step<false>(a.stream, pos, ~0ull, rem, base, lane);
-      if (d.count == 0) {  // unreachable on a validated stream
+      __syncwarp();  // every lane finished reading the previous window's ids
+      const Decode4 d = decode_step4<SKIP, BATCH>(a.stream, pos, rem, base, a.changed_in, buf, lane);
+      if (d.advance == 0) {  // unreachable on a validated stream
         rem = 0;
         return false;
       }
-      pos += d.last + 1;
-      rem -= d.count;
-      base = __shfl_sync(FULL, d.id, d.last);
-      uint32_t keep = d.mask;
-      if (SKIP) {
-        // Only neighbours whose registers changed in the previous iteration can
-        // raise next[v]: an unchanged w was already folded into cur[v].
-        const bool c = ((d.mask >> lane) & 1u) && a.changed_in[d.id];
-        keep = __ballot_sync(FULL, c);
-      }
-      n = __popc(keep);
+      pos += d.advance;
+      rem -= d.wanted;
+      base = d.last;
+      n = d.count;
       i = 0;
-      if (n == 0) continue;
-      const int lastk = 31 - __clz(keep);
-      const uint32_t lastid = __shfl_sync(FULL, d.id, lastk);
-      __syncwarp();
-      if ((keep >> lane) & 1u) buf[__popc(keep & ((1u << lane) - 1u))] = d.id;
-      if (lane >= n) buf[lane] = lastid;
       __syncwarp();
     }
     return true;
   }
 };
 
+// Row base of this lane as an opaque 64-bit register, so each gathered row
+// address is a single IMAD.WIDE.U32 (id * ROW + base) on the FMA pipe instead
+// of a multiply plus a 64-bit add chain on the ALU pipe (which the LOP3 max
+// already saturates).
+__device__ __forceinline__ const uint8_t* opaque(const uint8_t* p) {
+  asm volatile("" : "+l"(p));
+  return p;
+}
+
 template <int P, int U>
-__device__ __forceinline__ void load_batch(Grp (&x)[U], const uint8_t* __restrict__ curb,
-                                           const uint32_t* buf, int i, int sub) {
+__device__ __forceinline__ void load_batch(Grp (&x)[U], const uint8_t* curb, const uint32_t* buf, int i, int sub) {
   using G = Geo<P>;
   using IO = GrpIO<G::GB>;
 #pragma unroll
   for (int q = 0; q < U; ++q) x[q] = IO::ld(curb + static_cast<uint64_t>(buf[i + q * G::SUB + sub]) * G::ROW);
 }
 
-// One warp per work unit u = item * SLICES + slice.  Item = <= chunk consecutive
-// neighbours of one node.  next[v] = max(cur[v], max_w cur[w])
+// acc <- max(acc, x[0..U)) as a balanced tree: depth log2(U)+1 maxes instead
+// of a U-long serial chain through acc (the ripple LOP3s are latency-bound).
+template <int U>
+__device__ __forceinline__ void tree_max(Grp& acc, Grp (&x)[U]) {
+#pragma unroll
+  for (int s = 1; s < U; s <<= 1) {
+#pragma unroll
+    for (int q = 0; q + s < U; q += 2 * s) bsmax(x[q], x[q + s]);
+  }
+  bsmax(acc, x[0]);
+}
+
+// Processes one work unit: item `item` (<= chunk neighbours of one node) for
+// row slice `slice`.  next[v] = max(cur[v], max_w cur[w])
 // register-wise; a node split over several items is merged by the last item
 // to finish (partials in `scratch`, arrival counter per node-slice).
 // Gathers are software-pipelined: batch k+1's row loads (and, when needed, the
 // next window decode) are issued before batch k's max, so U..2U 16-byte loads
 // per lane stay in flight.
 template <int P, bool SKIP>
-__global__ void __launch_bounds__(256) union_kernel(UnionArgs a) {
+__device__ __forceinline__ void process_item(const UnionArgs& a, uint64_t item, int slice, int lane,
+                                             uint32_t* buf) {
   using G = Geo<P>;
   using IO = GrpIO<G::GB>;
   using F = Feeder<P, SKIP>;
   constexpr int U = F::U;
-  __shared__ uint32_t ids_s[8][32];
-  const int lane = threadIdx.x & 31;
-  const uint64_t total = a.n_items * G::SLICES;
   const int sub = lane / G::LPR;
   const int gl = lane % G::LPR;
-  for (;;) {
-    unsigned long long u = 0;
-    if (lane == 0) u = atomicAdd(a.work, 1ull);
-    u = __shfl_sync(FULL, u, 0);
-    if (u >= total) break;
-    const uint64_t item = u / G::SLICES;
-    const int slice = static_cast<int>(u % G::SLICES);
-    const uint32_t node = a.item_node[item];
-    const uint64_t v = a.node_begin + node;
-    const uint32_t first = a.node_item[node];
-    const uint32_t nit = a.node_item[node + 1] - first;
-    const uint64_t goff = static_cast<uint64_t>(slice) * G::SLICE_BYTES + static_cast<uint64_t>(gl) * G::GB;
-    const uint8_t* __restrict__ curb = a.cur + goff;
-    Grp acc = (item == first) ? IO::ld(curb + v * G::ROW) : grp_zero();  // next[v] <- cur[v]
-    F f;
-    f.buf = ids_s[threadIdx.x >> 5];
-    f.pos = a.item_off[item];
-    f.rem = a.item_count[item];
-    f.base = a.item_base[item];
-    f.n = 0;
-    f.i = 0;
-    Grp xa[U], xb[U];
-    bool ha = f.next(a, lane);
+  const uint64_t u = item * G::SLICES + slice;
+  const uint32_t node = a.item_node[item];
+  const uint64_t v = a.node_begin + node;
+  const uint32_t first = a.node_item[node];
+  const uint32_t nit = a.node_item[node + 1] - first;
+  const uint64_t goff = static_cast<uint64_t>(slice) * G::SLICE_BYTES + static_cast<uint64_t>(gl) * G::GB;
+  const uint8_t* curb = opaque(a.cur + goff);
+  Grp acc = (item == first) ? IO::ld(curb + v * G::ROW) : grp_zero();  // next[v] <- cur[v]
+  F f;
+  f.buf = buf;
+  f.pos = a.item_off[item];
+  f.rem = a.item_count[item];
+  f.base = a.item_base[item];
+  f.n = 0;
+  f.i = 0;
+  Grp xa[U], xb[U];
+  bool ha = f.next(a, lane);
+  if (ha) {
+    load_batch<P, U>(xa, curb, f.buf, f.i, sub);
+    f.i += F::BATCH;
+  }
+  while (ha) {
+    const bool hb = f.next(a, lane);
+    if (hb) {
+      load_batch<P, U>(xb, curb, f.buf, f.i, sub);
+      f.i += F::BATCH;
+    }
+    tree_max<U>(acc, xa);
+    if (!hb) break;
+    ha = f.next(a, lane);
     if (ha) {
       load_batch<P, U>(xa, curb, f.buf, f.i, sub);
       f.i += F::BATCH;
     }
-    while (ha) {
-      const bool hb = f.next(a, lane);
-      if (hb) {
-        load_batch<P, U>(xb, curb, f.buf, f.i, sub);
-        f.i += F::BATCH;
-      }
+    tree_max<U>(acc, xb);
+  }
+  if (G::SUB > 1) {
 #pragma unroll
-      for (int q = 0; q < U; ++q) bsmax(acc, xa[q]);
-      if (!hb) break;
-      ha = f.next(a, lane);
-      if (ha) {
-        load_batch<P, U>(xa, curb, f.buf, f.i, sub);
-        f.i += F::BATCH;
-      }
-#pragma unroll
-      for (int q = 0; q < U; ++q) bsmax(acc, xb[q]);
-    }
-    if (G::SUB > 1) {
-#pragma unroll
-      for (int m = G::LPR; m < 32; m <<= 1) bsmax(acc, grp_shfl_xor(acc, m));
-    }
-    uint8_t* nextb = a.next + goff + v * G::ROW;
-    bool finish = nit == 1;
-    if (!finish) {
-      if (lane < G::LPR) IO::st(a.scratch + u * G::SLICE_BYTES + static_cast<uint64_t>(gl) * G::GB, acc);
-      __threadfence();
-      uint32_t prev = 0;
-      if (lane == 0) prev = atomicAdd(&a.node_counter[static_cast<uint64_t>(node) * G::SLICES + slice], 1u);
-      prev = __shfl_sync(FULL, prev, 0);
-      finish = prev == nit - 1;
-      if (finish) {
-        __threadfence();
-        for (uint32_t i = first; i < first + nit; ++i) {
-          if (i == item) continue;
-          const uint64_t uu = static_cast<uint64_t>(i) * G::SLICES + slice;
-          bsmax(acc, IO::ld_cg(a.scratch + uu * G::SLICE_BYTES + static_cast<uint64_t>(gl) * G::GB));
-        }
-        if (lane == 0) a.node_counter[static_cast<uint64_t>(node) * G::SLICES + slice] = 0u;
-      }
-    }
+    for (int m = G::LPR; m < 32; m <<= 1) bsmax(acc, grp_shfl_xor(acc, m));
+  }
+  uint8_t* nextb = a.next + goff + v * G::ROW;
+  bool finish = nit == 1;
+  if (!finish) {
+    if (lane < G::LPR) IO::st(a.scratch + u * G::SLICE_BYTES + static_cast<uint64_t>(gl) * G::GB, acc);
+    __threadfence();
+    uint32_t prev = 0;
+    if (lane == 0) prev = atomicAdd(&a.node_counter[static_cast<uint64_t>(node) * G::SLICES + slice], 1u);
+    prev = __shfl_sync(FULL, prev, 0);
+    finish = prev == nit - 1;
     if (finish) {
-      const Grp own = IO::ld(curb + v * G::ROW);
-      const bool ch = lane < G::LPR && grp_ne(acc, own);
-      if (lane < G::LPR) IO::st(nextb, acc);
-      if (__any_sync(FULL, ch) && lane == 0) a.changed_out[v] = 1;
+      __threadfence();
+      for (uint32_t i = first; i < first + nit; ++i) {
+        if (i == item) continue;
+        const uint64_t uu = static_cast<uint64_t>(i) * G::SLICES + slice;
+        bsmax(acc, IO::ld_cg(a.scratch + uu * G::SLICE_BYTES + static_cast<uint64_t>(gl) * G::GB));
+      }
+      if (lane == 0) a.node_counter[static_cast<uint64_t>(node) * G::SLICES + slice] = 0u;
+    }
+  }
+  if (finish) {
+    const Grp own = IO::ld(curb + v * G::ROW);
+    const bool ch = lane < G::LPR && grp_ne(acc, own);
+    if (lane < G::LPR) IO::st(nextb, acc);
+    if (__any_sync(FULL, ch) && lane == 0) a.changed_out[v] = 1;
+  }
+}
+
+// Fused decode-union kernel.  Two schedules over the same work units:
+//  TILE=false: each warp grabs the next (item, slice) from a global counter.
+//  TILE=true : each CTA grabs a tile = (8 consecutive nodes, chunk index q,
+//              slice); warp w takes node 8g+w's chunk q.  Consecutive raster
+//              nodes see almost the same neighbour ids at the same stream
+//              position, so the CTA's 8 warps re-read each row from L1
+//              instead of L2.
+template <int P, bool SKIP, bool TILE>
+__global__ void __launch_bounds__(256) union_kernel(UnionArgs a) {
+  using G = Geo<P>;
+  __shared__ uint32_t ids_s[8][Feeder<P, SKIP>::BUF];
+  __shared__ unsigned long long s_unit[2];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  uint32_t* buf = ids_s[warp];
+  if (!TILE) {
+    const uint64_t total = a.n_items * G::SLICES;
+    for (;;) {
+      unsigned long long u = 0;
+      if (lane == 0) u = atomicAdd(a.work, 1ull);
+      u = __shfl_sync(FULL, u, 0);
+      if (u >= total) break;
+      process_item<P, SKIP>(a, u / G::SLICES, static_cast<int>(u % G::SLICES), lane, buf);
+    }
+  } else {
+    const uint64_t total = a.n_tiles * G::SLICES;
+    for (int k = 0;; ++k) {
+      if (threadIdx.x == 0) s_unit[k & 1] = atomicAdd(a.work, 1ull);
+      __syncthreads();
+      const unsigned long long u = s_unit[k & 1];
+      if (u >= total) break;
+      const uint64_t t = u / G::SLICES;
+      const uint32_t node = a.tile_node0[t] + warp;
+      const uint32_t q = a.tile_q[t];
+      if (node < a.n_local) {
+        const uint32_t first = a.node_item[node];
+        if (q < a.node_item[node + 1] - first)
+          process_item<P, SKIP>(a, first + q, static_cast<int>(u % G::SLICES), lane, buf);
+      }
     }
   }
 }
@@ -455,18 +496,23 @@ cudaError_t launch_init(int p, uint8_t* plane, uint64_t n, const uint32_t* orig,
 int union_slices(int p) { return p > 10 ? 1 << (p - 10) : 1; }
 
 cudaError_t launch_union(int p, bool skip, const UnionArgs& a, cudaStream_t s) {
-#define SB_L(P)                                                                           \
-  {                                                                                       \
-    if (skip) {                                                                           \
-      static int g = grid_for(reinterpret_cast<const void*>(union_kernel<P, true>), 256);  \
-      union_kernel<P, true><<<g, 256, 0, s>>>(a);                                         \
-    } else {                                                                              \
-      static int g = grid_for(reinterpret_cast<const void*>(union_kernel<P, false>), 256); \
-      union_kernel<P, false><<<g, 256, 0, s>>>(a);                                        \
-    }                                                                                     \
+  const bool tile = a.n_tiles != 0;
+#define SB_UL(P, SK, TL)                                                                         \
+  {                                                                                              \
+    static int g = grid_for(reinterpret_cast<const void*>(union_kernel<P, SK, TL>), 256);         \
+    union_kernel<P, SK, TL><<<g, 256, 0, s>>>(a);                                                \
+  }
+#define SB_L(P)                                                     \
+  {                                                                 \
+    if (skip) {                                                     \
+      if (tile) SB_UL(P, true, true) else SB_UL(P, true, false)     \
+    } else {                                                        \
+      if (tile) SB_UL(P, false, true) else SB_UL(P, false, false)   \
+    }                                                               \
   }
   SB_DISPATCH_P(p, SB_L)
 #undef SB_L
+#undef SB_UL
   return cudaGetLastError();
 }
 

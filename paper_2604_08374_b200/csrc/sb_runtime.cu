@@ -98,10 +98,14 @@ struct sb_graph {
   uint32_t* d_item_base = nullptr;
   uint32_t* d_item_count = nullptr;
   uint32_t* d_item_node = nullptr;
+  uint64_t n_tiles = 0;               // CTA tiles: (8-node group, chunk index)
+  uint32_t* d_tile_node0 = nullptr;
+  uint32_t* d_tile_q = nullptr;
   ~sb_graph() {
     DeviceGuard dg(device);
     dfree(d_stream); dfree(d_rowoff); dfree(d_deg); dfree(d_orig); dfree(d_node_item);
     dfree(d_item_off); dfree(d_item_base); dfree(d_item_count); dfree(d_item_node);
+    dfree(d_tile_node0); dfree(d_tile_q);
   }
 };
 
@@ -206,8 +210,9 @@ int sb_graph_create(uint64_t n, const uint64_t* offsets, const uint32_t* degrees
     cudaError_t e_ = (x);                                     \
     if (e_ != cudaSuccess) return bail(cuda_fail(e_, #x));    \
   } while (0)
-  GK(cudaMalloc(&g->d_stream, g->stream_local + 64));
-  GK(cudaMemset(g->d_stream + g->stream_local, 0, 64));
+  // 256 B of zero padding: the decoder reads whole 128-byte windows (+8 for alignment).
+  GK(cudaMalloc(&g->d_stream, g->stream_local + 256));
+  GK(cudaMemset(g->d_stream + g->stream_local, 0, 256));
   if (g->stream_local) GK(cudaMemcpy(g->d_stream, stream + b0, g->stream_local, cudaMemcpyHostToDevice));
   std::vector<uint64_t> ro(g->n_local + 1);
   for (uint64_t i = 0; i <= g->n_local; ++i) ro[i] = offsets[node_begin + i] - b0;
@@ -236,6 +241,24 @@ int sb_graph_create(uint64_t n, const uint64_t* offsets, const uint32_t* degrees
   if (items > 0xffffffffull) return bail(fail(SB_EINVAL, "too many work items"));
   node_item[g->n_local] = static_cast<uint32_t>(items);
   g->n_items = items;
+  // Tiles for the CTA schedule: group k = local nodes [8k, 8k+8), one tile per
+  // chunk index up to the group's largest item count.
+  std::vector<uint32_t> tn0, tq;
+  for (uint64_t k = 0; k < g->n_local; k += 8) {
+    uint32_t mx = 0;
+    for (uint64_t i = k; i < std::min<uint64_t>(k + 8, g->n_local); ++i) mx = std::max(mx, node_item[i + 1] - node_item[i]);
+    for (uint32_t q = 0; q < mx; ++q) {
+      tn0.push_back(static_cast<uint32_t>(k));
+      tq.push_back(q);
+    }
+  }
+  g->n_tiles = tn0.size();
+  GK(cudaMalloc(&g->d_tile_node0, std::max<size_t>(tn0.size(), 1) * 4));
+  GK(cudaMalloc(&g->d_tile_q, std::max<size_t>(tq.size(), 1) * 4));
+  if (!tn0.empty()) {
+    GK(cudaMemcpy(g->d_tile_node0, tn0.data(), tn0.size() * 4, cudaMemcpyHostToDevice));
+    GK(cudaMemcpy(g->d_tile_q, tq.data(), tq.size() * 4, cudaMemcpyHostToDevice));
+  }
   GK(cudaMalloc(&g->d_node_item, node_item.size() * 4));
   GK(cudaMemcpy(g->d_node_item, node_item.data(), node_item.size() * 4, cudaMemcpyHostToDevice));
   const uint64_t ni = std::max<uint64_t>(items, 1);
@@ -328,6 +351,10 @@ int sb_hb_create(sb_graph* g, unsigned p, uint32_t depth_limit, uint32_t flags, 
   h->p = p;
   h->depth = depth_limit;
   h->flags = flags;
+  if (const char* e = getenv("SB_UNION_SCHEDULE")) {  // A/B override for benchmarking
+    if (!strcmp(e, "warp")) h->flags |= SB_HB_SCHEDULE_WARP;
+    if (!strcmp(e, "tile")) h->flags &= ~SB_HB_SCHEDULE_WARP;
+  }
   const uint32_t m = 1u << p;
   h->row = m / 2;
   h->slices = sb::union_slices(static_cast<int>(p));
@@ -413,6 +440,10 @@ int sb_hb_step_compute(sb_hb* h, double* local_max) {
     u.changed_out = h->d_changed[N];
     u.changed_in = h->d_changed[L];
     u.work = h->d_misc;
+    u.n_local = g->n_local;
+    u.n_tiles = (h->flags & SB_HB_SCHEDULE_WARP) ? 0 : g->n_tiles;
+    u.tile_node0 = g->d_tile_node0;
+    u.tile_q = g->d_tile_q;
     CK(cudaEventRecord(h->ev[1], h->stream));
     CK(sb::launch_union(static_cast<int>(h->p), skip, u, h->stream));
     CK(cudaEventRecord(h->ev[2], h->stream));
