@@ -241,7 +241,8 @@ def main():
 
     import torch
     import torch.distributed as dist
-    from paper_2604_08374_b200 import Comm, DeviceGraph, HllParams, HyperBall
+    from paper_2604_08374_b200 import DeviceGraph, HllParams, HyperBall
+    from paper_2604_08374_b200.distributed import init_comm, sharded_hyperball
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -267,18 +268,10 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    comm = None
-    if world > 1:
-        uid = [Comm.unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        comm = Comm(world, rank, uid[0], local)
+    comm = init_comm(rank, world, local)
 
     def make_hb(skip=False):
-        dg = DeviceGraph(g, local, (v0, v1))
-        hb = HyperBall(dg, P, args.depth or None, skip_unchanged=skip)
-        if comm is not None:
-            hb.attach_comm(comm, bounds)
-        return hb
+        return sharded_hyperball(g, P, args.depth or None, rank, world, local, comm, skip, bounds)
 
     t0 = time.perf_counter()
     hb = make_hb()

@@ -1,0 +1,58 @@
+"""Node-range sharding across GPUs (one process per GPU).
+
+The reference parallelises iterate_once over contiguous node ranges inside one
+process (parallel.hpp:20-47).  Here each rank owns a contiguous,
+edge-balanced node range of the CSR in its own HBM plus a full replica of the
+register plane; after every iteration the ranks exchange their freshly
+computed rows (grouped NCCL broadcasts, one per shard, inside
+libsieveball_cuda) and take the global max increase (NCCL all-reduce) before
+the convergence test.  torch.distributed only bootstraps: it broadcasts the
+NCCL unique id and gathers results for reporting.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from .cgraph import CompressedCsr
+from .hyperball import Comm, DeviceGraph, HllParams, HyperBall
+
+
+def shard_bounds(csr: CompressedCsr, world: int) -> np.ndarray:
+    """Edge-balanced contiguous node ranges (bounds[world+1])."""
+    return csr.partition(world)
+
+
+def init_comm(rank: int, world: int, device: int) -> Comm | None:
+    """NCCL communicator bootstrapped over the default torch.distributed group."""
+    if world <= 1:
+        return None
+    import torch.distributed as dist
+    uid = [Comm.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    return Comm(world, rank, uid[0], device)
+
+
+def sharded_hyperball(csr: CompressedCsr, params: HllParams | int, depth_limit: int | None, rank: int,
+                      world: int, device: int, comm: Comm | None, skip_unchanged: bool = False,
+                      bounds: np.ndarray | None = None) -> HyperBall:
+    """This rank's HyperBall over its node range, wired to the communicator."""
+    b = shard_bounds(csr, world) if bounds is None else bounds
+    v0, v1 = int(b[rank]), int(b[rank + 1])
+    hb = HyperBall(DeviceGraph(csr, device, (v0, v1)), params, depth_limit, skip_unchanged=skip_unchanged)
+    if comm is not None:
+        hb.attach_comm(comm, b)
+    return hb
+
+
+def gather_to_root(local: np.ndarray, bounds: np.ndarray, rank: int, world: int) -> np.ndarray | None:
+    """Concatenate every rank's local-range array on rank 0 (node order)."""
+    if world <= 1:
+        return local
+    import torch.distributed as dist
+    parts = [None] * world if rank == 0 else None
+    dist.gather_object(local, parts, dst=0)
+    if rank != 0:
+        return None
+    out = np.concatenate(parts)
+    assert out.shape[0] == int(bounds[-1])
+    return out
