@@ -12,6 +12,7 @@
 //   sb_to_packed / sb_from_packed : export/import in the reference packed layout
 //   sb_metrics       : MD / IHH / Tekl / PV / moments
 #include <cstdio>
+#include <cstdlib>
 
 #include "sb_device.cuh"
 #include "sb_internal.h"
@@ -112,14 +113,28 @@ __global__ void __launch_bounds__(256) init_kernel(uint8_t* plane, uint64_t n, c
 }
 
 // ------------------------------------------------------------------ union
+// Union kernel tuning knobs (A/B-selectable at run time for p=10):
+//   U    rows per batch (loads in flight per lane per buffer)
+//   DB   double-buffered batches (batch k+1 loads issued before batch k's max)
+//   MINB minimum resident CTAs per SM (__launch_bounds__ register cap)
+//   ACC2 two accumulators alternating between batches (shorter dependency chain)
+template <int U_, bool DB_, int MINB_, bool ACC2_>
+struct UCfg {
+  static constexpr int U = U_;
+  static constexpr bool DB = DB_;
+  static constexpr int MINB = MINB_;
+  static constexpr bool ACC2 = ACC2_;
+};
+template <int P>
+using DefaultCfg = UCfg<((32 / Geo<P>::SUB) < 8 ? (32 / Geo<P>::SUB) : 8), false, 4, false>;
+
 // Per-warp id feeder: decodes one 128-byte window of the item's LEB128 stream
 // at a time (decode_step4) into a shared buffer (compacted; tail padded with
 // the last id, harmless because max is idempotent) and hands out batches of
 // BATCH = U * SUB ids.
-template <int P, bool SKIP>
+template <int P, bool SKIP, int U>
 struct Feeder {
   using G = Geo<P>;
-  static constexpr int U = (32 / G::SUB) < 8 ? (32 / G::SUB) : 8;  // row loads in flight per lane
   static constexpr int BATCH = U * G::SUB;
   static constexpr int BUF = 128 + BATCH;  // one 128-byte window of ids + padding
   uint32_t* buf;
@@ -181,16 +196,13 @@ __device__ __forceinline__ void tree_max(Grp& acc, Grp (&x)[U]) {
 // row slice `slice`.  next[v] = max(cur[v], max_w cur[w])
 // register-wise; a node split over several items is merged by the last item
 // to finish (partials in `scratch`, arrival counter per node-slice).
-// Gathers are software-pipelined: batch k+1's row loads (and, when needed, the
-// next window decode) are issued before batch k's max, so U..2U 16-byte loads
-// per lane stay in flight.
-template <int P, bool SKIP>
+template <int P, bool SKIP, class C>
 __device__ __forceinline__ void process_item(const UnionArgs& a, uint64_t item, int slice, int lane,
                                              uint32_t* buf) {
   using G = Geo<P>;
   using IO = GrpIO<G::GB>;
-  using F = Feeder<P, SKIP>;
-  constexpr int U = F::U;
+  constexpr int U = C::U;
+  using F = Feeder<P, SKIP, U>;
   const int sub = lane / G::LPR;
   const int gl = lane % G::LPR;
   const uint64_t u = item * G::SLICES + slice;
@@ -201,6 +213,7 @@ __device__ __forceinline__ void process_item(const UnionArgs& a, uint64_t item, 
   const uint64_t goff = static_cast<uint64_t>(slice) * G::SLICE_BYTES + static_cast<uint64_t>(gl) * G::GB;
   const uint8_t* curb = opaque(a.cur + goff);
   Grp acc = (item == first) ? IO::ld(curb + v * G::ROW) : grp_zero();  // next[v] <- cur[v]
+  Grp acc2 = grp_zero();
   F f;
   f.buf = buf;
   f.pos = a.item_off[item];
@@ -208,27 +221,39 @@ __device__ __forceinline__ void process_item(const UnionArgs& a, uint64_t item, 
   f.base = a.item_base[item];
   f.n = 0;
   f.i = 0;
-  Grp xa[U], xb[U];
-  bool ha = f.next(a, lane);
-  if (ha) {
-    load_batch<P, U>(xa, curb, f.buf, f.i, sub);
-    f.i += F::BATCH;
-  }
-  while (ha) {
-    const bool hb = f.next(a, lane);
-    if (hb) {
-      load_batch<P, U>(xb, curb, f.buf, f.i, sub);
-      f.i += F::BATCH;
-    }
-    tree_max<U>(acc, xa);
-    if (!hb) break;
-    ha = f.next(a, lane);
+  if (C::DB) {
+    // software pipeline: batch k+1's loads (and the next window decode when
+    // needed) are in flight while batch k is reduced.
+    Grp xa[U], xb[U];
+    bool ha = f.next(a, lane);
     if (ha) {
       load_batch<P, U>(xa, curb, f.buf, f.i, sub);
       f.i += F::BATCH;
     }
-    tree_max<U>(acc, xb);
+    while (ha) {
+      const bool hb = f.next(a, lane);
+      if (hb) {
+        load_batch<P, U>(xb, curb, f.buf, f.i, sub);
+        f.i += F::BATCH;
+      }
+      tree_max<U>(acc, xa);
+      if (!hb) break;
+      ha = f.next(a, lane);
+      if (ha) {
+        load_batch<P, U>(xa, curb, f.buf, f.i, sub);
+        f.i += F::BATCH;
+      }
+      tree_max<U>(C::ACC2 ? acc2 : acc, xb);
+    }
+  } else {
+    Grp x[U];
+    while (f.next(a, lane)) {
+      load_batch<P, U>(x, curb, f.buf, f.i, sub);
+      f.i += F::BATCH;
+      tree_max<U>(acc, x);
+    }
   }
+  if (C::ACC2) bsmax(acc, acc2);
   if (G::SUB > 1) {
 #pragma unroll
     for (int m = G::LPR; m < 32; m <<= 1) bsmax(acc, grp_shfl_xor(acc, m));
@@ -267,10 +292,10 @@ __device__ __forceinline__ void process_item(const UnionArgs& a, uint64_t item, 
 //              nodes see almost the same neighbour ids at the same stream
 //              position, so the CTA's 8 warps re-read each row from L1
 //              instead of L2.
-template <int P, bool SKIP, bool TILE>
-__global__ void __launch_bounds__(256) union_kernel(UnionArgs a) {
+template <int P, bool SKIP, bool TILE, class C = DefaultCfg<P>>
+__global__ void __launch_bounds__(256, C::MINB) union_kernel(UnionArgs a) {
   using G = Geo<P>;
-  __shared__ uint32_t ids_s[8][Feeder<P, SKIP>::BUF];
+  __shared__ uint32_t ids_s[8][Feeder<P, SKIP, C::U>::BUF];
   __shared__ unsigned long long s_unit[2];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -282,7 +307,7 @@ __global__ void __launch_bounds__(256) union_kernel(UnionArgs a) {
       if (lane == 0) u = atomicAdd(a.work, 1ull);
       u = __shfl_sync(FULL, u, 0);
       if (u >= total) break;
-      process_item<P, SKIP>(a, u / G::SLICES, static_cast<int>(u % G::SLICES), lane, buf);
+      process_item<P, SKIP, C>(a, u / G::SLICES, static_cast<int>(u % G::SLICES), lane, buf);
     }
   } else {
     const uint64_t total = a.n_tiles * G::SLICES;
@@ -297,7 +322,7 @@ __global__ void __launch_bounds__(256) union_kernel(UnionArgs a) {
       if (node < a.n_local) {
         const uint32_t first = a.node_item[node];
         if (q < a.node_item[node + 1] - first)
-          process_item<P, SKIP>(a, first + q, static_cast<int>(u % G::SLICES), lane, buf);
+          process_item<P, SKIP, C>(a, first + q, static_cast<int>(u % G::SLICES), lane, buf);
       }
     }
   }
@@ -495,12 +520,36 @@ cudaError_t launch_init(int p, uint8_t* plane, uint64_t n, const uint32_t* orig,
 
 int union_slices(int p) { return p > 10 ? 1 << (p - 10) : 1; }
 
+// p=10 dense tile kernel variants for A/B runs (SB_UNION_VARIANT=0..4);
+// 0 = DefaultCfg (8-row single buffer, 4 CTAs/SM).
+using V10_1 = UCfg<8, true, 2, false>;   // 8-row double buffer (round-1 first design)
+using V10_2 = UCfg<4, false, 6, false>;  // 4-row single buffer, 6 CTAs/SM
+using V10_3 = UCfg<6, false, 5, false>;  // 6-row single buffer, 5 CTAs/SM
+using V10_4 = UCfg<12, false, 3, false>; // 12-row single buffer, 3 CTAs/SM
+
+static int union_variant() {
+  static const int v = [] {
+    const char* e = getenv("SB_UNION_VARIANT");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
 cudaError_t launch_union(int p, bool skip, const UnionArgs& a, cudaStream_t s) {
   const bool tile = a.n_tiles != 0;
-#define SB_UL(P, SK, TL)                                                                         \
-  {                                                                                              \
-    static int g = grid_for(reinterpret_cast<const void*>(union_kernel<P, SK, TL>), 256);         \
-    union_kernel<P, SK, TL><<<g, 256, 0, s>>>(a);                                                \
+#define SB_UL(P, SK, TL, ...)                                                                        \
+  {                                                                                                  \
+    static int g = grid_for(reinterpret_cast<const void*>(union_kernel<P, SK, TL, ##__VA_ARGS__>), 256); \
+    union_kernel<P, SK, TL, ##__VA_ARGS__><<<g, 256, 0, s>>>(a);                                     \
+  }
+  if (p == 10 && !skip && tile && union_variant() != 0) {
+    switch (union_variant()) {
+      case 1: SB_UL(10, false, true, V10_1) break;
+      case 2: SB_UL(10, false, true, V10_2) break;
+      case 3: SB_UL(10, false, true, V10_3) break;
+      default: SB_UL(10, false, true, V10_4) break;
+    }
+    return cudaGetLastError();
   }
 #define SB_L(P)                                                     \
   {                                                                 \
