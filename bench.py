@@ -388,6 +388,23 @@ def main():
             "per_iteration_union_ms": [round(s["union_ms"], 3) for s in hs.stats()],
             "note": "gathers only neighbours whose registers changed last iteration; not used for value/roofline"}}
         del hs
+        if args.p >= 10:
+            hi = sharded_hyperball(g, P, args.depth or None, rank, world, local, comm, False, bounds, interval=True)
+            one_run(hi)
+            barrier()
+            s3 = torch.cuda.ExternalStream(hi.stream_handle())
+            e0.record(s3)
+            iti = one_run(hi)
+            e1.record(s3)
+            e1.synchronize()
+            ti = max_over_ranks(e0.elapsed_time(e1) / 1e3)
+            line["variants"]["interval"] = {
+                "seconds_per_run": ti, "iterations": iti, "dense_equivalent_updates_per_s": iti * g.edges * m / ti,
+                "sum_d_identical_to_dense": bool(np.array_equal(hi.state().sum_d, hb.state().sum_d)),
+                "per_iteration_union_ms": [round(s["union_ms"], 3) for s in hi.stats()],
+                "note": "runs of consecutive ids folded with 2 sparse-table rows (per-iteration table build "
+                        "included); bit-exact; reported separately from value/roofline"}
+            del hi
 
     # ---- CPU baseline (rank 0, N=1)
     if not args.no_cpu and world == 1 and rank == 0:

@@ -18,6 +18,7 @@ struct BuildArgs {
   uint32_t* item_count;
   uint32_t* item_node;
   unsigned long long* err_node;  // min local node with a malformed row (~0 = none)
+  unsigned int* max_run;         // longest run of consecutive neighbour ids (interval mode)
 };
 
 struct UnionArgs {
@@ -41,6 +42,15 @@ struct UnionArgs {
   uint64_t n_local;
   const uint32_t* tile_node0;  // first local node of the 8-node group
   const uint32_t* tile_q;      // chunk index within each node of the group
+};
+
+// Interval mode: runs of consecutive neighbour ids [s, e] are folded with two
+// sparse-table rows max(ST_k[s], ST_k[e - 2^k + 1]), k = floor(log2(e - s + 1)).
+struct IntervalArgs {
+  UnionArgs u;                 // work items / tiles / planes as in the dense kernel
+  const uint8_t* st;           // levels 1..K, level k at st + (k-1) * n_global * ROW
+  uint64_t n_global;
+  int levels;                  // K
 };
 
 struct EstArgs {
@@ -72,6 +82,8 @@ struct MetricArgs {
 cudaError_t launch_build_items(const BuildArgs& a, cudaStream_t s);
 cudaError_t launch_init(int p, uint8_t* plane, uint64_t n, const uint32_t* orig, cudaStream_t s);
 cudaError_t launch_union(int p, bool skip, const UnionArgs& a, cudaStream_t s);
+cudaError_t launch_st_build(int p, const uint8_t* cur, uint8_t* st, uint64_t n, int levels, cudaStream_t s);
+cudaError_t launch_union_interval(int p, const IntervalArgs& a, cudaStream_t s);
 cudaError_t launch_estimate(int p, int mode, const EstArgs& a, cudaStream_t s);
 cudaError_t launch_to_packed(int p, const uint8_t* bits, uint8_t* packed, uint64_t rows, cudaStream_t s);
 cudaError_t launch_from_packed(int p, const uint8_t* packed, uint8_t* bits, uint64_t rows, cudaStream_t s);

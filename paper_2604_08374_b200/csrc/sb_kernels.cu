@@ -35,7 +35,7 @@ __global__ void __launch_bounds__(256) build_items_kernel(BuildArgs a) {
       a.item_count[i0] = deg < a.chunk ? deg : a.chunk;
       a.item_node[i0] = static_cast<uint32_t>(node);
     }
-    uint32_t rem = deg, base = 0, k0 = 0;
+    uint32_t rem = deg, base = 0, k0 = 0, run_start = 0, maxrun = 0;
     bool bad = false;
     while (rem > 0) {
       const DecodeOut d = decode_step<true>(a.stream, pos, end, rem, base, lane);
@@ -64,6 +64,15 @@ __global__ void __launch_bounds__(256) build_items_kernel(BuildArgs a) {
         bad = true;
         break;
       }
+      // longest run of consecutive ids (sizes the interval-mode sparse table)
+      const bool st = want && (j == 0 || d.id != prev + 1);
+      const uint32_t S = __ballot_sync(FULL, st);
+      const uint32_t sb = S & ((1u << lane) - 1u);
+      const int pl = sb ? 31 - __clz(sb) : -1;
+      const uint32_t pj = __shfl_sync(FULL, j, pl < 0 ? 0 : pl);
+      const uint32_t prev_start = pl < 0 ? run_start : pj;
+      if (st && j > 0) maxrun = max(maxrun, j - prev_start);
+      if (S) run_start = __shfl_sync(FULL, j, 31 - __clz(S));
       pos += d.last + 1;
       rem -= d.count;
       base = __shfl_sync(FULL, d.id, d.last);
@@ -71,6 +80,10 @@ __global__ void __launch_bounds__(256) build_items_kernel(BuildArgs a) {
     }
     if (!bad && pos != end) bad = true;  // trailing bytes in the row
     if (bad && lane == 0) atomicMin(a.err_node, static_cast<unsigned long long>(node));
+    if (deg > 0) maxrun = max(maxrun, deg - run_start);
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) maxrun = max(maxrun, __shfl_xor_sync(FULL, maxrun, o));
+    if (lane == 0 && maxrun) atomicMax(a.max_run, maxrun);
   }
 }
 
@@ -328,6 +341,204 @@ __global__ void __launch_bounds__(256, C::MINB) union_kernel(UnionArgs a) {
   }
 }
 
+
+// ------------------------------------------------------------------ interval mode
+// Sparse table over the current plane: level k row j = max(cur[j .. j+2^k)),
+// built level by level (level k = max(level k-1 [j], level k-1 [j + 2^(k-1)])).
+// Rows j > n - 2^k are never addressed by a query; they copy level k-1.
+template <int P>
+__global__ void st_build_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, uint64_t n,
+                                uint64_t half) {
+  using G = Geo<P>;
+  using IO = GrpIO<G::GB>;
+  const uint64_t groups = n * G::GROUPS;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < groups;
+       i += gridDim.x * (uint64_t)blockDim.x) {
+    const uint64_t j = i / G::GROUPS;
+    Grp x = IO::ld(src + i * G::GB);
+    if (j + half < n) bsmax(x, IO::ld(src + (i + half * G::GROUPS) * G::GB));
+    IO::st(dst + i * G::GB, x);
+  }
+}
+
+// Turns the window's ids (buf[0..n)) into closed runs of consecutive ids and
+// folds each with <= 2 sparse-table rows.  The open run is carried across
+// windows and items' ends close it.
+template <int P>
+struct RunFolder {
+  using G = Geo<P>;
+  using IO = GrpIO<G::GB>;
+  uint32_t* rs;   // run starts (32 per chunk)
+  uint32_t* re;   // run ends (inclusive)
+  bool open;
+  uint32_t ostart, oprev;
+
+  __device__ __forceinline__ const uint8_t* level_row(const IntervalArgs& a, const uint8_t* curb, int k,
+                                                      uint32_t id) const {
+    const uint8_t* b = k == 0 ? curb : curb + (a.st - a.u.cur) + static_cast<uint64_t>(k - 1) * a.n_global * G::ROW;
+    return b + static_cast<uint64_t>(id) * G::ROW;
+  }
+
+  // Folds runs rs/re[0..nr) into acc, 4 runs (8 rows) per batch.
+  __device__ __forceinline__ void fold(const IntervalArgs& a, const uint8_t* curb, int nr, Grp& acc) const {
+    for (int r0 = 0; r0 < nr; r0 += 4) {
+      Grp x[8];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int r = min(r0 + q, nr - 1);  // duplicates are harmless
+        uint32_t s = rs[r];
+        const uint32_t e = re[r];
+        uint32_t L = e - s + 1;
+        const int K = a.levels;
+        while (L >= (2u << K)) {  // longer than the table covers: peel 2^K blocks
+          bsmax(acc, IO::ld(level_row(a, curb, K, s)));
+          s += 1u << K;
+          L -= 1u << K;
+        }
+        const int k = 31 - __clz(L);
+        x[2 * q] = IO::ld(level_row(a, curb, k, s));
+        x[2 * q + 1] = IO::ld(level_row(a, curb, k, e - (1u << k) + 1));
+      }
+      tree_max<8>(acc, x);
+    }
+  }
+
+  // Consumes ids buf[i0 .. n) in chunks of 32.
+  __device__ __forceinline__ void consume(const IntervalArgs& a, const uint8_t* curb, const uint32_t* buf, int n,
+                                          int lane, Grp& acc) {
+    for (int i0 = 0; i0 < n; i0 += 32) {
+      const int cnt = min(32, n - i0);
+      const bool valid = lane < cnt;
+      const uint32_t id = buf[i0 + (valid ? lane : 0)];
+      uint32_t prev = __shfl_up_sync(FULL, id, 1);
+      if (lane == 0) prev = oprev;
+      const bool has_prev = lane > 0 || open;
+      const bool start = valid && !(has_prev && id == prev + 1);
+      const uint32_t S = __ballot_sync(FULL, start);
+      const uint32_t lt = (1u << lane) - 1u;
+      const uint32_t sb = S & lt;
+      const int pl = sb ? 31 - __clz(sb) : -1;
+      const uint32_t pid = __shfl_sync(FULL, id, pl < 0 ? 0 : pl);
+      const uint32_t run_s = pl < 0 ? ostart : pid;
+      const int rank = __popc(sb);
+      const bool emit = start && (pl >= 0 || open);
+      const int slot = open ? rank : rank - 1;
+      __syncwarp();
+      if (emit) {
+        rs[slot] = run_s;
+        re[slot] = prev;
+      }
+      __syncwarp();
+      const int nemit = S ? __popc(S) - (open ? 0 : 1) : 0;
+      if (S) {
+        ostart = __shfl_sync(FULL, id, 31 - __clz(S));
+        open = true;
+      }
+      oprev = __shfl_sync(FULL, id, cnt - 1);
+      if (nemit > 0) fold(a, curb, nemit, acc);
+    }
+  }
+
+  __device__ __forceinline__ void close(const IntervalArgs& a, const uint8_t* curb, int lane, Grp& acc) {
+    if (!open) return;
+    __syncwarp();
+    if (lane == 0) {
+      rs[0] = ostart;
+      re[0] = oprev;
+    }
+    __syncwarp();
+    fold(a, curb, 1, acc);
+    open = false;
+  }
+};
+
+template <int P>
+__device__ __forceinline__ void process_item_interval(const IntervalArgs& ia, uint64_t item, int slice, int lane,
+                                                      uint32_t* buf, uint32_t* rbuf) {
+  using G = Geo<P>;
+  using IO = GrpIO<G::GB>;
+  using F = Feeder<P, false, 8>;
+  static_assert(G::SUB == 1, "interval mode maps one 512-byte slice per warp (p >= 10)");
+  const UnionArgs& a = ia.u;
+  const int gl = lane;
+  const uint64_t u = item * G::SLICES + slice;
+  const uint32_t node = a.item_node[item];
+  const uint64_t v = a.node_begin + node;
+  const uint32_t first = a.node_item[node];
+  const uint32_t nit = a.node_item[node + 1] - first;
+  const uint64_t goff = static_cast<uint64_t>(slice) * G::SLICE_BYTES + static_cast<uint64_t>(gl) * G::GB;
+  const uint8_t* curb = opaque(a.cur + goff);
+  Grp acc = (item == first) ? IO::ld(curb + v * G::ROW) : grp_zero();
+  F f;
+  f.buf = buf;
+  f.pos = a.item_off[item];
+  f.rem = a.item_count[item];
+  f.base = a.item_base[item];
+  f.n = 0;
+  f.i = 0;
+  RunFolder<P> rf;
+  rf.rs = rbuf;
+  rf.re = rbuf + 32;
+  rf.open = false;
+  rf.ostart = rf.oprev = 0;
+  while (f.next(a, lane)) {
+    rf.consume(ia, curb, f.buf, f.n, lane, acc);
+    f.i = f.n;
+  }
+  rf.close(ia, curb, lane, acc);
+  uint8_t* nextb = a.next + goff + v * G::ROW;
+  bool finish = nit == 1;
+  if (!finish) {
+    IO::st(a.scratch + u * G::SLICE_BYTES + static_cast<uint64_t>(gl) * G::GB, acc);
+    __threadfence();
+    uint32_t prev = 0;
+    if (lane == 0) prev = atomicAdd(&a.node_counter[static_cast<uint64_t>(node) * G::SLICES + slice], 1u);
+    prev = __shfl_sync(FULL, prev, 0);
+    finish = prev == nit - 1;
+    if (finish) {
+      __threadfence();
+      for (uint32_t i = first; i < first + nit; ++i) {
+        if (i == item) continue;
+        const uint64_t uu = static_cast<uint64_t>(i) * G::SLICES + slice;
+        bsmax(acc, IO::ld_cg(a.scratch + uu * G::SLICE_BYTES + static_cast<uint64_t>(gl) * G::GB));
+      }
+      if (lane == 0) a.node_counter[static_cast<uint64_t>(node) * G::SLICES + slice] = 0u;
+    }
+  }
+  if (finish) {
+    const Grp own = IO::ld(curb + v * G::ROW);
+    const bool ch = grp_ne(acc, own);
+    IO::st(nextb, acc);
+    if (__any_sync(FULL, ch) && lane == 0) a.changed_out[v] = 1;
+  }
+}
+
+template <int P>
+__global__ void __launch_bounds__(256, 4) union_interval_kernel(IntervalArgs ia) {
+  using G = Geo<P>;
+  __shared__ uint32_t ids_s[8][Feeder<P, false, 8>::BUF];
+  __shared__ uint32_t runs_s[8][64];
+  __shared__ unsigned long long s_unit[2];
+  const UnionArgs& a = ia.u;
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const uint64_t total = a.n_tiles * G::SLICES;
+  for (int k = 0;; ++k) {
+    if (threadIdx.x == 0) s_unit[k & 1] = atomicAdd(a.work, 1ull);
+    __syncthreads();
+    const unsigned long long u = s_unit[k & 1];
+    if (u >= total) break;
+    const uint64_t t = u / G::SLICES;
+    const uint32_t node = a.tile_node0[t] + warp;
+    const uint32_t q = a.tile_q[t];
+    if (node < a.n_local) {
+      const uint32_t first = a.node_item[node];
+      if (q < a.node_item[node + 1] - first)
+        process_item_interval<P>(ia, first + q, static_cast<int>(u % G::SLICES), lane, ids_s[warp], runs_s[warp]);
+    }
+  }
+}
+
 // ------------------------------------------------------------------ estimate
 // MODE 0: init (c -> c_cur only); 1: dense accumulate; 2: skip unchanged rows.
 template <int P, int MODE>
@@ -562,6 +773,43 @@ cudaError_t launch_union(int p, bool skip, const UnionArgs& a, cudaStream_t s) {
   SB_DISPATCH_P(p, SB_L)
 #undef SB_L
 #undef SB_UL
+  return cudaGetLastError();
+}
+
+cudaError_t launch_st_build(int p, const uint8_t* cur, uint8_t* st, uint64_t n, int levels, cudaStream_t s) {
+#define SB_L(P)                                                                                  \
+  {                                                                                              \
+    const uint64_t groups = n * Geo<P>::GROUPS;                                                  \
+    const int g = static_cast<int>(groups / 256 + 1 < 148 * 16 ? groups / 256 + 1 : 148 * 16);   \
+    const uint64_t rowb = n * Geo<P>::ROW;                                                       \
+    for (int k = 1; k <= levels; ++k) {                                                          \
+      const uint8_t* src = k == 1 ? cur : st + static_cast<uint64_t>(k - 2) * rowb;              \
+      st_build_kernel<P><<<g, 256, 0, s>>>(src, st + static_cast<uint64_t>(k - 1) * rowb, n, 1ull << (k - 1)); \
+    }                                                                                            \
+  }
+  SB_DISPATCH_P(p, SB_L)
+#undef SB_L
+  return cudaGetLastError();
+}
+
+cudaError_t launch_union_interval(int p, const IntervalArgs& a, cudaStream_t s) {
+#define SB_LI(P)                                                                                    \
+  {                                                                                                 \
+    static int g = grid_for(reinterpret_cast<const void*>(union_interval_kernel<P>), 256);           \
+    union_interval_kernel<P><<<g, 256, 0, s>>>(a);                                                  \
+    break;                                                                                          \
+  }
+  switch (p) {
+    case 10: SB_LI(10)
+    case 11: SB_LI(11)
+    case 12: SB_LI(12)
+    case 13: SB_LI(13)
+    case 14: SB_LI(14)
+    case 15: SB_LI(15)
+    case 16: SB_LI(16)
+    default: return cudaErrorInvalidValue;
+  }
+#undef SB_LI
   return cudaGetLastError();
 }
 

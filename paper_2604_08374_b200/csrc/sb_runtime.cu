@@ -98,6 +98,7 @@ struct sb_graph {
   uint32_t* d_item_base = nullptr;
   uint32_t* d_item_count = nullptr;
   uint32_t* d_item_node = nullptr;
+  uint32_t max_run = 0;               // longest run of consecutive neighbour ids
   uint64_t n_tiles = 0;               // CTA tiles: (8-node group, chunk index)
   uint32_t* d_tile_node0 = nullptr;
   uint32_t* d_tile_q = nullptr;
@@ -134,6 +135,8 @@ struct sb_hb {
   unsigned long long* d_misc = nullptr;  // [0] work, [1] max_ord, [2] changed count
   unsigned long long* h_misc = nullptr;  // pinned
   uint8_t* d_tmp = nullptr;              // packed export buffer
+  uint8_t* d_st = nullptr;               // interval mode: sparse-table levels 1..levels
+  int levels = 0;
   uint64_t tmp_bytes = 0;
   int latest = 0;     // plane / c / changed index holding iteration t
   uint32_t t = 0;
@@ -149,7 +152,7 @@ struct sb_hb {
     DeviceGuard dg(g ? g->device : 0);
     for (int i = 0; i < 2; ++i) { dfree(d_plane[i]); dfree(d_changed[i]); dfree(d_c[i]); }
     dfree(d_sum_d); dfree(d_sum_d2); dfree(d_lc); dfree(d_scratch); dfree(d_counter);
-    dfree(d_misc); dfree(d_tmp);
+    dfree(d_misc); dfree(d_tmp); dfree(d_st);
     if (h_misc) cudaFreeHost(h_misc);
     for (auto& e : ev) if (e) cudaEventDestroy(e);
     if (stream) cudaStreamDestroy(stream);
@@ -267,8 +270,9 @@ int sb_graph_create(uint64_t n, const uint64_t* offsets, const uint32_t* degrees
   GK(cudaMalloc(&g->d_item_count, ni * 4));
   GK(cudaMalloc(&g->d_item_node, ni * 4));
   unsigned long long* d_err = nullptr;
-  GK(cudaMalloc(&d_err, 8));
+  GK(cudaMalloc(&d_err, 16));
   GK(cudaMemset(d_err, 0xff, 8));
+  GK(cudaMemset(reinterpret_cast<uint8_t*>(d_err) + 8, 0, 8));
   if (g->n_local) {
     sb::BuildArgs a{};
     a.stream = g->d_stream;
@@ -283,11 +287,13 @@ int sb_graph_create(uint64_t n, const uint64_t* offsets, const uint32_t* degrees
     a.item_count = g->d_item_count;
     a.item_node = g->d_item_node;
     a.err_node = d_err;
+    a.max_run = reinterpret_cast<unsigned int*>(d_err + 1);
     GK(sb::launch_build_items(a, 0));
   }
   GK(sync_stream(0));
   unsigned long long err = 0;
   GK(cudaMemcpy(&err, d_err, 8, cudaMemcpyDeviceToHost));
+  GK(cudaMemcpy(&g->max_run, d_err + 1, 4, cudaMemcpyDeviceToHost));
   cudaFree(d_err);
   if (err != ~0ull)
     return bail(fail(SB_ERUNTIME, "cgraph: malformed compressed row at node %llu (bad varint, "
@@ -345,6 +351,8 @@ int sb_hb_create(sb_graph* g, unsigned p, uint32_t depth_limit, uint32_t flags, 
   *out = nullptr;
   if (!g) return fail(SB_EINVAL, "sb_hb_create: NULL graph");
   if (p < 4 || p > 16) return fail(SB_EINVAL, "hll: precision must be in [4, 16]");
+  if ((flags & SB_HB_INTERVAL) && (p < 10 || (flags & SB_HB_SKIP_UNCHANGED)))
+    return fail(SB_EINVAL, "interval mode needs p >= 10 and excludes SB_HB_SKIP_UNCHANGED");
   DeviceGuard dg(g->device);
   auto* h = new sb_hb();
   h->g = g;
@@ -393,6 +401,13 @@ int sb_hb_create(sb_graph* g, unsigned p, uint32_t depth_limit, uint32_t flags, 
   HK(cudaMalloc(&h->d_scratch, std::max<uint64_t>(g->n_items, 1) * h->slices * slice_bytes));
   HK(cudaMalloc(&h->d_counter, nl * h->slices * 4));
   HK(cudaMalloc(&h->d_misc, 4 * 8));
+  if (flags & SB_HB_INTERVAL) {
+    // levels K = floor(log2(longest run)), capped at 10 (longer runs peel 2^K blocks)
+    int K = 0;
+    while (K < 10 && (2u << K) <= g->max_run) ++K;
+    h->levels = K;
+    if (K) HK(cudaMalloc(&h->d_st, static_cast<uint64_t>(K) * plane + 64));
+  }
   HK(cudaMallocHost(&h->h_misc, 4 * 8));
 #undef HK
   const int rc = hb_init(h);
@@ -445,7 +460,18 @@ int sb_hb_step_compute(sb_hb* h, double* local_max) {
     u.tile_node0 = g->d_tile_node0;
     u.tile_q = g->d_tile_q;
     CK(cudaEventRecord(h->ev[1], h->stream));
-    CK(sb::launch_union(static_cast<int>(h->p), skip, u, h->stream));
+    if (h->flags & SB_HB_INTERVAL) {
+      if (h->levels) CK(sb::launch_st_build(static_cast<int>(h->p), h->d_plane[L], h->d_st, g->n, h->levels, h->stream));
+      sb::IntervalArgs ia{};
+      ia.u = u;
+      if (!ia.u.n_tiles) ia.u.n_tiles = g->n_tiles;  // interval kernel uses the tile schedule
+      ia.st = h->d_st ? h->d_st : h->d_plane[L];
+      ia.n_global = g->n;
+      ia.levels = h->levels;
+      CK(sb::launch_union_interval(static_cast<int>(h->p), ia, h->stream));
+    } else {
+      CK(sb::launch_union(static_cast<int>(h->p), skip, u, h->stream));
+    }
     CK(cudaEventRecord(h->ev[2], h->stream));
     sb::EstArgs e{};
     e.plane = h->d_plane[N];

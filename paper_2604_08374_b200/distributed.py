@@ -34,11 +34,12 @@ def init_comm(rank: int, world: int, device: int) -> Comm | None:
 
 def sharded_hyperball(csr: CompressedCsr, params: HllParams | int, depth_limit: int | None, rank: int,
                       world: int, device: int, comm: Comm | None, skip_unchanged: bool = False,
-                      bounds: np.ndarray | None = None) -> HyperBall:
+                      bounds: np.ndarray | None = None, interval: bool = False) -> HyperBall:
     """This rank's HyperBall over its node range, wired to the communicator."""
     b = shard_bounds(csr, world) if bounds is None else bounds
     v0, v1 = int(b[rank]), int(b[rank + 1])
-    hb = HyperBall(DeviceGraph(csr, device, (v0, v1)), params, depth_limit, skip_unchanged=skip_unchanged)
+    hb = HyperBall(DeviceGraph(csr, device, (v0, v1)), params, depth_limit, skip_unchanged=skip_unchanged,
+                   interval=interval)
     if comm is not None:
         hb.attach_comm(comm, b)
     return hb

@@ -14,7 +14,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from ._lib import (SB_HB_SKIP_UNCHANGED, SB_REGS_LATEST, SB_REGS_PREVIOUS, SB_COMM_ID_BYTES, check,
+from ._lib import (SB_HB_INTERVAL, SB_HB_SKIP_UNCHANGED, SB_REGS_LATEST, SB_REGS_PREVIOUS, SB_COMM_ID_BYTES, check,
                    lib, ptr, sb_iter_stats)
 from .cgraph import CompressedCsr
 
@@ -126,12 +126,12 @@ class HyperBall:
 
     def __init__(self, graph: CompressedCsr | DeviceGraph, params: HllParams | int,
                  depth_limit: int | None = None, device: int = 0, skip_unchanged: bool = False,
-                 node_range: tuple[int, int] | None = None):
+                 node_range: tuple[int, int] | None = None, interval: bool = False):
         self.params = params if isinstance(params, HllParams) else HllParams(params)
         self.graph = graph if isinstance(graph, DeviceGraph) else DeviceGraph(graph, device, node_range)
         self.depth_limit = depth_limit
         self._h = C.c_void_p()
-        flags = SB_HB_SKIP_UNCHANGED if skip_unchanged else 0
+        flags = (SB_HB_SKIP_UNCHANGED if skip_unchanged else 0) | (SB_HB_INTERVAL if interval else 0)
         check(lib().sb_hb_create(self.graph._h, self.params.p, int(depth_limit or 0), flags, C.byref(self._h)))
         self._comm = None
 

@@ -29,9 +29,9 @@ def csr_of(adj):
     return CompressedCsr.from_adjacency(adj)
 
 
-def lockstep(csr, p, depth, O, skip=False, threads=0):
+def lockstep(csr, p, depth, O, skip=False, threads=0, interval=False):
     """Run GPU and oracle side by side; assert bit-exact state after every iteration."""
-    hb = HyperBall(csr, HllParams(p), depth, skip_unchanged=skip)
+    hb = HyperBall(csr, HllParams(p), depth, skip_unchanged=skip, interval=interval)
     n = csr.n
     cur, c_prev = O.hb_init(n, p)
     assert np.array_equal(hb.registers(), cur), "init registers"
@@ -127,6 +127,63 @@ def test_gpu_edge_cases(oracle_best):
     for p in (4, 10, 16):
         lockstep(csr_of(adj), p, None, oracle_best)
     lockstep(csr_of([[]]), 10, None, oracle_best)
+
+
+# ---------------------------------------------------------------- interval (sparse-table) variant
+@pytest.mark.parametrize("p", [10, 11, 12, 14, 16])
+def test_gpu_interval_lockstep_c1(c1, oracle_best, p):
+    lockstep(c1, p, None if p <= 12 else 2, oracle_best, interval=True)
+
+
+def test_gpu_interval_radius_obstacles(oracle_best):
+    g = CompressedCsr.synth_grid(90, 70, 40, 2, 8, 99, 15 * 15)
+    lockstep(g, 10, None, oracle_best, interval=True)
+    g = CompressedCsr.synth_grid(60, 80, 0, 1, 1, 5, 20 * 20)  # open grid: long runs
+    lockstep(g, 10, None, oracle_best, interval=True)
+
+
+@pytest.mark.parametrize("case", [i for i, c in enumerate(GOLD["hyperball"]) if c["p"] >= 10])
+def test_gpu_interval_matches_reference_golden(case):
+    c = GOLD["hyperball"][case]
+    hb = HyperBall(csr_of(GOLD["graphs"][c["graph"]]), HllParams(c["p"]), c["depth"] or None, interval=True)
+    hashes = []
+    while not hb.finished:
+        hb.iterate_once()
+        hashes.append(hashlib.sha256(hb.registers().tobytes()).hexdigest())
+    assert hashes == c["register_sha256_per_iteration"]
+    assert hashlib.sha256(hb.state().sum_d2.tobytes()).hexdigest() == c["sum_d2_sha256"]
+
+
+def test_gpu_interval_long_runs_peel(oracle_best):
+    # a 2600-clique: runs of 2599 ids exceed the 2^(K+1) table span (K capped at 10)
+    n = 2600
+    adj = [[w for w in range(n) if w != v] for v in range(n)]
+    g = csr_of(adj)
+    lockstep(g, 10, 2, oracle_best, interval=True)
+
+
+def test_gpu_interval_rejects_bad_flags():
+    g = csr_of([[1], [0]])
+    with pytest.raises(ValueError):
+        HyperBall(g, 8, interval=True)
+    with pytest.raises(ValueError):
+        HyperBall(g, 10, interval=True, skip_unchanged=True)
+
+
+@pytest.mark.parametrize("p", [10, 12])
+def test_gpu_interval_random_registers(oracle_best, p):
+    g = CompressedCsr.synth_grid(30, 30, 5, 2, 4, p, 0)
+    n, rb = g.n, (1 << p) // 2
+    rng = np.random.default_rng(100 + p)
+    regs = rng.integers(0, 256, n * rb, dtype=np.uint8)
+    hb = HyperBall(g, p, None, interval=True)
+    hb.set_registers(regs)
+    c_prev = hb.state().c_curr.copy()
+    nxt = np.zeros_like(regs)
+    c_cur, sd, sd2 = np.zeros(n), np.zeros(n), np.zeros(n)
+    oracle_best.hb_iterate(g, p, 1, regs, nxt, c_prev, c_cur, sd, sd2)
+    hb.iterate_once()
+    assert np.array_equal(hb.registers(), nxt)
 
 
 # ---------------------------------------------------------------- random registers (all nibble values)
