@@ -37,7 +37,7 @@ sys.path.insert(0, ROOT)
 CONFIGS = {
     # name: (rows, cols, n_rects, rect_min, rect_max, seed, radius2, description)
     "c1": (64, 64, 20, 2, 9, 20261017, 0, "C1 64x64 grid, 20 rectangles, unlimited radius"),
-    "c2": (215, 215, 60, 3, 10, 20261017, 38 * 38, "C2 215x215 grid, 60 rectangles, radius 38 cells"),
+    "c2": (212, 212, 60, 3, 10, 20261017, 44 * 44, "C2 212x212 grid, 60 rectangles (3-10 cells), radius 44 cells"),
     "c3": (486, 486, 0, 1, 1, 20261017, 87 * 87, "C3 open 486x486 grid, radius 87 cells"),
 }
 METRIC = "HyperBall edge-register updates/s"

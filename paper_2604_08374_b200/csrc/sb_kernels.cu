@@ -361,104 +361,49 @@ __global__ void st_build_kernel(const uint8_t* __restrict__ src, uint8_t* __rest
   }
 }
 
-// Turns the window's ids (buf[0..n)) into closed runs of consecutive ids and
-// folds each with <= 2 sparse-table rows.  The open run is carried across
-// windows and items' ends close it.
 template <int P>
-struct RunFolder {
+__device__ __forceinline__ const uint8_t* level_row(const IntervalArgs& a, const uint8_t* curb, int k, uint32_t id) {
   using G = Geo<P>;
-  using IO = GrpIO<G::GB>;
-  uint32_t* rs;   // run starts (32 per chunk)
-  uint32_t* re;   // run ends (inclusive)
-  bool open;
-  uint32_t ostart, oprev;
+  const uint8_t* b = k == 0 ? curb : curb + (a.st - a.u.cur) + static_cast<uint64_t>(k - 1) * a.n_global * G::ROW;
+  return b + static_cast<uint64_t>(id) * G::ROW;
+}
 
-  __device__ __forceinline__ const uint8_t* level_row(const IntervalArgs& a, const uint8_t* curb, int k,
-                                                      uint32_t id) const {
-    const uint8_t* b = k == 0 ? curb : curb + (a.st - a.u.cur) + static_cast<uint64_t>(k - 1) * a.n_global * G::ROW;
-    return b + static_cast<uint64_t>(id) * G::ROW;
-  }
-
-  // Folds runs rs/re[0..nr) into acc, 4 runs (8 rows) per batch.
-  __device__ __forceinline__ void fold(const IntervalArgs& a, const uint8_t* curb, int nr, Grp& acc) const {
-    for (int r0 = 0; r0 < nr; r0 += 4) {
-      Grp x[8];
+// acc <- max over runs rs/re[0..nr): each run [s, e] costs two sparse-table
+// rows max(ST_k[s], ST_k[e - 2^k + 1]), k = floor(log2(e - s + 1)); 4 runs
+// (8 row loads) per batch, tail padded with duplicates.
+template <int P>
+__device__ __forceinline__ void fold_runs(const IntervalArgs& a, const uint8_t* curb, const uint32_t* rs,
+                                          const uint32_t* re, int nr, Grp& acc) {
+  using IO = GrpIO<Geo<P>::GB>;
+  for (int r0 = 0; r0 < nr; r0 += 4) {
+    Grp x[8];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int r = min(r0 + q, nr - 1);  // duplicates are harmless
-        uint32_t s = rs[r];
-        const uint32_t e = re[r];
-        uint32_t L = e - s + 1;
-        const int K = a.levels;
-        while (L >= (2u << K)) {  // longer than the table covers: peel 2^K blocks
-          bsmax(acc, IO::ld(level_row(a, curb, K, s)));
-          s += 1u << K;
-          L -= 1u << K;
-        }
-        const int k = 31 - __clz(L);
-        x[2 * q] = IO::ld(level_row(a, curb, k, s));
-        x[2 * q + 1] = IO::ld(level_row(a, curb, k, e - (1u << k) + 1));
+    for (int q = 0; q < 4; ++q) {
+      const int r = min(r0 + q, nr - 1);
+      uint32_t s = rs[r];
+      const uint32_t e = re[r];
+      uint32_t L = e - s + 1;
+      const int K = a.levels;
+      while (L >= (2u << K)) {  // longer than the table covers: peel 2^K blocks
+        bsmax(acc, IO::ld(level_row<P>(a, curb, K, s)));
+        s += 1u << K;
+        L -= 1u << K;
       }
-      tree_max<8>(acc, x);
+      const int k = 31 - __clz(L);
+      x[2 * q] = IO::ld(level_row<P>(a, curb, k, s));
+      x[2 * q + 1] = IO::ld(level_row<P>(a, curb, k, e - (1u << k) + 1));
     }
+    tree_max<8>(acc, x);
   }
-
-  // Consumes ids buf[i0 .. n) in chunks of 32.
-  __device__ __forceinline__ void consume(const IntervalArgs& a, const uint8_t* curb, const uint32_t* buf, int n,
-                                          int lane, Grp& acc) {
-    for (int i0 = 0; i0 < n; i0 += 32) {
-      const int cnt = min(32, n - i0);
-      const bool valid = lane < cnt;
-      const uint32_t id = buf[i0 + (valid ? lane : 0)];
-      uint32_t prev = __shfl_up_sync(FULL, id, 1);
-      if (lane == 0) prev = oprev;
-      const bool has_prev = lane > 0 || open;
-      const bool start = valid && !(has_prev && id == prev + 1);
-      const uint32_t S = __ballot_sync(FULL, start);
-      const uint32_t lt = (1u << lane) - 1u;
-      const uint32_t sb = S & lt;
-      const int pl = sb ? 31 - __clz(sb) : -1;
-      const uint32_t pid = __shfl_sync(FULL, id, pl < 0 ? 0 : pl);
-      const uint32_t run_s = pl < 0 ? ostart : pid;
-      const int rank = __popc(sb);
-      const bool emit = start && (pl >= 0 || open);
-      const int slot = open ? rank : rank - 1;
-      __syncwarp();
-      if (emit) {
-        rs[slot] = run_s;
-        re[slot] = prev;
-      }
-      __syncwarp();
-      const int nemit = S ? __popc(S) - (open ? 0 : 1) : 0;
-      if (S) {
-        ostart = __shfl_sync(FULL, id, 31 - __clz(S));
-        open = true;
-      }
-      oprev = __shfl_sync(FULL, id, cnt - 1);
-      if (nemit > 0) fold(a, curb, nemit, acc);
-    }
-  }
-
-  __device__ __forceinline__ void close(const IntervalArgs& a, const uint8_t* curb, int lane, Grp& acc) {
-    if (!open) return;
-    __syncwarp();
-    if (lane == 0) {
-      rs[0] = ostart;
-      re[0] = oprev;
-    }
-    __syncwarp();
-    fold(a, curb, 1, acc);
-    open = false;
-  }
-};
+}
 
 template <int P>
 __device__ __forceinline__ void process_item_interval(const IntervalArgs& ia, uint64_t item, int slice, int lane,
-                                                      uint32_t* buf, uint32_t* rbuf) {
+                                                      uint32_t* rbuf) {
   using G = Geo<P>;
   using IO = GrpIO<G::GB>;
-  using F = Feeder<P, false, 8>;
   static_assert(G::SUB == 1, "interval mode maps one 512-byte slice per warp (p >= 10)");
+  constexpr int RCAP = 32 + 128;
   const UnionArgs& a = ia.u;
   const int gl = lane;
   const uint64_t u = item * G::SLICES + slice;
@@ -469,23 +414,38 @@ __device__ __forceinline__ void process_item_interval(const IntervalArgs& ia, ui
   const uint64_t goff = static_cast<uint64_t>(slice) * G::SLICE_BYTES + static_cast<uint64_t>(gl) * G::GB;
   const uint8_t* curb = opaque(a.cur + goff);
   Grp acc = (item == first) ? IO::ld(curb + v * G::ROW) : grp_zero();
-  F f;
-  f.buf = buf;
-  f.pos = a.item_off[item];
-  f.rem = a.item_count[item];
-  f.base = a.item_base[item];
-  f.n = 0;
-  f.i = 0;
-  RunFolder<P> rf;
-  rf.rs = rbuf;
-  rf.re = rbuf + 32;
-  rf.open = false;
-  rf.ostart = rf.oprev = 0;
-  while (f.next(a, lane)) {
-    rf.consume(ia, curb, f.buf, f.n, lane, acc);
-    f.i = f.n;
+  uint32_t* rs = rbuf;
+  uint32_t* re = rbuf + RCAP;
+  uint64_t pos = a.item_off[item];
+  uint32_t rem = a.item_count[item];
+  uint32_t base = a.item_base[item];
+  bool open = false;
+  uint32_t ostart = 0;
+  int nr = 0;
+  while (rem > 0) {
+    __syncwarp();
+    const RunWindow o = decode_runs4(a.stream, pos, rem, base, open, ostart, rs, re, nr, lane);
+    if (o.advance == 0) break;  // unreachable on a validated stream
+    pos += o.advance;
+    rem -= o.wanted;
+    base = o.last;
+    nr += o.emitted;
+    if (nr >= 32) {
+      __syncwarp();
+      fold_runs<P>(ia, curb, rs, re, nr, acc);
+      nr = 0;
+    }
   }
-  rf.close(ia, curb, lane, acc);
+  if (open) {
+    __syncwarp();
+    if (lane == 0) {
+      rs[nr] = ostart;
+      re[nr] = base;
+    }
+    ++nr;
+  }
+  __syncwarp();
+  if (nr) fold_runs<P>(ia, curb, rs, re, nr, acc);
   uint8_t* nextb = a.next + goff + v * G::ROW;
   bool finish = nit == 1;
   if (!finish) {
@@ -516,8 +476,7 @@ __device__ __forceinline__ void process_item_interval(const IntervalArgs& ia, ui
 template <int P>
 __global__ void __launch_bounds__(256, 4) union_interval_kernel(IntervalArgs ia) {
   using G = Geo<P>;
-  __shared__ uint32_t ids_s[8][Feeder<P, false, 8>::BUF];
-  __shared__ uint32_t runs_s[8][64];
+  __shared__ uint32_t runs_s[8][2 * (32 + 128)];
   __shared__ unsigned long long s_unit[2];
   const UnionArgs& a = ia.u;
   const int lane = threadIdx.x & 31;
@@ -534,7 +493,7 @@ __global__ void __launch_bounds__(256, 4) union_interval_kernel(IntervalArgs ia)
     if (node < a.n_local) {
       const uint32_t first = a.node_item[node];
       if (q < a.node_item[node + 1] - first)
-        process_item_interval<P>(ia, first + q, static_cast<int>(u % G::SLICES), lane, ids_s[warp], runs_s[warp]);
+        process_item_interval<P>(ia, first + q, static_cast<int>(u % G::SLICES), lane, runs_s[warp]);
     }
   }
 }
