@@ -51,6 +51,22 @@ struct IntervalArgs {
   const uint8_t* st;           // levels 1..K, level k at st + (k-1) * n_global * ROW
   uint64_t n_global;
   int levels;                  // K
+  const uint64_t* run_off;     // per item: first run (n_items + 1)
+  const uint32_t* run_s;       // run start ids
+  const uint32_t* run_e;       // run end ids (inclusive)
+};
+
+// Run index, derived once at upload from the LEB128 stream (decode_runs4).
+struct RunIndexArgs {
+  const uint8_t* stream;
+  const uint64_t* item_off;
+  const uint32_t* item_base;
+  const uint32_t* item_count;
+  uint64_t n_items;
+  uint64_t* run_count;         // count pass: runs per item
+  const uint64_t* run_off;     // fill pass: offsets (n_items + 1)
+  uint32_t* run_s;
+  uint32_t* run_e;
 };
 
 struct EstArgs {
@@ -84,6 +100,7 @@ cudaError_t launch_init(int p, uint8_t* plane, uint64_t n, const uint32_t* orig,
 cudaError_t launch_union(int p, bool skip, const UnionArgs& a, cudaStream_t s);
 cudaError_t launch_st_build(int p, const uint8_t* cur, uint8_t* st, uint64_t n, int levels, cudaStream_t s);
 cudaError_t launch_union_interval(int p, const IntervalArgs& a, cudaStream_t s);
+cudaError_t launch_run_index(const RunIndexArgs& a, bool fill, cudaStream_t s);
 cudaError_t launch_estimate(int p, int mode, const EstArgs& a, cudaStream_t s);
 cudaError_t launch_to_packed(int p, const uint8_t* bits, uint8_t* packed, uint64_t rows, cudaStream_t s);
 cudaError_t launch_from_packed(int p, const uint8_t* packed, uint8_t* bits, uint64_t rows, cudaStream_t s);

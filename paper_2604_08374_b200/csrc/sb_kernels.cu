@@ -361,49 +361,71 @@ __global__ void st_build_kernel(const uint8_t* __restrict__ src, uint8_t* __rest
   }
 }
 
-template <int P>
-__device__ __forceinline__ const uint8_t* level_row(const IntervalArgs& a, const uint8_t* curb, int k, uint32_t id) {
-  using G = Geo<P>;
-  const uint8_t* b = k == 0 ? curb : curb + (a.st - a.u.cur) + static_cast<uint64_t>(k - 1) * a.n_global * G::ROW;
-  return b + static_cast<uint64_t>(id) * G::ROW;
-}
-
-// acc <- max over runs rs/re[0..nr): each run [s, e] costs two sparse-table
-// rows max(ST_k[s], ST_k[e - 2^k + 1]), k = floor(log2(e - s + 1)); 4 runs
-// (8 row loads) per batch, tail padded with duplicates.
-template <int P>
-__device__ __forceinline__ void fold_runs(const IntervalArgs& a, const uint8_t* curb, const uint32_t* rs,
-                                          const uint32_t* re, int nr, Grp& acc) {
-  using IO = GrpIO<Geo<P>::GB>;
-  for (int r0 = 0; r0 < nr; r0 += 4) {
-    Grp x[8];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int r = min(r0 + q, nr - 1);
-      uint32_t s = rs[r];
-      const uint32_t e = re[r];
-      uint32_t L = e - s + 1;
-      const int K = a.levels;
-      while (L >= (2u << K)) {  // longer than the table covers: peel 2^K blocks
-        bsmax(acc, IO::ld(level_row<P>(a, curb, K, s)));
-        s += 1u << K;
-        L -= 1u << K;
+// Run index: one warp per work item decodes its LEB128 bytes straight to runs
+// of consecutive ids (decode_runs4); pass 1 counts, pass 2 writes them at the
+// item's offset.  Built once per graph, used by every interval iteration.
+template <bool FILL>
+__global__ void __launch_bounds__(256) run_index_kernel(RunIndexArgs a) {
+  __shared__ uint32_t rb_s[8][2 * 160];
+  const int lane = threadIdx.x & 31;
+  uint32_t* rs = rb_s[threadIdx.x >> 5];
+  uint32_t* re = rs + 160;
+  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = (gridDim.x * (uint64_t)blockDim.x) >> 5;
+  for (uint64_t item = gw; item < a.n_items; item += nw) {
+    uint64_t pos = a.item_off[item];
+    uint32_t rem = a.item_count[item];
+    uint32_t base = a.item_base[item];
+    bool open = false;
+    uint32_t ostart = 0;
+    uint64_t out = FILL ? a.run_off[item] : 0;
+    int nr = 0;
+    while (rem > 0) {
+      __syncwarp();
+      const RunWindow o = decode_runs4(a.stream, pos, rem, base, open, ostart, rs, re, nr, lane);
+      if (o.advance == 0) break;
+      pos += o.advance;
+      rem -= o.wanted;
+      base = o.last;
+      nr += o.emitted;
+      if (nr >= 32) {
+        __syncwarp();
+        if (FILL)
+          for (int i = lane; i < nr; i += 32) {
+            a.run_s[out + i] = rs[i];
+            a.run_e[out + i] = re[i];
+          }
+        out += nr;
+        nr = 0;
       }
-      const int k = 31 - __clz(L);
-      x[2 * q] = IO::ld(level_row<P>(a, curb, k, s));
-      x[2 * q + 1] = IO::ld(level_row<P>(a, curb, k, e - (1u << k) + 1));
     }
-    tree_max<8>(acc, x);
+    __syncwarp();
+    if (open) {
+      if (lane == 0) {
+        rs[nr] = ostart;
+        re[nr] = base;
+      }
+      ++nr;
+    }
+    __syncwarp();
+    if (FILL)
+      for (int i = lane; i < nr; i += 32) {
+        a.run_s[out + i] = rs[i];
+        a.run_e[out + i] = re[i];
+      }
+    out += nr;
+    if (!FILL && lane == 0) a.run_count[item] = out;
   }
 }
 
+// Folds one work unit's runs: lane i stages run i of each 32-run chunk in
+// registers, then runs are broadcast 4 at a time (8 sparse-table rows per
+// batch, tree-reduced).
 template <int P>
-__device__ __forceinline__ void process_item_interval(const IntervalArgs& ia, uint64_t item, int slice, int lane,
-                                                      uint32_t* rbuf) {
+__device__ __forceinline__ void process_item_runs(const IntervalArgs& ia, uint64_t item, int slice, int lane) {
   using G = Geo<P>;
   using IO = GrpIO<G::GB>;
   static_assert(G::SUB == 1, "interval mode maps one 512-byte slice per warp (p >= 10)");
-  constexpr int RCAP = 32 + 128;
   const UnionArgs& a = ia.u;
   const int gl = lane;
   const uint64_t u = item * G::SLICES + slice;
@@ -413,39 +435,39 @@ __device__ __forceinline__ void process_item_interval(const IntervalArgs& ia, ui
   const uint32_t nit = a.node_item[node + 1] - first;
   const uint64_t goff = static_cast<uint64_t>(slice) * G::SLICE_BYTES + static_cast<uint64_t>(gl) * G::GB;
   const uint8_t* curb = opaque(a.cur + goff);
+  const uint8_t* stb = curb + (ia.st - a.cur);
+  const uint64_t lvl = ia.n_global * G::ROW;
   Grp acc = (item == first) ? IO::ld(curb + v * G::ROW) : grp_zero();
-  uint32_t* rs = rbuf;
-  uint32_t* re = rbuf + RCAP;
-  uint64_t pos = a.item_off[item];
-  uint32_t rem = a.item_count[item];
-  uint32_t base = a.item_base[item];
-  bool open = false;
-  uint32_t ostart = 0;
-  int nr = 0;
-  while (rem > 0) {
-    __syncwarp();
-    const RunWindow o = decode_runs4(a.stream, pos, rem, base, open, ostart, rs, re, nr, lane);
-    if (o.advance == 0) break;  // unreachable on a validated stream
-    pos += o.advance;
-    rem -= o.wanted;
-    base = o.last;
-    nr += o.emitted;
-    if (nr >= 32) {
-      __syncwarp();
-      fold_runs<P>(ia, curb, rs, re, nr, acc);
-      nr = 0;
+  const uint64_t r0 = ia.run_off[item], r1 = ia.run_off[item + 1];
+  const int K = ia.levels;
+  for (uint64_t c = r0; c < r1; c += 32) {
+    const int cnt = static_cast<int>(r1 - c < 32 ? r1 - c : 32);
+    uint32_t ms = 0, me = 0;
+    if (lane < cnt) {
+      ms = ia.run_s[c + lane];
+      me = ia.run_e[c + lane];
+    }
+    for (int q0 = 0; q0 < cnt; q0 += 4) {
+      Grp x[8];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int r = min(q0 + q, cnt - 1);
+        uint32_t s = __shfl_sync(FULL, ms, r);
+        const uint32_t e = __shfl_sync(FULL, me, r);
+        uint32_t L = e - s + 1;
+        while (L >= (2u << K)) {  // longer than the table covers: peel 2^K blocks
+          bsmax(acc, IO::ld(stb + static_cast<uint64_t>(K - 1) * lvl + static_cast<uint64_t>(s) * G::ROW));
+          s += 1u << K;
+          L -= 1u << K;
+        }
+        const int k = 31 - __clz(L);
+        const uint8_t* lb = k == 0 ? curb : stb + static_cast<uint64_t>(k - 1) * lvl;
+        x[2 * q] = IO::ld(lb + static_cast<uint64_t>(s) * G::ROW);
+        x[2 * q + 1] = IO::ld(lb + static_cast<uint64_t>(e - (1u << k) + 1) * G::ROW);
+      }
+      tree_max<8>(acc, x);
     }
   }
-  if (open) {
-    __syncwarp();
-    if (lane == 0) {
-      rs[nr] = ostart;
-      re[nr] = base;
-    }
-    ++nr;
-  }
-  __syncwarp();
-  if (nr) fold_runs<P>(ia, curb, rs, re, nr, acc);
   uint8_t* nextb = a.next + goff + v * G::ROW;
   bool finish = nit == 1;
   if (!finish) {
@@ -476,7 +498,6 @@ __device__ __forceinline__ void process_item_interval(const IntervalArgs& ia, ui
 template <int P>
 __global__ void __launch_bounds__(256, 4) union_interval_kernel(IntervalArgs ia) {
   using G = Geo<P>;
-  __shared__ uint32_t runs_s[8][2 * (32 + 128)];
   __shared__ unsigned long long s_unit[2];
   const UnionArgs& a = ia.u;
   const int lane = threadIdx.x & 31;
@@ -493,7 +514,7 @@ __global__ void __launch_bounds__(256, 4) union_interval_kernel(IntervalArgs ia)
     if (node < a.n_local) {
       const uint32_t first = a.node_item[node];
       if (q < a.node_item[node + 1] - first)
-        process_item_interval<P>(ia, first + q, static_cast<int>(u % G::SLICES), lane, runs_s[warp]);
+        process_item_runs<P>(ia, first + q, static_cast<int>(u % G::SLICES), lane);
     }
   }
 }
@@ -769,6 +790,17 @@ cudaError_t launch_union_interval(int p, const IntervalArgs& a, cudaStream_t s) 
     default: return cudaErrorInvalidValue;
   }
 #undef SB_LI
+  return cudaGetLastError();
+}
+
+cudaError_t launch_run_index(const RunIndexArgs& a, bool fill, cudaStream_t s) {
+  if (fill) {
+    const int g = grid_for(reinterpret_cast<const void*>(run_index_kernel<true>), 256);
+    run_index_kernel<true><<<g, 256, 0, s>>>(a);
+  } else {
+    const int g = grid_for(reinterpret_cast<const void*>(run_index_kernel<false>), 256);
+    run_index_kernel<false><<<g, 256, 0, s>>>(a);
+  }
   return cudaGetLastError();
 }
 

@@ -99,6 +99,10 @@ struct sb_graph {
   uint32_t* d_item_count = nullptr;
   uint32_t* d_item_node = nullptr;
   uint32_t max_run = 0;               // longest run of consecutive neighbour ids
+  uint64_t n_runs = 0;                // interval-mode run index (built on first use)
+  uint64_t* d_run_off = nullptr;
+  uint32_t* d_run_s = nullptr;
+  uint32_t* d_run_e = nullptr;
   uint64_t n_tiles = 0;               // CTA tiles: (8-node group, chunk index)
   uint32_t* d_tile_node0 = nullptr;
   uint32_t* d_tile_q = nullptr;
@@ -107,6 +111,7 @@ struct sb_graph {
     dfree(d_stream); dfree(d_rowoff); dfree(d_deg); dfree(d_orig); dfree(d_node_item);
     dfree(d_item_off); dfree(d_item_base); dfree(d_item_count); dfree(d_item_node);
     dfree(d_tile_node0); dfree(d_tile_q);
+    dfree(d_run_off); dfree(d_run_s); dfree(d_run_e);
   }
 };
 
@@ -346,6 +351,38 @@ static int hb_init(sb_hb* h) {
   return SB_OK;
 }
 
+// Interval mode: runs of consecutive ids per work item, decoded once from the
+// device-resident LEB128 stream (count pass, host scan, fill pass).
+static int build_run_index(sb_graph* g) {
+  if (g->d_run_off || g->n_items == 0) return SB_OK;
+  sb::RunIndexArgs a{};
+  a.stream = g->d_stream;
+  a.item_off = g->d_item_off;
+  a.item_base = g->d_item_base;
+  a.item_count = g->d_item_count;
+  a.n_items = g->n_items;
+  uint64_t* d_cnt = nullptr;
+  CK(cudaMalloc(&d_cnt, g->n_items * 8));
+  a.run_count = d_cnt;
+  CK(sb::launch_run_index(a, false, 0));
+  CK(sync_stream(0));
+  std::vector<uint64_t> off(g->n_items + 1, 0);
+  CK(cudaMemcpy(off.data() + 1, d_cnt, g->n_items * 8, cudaMemcpyDeviceToHost));
+  cudaFree(d_cnt);
+  for (uint64_t i = 0; i < g->n_items; ++i) off[i + 1] += off[i];
+  g->n_runs = off[g->n_items];
+  CK(cudaMalloc(&g->d_run_off, off.size() * 8));
+  CK(cudaMemcpy(g->d_run_off, off.data(), off.size() * 8, cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&g->d_run_s, std::max<uint64_t>(g->n_runs, 1) * 4));
+  CK(cudaMalloc(&g->d_run_e, std::max<uint64_t>(g->n_runs, 1) * 4));
+  a.run_off = g->d_run_off;
+  a.run_s = g->d_run_s;
+  a.run_e = g->d_run_e;
+  CK(sb::launch_run_index(a, true, 0));
+  CK(sync_stream(0));
+  return SB_OK;
+}
+
 int sb_hb_create(sb_graph* g, unsigned p, uint32_t depth_limit, uint32_t flags, sb_hb** out) {
   if (!out) return fail(SB_EINVAL, "sb_hb_create: out is NULL");
   *out = nullptr;
@@ -407,6 +444,8 @@ int sb_hb_create(sb_graph* g, unsigned p, uint32_t depth_limit, uint32_t flags, 
     while (K < 10 && (2u << K) <= g->max_run) ++K;
     h->levels = K;
     if (K) HK(cudaMalloc(&h->d_st, static_cast<uint64_t>(K) * plane + 64));
+    const int rc = build_run_index(g);
+    if (rc) return bail(rc);
   }
   HK(cudaMallocHost(&h->h_misc, 4 * 8));
 #undef HK
@@ -468,6 +507,9 @@ int sb_hb_step_compute(sb_hb* h, double* local_max) {
       ia.st = h->d_st ? h->d_st : h->d_plane[L];
       ia.n_global = g->n;
       ia.levels = h->levels;
+      ia.run_off = g->d_run_off;
+      ia.run_s = g->d_run_s;
+      ia.run_e = g->d_run_e;
       CK(sb::launch_union_interval(static_cast<int>(h->p), ia, h->stream));
     } else {
       CK(sb::launch_union(static_cast<int>(h->p), skip, u, h->stream));
