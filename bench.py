@@ -201,7 +201,9 @@ def reference_arm(args):
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(times),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
-        "data": "synthetic", "config": workload_config(args, g, None),
+        "data": "synthetic", "config": dict(workload_config(args, g, None),
+                                            register_layout="reference packed 4-bit (hll.hpp:31-32)",
+                                            parallelism=f"{threads} host threads (parallel_ranges)"),
         "cpu_baseline": cb, "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)

@@ -301,3 +301,19 @@ def test_gpu_hilbert_permutation_equivariance(c1):
     ra = sa.registers.reshape(-1, rb)
     rbm = sb_.registers.reshape(-1, rb)
     assert np.array_equal(rbm, ra[inv])
+
+
+def test_gpu_cpp_facade_tool(oracle_best):
+    """tools/sb_hyperball (C++ host over the facade) vs the oracle on C1."""
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([os.path.join(root, "tools", "sb_hyperball"), "synth", "64", "64", "20", "2", "9",
+                        "20261017", "0", "10", "0"], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stderr
+    g = CompressedCsr.synth_grid(64, 64, 20, 2, 9, 20261017, 0)
+    ref = oracle_best.hb_run(g, 10)
+    nv = g.node_count_of_component().astype(np.float64)
+    md = ref["sum_d"] / (nv - 1.0)
+    line = [ln for ln in r.stdout.splitlines() if ln.startswith("mean MD")][0]
+    assert f"iterations={ref['iterations']}" in r.stdout
+    assert float(line.split("=")[1]) == pytest.approx(float(np.mean(md)), rel=1e-9)
