@@ -316,4 +316,4 @@ def test_gpu_cpp_facade_tool(oracle_best):
     md = ref["sum_d"] / (nv - 1.0)
     line = [ln for ln in r.stdout.splitlines() if ln.startswith("mean MD")][0]
     assert f"iterations={ref['iterations']}" in r.stdout
-    assert float(line.split("=")[1]) == pytest.approx(float(np.mean(md)), rel=1e-9)
+    assert float(line.split("=")[1]) == pytest.approx(float(np.mean(md)), rel=1e-6)  # printed with %.6f
