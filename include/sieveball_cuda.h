@@ -184,6 +184,18 @@ int sb_comm_create(int nranks, int rank, const void* id, int device, sb_comm** o
 int sb_hb_attach_comm(sb_hb* h, sb_comm* c, const uint64_t* bounds);
 void sb_comm_destroy(sb_comm* c);
 
+/* Fused shard exchange over peer memory (CUDA IPC -> NVLink P2P): the union
+ * kernel's epilogue stores every finished row and changed flag straight into
+ * each peer's replica, so no separate row collective runs.  Export this rank's
+ * handles, gather all ranks' (any transport), attach.  Iterations are then
+ * ordered by the 8-byte max reduction: NCCL all-reduce inside sb_hb_step when
+ * a communicator is attached, otherwise the caller's barrier between
+ * sb_hb_step_compute and sb_hb_step_finish. */
+#define SB_IPC_HANDLE_BYTES 256
+int sb_hb_ipc_handles(const sb_hb* h, void* out, size_t cap);
+int sb_hb_attach_peers(sb_hb* h, int nranks, int rank, const void* handles /* nranks * SB_IPC_HANDLE_BYTES */,
+                       const uint64_t* bounds);
+
 #ifdef __cplusplus
 }
 #endif

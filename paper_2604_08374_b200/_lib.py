@@ -17,6 +17,7 @@ SB_HB_SCHEDULE_WARP = 2
 SB_HB_INTERVAL = 4
 SB_REGS_LATEST, SB_REGS_PREVIOUS = 0, 1
 SB_COMM_ID_BYTES = 128
+SB_IPC_HANDLE_BYTES = 256
 
 
 class CudaError(RuntimeError):
@@ -91,6 +92,8 @@ _SIGS = {
     "sb_comm_create": (_i, [_i, _i, _vp, _i, _pp]),
     "sb_hb_attach_comm": (_i, [_vp, _vp, _vp]),
     "sb_comm_destroy": (None, [_vp]),
+    "sb_hb_ipc_handles": (_i, [_vp, _vp, C.c_size_t]),
+    "sb_hb_attach_peers": (_i, [_vp, _i, _i, _vp, _vp]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -42,6 +42,11 @@ struct UnionArgs {
   uint64_t n_local;
   const uint32_t* tile_node0;  // first local node of the 8-node group
   const uint32_t* tile_q;      // chunk index within each node of the group
+  // Fused shard exchange: every finished row (and its changed flag) is also
+  // stored straight into each peer GPU's replica (CUDA IPC / NVLink P2P).
+  uint8_t* const* peer_next;     // [npeers] peers' `next` planes
+  uint8_t* const* peer_changed;  // [npeers] peers' `changed_out` flags
+  int npeers;
 };
 
 // Interval mode: runs of consecutive neighbour ids [s, e] are folded with two

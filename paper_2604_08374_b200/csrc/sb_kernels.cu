@@ -205,6 +205,27 @@ __device__ __forceinline__ void tree_max(Grp& acc, Grp (&x)[U]) {
   bsmax(acc, x[0]);
 }
 
+// Writes the finished row next[v] (this lane's group) and the changed flag,
+// locally and -- fused exchange -- into every peer replica over P2P, so the
+// shard transfer overlaps the remaining union work instead of following it.
+template <int P>
+__device__ __forceinline__ void publish_row(const UnionArgs& a, const uint8_t* curb, uint8_t* nextb, uint64_t goff,
+                                            uint64_t v, const Grp& acc, int lane) {
+  using G = Geo<P>;
+  using IO = GrpIO<G::GB>;
+  const Grp own = IO::ld(curb + v * G::ROW);
+  const bool ch = lane < G::LPR && grp_ne(acc, own);
+  const bool any = __any_sync(FULL, ch);
+  if (lane < G::LPR) {
+    IO::st(nextb, acc);
+    for (int r = 0; r < a.npeers; ++r) IO::st(a.peer_next[r] + goff + v * G::ROW, acc);
+  }
+  if (any && lane == 0) {
+    a.changed_out[v] = 1;
+    for (int r = 0; r < a.npeers; ++r) a.peer_changed[r][v] = 1;
+  }
+}
+
 // Processes one work unit: item `item` (<= chunk neighbours of one node) for
 // row slice `slice`.  next[v] = max(cur[v], max_w cur[w])
 // register-wise; a node split over several items is merged by the last item
@@ -290,12 +311,7 @@ __device__ __forceinline__ void process_item(const UnionArgs& a, uint64_t item, 
       if (lane == 0) a.node_counter[static_cast<uint64_t>(node) * G::SLICES + slice] = 0u;
     }
   }
-  if (finish) {
-    const Grp own = IO::ld(curb + v * G::ROW);
-    const bool ch = lane < G::LPR && grp_ne(acc, own);
-    if (lane < G::LPR) IO::st(nextb, acc);
-    if (__any_sync(FULL, ch) && lane == 0) a.changed_out[v] = 1;
-  }
+  if (finish) publish_row<P>(a, curb, nextb, goff, v, acc, lane);
 }
 
 // Fused decode-union kernel.  Two schedules over the same work units:
@@ -487,12 +503,7 @@ __device__ __forceinline__ void process_item_runs(const IntervalArgs& ia, uint64
       if (lane == 0) a.node_counter[static_cast<uint64_t>(node) * G::SLICES + slice] = 0u;
     }
   }
-  if (finish) {
-    const Grp own = IO::ld(curb + v * G::ROW);
-    const bool ch = grp_ne(acc, own);
-    IO::st(nextb, acc);
-    if (__any_sync(FULL, ch) && lane == 0) a.changed_out[v] = 1;
-  }
+  if (finish) publish_row<P>(a, curb, nextb, goff, v, acc, lane);
 }
 
 template <int P>

@@ -153,8 +153,15 @@ struct sb_hb {
   sb_iter_stats cur_stats{};
   sb_comm* comm = nullptr;
   std::vector<uint64_t> bounds;
+  // fused P2P exchange (CUDA IPC): peers' planes / changed flags by parity
+  int npeers = 0;
+  std::vector<void*> ipc_opened;
+  uint8_t** d_peer_plane[2] = {nullptr, nullptr};
+  uint8_t** d_peer_chg[2] = {nullptr, nullptr};
   ~sb_hb() {
     DeviceGuard dg(g ? g->device : 0);
+    for (void* q : ipc_opened) cudaIpcCloseMemHandle(q);
+    for (int i = 0; i < 2; ++i) { dfree(d_peer_plane[i]); dfree(d_peer_chg[i]); }
     for (int i = 0; i < 2; ++i) { dfree(d_plane[i]); dfree(d_changed[i]); dfree(d_c[i]); }
     dfree(d_sum_d); dfree(d_sum_d2); dfree(d_lc); dfree(d_scratch); dfree(d_counter);
     dfree(d_misc); dfree(d_tmp); dfree(d_st);
@@ -498,6 +505,9 @@ int sb_hb_step_compute(sb_hb* h, double* local_max) {
     u.n_tiles = (h->flags & SB_HB_SCHEDULE_WARP) ? 0 : g->n_tiles;
     u.tile_node0 = g->d_tile_node0;
     u.tile_q = g->d_tile_q;
+    u.npeers = h->npeers;
+    u.peer_next = h->d_peer_plane[N];
+    u.peer_changed = h->d_peer_chg[N];
     CK(cudaEventRecord(h->ev[1], h->stream));
     if (h->flags & SB_HB_INTERVAL) {
       if (h->levels) CK(sb::launch_st_build(static_cast<int>(h->p), h->d_plane[L], h->d_st, g->n, h->levels, h->stream));
@@ -535,6 +545,10 @@ int sb_hb_step_compute(sb_hb* h, double* local_max) {
     CK(cudaEventRecord(h->ev[1], h->stream));
     CK(cudaEventRecord(h->ev[2], h->stream));
   }
+  // The input flags are consumed: clear them now, so they can serve as next
+  // iteration's output -- peers write into them only after the iteration
+  // barrier (global max), never before this clear.
+  CK(cudaMemsetAsync(h->d_changed[L], 0, g->n, h->stream));
   CK(cudaEventRecord(h->ev[3], h->stream));
   CK(cudaMemcpyAsync(h->h_misc, h->d_misc, 4 * 8, cudaMemcpyDeviceToHost, h->stream));
   CK(sync_stream(h->stream));
@@ -601,16 +615,20 @@ static int exchange_nccl(sb_hb* h, double* gmax) {
   sb_graph* g = h->g;
   const int N = 1 - h->latest;
   CK(cudaEventRecord(h->ev[0], h->stream));
-  NK(ncclGroupStart());
-  for (int r = 0; r < c->nranks; ++r) {
-    const uint64_t a = h->bounds[r], b = h->bounds[r + 1];
-    if (b == a) continue;
-    uint8_t* rows = h->d_plane[N] + a * h->row;
-    NK(ncclBroadcast(rows, rows, (b - a) * h->row, ncclUint8, r, c->comm, h->stream));
-    uint8_t* ch = h->d_changed[N] + a;
-    NK(ncclBroadcast(ch, ch, b - a, ncclUint8, r, c->comm, h->stream));
+  if (!h->npeers) {  // rows were not pushed by the kernel epilogue: broadcast the shards
+    NK(ncclGroupStart());
+    for (int r = 0; r < c->nranks; ++r) {
+      const uint64_t a = h->bounds[r], b = h->bounds[r + 1];
+      if (b == a) continue;
+      uint8_t* rows = h->d_plane[N] + a * h->row;
+      NK(ncclBroadcast(rows, rows, (b - a) * h->row, ncclUint8, r, c->comm, h->stream));
+      uint8_t* ch = h->d_changed[N] + a;
+      NK(ncclBroadcast(ch, ch, b - a, ncclUint8, r, c->comm, h->stream));
+    }
+    NK(ncclGroupEnd());
   }
-  NK(ncclGroupEnd());
+  // 8-byte max; with fused P2P rows it is also the iteration barrier
+  // (every rank's union kernel, and so its peer stores, has completed).
   NK(ncclAllReduce(h->d_misc + 1, h->d_misc + 1, 1, ncclUint64, ncclMax, c->comm, h->stream));
   CK(cudaEventRecord(h->ev[1], h->stream));
   CK(cudaMemcpyAsync(h->h_misc + 1, h->d_misc + 1, 8, cudaMemcpyDeviceToHost, h->stream));
@@ -624,6 +642,9 @@ static int exchange_nccl(sb_hb* h, double* gmax) {
 }
 
 int sb_hb_step(sb_hb* h, double* max_increase, int* converged, int* finished) {
+  if (h && h->npeers && !(h->comm && h->comm->nranks > 1))
+    return fail(SB_EINVAL, "peers attached without a communicator: use step_compute / step_finish "
+                           "with an external barrier");
   double mx = 0.0;
   int rc = sb_hb_step_compute(h, &mx);
   if (rc) return rc;
@@ -816,5 +837,56 @@ int sb_hb_attach_comm(sb_hb* h, sb_comm* c, const uint64_t* bounds) {
 }
 
 void sb_comm_destroy(sb_comm* c) { delete c; }
+
+// ------------------------------------------------------------------ fused P2P exchange
+int sb_hb_ipc_handles(const sb_hb* h, void* out, size_t cap) {
+  if (!h || !out) return fail(SB_EINVAL, "NULL argument");
+  if (cap < SB_IPC_HANDLE_BYTES) return fail(SB_EINVAL, "handle buffer too small (%d bytes needed)", SB_IPC_HANDLE_BYTES);
+  static_assert(sizeof(cudaIpcMemHandle_t) * 4 == SB_IPC_HANDLE_BYTES, "ipc handle size");
+  DeviceGuard dg(h->g->device);
+  cudaIpcMemHandle_t hs[4];
+  CK(cudaIpcGetMemHandle(&hs[0], h->d_plane[0]));
+  CK(cudaIpcGetMemHandle(&hs[1], h->d_plane[1]));
+  CK(cudaIpcGetMemHandle(&hs[2], h->d_changed[0]));
+  CK(cudaIpcGetMemHandle(&hs[3], h->d_changed[1]));
+  memcpy(out, hs, sizeof(hs));
+  return SB_OK;
+}
+
+int sb_hb_attach_peers(sb_hb* h, int nranks, int rank, const void* handles, const uint64_t* bounds) {
+  if (!h || !handles || !bounds) return fail(SB_EINVAL, "NULL argument");
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(SB_EINVAL, "bad rank/nranks");
+  if (h->npeers) return fail(SB_EINVAL, "peers already attached");
+  if (bounds[0] != 0 || bounds[nranks] != h->g->n) return fail(SB_EINVAL, "bounds must cover [0, N)");
+  if (bounds[rank] != h->g->v0 || bounds[rank + 1] != h->g->v1)
+    return fail(SB_EINVAL, "graph range does not match this rank's bounds");
+  DeviceGuard dg(h->g->device);
+  std::vector<uint8_t*> pl[2], ch[2];
+  const auto* hs = static_cast<const cudaIpcMemHandle_t*>(handles);
+  for (int r = 0; r < nranks; ++r) {
+    if (r == rank) continue;
+    void* q[4];
+    for (int k = 0; k < 4; ++k) {
+      CK(cudaIpcOpenMemHandle(&q[k], hs[4 * r + k], cudaIpcMemLazyEnablePeerAccess));
+      h->ipc_opened.push_back(q[k]);
+    }
+    pl[0].push_back(static_cast<uint8_t*>(q[0]));
+    pl[1].push_back(static_cast<uint8_t*>(q[1]));
+    ch[0].push_back(static_cast<uint8_t*>(q[2]));
+    ch[1].push_back(static_cast<uint8_t*>(q[3]));
+  }
+  const int np = nranks - 1;
+  for (int i = 0; i < 2; ++i) {
+    CK(cudaMalloc(&h->d_peer_plane[i], std::max(np, 1) * sizeof(uint8_t*)));
+    CK(cudaMalloc(&h->d_peer_chg[i], std::max(np, 1) * sizeof(uint8_t*)));
+    if (np) {
+      CK(cudaMemcpy(h->d_peer_plane[i], pl[i].data(), np * sizeof(uint8_t*), cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(h->d_peer_chg[i], ch[i].data(), np * sizeof(uint8_t*), cudaMemcpyHostToDevice));
+    }
+  }
+  h->npeers = np;
+  h->bounds.assign(bounds, bounds + nranks + 1);
+  return SB_OK;
+}
 
 }  // extern "C"

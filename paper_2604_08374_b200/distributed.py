@@ -32,14 +32,28 @@ def init_comm(rank: int, world: int, device: int) -> Comm | None:
     return Comm(world, rank, uid[0], device)
 
 
+def attach_peers(hb: HyperBall, rank: int, world: int, bounds: np.ndarray) -> None:
+    """Fused P2P exchange: all-gather the CUDA IPC handles over torch.distributed
+    and attach them, so the union kernel stores rows into every peer replica."""
+    import torch.distributed as dist
+    hs = [None] * world
+    dist.all_gather_object(hs, hb.ipc_handles())
+    hb.attach_peers(rank, hs, bounds)
+
+
 def sharded_hyperball(csr: CompressedCsr, params: HllParams | int, depth_limit: int | None, rank: int,
                       world: int, device: int, comm: Comm | None, skip_unchanged: bool = False,
-                      bounds: np.ndarray | None = None, interval: bool = False) -> HyperBall:
-    """This rank's HyperBall over its node range, wired to the communicator."""
+                      bounds: np.ndarray | None = None, interval: bool = False,
+                      fused_p2p: bool = True) -> HyperBall:
+    """This rank's HyperBall over its node range, wired to the communicator.
+    fused_p2p: rows travel as P2P stores from the union kernel (NCCL only
+    carries the 8-byte max / barrier); otherwise grouped ncclBroadcast."""
     b = shard_bounds(csr, world) if bounds is None else bounds
     v0, v1 = int(b[rank]), int(b[rank + 1])
     hb = HyperBall(DeviceGraph(csr, device, (v0, v1)), params, depth_limit, skip_unchanged=skip_unchanged,
                    interval=interval)
+    if world > 1 and fused_p2p:
+        attach_peers(hb, rank, world, b)
     if comm is not None:
         hb.attach_comm(comm, b)
     return hb

@@ -14,8 +14,8 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from ._lib import (SB_HB_INTERVAL, SB_HB_SKIP_UNCHANGED, SB_REGS_LATEST, SB_REGS_PREVIOUS, SB_COMM_ID_BYTES, check,
-                   lib, ptr, sb_iter_stats)
+from ._lib import (SB_HB_INTERVAL, SB_HB_SKIP_UNCHANGED, SB_IPC_HANDLE_BYTES, SB_REGS_LATEST, SB_REGS_PREVIOUS,
+                   SB_COMM_ID_BYTES, check, lib, ptr, sb_iter_stats)
 from .cgraph import CompressedCsr
 
 
@@ -174,6 +174,19 @@ class HyperBall:
         b = np.ascontiguousarray(bounds, np.uint64)
         check(lib().sb_hb_attach_comm(self._h, comm._h, ptr(b)))
         self._comm = comm
+
+    def ipc_handles(self) -> bytes:
+        """CUDA IPC handles of this rank's planes / changed flags (for attach_peers)."""
+        buf = C.create_string_buffer(SB_IPC_HANDLE_BYTES)
+        check(lib().sb_hb_ipc_handles(self._h, buf, SB_IPC_HANDLE_BYTES))
+        return buf.raw
+
+    def attach_peers(self, rank: int, handles: list[bytes], bounds) -> None:
+        """Fused P2P exchange: the union epilogue stores rows into every peer replica."""
+        b = np.ascontiguousarray(bounds, np.uint64)
+        blob = b"".join(handles)
+        assert len(blob) == len(handles) * SB_IPC_HANDLE_BYTES
+        check(lib().sb_hb_attach_peers(self._h, len(handles), rank, blob, ptr(b)))
 
     def reset(self) -> None:
         check(lib().sb_hb_reset(self._h))

@@ -78,3 +78,53 @@ def test_nccl_sharded_bit_identical(world, interval):
     _, same_t, same_sum, same_regs, xms = res
     assert same_t and same_sum and same_regs
     assert xms > 0.0  # the exchange actually ran
+
+
+def _rank_p2p(rank, world, port, q, mode):
+    """Two+ processes, fused P2P row stores over CUDA IPC, gloo barrier + max."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2604_08374_b200 import CompressedCsr, HyperBall
+        from paper_2604_08374_b200.distributed import attach_peers, gather_to_root, shard_bounds
+        dev = rank % torch.cuda.device_count()
+        g = CompressedCsr.synth_grid(64, 64, 20, 2, 9, 20261017, 0)
+        b = shard_bounds(g, world)
+        hb = HyperBall(g, 10, None, device=dev, node_range=(int(b[rank]), int(b[rank + 1])),
+                       skip_unchanged=(mode == "skip"), interval=(mode == "interval"))
+        attach_peers(hb, rank, world, b)
+        while True:
+            mx = torch.tensor([hb.step_compute()], dtype=torch.float64)
+            dist.all_reduce(mx, op=dist.ReduceOp.MAX)  # barrier: every rank's rows are pushed
+            if hb.step_finish(mx.item())[1]:
+                break
+        sd = gather_to_root(hb.state().sum_d, b, rank, world)
+        regs = hb.registers()
+        if rank == 0:
+            ref = HyperBall(g, 10, None, device=dev)
+            ref.run()
+            rs = ref.state(with_registers=True)
+            q.put((hb.t == rs.t, bool(np.array_equal(sd, rs.sum_d)), bool(np.array_equal(regs, rs.registers))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,mode", [(2, "dense"), (3, "dense"), (2, "skip"), (2, "interval")])
+def test_fused_p2p_exchange_bit_identical(world, mode):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    ps = [ctx.Process(target=_rank_p2p, args=(r, world, port, q, mode)) for r in range(world)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(timeout=300)
+    for p in ps:
+        if p.is_alive():
+            p.kill()
+    assert all(p.exitcode == 0 for p in ps), [p.exitcode for p in ps]
+    same_t, same_sum, same_regs = q.get(timeout=10)
+    assert same_t and same_sum and same_regs
