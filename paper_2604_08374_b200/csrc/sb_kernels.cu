@@ -131,15 +131,17 @@ __global__ void __launch_bounds__(256) init_kernel(uint8_t* plane, uint64_t n, c
 //   DB   double-buffered batches (batch k+1 loads issued before batch k's max)
 //   MINB minimum resident CTAs per SM (__launch_bounds__ register cap)
 //   ACC2 two accumulators alternating between batches (shorter dependency chain)
-template <int U_, bool DB_, int MINB_, bool ACC2_>
+//   KWAY bit-serial (U+1)-way max instead of the pairwise tree (kway_max)
+template <int U_, bool DB_, int MINB_, bool ACC2_, bool KWAY_ = false>
 struct UCfg {
   static constexpr int U = U_;
   static constexpr bool DB = DB_;
   static constexpr int MINB = MINB_;
   static constexpr bool ACC2 = ACC2_;
+  static constexpr bool KWAY = KWAY_;
 };
 template <int P>
-using DefaultCfg = UCfg<((32 / Geo<P>::SUB) < 8 ? (32 / Geo<P>::SUB) : 8), false, 4, false>;
+using DefaultCfg = UCfg<((32 / Geo<P>::SUB) < 8 ? (32 / Geo<P>::SUB) : 8), false, 4, false, true>;
 
 // Per-warp id feeder: decodes one 128-byte window of the item's LEB128 stream
 // at a time (decode_step4) into a shared buffer (compacted; tail padded with
@@ -203,6 +205,46 @@ __device__ __forceinline__ void tree_max(Grp& acc, Grp (&x)[U]) {
     for (int q = 0; q + s < U; q += 2 * s) bsmax(x[q], x[q + s]);
   }
   bsmax(acc, x[0]);
+}
+
+// acc <- max(acc, x[0..U)) decided MSB-first over all K = U+1 values at once:
+// M3 = OR of the b3 planes; a value stays "alive" at a register position while
+// its bits so far equal the maximum's; M_k = OR of b_k over the alive values.
+// With the AND folded into the OR-accumulate (one LOP3 each) this is
+// ceil((K-1)/2) + 6K LOP3 (58 for K = 9) instead of 8U (64) for the tree.
+template <int U>
+__device__ __forceinline__ void kway_max(Grp& acc, const Grp (&x)[U]) {
+  uint32_t m3 = acc.b3;
+#pragma unroll
+  for (int q = 0; q < U; ++q) m3 |= x[q].b3;
+  uint32_t al[U + 1];
+  al[U] = acc.b3 | ~m3;
+#pragma unroll
+  for (int q = 0; q < U; ++q) al[q] = x[q].b3 | ~m3;
+  uint32_t m2 = al[U] & acc.b2;
+#pragma unroll
+  for (int q = 0; q < U; ++q) m2 |= al[q] & x[q].b2;
+  al[U] &= acc.b2 | ~m2;
+#pragma unroll
+  for (int q = 0; q < U; ++q) al[q] &= x[q].b2 | ~m2;
+  uint32_t m1 = al[U] & acc.b1;
+#pragma unroll
+  for (int q = 0; q < U; ++q) m1 |= al[q] & x[q].b1;
+  al[U] &= acc.b1 | ~m1;
+#pragma unroll
+  for (int q = 0; q < U; ++q) al[q] &= x[q].b1 | ~m1;
+  uint32_t m0 = al[U] & acc.b0;
+#pragma unroll
+  for (int q = 0; q < U; ++q) m0 |= al[q] & x[q].b0;
+  acc = Grp{m0, m1, m2, m3};
+}
+
+template <class C, int U>
+__device__ __forceinline__ void batch_max(Grp& acc, Grp (&x)[U]) {
+  if (C::KWAY)
+    kway_max<U>(acc, x);
+  else
+    tree_max<U>(acc, x);
 }
 
 // Writes the finished row next[v] (this lane's group) and the changed flag,
@@ -270,21 +312,21 @@ __device__ __forceinline__ void process_item(const UnionArgs& a, uint64_t item, 
         load_batch<P, U>(xb, curb, f.buf, f.i, sub);
         f.i += F::BATCH;
       }
-      tree_max<U>(acc, xa);
+      batch_max<C, U>(acc, xa);
       if (!hb) break;
       ha = f.next(a, lane);
       if (ha) {
         load_batch<P, U>(xa, curb, f.buf, f.i, sub);
         f.i += F::BATCH;
       }
-      tree_max<U>(C::ACC2 ? acc2 : acc, xb);
+      batch_max<C, U>(C::ACC2 ? acc2 : acc, xb);
     }
   } else {
     Grp x[U];
     while (f.next(a, lane)) {
       load_batch<P, U>(x, curb, f.buf, f.i, sub);
       f.i += F::BATCH;
-      tree_max<U>(acc, x);
+      batch_max<C, U>(acc, x);
     }
   }
   if (C::ACC2) bsmax(acc, acc2);
@@ -481,7 +523,7 @@ __device__ __forceinline__ void process_item_runs(const IntervalArgs& ia, uint64
         x[2 * q] = IO::ld(lb + static_cast<uint64_t>(s) * G::ROW);
         x[2 * q + 1] = IO::ld(lb + static_cast<uint64_t>(e - (1u << k) + 1) * G::ROW);
       }
-      tree_max<8>(acc, x);
+      kway_max<8>(acc, x);
     }
   }
   uint8_t* nextb = a.next + goff + v * G::ROW;
@@ -722,12 +764,19 @@ cudaError_t launch_init(int p, uint8_t* plane, uint64_t n, const uint32_t* orig,
 
 int union_slices(int p) { return p > 10 ? 1 << (p - 10) : 1; }
 
-// p=10 dense tile kernel variants for A/B runs (SB_UNION_VARIANT=0..4);
-// 0 = DefaultCfg (8-row single buffer, 4 CTAs/SM).
+// p=10 dense tile kernel variants for A/B runs (SB_UNION_VARIANT=0..9);
+// 0 = DefaultCfg (8-row single buffer, bit-serial 9-way max, 4 CTAs/SM).
+// C3 union ms/iter on one B200 (profiles/r01b_union_variants.txt): tree max
+// 97.9; 5: 94.7; 6: 95.8; 7: 99.2; 8: 106.8.
 using V10_1 = UCfg<8, true, 2, false>;   // 8-row double buffer (round-1 first design)
 using V10_2 = UCfg<4, false, 6, false>;  // 4-row single buffer, 6 CTAs/SM
 using V10_3 = UCfg<6, false, 5, false>;  // 6-row single buffer, 5 CTAs/SM
 using V10_4 = UCfg<12, false, 3, false>; // 12-row single buffer, 3 CTAs/SM
+using V10_5 = UCfg<8, false, 4, false, false>;  // 8-row single buffer, pairwise tree max (round-1 default)
+using V10_6 = UCfg<12, false, 3, false, true>;  // 12-row, bit-serial 13-way max
+using V10_7 = UCfg<16, false, 2, false, true>;  // 16-row, bit-serial 17-way max
+using V10_8 = UCfg<6, false, 5, false, true>;   // 6-row, bit-serial 7-way max
+using V10_9 = UCfg<16, false, 3, false, true>;  // 16-row, bit-serial 17-way max, 3 CTAs/SM
 
 static int union_variant() {
   static const int v = [] {
@@ -749,7 +798,12 @@ cudaError_t launch_union(int p, bool skip, const UnionArgs& a, cudaStream_t s) {
       case 1: SB_UL(10, false, true, V10_1) break;
       case 2: SB_UL(10, false, true, V10_2) break;
       case 3: SB_UL(10, false, true, V10_3) break;
-      default: SB_UL(10, false, true, V10_4) break;
+      case 4: SB_UL(10, false, true, V10_4) break;
+      case 5: SB_UL(10, false, true, V10_5) break;
+      case 6: SB_UL(10, false, true, V10_6) break;
+      case 7: SB_UL(10, false, true, V10_7) break;
+      case 8: SB_UL(10, false, true, V10_8) break;
+      default: SB_UL(10, false, true, V10_9) break;
     }
     return cudaGetLastError();
   }
