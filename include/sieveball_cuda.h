@@ -19,6 +19,7 @@
  *     (kernels.hpp:21-37)                                  (bit-exact by contract)
  *   metrics: mean_depth, integration_* , moments           sb_hb_metrics
  *
+ *   metrics::local_metrics               sb_local_metrics
  *   parallel_ranges (parallel.hpp:20-47)                   sb_partition_edges + sb_comm
  *
  * Conventions: every function returns SB_OK (0) or an error code; the message
@@ -155,6 +156,19 @@ int sb_hb_read_state(const sb_hb* h, double* c_latest, double* c_previous, doubl
  * node, deg = degree per local node.  Outputs may be NULL. */
 int sb_hb_metrics(const sb_hb* h, const uint32_t* nv, const uint32_t* deg, double* md,
                   double* ihh, double* tekl, double* pv, double* m1, double* m2);
+
+/* ---------------- exact local metrics ----------------
+ * For nodes [v0, v1) of a device graph that holds the FULL graph (created with
+ * node range [0, N); the 2-hop rows of any node are read):
+ *   control         = sum_{w in N(v)} 1/deg(w), the correctly rounded sum
+ *                     (128-bit fixed point; order independent); 0 if deg 0
+ *   controllability = deg(v) / |N2(v)|, N2 = nodes within 2 hops except v; NaN if empty
+ *   clustering      = edges_among(v) / (deg(v) (deg(v) - 1)), NaN if deg < 2
+ *   edges_among     = sum_{w in N(v)} |N(w) & N(v)| (directed count), n2 = |N2(v)|
+ * connectivity is deg(v).  Outputs have v1 - v0 entries; any may be NULL.
+ * Shard by node range across GPUs: no exchange is needed. */
+int sb_local_metrics(sb_graph* g, uint64_t v0, uint64_t v1, double* control, double* controllability,
+                     double* clustering, uint64_t* edges_among, uint64_t* n2);
 
 typedef struct {
   uint32_t t;              /* iteration number */

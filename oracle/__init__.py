@@ -77,6 +77,12 @@ class Oracle:
             self._harm.argtypes = [_u8p, C.c_size_t, C.POINTER(C.c_uint64), C.POINTER(C.c_uint32)]
             self._metrics = L.sbo_metrics
             self._metrics.argtypes = [C.c_uint64, _f64p, _f64p, _u32p, _u32p] + [_f64p] * 6
+            self._local = L.sbo_local_metrics
+            self._local.restype = C.c_int
+            self._local.argtypes = [C.c_uint64, _u64p, _u32p, _u8p, C.c_uint64, C.c_uint64] + [_f64p] * 3 + [_u64p] * 2
+            self._sum_recip = L.sbo_exact_sum_recip
+            self._sum_recip.restype = C.c_double
+            self._sum_recip.argtypes = [_u32p, C.c_uint64]
         else:
             self._nmax = L.sbref_nibble_max
             self._nmax.argtypes = [_u8p, _u8p, C.c_size_t, C.c_int]
@@ -195,6 +201,23 @@ class Oracle:
         self._metrics(n, np.ascontiguousarray(sum_d), np.ascontiguousarray(sum_d2),
                       np.ascontiguousarray(nv, np.uint32), np.ascontiguousarray(deg, np.uint32), *outs)
         return dict(zip(["md", "ihh", "tekl", "pv", "m1", "m2"], outs))
+
+    def local_metrics(self, csr, v0: int = 0, v1: int | None = None):
+        """Exact control / controllability / clustering, brute force."""
+        if self.kind != "port":
+            raise NotImplementedError("local metrics are restated in the port only (reference ships none)")
+        v1 = csr.n if v1 is None else v1
+        nl = v1 - v0
+        f = [np.zeros(nl, np.float64) for _ in range(3)]
+        u = [np.zeros(nl, np.uint64) for _ in range(2)]
+        rc = self._local(csr.n, csr.offsets, csr.degrees, csr.stream_padded(), v0, v1, *f, *u)
+        if rc:
+            raise RuntimeError("local metrics: malformed graph")
+        return dict(zip(["control", "controllability", "clustering", "edges_among", "n2"], f + u))
+
+    def exact_sum_recip(self, degs) -> float:
+        d = np.ascontiguousarray(degs, np.uint32)
+        return float(self._sum_recip(d, d.size))
 
 
 _cache: dict = {}

@@ -350,3 +350,83 @@ void sbo_metrics(uint64_t n, const double* sum_d, const double* sum_d2, const ui
     md[v] = MD; ihh[v] = IHH; tekl[v] = TK; pv[v] = PV; m1[v] = M1; m2[v] = M2;
   }
 }
+
+/* ---- local metrics, brute force over decoded rows ----
+ * control = sum_{w in N(v)} 1/deg(w) as the correctly rounded sum (exact
+ * 128-bit fixed point with 96 fractional bits, then one rounding; the SPEC
+ * does not pin a summation order, so the order-independent exact sum is the
+ * contract); controllability = deg / |N2(v)| (N2 = nodes within 2 hops, v
+ * excluded); clustering = edges among N(v) (directed) / (deg (deg - 1)). */
+static int decode_rows(uint64_t n, const uint64_t* offsets, const uint32_t* degrees,
+                       const uint8_t* stream, uint64_t** off_out, uint32_t** ids_out) {
+  uint64_t* off = (uint64_t*)malloc((n + 1) * sizeof(uint64_t));
+  uint64_t tot = 0;
+  for (uint64_t v = 0; v < n; ++v) { off[v] = tot; tot += degrees[v]; }
+  off[n] = tot;
+  uint32_t* ids = (uint32_t*)malloc((tot ? tot : 1) * sizeof(uint32_t));
+  for (uint64_t v = 0; v < n; ++v) {
+    size_t pos = (size_t)offsets[v];
+    uint64_t prev = 0;
+    for (uint32_t k = 0; k < degrees[v]; ++k) {
+      uint64_t x;
+      if (sbo_leb128_decode(stream, (size_t)offsets[v + 1], &pos, &x) != SBO_OK) {
+        free(off); free(ids);
+        return SBO_ERUNTIME;
+      }
+      prev = k == 0 ? x : prev + x;
+      ids[off[v] + k] = (uint32_t)prev;
+    }
+  }
+  *off_out = off;
+  *ids_out = ids;
+  return SBO_OK;
+}
+
+double sbo_exact_sum_recip(const uint32_t* degs, uint64_t count) {
+  unsigned __int128 acc = 0;
+  for (uint64_t k = 0; k < count; ++k) {
+    if (degs[k] == 0) return INFINITY;
+    int e;
+    const double m = frexp(1.0 / (double)degs[k], &e); /* 1/d = m 2^e, m in [0.5, 1) */
+    const uint64_t mant = (uint64_t)ldexp(m, 53);      /* exact, < 2^53 */
+    acc += (unsigned __int128)mant << (96 + e - 53);
+  }
+  return ldexp((double)acc, -96); /* one round-to-nearest-even conversion */
+}
+
+int sbo_local_metrics(uint64_t n, const uint64_t* offsets, const uint32_t* degrees,
+                      const uint8_t* stream, uint64_t v0, uint64_t v1, double* control,
+                      double* controllability, double* clustering, uint64_t* among,
+                      uint64_t* n2) {
+  uint64_t* off;
+  uint32_t* ids;
+  if (v0 > v1 || v1 > n) return SBO_EINVAL;
+  if (decode_rows(n, offsets, degrees, stream, &off, &ids) != SBO_OK) return SBO_ERUNTIME;
+  uint64_t* mark = (uint64_t*)calloc(n ? n : 1, sizeof(uint64_t));
+  uint64_t* mark2 = (uint64_t*)calloc(n ? n : 1, sizeof(uint64_t));
+  uint32_t* dg = (uint32_t*)malloc((off[n] ? off[n] : 1) * sizeof(uint32_t));
+  for (uint64_t v = v0; v < v1; ++v) {
+    const uint64_t i = v - v0, stamp = v + 1;
+    const uint32_t deg = degrees[v];
+    const uint32_t* nv = ids + off[v];
+    for (uint32_t k = 0; k < deg; ++k) dg[k] = degrees[nv[k]];
+    control[i] = sbo_exact_sum_recip(dg, deg);
+    for (uint32_t k = 0; k < deg; ++k) mark[nv[k]] = stamp;
+    uint64_t tri = 0, cnt = 0;
+    for (uint32_t k = 0; k < deg; ++k) {
+      const uint32_t w = nv[k];
+      if (w != v && mark2[w] != stamp) { mark2[w] = stamp; ++cnt; }
+      for (uint64_t q = off[w]; q < off[w + 1]; ++q) {
+        const uint32_t u = ids[q];
+        if (mark[u] == stamp) ++tri;
+        if (u != v && mark2[u] != stamp) { mark2[u] = stamp; ++cnt; }
+      }
+    }
+    controllability[i] = cnt ? (double)deg / (double)cnt : NAN;
+    clustering[i] = deg >= 2 ? (double)tri / ((double)deg * (double)(deg - 1)) : NAN;
+    if (among) among[i] = tri;
+    if (n2) n2[i] = cnt;
+  }
+  free(mark); free(mark2); free(dg); free(off); free(ids);
+  return SBO_OK;
+}

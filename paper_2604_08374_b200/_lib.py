@@ -84,6 +84,7 @@ _SIGS = {
     "sb_hb_set_registers": (_i, [_vp, _vp]),
     "sb_hb_read_state": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, C.POINTER(_u32), C.POINTER(_i), C.POINTER(_i)]),
     "sb_hb_metrics": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "sb_local_metrics": (_i, [_vp, _u64, _u64, _vp, _vp, _vp, _vp, _vp]),
     "sb_hb_stats": (_i, [_vp, C.POINTER(sb_iter_stats), _u32, C.POINTER(_u32)]),
     "sb_hb_reset": (_i, [_vp]),
     "sb_hb_stream": (_vp, [_vp]),

@@ -91,6 +91,21 @@ struct EstArgs {
   unsigned long long* changed_count;
 };
 
+// Exact mode (bit-parallel BFS over blocks of 2^(P+2) sources).
+struct ExactArgs {
+  uint8_t* plane;              // init target / count source (global rows)
+  uint64_t n;
+  uint64_t s0, s1;             // source block
+  uint32_t* pop;               // per node popcount after the previous iteration
+  unsigned long long* sum_d;   // exact sum of depths
+  unsigned long long* sum_d2;  // exact sum of squared depths
+  uint32_t* reach;             // nodes reached (incl. itself), accumulated over blocks
+  uint32_t* hist;              // hist[v * hist_cap + t] = # sources at depth t
+  uint32_t hist_cap;
+  uint32_t t;
+  unsigned long long* changed_count;
+};
+
 struct MetricArgs {
   uint64_t n;
   const double* sum_d;
@@ -100,11 +115,45 @@ struct MetricArgs {
   double *md, *ihh, *tekl, *pv, *m1, *m2;
 };
 
+// Exact local metrics (sb_local.cu).  Requires the full graph on the device.
+struct LocalArgs {
+  uint64_t n;                  // nodes of the graph
+  uint64_t v0, v1;             // nodes to compute
+  const uint32_t* degrees;     // N
+  const uint32_t* node_item;   // N + 1
+  const uint64_t* run_off;     // per item (n_items + 1)
+  const uint32_t* run_s;
+  const uint32_t* run_e;
+  uint32_t* span_lo;           // N: first neighbour id (0xffffffff if none)
+  uint32_t* span_hi;           // N: last neighbour id
+  uint32_t* lo2;               // [v1 - v0]: 2-hop window
+  uint32_t* hi2;
+  unsigned int* max_words;     // [0] max 1-hop window words, [1] max 2-hop window words
+  double* control;             // [v1 - v0]
+  double* controllability;
+  double* clustering;
+  unsigned long long* edges_among;  // optional
+  unsigned long long* n2;           // optional
+  uint32_t* scratch;           // global bitmaps (non-smem path): grid * stride_words
+  uint64_t stride_words;       // 2 * (w1_words + 1) + w2_words
+  uint32_t w1_words, w2_words;
+  unsigned long long* work;
+};
+
+cudaError_t launch_local_spans(const LocalArgs& a, cudaStream_t s);
+// grid_out != NULL: only returns the grid the launch would use.
+cudaError_t launch_local(const LocalArgs& a, bool smem, int* grid_out, cudaStream_t s);
+size_t local_smem_limit();
+
 cudaError_t launch_build_items(const BuildArgs& a, cudaStream_t s);
 cudaError_t launch_init(int p, uint8_t* plane, uint64_t n, const uint32_t* orig, cudaStream_t s);
 cudaError_t launch_union(int p, bool skip, const UnionArgs& a, cudaStream_t s);
-cudaError_t launch_st_build(int p, const uint8_t* cur, uint8_t* st, uint64_t n, int levels, cudaStream_t s);
-cudaError_t launch_union_interval(int p, const IntervalArgs& a, cudaStream_t s);
+cudaError_t launch_st_build(int p, const uint8_t* cur, uint8_t* st, uint64_t n, int levels, cudaStream_t s,
+                            bool orop = false);
+cudaError_t launch_union_interval(int p, const IntervalArgs& a, cudaStream_t s, bool orop = false);
+cudaError_t launch_union_or(int p, const UnionArgs& a, cudaStream_t s);
+cudaError_t launch_exact_init(int p, const ExactArgs& a, cudaStream_t s);
+cudaError_t launch_exact_count(int p, const ExactArgs& a, cudaStream_t s);
 cudaError_t launch_run_index(const RunIndexArgs& a, bool fill, cudaStream_t s);
 cudaError_t launch_estimate(int p, int mode, const EstArgs& a, cudaStream_t s);
 cudaError_t launch_to_packed(int p, const uint8_t* bits, uint8_t* packed, uint64_t rows, cudaStream_t s);

@@ -132,13 +132,15 @@ __global__ void __launch_bounds__(256) init_kernel(uint8_t* plane, uint64_t n, c
 //   MINB minimum resident CTAs per SM (__launch_bounds__ register cap)
 //   ACC2 two accumulators alternating between batches (shorter dependency chain)
 //   KWAY bit-serial (U+1)-way max instead of the pairwise tree (kway_max)
-template <int U_, bool DB_, int MINB_, bool ACC2_, bool KWAY_ = false>
+//   OR   exact mode: rows are reachability bitsets, the union is a plain OR
+template <int U_, bool DB_, int MINB_, bool ACC2_, bool KWAY_ = false, bool OR_ = false>
 struct UCfg {
   static constexpr int U = U_;
   static constexpr bool DB = DB_;
   static constexpr int MINB = MINB_;
   static constexpr bool ACC2 = ACC2_;
   static constexpr bool KWAY = KWAY_;
+  static constexpr bool OR = OR_;
 };
 template <int P>
 using DefaultCfg = UCfg<((32 / Geo<P>::SUB) < 8 ? (32 / Geo<P>::SUB) : 8), false, 4, false, true>;
@@ -239,9 +241,30 @@ __device__ __forceinline__ void kway_max(Grp& acc, const Grp (&x)[U]) {
   acc = Grp{m0, m1, m2, m3};
 }
 
+// Exact mode (bitset rows): the register max degenerates to OR.
+template <bool OR>
+__device__ __forceinline__ void combine(Grp& a, const Grp& b) {
+  if (OR) {
+    a.b0 |= b.b0;
+    a.b1 |= b.b1;
+    a.b2 |= b.b2;
+    a.b3 |= b.b3;
+  } else {
+    bsmax(a, b);
+  }
+}
+
+template <int U>
+__device__ __forceinline__ void or_all(Grp& acc, const Grp (&x)[U]) {
+#pragma unroll
+  for (int q = 0; q < U; ++q) combine<true>(acc, x[q]);
+}
+
 template <class C, int U>
 __device__ __forceinline__ void batch_max(Grp& acc, Grp (&x)[U]) {
-  if (C::KWAY)
+  if (C::OR)
+    or_all<U>(acc, x);
+  else if (C::KWAY)
     kway_max<U>(acc, x);
   else
     tree_max<U>(acc, x);
@@ -329,10 +352,10 @@ __device__ __forceinline__ void process_item(const UnionArgs& a, uint64_t item, 
       batch_max<C, U>(acc, x);
     }
   }
-  if (C::ACC2) bsmax(acc, acc2);
+  if (C::ACC2) combine<C::OR>(acc, acc2);
   if (G::SUB > 1) {
 #pragma unroll
-    for (int m = G::LPR; m < 32; m <<= 1) bsmax(acc, grp_shfl_xor(acc, m));
+    for (int m = G::LPR; m < 32; m <<= 1) combine<C::OR>(acc, grp_shfl_xor(acc, m));
   }
   uint8_t* nextb = a.next + goff + v * G::ROW;
   bool finish = nit == 1;
@@ -348,7 +371,7 @@ __device__ __forceinline__ void process_item(const UnionArgs& a, uint64_t item, 
       for (uint32_t i = first; i < first + nit; ++i) {
         if (i == item) continue;
         const uint64_t uu = static_cast<uint64_t>(i) * G::SLICES + slice;
-        bsmax(acc, IO::ld_cg(a.scratch + uu * G::SLICE_BYTES + static_cast<uint64_t>(gl) * G::GB));
+        combine<C::OR>(acc, IO::ld_cg(a.scratch + uu * G::SLICE_BYTES + static_cast<uint64_t>(gl) * G::GB));
       }
       if (lane == 0) a.node_counter[static_cast<uint64_t>(node) * G::SLICES + slice] = 0u;
     }
@@ -404,7 +427,7 @@ __global__ void __launch_bounds__(256, C::MINB) union_kernel(UnionArgs a) {
 // Sparse table over the current plane: level k row j = max(cur[j .. j+2^k)),
 // built level by level (level k = max(level k-1 [j], level k-1 [j + 2^(k-1)])).
 // Rows j > n - 2^k are never addressed by a query; they copy level k-1.
-template <int P>
+template <int P, bool OR>
 __global__ void st_build_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, uint64_t n,
                                 uint64_t half) {
   using G = Geo<P>;
@@ -414,7 +437,7 @@ __global__ void st_build_kernel(const uint8_t* __restrict__ src, uint8_t* __rest
        i += gridDim.x * (uint64_t)blockDim.x) {
     const uint64_t j = i / G::GROUPS;
     Grp x = IO::ld(src + i * G::GB);
-    if (j + half < n) bsmax(x, IO::ld(src + (i + half * G::GROUPS) * G::GB));
+    if (j + half < n) combine<OR>(x, IO::ld(src + (i + half * G::GROUPS) * G::GB));
     IO::st(dst + i * G::GB, x);
   }
 }
@@ -479,7 +502,7 @@ __global__ void __launch_bounds__(256) run_index_kernel(RunIndexArgs a) {
 // Folds one work unit's runs: lane i stages run i of each 32-run chunk in
 // registers, then runs are broadcast 4 at a time (8 sparse-table rows per
 // batch, tree-reduced).
-template <int P>
+template <int P, bool OR>
 __device__ __forceinline__ void process_item_runs(const IntervalArgs& ia, uint64_t item, int slice, int lane) {
   using G = Geo<P>;
   using IO = GrpIO<G::GB>;
@@ -514,7 +537,7 @@ __device__ __forceinline__ void process_item_runs(const IntervalArgs& ia, uint64
         const uint32_t e = __shfl_sync(FULL, me, r);
         uint32_t L = e - s + 1;
         while (L >= (2u << K)) {  // longer than the table covers: peel 2^K blocks
-          bsmax(acc, IO::ld(stb + static_cast<uint64_t>(K - 1) * lvl + static_cast<uint64_t>(s) * G::ROW));
+          combine<OR>(acc, IO::ld(stb + static_cast<uint64_t>(K - 1) * lvl + static_cast<uint64_t>(s) * G::ROW));
           s += 1u << K;
           L -= 1u << K;
         }
@@ -523,7 +546,10 @@ __device__ __forceinline__ void process_item_runs(const IntervalArgs& ia, uint64
         x[2 * q] = IO::ld(lb + static_cast<uint64_t>(s) * G::ROW);
         x[2 * q + 1] = IO::ld(lb + static_cast<uint64_t>(e - (1u << k) + 1) * G::ROW);
       }
-      kway_max<8>(acc, x);
+      if (OR)
+        or_all<8>(acc, x);
+      else
+        kway_max<8>(acc, x);
     }
   }
   uint8_t* nextb = a.next + goff + v * G::ROW;
@@ -540,7 +566,7 @@ __device__ __forceinline__ void process_item_runs(const IntervalArgs& ia, uint64
       for (uint32_t i = first; i < first + nit; ++i) {
         if (i == item) continue;
         const uint64_t uu = static_cast<uint64_t>(i) * G::SLICES + slice;
-        bsmax(acc, IO::ld_cg(a.scratch + uu * G::SLICE_BYTES + static_cast<uint64_t>(gl) * G::GB));
+        combine<OR>(acc, IO::ld_cg(a.scratch + uu * G::SLICE_BYTES + static_cast<uint64_t>(gl) * G::GB));
       }
       if (lane == 0) a.node_counter[static_cast<uint64_t>(node) * G::SLICES + slice] = 0u;
     }
@@ -548,7 +574,7 @@ __device__ __forceinline__ void process_item_runs(const IntervalArgs& ia, uint64
   if (finish) publish_row<P>(a, curb, nextb, goff, v, acc, lane);
 }
 
-template <int P>
+template <int P, bool OR>
 __global__ void __launch_bounds__(256, 4) union_interval_kernel(IntervalArgs ia) {
   using G = Geo<P>;
   __shared__ unsigned long long s_unit[2];
@@ -567,7 +593,7 @@ __global__ void __launch_bounds__(256, 4) union_interval_kernel(IntervalArgs ia)
     if (node < a.n_local) {
       const uint32_t first = a.node_item[node];
       if (q < a.node_item[node + 1] - first)
-        process_item_runs<P>(ia, first + q, static_cast<int>(u % G::SLICES), lane);
+        process_item_runs<P, OR>(ia, first + q, static_cast<int>(u % G::SLICES), lane);
     }
   }
 }
@@ -718,6 +744,67 @@ __global__ void metrics_kernel(MetricArgs a) {
 }
 
 // ------------------------------------------------------------------ launchers
+// ------------------------------------------------------------------ exact mode
+// Exact neighbourhood function (the "exact oracle" mode):
+// the HyperBall loop with each HLL row replaced by a reachability bitset over
+// a block of S = 8 * ROW sources (bit j of row v: source s0 + j reached by v
+// within t hops).  union_kernel / union_interval_kernel run with the OR
+// combine; exact_count_kernel turns the popcount increase into exact depth
+// sums and the per-node depth histogram.
+template <int P>
+__global__ void __launch_bounds__(256) exact_init_kernel(ExactArgs a) {
+  using G = Geo<P>;
+  const uint64_t words = a.n * (G::ROW / 4);
+  uint32_t* plane = reinterpret_cast<uint32_t*>(a.plane);
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < words;
+       i += gridDim.x * (uint64_t)blockDim.x) {
+    const uint64_t v = i / (G::ROW / 4), wi = i % (G::ROW / 4);
+    uint32_t x = 0u;
+    if (v >= a.s0 && v < a.s1) {
+      const uint64_t j = v - a.s0;
+      if (j / 32 == wi) x = 1u << (j % 32);
+    }
+    plane[i] = x;
+    if (wi == 0) {
+      const uint32_t in = (v >= a.s0 && v < a.s1) ? 1u : 0u;
+      a.pop[v] = in;
+      a.reach[v] += in;
+    }
+  }
+}
+
+template <int P>
+__global__ void __launch_bounds__(256) exact_count_kernel(ExactArgs a) {
+  using G = Geo<P>;
+  const int lane = threadIdx.x & 31;
+  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = (gridDim.x * (uint64_t)blockDim.x) >> 5;
+  unsigned long long nchanged = 0;
+  const unsigned long long t = a.t;
+  for (uint64_t v = gw; v < a.n; v += nw) {
+    const uint4* row = reinterpret_cast<const uint4*>(a.plane + v * G::ROW);
+    uint32_t c = 0;
+    for (int k = lane; k < G::ROW / 16; k += 32) {
+      const uint4 x = row[k];
+      c += __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w);
+    }
+#pragma unroll
+    for (int d = 16; d; d >>= 1) c += __shfl_xor_sync(FULL, c, d);
+    if (lane == 0) {
+      const uint32_t delta = c - a.pop[v];  // reachability only grows
+      if (delta) {
+        a.pop[v] = c;
+        a.sum_d[v] += t * delta;
+        a.sum_d2[v] += t * t * delta;
+        a.hist[v * a.hist_cap + t] += delta;
+        a.reach[v] += delta;
+        ++nchanged;
+      }
+    }
+  }
+  if (lane == 0 && nchanged) atomicAdd(a.changed_count, nchanged);
+}
+
 static int grid_for(const void* fn, int block, size_t smem = 0) {
   int dev = 0, sms = 0, per = 0;
   cudaGetDevice(&dev);
@@ -821,7 +908,8 @@ cudaError_t launch_union(int p, bool skip, const UnionArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_st_build(int p, const uint8_t* cur, uint8_t* st, uint64_t n, int levels, cudaStream_t s) {
+cudaError_t launch_st_build(int p, const uint8_t* cur, uint8_t* st, uint64_t n, int levels, cudaStream_t s,
+                            bool orop) {
 #define SB_L(P)                                                                                  \
   {                                                                                              \
     const uint64_t groups = n * Geo<P>::GROUPS;                                                  \
@@ -829,7 +917,10 @@ cudaError_t launch_st_build(int p, const uint8_t* cur, uint8_t* st, uint64_t n, 
     const uint64_t rowb = n * Geo<P>::ROW;                                                       \
     for (int k = 1; k <= levels; ++k) {                                                          \
       const uint8_t* src = k == 1 ? cur : st + static_cast<uint64_t>(k - 2) * rowb;              \
-      st_build_kernel<P><<<g, 256, 0, s>>>(src, st + static_cast<uint64_t>(k - 1) * rowb, n, 1ull << (k - 1)); \
+      if (orop)                                                                                  \
+        st_build_kernel<P, true><<<g, 256, 0, s>>>(src, st + static_cast<uint64_t>(k - 1) * rowb, n, 1ull << (k - 1)); \
+      else                                                                                       \
+        st_build_kernel<P, false><<<g, 256, 0, s>>>(src, st + static_cast<uint64_t>(k - 1) * rowb, n, 1ull << (k - 1)); \
     }                                                                                            \
   }
   SB_DISPATCH_P(p, SB_L)
@@ -837,11 +928,16 @@ cudaError_t launch_st_build(int p, const uint8_t* cur, uint8_t* st, uint64_t n, 
   return cudaGetLastError();
 }
 
-cudaError_t launch_union_interval(int p, const IntervalArgs& a, cudaStream_t s) {
+cudaError_t launch_union_interval(int p, const IntervalArgs& a, cudaStream_t s, bool orop) {
 #define SB_LI(P)                                                                                    \
   {                                                                                                 \
-    static int g = grid_for(reinterpret_cast<const void*>(union_interval_kernel<P>), 256);           \
-    union_interval_kernel<P><<<g, 256, 0, s>>>(a);                                                  \
+    if (orop) {                                                                                     \
+      static int g = grid_for(reinterpret_cast<const void*>(union_interval_kernel<P, true>), 256);  \
+      union_interval_kernel<P, true><<<g, 256, 0, s>>>(a);                                          \
+    } else {                                                                                        \
+      static int g = grid_for(reinterpret_cast<const void*>(union_interval_kernel<P, false>), 256); \
+      union_interval_kernel<P, false><<<g, 256, 0, s>>>(a);                                         \
+    }                                                                                               \
     break;                                                                                          \
   }
   switch (p) {
@@ -855,6 +951,67 @@ cudaError_t launch_union_interval(int p, const IntervalArgs& a, cudaStream_t s) 
     default: return cudaErrorInvalidValue;
   }
 #undef SB_LI
+  return cudaGetLastError();
+}
+
+// Exact mode: OR-union over bitset rows (block of 2^(P+2) sources), P in 10..14.
+template <int P>
+using OrCfg = UCfg<8, false, 4, false, false, true>;
+
+cudaError_t launch_union_or(int p, const UnionArgs& a, cudaStream_t s) {
+#define SB_LO(P)                                                                                         \
+  {                                                                                                      \
+    static int g = grid_for(reinterpret_cast<const void*>(union_kernel<P, false, true, OrCfg<P>>), 256); \
+    union_kernel<P, false, true, OrCfg<P>><<<g, 256, 0, s>>>(a);                                        \
+    break;                                                                                               \
+  }
+  switch (p) {
+    case 10: SB_LO(10)
+    case 11: SB_LO(11)
+    case 12: SB_LO(12)
+    case 13: SB_LO(13)
+    case 14: SB_LO(14)
+    default: return cudaErrorInvalidValue;
+  }
+#undef SB_LO
+  return cudaGetLastError();
+}
+
+cudaError_t launch_exact_init(int p, const ExactArgs& a, cudaStream_t s) {
+#define SB_L(P)                                                                         \
+  {                                                                                     \
+    const int g = grid_for(reinterpret_cast<const void*>(exact_init_kernel<P>), 256);   \
+    exact_init_kernel<P><<<g, 256, 0, s>>>(a);                                          \
+    break;                                                                              \
+  }
+  switch (p) {
+    case 10: SB_L(10)
+    case 11: SB_L(11)
+    case 12: SB_L(12)
+    case 13: SB_L(13)
+    case 14: SB_L(14)
+    default: return cudaErrorInvalidValue;
+  }
+#undef SB_L
+  return cudaGetLastError();
+}
+
+cudaError_t launch_exact_count(int p, const ExactArgs& a, cudaStream_t s) {
+#define SB_L(P)                                                                         \
+  {                                                                                     \
+    const int g = grid_for(reinterpret_cast<const void*>(exact_count_kernel<P>), 256);  \
+    exact_count_kernel<P><<<g, 256, 0, s>>>(a);                                         \
+    break;                                                                              \
+  }
+  switch (p) {
+    case 10: SB_L(10)
+    case 11: SB_L(11)
+    case 12: SB_L(12)
+    case 13: SB_L(13)
+    case 14: SB_L(14)
+    default: return cudaErrorInvalidValue;
+  }
+#undef SB_L
   return cudaGetLastError();
 }
 

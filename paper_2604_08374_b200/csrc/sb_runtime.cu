@@ -781,6 +781,80 @@ int sb_hb_metrics(const sb_hb* hc, const uint32_t* nv, const uint32_t* deg, doub
   return SB_OK;
 }
 
+// ------------------------------------------------------------------ local metrics
+// Exact 1-/2-hop metrics over the device-resident run index.
+int sb_local_metrics(sb_graph* g, uint64_t v0, uint64_t v1, double* control, double* controllability,
+                     double* clustering, uint64_t* edges_among, uint64_t* n2) {
+  if (!g) return fail(SB_EINVAL, "sb_local_metrics: NULL graph");
+  if (g->v0 != 0 || g->v1 != g->n)
+    return fail(SB_EINVAL, "sb_local_metrics: needs the full graph on the device (2-hop rows of any node)");
+  if (v0 > v1 || v1 > g->n) return fail(SB_EINVAL, "sb_local_metrics: bad node range");
+  DeviceGuard dg(g->device);
+  int rc = build_run_index(g);
+  if (rc) return rc;
+  const uint64_t n = g->n, nl = v1 - v0;
+  if (nl == 0) return SB_OK;
+  // [span_lo N | span_hi N | lo2 nl | hi2 nl | max 2] u32, [control | ctrl | clus] f64 nl, [among | n2] u64 nl
+  const uint64_t u32_words = 2 * n + 2 * nl + 2;
+  const uint64_t bytes = ((u32_words * 4 + 7) & ~7ull) + 5 * nl * 8 + 8;
+  uint8_t* blk = nullptr;
+  CK(cudaMalloc(&blk, bytes));
+  struct Free {
+    uint8_t*& p;
+    uint32_t*& q;
+    ~Free() { if (p) cudaFree(p); if (q) cudaFree(q); }
+  };
+  uint32_t* scratch = nullptr;
+  Free fr{blk, scratch};
+  sb::LocalArgs a{};
+  a.n = n;
+  a.v0 = v0;
+  a.v1 = v1;
+  a.degrees = g->d_deg;
+  a.node_item = g->d_node_item;
+  a.run_off = g->d_run_off;
+  a.run_s = g->d_run_s;
+  a.run_e = g->d_run_e;
+  uint32_t* u = reinterpret_cast<uint32_t*>(blk);
+  a.span_lo = u;
+  a.span_hi = u + n;
+  a.lo2 = u + 2 * n;
+  a.hi2 = u + 2 * n + nl;
+  a.max_words = u + 2 * n + 2 * nl;
+  double* f = reinterpret_cast<double*>(blk + ((u32_words * 4 + 7) & ~7ull));
+  a.control = f;
+  a.controllability = f + nl;
+  a.clustering = f + 2 * nl;
+  a.edges_among = reinterpret_cast<unsigned long long*>(f + 3 * nl);
+  a.n2 = a.edges_among + nl;
+  a.work = a.n2 + nl;
+  CK(cudaMemsetAsync(a.max_words, 0, 8, 0));
+  CK(cudaMemsetAsync(a.work, 0, 8, 0));
+  CK(sb::launch_local_spans(a, 0));
+  unsigned int mw[2] = {0, 0};
+  CK(cudaMemcpy(mw, a.max_words, 8, cudaMemcpyDeviceToHost));
+  a.w1_words = std::max(mw[0], 1u);
+  a.w2_words = std::max(mw[1], 1u);
+  a.stride_words = 2ull * (a.w1_words + 1) + a.w2_words;
+  // SB_LOCAL_GLOBAL=1 forces the global-scratch bitmaps (test hook for wide windows)
+  const char* force = getenv("SB_LOCAL_GLOBAL");
+  const bool smem = a.stride_words * 4 <= sb::local_smem_limit() && !(force && atoi(force));
+  if (!smem) {
+    int grid = 0;
+    CK(sb::launch_local(a, false, &grid, 0));
+    CK(cudaMalloc(&scratch, static_cast<uint64_t>(grid) * a.stride_words * 4));
+    a.scratch = scratch;
+  }
+  CK(sb::launch_local(a, smem, nullptr, 0));
+  CK(sync_stream(0));
+  if (control) CK(cudaMemcpy(control, a.control, nl * 8, cudaMemcpyDeviceToHost));
+  if (controllability) CK(cudaMemcpy(controllability, a.controllability, nl * 8, cudaMemcpyDeviceToHost));
+  if (clustering) CK(cudaMemcpy(clustering, a.clustering, nl * 8, cudaMemcpyDeviceToHost));
+  if (edges_among) CK(cudaMemcpy(edges_among, a.edges_among, nl * 8, cudaMemcpyDeviceToHost));
+  if (n2) CK(cudaMemcpy(n2, a.n2, nl * 8, cudaMemcpyDeviceToHost));
+  return SB_OK;
+}
+
 int sb_hb_stats(const sb_hb* h, sb_iter_stats* out, uint32_t cap, uint32_t* count) {
   if (!h) return fail(SB_EINVAL, "NULL handle");
   const uint32_t n = static_cast<uint32_t>(h->stats.size());

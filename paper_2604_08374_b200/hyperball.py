@@ -112,6 +112,17 @@ class DeviceGraph:
         self.n_local = v1 - v0
         return self
 
+    def local_metrics(self, v0: int = 0, v1: int | None = None) -> dict[str, np.ndarray]:
+        """Exact control / controllability / clustering for nodes [v0, v1).
+
+        Needs the full graph on this device (node_range (0, N)); see sb_local_metrics."""
+        v1 = self.n if v1 is None else v1
+        nl = max(v1 - v0, 0)
+        f = [np.zeros(nl, np.float64) for _ in range(3)]
+        u = [np.zeros(nl, np.uint64) for _ in range(2)]
+        check(lib().sb_local_metrics(self._h, v0, v1, *[ptr(x) for x in f], *[ptr(x) for x in u]))
+        return dict(zip(["control", "controllability", "clustering", "edges_among", "n2"], f + u))
+
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:
             lib().sb_graph_destroy(self._h)
