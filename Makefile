@@ -12,7 +12,7 @@ CXXFLAGS := -O3 -std=c++17 -fPIC -Wall -ffp-contract=off -I$(CUDA_INC)
 LIB      := $(PKG)/libsieveball_cuda.so
 TOOL     := tools/sb_hyperball
 
-OBJS := $(BUILD)/sb_kernels.o $(BUILD)/sb_local.o $(BUILD)/sb_runtime.o $(BUILD)/sb_csr.o $(BUILD)/sb_error.o
+OBJS := $(BUILD)/sb_kernels.o $(BUILD)/sb_local.o $(BUILD)/sb_vis.o $(BUILD)/sb_runtime.o $(BUILD)/sb_csr.o $(BUILD)/sb_error.o
 HDRS := $(CSRC)/sb_device.cuh $(CSRC)/sb_internal.h $(CSRC)/sb_error.h include/sieveball_cuda.h
 
 all: $(LIB) $(TOOL) oracle
@@ -25,6 +25,9 @@ $(BUILD)/sb_kernels.o: $(CSRC)/sb_kernels.cu $(HDRS) | $(BUILD)
 
 $(BUILD)/sb_local.o: $(CSRC)/sb_local.cu $(HDRS) | $(BUILD)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(BUILD)/ptxas_local.txt || (cat $(BUILD)/ptxas_local.txt; false)
+
+$(BUILD)/sb_vis.o: $(CSRC)/sb_vis.cu $(HDRS) | $(BUILD)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(BUILD)/ptxas_vis.txt || (cat $(BUILD)/ptxas_vis.txt; false)
 
 $(BUILD)/sb_runtime.o: $(CSRC)/sb_runtime.cu $(HDRS) | $(BUILD)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(BUILD)/ptxas_runtime.txt || (cat $(BUILD)/ptxas_runtime.txt; false)

@@ -20,6 +20,8 @@
  *   metrics: mean_depth, integration_* , moments           sb_hb_metrics
  *
  *   metrics::local_metrics               sb_local_metrics
+ *   oracle exact BFS / neighbourhood function sb_exact_* (bit-parallel, on device)
+ *   cli cmd_analyze CSV                      sb_metrics_write_csv
  *   parallel_ranges (parallel.hpp:20-47)                   sb_partition_edges + sb_comm
  *
  * Conventions: every function returns SB_OK (0) or an error code; the message
@@ -157,6 +159,32 @@ int sb_hb_read_state(const sb_hb* h, double* c_latest, double* c_previous, doubl
 int sb_hb_metrics(const sb_hb* h, const uint32_t* nv, const uint32_t* deg, double* md,
                   double* ihh, double* tekl, double* pv, double* m1, double* m2);
 
+/* ---------------- exact neighbourhood function ----------------
+ * The reference's exact oracle mode (per-source BFS, true neighbourhood
+ * function, Eq. 1 identity) as a bit-parallel BFS on the device: the
+ * HyperBall loop with every HLL row replaced by a reachability bitset over a
+ * block of 2^log2_block sources (log2_block in [12, 16]) and the register max
+ * replaced by OR.  Needs the full graph on the device.  depth_limit 0 =
+ * unlimited; flags: SB_HB_INTERVAL folds runs of consecutive ids through a
+ * sparse table (same result).  sb_exact_run accumulates over the sources
+ * [src_begin, src_end) -- shard sources across GPUs and sum the outputs. */
+typedef struct sb_exact sb_exact;
+int sb_exact_create(sb_graph* g, unsigned log2_block, uint32_t depth_limit, uint32_t flags, sb_exact** out);
+int sb_exact_run(sb_exact* x, uint64_t src_begin, uint64_t src_end, uint32_t* max_depth);
+/* Per node (N entries): sum_d = sum of BFS depths to every reached source,
+ * sum_d2 = sum of squared depths, reach = sources reached incl. itself (the
+ * component size N_v when all sources ran, unlimited depth); hist (N x
+ * hist_cap, row-major, hist_cap > max depth) = # sources at each depth. */
+int sb_exact_read(const sb_exact* x, uint64_t* sum_d, uint64_t* sum_d2, uint32_t* reach, uint32_t* hist,
+                  uint32_t hist_cap);
+int sb_exact_stats(const sb_exact* x, uint64_t* sources_done, uint32_t* max_depth, double* union_ms,
+                   uint64_t* union_launches);
+void sb_exact_destroy(sb_exact* x);
+/* Shannon entropy (bits) of each node's depth distribution (SPEC.md:531-535,
+ * exact-oracle mode): H = -sum_t p_t log2 p_t, p_t = hist[t] / sum_{t>=1} hist[t];
+ * NaN for a node that reaches nothing.  Host computation (libm log2). */
+int sb_depth_entropy(uint64_t n, const uint32_t* hist, uint32_t hist_cap, double* entropy);
+
 /* ---------------- exact local metrics ----------------
  * For nodes [v0, v1) of a device graph that holds the FULL graph (created with
  * node range [0, N); the 2-hop rows of any node are read):
@@ -169,6 +197,20 @@ int sb_hb_metrics(const sb_hb* h, const uint32_t* nv, const uint32_t* deg, doubl
  * Shard by node range across GPUs: no exchange is needed. */
 int sb_local_metrics(sb_graph* g, uint64_t v0, uint64_t v1, double* control, double* controllability,
                      double* clustering, uint64_t* edges_among, uint64_t* n2);
+
+/* ---------------- metric table + CSV ----------------
+ * One row per node; NULL columns are written as NaN (0 for the counts). */
+typedef struct {
+  uint64_t n;
+  const uint32_t* node_id;          /* NULL: 0..n-1 */
+  const double *x, *y;              /* world coordinates of the cell centre */
+  const uint32_t* component_id;
+  const uint32_t* node_count;       /* N_v */
+  const uint32_t* connectivity;     /* deg */
+  const double *md, *ihh, *tekl, *pv, *control, *controllability, *clustering, *entropy, *rel_entropy,
+      *m1, *m2;
+} sb_metric_table;
+int sb_metrics_write_csv(const char* path, const sb_metric_table* t);
 
 typedef struct {
   uint32_t t;              /* iteration number */

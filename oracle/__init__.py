@@ -80,6 +80,12 @@ class Oracle:
             self._local = L.sbo_local_metrics
             self._local.restype = C.c_int
             self._local.argtypes = [C.c_uint64, _u64p, _u32p, _u8p, C.c_uint64, C.c_uint64] + [_f64p] * 3 + [_u64p] * 2
+            self._bfs = L.sbo_exact_bfs
+            self._bfs.restype = C.c_int
+            self._bfs.argtypes = [C.c_uint64, _u64p, _u32p, _u8p, C.c_uint32, _u64p, _u64p, _u32p, _u32p,
+                                  C.c_uint32, C.POINTER(C.c_uint32)]
+            self._entropy = L.sbo_depth_entropy
+            self._entropy.argtypes = [C.c_uint64, _u32p, C.c_uint32, _f64p]
             self._sum_recip = L.sbo_exact_sum_recip
             self._sum_recip.restype = C.c_double
             self._sum_recip.argtypes = [_u32p, C.c_uint64]
@@ -214,6 +220,26 @@ class Oracle:
         if rc:
             raise RuntimeError("local metrics: malformed graph")
         return dict(zip(["control", "controllability", "clustering", "edges_among", "n2"], f + u))
+
+    def exact_bfs(self, csr, depth_limit: int | None = None, cap: int = 64):
+        """Exact per-root BFS: sum_d, sum_d2, reach, depth histogram, entropy."""
+        if self.kind != "port":
+            raise NotImplementedError("the exact oracle is restated in the port only")
+        n = csr.n
+        sd, sd2 = np.zeros(n, np.uint64), np.zeros(n, np.uint64)
+        reach = np.zeros(n, np.uint32)
+        hist = np.zeros(n * cap, np.uint32)
+        md = C.c_uint32()
+        rc = self._bfs(n, csr.offsets, csr.degrees, csr.stream_padded(), int(depth_limit or 0), sd, sd2, reach,
+                       hist, cap, C.byref(md))
+        if rc:
+            raise RuntimeError("exact bfs: malformed graph")
+        if md.value >= cap:
+            return self.exact_bfs(csr, depth_limit, cap=2 * md.value + 1)
+        ent = np.zeros(n, np.float64)
+        self._entropy(n, hist, cap, ent)
+        return dict(sum_d=sd, sum_d2=sd2, reach=reach, hist=hist.reshape(n, cap), entropy=ent,
+                    max_depth=md.value)
 
     def exact_sum_recip(self, degs) -> float:
         d = np.ascontiguousarray(degs, np.uint32)

@@ -430,3 +430,69 @@ int sbo_local_metrics(uint64_t n, const uint64_t* offsets, const uint32_t* degre
   free(mark); free(mark2); free(dg); free(off); free(ids);
   return SBO_OK;
 }
+
+/* ---- exact BFS oracle: per-root BFS over the decoded rows ----
+ * For every root v: sum_d[v] = sum of depths of every node reached within
+ * depth_limit (0 = unlimited), sum_d2 = sum of squared depths, reach[v] = nodes
+ * reached incl. v, hist[v * cap + t] = nodes at depth t (t < cap; deeper
+ * levels are dropped and *max_depth tells the caller).  O(N |E|). */
+int sbo_exact_bfs(uint64_t n, const uint64_t* offsets, const uint32_t* degrees,
+                  const uint8_t* stream, uint32_t depth_limit, uint64_t* sum_d,
+                  uint64_t* sum_d2, uint32_t* reach, uint32_t* hist, uint32_t cap,
+                  uint32_t* max_depth) {
+  uint64_t* off;
+  uint32_t* ids;
+  if (decode_rows(n, offsets, degrees, stream, &off, &ids) != SBO_OK) return SBO_ERUNTIME;
+  uint32_t* dist = (uint32_t*)malloc((n ? n : 1) * sizeof(uint32_t));
+  uint32_t* queue = (uint32_t*)malloc((n ? n : 1) * sizeof(uint32_t));
+  uint32_t dmax = 0;
+  if (hist) memset(hist, 0, n * cap * sizeof(uint32_t));
+  for (uint64_t v = 0; v < n; ++v) {
+    for (uint64_t u = 0; u < n; ++u) dist[u] = UINT32_MAX;
+    uint64_t head = 0, tail = 0, s1 = 0, s2 = 0;
+    dist[v] = 0;
+    queue[tail++] = (uint32_t)v;
+    while (head < tail) {
+      const uint32_t u = queue[head++];
+      const uint32_t du = dist[u];
+      if (du) {
+        s1 += du;
+        s2 += (uint64_t)du * du;
+        if (hist && du < cap) hist[v * cap + du] += 1;
+        if (du > dmax) dmax = du;
+      }
+      if (depth_limit && du == depth_limit) continue;
+      for (uint64_t q = off[u]; q < off[u + 1]; ++q) {
+        const uint32_t w = ids[q];
+        if (dist[w] == UINT32_MAX) {
+          dist[w] = du + 1;
+          queue[tail++] = w;
+        }
+      }
+    }
+    sum_d[v] = s1;
+    sum_d2[v] = s2;
+    reach[v] = (uint32_t)tail;
+  }
+  if (max_depth) *max_depth = dmax;
+  free(dist); free(queue); free(off); free(ids);
+  return SBO_OK;
+}
+
+/* Depth entropy (SPEC.md:531-535 exact mode): H = -sum_t p_t log2 p_t,
+ * p_t = n_t / sum_{t>=1} n_t, increasing t; NaN when nothing is reached. */
+void sbo_depth_entropy(uint64_t n, const uint32_t* hist, uint32_t cap, double* entropy) {
+  for (uint64_t v = 0; v < n; ++v) {
+    const uint32_t* h = hist + v * cap;
+    uint64_t tot = 0;
+    for (uint32_t t = 1; t < cap; ++t) tot += h[t];
+    if (!tot) { entropy[v] = NAN; continue; }
+    double H = 0.0;
+    for (uint32_t t = 1; t < cap; ++t) {
+      if (!h[t]) continue;
+      const double p = (double)h[t] / (double)tot;
+      H -= p * log2(p);
+    }
+    entropy[v] = H + 0.0;
+  }
+}

@@ -48,6 +48,13 @@ class sb_iter_stats(C.Structure):
     ]
 
 
+class sb_metric_table(C.Structure):
+    _fields_ = [("n", C.c_uint64), ("node_id", C.c_void_p), ("x", C.c_void_p), ("y", C.c_void_p),
+                ("component_id", C.c_void_p), ("node_count", C.c_void_p), ("connectivity", C.c_void_p)] + [
+        (k, C.c_void_p) for k in ("md", "ihh", "tekl", "pv", "control", "controllability", "clustering",
+                                  "entropy", "rel_entropy", "m1", "m2")]
+
+
 _vp = C.c_void_p
 _u64 = C.c_uint64
 _u32 = C.c_uint32
@@ -85,6 +92,13 @@ _SIGS = {
     "sb_hb_read_state": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, C.POINTER(_u32), C.POINTER(_i), C.POINTER(_i)]),
     "sb_hb_metrics": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "sb_local_metrics": (_i, [_vp, _u64, _u64, _vp, _vp, _vp, _vp, _vp]),
+    "sb_exact_create": (_i, [_vp, C.c_uint, _u32, _u32, _pp]),
+    "sb_exact_run": (_i, [_vp, _u64, _u64, C.POINTER(_u32)]),
+    "sb_exact_read": (_i, [_vp, _vp, _vp, _vp, _vp, _u32]),
+    "sb_exact_stats": (_i, [_vp, C.POINTER(_u64), C.POINTER(_u32), C.POINTER(C.c_double), C.POINTER(_u64)]),
+    "sb_exact_destroy": (None, [_vp]),
+    "sb_depth_entropy": (_i, [_u64, _vp, _u32, _vp]),
+    "sb_metrics_write_csv": (_i, [C.c_char_p, C.POINTER(sb_metric_table)]),
     "sb_hb_stats": (_i, [_vp, C.POINTER(sb_iter_stats), _u32, C.POINTER(_u32)]),
     "sb_hb_reset": (_i, [_vp]),
     "sb_hb_stream": (_vp, [_vp]),

@@ -80,6 +80,8 @@ class CompressedCsr:
         self.cell_of_node = _view(d.cell_of_node, self.n, np.uint32) if d.cell_of_node else None
         self.hilbert_inverse = _view(d.hilbert_inverse, self.n, np.uint32) if d.hilbert_inverse else None
         self.rows, self.cols = int(d.rows), int(d.cols)
+        self.origin = (float(d.origin_x), float(d.origin_y))
+        self.spacing = float(d.spacing)
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -154,6 +156,15 @@ class CompressedCsr:
     def node_count_of_component(self) -> np.ndarray:
         """N_v per node: exact component size."""
         return self.component_sizes[self.component_id]
+
+    def coordinates(self) -> tuple[np.ndarray, np.ndarray]:
+        """World (x, y) of each node's cell centre: origin + (col + 0.5, row + 0.5) * spacing."""
+        if self.cell_of_node is None or self.cols == 0:
+            nan = np.full(self.n, np.nan)
+            return nan, nan.copy()
+        cell = self.cell_of_node.astype(np.int64)
+        row, col = cell // self.cols, cell % self.cols
+        return (self.origin[0] + (col + 0.5) * self.spacing, self.origin[1] + (row + 0.5) * self.spacing)
 
     def partition(self, parts: int) -> np.ndarray:
         """Edge-balanced contiguous node ranges (bounds[parts+1])."""

@@ -654,4 +654,67 @@ int sb_partition_edges(uint64_t n, const uint64_t* offsets, const uint32_t* degr
   return SB_OK;
 }
 
+// ---------------------------------------------------------------- depth entropy
+// Exact-oracle-mode entropy: Shannon entropy in bits of the
+// node's depth distribution, H = -sum_t p_t log2 p_t with p_t = n_t / S,
+// S = sum_{t>=1} n_t, summed in increasing t (no FMA: -ffp-contract=off).
+int sb_depth_entropy(uint64_t n, const uint32_t* hist, uint32_t hist_cap, double* entropy) {
+  if (!hist || !entropy || hist_cap == 0) return cfail(SB_EINVAL, "sb_depth_entropy: bad arguments");
+  for (uint64_t v = 0; v < n; ++v) {
+    const uint32_t* h = hist + v * hist_cap;
+    uint64_t tot = 0;
+    for (uint32_t t = 1; t < hist_cap; ++t) tot += h[t];
+    if (!tot) {
+      entropy[v] = NAN;
+      continue;
+    }
+    double H = 0.0;
+    for (uint32_t t = 1; t < hist_cap; ++t) {
+      if (!h[t]) continue;
+      const double p = static_cast<double>(h[t]) / static_cast<double>(tot);
+      H -= p * std::log2(p);
+    }
+    entropy[v] = H + 0.0;  // -0.0 -> 0.0 for a single depth bin
+  }
+  return SB_OK;
+}
+
+// ---------------------------------------------------------------- CSV writer
+// cmd_analyze output: one row per node, NaN serialised "NaN",
+// doubles with 17 significant digits (round-trip exact, byte-deterministic).
+static void put_num(FILE* f, double x) {
+  if (std::isnan(x))
+    fputs("NaN", f);
+  else if (std::isinf(x))
+    fputs(x > 0 ? "inf" : "-inf", f);
+  else
+    fprintf(f, "%.17g", x);
+}
+
+int sb_metrics_write_csv(const char* path, const sb_metric_table* t) {
+  if (!path || !t) return cfail(SB_EINVAL, "sb_metrics_write_csv: NULL argument");
+  FILE* f = fopen(path, "wb");
+  if (!f) return cfail(SB_ERUNTIME, "cannot open %s for writing", path);
+  fputs("x,y,node_id,component_id,node_count,connectivity,visual_mean_depth,integration_hh,integration_tekl,"
+        "integration_pv,control,controllability,clustering,entropy,rel_entropy,first_moment,second_moment\n", f);
+  auto col = [](const double* c, uint64_t i) { return c ? c[i] : NAN; };
+  for (uint64_t i = 0; i < t->n; ++i) {
+    put_num(f, col(t->x, i));
+    fputc(',', f);
+    put_num(f, col(t->y, i));
+    fprintf(f, ",%llu,%u,%u,%u,", static_cast<unsigned long long>(t->node_id ? t->node_id[i] : i),
+            t->component_id ? t->component_id[i] : 0u, t->node_count ? t->node_count[i] : 0u,
+            t->connectivity ? t->connectivity[i] : 0u);
+    const double* cols[11] = {t->md, t->ihh, t->tekl, t->pv, t->control, t->controllability,
+                              t->clustering, t->entropy, t->rel_entropy, t->m1, t->m2};
+    for (int k = 0; k < 11; ++k) {
+      put_num(f, col(cols[k], i));
+      fputc(k == 10 ? '\n' : ',', f);
+    }
+  }
+  const bool bad = ferror(f) != 0;
+  if (fclose(f) != 0 || bad) return cfail(SB_ERUNTIME, "write error on %s", path);
+  return SB_OK;
+}
+
 }  // extern "C"

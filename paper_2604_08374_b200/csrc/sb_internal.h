@@ -106,6 +106,31 @@ struct ExactArgs {
   unsigned long long* changed_count;
 };
 
+// On-device grid visibility graph construction (sb_vis.cu).
+struct VisArgs {
+  uint32_t rows, cols;
+  uint64_t radius2;            // 0 = unlimited
+  int64_t R;                   // row reach: isqrt(radius2) or max(rows, cols)
+  const uint8_t* blocked;      // rows * cols, 1 = obstacle cell
+  const uint32_t* pref;        // (rows + 1) * (cols + 1) prefix counts of blocked cells
+  const uint32_t* node_of_cell;
+  const uint32_t* cell_of_node;
+  uint64_t n;
+  uint32_t* deg;               // pass 1
+  uint64_t* bytes;             // pass 1
+  const uint64_t* offsets;     // pass 2
+  uint8_t* stream;             // pass 2
+  uint32_t* parent;            // components
+};
+
+cudaError_t launch_vis_prepare(VisArgs& a, uint32_t* pref, uint32_t* tmp_scan, uint64_t* n_out, cudaStream_t s);
+cudaError_t launch_vis_maps(const VisArgs& a, const uint32_t* scan, uint32_t* node_of_cell, uint32_t* cell_of_node,
+                            cudaStream_t s);
+cudaError_t launch_vis_rows(const VisArgs& a, bool write, cudaStream_t s);
+cudaError_t launch_scan_u64(const uint64_t* in, uint64_t* out, uint64_t count, cudaStream_t s);
+cudaError_t launch_vis_components(const VisArgs& a, uint32_t* comp, uint32_t* sizes, uint32_t* tmp2n,
+                                  uint64_t* n_comp, cudaStream_t s);
+
 struct MetricArgs {
   uint64_t n;
   const double* sum_d;

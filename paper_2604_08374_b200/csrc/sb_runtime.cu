@@ -190,6 +190,84 @@ int sb_device_count(int* n) {
 int sb_check_convergence(double max_increase) { return max_increase <= 0.5 ? 1 : 0; }
 
 // ------------------------------------------------------------------ graph
+// Work items, CTA tiles and the upload-time validation of the device-resident
+// stream slice (shared by sb_graph_create and the on-device grid builder).
+static int graph_setup(sb_graph* g, const uint32_t* deg_local) {
+  // Work items: <= chunk neighbours each, sized so the edge work splits into
+  // ~4 items per resident warp (load balance) but stays >= 512 ids (decode
+  // and merge amortisation).
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
+  const uint64_t target = g->edges_local / (static_cast<uint64_t>(sms) * 64 * 4);
+  g->chunk = static_cast<uint32_t>(std::min<uint64_t>(8192, std::max<uint64_t>(512, target)));
+  std::vector<uint32_t> node_item(g->n_local + 1);
+  uint64_t items = 0;
+  for (uint64_t i = 0; i < g->n_local; ++i) {
+    node_item[i] = static_cast<uint32_t>(items);
+    const uint32_t d = deg_local[i];
+    items += d ? (d + g->chunk - 1) / g->chunk : 1;
+  }
+  if (items > 0xffffffffull) return fail(SB_EINVAL, "too many work items");
+  node_item[g->n_local] = static_cast<uint32_t>(items);
+  g->n_items = items;
+  // Tiles for the CTA schedule: group k = local nodes [8k, 8k+8), one tile per
+  // chunk index up to the group's largest item count.
+  std::vector<uint32_t> tn0, tq;
+  for (uint64_t k = 0; k < g->n_local; k += 8) {
+    uint32_t mx = 0;
+    for (uint64_t i = k; i < std::min<uint64_t>(k + 8, g->n_local); ++i) mx = std::max(mx, node_item[i + 1] - node_item[i]);
+    for (uint32_t q = 0; q < mx; ++q) {
+      tn0.push_back(static_cast<uint32_t>(k));
+      tq.push_back(q);
+    }
+  }
+  g->n_tiles = tn0.size();
+  CK(cudaMalloc(&g->d_tile_node0, std::max<size_t>(tn0.size(), 1) * 4));
+  CK(cudaMalloc(&g->d_tile_q, std::max<size_t>(tq.size(), 1) * 4));
+  if (!tn0.empty()) {
+    CK(cudaMemcpy(g->d_tile_node0, tn0.data(), tn0.size() * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(g->d_tile_q, tq.data(), tq.size() * 4, cudaMemcpyHostToDevice));
+  }
+  CK(cudaMalloc(&g->d_node_item, node_item.size() * 4));
+  CK(cudaMemcpy(g->d_node_item, node_item.data(), node_item.size() * 4, cudaMemcpyHostToDevice));
+  const uint64_t ni = std::max<uint64_t>(items, 1);
+  CK(cudaMalloc(&g->d_item_off, ni * 8));
+  CK(cudaMalloc(&g->d_item_base, ni * 4));
+  CK(cudaMalloc(&g->d_item_count, ni * 4));
+  CK(cudaMalloc(&g->d_item_node, ni * 4));
+  unsigned long long* d_err = nullptr;
+  CK(cudaMalloc(&d_err, 16));
+  CK(cudaMemset(d_err, 0xff, 8));
+  CK(cudaMemset(reinterpret_cast<uint8_t*>(d_err) + 8, 0, 8));
+  if (g->n_local) {
+    sb::BuildArgs a{};
+    a.stream = g->d_stream;
+    a.row_off = g->d_rowoff;
+    a.degrees = g->d_deg;
+    a.n_local = g->n_local;
+    a.n_global = g->n;
+    a.chunk = g->chunk;
+    a.node_item = g->d_node_item;
+    a.item_off = g->d_item_off;
+    a.item_base = g->d_item_base;
+    a.item_count = g->d_item_count;
+    a.item_node = g->d_item_node;
+    a.err_node = d_err;
+    a.max_run = reinterpret_cast<unsigned int*>(d_err + 1);
+    CK(sb::launch_build_items(a, 0));
+  }
+  CK(sync_stream(0));
+  unsigned long long err = 0;
+  CK(cudaMemcpy(&err, d_err, 8, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(&g->max_run, d_err + 1, 4, cudaMemcpyDeviceToHost));
+  cudaFree(d_err);
+  if (err != ~0ull)
+    return fail(SB_ERUNTIME, "cgraph: malformed compressed row at node %llu (bad varint, "
+                             "non-increasing or out-of-range id, or degree mismatch)",
+                (unsigned long long)(err + g->v0));
+  return SB_OK;
+}
+
 int sb_graph_create(uint64_t n, const uint64_t* offsets, const uint32_t* degrees,
                     const uint8_t* stream, uint64_t stream_len, const uint32_t* orig_id,
                     uint64_t node_begin, uint64_t node_end, int device, sb_graph** out) {
@@ -239,78 +317,8 @@ int sb_graph_create(uint64_t n, const uint64_t* offsets, const uint32_t* degrees
     GK(cudaMalloc(&g->d_orig, n * 4));
     GK(cudaMemcpy(g->d_orig, orig_id, n * 4, cudaMemcpyHostToDevice));
   }
-  // Work items: <= chunk neighbours each, sized so the edge work splits into
-  // ~4 items per resident warp (load balance) but stays >= 512 ids (decode
-  // and merge amortisation).
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-  const uint64_t target = edges / (static_cast<uint64_t>(sms) * 64 * 4);
-  g->chunk = static_cast<uint32_t>(std::min<uint64_t>(8192, std::max<uint64_t>(512, target)));
-  std::vector<uint32_t> node_item(g->n_local + 1);
-  uint64_t items = 0;
-  for (uint64_t i = 0; i < g->n_local; ++i) {
-    node_item[i] = static_cast<uint32_t>(items);
-    const uint32_t d = degrees[node_begin + i];
-    items += d ? (d + g->chunk - 1) / g->chunk : 1;
-  }
-  if (items > 0xffffffffull) return bail(fail(SB_EINVAL, "too many work items"));
-  node_item[g->n_local] = static_cast<uint32_t>(items);
-  g->n_items = items;
-  // Tiles for the CTA schedule: group k = local nodes [8k, 8k+8), one tile per
-  // chunk index up to the group's largest item count.
-  std::vector<uint32_t> tn0, tq;
-  for (uint64_t k = 0; k < g->n_local; k += 8) {
-    uint32_t mx = 0;
-    for (uint64_t i = k; i < std::min<uint64_t>(k + 8, g->n_local); ++i) mx = std::max(mx, node_item[i + 1] - node_item[i]);
-    for (uint32_t q = 0; q < mx; ++q) {
-      tn0.push_back(static_cast<uint32_t>(k));
-      tq.push_back(q);
-    }
-  }
-  g->n_tiles = tn0.size();
-  GK(cudaMalloc(&g->d_tile_node0, std::max<size_t>(tn0.size(), 1) * 4));
-  GK(cudaMalloc(&g->d_tile_q, std::max<size_t>(tq.size(), 1) * 4));
-  if (!tn0.empty()) {
-    GK(cudaMemcpy(g->d_tile_node0, tn0.data(), tn0.size() * 4, cudaMemcpyHostToDevice));
-    GK(cudaMemcpy(g->d_tile_q, tq.data(), tq.size() * 4, cudaMemcpyHostToDevice));
-  }
-  GK(cudaMalloc(&g->d_node_item, node_item.size() * 4));
-  GK(cudaMemcpy(g->d_node_item, node_item.data(), node_item.size() * 4, cudaMemcpyHostToDevice));
-  const uint64_t ni = std::max<uint64_t>(items, 1);
-  GK(cudaMalloc(&g->d_item_off, ni * 8));
-  GK(cudaMalloc(&g->d_item_base, ni * 4));
-  GK(cudaMalloc(&g->d_item_count, ni * 4));
-  GK(cudaMalloc(&g->d_item_node, ni * 4));
-  unsigned long long* d_err = nullptr;
-  GK(cudaMalloc(&d_err, 16));
-  GK(cudaMemset(d_err, 0xff, 8));
-  GK(cudaMemset(reinterpret_cast<uint8_t*>(d_err) + 8, 0, 8));
-  if (g->n_local) {
-    sb::BuildArgs a{};
-    a.stream = g->d_stream;
-    a.row_off = g->d_rowoff;
-    a.degrees = g->d_deg;
-    a.n_local = g->n_local;
-    a.n_global = n;
-    a.chunk = g->chunk;
-    a.node_item = g->d_node_item;
-    a.item_off = g->d_item_off;
-    a.item_base = g->d_item_base;
-    a.item_count = g->d_item_count;
-    a.item_node = g->d_item_node;
-    a.err_node = d_err;
-    a.max_run = reinterpret_cast<unsigned int*>(d_err + 1);
-    GK(sb::launch_build_items(a, 0));
-  }
-  GK(sync_stream(0));
-  unsigned long long err = 0;
-  GK(cudaMemcpy(&err, d_err, 8, cudaMemcpyDeviceToHost));
-  GK(cudaMemcpy(&g->max_run, d_err + 1, 4, cudaMemcpyDeviceToHost));
-  cudaFree(d_err);
-  if (err != ~0ull)
-    return bail(fail(SB_ERUNTIME, "cgraph: malformed compressed row at node %llu (bad varint, "
-                                  "non-increasing or out-of-range id, or degree mismatch)",
-                     (unsigned long long)(err + node_begin)));
+  const int rc = graph_setup(g, degrees + node_begin);
+  if (rc) return bail(rc);
 #undef GK
   *out = g;
   return SB_OK;
@@ -780,6 +788,225 @@ int sb_hb_metrics(const sb_hb* hc, const uint32_t* nv, const uint32_t* deg, doub
   CK(sync_stream(h->stream));
   return SB_OK;
 }
+
+// ------------------------------------------------------------------ exact mode
+// Exact neighbourhood function: bit-parallel BFS, the
+// HyperBall loop with bitset rows and an OR union (see exact_* kernels).
+struct sb_exact {
+  sb_graph* g = nullptr;
+  int P = 10;                       // row geometry: 2^(P-1) bytes = 2^(P+2) sources
+  uint64_t row = 0, block = 0;
+  uint32_t depth = 0, flags = 0;
+  int slices = 1, levels = 0;
+  uint8_t* d_plane[2] = {nullptr, nullptr};
+  uint8_t* d_changed = nullptr;     // union epilogue flags (unused by the count)
+  uint8_t* d_scratch = nullptr;
+  uint32_t* d_counter = nullptr;
+  uint8_t* d_st = nullptr;
+  uint32_t* d_pop = nullptr;
+  uint32_t* d_reach = nullptr;
+  unsigned long long* d_sum = nullptr;   // [sum_d n | sum_d2 n]
+  uint32_t* d_hist = nullptr;
+  uint32_t hist_cap = 0;
+  unsigned long long* d_misc = nullptr;  // [0] work, [1] changed count
+  uint32_t max_depth = 0;
+  uint64_t sources_done = 0;
+  double union_ms = 0.0;
+  uint64_t union_launches = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  ~sb_exact() {
+    DeviceGuard dg(g ? g->device : 0);
+    for (int i = 0; i < 2; ++i) dfree(d_plane[i]);
+    dfree(d_changed); dfree(d_scratch); dfree(d_counter); dfree(d_st); dfree(d_pop);
+    dfree(d_reach); dfree(d_sum); dfree(d_hist); dfree(d_misc);
+    for (auto e : ev) if (e) cudaEventDestroy(e);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+static int exact_grow_hist(sb_exact* x, uint32_t need) {
+  if (need < x->hist_cap) return SB_OK;
+  uint32_t cap = std::max<uint32_t>(x->hist_cap * 2, 16);
+  while (cap <= need) cap *= 2;
+  const uint64_t n = x->g->n;
+  uint32_t* nh = nullptr;
+  CK(cudaMalloc(&nh, n * cap * 4));
+  CK(cudaMemsetAsync(nh, 0, n * cap * 4, x->stream));
+  if (x->d_hist)
+    CK(cudaMemcpy2DAsync(nh, cap * 4, x->d_hist, x->hist_cap * 4, x->hist_cap * 4, n, cudaMemcpyDeviceToDevice,
+                         x->stream));
+  CK(sync_stream(x->stream));
+  dfree(x->d_hist);
+  x->d_hist = nh;
+  x->hist_cap = cap;
+  return SB_OK;
+}
+
+int sb_exact_create(sb_graph* g, unsigned log2_block, uint32_t depth_limit, uint32_t flags, sb_exact** out) {
+  if (!out) return fail(SB_EINVAL, "sb_exact_create: out is NULL");
+  *out = nullptr;
+  if (!g) return fail(SB_EINVAL, "sb_exact_create: NULL graph");
+  if (g->v0 != 0 || g->v1 != g->n) return fail(SB_EINVAL, "sb_exact_create: needs the full graph on the device");
+  if (log2_block < 12 || log2_block > 16) return fail(SB_EINVAL, "sb_exact_create: log2_block must be in [12, 16]");
+  if (flags & ~(uint32_t)SB_HB_INTERVAL) return fail(SB_EINVAL, "sb_exact_create: only SB_HB_INTERVAL is supported");
+  if (g->n == 0) return fail(SB_EINVAL, "sb_exact_create: graph empty");
+  DeviceGuard dg(g->device);
+  auto* x = new sb_exact();
+  x->g = g;
+  x->P = static_cast<int>(log2_block) - 2;
+  x->row = 1ull << (x->P - 1);
+  x->block = 1ull << log2_block;
+  x->depth = depth_limit;
+  x->flags = flags;
+  x->slices = sb::union_slices(x->P);
+  auto bail = [&](int rc) { delete x; return rc; };
+#define XK(e)                                                 \
+  do {                                                        \
+    cudaError_t e_ = (e);                                     \
+    if (e_ != cudaSuccess) return bail(cuda_fail(e_, #e));    \
+  } while (0)
+  XK(cudaStreamCreateWithFlags(&x->stream, cudaStreamNonBlocking));
+  for (auto& e : x->ev) XK(cudaEventCreate(&e));
+  const uint64_t n = g->n, plane = n * x->row;
+  for (int i = 0; i < 2; ++i) XK(cudaMalloc(&x->d_plane[i], plane + 64));
+  XK(cudaMalloc(&x->d_changed, n));
+  XK(cudaMalloc(&x->d_scratch, std::max<uint64_t>(g->n_items, 1) * x->slices * 512));
+  XK(cudaMalloc(&x->d_counter, n * x->slices * 4));
+  XK(cudaMemset(x->d_counter, 0, n * x->slices * 4));
+  XK(cudaMalloc(&x->d_pop, n * 4));
+  XK(cudaMalloc(&x->d_reach, n * 4));
+  XK(cudaMemset(x->d_reach, 0, n * 4));
+  XK(cudaMalloc(&x->d_sum, 2 * n * 8));
+  XK(cudaMemset(x->d_sum, 0, 2 * n * 8));
+  XK(cudaMalloc(&x->d_misc, 2 * 8));
+  if (flags & SB_HB_INTERVAL) {
+    int K = 0;
+    while (K < 10 && (2u << K) <= g->max_run) ++K;
+    x->levels = K;
+    if (K) XK(cudaMalloc(&x->d_st, static_cast<uint64_t>(K) * plane + 64));
+    const int rc = build_run_index(g);
+    if (rc) return bail(rc);
+  }
+#undef XK
+  const int rc = exact_grow_hist(x, 15);
+  if (rc) return bail(rc);
+  *out = x;
+  return SB_OK;
+}
+
+int sb_exact_run(sb_exact* x, uint64_t src_begin, uint64_t src_end, uint32_t* max_depth) {
+  if (!x) return fail(SB_EINVAL, "NULL handle");
+  sb_graph* g = x->g;
+  if (src_begin > src_end || src_end > g->n) return fail(SB_EINVAL, "sb_exact_run: bad source range");
+  DeviceGuard dg(g->device);
+  const uint64_t n = g->n;
+  sb::ExactArgs e{};
+  e.n = n;
+  e.pop = x->d_pop;
+  e.reach = x->d_reach;
+  e.sum_d = x->d_sum;
+  e.sum_d2 = x->d_sum + n;
+  e.changed_count = x->d_misc + 1;
+  for (uint64_t s0 = src_begin; s0 < src_end; s0 += x->block) {
+    const uint64_t s1 = std::min(s0 + x->block, src_end);
+    int L = 0;
+    e.plane = x->d_plane[L];
+    e.s0 = s0;
+    e.s1 = s1;
+    CK(sb::launch_exact_init(x->P, e, x->stream));
+    for (uint32_t t = 1;; ++t) {
+      int rc = exact_grow_hist(x, t);
+      if (rc) return rc;
+      e.hist = x->d_hist;
+      e.hist_cap = x->hist_cap;
+      CK(cudaMemsetAsync(x->d_misc, 0, 16, x->stream));
+      sb::UnionArgs u{};
+      u.stream = g->d_stream;
+      u.item_off = g->d_item_off;
+      u.item_base = g->d_item_base;
+      u.item_count = g->d_item_count;
+      u.item_node = g->d_item_node;
+      u.node_item = g->d_node_item;
+      u.n_items = g->n_items;
+      u.node_begin = 0;
+      u.cur = x->d_plane[L];
+      u.next = x->d_plane[1 - L];
+      u.scratch = x->d_scratch;
+      u.node_counter = x->d_counter;
+      u.changed_out = x->d_changed;
+      u.changed_in = x->d_changed;
+      u.work = x->d_misc;
+      u.n_local = n;
+      u.n_tiles = g->n_tiles;
+      u.tile_node0 = g->d_tile_node0;
+      u.tile_q = g->d_tile_q;
+      CK(cudaEventRecord(x->ev[0], x->stream));
+      if (x->flags & SB_HB_INTERVAL) {
+        if (x->levels) CK(sb::launch_st_build(x->P, x->d_plane[L], x->d_st, n, x->levels, x->stream, true));
+        sb::IntervalArgs ia{};
+        ia.u = u;
+        ia.st = x->d_st ? x->d_st : x->d_plane[L];
+        ia.n_global = n;
+        ia.levels = x->levels;
+        ia.run_off = g->d_run_off;
+        ia.run_s = g->d_run_s;
+        ia.run_e = g->d_run_e;
+        CK(sb::launch_union_interval(x->P, ia, x->stream, true));
+      } else {
+        CK(sb::launch_union_or(x->P, u, x->stream));
+      }
+      CK(cudaEventRecord(x->ev[1], x->stream));
+      e.plane = x->d_plane[1 - L];
+      e.t = t;
+      CK(sb::launch_exact_count(x->P, e, x->stream));
+      unsigned long long changed = 0;
+      CK(cudaMemcpyAsync(&changed, x->d_misc + 1, 8, cudaMemcpyDeviceToHost, x->stream));
+      CK(sync_stream(x->stream));
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, x->ev[0], x->ev[1]);
+      x->union_ms += ms;
+      x->union_launches += 1;
+      if (changed == 0) break;  // no row grew: every BFS of the block is complete
+      x->max_depth = std::max(x->max_depth, t);
+      if (x->depth && t == x->depth) break;
+      L = 1 - L;
+    }
+    x->sources_done += s1 - s0;
+  }
+  if (max_depth) *max_depth = x->max_depth;
+  return SB_OK;
+}
+
+int sb_exact_read(const sb_exact* x, uint64_t* sum_d, uint64_t* sum_d2, uint32_t* reach, uint32_t* hist,
+                  uint32_t hist_cap) {
+  if (!x) return fail(SB_EINVAL, "NULL handle");
+  const uint64_t n = x->g->n;
+  if (hist && hist_cap <= x->max_depth)
+    return fail(SB_EINVAL, "sb_exact_read: hist_cap %u <= max depth %u", hist_cap, x->max_depth);
+  DeviceGuard dg(x->g->device);
+  if (sum_d) CK(cudaMemcpy(sum_d, x->d_sum, n * 8, cudaMemcpyDeviceToHost));
+  if (sum_d2) CK(cudaMemcpy(sum_d2, x->d_sum + n, n * 8, cudaMemcpyDeviceToHost));
+  if (reach) CK(cudaMemcpy(reach, x->d_reach, n * 4, cudaMemcpyDeviceToHost));
+  if (hist) {
+    const uint32_t w = std::min(hist_cap, x->hist_cap);
+    memset(hist, 0, n * hist_cap * 4);
+    CK(cudaMemcpy2D(hist, hist_cap * 4, x->d_hist, x->hist_cap * 4, w * 4, n, cudaMemcpyDeviceToHost));
+  }
+  return SB_OK;
+}
+
+int sb_exact_stats(const sb_exact* x, uint64_t* sources_done, uint32_t* max_depth, double* union_ms,
+                   uint64_t* union_launches) {
+  if (!x) return fail(SB_EINVAL, "NULL handle");
+  if (sources_done) *sources_done = x->sources_done;
+  if (max_depth) *max_depth = x->max_depth;
+  if (union_ms) *union_ms = x->union_ms;
+  if (union_launches) *union_launches = x->union_launches;
+  return SB_OK;
+}
+
+void sb_exact_destroy(sb_exact* x) { delete x; }
 
 // ------------------------------------------------------------------ local metrics
 // Exact 1-/2-hop metrics over the device-resident run index.

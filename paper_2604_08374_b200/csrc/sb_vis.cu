@@ -1,0 +1,350 @@
+// sb_vis.cu -- on-device construction of the grid visibility graph straight
+// into the HBM-resident LEB128 delta-CSR (replaces the CPU build of
+// cmd_build_graph: grid -> visibility -> compressed CSR, SPEC.md:100-219,
+// PAPER.md:222-307), so the HyperBall path never round-trips the 4.8 GB
+// stream through the host.
+//
+// Byte-identical to the host generator (sb_csr_synth_grid, sb_csr.cpp):
+//   * same exact integer line of sight (cell centres at odd coordinates, the
+//     open segment may not cross an obstacle cell's interior, exact corner
+//     crossings step diagonally) behind the same blocked-box prefix-sum test;
+//   * same candidate order (row by row, column ascending = raster id order);
+//   * same delta-LEB128 rows (first id absolute);
+//   * same component ids (UnionFind::finalize: dense ids by first node,
+//     union_find.hpp:37-52) from the same 8-neighbour union.
+//
+//   vis_rows_kernel<false>  warp per node: degree and row bytes
+//   vis_rows_kernel<true>   warp per node: writes the row at offsets[v]
+//   Each warp step tests 32 consecutive candidate cells of one grid row; the
+//   visible ones are ordered by a ballot, their deltas / varint lengths come
+//   from the previous visible lane (or the carried previous id) and a warp
+//   prefix sum of the lengths places every varint.
+#include <cub/cub.cuh>
+
+#include "sb_device.cuh"
+#include "sb_internal.h"
+
+namespace sb {
+
+__device__ __forceinline__ int64_t imax64(int64_t a, int64_t b) { return a > b ? a : b; }
+__device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+__device__ __forceinline__ uint64_t isqrt64_dev(uint64_t v) {
+  uint64_t r = static_cast<uint64_t>(sqrt(static_cast<double>(v)));
+  while (r * r > v) --r;
+  while ((r + 1) * (r + 1) <= v) ++r;
+  return r;
+}
+
+__device__ __forceinline__ bool any_blocked(const VisArgs& a, int r0, int c0, int r1, int c1) {
+  if (r0 > r1) {
+    const int t = r0;
+    r0 = r1;
+    r1 = t;
+  }
+  if (c0 > c1) {
+    const int t = c0;
+    c0 = c1;
+    c1 = t;
+  }
+  const uint64_t W = a.cols + 1;
+  const uint32_t s = a.pref[(r1 + 1) * W + (c1 + 1)] - a.pref[r0 * W + (c1 + 1)] - a.pref[(r1 + 1) * W + c0] +
+                     a.pref[r0 * W + c0];
+  return s != 0;
+}
+
+// Exact integer line of sight between the centres of (r1,c1) and (r2,c2).
+__device__ bool visible(const VisArgs& a, int r1, int c1, int r2, int c2) {
+  if (!any_blocked(a, r1, c1, r2, c2)) return true;
+  const int dx = c2 - c1, dy = r2 - r1;
+  const int sx = dx > 0 ? 1 : -1, sy = dy > 0 ? 1 : -1;
+  const int64_t ax = dx < 0 ? -dx : dx, ay = dy < 0 ? -dy : dy;
+  int x = c1, y = r1;
+  int64_t k = 0, j = 0;
+  while (k < ax || j < ay) {
+    if (k < ax && j < ay) {
+      const int64_t lhs = (2 * k + 1) * ay, rhs = (2 * j + 1) * ax;
+      if (lhs < rhs) {
+        x += sx;
+        ++k;
+      } else if (lhs > rhs) {
+        y += sy;
+        ++j;
+      } else {
+        x += sx;
+        y += sy;
+        ++k;
+        ++j;
+      }
+    } else if (k < ax) {
+      x += sx;
+      ++k;
+    } else {
+      y += sy;
+      ++j;
+    }
+    if (x == c2 && y == r2) break;
+    if (a.blocked[static_cast<uint64_t>(y) * a.cols + x]) return false;
+  }
+  return true;
+}
+
+__device__ __forceinline__ uint32_t leb_len32(uint32_t v) {
+  return v < (1u << 7) ? 1u : v < (1u << 14) ? 2u : v < (1u << 21) ? 3u : v < (1u << 28) ? 4u : 5u;
+}
+
+template <bool WRITE>
+__global__ void __launch_bounds__(256) vis_rows_kernel(VisArgs a) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t ltm = (1u << lane) - 1u;
+  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = (gridDim.x * (uint64_t)blockDim.x) >> 5;
+  for (uint64_t v = gw; v < a.n; v += nw) {
+    const uint32_t cell = a.cell_of_node[v];
+    const int r = static_cast<int>(cell / a.cols), cc = static_cast<int>(cell % a.cols);
+    const int r_lo = static_cast<int>(imax64(0, r - a.R));
+    const int r_hi = static_cast<int>(imin64(static_cast<int64_t>(a.rows) - 1, r + a.R));
+    uint32_t deg = 0;
+    uint64_t pos = WRITE ? a.offsets[v] : 0, bytes = 0;
+    bool have_prev = false;
+    uint32_t prev = 0;
+    for (int r2 = r_lo; r2 <= r_hi; ++r2) {
+      const int64_t dr = r2 - r;
+      int64_t span = a.cols;
+      if (a.radius2) span = static_cast<int64_t>(isqrt64_dev(a.radius2 - static_cast<uint64_t>(dr * dr)));
+      const int c_lo = static_cast<int>(imax64(0, cc - span));
+      const int c_hi = static_cast<int>(imin64(static_cast<int64_t>(a.cols) - 1, cc + span));
+      const uint64_t rowbase = static_cast<uint64_t>(r2) * a.cols;
+      for (int base = c_lo; base <= c_hi; base += 32) {
+        const int c2 = base + lane;
+        bool emit = false;
+        uint32_t w = 0;
+        if (c2 <= c_hi && !(r2 == r && c2 == cc)) {
+          w = a.node_of_cell[rowbase + c2];
+          if (w != 0xffffffffu) emit = visible(a, r, cc, r2, c2);
+        }
+        const uint32_t mask = __ballot_sync(FULL, emit);
+        if (!mask) continue;
+        const uint32_t lower = mask & ltm;
+        const uint32_t pw = __shfl_sync(FULL, w, lower ? 31 - __clz(lower) : 0);
+        const uint32_t delta = lower ? w - pw : (have_prev ? w - prev : w);
+        const uint32_t len = emit ? leb_len32(delta) : 0u;
+        uint32_t incl = len;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const uint32_t y = __shfl_up_sync(FULL, incl, d);
+          if (lane >= d) incl += y;
+        }
+        if (WRITE && emit) {
+          uint8_t* o = a.stream + pos + (incl - len);
+          uint32_t x = delta;
+          while (x >= 0x80u) {  // leb128.hpp:12-18
+            *o++ = static_cast<uint8_t>(x) | 0x80u;
+            x >>= 7;
+          }
+          *o = static_cast<uint8_t>(x);
+        }
+        const uint32_t total = __shfl_sync(FULL, incl, 31);
+        pos += total;
+        bytes += total;
+        deg += __popc(mask);
+        prev = __shfl_sync(FULL, w, 31 - __clz(mask));
+        have_prev = true;
+      }
+    }
+    if (!WRITE && lane == 0) {
+      a.deg[v] = deg;
+      a.bytes[v] = bytes;
+    }
+  }
+}
+
+// ---- grid preparation -------------------------------------------------------
+__global__ void pref_rows_kernel(VisArgs a, uint32_t* pref) {
+  const uint64_t W = a.cols + 1;
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r <= a.rows; r += gridDim.x * blockDim.x) {
+    uint32_t acc = 0;
+    pref[r * W] = 0;
+    for (uint32_t c = 0; c < a.cols; ++c) {
+      if (r > 0) acc += a.blocked[static_cast<uint64_t>(r - 1) * a.cols + c];
+      pref[r * W + c + 1] = acc;
+    }
+  }
+}
+
+__global__ void pref_cols_kernel(VisArgs a, uint32_t* pref) {
+  const uint64_t W = a.cols + 1;
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c <= a.cols; c += gridDim.x * blockDim.x)
+    for (uint32_t r = 1; r <= a.rows; ++r) pref[r * W + c] += pref[(r - 1) * W + c];
+}
+
+__global__ void free_flags_kernel(const uint8_t* blocked, uint64_t cells, uint32_t* flag) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cells; i += gridDim.x * (uint64_t)blockDim.x)
+    flag[i] = blocked[i] ? 0u : 1u;
+}
+
+__global__ void node_maps_kernel(const uint8_t* blocked, uint64_t cells, const uint32_t* scan, uint32_t* node_of_cell,
+                                 uint32_t* cell_of_node) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cells;
+       i += gridDim.x * (uint64_t)blockDim.x) {
+    if (blocked[i]) {
+      node_of_cell[i] = 0xffffffffu;
+    } else {
+      node_of_cell[i] = scan[i];
+      cell_of_node[scan[i]] = static_cast<uint32_t>(i);
+    }
+  }
+}
+
+// ---- components (8-neighbour union, lock-free union-find) -------------------
+__device__ __forceinline__ uint32_t uf_find(uint32_t* parent, uint32_t v) {
+  uint32_t p = parent[v];
+  while (p != v) {
+    const uint32_t gp = parent[p];
+    if (gp != p) parent[v] = gp;  // path halving (benign race)
+    v = p;
+    p = gp;
+  }
+  return v;
+}
+
+__global__ void cc_init_kernel(uint32_t* parent, uint64_t n) {
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += gridDim.x * (uint64_t)blockDim.x)
+    parent[v] = static_cast<uint32_t>(v);
+}
+
+// Hooks the larger root under the smaller one, so every root is its
+// component's smallest node id (= UnionFind's first-occurrence order).
+__global__ void cc_hook_kernel(VisArgs a) {
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < a.n; v += gridDim.x * (uint64_t)blockDim.x) {
+    const uint32_t cell = a.cell_of_node[v];
+    const int r = static_cast<int>(cell / a.cols), cc = static_cast<int>(cell % a.cols);
+    for (int dr = -1; dr <= 1; ++dr)
+      for (int dc = -1; dc <= 1; ++dc) {
+        if (!dr && !dc) continue;
+        const int r2 = r + dr, c2 = cc + dc;
+        if (r2 < 0 || c2 < 0 || r2 >= static_cast<int>(a.rows) || c2 >= static_cast<int>(a.cols)) continue;
+        if (a.radius2 && static_cast<uint64_t>(dr * dr + dc * dc) > a.radius2) continue;
+        const uint32_t w = a.node_of_cell[static_cast<uint64_t>(r2) * a.cols + c2];
+        if (w == 0xffffffffu || !visible(a, r, cc, r2, c2)) continue;
+        uint32_t u = static_cast<uint32_t>(v), x = w;
+        for (;;) {
+          u = uf_find(a.parent, u);
+          x = uf_find(a.parent, x);
+          if (u == x) break;
+          if (u < x) {
+            const uint32_t t = u;
+            u = x;
+            x = t;
+          }
+          if (atomicCAS(a.parent + u, u, x) == u) break;
+        }
+      }
+  }
+}
+
+__global__ void cc_flatten_kernel(uint32_t* parent, uint64_t n, uint32_t* is_root) {
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += gridDim.x * (uint64_t)blockDim.x) {
+    const uint32_t r = uf_find(parent, static_cast<uint32_t>(v));
+    parent[v] = r;
+    is_root[v] = r == v ? 1u : 0u;
+  }
+}
+
+__global__ void cc_label_kernel(const uint32_t* parent, const uint32_t* root_rank, uint64_t n, uint32_t* comp,
+                                uint32_t* sizes) {
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += gridDim.x * (uint64_t)blockDim.x) {
+    const uint32_t c = root_rank[parent[v]];
+    comp[v] = c;
+    atomicAdd(sizes + c, 1u);
+  }
+}
+
+static int sms() {
+  int dev = 0, s = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&s, cudaDevAttrMultiProcessorCount, dev);
+  return s;
+}
+
+cudaError_t launch_vis_prepare(VisArgs& a, uint32_t* pref, uint32_t* tmp_scan, uint64_t* n_out, cudaStream_t s) {
+  const uint64_t cells = static_cast<uint64_t>(a.rows) * a.cols;
+  pref_rows_kernel<<<(a.rows + 256) / 256, 256, 0, s>>>(a, pref);
+  pref_cols_kernel<<<(a.cols + 256) / 256, 256, 0, s>>>(a, pref);
+  uint32_t* flag = tmp_scan + cells;  // [scan cells | flags cells]
+  free_flags_kernel<<<sms() * 8, 256, 0, s>>>(a.blocked, cells, flag);
+  size_t tb = 0;
+  cudaError_t e = cub::DeviceScan::ExclusiveSum(nullptr, tb, flag, tmp_scan, cells, s);
+  if (e != cudaSuccess) return e;
+  void* t = nullptr;
+  e = cudaMallocAsync(&t, tb, s);
+  if (e != cudaSuccess) return e;
+  e = cub::DeviceScan::ExclusiveSum(t, tb, flag, tmp_scan, cells, s);
+  cudaFreeAsync(t, s);
+  if (e != cudaSuccess) return e;
+  uint32_t last_scan = 0, last_flag = 0;
+  cudaMemcpyAsync(&last_scan, tmp_scan + cells - 1, 4, cudaMemcpyDeviceToHost, s);
+  cudaMemcpyAsync(&last_flag, flag + cells - 1, 4, cudaMemcpyDeviceToHost, s);
+  e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return e;
+  *n_out = static_cast<uint64_t>(last_scan) + last_flag;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_vis_maps(const VisArgs& a, const uint32_t* scan, uint32_t* node_of_cell, uint32_t* cell_of_node,
+                            cudaStream_t s) {
+  const uint64_t cells = static_cast<uint64_t>(a.rows) * a.cols;
+  node_maps_kernel<<<sms() * 8, 256, 0, s>>>(a.blocked, cells, scan, node_of_cell, cell_of_node);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_vis_rows(const VisArgs& a, bool write, cudaStream_t s) {
+  if (write)
+    vis_rows_kernel<true><<<sms() * 8, 256, 0, s>>>(a);
+  else
+    vis_rows_kernel<false><<<sms() * 8, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scan_u64(const uint64_t* in, uint64_t* out, uint64_t count, cudaStream_t s) {
+  size_t tb = 0;
+  cudaError_t e = cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, count, s);
+  if (e != cudaSuccess) return e;
+  void* t = nullptr;
+  e = cudaMallocAsync(&t, tb, s);
+  if (e != cudaSuccess) return e;
+  e = cub::DeviceScan::ExclusiveSum(t, tb, in, out, count, s);
+  cudaFreeAsync(t, s);
+  return e;
+}
+
+// comp / sizes must hold n entries; returns the component count.
+cudaError_t launch_vis_components(const VisArgs& a, uint32_t* comp, uint32_t* sizes, uint32_t* tmp2n,
+                                  uint64_t* n_comp, cudaStream_t s) {
+  const int g = sms() * 8;
+  cc_init_kernel<<<g, 256, 0, s>>>(a.parent, a.n);
+  cc_hook_kernel<<<g, 256, 0, s>>>(a);
+  uint32_t* is_root = tmp2n;
+  uint32_t* rank = tmp2n + a.n;
+  cc_flatten_kernel<<<g, 256, 0, s>>>(a.parent, a.n, is_root);
+  size_t tb = 0;
+  cudaError_t e = cub::DeviceScan::ExclusiveSum(nullptr, tb, is_root, rank, a.n, s);
+  if (e != cudaSuccess) return e;
+  void* t = nullptr;
+  e = cudaMallocAsync(&t, tb, s);
+  if (e != cudaSuccess) return e;
+  e = cub::DeviceScan::ExclusiveSum(t, tb, is_root, rank, a.n, s);
+  cudaFreeAsync(t, s);
+  if (e != cudaSuccess) return e;
+  cudaMemsetAsync(sizes, 0, a.n * 4, s);
+  cc_label_kernel<<<g, 256, 0, s>>>(a.parent, rank, a.n, comp, sizes);
+  uint32_t lr = 0, lf = 0;
+  cudaMemcpyAsync(&lr, rank + a.n - 1, 4, cudaMemcpyDeviceToHost, s);
+  cudaMemcpyAsync(&lf, is_root + a.n - 1, 4, cudaMemcpyDeviceToHost, s);
+  e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return e;
+  *n_comp = static_cast<uint64_t>(lr) + lf;
+  return cudaGetLastError();
+}
+
+}  // namespace sb
