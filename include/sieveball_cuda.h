@@ -22,6 +22,7 @@
  *   metrics::local_metrics               sb_local_metrics
  *   oracle exact BFS / neighbourhood function sb_exact_* (bit-parallel, on device)
  *   cli cmd_analyze CSV                      sb_metrics_write_csv
+ *   cmd_build_graph grid/visibility/CSR  sb_graph_build_grid (on device), sb_grid_synth_mask
  *   parallel_ranges (parallel.hpp:20-47)                   sb_partition_edges + sb_comm
  *
  * Conventions: every function returns SB_OK (0) or an error code; the message
@@ -93,6 +94,9 @@ typedef struct {
 int sb_csr_synth_grid(uint32_t rows, uint32_t cols, uint32_t n_rects, uint32_t rect_min,
                       uint32_t rect_max, uint64_t seed, uint64_t radius2, unsigned threads,
                       sb_csr** out);
+/* The obstacle mask sb_csr_synth_grid draws (rows * cols bytes, 1 = blocked). */
+int sb_grid_synth_mask(uint32_t rows, uint32_t cols, uint32_t n_rects, uint32_t rect_min, uint32_t rect_max,
+                       uint64_t seed, uint8_t* blocked);
 /* Builds from an uncompressed sorted adjacency (adj_offsets[n+1], adj_ids);
  * rows must be strictly increasing ("non-increasing input -> error"). */
 int sb_csr_from_adjacency(uint64_t n, const uint64_t* adj_offsets, const uint32_t* adj_ids,
@@ -125,6 +129,20 @@ int sb_partition_edges(uint64_t n, const uint64_t* offsets, const uint32_t* degr
 int sb_graph_create(uint64_t n, const uint64_t* offsets, const uint32_t* degrees,
                     const uint8_t* stream, uint64_t stream_len, const uint32_t* orig_id,
                     uint64_t node_begin, uint64_t node_end, int device, sb_graph** out);
+/* On-device graph construction (cmd_build_graph's grid -> visibility -> CSR
+ * phases, SPEC.md:100-219 / PAPER.md:222-307, run in HBM): rows x cols grid,
+ * blocked[r * cols + c] = 1 for obstacle cells, visibility radius^2 in cells^2
+ * (0 = unlimited).  Produces the full graph on `device` -- stream, offsets,
+ * degrees, UnionFind components and cell map -- byte-identical to
+ * sb_csr_synth_grid on the same mask (same exact integer line of sight).
+ * Errors: SB_EINVAL (bad sizes), SB_ERUNTIME (no free cell). */
+int sb_graph_build_grid(uint32_t rows, uint32_t cols, const uint8_t* blocked, uint64_t radius2, int device,
+                        sb_graph** out);
+/* Grid metadata of a device-built graph (NULL outputs skipped). */
+int sb_graph_grid_info(const sb_graph* g, uint32_t* rows, uint32_t* cols, uint32_t* cell_of_node,
+                       uint32_t* component_id, uint32_t* component_sizes, uint64_t* n_components);
+/* Copies the device CSR slice back: offsets (n_local + 1, slice-relative), degrees, stream bytes. */
+int sb_graph_download(const sb_graph* g, uint64_t* offsets, uint32_t* degrees, uint8_t* stream);
 int sb_graph_stats(const sb_graph* g, uint64_t* n_local, uint64_t* edges_local,
                    uint64_t* stream_bytes_local, uint64_t* n_items, uint32_t* chunk);
 void sb_graph_destroy(sb_graph* g);

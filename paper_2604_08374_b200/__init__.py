@@ -5,7 +5,7 @@ runner, VGA metrics).  Host API mirrors SPEC.md's hyperball / cgraph / hll /
 metrics modules; compute runs in libsieveball_cuda.so (sm_100a).
 """
 from ._lib import CudaError, NcclError, lib  # noqa: F401
-from .cgraph import CompressedCsr, encode_neighbor_row, leb128_decode, leb128_encode  # noqa: F401
+from .cgraph import CompressedCsr, encode_neighbor_row, grid_mask, leb128_decode, leb128_encode  # noqa: F401
 from .hyperball import (Comm, DeviceGraph, HllParams, HyperBall, HyperBallState,  # noqa: F401
                         check_convergence, run)
 from . import metrics  # noqa: F401
@@ -17,4 +17,4 @@ __all__ = ["CompressedCsr", "DeviceGraph", "HllParams", "HyperBall", "HyperBallS
            "check_convergence", "run", "metrics", "leb128_encode", "leb128_decode",
            "encode_neighbor_row", "lib", "ExactBfs",
            "exact_bfs_all", "depth_entropy", "neighbourhood_function", "analyze", "metrics_from_sums", "write_csv",
-           "validate"]
+           "validate", "grid_mask"]

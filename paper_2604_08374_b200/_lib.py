@@ -81,6 +81,10 @@ _SIGS = {
     "sb_graph_create": (_i, [_u64, _vp, _vp, _vp, _u64, _vp, _u64, _u64, _i, _pp]),
     "sb_graph_stats": (_i, [_vp, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u32)]),
     "sb_graph_destroy": (None, [_vp]),
+    "sb_graph_build_grid": (_i, [_u32, _u32, _vp, _u64, _i, _pp]),
+    "sb_graph_grid_info": (_i, [_vp, C.POINTER(_u32), C.POINTER(_u32), _vp, _vp, _vp, C.POINTER(_u64)]),
+    "sb_graph_download": (_i, [_vp, _vp, _vp, _vp]),
+    "sb_grid_synth_mask": (_i, [_u32, _u32, _u32, _u32, _u32, _u64, _vp]),
     "sb_hb_create": (_i, [_vp, C.c_uint, _u32, _u32, _pp]),
     "sb_hb_step": (_i, [_vp, C.POINTER(C.c_double), C.POINTER(_i), C.POINTER(_i)]),
     "sb_hb_run": (_i, [_vp, C.POINTER(_u32), C.POINTER(_i)]),

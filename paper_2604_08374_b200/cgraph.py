@@ -61,6 +61,14 @@ def _view(p, n, dtype):
     return np.ctypeslib.as_array(p, shape=(int(n),)).view(dtype)
 
 
+def grid_mask(rows: int, cols: int, n_rects: int = 0, rect_min: int = 1, rect_max: int = 1,
+              seed: int = 20261017) -> np.ndarray:
+    """The (rows, cols) obstacle mask CompressedCsr.synth_grid draws (1 = blocked cell)."""
+    m = np.zeros((rows, cols), np.uint8)
+    check(lib().sb_grid_synth_mask(rows, cols, n_rects, rect_min, rect_max, seed, ptr(m)))
+    return m
+
+
 class CompressedCsr:
     """Immutable compressed CSR backed by a native sb_csr handle."""
 

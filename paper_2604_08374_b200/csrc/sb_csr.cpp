@@ -210,6 +210,20 @@ inline uint64_t rng_next(uint64_t& s) {  // splitmix64 stream (golden-gamma incr
   return z ^ (z >> 31);
 }
 
+// Seeded rectangular obstacles (side in [rect_min, rect_max] cells).
+void draw_rects(uint32_t rows, uint32_t cols, uint32_t n_rects, uint32_t rect_min, uint32_t rect_max, uint64_t seed,
+                uint8_t* blocked) {
+  uint64_t s = seed;
+  for (uint32_t i = 0; i < n_rects; ++i) {
+    const uint32_t h = rect_min + static_cast<uint32_t>(rng_next(s) % (rect_max - rect_min + 1));
+    const uint32_t w = rect_min + static_cast<uint32_t>(rng_next(s) % (rect_max - rect_min + 1));
+    const uint32_t r0 = static_cast<uint32_t>(rng_next(s) % rows);
+    const uint32_t c0 = static_cast<uint32_t>(rng_next(s) % cols);
+    for (uint32_t r = r0; r < std::min(rows, r0 + h); ++r)
+      for (uint32_t c = c0; c < std::min(cols, c0 + w); ++c) blocked[static_cast<uint64_t>(r) * cols + c] = 1;
+  }
+}
+
 void compute_components_from_stream(sb_csr* c) {
   UF uf(static_cast<uint32_t>(c->n));
   for (uint64_t v = 0; v < c->n; ++v) {
@@ -228,6 +242,16 @@ void compute_components_from_stream(sb_csr* c) {
 
 extern "C" {
 
+int sb_grid_synth_mask(uint32_t rows, uint32_t cols, uint32_t n_rects, uint32_t rect_min, uint32_t rect_max,
+                       uint64_t seed, uint8_t* blocked) {
+  if (!blocked) return cfail(SB_EINVAL, "NULL mask");
+  if (rows == 0 || cols == 0) return cfail(SB_EINVAL, "grid: rows and cols must be >= 1");
+  if (n_rects && (rect_min == 0 || rect_max < rect_min)) return cfail(SB_EINVAL, "grid: bad rectangle size range");
+  memset(blocked, 0, static_cast<uint64_t>(rows) * cols);
+  draw_rects(rows, cols, n_rects, rect_min, rect_max, seed, blocked);
+  return SB_OK;
+}
+
 int sb_csr_synth_grid(uint32_t rows, uint32_t cols, uint32_t n_rects, uint32_t rect_min,
                       uint32_t rect_max, uint64_t seed, uint64_t radius2, unsigned threads,
                       sb_csr** out) {
@@ -239,15 +263,7 @@ int sb_csr_synth_grid(uint32_t rows, uint32_t cols, uint32_t n_rects, uint32_t r
   G.rows = rows;
   G.cols = cols;
   G.blocked.assign(static_cast<uint64_t>(rows) * cols, 0);
-  uint64_t s = seed;
-  for (uint32_t i = 0; i < n_rects; ++i) {
-    const uint32_t h = rect_min + static_cast<uint32_t>(rng_next(s) % (rect_max - rect_min + 1));
-    const uint32_t w = rect_min + static_cast<uint32_t>(rng_next(s) % (rect_max - rect_min + 1));
-    const uint32_t r0 = static_cast<uint32_t>(rng_next(s) % rows);
-    const uint32_t c0 = static_cast<uint32_t>(rng_next(s) % cols);
-    for (uint32_t r = r0; r < std::min(rows, r0 + h); ++r)
-      for (uint32_t c = c0; c < std::min(cols, c0 + w); ++c) G.blocked[static_cast<uint64_t>(r) * cols + c] = 1;
-  }
+  draw_rects(rows, cols, n_rects, rect_min, rect_max, seed, G.blocked.data());
   const uint64_t W = cols + 1;
   G.pref.assign(static_cast<uint64_t>(rows + 1) * W, 0);
   for (uint32_t r = 0; r < rows; ++r)

@@ -106,12 +106,19 @@ struct sb_graph {
   uint64_t n_tiles = 0;               // CTA tiles: (8-node group, chunk index)
   uint32_t* d_tile_node0 = nullptr;
   uint32_t* d_tile_q = nullptr;
+  // built on the device from a grid (sb_graph_build_grid)
+  uint32_t rows = 0, cols = 0;
+  uint64_t n_comp = 0;
+  uint32_t* d_cell = nullptr;         // cell_of_node
+  uint32_t* d_comp = nullptr;         // component id per node
+  uint32_t* d_comp_sizes = nullptr;   // n_comp sizes
   ~sb_graph() {
     DeviceGuard dg(device);
     dfree(d_stream); dfree(d_rowoff); dfree(d_deg); dfree(d_orig); dfree(d_node_item);
     dfree(d_item_off); dfree(d_item_base); dfree(d_item_count); dfree(d_item_node);
     dfree(d_tile_node0); dfree(d_tile_q);
     dfree(d_run_off); dfree(d_run_s); dfree(d_run_e);
+    dfree(d_cell); dfree(d_comp); dfree(d_comp_sizes);
   }
 };
 
@@ -321,6 +328,129 @@ int sb_graph_create(uint64_t n, const uint64_t* offsets, const uint32_t* degrees
   if (rc) return bail(rc);
 #undef GK
   *out = g;
+  return SB_OK;
+}
+
+// ------------------------------------------------------------------ on-device graph build
+// Grid -> visibility -> delta-LEB128 CSR entirely in HBM (sb_vis.cu), then the
+// same work-item setup and validation as an uploaded graph.
+int sb_graph_build_grid(uint32_t rows, uint32_t cols, const uint8_t* blocked, uint64_t radius2, int device,
+                        sb_graph** out) {
+  if (!out) return fail(SB_EINVAL, "sb_graph_build_grid: out is NULL");
+  *out = nullptr;
+  if (rows == 0 || cols == 0) return fail(SB_EINVAL, "grid: rows and cols must be >= 1");
+  if (!blocked) return fail(SB_EINVAL, "sb_graph_build_grid: NULL mask");
+  const uint64_t cells = static_cast<uint64_t>(rows) * cols;
+  if (cells >= 0xffffffffull) return fail(SB_EINVAL, "grid: more than 2^32 - 1 cells");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(SB_ECUDA, "no CUDA device: the HyperBall path has no CPU fallback");
+  if (device < 0 || device >= ndev) return fail(SB_EINVAL, "bad device %d", device);
+  DeviceGuard dg(device);
+  auto* g = new sb_graph();
+  g->device = device;
+  g->rows = rows;
+  g->cols = cols;
+  uint8_t* d_mask = nullptr;
+  uint32_t *d_pref = nullptr, *d_scan = nullptr, *d_noc = nullptr, *d_tmp = nullptr;
+  uint64_t* d_bytes = nullptr;
+  auto cleanup = [&] { dfree(d_mask); dfree(d_pref); dfree(d_scan); dfree(d_noc); dfree(d_tmp); dfree(d_bytes); };
+  auto bail = [&](int rc) { cleanup(); delete g; return rc; };
+#define BK(x)                                                 \
+  do {                                                        \
+    cudaError_t e_ = (x);                                     \
+    if (e_ != cudaSuccess) return bail(cuda_fail(e_, #x));    \
+  } while (0)
+  cudaStream_t s = 0;
+  BK(cudaMalloc(&d_mask, cells));
+  BK(cudaMemcpy(d_mask, blocked, cells, cudaMemcpyHostToDevice));
+  BK(cudaMalloc(&d_pref, static_cast<uint64_t>(rows + 1) * (cols + 1) * 4));
+  BK(cudaMalloc(&d_scan, 2 * cells * 4));
+  sb::VisArgs a{};
+  a.rows = rows;
+  a.cols = cols;
+  a.radius2 = radius2;
+  a.blocked = d_mask;
+  a.pref = d_pref;
+  uint64_t n = 0;
+  BK(sb::launch_vis_prepare(a, d_pref, d_scan, &n, s));
+  if (n == 0) return bail(fail(SB_ERUNTIME, "grid: zero active cells"));
+  g->n = n;
+  g->v0 = 0;
+  g->v1 = n;
+  g->n_local = n;
+  BK(cudaMalloc(&d_noc, cells * 4));
+  BK(cudaMalloc(&g->d_cell, n * 4));
+  BK(sb::launch_vis_maps(a, d_scan, d_noc, g->d_cell, s));
+  a.node_of_cell = d_noc;
+  a.cell_of_node = g->d_cell;
+  a.n = n;
+  if (radius2) {  // isqrt64 as the host generator
+    uint64_t r = static_cast<uint64_t>(std::sqrt(static_cast<double>(radius2)));
+    while (r * r > radius2) --r;
+    while ((r + 1) * (r + 1) <= radius2) ++r;
+    a.R = static_cast<int64_t>(r);
+  } else {
+    a.R = std::max(rows, cols);
+  }
+  BK(cudaMalloc(&g->d_deg, n * 4));
+  BK(cudaMalloc(&d_bytes, (n + 1) * 8));
+  BK(cudaMemsetAsync(d_bytes + n, 0, 8, s));
+  a.deg = g->d_deg;
+  a.bytes = d_bytes;
+  BK(sb::launch_vis_rows(a, false, s));
+  BK(cudaMalloc(&g->d_rowoff, (n + 1) * 8));
+  BK(sb::launch_scan_u64(d_bytes, g->d_rowoff, n + 1, s));
+  uint64_t total = 0;
+  BK(cudaMemcpy(&total, g->d_rowoff + n, 8, cudaMemcpyDeviceToHost));
+  g->stream_local = total;
+  BK(cudaMalloc(&g->d_stream, total + 256));
+  BK(cudaMemsetAsync(g->d_stream + total, 0, 256, s));
+  a.offsets = g->d_rowoff;
+  a.stream = g->d_stream;
+  BK(sb::launch_vis_rows(a, true, s));
+  // components (the 2n scratch doubles as the union-find parent array + ranks)
+  BK(cudaMalloc(&d_tmp, 3 * n * 4));
+  BK(cudaMalloc(&g->d_comp, n * 4));
+  BK(cudaMalloc(&g->d_comp_sizes, n * 4));
+  a.parent = d_tmp;
+  BK(sb::launch_vis_components(a, g->d_comp, g->d_comp_sizes, d_tmp + n, &g->n_comp, s));
+  std::vector<uint32_t> deg(n);
+  BK(cudaMemcpy(deg.data(), g->d_deg, n * 4, cudaMemcpyDeviceToHost));
+  uint64_t edges = 0;
+  for (uint64_t v = 0; v < n; ++v) edges += deg[v];
+  g->edges_local = edges;
+  cleanup();
+  const int rc = graph_setup(g, deg.data());
+  if (rc) {
+    delete g;
+    return rc;
+  }
+#undef BK
+  *out = g;
+  return SB_OK;
+}
+
+int sb_graph_grid_info(const sb_graph* g, uint32_t* rows, uint32_t* cols, uint32_t* cell_of_node,
+                       uint32_t* component_id, uint32_t* component_sizes, uint64_t* n_components) {
+  if (!g) return fail(SB_EINVAL, "NULL graph");
+  if (!g->d_cell) return fail(SB_EINVAL, "sb_graph_grid_info: graph was not built from a grid");
+  DeviceGuard dg(g->device);
+  if (rows) *rows = g->rows;
+  if (cols) *cols = g->cols;
+  if (n_components) *n_components = g->n_comp;
+  if (cell_of_node) CK(cudaMemcpy(cell_of_node, g->d_cell, g->n * 4, cudaMemcpyDeviceToHost));
+  if (component_id) CK(cudaMemcpy(component_id, g->d_comp, g->n * 4, cudaMemcpyDeviceToHost));
+  if (component_sizes) CK(cudaMemcpy(component_sizes, g->d_comp_sizes, g->n_comp * 4, cudaMemcpyDeviceToHost));
+  return SB_OK;
+}
+
+int sb_graph_download(const sb_graph* g, uint64_t* offsets, uint32_t* degrees, uint8_t* stream) {
+  if (!g) return fail(SB_EINVAL, "NULL graph");
+  DeviceGuard dg(g->device);
+  if (offsets) CK(cudaMemcpy(offsets, g->d_rowoff, (g->n_local + 1) * 8, cudaMemcpyDeviceToHost));
+  if (degrees) CK(cudaMemcpy(degrees, g->d_deg, g->n_local * 4, cudaMemcpyDeviceToHost));
+  if (stream && g->stream_local) CK(cudaMemcpy(stream, g->d_stream, g->stream_local, cudaMemcpyDeviceToHost));
   return SB_OK;
 }
 

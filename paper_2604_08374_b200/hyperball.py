@@ -98,6 +98,48 @@ class DeviceGraph:
         self.n_items, self.chunk = ni.value, ch.value
 
     @classmethod
+    def from_grid(cls, blocked: np.ndarray, radius2: int = 0, device: int = 0) -> "DeviceGraph":
+        """Builds the grid visibility graph ON THE DEVICE (sb_graph_build_grid): blocked is a
+        (rows, cols) mask of obstacle cells; radius2 in cells^2 (0 = unlimited)."""
+        m = np.ascontiguousarray(blocked, np.uint8)
+        if m.ndim != 2:
+            raise ValueError("blocked must be a 2-D (rows, cols) mask")
+        self = cls.__new__(cls)
+        self._h = C.c_void_p()
+        check(lib().sb_graph_build_grid(m.shape[0], m.shape[1], ptr(m), int(radius2), device, C.byref(self._h)))
+        nl, el, sl, ni = C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_uint64()
+        ch = C.c_uint32()
+        check(lib().sb_graph_stats(self._h, C.byref(nl), C.byref(el), C.byref(sl), C.byref(ni), C.byref(ch)))
+        self.n, self.v0, self.v1, self.device = nl.value, 0, nl.value, device
+        self.n_local, self.edges_local, self.stream_bytes_local = nl.value, el.value, sl.value
+        self.n_items, self.chunk = ni.value, ch.value
+        self.edges = el.value
+        return self
+
+    def grid_info(self) -> dict[str, np.ndarray]:
+        """cell_of_node, component_id, component_sizes of a device-built graph."""
+        r, c, nc = C.c_uint32(), C.c_uint32(), C.c_uint64()
+        check(lib().sb_graph_grid_info(self._h, C.byref(r), C.byref(c), None, None, None, C.byref(nc)))
+        cell = np.zeros(self.n, np.uint32)
+        comp = np.zeros(self.n, np.uint32)
+        sizes = np.zeros(max(nc.value, 1), np.uint32)
+        check(lib().sb_graph_grid_info(self._h, None, None, ptr(cell), ptr(comp), ptr(sizes), None))
+        return dict(rows=r.value, cols=c.value, cell_of_node=cell, component_id=comp,
+                    component_sizes=sizes[: nc.value])
+
+    def node_count_of_component(self) -> np.ndarray:
+        gi = self.grid_info()
+        return gi["component_sizes"][gi["component_id"]]
+
+    def download(self) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+        """(offsets, degrees, stream) of the device CSR slice."""
+        off = np.zeros(self.n_local + 1, np.uint64)
+        deg = np.zeros(max(self.n_local, 1), np.uint32)
+        st = np.zeros(max(self.stream_bytes_local, 1), np.uint8)
+        check(lib().sb_graph_download(self._h, ptr(off), ptr(deg), ptr(st)))
+        return off, deg[: self.n_local], st[: self.stream_bytes_local]
+
+    @classmethod
     def from_raw(cls, n, offsets, degrees, stream, device=0, node_range=None):
         """Upload raw arrays (used to exercise the upload-time stream validation)."""
         self = cls.__new__(cls)
