@@ -243,18 +243,20 @@ __global__ void cc_hook_kernel(VisArgs a) {
   }
 }
 
-__global__ void cc_flatten_kernel(uint32_t* parent, uint64_t n, uint32_t* is_root) {
+// root[v] goes to a separate array: a concurrent path-halving write may still
+// move parent[v] to a non-root ancestor after v's own find returned.
+__global__ void cc_flatten_kernel(uint32_t* parent, uint64_t n, uint32_t* root, uint32_t* is_root) {
   for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += gridDim.x * (uint64_t)blockDim.x) {
     const uint32_t r = uf_find(parent, static_cast<uint32_t>(v));
-    parent[v] = r;
+    root[v] = r;
     is_root[v] = r == v ? 1u : 0u;
   }
 }
 
-__global__ void cc_label_kernel(const uint32_t* parent, const uint32_t* root_rank, uint64_t n, uint32_t* comp,
-                                uint32_t* sizes) {
+// comp[v] holds v's root on entry, its dense component id on exit.
+__global__ void cc_label_kernel(const uint32_t* root_rank, uint64_t n, uint32_t* comp, uint32_t* sizes) {
   for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += gridDim.x * (uint64_t)blockDim.x) {
-    const uint32_t c = root_rank[parent[v]];
+    const uint32_t c = root_rank[comp[v]];
     comp[v] = c;
     atomicAdd(sizes + c, 1u);
   }
@@ -326,7 +328,7 @@ cudaError_t launch_vis_components(const VisArgs& a, uint32_t* comp, uint32_t* si
   cc_hook_kernel<<<g, 256, 0, s>>>(a);
   uint32_t* is_root = tmp2n;
   uint32_t* rank = tmp2n + a.n;
-  cc_flatten_kernel<<<g, 256, 0, s>>>(a.parent, a.n, is_root);
+  cc_flatten_kernel<<<g, 256, 0, s>>>(a.parent, a.n, comp, is_root);
   size_t tb = 0;
   cudaError_t e = cub::DeviceScan::ExclusiveSum(nullptr, tb, is_root, rank, a.n, s);
   if (e != cudaSuccess) return e;
@@ -337,7 +339,7 @@ cudaError_t launch_vis_components(const VisArgs& a, uint32_t* comp, uint32_t* si
   cudaFreeAsync(t, s);
   if (e != cudaSuccess) return e;
   cudaMemsetAsync(sizes, 0, a.n * 4, s);
-  cc_label_kernel<<<g, 256, 0, s>>>(a.parent, rank, a.n, comp, sizes);
+  cc_label_kernel<<<g, 256, 0, s>>>(rank, a.n, comp, sizes);
   uint32_t lr = 0, lf = 0;
   cudaMemcpyAsync(&lr, rank + a.n - 1, 4, cudaMemcpyDeviceToHost, s);
   cudaMemcpyAsync(&lf, is_root + a.n - 1, 4, cudaMemcpyDeviceToHost, s);

@@ -139,6 +139,12 @@ class DeviceGraph:
         check(lib().sb_graph_download(self._h, ptr(off), ptr(deg), ptr(st)))
         return off, deg[: self.n_local], st[: self.stream_bytes_local]
 
+    def degrees(self) -> np.ndarray:
+        """Degrees of the local nodes (device copy)."""
+        deg = np.zeros(max(self.n_local, 1), np.uint32)
+        check(lib().sb_graph_download(self._h, None, ptr(deg), None))
+        return deg[: self.n_local]
+
     @classmethod
     def from_raw(cls, n, offsets, degrees, stream, device=0, node_range=None):
         """Upload raw arrays (used to exercise the upload-time stream validation)."""

@@ -47,6 +47,16 @@ def test_gpu_build_is_byte_identical(case):
 
 
 @pytest.mark.gpu
+def test_gpu_build_large_components():
+    """Union-find at scale (the flatten/label race shows up only on big graphs)."""
+    for rows, cols, k, a, b, seed, r2 in ((300, 300, 0, 1, 1, 1, 20 * 20), (300, 300, 400, 1, 6, 4, 12 * 12)):
+        ref = CompressedCsr.synth_grid(rows, cols, k, a, b, seed, r2)
+        gi = DeviceGraph.from_grid(grid_mask(rows, cols, k, a, b, seed), r2).grid_info()
+        assert np.array_equal(gi["component_id"], ref.component_id)
+        assert np.array_equal(gi["component_sizes"], ref.component_sizes)
+
+
+@pytest.mark.gpu
 def test_gpu_build_errors():
     with pytest.raises(RuntimeError):
         DeviceGraph.from_grid(np.ones((4, 4), np.uint8))
