@@ -223,3 +223,27 @@ def test_gpu_analyze_modes_and_csv(tmp_path):
     rows = list(csv.DictReader(open(tmp_path / "ex.csv")))
     assert len(rows) == g.n and tuple(rows[0].keys()) == COLUMNS
     assert a2["iterations"] == a["iterations"] and a["iterations"] >= 1
+
+
+@pytest.mark.gpu
+def test_gpu_cpp_tool_analyze_matches_python(tmp_path):
+    """tools/sb_hyperball analyze (C++ facade: device-built graph -> HyperBall -> local
+    metrics -> CSV) writes the same bytes as the Python analyze() on the host-built graph."""
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out_cpp, out_py = tmp_path / "cpp.csv", tmp_path / "py.csv"
+    args = ["40", "40", "12", "2", "6", "3", "0", "10", "0"]
+    r = subprocess.run([os.path.join(root, "tools", "sb_hyperball"), "analyze", *args, "hyperball", str(out_cpp)],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    g = CompressedCsr.synth_grid(40, 40, 12, 2, 6, 3, 0)
+    analyze(g, 10, None, "hyperball", out=str(out_py))
+    assert out_cpp.read_bytes() == out_py.read_bytes()
+    r = subprocess.run([os.path.join(root, "tools", "sb_hyperball"), "analyze", *args, "exact", str(out_cpp),
+                        "--interval"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    ex = list(csv.DictReader(open(out_cpp)))
+    ref = oracle.port().exact_bfs(g)
+    md = [float(row["visual_mean_depth"]) for row in ex]
+    nv = g.node_count_of_component()
+    np.testing.assert_array_equal(np.array(md), np.where(nv >= 2, ref["sum_d"] / np.maximum(nv - 1.0, 1.0), np.nan))
