@@ -151,17 +151,16 @@ struct LocalArgs {
   const uint32_t* run_e;
   uint32_t* span_lo;           // N: first neighbour id (0xffffffff if none)
   uint32_t* span_hi;           // N: last neighbour id
-  uint32_t* lo2;               // [v1 - v0]: 2-hop window
-  uint32_t* hi2;
-  unsigned int* max_words;     // [0] max 1-hop window words, [1] max 2-hop window words
+  const uint32_t* reach2;      // N: |B(v, 2)| from the exact BFS at depth 2
+  unsigned int* max_words;     // max 1-hop window words
   double* control;             // [v1 - v0]
   double* controllability;
   double* clustering;
   unsigned long long* edges_among;  // optional
   unsigned long long* n2;           // optional
   uint32_t* scratch;           // global bitmaps (non-smem path): grid * stride_words
-  uint64_t stride_words;       // 2 * (w1_words + 1) + w2_words
-  uint32_t w1_words, w2_words;
+  uint64_t stride_words;       // 2 * (w1_words + 1)
+  uint32_t w1_words;
   unsigned long long* work;
 };
 

@@ -7,20 +7,24 @@
 // by the HLL approximation" (§3.3) and must bit-equal the oracle
 // (acceptance criterion 9).
 //
-// All three passes read the device-resident run index (runs of consecutive
+// The passes read the device-resident run index (runs of consecutive
 // neighbour ids, built once from the LEB128 stream by run_index_kernel), so
 // the per-edge work is proportional to the number of RUNS of the neighbour's
 // row, not its degree (~175 runs vs ~20k ids per row on C3):
 //   span_kernel   thread per node: first / last neighbour id
-//   hop2_kernel   warp per node: the 2-hop id window [lo2, hi2] and control,
-//                 summed in 128-bit fixed point (2^-96 units) so the result is
-//                 the correctly rounded sum, independent of summation order
-//   local_kernel  CTA per node: bitmap of N(v) over [lo1, hi1] + word prefix
-//                 popcounts; for every w in N(v) and every run of N(w):
-//                 |run & N(v)| by two rank queries (clustering) and a range-OR
-//                 into the 2-hop bitmap over [lo2, hi2] (controllability).
-//                 Bitmaps live in shared memory when the widest window fits,
+//   ctrl_kernel   warp per node: control, summed in 128-bit fixed point
+//                 (2^-96 units) so the result is the correctly rounded sum,
+//                 independent of summation order
+//   local_kernel  CTA per node: bitmap of N(v) over [lo1, hi1] interleaved with
+//                 word prefix popcounts; for every w in N(v) and every run of
+//                 N(w): |run & N(v)| by two rank queries (clustering).  The
+//                 runs of all w in one run [s, e] of N(v) are one contiguous
+//                 range of the run index, strided over by the whole CTA.  The
+//                 bitmap lives in shared memory when the widest window fits,
 //                 else in a per-CTA global scratch (L2-resident).
+// |N2(v)| (controllability) is |B(v, 2)| - 1 from the exact bit-parallel BFS
+// at depth 2 (sb_exact_*, the same fused decode-union kernels with OR), run by
+// the caller; local_kernel only divides.
 #include <cmath>
 
 #include "sb_device.cuh"
@@ -91,23 +95,20 @@ __global__ void __launch_bounds__(256) span_kernel(LocalArgs a) {
   }
 }
 
-// Warp per node of [v0, v1): lo2 / hi2 and control.
-__global__ void __launch_bounds__(256) hop2_kernel(LocalArgs a) {
+// Warp per node of [v0, v1): control and the widest 1-hop id window.
+__global__ void __launch_bounds__(256) ctrl_kernel(LocalArgs a) {
   const int lane = threadIdx.x & 31;
   const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = (gridDim.x * (uint64_t)blockDim.x) >> 5;
   for (uint64_t v = a.v0 + gw; v < a.v1; v += nw) {
     uint64_t r0, r1;
     node_runs(a, v, r0, r1);
-    uint32_t lo = a.span_lo[v], hi = a.span_hi[v];
     U128 acc{0ull, 0ull};
     bool zero_deg = false;
     for (uint64_t r = r0; r < r1; ++r) {
       const uint32_t s = a.run_s[r], e = a.run_e[r];
       for (uint64_t w = s + lane; w <= e; w += 32) {
         const uint32_t dw = a.degrees[w];
-        lo = min(lo, a.span_lo[w]);
-        hi = max(hi, a.span_hi[w]);
         if (dw == 0) {
           zero_deg = true;  // only in an asymmetric graph: 1/0 = +inf
         } else {
@@ -115,57 +116,30 @@ __global__ void __launch_bounds__(256) hop2_kernel(LocalArgs a) {
         }
       }
     }
-#pragma unroll
-    for (int d = 16; d; d >>= 1) {
-      lo = min(lo, __shfl_xor_sync(FULL, lo, d));
-      hi = max(hi, __shfl_xor_sync(FULL, hi, d));
-    }
     acc = warp_sum128(acc);
     zero_deg = __any_sync(FULL, zero_deg);
     if (lane == 0) {
-      const uint64_t i = v - a.v0;
-      a.lo2[i] = lo;
-      a.hi2[i] = hi;
-      a.control[i] = zero_deg ? INFINITY : fixed96_to_double(acc);
-      if (r1 > r0) {
-        atomicMax(a.max_words + 0, (a.span_hi[v] - a.span_lo[v]) / 32 + 1);
-        atomicMax(a.max_words + 1, (hi - lo) / 32 + 1);
-      }
+      a.control[v - a.v0] = zero_deg ? INFINITY : fixed96_to_double(acc);
+      if (r1 > r0) atomicMax(a.max_words, (a.span_hi[v] - a.span_lo[v]) / 32 + 1);
     }
   }
 }
 
-// Sets bits [s, e] (relative to the window) of bm.  Interior words are plain
-// all-ones stores (any concurrent OR of a subset leaves them all-ones).
-__device__ __forceinline__ void range_set(uint32_t* bm, uint32_t s, uint32_t e) {
-  const uint32_t ws = s >> 5, we = e >> 5;
-  const uint32_t ms = 0xffffffffu << (s & 31), me = 0xffffffffu >> (31 - (e & 31));
-  if (ws == we) {
-    atomicOr(bm + ws, ms & me);
-  } else {
-    atomicOr(bm + ws, ms);
-    for (uint32_t w = ws + 1; w < we; ++w) bm[w] = 0xffffffffu;
-    atomicOr(bm + we, me);
-  }
-}
-
-// # set bits of bm at relative positions < i.
-__device__ __forceinline__ uint32_t rank1(const uint32_t* bm, const uint32_t* pre, uint32_t i) {
-  return pre[i >> 5] + __popc(bm[i >> 5] & ((1u << (i & 31)) - 1u));
+// rk[k] = {# set bits in words < k, word k} of the N(v) bitmap: one 8-byte
+// shared load per rank query.  rank(i) = # set bits at relative positions < i.
+__device__ __forceinline__ uint32_t rank1(const uint2* rk, uint32_t i) {
+  const uint2 x = rk[i >> 5];
+  return x.x + __popc(x.y & ((1u << (i & 31)) - 1u));
 }
 
 template <bool SMEM>
 __global__ void __launch_bounds__(256) local_kernel(LocalArgs a) {
-  extern __shared__ uint32_t dyn_s[];
+  extern __shared__ uint2 dyn_s[];
   __shared__ unsigned long long s_node;
-  __shared__ unsigned long long s_red[2][8];
+  __shared__ unsigned long long s_red[8];
   __shared__ uint32_t s_scan[8];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t w1 = a.w1_words, w2 = a.w2_words;
-  uint32_t* base = SMEM ? dyn_s : a.scratch + blockIdx.x * a.stride_words;
-  uint32_t* bm1 = base;            // w1 + 1 words (last word stays 0)
-  uint32_t* pre1 = base + w1 + 1;  // w1 + 1 words
-  uint32_t* bm2 = base + 2 * (w1 + 1);
+  uint2* rk = SMEM ? dyn_s : reinterpret_cast<uint2*>(a.scratch + blockIdx.x * a.stride_words);  // w1 + 1
   for (;;) {
     if (threadIdx.x == 0) s_node = atomicAdd(a.work, 1ull);
     __syncthreads();
@@ -186,23 +160,28 @@ __global__ void __launch_bounds__(256) local_kernel(LocalArgs a) {
       continue;
     }
     const uint32_t lo1 = a.span_lo[v], hi1 = a.span_hi[v];
-    const uint32_t lo2 = a.lo2[i], hi2 = a.hi2[i];
-    const uint32_t n1w = (hi1 - lo1) / 32 + 1, n2w = (hi2 - lo2) / 32 + 1;
-    for (uint32_t k = threadIdx.x; k <= n1w; k += blockDim.x) bm1[k] = 0u;
-    for (uint32_t k = threadIdx.x; k < n2w; k += blockDim.x) bm2[k] = 0u;
+    const uint32_t n1w = (hi1 - lo1) / 32 + 1;
+    for (uint32_t k = threadIdx.x; k <= n1w; k += blockDim.x) rk[k] = make_uint2(0u, 0u);
     __syncthreads();
-    for (uint64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
-      const uint32_t s = a.run_s[r], e = a.run_e[r];
-      range_set(bm1, s - lo1, e - lo1);
-      range_set(bm2, s - lo2, e - lo2);
+    for (uint64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {  // runs of N(v) are disjoint
+      const uint32_t s = a.run_s[r] - lo1, e = a.run_e[r] - lo1;
+      const uint32_t ws = s >> 5, we = e >> 5;
+      const uint32_t ms = 0xffffffffu << (s & 31), me = 0xffffffffu >> (31 - (e & 31));
+      if (ws == we) {
+        atomicOr(&rk[ws].y, ms & me);
+      } else {
+        atomicOr(&rk[ws].y, ms);
+        for (uint32_t w = ws + 1; w < we; ++w) rk[w].y = 0xffffffffu;  // all-ones is OR-stable
+        atomicOr(&rk[we].y, me);
+      }
     }
     __syncthreads();
-    // exclusive prefix popcount of bm1 words [0, n1w]
+    // exclusive prefix popcount of the words [0, n1w]
     {
       const uint32_t per = (n1w + 1 + blockDim.x - 1) / blockDim.x;
       const uint32_t k0 = threadIdx.x * per, k1 = min(k0 + per, n1w + 1);
       uint32_t sum = 0;
-      for (uint32_t k = k0; k < k1; ++k) sum += __popc(bm1[k]);
+      for (uint32_t k = k0; k < k1; ++k) sum += __popc(rk[k].y);
       uint32_t incl = sum;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
@@ -215,54 +194,30 @@ __global__ void __launch_bounds__(256) local_kernel(LocalArgs a) {
       for (int q = 0; q < warp; ++q) off += s_scan[q];
       uint32_t run = off + incl - sum;
       for (uint32_t k = k0; k < k1; ++k) {
-        pre1[k] = run;
-        run += __popc(bm1[k]);
+        rk[k].x = run;
+        run += __popc(rk[k].y);
       }
     }
     __syncthreads();
-    // every w in N(v): warp j takes neighbour indices j, j + 8, ...
+    // For a run [s, e] of N(v) the runs of N(s), ..., N(e) are ONE contiguous
+    // range of the (node-ordered) run index: the whole CTA strides over it.
     unsigned long long among = 0;
-    {
-      uint64_t idx = 0;
-      for (uint64_t r = r0; r < r1; ++r) {
-        const uint32_t s = a.run_s[r], e = a.run_e[r];
-        const uint64_t len = static_cast<uint64_t>(e - s) + 1;
-        // first index >= idx in this run with index % 8 == warp
-        uint64_t k = (static_cast<uint64_t>(warp) + 8 - idx % 8) % 8;
-        for (; k < len; k += 8) {
-          const uint32_t w = s + static_cast<uint32_t>(k);
-          uint64_t q0, q1;
-          node_runs(a, w, q0, q1);
-          for (uint64_t q = q0 + lane; q < q1; q += 32) {
-            const uint32_t ws = a.run_s[q], we = a.run_e[q];
-            const uint32_t cs = max(ws, lo1), ce = min(we, hi1);
-            if (cs <= ce) among += rank1(bm1, pre1, ce - lo1 + 1) - rank1(bm1, pre1, cs - lo1);
-            range_set(bm2, ws - lo2, we - lo2);
-          }
-        }
-        idx += len;
+    for (uint64_t r = r0; r < r1; ++r) {
+      const uint32_t s = a.run_s[r], e = a.run_e[r];
+      const uint64_t q0 = a.run_off[a.node_item[s]], q1 = a.run_off[a.node_item[e + 1]];
+      for (uint64_t q = q0 + threadIdx.x; q < q1; q += blockDim.x) {
+        const uint32_t cs = max(a.run_s[q], lo1), ce = min(a.run_e[q], hi1);
+        if (cs <= ce) among += rank1(rk, ce - lo1 + 1) - rank1(rk, cs - lo1);
       }
     }
-    __syncthreads();
-    unsigned long long reach = 0;
-    for (uint32_t k = threadIdx.x; k < n2w; k += blockDim.x) reach += __popc(bm2[k]);
 #pragma unroll
-    for (int d = 16; d; d >>= 1) {
-      among += __shfl_xor_sync(FULL, among, d);
-      reach += __shfl_xor_sync(FULL, reach, d);
-    }
-    if (lane == 0) {
-      s_red[0][warp] = among;
-      s_red[1][warp] = reach;
-    }
+    for (int d = 16; d; d >>= 1) among += __shfl_xor_sync(FULL, among, d);
+    if (lane == 0) s_red[warp] = among;
     __syncthreads();
     if (threadIdx.x == 0) {
-      unsigned long long tri = 0, n2 = 0;
-      for (int q = 0; q < 8; ++q) {
-        tri += s_red[0][q];
-        n2 += s_red[1][q];
-      }
-      if (v >= lo2 && v <= hi2 && ((bm2[(v - lo2) >> 5] >> ((v - lo2) & 31)) & 1u)) --n2;  // v itself
+      unsigned long long tri = 0;
+      for (int q = 0; q < 8; ++q) tri += s_red[q];
+      const unsigned long long n2 = a.reach2[v] - 1ull;  // |B(v, 2)| minus v itself
       a.controllability[i] = n2 ? __ddiv_rn(static_cast<double>(deg), static_cast<double>(n2)) : NAN;
       a.clustering[i] = deg >= 2 ? __ddiv_rn(static_cast<double>(tri),
                                              __dmul_rn(static_cast<double>(deg), static_cast<double>(deg - 1)))
@@ -283,7 +238,7 @@ static int sm_count() {
 
 cudaError_t launch_local_spans(const LocalArgs& a, cudaStream_t s) {
   span_kernel<<<sm_count() * 4, 256, 0, s>>>(a);
-  if (a.v1 > a.v0) hop2_kernel<<<sm_count() * 8, 256, 0, s>>>(a);
+  if (a.v1 > a.v0) ctrl_kernel<<<sm_count() * 8, 256, 0, s>>>(a);
   return cudaGetLastError();
 }
 

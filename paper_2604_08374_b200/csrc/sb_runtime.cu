@@ -3,6 +3,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <memory>
 #include <chrono>
 #include <cstdlib>
 #include <thread>
@@ -1139,7 +1140,8 @@ int sb_exact_stats(const sb_exact* x, uint64_t* sources_done, uint32_t* max_dept
 void sb_exact_destroy(sb_exact* x) { delete x; }
 
 // ------------------------------------------------------------------ local metrics
-// Exact 1-/2-hop metrics over the device-resident run index.
+// Exact 1-/2-hop metrics over the device-resident run index;
+// |N2(v)| = |B(v, 2)| - 1 from the exact bit-parallel BFS at depth 2.
 int sb_local_metrics(sb_graph* g, uint64_t v0, uint64_t v1, double* control, double* controllability,
                      double* clustering, uint64_t* edges_among, uint64_t* n2) {
   if (!g) return fail(SB_EINVAL, "sb_local_metrics: NULL graph");
@@ -1151,18 +1153,24 @@ int sb_local_metrics(sb_graph* g, uint64_t v0, uint64_t v1, double* control, dou
   if (rc) return rc;
   const uint64_t n = g->n, nl = v1 - v0;
   if (nl == 0) return SB_OK;
-  // [span_lo N | span_hi N | lo2 nl | hi2 nl | max 2] u32, [control | ctrl | clus] f64 nl, [among | n2] u64 nl
-  const uint64_t u32_words = 2 * n + 2 * nl + 2;
+  // |B(v, 2)| for every node: two OR-union iterations per 4096-source block
+  sb_exact* x = nullptr;
+  rc = sb_exact_create(g, 12, 2, SB_HB_INTERVAL, &x);
+  if (rc) return rc;
+  std::unique_ptr<sb_exact, void (*)(sb_exact*)> xg(x, sb_exact_destroy);
+  rc = sb_exact_run(x, 0, n, nullptr);
+  if (rc) return rc;
+  // [span_lo N | span_hi N | max 1] u32, [control | ctrl | clus] f64 nl, [among | n2 | work] u64
+  const uint64_t u32_words = 2 * n + 1;
   const uint64_t bytes = ((u32_words * 4 + 7) & ~7ull) + 5 * nl * 8 + 8;
   uint8_t* blk = nullptr;
   CK(cudaMalloc(&blk, bytes));
+  uint32_t* scratch = nullptr;
   struct Free {
     uint8_t*& p;
     uint32_t*& q;
     ~Free() { if (p) cudaFree(p); if (q) cudaFree(q); }
-  };
-  uint32_t* scratch = nullptr;
-  Free fr{blk, scratch};
+  } fr{blk, scratch};
   sb::LocalArgs a{};
   a.n = n;
   a.v0 = v0;
@@ -1172,12 +1180,11 @@ int sb_local_metrics(sb_graph* g, uint64_t v0, uint64_t v1, double* control, dou
   a.run_off = g->d_run_off;
   a.run_s = g->d_run_s;
   a.run_e = g->d_run_e;
+  a.reach2 = x->d_reach;
   uint32_t* u = reinterpret_cast<uint32_t*>(blk);
   a.span_lo = u;
   a.span_hi = u + n;
-  a.lo2 = u + 2 * n;
-  a.hi2 = u + 2 * n + nl;
-  a.max_words = u + 2 * n + 2 * nl;
+  a.max_words = u + 2 * n;
   double* f = reinterpret_cast<double*>(blk + ((u32_words * 4 + 7) & ~7ull));
   a.control = f;
   a.controllability = f + nl;
@@ -1185,14 +1192,13 @@ int sb_local_metrics(sb_graph* g, uint64_t v0, uint64_t v1, double* control, dou
   a.edges_among = reinterpret_cast<unsigned long long*>(f + 3 * nl);
   a.n2 = a.edges_among + nl;
   a.work = a.n2 + nl;
-  CK(cudaMemsetAsync(a.max_words, 0, 8, 0));
+  CK(cudaMemsetAsync(a.max_words, 0, 4, 0));
   CK(cudaMemsetAsync(a.work, 0, 8, 0));
   CK(sb::launch_local_spans(a, 0));
-  unsigned int mw[2] = {0, 0};
-  CK(cudaMemcpy(mw, a.max_words, 8, cudaMemcpyDeviceToHost));
-  a.w1_words = std::max(mw[0], 1u);
-  a.w2_words = std::max(mw[1], 1u);
-  a.stride_words = 2ull * (a.w1_words + 1) + a.w2_words;
+  unsigned int mw = 0;
+  CK(cudaMemcpy(&mw, a.max_words, 4, cudaMemcpyDeviceToHost));
+  a.w1_words = std::max(mw, 1u);
+  a.stride_words = 2ull * (a.w1_words + 1);
   // SB_LOCAL_GLOBAL=1 forces the global-scratch bitmaps (test hook for wide windows)
   const char* force = getenv("SB_LOCAL_GLOBAL");
   const bool smem = a.stride_words * 4 <= sb::local_smem_limit() && !(force && atoi(force));
