@@ -289,6 +289,10 @@ __device__ __forceinline__ void publish_row(const UnionArgs& a, const uint8_t* c
     a.changed_out[v] = 1;
     for (int r = 0; r < a.npeers; ++r) a.peer_changed[r][v] = 1;
   }
+  // Peer stores are ordered before everything this thread does afterwards --
+  // in particular before the iteration barrier (the 8-byte max all-reduce)
+  // that releases the peers' next iteration.
+  if (a.npeers) __threadfence_system();
 }
 
 // Processes one work unit: item `item` (<= chunk neighbours of one node) for

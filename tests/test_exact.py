@@ -247,3 +247,13 @@ def test_gpu_cpp_tool_analyze_matches_python(tmp_path):
     md = [float(row["visual_mean_depth"]) for row in ex]
     nv = g.node_count_of_component()
     np.testing.assert_array_equal(np.array(md), np.where(nv >= 2, ref["sum_d"] / np.maximum(nv - 1.0, 1.0), np.nan))
+
+
+@pytest.mark.gpu
+def test_gpu_exact_bfs_hilbert_equivariant():
+    g = CompressedCsr.synth_grid(50, 50, 16, 2, 6, 8, 0)
+    h = g.hilbert_reorder()
+    inv = h.hilbert_inverse.astype(np.int64)
+    a, b = exact_bfs_all(g), exact_bfs_all(h, interval=True)
+    for k in ("sum_d", "sum_d2", "reach", "entropy"):
+        assert np.array_equal(b[k], a[k][inv], equal_nan=True), k

@@ -143,3 +143,20 @@ def test_gpu_local_metrics_global_scratch_path():
     env = dict(os.environ, SB_LOCAL_GLOBAL="1")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+@pytest.mark.gpu
+def test_gpu_local_metrics_hilbert_equivariant(tmp_path):
+    """Renumbering (SPEC.md:235-243) permutes the exact local metrics and nothing else;
+    also through a VGACSR03 save/load round trip."""
+    g = CompressedCsr.synth_grid(40, 44, 14, 2, 6, 12, 9 * 9)
+    h = g.hilbert_reorder()
+    path = str(tmp_path / "h.vgacsr")
+    h.save_vgacsr(path)
+    h2 = CompressedCsr.load_vgacsr(path)
+    inv = h.hilbert_inverse.astype(np.int64)
+    ref = DeviceGraph(g).local_metrics()
+    for hh in (h, h2):
+        got = DeviceGraph(hh).local_metrics()
+        for k in ref:
+            assert same(got[k], ref[k][inv]), k
