@@ -241,7 +241,10 @@ typedef struct {
 } sb_iter_stats;
 /* Copies up to `cap` per-iteration records since create/reset; *count = total. */
 int sb_hb_stats(const sb_hb* h, sb_iter_stats* out, uint32_t cap, uint32_t* count);
-/* Re-initialises the state (t = 0, registers from orig_id, sums zeroed). */
+/* Re-initialises the state (t = 0, registers from orig_id, sums zeroed).
+ * Collective with fused P2P peers: with a communicator attached it ends in a
+ * barrier; with an external barrier the caller must synchronise all ranks
+ * after sb_hb_reset and before the next step. */
 int sb_hb_reset(sb_hb* h);
 /* Raw CUDA stream the handle launches on (cudaStream_t as void*). */
 void* sb_hb_stream(const sb_hb* h);

@@ -604,7 +604,16 @@ int sb_hb_create(sb_graph* g, unsigned p, uint32_t depth_limit, uint32_t flags, 
 int sb_hb_reset(sb_hb* h) {
   if (!h) return fail(SB_EINVAL, "NULL handle");
   DeviceGuard dg(h->g->device);
-  return hb_init(h);
+  const int rc = hb_init(h);
+  if (rc) return rc;
+  // With fused P2P, a peer that already started iteration 1 stores rows and
+  // changed flags into this replica: nobody may pass reset until every rank
+  // has re-initialised its planes and flags (NCCL barrier on 8 bytes).
+  if (h->npeers && h->comm && h->comm->nranks > 1) {
+    NK(ncclAllReduce(h->d_misc + 3, h->d_misc + 3, 1, ncclUint64, ncclMax, h->comm->comm, h->stream));
+    CK(sync_stream(h->stream));
+  }
+  return SB_OK;
 }
 
 void* sb_hb_stream(const sb_hb* h) { return h ? static_cast<void*>(h->stream) : nullptr; }

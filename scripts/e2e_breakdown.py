@@ -1,0 +1,28 @@
+"""Phase breakdown of the end-to-end C-ABI path on C3 (host CSR -> HBM -> run -> read-back)."""
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from bench import build_graph  # noqa: E402
+from paper_2604_08374_b200 import DeviceGraph, HllParams, HyperBall  # noqa: E402
+
+g = build_graph("c3")
+g.pin(True)
+P = HllParams(10)
+for rep in range(3):
+    t0 = time.perf_counter()
+    dg = DeviceGraph(g, 0)
+    t1 = time.perf_counter()
+    h = HyperBall(dg, P, None)
+    t2 = time.perf_counter()
+    it = h.run()
+    t3 = time.perf_counter()
+    s = h.state()
+    torch.cuda.synchronize()
+    t4 = time.perf_counter()
+    print(f"rep {rep}: graph_create {t1 - t0:.3f} s, hb_create {t2 - t1:.3f} s, run {t3 - t2:.3f} s ({it} it), "
+          f"read_state {t4 - t3:.3f} s, total {t4 - t0:.3f} s", flush=True)
+    del h, dg, s
