@@ -145,7 +145,7 @@ def binding_from_profile(cfg, p):
     if not e:
         return None
     keys = ("alu_pipe_pct", "l1_throughput_pct", "l1_hit_rate_pct", "l2_hit_rate_pct", "issue_active_pct",
-            "top_stalls_pct_of_samples", "duration_ms")
+            "sectors_per_request", "top_stalls_pct_of_samples", "duration_ms")
     out = {k: e[k] for k in keys if k in e}
     out["source"] = e.get("source")
     return out

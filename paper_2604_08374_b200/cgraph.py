@@ -120,6 +120,15 @@ class CompressedCsr:
         return cls(h.value)
 
     @classmethod
+    def from_sorted_csr(cls, adj_offsets, adj_ids) -> "CompressedCsr":
+        """Uncompressed sorted CSR arrays (adj_offsets[n+1], adj_ids) -> compressed graph."""
+        off = np.ascontiguousarray(adj_offsets, np.uint64)
+        ids = np.ascontiguousarray(adj_ids if len(adj_ids) else np.zeros(1), np.uint32)
+        h = C.c_void_p()
+        check(lib().sb_csr_from_adjacency(off.size - 1, ptr(off), ptr(ids), C.byref(h)))
+        return cls(h.value)
+
+    @classmethod
     def from_arrays(cls, offsets, degrees, stream) -> "CompressedCsr":
         """Wrap raw arrays (copied; components recomputed).  No validation beyond offsets[N]."""
         off = np.ascontiguousarray(offsets, np.uint64)
