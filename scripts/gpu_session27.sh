@@ -1,1 +1,1 @@
-timeout 900 python -u -m pytest tests/test_hll_statistics.py -q -m gpu 2>&1 | tail -3
+timeout 900 python -u -m pytest tests/test_exact.py -q -m gpu -k contract 2>&1 | tail -15

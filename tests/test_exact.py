@@ -257,3 +257,22 @@ def test_gpu_exact_bfs_hilbert_equivariant():
     a, b = exact_bfs_all(g), exact_bfs_all(h, interval=True)
     for k in ("sum_d", "sum_d2", "reach", "entropy"):
         assert np.array_equal(b[k], a[k][inv], equal_nan=True), k
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("D,g", [(4, path_graph(5)), (8, path_graph(9)), (16, path_graph(17)),
+                                 (4, CompressedCsr.synth_grid(3, 3, 0, 1, 1, 1, 1)),
+                                 (8, CompressedCsr.synth_grid(5, 5, 0, 1, 1, 1, 1)),
+                                 (16, CompressedCsr.synth_grid(9, 9, 0, 1, 1, 1, 1))],
+                         ids=["path4", "path8", "path16", "grid4", "grid8", "grid16"])
+def test_gpu_iteration_contract(D, g):
+    """Acceptance criterion 5: a depth-d run executes min(d, D) growth
+    iterations.  Alg. 1 tests convergence after the union, so an
+    unlimited run spends one more pass to observe max increase <= 0.5: t = D + 1; the
+    exact BFS reports the diameter as its deepest level."""
+    assert exact_bfs_all(g)["stats"]["max_depth"] == D
+    for d in (3, 5, 10, None):
+        hb = HyperBall(g, 10, d)
+        it = hb.run()
+        assert it == (min(d, D + 1) if d else D + 1), (d, it)
+        assert hb.state().converged == (d is None or d > D)
