@@ -143,6 +143,18 @@ int sb_graph_grid_info(const sb_graph* g, uint32_t* rows, uint32_t* cols, uint32
                        uint32_t* component_id, uint32_t* component_sizes, uint64_t* n_components);
 /* Copies the device CSR slice back: offsets (n_local + 1, slice-relative), degrees, stream bytes. */
 int sb_graph_download(const sb_graph* g, uint64_t* offsets, uint32_t* degrees, uint8_t* stream);
+/* Same as sb_graph_create, but the stream bytes are copied in ~16 chunks on a
+ * copy stream and validated chunk by chunk on a second stream; the call
+ * returns once the copies are enqueued.  The first sb_hb_step starts each
+ * chunk's tiles as soon as that chunk is validated, so the PCIe upload
+ * overlaps the first iteration.  The host stream buffer must stay valid and
+ * unmodified (pinned for full speed) until sb_graph_wait or the first step
+ * returns; a malformed stream is reported there (SB_ERUNTIME, sticky). */
+int sb_graph_create_async(uint64_t n, const uint64_t* offsets, const uint32_t* degrees,
+                          const uint8_t* stream, uint64_t stream_len, const uint32_t* orig_id,
+                          uint64_t node_begin, uint64_t node_end, int device, sb_graph** out);
+/* Waits for an asynchronous upload and reports its validation result. */
+int sb_graph_wait(sb_graph* g);
 int sb_graph_stats(const sb_graph* g, uint64_t* n_local, uint64_t* edges_local,
                    uint64_t* stream_bytes_local, uint64_t* n_items, uint32_t* chunk);
 void sb_graph_destroy(sb_graph* g);

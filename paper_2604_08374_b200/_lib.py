@@ -81,6 +81,8 @@ _SIGS = {
     "sb_graph_create": (_i, [_u64, _vp, _vp, _vp, _u64, _vp, _u64, _u64, _i, _pp]),
     "sb_graph_stats": (_i, [_vp, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u32)]),
     "sb_graph_destroy": (None, [_vp]),
+    "sb_graph_create_async": (_i, [_u64, _vp, _vp, _vp, _u64, _vp, _u64, _u64, _i, _pp]),
+    "sb_graph_wait": (_i, [_vp]),
     "sb_graph_build_grid": (_i, [_u32, _u32, _vp, _u64, _i, _pp]),
     "sb_graph_grid_info": (_i, [_vp, C.POINTER(_u32), C.POINTER(_u32), _vp, _vp, _vp, C.POINTER(_u64)]),
     "sb_graph_download": (_i, [_vp, _vp, _vp, _vp]),

@@ -11,6 +11,7 @@ struct BuildArgs {
   const uint32_t* degrees;     // local degrees
   uint64_t n_local;
   uint64_t n_global;
+  uint64_t node_begin, node_end;  // local nodes to validate (node_end 0 = n_local)
   uint32_t chunk;              // neighbours per work item
   const uint32_t* node_item;   // local node -> first item (n_local + 1)
   uint64_t* item_off;

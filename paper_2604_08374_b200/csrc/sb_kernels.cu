@@ -24,7 +24,8 @@ __global__ void __launch_bounds__(256) build_items_kernel(BuildArgs a) {
   const int lane = threadIdx.x & 31;
   const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = (gridDim.x * (uint64_t)blockDim.x) >> 5;
-  for (uint64_t node = gw; node < a.n_local; node += nw) {
+  const uint64_t node_end = a.node_end ? a.node_end : a.n_local;
+  for (uint64_t node = a.node_begin + gw; node < node_end; node += nw) {
     uint64_t pos = a.row_off[node];
     const uint64_t end = a.row_off[node + 1];
     const uint32_t deg = a.degrees[node];

@@ -113,6 +113,15 @@ struct sb_graph {
   uint32_t* d_cell = nullptr;         // cell_of_node
   uint32_t* d_comp = nullptr;         // component id per node
   uint32_t* d_comp_sizes = nullptr;   // n_comp sizes
+  // asynchronous chunked upload (sb_graph_create_async): chunk k's stream
+  // bytes are copied on up_stream and validated on val_stream; val_ev[k]
+  // fires when chunk k (nodes [chunk_node[k], chunk_node[k+1])) is usable.
+  bool pending = false;
+  int broken = 0;                     // validation failed (sticky SB_ERUNTIME)
+  unsigned long long* d_err = nullptr;  // [0] min bad node, [1] max run
+  cudaStream_t up_stream = nullptr, val_stream = nullptr;
+  std::vector<cudaEvent_t> val_ev;
+  std::vector<uint64_t> chunk_node, chunk_tile;
   ~sb_graph() {
     DeviceGuard dg(device);
     dfree(d_stream); dfree(d_rowoff); dfree(d_deg); dfree(d_orig); dfree(d_node_item);
@@ -120,6 +129,12 @@ struct sb_graph {
     dfree(d_tile_node0); dfree(d_tile_q);
     dfree(d_run_off); dfree(d_run_s); dfree(d_run_e);
     dfree(d_cell); dfree(d_comp); dfree(d_comp_sizes);
+    if (up_stream) cudaStreamSynchronize(up_stream);
+    if (val_stream) cudaStreamSynchronize(val_stream);
+    for (auto e : val_ev) cudaEventDestroy(e);
+    if (up_stream) cudaStreamDestroy(up_stream);
+    if (val_stream) cudaStreamDestroy(val_stream);
+    dfree(d_err);
   }
 };
 
@@ -200,7 +215,7 @@ int sb_check_convergence(double max_increase) { return max_increase <= 0.5 ? 1 :
 // ------------------------------------------------------------------ graph
 // Work items, CTA tiles and the upload-time validation of the device-resident
 // stream slice (shared by sb_graph_create and the on-device grid builder).
-static int graph_setup(sb_graph* g, const uint32_t* deg_local) {
+static int graph_setup_host(sb_graph* g, const uint32_t* deg_local) {
   // Work items: <= chunk neighbours each, sized so the edge work splits into
   // ~4 items per resident warp (load balance) but stays >= 512 ids (decode
   // and merge amortisation).
@@ -243,42 +258,73 @@ static int graph_setup(sb_graph* g, const uint32_t* deg_local) {
   CK(cudaMalloc(&g->d_item_base, ni * 4));
   CK(cudaMalloc(&g->d_item_count, ni * 4));
   CK(cudaMalloc(&g->d_item_node, ni * 4));
-  unsigned long long* d_err = nullptr;
-  CK(cudaMalloc(&d_err, 16));
-  CK(cudaMemset(d_err, 0xff, 8));
-  CK(cudaMemset(reinterpret_cast<uint8_t*>(d_err) + 8, 0, 8));
-  if (g->n_local) {
-    sb::BuildArgs a{};
-    a.stream = g->d_stream;
-    a.row_off = g->d_rowoff;
-    a.degrees = g->d_deg;
-    a.n_local = g->n_local;
-    a.n_global = g->n;
-    a.chunk = g->chunk;
-    a.node_item = g->d_node_item;
-    a.item_off = g->d_item_off;
-    a.item_base = g->d_item_base;
-    a.item_count = g->d_item_count;
-    a.item_node = g->d_item_node;
-    a.err_node = d_err;
-    a.max_run = reinterpret_cast<unsigned int*>(d_err + 1);
-    CK(sb::launch_build_items(a, 0));
-  }
-  CK(sync_stream(0));
-  unsigned long long err = 0;
-  CK(cudaMemcpy(&err, d_err, 8, cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(&g->max_run, d_err + 1, 4, cudaMemcpyDeviceToHost));
-  cudaFree(d_err);
-  if (err != ~0ull)
-    return fail(SB_ERUNTIME, "cgraph: malformed compressed row at node %llu (bad varint, "
-                             "non-increasing or out-of-range id, or degree mismatch)",
-                (unsigned long long)(err + g->v0));
+  CK(cudaMalloc(&g->d_err, 16));
+  CK(cudaMemset(g->d_err, 0xff, 8));
+  CK(cudaMemset(reinterpret_cast<uint8_t*>(g->d_err) + 8, 0, 8));
   return SB_OK;
 }
 
-int sb_graph_create(uint64_t n, const uint64_t* offsets, const uint32_t* degrees,
-                    const uint8_t* stream, uint64_t stream_len, const uint32_t* orig_id,
-                    uint64_t node_begin, uint64_t node_end, int device, sb_graph** out) {
+// Upload-time validation of local nodes [n0, n1) (LEB128 well-formed, strictly
+// increasing ids < n, exactly degrees[v] ids) + work items; errors land in d_err.
+static cudaError_t launch_validate(sb_graph* g, uint64_t n0, uint64_t n1, cudaStream_t s) {
+  if (n1 <= n0) return cudaSuccess;
+  sb::BuildArgs a{};
+  a.stream = g->d_stream;
+  a.row_off = g->d_rowoff;
+  a.degrees = g->d_deg;
+  a.n_local = g->n_local;
+  a.n_global = g->n;
+  a.node_begin = n0;
+  a.node_end = n1;
+  a.chunk = g->chunk;
+  a.node_item = g->d_node_item;
+  a.item_off = g->d_item_off;
+  a.item_base = g->d_item_base;
+  a.item_count = g->d_item_count;
+  a.item_node = g->d_item_node;
+  a.err_node = g->d_err;
+  a.max_run = reinterpret_cast<unsigned int*>(g->d_err + 1);
+  return sb::launch_build_items(a, s);
+}
+
+static int graph_check(sb_graph* g) {
+  unsigned long long err = 0;
+  CK(cudaMemcpy(&err, g->d_err, 8, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(&g->max_run, g->d_err + 1, 4, cudaMemcpyDeviceToHost));
+  if (err != ~0ull) {
+    g->broken = 1;
+    return fail(SB_ERUNTIME, "cgraph: malformed compressed row at node %llu (bad varint, "
+                             "non-increasing or out-of-range id, or degree mismatch)",
+                (unsigned long long)(err + g->v0));
+  }
+  return SB_OK;
+}
+
+// Work items, CTA tiles and the upload-time validation of the device-resident
+// stream slice (shared by sb_graph_create and the on-device grid builder).
+static int graph_setup(sb_graph* g, const uint32_t* deg_local) {
+  int rc = graph_setup_host(g, deg_local);
+  if (rc) return rc;
+  CK(launch_validate(g, 0, g->n_local, 0));
+  CK(sync_stream(0));
+  return graph_check(g);
+}
+
+// Completes an asynchronous upload (sb_graph_create_async): waits for every
+// chunk's copy + validation and reports a malformed stream (sticky).
+static int graph_wait(sb_graph* g) {
+  if (g->broken) return fail(SB_ERUNTIME, "cgraph: the graph failed validation at upload");
+  if (!g->pending) return SB_OK;
+  DeviceGuard dg(g->device);
+  CK(sync_stream(g->up_stream));
+  CK(sync_stream(g->val_stream));
+  g->pending = false;
+  return graph_check(g);
+}
+
+static int graph_create(uint64_t n, const uint64_t* offsets, const uint32_t* degrees, const uint8_t* stream,
+                        uint64_t stream_len, const uint32_t* orig_id, uint64_t node_begin, uint64_t node_end,
+                        int device, bool async, sb_graph** out) {
   if (!out) return fail(SB_EINVAL, "sb_graph_create: out is NULL");
   *out = nullptr;
   if (n == 0) return fail(SB_EINVAL, "hyperball: graph empty");
@@ -314,7 +360,8 @@ int sb_graph_create(uint64_t n, const uint64_t* offsets, const uint32_t* degrees
   // 256 B of zero padding: the decoder reads whole 128-byte windows (+8 for alignment).
   GK(cudaMalloc(&g->d_stream, g->stream_local + 256));
   GK(cudaMemset(g->d_stream + g->stream_local, 0, 256));
-  if (g->stream_local) GK(cudaMemcpy(g->d_stream, stream + b0, g->stream_local, cudaMemcpyHostToDevice));
+  if (g->stream_local && !async)
+    GK(cudaMemcpy(g->d_stream, stream + b0, g->stream_local, cudaMemcpyHostToDevice));
   std::vector<uint64_t> ro(g->n_local + 1);
   for (uint64_t i = 0; i <= g->n_local; ++i) ro[i] = offsets[node_begin + i] - b0;
   GK(cudaMalloc(&g->d_rowoff, ro.size() * 8));
@@ -325,11 +372,69 @@ int sb_graph_create(uint64_t n, const uint64_t* offsets, const uint32_t* degrees
     GK(cudaMalloc(&g->d_orig, n * 4));
     GK(cudaMemcpy(g->d_orig, orig_id, n * 4, cudaMemcpyHostToDevice));
   }
-  const int rc = graph_setup(g, degrees + node_begin);
+  if (!async) {
+    const int rc = graph_setup(g, degrees + node_begin);
+    if (rc) return bail(rc);
+    *out = g;
+    return SB_OK;
+  }
+  // Asynchronous: K chunks of ~equal stream bytes on 8-node (tile group)
+  // boundaries; copy k on up_stream, validation k on val_stream after copy k.
+  const int rc = graph_setup_host(g, degrees + node_begin);
   if (rc) return bail(rc);
+  GK(cudaStreamCreateWithFlags(&g->up_stream, cudaStreamNonBlocking));
+  GK(cudaStreamCreateWithFlags(&g->val_stream, cudaStreamNonBlocking));
+  const int K = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(16, g->n_local / 64)));
+  g->chunk_node.assign(1, 0);
+  for (int k = 1; k < K; ++k) {
+    const uint64_t goal = b0 + g->stream_local * k / K;
+    uint64_t v = std::lower_bound(offsets + node_begin, offsets + node_end, goal) - (offsets + node_begin);
+    v = std::min<uint64_t>(v & ~7ull, g->n_local);
+    if (v > g->chunk_node.back()) g->chunk_node.push_back(v);
+  }
+  if (g->chunk_node.back() != g->n_local) g->chunk_node.push_back(g->n_local);
+  // tile ranges: tiles are ordered by 8-node group
+  std::vector<uint32_t> tn0(g->n_tiles);
+  if (g->n_tiles) GK(cudaMemcpy(tn0.data(), g->d_tile_node0, g->n_tiles * 4, cudaMemcpyDeviceToHost));
+  g->chunk_tile.clear();
+  for (uint64_t cn : g->chunk_node)
+    g->chunk_tile.push_back(std::lower_bound(tn0.begin(), tn0.end(), static_cast<uint32_t>(std::min<uint64_t>(cn, 0xffffffffull))) - tn0.begin());
+  g->chunk_tile.back() = g->n_tiles;
+  const size_t nk = g->chunk_node.size() - 1;
+  g->val_ev.resize(nk, nullptr);
+  for (size_t k = 0; k < nk; ++k) {
+    cudaEvent_t copied = nullptr;
+    GK(cudaEventCreateWithFlags(&g->val_ev[k], cudaEventDisableTiming));
+    GK(cudaEventCreateWithFlags(&copied, cudaEventDisableTiming));
+    const uint64_t s0 = ro[g->chunk_node[k]], s1 = ro[g->chunk_node[k + 1]];
+    if (s1 > s0) GK(cudaMemcpyAsync(g->d_stream + s0, stream + b0 + s0, s1 - s0, cudaMemcpyHostToDevice, g->up_stream));
+    GK(cudaEventRecord(copied, g->up_stream));
+    GK(cudaStreamWaitEvent(g->val_stream, copied, 0));
+    cudaEventDestroy(copied);  // released once the wait is enqueued
+    GK(launch_validate(g, g->chunk_node[k], g->chunk_node[k + 1], g->val_stream));
+    GK(cudaEventRecord(g->val_ev[k], g->val_stream));
+  }
+  g->pending = true;
 #undef GK
   *out = g;
   return SB_OK;
+}
+
+int sb_graph_create(uint64_t n, const uint64_t* offsets, const uint32_t* degrees, const uint8_t* stream,
+                    uint64_t stream_len, const uint32_t* orig_id, uint64_t node_begin, uint64_t node_end,
+                    int device, sb_graph** out) {
+  return graph_create(n, offsets, degrees, stream, stream_len, orig_id, node_begin, node_end, device, false, out);
+}
+
+int sb_graph_create_async(uint64_t n, const uint64_t* offsets, const uint32_t* degrees, const uint8_t* stream,
+                          uint64_t stream_len, const uint32_t* orig_id, uint64_t node_begin, uint64_t node_end,
+                          int device, sb_graph** out) {
+  return graph_create(n, offsets, degrees, stream, stream_len, orig_id, node_begin, node_end, device, true, out);
+}
+
+int sb_graph_wait(sb_graph* g) {
+  if (!g) return fail(SB_EINVAL, "NULL graph");
+  return graph_wait(g);
 }
 
 // ------------------------------------------------------------------ on-device graph build
@@ -449,6 +554,7 @@ int sb_graph_grid_info(const sb_graph* g, uint32_t* rows, uint32_t* cols, uint32
 int sb_graph_download(const sb_graph* g, uint64_t* offsets, uint32_t* degrees, uint8_t* stream) {
   if (!g) return fail(SB_EINVAL, "NULL graph");
   DeviceGuard dg(g->device);
+  if (const int rc = graph_wait(const_cast<sb_graph*>(g))) return rc;
   if (offsets) CK(cudaMemcpy(offsets, g->d_rowoff, (g->n_local + 1) * 8, cudaMemcpyDeviceToHost));
   if (degrees) CK(cudaMemcpy(degrees, g->d_deg, g->n_local * 4, cudaMemcpyDeviceToHost));
   if (stream && g->stream_local) CK(cudaMemcpy(stream, g->d_stream, g->stream_local, cudaMemcpyDeviceToHost));
@@ -585,6 +691,7 @@ int sb_hb_create(sb_graph* g, unsigned p, uint32_t depth_limit, uint32_t flags, 
   HK(cudaMalloc(&h->d_counter, nl * h->slices * 4));
   HK(cudaMalloc(&h->d_misc, 4 * 8));
   if (flags & SB_HB_INTERVAL) {
+    if (const int rc = graph_wait(g)) return bail(rc);  // max_run comes from the validation pass
     // levels K = floor(log2(longest run)), capped at 10 (longer runs peel 2^K blocks)
     int K = 0;
     while (K < 10 && (2u << K) <= g->max_run) ++K;
@@ -624,6 +731,11 @@ int sb_hb_step_compute(sb_hb* h, double* local_max) {
   if (h->computed) return fail(SB_EINVAL, "hyperball: step_compute called twice without finish");
   sb_graph* g = h->g;
   DeviceGuard dg(g->device);
+  if (g->broken) return fail(SB_ERUNTIME, "cgraph: the graph failed validation at upload");
+  if (g->pending && (h->flags & SB_HB_SCHEDULE_WARP)) {  // the chunk pipeline needs the tile schedule
+    const int rc = graph_wait(g);
+    if (rc) return rc;
+  }
   h->t += 1;
   const int L = h->latest, N = 1 - L;
   const bool skip = (h->flags & SB_HB_SKIP_UNCHANGED) != 0;
@@ -669,6 +781,20 @@ int sb_hb_step_compute(sb_hb* h, double* local_max) {
       ia.run_s = g->d_run_s;
       ia.run_e = g->d_run_e;
       CK(sb::launch_union_interval(static_cast<int>(h->p), ia, h->stream));
+    } else if (g->pending) {
+      // First pass over a graph still streaming in: chunk k's tiles start as
+      // soon as its bytes are copied and validated (overlaps PCIe with compute).
+      for (size_t k = 0; k + 1 < g->chunk_node.size(); ++k) {
+        const uint64_t t0 = g->chunk_tile[k], t1 = g->chunk_tile[k + 1];
+        if (t1 == t0) continue;
+        CK(cudaStreamWaitEvent(h->stream, g->val_ev[k], 0));
+        CK(cudaMemsetAsync(h->d_misc, 0, 8, h->stream));  // work counter
+        sb::UnionArgs uk = u;
+        uk.tile_node0 = g->d_tile_node0 + t0;
+        uk.tile_q = g->d_tile_q + t0;
+        uk.n_tiles = t1 - t0;
+        CK(sb::launch_union(static_cast<int>(h->p), skip, uk, h->stream));
+      }
     } else {
       CK(sb::launch_union(static_cast<int>(h->p), skip, u, h->stream));
     }
@@ -700,6 +826,13 @@ int sb_hb_step_compute(sb_hb* h, double* local_max) {
   CK(cudaEventRecord(h->ev[3], h->stream));
   CK(cudaMemcpyAsync(h->h_misc, h->d_misc, 4 * 8, cudaMemcpyDeviceToHost, h->stream));
   CK(sync_stream(h->stream));
+  if (g->pending) {  // the upload finished inside this step: report a malformed stream now
+    const int rc = graph_wait(g);
+    if (rc) {
+      h->t -= 1;
+      return rc;
+    }
+  }
   float ms = 0.f;
   cudaEventElapsedTime(&ms, h->ev[1], h->ev[2]);
   h->cur_stats.union_ms = ms;
@@ -992,6 +1125,7 @@ int sb_exact_create(sb_graph* g, unsigned log2_block, uint32_t depth_limit, uint
   if (flags & ~(uint32_t)SB_HB_INTERVAL) return fail(SB_EINVAL, "sb_exact_create: only SB_HB_INTERVAL is supported");
   if (g->n == 0) return fail(SB_EINVAL, "sb_exact_create: graph empty");
   DeviceGuard dg(g->device);
+  if (const int rc = graph_wait(g)) return rc;
   auto* x = new sb_exact();
   x->g = g;
   x->P = static_cast<int>(log2_block) - 2;
@@ -1158,7 +1292,9 @@ int sb_local_metrics(sb_graph* g, uint64_t v0, uint64_t v1, double* control, dou
     return fail(SB_EINVAL, "sb_local_metrics: needs the full graph on the device (2-hop rows of any node)");
   if (v0 > v1 || v1 > g->n) return fail(SB_EINVAL, "sb_local_metrics: bad node range");
   DeviceGuard dg(g->device);
-  int rc = build_run_index(g);
+  int rc = graph_wait(g);
+  if (rc) return rc;
+  rc = build_run_index(g);
   if (rc) return rc;
   const uint64_t n = g->n, nl = v1 - v0;
   if (nl == 0) return SB_OK;

@@ -83,13 +83,17 @@ class DeviceGraph:
     """Rows [v0, v1) of a CompressedCsr resident in HBM (validated at upload)."""
 
     def __init__(self, csr: CompressedCsr, device: int = 0, node_range: tuple[int, int] | None = None,
-                 orig_id: np.ndarray | None = None):
+                 orig_id: np.ndarray | None = None, async_upload: bool = False):
+        """async_upload: chunked upload overlapped with the first HyperBall pass
+        (sb_graph_create_async); `csr` must stay alive until wait() / the first step."""
         v0, v1 = node_range if node_range is not None else (0, csr.n)
         oid = orig_id if orig_id is not None else csr.hilbert_inverse
         oid = None if oid is None else np.ascontiguousarray(oid, np.uint32)
         self._h = C.c_void_p()
-        check(lib().sb_graph_create(csr.n, ptr(csr.offsets), ptr(csr.degrees), ptr(csr.stream_padded()),
-                                    csr.stream_len, ptr(oid), v0, v1, device, C.byref(self._h)))
+        self._csr = csr if async_upload else None  # keeps the host stream alive during the upload
+        fn = lib().sb_graph_create_async if async_upload else lib().sb_graph_create
+        check(fn(csr.n, ptr(csr.offsets), ptr(csr.degrees), ptr(csr.stream_padded()), csr.stream_len, ptr(oid),
+                 v0, v1, device, C.byref(self._h)))
         self.n, self.v0, self.v1, self.device = csr.n, v0, v1, device
         nl, el, sl, ni = C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_uint64()
         ch = C.c_uint32()
@@ -159,6 +163,10 @@ class DeviceGraph:
         self.n, self.v0, self.v1, self.device = n, v0, v1, device
         self.n_local = v1 - v0
         return self
+
+    def wait(self) -> None:
+        """Completes an asynchronous upload (raises RuntimeError on a malformed stream)."""
+        check(lib().sb_graph_wait(self._h))
 
     def local_metrics(self, v0: int = 0, v1: int | None = None) -> dict[str, np.ndarray]:
         """Exact control / controllability / clustering for nodes [v0, v1).

@@ -12,9 +12,9 @@ from paper_2604_08374_b200 import DeviceGraph, HllParams, HyperBall  # noqa: E40
 g = build_graph("c3")
 g.pin(True)
 P = HllParams(10)
-for rep in range(3):
+for rep in range(6):
     t0 = time.perf_counter()
-    dg = DeviceGraph(g, 0)
+    dg = DeviceGraph(g, 0, async_upload=rep >= 3)
     t1 = time.perf_counter()
     h = HyperBall(dg, P, None)
     t2 = time.perf_counter()

@@ -1,0 +1,72 @@
+"""sb_graph_create_async: chunked PCIe upload overlapped with the first HyperBall
+pass.  Results must be bit-identical to the synchronous upload, and a malformed
+stream must still surface as std::runtime_error (RuntimeError) -- at the first
+step or at sb_graph_wait instead of at create."""
+import numpy as np
+import pytest
+
+from paper_2604_08374_b200 import CompressedCsr, DeviceGraph, HyperBall
+
+pytestmark = pytest.mark.gpu
+
+
+def graphs():
+    yield "c1like", CompressedCsr.synth_grid(32, 32, 8, 2, 5, 20261017, 0)  # multi-item nodes
+    yield "radius", CompressedCsr.synth_grid(60, 70, 20, 2, 6, 3, 9 * 9)
+    yield "tiny", CompressedCsr.from_adjacency([[1], [0, 2], [1], []])
+
+
+@pytest.mark.parametrize("flags", [{}, {"skip_unchanged": True}, {"interval": True}], ids=["dense", "skip", "interval"])
+@pytest.mark.parametrize("p", [6, 10, 12])
+@pytest.mark.parametrize("name,g", list(graphs()), ids=[n for n, _ in graphs()])
+def test_async_upload_bit_identical(name, g, p, flags):
+    if flags.get("interval") and p < 10:
+        pytest.skip("interval mode needs p >= 10")
+    ref = HyperBall(g, p, None, **flags)
+    ref.run()
+    hb = HyperBall(DeviceGraph(g, async_upload=True), p, None, **flags)
+    hb.run()
+    assert np.array_equal(hb.registers(), ref.registers())
+    a, b = hb.state(), ref.state()
+    assert a.t == b.t and np.array_equal(a.sum_d, b.sum_d) and np.array_equal(a.sum_d2, b.sum_d2)
+
+
+def test_async_upload_shards_and_other_users():
+    g = CompressedCsr.synth_grid(60, 70, 20, 2, 6, 3, 9 * 9)
+    ref = HyperBall(g, 10, None)
+    ref.run()
+    n = g.n
+    parts = [(0, n // 3), (n // 3, n)]
+    hs = [HyperBall(DeviceGraph(g, node_range=r, async_upload=True), 10, None, node_range=r) for r in parts]
+    while True:
+        mx = max(h.step_compute() for h in hs)
+        HyperBall.exchange_local(hs)
+        if hs[0].step_finish(mx)[1] | hs[1].step_finish(mx)[1]:
+            break
+    assert np.array_equal(np.concatenate([h.state().sum_d for h in hs]), ref.state().sum_d)
+    dg = DeviceGraph(g, async_upload=True)  # local metrics / download wait for the upload themselves
+    off, deg, st = dg.download()
+    assert np.array_equal(st, g.stream) and np.array_equal(deg, g.degrees)
+    assert np.array_equal(DeviceGraph(g, async_upload=True).local_metrics()["clustering"],
+                          DeviceGraph(g).local_metrics()["clustering"], equal_nan=True)
+
+
+def _raw(n, offsets, degrees, stream):
+    return CompressedCsr.from_arrays(offsets, degrees, bytes(stream))
+
+
+@pytest.mark.parametrize("bad", [
+    (2, [0, 1, 2], [1, 1], [0x81, 0x80]),                  # truncated varint
+    (3, [0, 2, 3, 4], [1, 1, 1], [1, 1, 0, 1]),             # degree mismatch
+    (2, [0, 1, 2], [1, 1], [5, 0]),                         # id out of range
+], ids=["truncated", "degree", "range"])
+def test_async_upload_reports_malformed_stream(bad):
+    g = _raw(*bad)
+    dg = DeviceGraph(g, async_upload=True)
+    hb = HyperBall(dg, 10, None)
+    with pytest.raises(RuntimeError):
+        hb.iterate_once()
+    with pytest.raises(RuntimeError):  # sticky
+        hb.iterate_once()
+    with pytest.raises(RuntimeError):
+        DeviceGraph(g, async_upload=True).wait()
