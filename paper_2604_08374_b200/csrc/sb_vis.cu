@@ -15,8 +15,10 @@
 //
 //   vis_rows_kernel<false>  warp per node: degree and row bytes
 //   vis_rows_kernel<true>   warp per node: writes the row at offsets[v]
-//   Each warp step tests 32 consecutive candidate cells of one grid row; the
-//   visible ones are ordered by a ballot, their deltas / varint lengths come
+//   Each warp step tests 32 consecutive candidate cells of one grid row (one
+//   blocked-box test per grid row first: an obstacle-free box spanned by v and
+//   the row's candidates makes the whole row visible); the visible ones are
+//   ordered by a ballot, their deltas / varint lengths come
 //   from the previous visible lane (or the carried previous id) and a warp
 //   prefix sum of the lengths places every varint.
 #include <cub/cub.cuh>
@@ -115,13 +117,52 @@ __global__ void __launch_bounds__(256) vis_rows_kernel(VisArgs a) {
       const int c_lo = static_cast<int>(imax64(0, cc - span));
       const int c_hi = static_cast<int>(imin64(static_cast<int64_t>(a.cols) - 1, cc + span));
       const uint64_t rowbase = static_cast<uint64_t>(r2) * a.cols;
+      // Every candidate segment of this grid row lies in the box spanned by
+      // (r, cc) and the row's column range: no obstacle in it -> all visible.
+      const bool clear = !any_blocked(a, r, min(cc, c_lo), r2, max(cc, c_hi));
+      if (clear) {
+        // Obstacle-free row: its candidates are consecutive free cells, so their
+        // node ids are consecutive (raster order) and every delta after the
+        // row's first is 1 (2 across v itself): one varint + (count - 1) bytes.
+        const bool self_row = r2 == r;
+        const uint32_t span = static_cast<uint32_t>(c_hi - c_lo + 1);
+        const uint32_t cnt = span - (self_row ? 1u : 0u);
+        if (cnt == 0) continue;
+        const uint32_t w0 = a.node_of_cell[rowbase + c_lo];
+        const uint32_t first = w0 + ((self_row && c_lo == cc) ? 1u : 0u);
+        const uint32_t last = w0 + span - 1u - ((self_row && c_hi == cc) ? 1u : 0u);
+        const uint32_t d0 = have_prev ? first - prev : first;
+        const uint32_t l0 = leb_len32(d0);
+        if (WRITE) {
+          if (lane == 0) {
+            uint8_t* o = a.stream + pos;
+            uint32_t x = d0;
+            while (x >= 0x80u) {
+              *o++ = static_cast<uint8_t>(x) | 0x80u;
+              x >>= 7;
+            }
+            *o = static_cast<uint8_t>(x);
+          }
+          // emitted index j >= 1 -> column; its delta is 2 right after v itself
+          for (uint32_t j = 1 + lane; j < cnt; j += 32) {
+            const int cj = c_lo + static_cast<int>(j) + ((self_row && c_lo + static_cast<int>(j) >= cc) ? 1 : 0);
+            a.stream[pos + l0 + j - 1] = (self_row && cj == cc + 1 && cj - 2 >= c_lo) ? 2u : 1u;
+          }
+        }
+        pos += l0 + cnt - 1;
+        bytes += l0 + cnt - 1;
+        deg += cnt;
+        prev = last;
+        have_prev = true;
+        continue;
+      }
       for (int base = c_lo; base <= c_hi; base += 32) {
         const int c2 = base + lane;
         bool emit = false;
         uint32_t w = 0;
         if (c2 <= c_hi && !(r2 == r && c2 == cc)) {
           w = a.node_of_cell[rowbase + c2];
-          if (w != 0xffffffffu) emit = visible(a, r, cc, r2, c2);
+          if (w != 0xffffffffu) emit = clear || visible(a, r, cc, r2, c2);
         }
         const uint32_t mask = __ballot_sync(FULL, emit);
         if (!mask) continue;
