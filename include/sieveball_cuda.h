@@ -247,7 +247,7 @@ typedef struct {
   float union_ms;          /* fused decode-union kernel (CUDA events) */
   float estimate_ms;       /* estimate + accumulate kernel */
   float exchange_ms;       /* shard exchange (NCCL / local copies) */
-  float step_ms;           /* whole step incl. host sync */
+  float step_ms;           /* device time from the step's first to its last enqueued operation */
   double max_increase;
   uint64_t changed_nodes;  /* local nodes whose registers changed */
 } sb_iter_stats;
