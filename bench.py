@@ -395,7 +395,7 @@ def main():
     if not args.no_e2e:
         g.pin(True)
         h2d = g.stream_len + 8 * (g.n + 1) + 4 * g.n
-        d2h = 3 * 8 * nl
+        d2h = 4 * 8 * nl + nl  # state(): c_t, c_(t-1), sum_d, sum_d2 (f64) + changed flags (u8)
         def e2e_once():
             t = time.perf_counter()
             dg = DeviceGraph(g, local, (v0, v1), async_upload=True)
