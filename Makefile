@@ -12,8 +12,8 @@ CXXFLAGS := -O3 -std=c++17 -fPIC -Wall -ffp-contract=off -I$(CUDA_INC)
 LIB      := $(PKG)/libsieveball_cuda.so
 TOOL     := tools/sb_hyperball
 
-OBJS := $(BUILD)/sb_kernels.o $(BUILD)/sb_local.o $(BUILD)/sb_vis.o $(BUILD)/sb_runtime.o $(BUILD)/sb_csr.o $(BUILD)/sb_error.o
-HDRS := $(CSRC)/sb_device.cuh $(CSRC)/sb_internal.h $(CSRC)/sb_error.h include/sieveball_cuda.h
+OBJS := $(BUILD)/sb_kernels.o $(BUILD)/sb_local.o $(BUILD)/sb_vis.o $(BUILD)/sb_graph_api.o $(BUILD)/sb_hb_api.o $(BUILD)/sb_exact_api.o $(BUILD)/sb_csr.o $(BUILD)/sb_error.o
+HDRS := $(CSRC)/sb_device.cuh $(CSRC)/sb_internal.h $(CSRC)/sb_error.h $(CSRC)/sb_handles.h include/sieveball_cuda.h
 
 all: $(LIB) $(TOOL) oracle
 
@@ -29,8 +29,8 @@ $(BUILD)/sb_local.o: $(CSRC)/sb_local.cu $(HDRS) | $(BUILD)
 $(BUILD)/sb_vis.o: $(CSRC)/sb_vis.cu $(HDRS) | $(BUILD)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(BUILD)/ptxas_vis.txt || (cat $(BUILD)/ptxas_vis.txt; false)
 
-$(BUILD)/sb_runtime.o: $(CSRC)/sb_runtime.cu $(HDRS) | $(BUILD)
-	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(BUILD)/ptxas_runtime.txt || (cat $(BUILD)/ptxas_runtime.txt; false)
+$(BUILD)/%_api.o: $(CSRC)/%_api.cu $(HDRS) | $(BUILD)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(BUILD)/ptxas_$*_api.txt || (cat $(BUILD)/ptxas_$*_api.txt; false)
 
 $(BUILD)/sb_csr.o: $(CSRC)/sb_csr.cpp $(HDRS) | $(BUILD)
 	$(CXX) $(CXXFLAGS) -c $< -o $@

@@ -1,0 +1,427 @@
+// sb_graph_api.cu -- C-ABI: device graphs (upload, asynchronous chunked upload,
+// on-device grid build), their validation, work items and run index.
+#include <algorithm>
+#include <cstdio>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "sb_device.cuh"
+#include "sb_handles.h"
+
+int build_run_index(sb_graph* g) {
+  if (g->d_run_off || g->n_items == 0) return SB_OK;
+  sb::RunIndexArgs a{};
+  a.stream = g->d_stream;
+  a.item_off = g->d_item_off;
+  a.item_base = g->d_item_base;
+  a.item_count = g->d_item_count;
+  a.n_items = g->n_items;
+  uint64_t* d_cnt = nullptr;
+  CK(cudaMalloc(&d_cnt, g->n_items * 8));
+  a.run_count = d_cnt;
+  CK(sb::launch_run_index(a, false, 0));
+  CK(sync_stream(0));
+  std::vector<uint64_t> off(g->n_items + 1, 0);
+  CK(cudaMemcpy(off.data() + 1, d_cnt, g->n_items * 8, cudaMemcpyDeviceToHost));
+  cudaFree(d_cnt);
+  for (uint64_t i = 0; i < g->n_items; ++i) off[i + 1] += off[i];
+  g->n_runs = off[g->n_items];
+  CK(cudaMalloc(&g->d_run_off, off.size() * 8));
+  CK(cudaMemcpy(g->d_run_off, off.data(), off.size() * 8, cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&g->d_run_s, std::max<uint64_t>(g->n_runs, 1) * 4));
+  CK(cudaMalloc(&g->d_run_e, std::max<uint64_t>(g->n_runs, 1) * 4));
+  a.run_off = g->d_run_off;
+  a.run_s = g->d_run_s;
+  a.run_e = g->d_run_e;
+  CK(sb::launch_run_index(a, true, 0));
+  CK(sync_stream(0));
+  return SB_OK;
+}
+
+
+extern "C" {
+
+const char* sb_last_error(void) { return sb::last_error(); }
+const char* sb_version(void) { return "sieveball-b200 0.1 (sm_100a)"; }
+
+int sb_device_count(int* n) {
+  int c = 0;
+  cudaError_t e = cudaGetDeviceCount(&c);
+  if (e != cudaSuccess) {
+    *n = 0;
+    return cuda_fail(e, "cudaGetDeviceCount");
+  }
+  *n = c;
+  return SB_OK;
+}
+
+int sb_check_convergence(double max_increase) { return max_increase <= 0.5 ? 1 : 0; }
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ graph
+// Work items, CTA tiles and the upload-time validation of the device-resident
+// stream slice (shared by sb_graph_create and the on-device grid builder).
+static int graph_setup_host(sb_graph* g, const uint32_t* deg_local) {
+  // Work items: <= chunk neighbours each, sized so the edge work splits into
+  // ~4 items per resident warp (load balance) but stays >= 512 ids (decode
+  // and merge amortisation).
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
+  const uint64_t target = g->edges_local / (static_cast<uint64_t>(sms) * 64 * 4);
+  g->chunk = static_cast<uint32_t>(std::min<uint64_t>(8192, std::max<uint64_t>(512, target)));
+  std::vector<uint32_t> node_item(g->n_local + 1);
+  uint64_t items = 0;
+  for (uint64_t i = 0; i < g->n_local; ++i) {
+    node_item[i] = static_cast<uint32_t>(items);
+    const uint32_t d = deg_local[i];
+    items += d ? (d + g->chunk - 1) / g->chunk : 1;
+  }
+  if (items > 0xffffffffull) return fail(SB_EINVAL, "too many work items");
+  node_item[g->n_local] = static_cast<uint32_t>(items);
+  g->n_items = items;
+  // Tiles for the CTA schedule: group k = local nodes [8k, 8k+8), one tile per
+  // chunk index up to the group's largest item count.
+  std::vector<uint32_t> tn0, tq;
+  for (uint64_t k = 0; k < g->n_local; k += 8) {
+    uint32_t mx = 0;
+    for (uint64_t i = k; i < std::min<uint64_t>(k + 8, g->n_local); ++i) mx = std::max(mx, node_item[i + 1] - node_item[i]);
+    for (uint32_t q = 0; q < mx; ++q) {
+      tn0.push_back(static_cast<uint32_t>(k));
+      tq.push_back(q);
+    }
+  }
+  g->n_tiles = tn0.size();
+  CK(cudaMalloc(&g->d_tile_node0, std::max<size_t>(tn0.size(), 1) * 4));
+  CK(cudaMalloc(&g->d_tile_q, std::max<size_t>(tq.size(), 1) * 4));
+  if (!tn0.empty()) {
+    CK(cudaMemcpy(g->d_tile_node0, tn0.data(), tn0.size() * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(g->d_tile_q, tq.data(), tq.size() * 4, cudaMemcpyHostToDevice));
+  }
+  CK(cudaMalloc(&g->d_node_item, node_item.size() * 4));
+  CK(cudaMemcpy(g->d_node_item, node_item.data(), node_item.size() * 4, cudaMemcpyHostToDevice));
+  const uint64_t ni = std::max<uint64_t>(items, 1);
+  CK(cudaMalloc(&g->d_item_off, ni * 8));
+  CK(cudaMalloc(&g->d_item_base, ni * 4));
+  CK(cudaMalloc(&g->d_item_count, ni * 4));
+  CK(cudaMalloc(&g->d_item_node, ni * 4));
+  CK(cudaMalloc(&g->d_err, 16));
+  CK(cudaMemset(g->d_err, 0xff, 8));
+  CK(cudaMemset(reinterpret_cast<uint8_t*>(g->d_err) + 8, 0, 8));
+  return SB_OK;
+}
+
+// Upload-time validation of local nodes [n0, n1) (LEB128 well-formed, strictly
+// increasing ids < n, exactly degrees[v] ids) + work items; errors land in d_err.
+static cudaError_t launch_validate(sb_graph* g, uint64_t n0, uint64_t n1, cudaStream_t s) {
+  if (n1 <= n0) return cudaSuccess;
+  sb::BuildArgs a{};
+  a.stream = g->d_stream;
+  a.row_off = g->d_rowoff;
+  a.degrees = g->d_deg;
+  a.n_local = g->n_local;
+  a.n_global = g->n;
+  a.node_begin = n0;
+  a.node_end = n1;
+  a.chunk = g->chunk;
+  a.node_item = g->d_node_item;
+  a.item_off = g->d_item_off;
+  a.item_base = g->d_item_base;
+  a.item_count = g->d_item_count;
+  a.item_node = g->d_item_node;
+  a.err_node = g->d_err;
+  a.max_run = reinterpret_cast<unsigned int*>(g->d_err + 1);
+  return sb::launch_build_items(a, s);
+}
+
+static int graph_check(sb_graph* g) {
+  unsigned long long err = 0;
+  CK(cudaMemcpy(&err, g->d_err, 8, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(&g->max_run, g->d_err + 1, 4, cudaMemcpyDeviceToHost));
+  if (err != ~0ull) {
+    g->broken = 1;
+    return fail(SB_ERUNTIME, "cgraph: malformed compressed row at node %llu (bad varint, "
+                             "non-increasing or out-of-range id, or degree mismatch)",
+                (unsigned long long)(err + g->v0));
+  }
+  return SB_OK;
+}
+
+// Work items, CTA tiles and the upload-time validation of the device-resident
+// stream slice (shared by sb_graph_create and the on-device grid builder).
+int graph_setup(sb_graph* g, const uint32_t* deg_local) {
+  int rc = graph_setup_host(g, deg_local);
+  if (rc) return rc;
+  CK(launch_validate(g, 0, g->n_local, 0));
+  CK(sync_stream(0));
+  return graph_check(g);
+}
+
+// Completes an asynchronous upload (sb_graph_create_async): waits for every
+// chunk's copy + validation and reports a malformed stream (sticky).
+int graph_wait(sb_graph* g) {
+  if (g->broken) return fail(SB_ERUNTIME, "cgraph: the graph failed validation at upload");
+  if (!g->pending) return SB_OK;
+  DeviceGuard dg(g->device);
+  CK(sync_stream(g->up_stream));
+  CK(sync_stream(g->val_stream));
+  g->pending = false;
+  return graph_check(g);
+}
+
+static int graph_create(uint64_t n, const uint64_t* offsets, const uint32_t* degrees, const uint8_t* stream,
+                        uint64_t stream_len, const uint32_t* orig_id, uint64_t node_begin, uint64_t node_end,
+                        int device, bool async, sb_graph** out) {
+  if (!out) return fail(SB_EINVAL, "sb_graph_create: out is NULL");
+  *out = nullptr;
+  if (n == 0) return fail(SB_EINVAL, "hyperball: graph empty");
+  if (n > 0xffffffffull) return fail(SB_EINVAL, "graph has more than 2^32 nodes");
+  if (!offsets || !degrees || (stream_len && !stream))
+    return fail(SB_EINVAL, "sb_graph_create: NULL array");
+  if (node_begin > node_end || node_end > n) return fail(SB_EINVAL, "sb_graph_create: bad node range");
+  if (offsets[n] != stream_len) return fail(SB_ERUNTIME, "cgraph: offsets[N] != stream length");
+  for (uint64_t v = node_begin; v < node_end; ++v)
+    if (offsets[v + 1] < offsets[v]) return fail(SB_ERUNTIME, "cgraph: offsets decrease at node %llu", (unsigned long long)v);
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(SB_ECUDA, "no CUDA device: the HyperBall path has no CPU fallback");
+  if (device < 0 || device >= ndev) return fail(SB_EINVAL, "bad device %d", device);
+  DeviceGuard dg(device);
+  auto* g = new sb_graph();
+  g->device = device;
+  g->n = n;
+  g->v0 = node_begin;
+  g->v1 = node_end;
+  g->n_local = node_end - node_begin;
+  const uint64_t b0 = offsets[node_begin], b1 = offsets[node_end];
+  g->stream_local = b1 - b0;
+  uint64_t edges = 0;
+  for (uint64_t v = node_begin; v < node_end; ++v) edges += degrees[v];
+  g->edges_local = edges;
+  auto bail = [&](int rc) { delete g; return rc; };
+#define GK(x)                                                 \
+  do {                                                        \
+    cudaError_t e_ = (x);                                     \
+    if (e_ != cudaSuccess) return bail(cuda_fail(e_, #x));    \
+  } while (0)
+  // 256 B of zero padding: the decoder reads whole 128-byte windows (+8 for alignment).
+  GK(cudaMalloc(&g->d_stream, g->stream_local + 256));
+  GK(cudaMemset(g->d_stream + g->stream_local, 0, 256));
+  if (g->stream_local && !async)
+    GK(cudaMemcpy(g->d_stream, stream + b0, g->stream_local, cudaMemcpyHostToDevice));
+  std::vector<uint64_t> ro(g->n_local + 1);
+  for (uint64_t i = 0; i <= g->n_local; ++i) ro[i] = offsets[node_begin + i] - b0;
+  GK(cudaMalloc(&g->d_rowoff, ro.size() * 8));
+  GK(cudaMemcpy(g->d_rowoff, ro.data(), ro.size() * 8, cudaMemcpyHostToDevice));
+  GK(cudaMalloc(&g->d_deg, std::max<uint64_t>(g->n_local, 1) * 4));
+  if (g->n_local) GK(cudaMemcpy(g->d_deg, degrees + node_begin, g->n_local * 4, cudaMemcpyHostToDevice));
+  if (orig_id) {
+    GK(cudaMalloc(&g->d_orig, n * 4));
+    GK(cudaMemcpy(g->d_orig, orig_id, n * 4, cudaMemcpyHostToDevice));
+  }
+  if (!async) {
+    const int rc = graph_setup(g, degrees + node_begin);
+    if (rc) return bail(rc);
+    *out = g;
+    return SB_OK;
+  }
+  // Asynchronous: K chunks of ~equal stream bytes on 8-node (tile group)
+  // boundaries; copy k on up_stream, validation k on val_stream after copy k.
+  const int rc = graph_setup_host(g, degrees + node_begin);
+  if (rc) return bail(rc);
+  GK(cudaStreamCreateWithFlags(&g->up_stream, cudaStreamNonBlocking));
+  GK(cudaStreamCreateWithFlags(&g->val_stream, cudaStreamNonBlocking));
+  const int K = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(16, g->n_local / 64)));
+  g->chunk_node.assign(1, 0);
+  for (int k = 1; k < K; ++k) {
+    const uint64_t goal = b0 + g->stream_local * k / K;
+    uint64_t v = std::lower_bound(offsets + node_begin, offsets + node_end, goal) - (offsets + node_begin);
+    v = std::min<uint64_t>(v & ~7ull, g->n_local);
+    if (v > g->chunk_node.back()) g->chunk_node.push_back(v);
+  }
+  if (g->chunk_node.back() != g->n_local) g->chunk_node.push_back(g->n_local);
+  // tile ranges: tiles are ordered by 8-node group
+  std::vector<uint32_t> tn0(g->n_tiles);
+  if (g->n_tiles) GK(cudaMemcpy(tn0.data(), g->d_tile_node0, g->n_tiles * 4, cudaMemcpyDeviceToHost));
+  g->chunk_tile.clear();
+  for (uint64_t cn : g->chunk_node)
+    g->chunk_tile.push_back(std::lower_bound(tn0.begin(), tn0.end(), static_cast<uint32_t>(std::min<uint64_t>(cn, 0xffffffffull))) - tn0.begin());
+  g->chunk_tile.back() = g->n_tiles;
+  const size_t nk = g->chunk_node.size() - 1;
+  g->val_ev.resize(nk, nullptr);
+  for (size_t k = 0; k < nk; ++k) {
+    cudaEvent_t copied = nullptr;
+    GK(cudaEventCreateWithFlags(&g->val_ev[k], cudaEventDisableTiming));
+    GK(cudaEventCreateWithFlags(&copied, cudaEventDisableTiming));
+    const uint64_t s0 = ro[g->chunk_node[k]], s1 = ro[g->chunk_node[k + 1]];
+    if (s1 > s0) GK(cudaMemcpyAsync(g->d_stream + s0, stream + b0 + s0, s1 - s0, cudaMemcpyHostToDevice, g->up_stream));
+    GK(cudaEventRecord(copied, g->up_stream));
+    GK(cudaStreamWaitEvent(g->val_stream, copied, 0));
+    cudaEventDestroy(copied);  // released once the wait is enqueued
+    GK(launch_validate(g, g->chunk_node[k], g->chunk_node[k + 1], g->val_stream));
+    GK(cudaEventRecord(g->val_ev[k], g->val_stream));
+  }
+  g->pending = true;
+#undef GK
+  *out = g;
+  return SB_OK;
+}
+
+extern "C" {
+
+int sb_graph_create(uint64_t n, const uint64_t* offsets, const uint32_t* degrees, const uint8_t* stream,
+                    uint64_t stream_len, const uint32_t* orig_id, uint64_t node_begin, uint64_t node_end,
+                    int device, sb_graph** out) {
+  return graph_create(n, offsets, degrees, stream, stream_len, orig_id, node_begin, node_end, device, false, out);
+}
+
+int sb_graph_create_async(uint64_t n, const uint64_t* offsets, const uint32_t* degrees, const uint8_t* stream,
+                          uint64_t stream_len, const uint32_t* orig_id, uint64_t node_begin, uint64_t node_end,
+                          int device, sb_graph** out) {
+  return graph_create(n, offsets, degrees, stream, stream_len, orig_id, node_begin, node_end, device, true, out);
+}
+
+int sb_graph_wait(sb_graph* g) {
+  if (!g) return fail(SB_EINVAL, "NULL graph");
+  return graph_wait(g);
+}
+
+// ------------------------------------------------------------------ on-device graph build
+// Grid -> visibility -> delta-LEB128 CSR entirely in HBM (sb_vis.cu), then the
+// same work-item setup and validation as an uploaded graph.
+int sb_graph_build_grid(uint32_t rows, uint32_t cols, const uint8_t* blocked, uint64_t radius2, int device,
+                        sb_graph** out) {
+  if (!out) return fail(SB_EINVAL, "sb_graph_build_grid: out is NULL");
+  *out = nullptr;
+  if (rows == 0 || cols == 0) return fail(SB_EINVAL, "grid: rows and cols must be >= 1");
+  if (!blocked) return fail(SB_EINVAL, "sb_graph_build_grid: NULL mask");
+  const uint64_t cells = static_cast<uint64_t>(rows) * cols;
+  if (cells >= 0xffffffffull) return fail(SB_EINVAL, "grid: more than 2^32 - 1 cells");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(SB_ECUDA, "no CUDA device: the HyperBall path has no CPU fallback");
+  if (device < 0 || device >= ndev) return fail(SB_EINVAL, "bad device %d", device);
+  DeviceGuard dg(device);
+  auto* g = new sb_graph();
+  g->device = device;
+  g->rows = rows;
+  g->cols = cols;
+  uint8_t* d_mask = nullptr;
+  uint32_t *d_pref = nullptr, *d_scan = nullptr, *d_noc = nullptr, *d_tmp = nullptr;
+  uint64_t* d_bytes = nullptr;
+  auto cleanup = [&] { dfree(d_mask); dfree(d_pref); dfree(d_scan); dfree(d_noc); dfree(d_tmp); dfree(d_bytes); };
+  auto bail = [&](int rc) { cleanup(); delete g; return rc; };
+#define BK(x)                                                 \
+  do {                                                        \
+    cudaError_t e_ = (x);                                     \
+    if (e_ != cudaSuccess) return bail(cuda_fail(e_, #x));    \
+  } while (0)
+  cudaStream_t s = 0;
+  BK(cudaMalloc(&d_mask, cells));
+  BK(cudaMemcpy(d_mask, blocked, cells, cudaMemcpyHostToDevice));
+  BK(cudaMalloc(&d_pref, static_cast<uint64_t>(rows + 1) * (cols + 1) * 4));
+  BK(cudaMalloc(&d_scan, 2 * cells * 4));
+  sb::VisArgs a{};
+  a.rows = rows;
+  a.cols = cols;
+  a.radius2 = radius2;
+  a.blocked = d_mask;
+  a.pref = d_pref;
+  uint64_t n = 0;
+  BK(sb::launch_vis_prepare(a, d_pref, d_scan, &n, s));
+  if (n == 0) return bail(fail(SB_ERUNTIME, "grid: zero active cells"));
+  g->n = n;
+  g->v0 = 0;
+  g->v1 = n;
+  g->n_local = n;
+  BK(cudaMalloc(&d_noc, cells * 4));
+  BK(cudaMalloc(&g->d_cell, n * 4));
+  BK(sb::launch_vis_maps(a, d_scan, d_noc, g->d_cell, s));
+  a.node_of_cell = d_noc;
+  a.cell_of_node = g->d_cell;
+  a.n = n;
+  if (radius2) {  // isqrt64 as the host generator
+    uint64_t r = static_cast<uint64_t>(std::sqrt(static_cast<double>(radius2)));
+    while (r * r > radius2) --r;
+    while ((r + 1) * (r + 1) <= radius2) ++r;
+    a.R = static_cast<int64_t>(r);
+  } else {
+    a.R = std::max(rows, cols);
+  }
+  BK(cudaMalloc(&g->d_deg, n * 4));
+  BK(cudaMalloc(&d_bytes, (n + 1) * 8));
+  BK(cudaMemsetAsync(d_bytes + n, 0, 8, s));
+  a.deg = g->d_deg;
+  a.bytes = d_bytes;
+  BK(sb::launch_vis_rows(a, false, s));
+  BK(cudaMalloc(&g->d_rowoff, (n + 1) * 8));
+  BK(sb::launch_scan_u64(d_bytes, g->d_rowoff, n + 1, s));
+  uint64_t total = 0;
+  BK(cudaMemcpy(&total, g->d_rowoff + n, 8, cudaMemcpyDeviceToHost));
+  g->stream_local = total;
+  BK(cudaMalloc(&g->d_stream, total + 256));
+  BK(cudaMemsetAsync(g->d_stream + total, 0, 256, s));
+  a.offsets = g->d_rowoff;
+  a.stream = g->d_stream;
+  BK(sb::launch_vis_rows(a, true, s));
+  // components (the 2n scratch doubles as the union-find parent array + ranks)
+  BK(cudaMalloc(&d_tmp, 3 * n * 4));
+  BK(cudaMalloc(&g->d_comp, n * 4));
+  BK(cudaMalloc(&g->d_comp_sizes, n * 4));
+  a.parent = d_tmp;
+  BK(sb::launch_vis_components(a, g->d_comp, g->d_comp_sizes, d_tmp + n, &g->n_comp, s));
+  std::vector<uint32_t> deg(n);
+  BK(cudaMemcpy(deg.data(), g->d_deg, n * 4, cudaMemcpyDeviceToHost));
+  uint64_t edges = 0;
+  for (uint64_t v = 0; v < n; ++v) edges += deg[v];
+  g->edges_local = edges;
+  cleanup();
+  const int rc = graph_setup(g, deg.data());
+  if (rc) {
+    delete g;
+    return rc;
+  }
+#undef BK
+  *out = g;
+  return SB_OK;
+}
+
+int sb_graph_grid_info(const sb_graph* g, uint32_t* rows, uint32_t* cols, uint32_t* cell_of_node,
+                       uint32_t* component_id, uint32_t* component_sizes, uint64_t* n_components) {
+  if (!g) return fail(SB_EINVAL, "NULL graph");
+  if (!g->d_cell) return fail(SB_EINVAL, "sb_graph_grid_info: graph was not built from a grid");
+  DeviceGuard dg(g->device);
+  if (rows) *rows = g->rows;
+  if (cols) *cols = g->cols;
+  if (n_components) *n_components = g->n_comp;
+  if (cell_of_node) CK(cudaMemcpy(cell_of_node, g->d_cell, g->n * 4, cudaMemcpyDeviceToHost));
+  if (component_id) CK(cudaMemcpy(component_id, g->d_comp, g->n * 4, cudaMemcpyDeviceToHost));
+  if (component_sizes) CK(cudaMemcpy(component_sizes, g->d_comp_sizes, g->n_comp * 4, cudaMemcpyDeviceToHost));
+  return SB_OK;
+}
+
+int sb_graph_download(const sb_graph* g, uint64_t* offsets, uint32_t* degrees, uint8_t* stream) {
+  if (!g) return fail(SB_EINVAL, "NULL graph");
+  DeviceGuard dg(g->device);
+  if (const int rc = graph_wait(const_cast<sb_graph*>(g))) return rc;
+  if (offsets) CK(cudaMemcpy(offsets, g->d_rowoff, (g->n_local + 1) * 8, cudaMemcpyDeviceToHost));
+  if (degrees) CK(cudaMemcpy(degrees, g->d_deg, g->n_local * 4, cudaMemcpyDeviceToHost));
+  if (stream && g->stream_local) CK(cudaMemcpy(stream, g->d_stream, g->stream_local, cudaMemcpyDeviceToHost));
+  return SB_OK;
+}
+
+int sb_graph_stats(const sb_graph* g, uint64_t* n_local, uint64_t* edges_local,
+                   uint64_t* stream_bytes_local, uint64_t* n_items, uint32_t* chunk) {
+  if (!g) return fail(SB_EINVAL, "NULL graph");
+  if (n_local) *n_local = g->n_local;
+  if (edges_local) *edges_local = g->edges_local;
+  if (stream_bytes_local) *stream_bytes_local = g->stream_local;
+  if (n_items) *n_items = g->n_items;
+  if (chunk) *chunk = g->chunk;
+  return SB_OK;
+}
+
+void sb_graph_destroy(sb_graph* g) { delete g; }
+
+}  // extern "C"

@@ -1,0 +1,237 @@
+// sb_handles.h -- PRIVATE: the C-ABI handle types (sb_graph, sb_hb, sb_comm,
+// sb_exact), the runtime utilities shared by the host translation units, and
+// the internal graph helpers.  Not installed; include/sieveball_cuda.h is the API.
+#pragma once
+#include <nccl.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <thread>
+#include <vector>
+
+#include "../../include/sieveball_cuda.h"
+#include "sb_error.h"
+#include "sb_internal.h"
+
+namespace sb {
+namespace rt {
+inline int cuda_fail(cudaError_t e, const char* what) {
+  return fail(e == cudaErrorMemoryAllocation ? SB_ENOMEM : SB_ECUDA, "%s: %s", what,
+              cudaGetErrorString(e));
+}
+
+#define CK(x)                                          \
+  do {                                                 \
+    cudaError_t e_ = (x);                              \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #x);   \
+  } while (0)
+
+#define NK(x)                                                               \
+  do {                                                                      \
+    ncclResult_t r_ = (x);                                                  \
+    if (r_ != ncclSuccess) return fail(SB_ENCCL, "%s: %s", #x, ncclGetErrorString(r_)); \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+template <class T>
+inline void dfree(T*& p) {
+  if (p) cudaFree(p);
+  p = nullptr;
+}
+
+// Stream sync with an optional watchdog: SB_SYNC_TIMEOUT_S=<seconds> turns a
+// device hang into an SB_ECUDA error instead of a blocked host thread.
+inline cudaError_t sync_stream(cudaStream_t s) {
+  static const double limit = [] {
+    const char* e = getenv("SB_SYNC_TIMEOUT_S");
+    return e ? atof(e) : 0.0;
+  }();
+  if (limit <= 0.0) return cudaStreamSynchronize(s);
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    const cudaError_t e = cudaStreamQuery(s);
+    if (e != cudaErrorNotReady) return e;
+    if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > limit)
+      return cudaErrorLaunchTimeout;
+    std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+}
+
+inline double decode_ord(unsigned long long e) {
+  if (e == 0ull) return -INFINITY;  // no node contributed
+  unsigned long long u = (e >> 63) ? (e & 0x7fffffffffffffffull) : ~e;
+  double x;
+  memcpy(&x, &u, 8);
+  return x;
+}
+}  // namespace rt
+}  // namespace sb
+
+using sb::fail;
+using sb::rt::cuda_fail;
+using sb::rt::DeviceGuard;
+using sb::rt::decode_ord;
+using sb::rt::dfree;
+using sb::rt::sync_stream;
+
+struct sb_graph {
+  int device = 0;
+  uint64_t n = 0, v0 = 0, v1 = 0, n_local = 0, edges_local = 0, stream_local = 0;
+  uint8_t* d_stream = nullptr;
+  uint64_t* d_rowoff = nullptr;
+  uint32_t* d_deg = nullptr;
+  uint32_t* d_orig = nullptr;
+  uint32_t chunk = 0;
+  uint64_t n_items = 0;
+  uint32_t* d_node_item = nullptr;
+  uint64_t* d_item_off = nullptr;
+  uint32_t* d_item_base = nullptr;
+  uint32_t* d_item_count = nullptr;
+  uint32_t* d_item_node = nullptr;
+  uint32_t max_run = 0;               // longest run of consecutive neighbour ids
+  uint64_t n_runs = 0;                // interval-mode run index (built on first use)
+  uint64_t* d_run_off = nullptr;
+  uint32_t* d_run_s = nullptr;
+  uint32_t* d_run_e = nullptr;
+  uint64_t n_tiles = 0;               // CTA tiles: (8-node group, chunk index)
+  uint32_t* d_tile_node0 = nullptr;
+  uint32_t* d_tile_q = nullptr;
+  // built on the device from a grid (sb_graph_build_grid)
+  uint32_t rows = 0, cols = 0;
+  uint64_t n_comp = 0;
+  uint32_t* d_cell = nullptr;         // cell_of_node
+  uint32_t* d_comp = nullptr;         // component id per node
+  uint32_t* d_comp_sizes = nullptr;   // n_comp sizes
+  // asynchronous chunked upload (sb_graph_create_async): chunk k's stream
+  // bytes are copied on up_stream and validated on val_stream; val_ev[k]
+  // fires when chunk k (nodes [chunk_node[k], chunk_node[k+1])) is usable.
+  bool pending = false;
+  int broken = 0;                     // validation failed (sticky SB_ERUNTIME)
+  unsigned long long* d_err = nullptr;  // [0] min bad node, [1] max run
+  cudaStream_t up_stream = nullptr, val_stream = nullptr;
+  std::vector<cudaEvent_t> val_ev;
+  std::vector<uint64_t> chunk_node, chunk_tile;
+  ~sb_graph() {
+    DeviceGuard dg(device);
+    dfree(d_stream); dfree(d_rowoff); dfree(d_deg); dfree(d_orig); dfree(d_node_item);
+    dfree(d_item_off); dfree(d_item_base); dfree(d_item_count); dfree(d_item_node);
+    dfree(d_tile_node0); dfree(d_tile_q);
+    dfree(d_run_off); dfree(d_run_s); dfree(d_run_e);
+    dfree(d_cell); dfree(d_comp); dfree(d_comp_sizes);
+    if (up_stream) cudaStreamSynchronize(up_stream);
+    if (val_stream) cudaStreamSynchronize(val_stream);
+    for (auto e : val_ev) cudaEventDestroy(e);
+    if (up_stream) cudaStreamDestroy(up_stream);
+    if (val_stream) cudaStreamDestroy(val_stream);
+    dfree(d_err);
+  }
+};
+
+struct sb_comm {
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0, device = 0;
+  ~sb_comm() {
+    if (comm) ncclCommDestroy(comm);
+  }
+};
+
+struct sb_hb {
+  sb_graph* g = nullptr;
+  unsigned p = 10;
+  uint32_t depth = 0, flags = 0;
+  uint64_t row = 0;
+  int slices = 1;
+  uint8_t* d_plane[2] = {nullptr, nullptr};
+  uint8_t* d_changed[2] = {nullptr, nullptr};
+  double* d_c[2] = {nullptr, nullptr};
+  double* d_sum_d = nullptr;
+  double* d_sum_d2 = nullptr;
+  double* d_lc = nullptr;
+  uint8_t* d_scratch = nullptr;
+  uint32_t* d_counter = nullptr;
+  unsigned long long* d_misc = nullptr;  // [0] work, [1] max_ord, [2] changed count
+  unsigned long long* h_misc = nullptr;  // pinned
+  uint8_t* d_tmp = nullptr;              // packed export buffer
+  uint8_t* d_st = nullptr;               // interval mode: sparse-table levels 1..levels
+  int levels = 0;
+  uint64_t tmp_bytes = 0;
+  int latest = 0;     // plane / c / changed index holding iteration t
+  uint32_t t = 0;
+  bool converged = false, finished = false, computed = false;
+  double alpha = 0.0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  std::vector<sb_iter_stats> stats;
+  sb_iter_stats cur_stats{};
+  sb_comm* comm = nullptr;
+  std::vector<uint64_t> bounds;
+  // fused P2P exchange (CUDA IPC): peers' planes / changed flags by parity
+  int npeers = 0;
+  std::vector<void*> ipc_opened;
+  uint8_t** d_peer_plane[2] = {nullptr, nullptr};
+  uint8_t** d_peer_chg[2] = {nullptr, nullptr};
+  ~sb_hb() {
+    DeviceGuard dg(g ? g->device : 0);
+    for (void* q : ipc_opened) cudaIpcCloseMemHandle(q);
+    for (int i = 0; i < 2; ++i) { dfree(d_peer_plane[i]); dfree(d_peer_chg[i]); }
+    for (int i = 0; i < 2; ++i) { dfree(d_plane[i]); dfree(d_changed[i]); dfree(d_c[i]); }
+    dfree(d_sum_d); dfree(d_sum_d2); dfree(d_lc); dfree(d_scratch); dfree(d_counter);
+    dfree(d_misc); dfree(d_tmp); dfree(d_st);
+    if (h_misc) cudaFreeHost(h_misc);
+    for (auto& e : ev) if (e) cudaEventDestroy(e);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+struct sb_exact {
+  sb_graph* g = nullptr;
+  int P = 10;                       // row geometry: 2^(P-1) bytes = 2^(P+2) sources
+  uint64_t row = 0, block = 0;
+  uint32_t depth = 0, flags = 0;
+  int slices = 1, levels = 0;
+  uint8_t* d_plane[2] = {nullptr, nullptr};
+  uint8_t* d_changed = nullptr;     // union epilogue flags (unused by the count)
+  uint8_t* d_scratch = nullptr;
+  uint32_t* d_counter = nullptr;
+  uint8_t* d_st = nullptr;
+  uint32_t* d_pop = nullptr;
+  uint32_t* d_reach = nullptr;
+  unsigned long long* d_sum = nullptr;   // [sum_d n | sum_d2 n]
+  uint32_t* d_hist = nullptr;
+  uint32_t hist_cap = 0;
+  unsigned long long* d_misc = nullptr;  // [0] work, [1] changed count
+  uint32_t max_depth = 0;
+  uint64_t sources_done = 0;
+  double union_ms = 0.0;
+  uint64_t union_launches = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  ~sb_exact() {
+    DeviceGuard dg(g ? g->device : 0);
+    for (int i = 0; i < 2; ++i) dfree(d_plane[i]);
+    dfree(d_changed); dfree(d_scratch); dfree(d_counter); dfree(d_st); dfree(d_pop);
+    dfree(d_reach); dfree(d_sum); dfree(d_hist); dfree(d_misc);
+    for (auto e : ev) if (e) cudaEventDestroy(e);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+// Internal graph helpers (sb_graph_api.cu).
+int graph_setup(sb_graph* g, const uint32_t* deg_local);
+int graph_wait(sb_graph* g);
+int build_run_index(sb_graph* g);

@@ -1,0 +1,580 @@
+// sb_hb_api.cu -- C-ABI: HyperBall state, the Alg. 1 control loop, shard
+// exchange (NCCL grouped broadcast / fused P2P peers / same-process copies), stats.
+#include <algorithm>
+#include <cstdio>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "sb_device.cuh"
+#include "sb_handles.h"
+
+static int hb_init(sb_hb* h) {
+  sb_graph* g = h->g;
+  const int L = h->latest = 0;
+  h->t = 0;
+  h->converged = h->finished = h->computed = false;
+  h->stats.clear();
+  CK(sb::launch_init(static_cast<int>(h->p), h->d_plane[L], g->n, g->d_orig, h->stream));
+  CK(cudaMemsetAsync(h->d_changed[L], 1, g->n, h->stream));  // t=1 gathers every neighbour
+  CK(cudaMemsetAsync(h->d_changed[1 - L], 0, g->n, h->stream));
+  if (g->n_local) {
+    CK(cudaMemsetAsync(h->d_sum_d, 0, g->n_local * 8, h->stream));
+    CK(cudaMemsetAsync(h->d_sum_d2, 0, g->n_local * 8, h->stream));
+    sb::EstArgs e{};
+    e.plane = h->d_plane[L];
+    e.node_begin = g->v0;
+    e.n_local = g->n_local;
+    e.lc = h->d_lc;
+    e.alpha = h->alpha;
+    e.m = static_cast<double>(1u << h->p);
+    e.c_cur = h->d_c[L];
+    e.t = 0;
+    CK(sb::launch_estimate(static_cast<int>(h->p), 0, e, h->stream));
+  }
+  if (h->d_counter) CK(cudaMemsetAsync(h->d_counter, 0, std::max<uint64_t>(g->n_local, 1) * h->slices * 4, h->stream));
+  CK(sync_stream(h->stream));
+  return SB_OK;
+}
+
+// Interval mode: runs of consecutive ids per work item, decoded once from the
+// device-resident LEB128 stream (count pass, host scan, fill pass).
+extern "C" {
+
+int sb_hb_create(sb_graph* g, unsigned p, uint32_t depth_limit, uint32_t flags, sb_hb** out) {
+  if (!out) return fail(SB_EINVAL, "sb_hb_create: out is NULL");
+  *out = nullptr;
+  if (!g) return fail(SB_EINVAL, "sb_hb_create: NULL graph");
+  if (p < 4 || p > 16) return fail(SB_EINVAL, "hll: precision must be in [4, 16]");
+  if ((flags & SB_HB_INTERVAL) && (p < 10 || (flags & SB_HB_SKIP_UNCHANGED)))
+    return fail(SB_EINVAL, "interval mode needs p >= 10 and excludes SB_HB_SKIP_UNCHANGED");
+  DeviceGuard dg(g->device);
+  auto* h = new sb_hb();
+  h->g = g;
+  h->p = p;
+  h->depth = depth_limit;
+  h->flags = flags;
+  if (const char* e = getenv("SB_UNION_SCHEDULE")) {  // A/B override for benchmarking
+    if (!strcmp(e, "warp")) h->flags |= SB_HB_SCHEDULE_WARP;
+    if (!strcmp(e, "tile")) h->flags &= ~SB_HB_SCHEDULE_WARP;
+  }
+  const uint32_t m = 1u << p;
+  h->row = m / 2;
+  h->slices = sb::union_slices(static_cast<int>(p));
+  // alpha_m exactly as hll.cpp:13-18
+  switch (m) {
+    case 16: h->alpha = 0.673; break;
+    case 32: h->alpha = 0.697; break;
+    case 64: h->alpha = 0.709; break;
+    default: h->alpha = 0.7213 / (1.0 + 1.079 / m); break;
+  }
+  auto bail = [&](int rc) { delete h; return rc; };
+#define HK(x)                                                 \
+  do {                                                        \
+    cudaError_t e_ = (x);                                     \
+    if (e_ != cudaSuccess) return bail(cuda_fail(e_, #x));    \
+  } while (0)
+  HK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  for (auto& e : h->ev) HK(cudaEventCreate(&e));
+  const uint64_t plane = g->n * h->row;
+  const uint64_t nl = std::max<uint64_t>(g->n_local, 1);
+  for (int i = 0; i < 2; ++i) {
+    HK(cudaMalloc(&h->d_plane[i], plane + 64));
+    HK(cudaMalloc(&h->d_changed[i], g->n));
+    HK(cudaMalloc(&h->d_c[i], nl * 8));
+  }
+  HK(cudaMalloc(&h->d_sum_d, nl * 8));
+  HK(cudaMalloc(&h->d_sum_d2, nl * 8));
+  // Linear-counting table lc[z] = m * log(m / z) built with the host libm, so
+  // the device never evaluates log (hll.cpp:35).
+  std::vector<double> lc(m + 1, 0.0);
+  const double md = static_cast<double>(m);
+  for (uint32_t z = 1; z <= m; ++z) lc[z] = md * std::log(md / static_cast<double>(z));
+  HK(cudaMalloc(&h->d_lc, lc.size() * 8));
+  HK(cudaMemcpy(h->d_lc, lc.data(), lc.size() * 8, cudaMemcpyHostToDevice));
+  const uint64_t slice_bytes = std::min<uint64_t>(h->row, 512);
+  HK(cudaMalloc(&h->d_scratch, std::max<uint64_t>(g->n_items, 1) * h->slices * slice_bytes));
+  HK(cudaMalloc(&h->d_counter, nl * h->slices * 4));
+  HK(cudaMalloc(&h->d_misc, 4 * 8));
+  if (flags & SB_HB_INTERVAL) {
+    if (const int rc = graph_wait(g)) return bail(rc);  // max_run comes from the validation pass
+    // levels K = floor(log2(longest run)), capped at 10 (longer runs peel 2^K blocks)
+    int K = 0;
+    while (K < 10 && (2u << K) <= g->max_run) ++K;
+    h->levels = K;
+    if (K) HK(cudaMalloc(&h->d_st, static_cast<uint64_t>(K) * plane + 64));
+    const int rc = build_run_index(g);
+    if (rc) return bail(rc);
+  }
+  HK(cudaMallocHost(&h->h_misc, 4 * 8));
+#undef HK
+  const int rc = hb_init(h);
+  if (rc != SB_OK) return bail(rc);
+  *out = h;
+  return SB_OK;
+}
+
+int sb_hb_reset(sb_hb* h) {
+  if (!h) return fail(SB_EINVAL, "NULL handle");
+  DeviceGuard dg(h->g->device);
+  const int rc = hb_init(h);
+  if (rc) return rc;
+  // With fused P2P, a peer that already started iteration 1 stores rows and
+  // changed flags into this replica: nobody may pass reset until every rank
+  // has re-initialised its planes and flags (NCCL barrier on 8 bytes).
+  if (h->npeers && h->comm && h->comm->nranks > 1) {
+    NK(ncclAllReduce(h->d_misc + 3, h->d_misc + 3, 1, ncclUint64, ncclMax, h->comm->comm, h->stream));
+    CK(sync_stream(h->stream));
+  }
+  return SB_OK;
+}
+
+void* sb_hb_stream(const sb_hb* h) { return h ? static_cast<void*>(h->stream) : nullptr; }
+
+int sb_hb_step_compute(sb_hb* h, double* local_max) {
+  if (!h) return fail(SB_EINVAL, "NULL handle");
+  if (h->finished) return fail(SB_EINVAL, "hyperball: already finished (t=%u)", h->t);
+  if (h->computed) return fail(SB_EINVAL, "hyperball: step_compute called twice without finish");
+  sb_graph* g = h->g;
+  DeviceGuard dg(g->device);
+  if (g->broken) return fail(SB_ERUNTIME, "cgraph: the graph failed validation at upload");
+  if (g->pending && (h->flags & SB_HB_SCHEDULE_WARP)) {  // the chunk pipeline needs the tile schedule
+    const int rc = graph_wait(g);
+    if (rc) return rc;
+  }
+  h->t += 1;
+  const int L = h->latest, N = 1 - L;
+  const bool skip = (h->flags & SB_HB_SKIP_UNCHANGED) != 0;
+  h->cur_stats = sb_iter_stats{};
+  h->cur_stats.t = h->t;
+  CK(cudaMemsetAsync(h->d_misc, 0, 4 * 8, h->stream));
+  CK(cudaEventRecord(h->ev[0], h->stream));
+  if (g->n_local) {
+    CK(cudaMemsetAsync(h->d_changed[N] + g->v0, 0, g->n_local, h->stream));
+    sb::UnionArgs u{};
+    u.stream = g->d_stream;
+    u.item_off = g->d_item_off;
+    u.item_base = g->d_item_base;
+    u.item_count = g->d_item_count;
+    u.item_node = g->d_item_node;
+    u.node_item = g->d_node_item;
+    u.n_items = g->n_items;
+    u.node_begin = g->v0;
+    u.cur = h->d_plane[L];
+    u.next = h->d_plane[N];
+    u.scratch = h->d_scratch;
+    u.node_counter = h->d_counter;
+    u.changed_out = h->d_changed[N];
+    u.changed_in = h->d_changed[L];
+    u.work = h->d_misc;
+    u.n_local = g->n_local;
+    u.n_tiles = (h->flags & SB_HB_SCHEDULE_WARP) ? 0 : g->n_tiles;
+    u.tile_node0 = g->d_tile_node0;
+    u.tile_q = g->d_tile_q;
+    u.npeers = h->npeers;
+    u.peer_next = h->d_peer_plane[N];
+    u.peer_changed = h->d_peer_chg[N];
+    CK(cudaEventRecord(h->ev[1], h->stream));
+    if (h->flags & SB_HB_INTERVAL) {
+      if (h->levels) CK(sb::launch_st_build(static_cast<int>(h->p), h->d_plane[L], h->d_st, g->n, h->levels, h->stream));
+      sb::IntervalArgs ia{};
+      ia.u = u;
+      if (!ia.u.n_tiles) ia.u.n_tiles = g->n_tiles;  // interval kernel uses the tile schedule
+      ia.st = h->d_st ? h->d_st : h->d_plane[L];
+      ia.n_global = g->n;
+      ia.levels = h->levels;
+      ia.run_off = g->d_run_off;
+      ia.run_s = g->d_run_s;
+      ia.run_e = g->d_run_e;
+      CK(sb::launch_union_interval(static_cast<int>(h->p), ia, h->stream));
+    } else if (g->pending) {
+      // First pass over a graph still streaming in: chunk k's tiles start as
+      // soon as its bytes are copied and validated (overlaps PCIe with compute).
+      for (size_t k = 0; k + 1 < g->chunk_node.size(); ++k) {
+        const uint64_t t0 = g->chunk_tile[k], t1 = g->chunk_tile[k + 1];
+        if (t1 == t0) continue;
+        CK(cudaStreamWaitEvent(h->stream, g->val_ev[k], 0));
+        CK(cudaMemsetAsync(h->d_misc, 0, 8, h->stream));  // work counter
+        sb::UnionArgs uk = u;
+        uk.tile_node0 = g->d_tile_node0 + t0;
+        uk.tile_q = g->d_tile_q + t0;
+        uk.n_tiles = t1 - t0;
+        CK(sb::launch_union(static_cast<int>(h->p), skip, uk, h->stream));
+      }
+    } else {
+      CK(sb::launch_union(static_cast<int>(h->p), skip, u, h->stream));
+    }
+    CK(cudaEventRecord(h->ev[2], h->stream));
+    sb::EstArgs e{};
+    e.plane = h->d_plane[N];
+    e.node_begin = g->v0;
+    e.n_local = g->n_local;
+    e.lc = h->d_lc;
+    e.alpha = h->alpha;
+    e.m = static_cast<double>(1u << h->p);
+    e.c_prev = h->d_c[L];
+    e.c_cur = h->d_c[N];
+    e.sum_d = h->d_sum_d;
+    e.sum_d2 = h->d_sum_d2;
+    e.changed = h->d_changed[N];
+    e.t = h->t;
+    e.max_ord = h->d_misc + 1;
+    e.changed_count = h->d_misc + 2;
+    CK(sb::launch_estimate(static_cast<int>(h->p), skip ? 2 : 1, e, h->stream));
+  } else {
+    CK(cudaEventRecord(h->ev[1], h->stream));
+    CK(cudaEventRecord(h->ev[2], h->stream));
+  }
+  // The input flags are consumed: clear them now, so they can serve as next
+  // iteration's output -- peers write into them only after the iteration
+  // barrier (global max), never before this clear.
+  CK(cudaMemsetAsync(h->d_changed[L], 0, g->n, h->stream));
+  CK(cudaEventRecord(h->ev[3], h->stream));
+  CK(cudaMemcpyAsync(h->h_misc, h->d_misc, 4 * 8, cudaMemcpyDeviceToHost, h->stream));
+  CK(sync_stream(h->stream));
+  if (g->pending) {  // the upload finished inside this step: report a malformed stream now
+    const int rc = graph_wait(g);
+    if (rc) {
+      h->t -= 1;
+      return rc;
+    }
+  }
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, h->ev[1], h->ev[2]);
+  h->cur_stats.union_ms = ms;
+  cudaEventElapsedTime(&ms, h->ev[2], h->ev[3]);
+  h->cur_stats.estimate_ms = ms;
+  cudaEventElapsedTime(&ms, h->ev[0], h->ev[3]);
+  h->cur_stats.step_ms = ms;
+  h->cur_stats.changed_nodes = h->h_misc[2];
+  h->computed = true;
+  if (local_max) *local_max = decode_ord(h->h_misc[1]);
+  return SB_OK;
+}
+
+int sb_hb_step_finish(sb_hb* h, double global_max, int* converged, int* finished) {
+  if (!h) return fail(SB_EINVAL, "NULL handle");
+  if (!h->computed) return fail(SB_EINVAL, "hyperball: step_finish without step_compute");
+  h->computed = false;
+  // Alg. 1: converged -> break (no swap); t == d -> stop.
+  h->converged = sb_check_convergence(global_max) != 0;
+  h->finished = h->converged || (h->depth != 0 && h->t == h->depth);
+  h->latest = 1 - h->latest;  // registers / c of iteration t become "latest"
+  h->cur_stats.max_increase = global_max;
+  h->stats.push_back(h->cur_stats);
+  if (converged) *converged = h->converged;
+  if (finished) *finished = h->finished;
+  return SB_OK;
+}
+
+int sb_hb_exchange_local(sb_hb* const* hs, int count) {
+  if (!hs || count < 1) return fail(SB_EINVAL, "sb_hb_exchange_local: no handles");
+  for (int i = 0; i < count; ++i) {
+    if (!hs[i] || !hs[i]->computed) return fail(SB_EINVAL, "exchange: handle %d not computed", i);
+    if (hs[i]->g->n != hs[0]->g->n || hs[i]->p != hs[0]->p) return fail(SB_EINVAL, "exchange: shape mismatch");
+  }
+  for (int i = 0; i < count; ++i) {
+    const sb_hb* src = hs[i];
+    const sb_graph* gs = src->g;
+    if (!gs->n_local) continue;
+    const int sN = 1 - src->latest;
+    for (int j = 0; j < count; ++j) {
+      if (j == i) continue;
+      sb_hb* dst = hs[j];
+      const int dN = 1 - dst->latest;
+      DeviceGuard dg(dst->g->device);
+      CK(cudaMemcpyPeerAsync(dst->d_plane[dN] + gs->v0 * src->row, dst->g->device,
+                             src->d_plane[sN] + gs->v0 * src->row, gs->device,
+                             gs->n_local * src->row, dst->stream));
+      CK(cudaMemcpyPeerAsync(dst->d_changed[dN] + gs->v0, dst->g->device, src->d_changed[sN] + gs->v0,
+                             gs->device, gs->n_local, dst->stream));
+    }
+  }
+  for (int j = 0; j < count; ++j) {
+    DeviceGuard dg(hs[j]->g->device);
+    CK(sync_stream(hs[j]->stream));
+  }
+  return SB_OK;
+}
+
+static int exchange_nccl(sb_hb* h, double* gmax) {
+  sb_comm* c = h->comm;
+  sb_graph* g = h->g;
+  const int N = 1 - h->latest;
+  CK(cudaEventRecord(h->ev[0], h->stream));
+  if (!h->npeers) {  // rows were not pushed by the kernel epilogue: broadcast the shards
+    NK(ncclGroupStart());
+    for (int r = 0; r < c->nranks; ++r) {
+      const uint64_t a = h->bounds[r], b = h->bounds[r + 1];
+      if (b == a) continue;
+      uint8_t* rows = h->d_plane[N] + a * h->row;
+      NK(ncclBroadcast(rows, rows, (b - a) * h->row, ncclUint8, r, c->comm, h->stream));
+      uint8_t* ch = h->d_changed[N] + a;
+      NK(ncclBroadcast(ch, ch, b - a, ncclUint8, r, c->comm, h->stream));
+    }
+    NK(ncclGroupEnd());
+  }
+  // 8-byte max; with fused P2P rows it is also the iteration barrier
+  // (every rank's union kernel, and so its peer stores, has completed).
+  NK(ncclAllReduce(h->d_misc + 1, h->d_misc + 1, 1, ncclUint64, ncclMax, c->comm, h->stream));
+  CK(cudaEventRecord(h->ev[1], h->stream));
+  CK(cudaMemcpyAsync(h->h_misc + 1, h->d_misc + 1, 8, cudaMemcpyDeviceToHost, h->stream));
+  CK(sync_stream(h->stream));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]);
+  h->cur_stats.exchange_ms = ms;
+  *gmax = decode_ord(h->h_misc[1]);
+  (void)g;
+  return SB_OK;
+}
+
+int sb_hb_step(sb_hb* h, double* max_increase, int* converged, int* finished) {
+  if (h && h->npeers && !(h->comm && h->comm->nranks > 1))
+    return fail(SB_EINVAL, "peers attached without a communicator: use step_compute / step_finish "
+                           "with an external barrier");
+  double mx = 0.0;
+  int rc = sb_hb_step_compute(h, &mx);
+  if (rc) return rc;
+  if (h->comm && h->comm->nranks > 1) {
+    DeviceGuard dg(h->g->device);
+    rc = exchange_nccl(h, &mx);
+    if (rc) {
+      h->computed = false;
+      return rc;
+    }
+  }
+  if (max_increase) *max_increase = mx;
+  return sb_hb_step_finish(h, mx, converged, finished);
+}
+
+int sb_hb_run(sb_hb* h, uint32_t* iterations, int* converged) {
+  if (!h) return fail(SB_EINVAL, "NULL handle");
+  int conv = 0, fin = h->finished ? 1 : 0;
+  while (!fin) {
+    const int rc = sb_hb_step(h, nullptr, &conv, &fin);
+    if (rc) return rc;
+  }
+  if (iterations) *iterations = h->t;
+  if (converged) *converged = h->converged;
+  return SB_OK;
+}
+
+static int ensure_tmp(sb_hb* h, uint64_t bytes) {
+  if (h->tmp_bytes >= bytes) return SB_OK;
+  dfree(h->d_tmp);
+  h->tmp_bytes = 0;
+  CK(cudaMalloc(&h->d_tmp, bytes));
+  h->tmp_bytes = bytes;
+  return SB_OK;
+}
+
+int sb_hb_read_registers(const sb_hb* hc, int which, uint64_t v0, uint64_t v1, uint8_t* dst) {
+  sb_hb* h = const_cast<sb_hb*>(hc);
+  if (!h || !dst) return fail(SB_EINVAL, "NULL argument");
+  if (v0 > v1 || v1 > h->g->n) return fail(SB_EINVAL, "bad row range");
+  if (which != SB_REGS_LATEST && which != SB_REGS_PREVIOUS) return fail(SB_EINVAL, "bad plane selector");
+  if (v0 == v1) return SB_OK;
+  DeviceGuard dg(h->g->device);
+  const int idx = which == SB_REGS_LATEST ? h->latest : 1 - h->latest;
+  const uint64_t bytes = (v1 - v0) * h->row;
+  int rc = ensure_tmp(h, bytes);
+  if (rc) return rc;
+  CK(sb::launch_to_packed(static_cast<int>(h->p), h->d_plane[idx] + v0 * h->row, h->d_tmp, v1 - v0, h->stream));
+  CK(cudaMemcpyAsync(dst, h->d_tmp, bytes, cudaMemcpyDeviceToHost, h->stream));
+  CK(sync_stream(h->stream));
+  return SB_OK;
+}
+
+int sb_hb_set_registers(sb_hb* h, const uint8_t* packed) {
+  if (!h || !packed) return fail(SB_EINVAL, "NULL argument");
+  if (h->computed) return fail(SB_EINVAL, "set_registers during a step");
+  sb_graph* g = h->g;
+  DeviceGuard dg(g->device);
+  const uint64_t bytes = g->n * h->row;
+  int rc = ensure_tmp(h, bytes);
+  if (rc) return rc;
+  const int L = h->latest;
+  CK(cudaMemcpyAsync(h->d_tmp, packed, bytes, cudaMemcpyHostToDevice, h->stream));
+  CK(sb::launch_from_packed(static_cast<int>(h->p), h->d_tmp, h->d_plane[L], g->n, h->stream));
+  CK(cudaMemsetAsync(h->d_changed[L], 1, g->n, h->stream));
+  if (g->n_local) {
+    sb::EstArgs e{};
+    e.plane = h->d_plane[L];
+    e.node_begin = g->v0;
+    e.n_local = g->n_local;
+    e.lc = h->d_lc;
+    e.alpha = h->alpha;
+    e.m = static_cast<double>(1u << h->p);
+    e.c_cur = h->d_c[L];
+    CK(sb::launch_estimate(static_cast<int>(h->p), 0, e, h->stream));
+  }
+  CK(sync_stream(h->stream));
+  h->finished = h->converged = false;
+  return SB_OK;
+}
+
+int sb_hb_read_state(const sb_hb* h, double* c_latest, double* c_previous, double* sum_d,
+                     double* sum_d2, uint8_t* changed, uint32_t* t, int* converged, int* finished) {
+  if (!h) return fail(SB_EINVAL, "NULL handle");
+  const sb_graph* g = h->g;
+  DeviceGuard dg(g->device);
+  const uint64_t nb = g->n_local * 8;
+  if (g->n_local) {
+    if (c_latest) CK(cudaMemcpy(c_latest, h->d_c[h->latest], nb, cudaMemcpyDeviceToHost));
+    if (c_previous) CK(cudaMemcpy(c_previous, h->d_c[1 - h->latest], nb, cudaMemcpyDeviceToHost));
+    if (sum_d) CK(cudaMemcpy(sum_d, h->d_sum_d, nb, cudaMemcpyDeviceToHost));
+    if (sum_d2) CK(cudaMemcpy(sum_d2, h->d_sum_d2, nb, cudaMemcpyDeviceToHost));
+    if (changed) CK(cudaMemcpy(changed, h->d_changed[h->latest] + g->v0, g->n_local, cudaMemcpyDeviceToHost));
+  }
+  if (t) *t = h->t;
+  if (converged) *converged = h->converged;
+  if (finished) *finished = h->finished;
+  return SB_OK;
+}
+
+int sb_hb_metrics(const sb_hb* hc, const uint32_t* nv, const uint32_t* deg, double* md, double* ihh,
+                  double* tekl, double* pv, double* m1, double* m2) {
+  sb_hb* h = const_cast<sb_hb*>(hc);
+  if (!h || !nv || !deg) return fail(SB_EINVAL, "NULL argument");
+  const uint64_t n = h->g->n_local;
+  if (!n) return SB_OK;
+  DeviceGuard dg(h->g->device);
+  // one device block: [nv u32 | deg u32 | 6 x f64 outputs]
+  const uint64_t bytes = n * 8 + 6 * n * 8;
+  int rc = ensure_tmp(h, bytes);
+  if (rc) return rc;
+  uint32_t* d_nv = reinterpret_cast<uint32_t*>(h->d_tmp);
+  uint32_t* d_deg = d_nv + n;
+  double* o = reinterpret_cast<double*>(h->d_tmp + n * 8);
+  CK(cudaMemcpyAsync(d_nv, nv, n * 4, cudaMemcpyHostToDevice, h->stream));
+  CK(cudaMemcpyAsync(d_deg, deg, n * 4, cudaMemcpyHostToDevice, h->stream));
+  sb::MetricArgs a{};
+  a.n = n;
+  a.sum_d = h->d_sum_d;
+  a.sum_d2 = h->d_sum_d2;
+  a.nv = d_nv;
+  a.deg = d_deg;
+  a.md = o;
+  a.ihh = o + n;
+  a.tekl = o + 2 * n;
+  a.pv = o + 3 * n;
+  a.m1 = o + 4 * n;
+  a.m2 = o + 5 * n;
+  CK(sb::launch_metrics(a, h->stream));
+  double* outs[6] = {md, ihh, tekl, pv, m1, m2};
+  for (int i = 0; i < 6; ++i)
+    if (outs[i]) CK(cudaMemcpyAsync(outs[i], o + i * n, n * 8, cudaMemcpyDeviceToHost, h->stream));
+  CK(sync_stream(h->stream));
+  return SB_OK;
+}
+
+int sb_hb_stats(const sb_hb* h, sb_iter_stats* out, uint32_t cap, uint32_t* count) {
+  if (!h) return fail(SB_EINVAL, "NULL handle");
+  const uint32_t n = static_cast<uint32_t>(h->stats.size());
+  if (out)
+    for (uint32_t i = 0; i < n && i < cap; ++i) out[i] = h->stats[i];
+  if (count) *count = n;
+  return SB_OK;
+}
+
+void sb_hb_destroy(sb_hb* h) { delete h; }
+
+// ------------------------------------------------------------------ NCCL
+int sb_comm_unique_id(void* id_out) {
+  if (!id_out) return fail(SB_EINVAL, "NULL id");
+  static_assert(sizeof(ncclUniqueId) == SB_COMM_ID_BYTES, "ncclUniqueId size");
+  ncclUniqueId id;
+  NK(ncclGetUniqueId(&id));
+  memcpy(id_out, &id, sizeof(id));
+  return SB_OK;
+}
+
+int sb_comm_create(int nranks, int rank, const void* id, int device, sb_comm** out) {
+  if (!out || !id) return fail(SB_EINVAL, "NULL argument");
+  *out = nullptr;
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(SB_EINVAL, "bad rank/nranks");
+  DeviceGuard dg(device);
+  auto* c = new sb_comm();
+  c->nranks = nranks;
+  c->rank = rank;
+  c->device = device;
+  ncclUniqueId uid;
+  memcpy(&uid, id, sizeof(uid));
+  const ncclResult_t r = ncclCommInitRank(&c->comm, nranks, uid, rank);
+  if (r != ncclSuccess) {
+    c->comm = nullptr;
+    delete c;
+    return fail(SB_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+  }
+  *out = c;
+  return SB_OK;
+}
+
+int sb_hb_attach_comm(sb_hb* h, sb_comm* c, const uint64_t* bounds) {
+  if (!h || !c || !bounds) return fail(SB_EINVAL, "NULL argument");
+  if (bounds[0] != 0 || bounds[c->nranks] != h->g->n) return fail(SB_EINVAL, "bounds must cover [0, N)");
+  for (int r = 0; r < c->nranks; ++r)
+    if (bounds[r + 1] < bounds[r]) return fail(SB_EINVAL, "bounds not monotone");
+  if (bounds[c->rank] != h->g->v0 || bounds[c->rank + 1] != h->g->v1)
+    return fail(SB_EINVAL, "graph range does not match this rank's bounds");
+  if (c->device != h->g->device) return fail(SB_EINVAL, "communicator device != graph device");
+  h->comm = c;
+  h->bounds.assign(bounds, bounds + c->nranks + 1);
+  return SB_OK;
+}
+
+void sb_comm_destroy(sb_comm* c) { delete c; }
+
+// ------------------------------------------------------------------ fused P2P exchange
+int sb_hb_ipc_handles(const sb_hb* h, void* out, size_t cap) {
+  if (!h || !out) return fail(SB_EINVAL, "NULL argument");
+  if (cap < SB_IPC_HANDLE_BYTES) return fail(SB_EINVAL, "handle buffer too small (%d bytes needed)", SB_IPC_HANDLE_BYTES);
+  static_assert(sizeof(cudaIpcMemHandle_t) * 4 == SB_IPC_HANDLE_BYTES, "ipc handle size");
+  DeviceGuard dg(h->g->device);
+  cudaIpcMemHandle_t hs[4];
+  CK(cudaIpcGetMemHandle(&hs[0], h->d_plane[0]));
+  CK(cudaIpcGetMemHandle(&hs[1], h->d_plane[1]));
+  CK(cudaIpcGetMemHandle(&hs[2], h->d_changed[0]));
+  CK(cudaIpcGetMemHandle(&hs[3], h->d_changed[1]));
+  memcpy(out, hs, sizeof(hs));
+  return SB_OK;
+}
+
+int sb_hb_attach_peers(sb_hb* h, int nranks, int rank, const void* handles, const uint64_t* bounds) {
+  if (!h || !handles || !bounds) return fail(SB_EINVAL, "NULL argument");
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(SB_EINVAL, "bad rank/nranks");
+  if (h->npeers) return fail(SB_EINVAL, "peers already attached");
+  if (bounds[0] != 0 || bounds[nranks] != h->g->n) return fail(SB_EINVAL, "bounds must cover [0, N)");
+  if (bounds[rank] != h->g->v0 || bounds[rank + 1] != h->g->v1)
+    return fail(SB_EINVAL, "graph range does not match this rank's bounds");
+  DeviceGuard dg(h->g->device);
+  std::vector<uint8_t*> pl[2], ch[2];
+  const auto* hs = static_cast<const cudaIpcMemHandle_t*>(handles);
+  for (int r = 0; r < nranks; ++r) {
+    if (r == rank) continue;
+    void* q[4];
+    for (int k = 0; k < 4; ++k) {
+      CK(cudaIpcOpenMemHandle(&q[k], hs[4 * r + k], cudaIpcMemLazyEnablePeerAccess));
+      h->ipc_opened.push_back(q[k]);
+    }
+    pl[0].push_back(static_cast<uint8_t*>(q[0]));
+    pl[1].push_back(static_cast<uint8_t*>(q[1]));
+    ch[0].push_back(static_cast<uint8_t*>(q[2]));
+    ch[1].push_back(static_cast<uint8_t*>(q[3]));
+  }
+  const int np = nranks - 1;
+  for (int i = 0; i < 2; ++i) {
+    CK(cudaMalloc(&h->d_peer_plane[i], std::max(np, 1) * sizeof(uint8_t*)));
+    CK(cudaMalloc(&h->d_peer_chg[i], std::max(np, 1) * sizeof(uint8_t*)));
+    if (np) {
+      CK(cudaMemcpy(h->d_peer_plane[i], pl[i].data(), np * sizeof(uint8_t*), cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(h->d_peer_chg[i], ch[i].data(), np * sizeof(uint8_t*), cudaMemcpyHostToDevice));
+    }
+  }
+  h->npeers = np;
+  h->bounds.assign(bounds, bounds + nranks + 1);
+  return SB_OK;
+}
+
+
+}  // extern "C"

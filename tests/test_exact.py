@@ -276,3 +276,29 @@ def test_gpu_iteration_contract(D, g):
         it = hb.run()
         assert it == (min(d, D + 1) if d else D + 1), (d, it)
         assert hb.state().converged == (d is None or d > D)
+
+
+def test_host_entry_point_errors(tmp_path):
+    with pytest.raises(RuntimeError):  # std::runtime_error on I/O failure
+        write_csv(str(tmp_path / "missing_dir" / "x.csv"), {"md": np.zeros(2)}, 2)
+    with pytest.raises(ValueError):
+        depth_entropy(np.zeros((3, 0), np.uint32))
+
+
+@pytest.mark.gpu
+def test_gpu_exact_argument_errors():
+    g = path_graph(10)
+    with pytest.raises(ValueError):
+        ExactBfs(g, None, log2_block=11)
+    with pytest.raises(ValueError):
+        ExactBfs(g, None, log2_block=17)
+    with pytest.raises(ValueError):
+        ExactBfs(DeviceGraph(g, node_range=(0, 5)))  # needs the full graph
+    x = ExactBfs(g)
+    with pytest.raises(ValueError):
+        x.run(5, 11)
+    x.run(0, 10)
+    from paper_2604_08374_b200._lib import check, lib
+    hist = np.zeros(10, np.uint32)
+    with pytest.raises(ValueError):  # histogram capacity must exceed the max depth (9)
+        check(lib().sb_exact_read(x._h, None, None, None, hist.ctypes.data, 1))
