@@ -94,14 +94,18 @@ class CompressedCsr {
 // built on the device from a raster obstacle mask.
 class DeviceGraph {
  public:
-  explicit DeviceGraph(const CompressedCsr& g, int device = 0, uint64_t v0 = 0, uint64_t v1 = UINT64_MAX) {
+  // async_upload: chunked upload overlapped with the first HyperBall pass
+  // (sb_graph_create_async); `g` must outlive the upload (wait() / first step).
+  explicit DeviceGraph(const CompressedCsr& g, int device = 0, uint64_t v0 = 0, uint64_t v1 = UINT64_MAX,
+                       bool async_upload = false) {
     const sb_csr_desc& d = g.desc();
     if (v1 == UINT64_MAX) v1 = d.n;
     sb_graph* gr = nullptr;
-    check(sb_graph_create(d.n, d.offsets, d.degrees, d.stream, d.stream_len, d.hilbert_inverse, v0, v1, device,
-                          &gr));
+    auto create = async_upload ? sb_graph_create_async : sb_graph_create;
+    check(create(d.n, d.offsets, d.degrees, d.stream, d.stream_len, d.hilbert_inverse, v0, v1, device, &gr));
     init(gr, d.n, v0, v1);
   }
+  void wait() const { check(sb_graph_wait(g_.get())); }
   static DeviceGraph from_grid(uint32_t rows, uint32_t cols, const std::vector<uint8_t>& blocked, uint64_t radius2,
                                int device = 0) {
     if (blocked.size() != static_cast<size_t>(rows) * cols) throw std::invalid_argument("mask size != rows * cols");

@@ -360,34 +360,68 @@ int sb_csr_synth_grid(uint32_t rows, uint32_t cols, uint32_t n_rects, uint32_t r
   return SB_OK;
 }
 
+}  // extern "C"
+
+namespace {
+// Delta-LEB128 encoding of a sorted adjacency, rows in
+// parallel (byte counts -> offsets -> writes).  Components are left to the caller.
+int encode_adjacency(sb_csr* c, uint64_t n, const uint64_t* adj_offsets, const uint32_t* adj_ids, unsigned threads) {
+  c->n = n;
+  c->degrees.assign(n, 0);
+  c->offsets.assign(n + 1, 0);
+  std::vector<uint64_t> rowbytes(n, 0);
+  std::atomic<uint64_t> bad{UINT64_MAX};
+  std::atomic<int> kind{0};
+  parallel_for(n, threads, [&](uint64_t b, uint64_t e) {
+    for (uint64_t v = b; v < e; ++v) {
+      uint64_t bytes = 0;
+      for (uint64_t k = adj_offsets[v]; k < adj_offsets[v + 1]; ++k) {
+        const uint32_t w = adj_ids[k];
+        int err = w >= n ? 1 : (k > adj_offsets[v] && w <= adj_ids[k - 1]) ? 2 : 0;
+        if (err) {
+          uint64_t cur = bad.load();
+          while (v < cur && !bad.compare_exchange_weak(cur, v)) {
+          }
+          if (bad.load() == v) kind = err;
+          break;
+        }
+        bytes += leb_len(k > adj_offsets[v] ? w - adj_ids[k - 1] : w);
+      }
+      c->degrees[v] = static_cast<uint32_t>(adj_offsets[v + 1] - adj_offsets[v]);
+      rowbytes[v] = bytes;
+    }
+  });
+  if (bad.load() != UINT64_MAX)
+    return cfail(SB_EINVAL, kind == 1 ? "cgraph: neighbour id out of range at node %llu"
+                                      : "cgraph: non-increasing neighbour list at node %llu",
+                 (unsigned long long)bad.load());
+  c->edges = 0;
+  for (uint64_t v = 0; v < n; ++v) {
+    c->offsets[v + 1] = c->offsets[v] + rowbytes[v];
+    c->edges += c->degrees[v];
+  }
+  if (!c->alloc_stream(c->offsets[n])) return cfail(SB_ENOMEM, "cannot allocate stream");
+  parallel_for(n, threads, [&](uint64_t b, uint64_t e) {
+    for (uint64_t v = b; v < e; ++v) {
+      uint8_t* o = c->stream + c->offsets[v];
+      for (uint64_t k = adj_offsets[v]; k < adj_offsets[v + 1]; ++k)
+        o = leb_put(o, k > adj_offsets[v] ? adj_ids[k] - adj_ids[k - 1] : adj_ids[k]);
+    }
+  });
+  return SB_OK;
+}
+}  // namespace
+
+extern "C" {
+
 int sb_csr_from_adjacency(uint64_t n, const uint64_t* adj_offsets, const uint32_t* adj_ids, sb_csr** out) {
   if (!out) return cfail(SB_EINVAL, "out is NULL");
   *out = nullptr;
   if (n == 0) return cfail(SB_EINVAL, "graph empty");
   if (n > 0xffffffffull) return cfail(SB_EINVAL, "too many nodes");
   auto c = std::make_unique<sb_csr>();
-  c->n = n;
-  c->degrees.assign(n, 0);
-  c->offsets.assign(n + 1, 0);
-  for (uint64_t v = 0; v < n; ++v) {
-    uint64_t bytes = 0;
-    for (uint64_t k = adj_offsets[v]; k < adj_offsets[v + 1]; ++k) {
-      const uint32_t w = adj_ids[k];
-      if (w >= n) return cfail(SB_EINVAL, "cgraph: neighbour id out of range at node %llu", (unsigned long long)v);
-      if (k > adj_offsets[v] && w <= adj_ids[k - 1])
-        return cfail(SB_EINVAL, "cgraph: non-increasing neighbour list at node %llu", (unsigned long long)v);
-      bytes += leb_len(k > adj_offsets[v] ? w - adj_ids[k - 1] : w);
-    }
-    c->degrees[v] = static_cast<uint32_t>(adj_offsets[v + 1] - adj_offsets[v]);
-    c->offsets[v + 1] = c->offsets[v] + bytes;
-    c->edges += c->degrees[v];
-  }
-  if (!c->alloc_stream(c->offsets[n])) return cfail(SB_ENOMEM, "cannot allocate stream");
-  for (uint64_t v = 0; v < n; ++v) {
-    uint8_t* o = c->stream + c->offsets[v];
-    for (uint64_t k = adj_offsets[v]; k < adj_offsets[v + 1]; ++k)
-      o = leb_put(o, k > adj_offsets[v] ? adj_ids[k] - adj_ids[k - 1] : adj_ids[k]);
-  }
+  const int rc = encode_adjacency(c.get(), n, adj_offsets, adj_ids, 0);
+  if (rc) return rc;
   UF uf(static_cast<uint32_t>(n));
   for (uint64_t v = 0; v < n; ++v)
     for (uint64_t k = adj_offsets[v]; k < adj_offsets[v + 1]; ++k) uf.unite(static_cast<uint32_t>(v), adj_ids[k]);
@@ -499,18 +533,35 @@ int sb_csr_hilbert_reorder(const sb_csr* c, sb_csr** out) {
   std::vector<uint64_t> aoff(n + 1, 0);
   for (uint64_t i = 0; i < n; ++i) aoff[i + 1] = aoff[i] + c->degrees[inv[i]];
   std::vector<uint32_t> ids(aoff[n]);
-  std::vector<uint32_t> tmp;
-  for (uint64_t i = 0; i < n; ++i) {
-    const uint32_t old = inv[i];
-    tmp.resize(c->degrees[old]);
-    if (sb_csr_neighbors(c, old, tmp.data()) != SB_OK) return SB_ERUNTIME;
-    for (auto& w : tmp) w = fwd[w];
-    std::sort(tmp.begin(), tmp.end());
-    std::copy(tmp.begin(), tmp.end(), ids.begin() + aoff[i]);
-  }
-  sb_csr* r = nullptr;
-  const int rc = sb_csr_from_adjacency(n, aoff.data(), ids.data(), &r);
+  std::atomic<int> failed{0};
+  parallel_for(n, 0, [&](uint64_t b, uint64_t e) {
+    for (uint64_t i = b; i < e; ++i) {
+      const uint32_t old = inv[i];
+      uint32_t* row = ids.data() + aoff[i];
+      if (sb_csr_neighbors(c, old, row) != SB_OK) {
+        failed = 1;
+        return;
+      }
+      for (uint64_t k = 0; k < c->degrees[old]; ++k) row[k] = fwd[row[k]];
+      std::sort(row, row + c->degrees[old]);
+    }
+  });
+  if (failed) return cfail(SB_ERUNTIME, "hilbert: malformed row in the source graph");
+  auto rr = std::make_unique<sb_csr>();
+  const int rc = encode_adjacency(rr.get(), n, aoff.data(), ids.data(), 0);
   if (rc) return rc;
+  // Renumbering permutes components; dense ids by first occurrence in the new order.
+  std::vector<uint32_t> remap(c->comp_sizes.size(), UINT32_MAX);
+  rr->comp_id.resize(n);
+  for (uint64_t i = 0; i < n; ++i) {
+    const uint32_t oc = c->comp_id[inv[i]];
+    if (remap[oc] == UINT32_MAX) {
+      remap[oc] = static_cast<uint32_t>(rr->comp_sizes.size());
+      rr->comp_sizes.push_back(c->comp_sizes[oc]);
+    }
+    rr->comp_id[i] = remap[oc];
+  }
+  sb_csr* r = rr.release();
   r->rows = c->rows;
   r->cols = c->cols;
   r->ox = c->ox;

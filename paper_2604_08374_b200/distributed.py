@@ -71,3 +71,24 @@ def gather_to_root(local: np.ndarray, bounds: np.ndarray, rank: int, world: int)
     out = np.concatenate(parts)
     assert out.shape[0] == int(bounds[-1])
     return out
+
+
+def sharded_local_metrics(csr: CompressedCsr, rank: int, world: int, device: int,
+                          bounds: np.ndarray | None = None) -> dict[str, np.ndarray]:
+    """Exact local metrics for this rank's node range (no exchange: every rank
+    holds the full CSR in its HBM; results concatenate in node order)."""
+    b = shard_bounds(csr, world) if bounds is None else bounds
+    return DeviceGraph(csr, device).local_metrics(int(b[rank]), int(b[rank + 1]))
+
+
+def sharded_exact_bfs(csr: CompressedCsr, rank: int, world: int, device: int, depth_limit: int | None = None,
+                      interval: bool = True) -> dict[str, np.ndarray]:
+    """Exact BFS over this rank's share of the SOURCES (contiguous 4096-source
+    blocks); per-node sum_d / sum_d2 / reach / histogram are partial sums that
+    the caller adds across ranks (all_reduce(SUM)) -- no exchange during the run."""
+    from .exact import ExactBfs
+    blocks = (csr.n + 4095) // 4096
+    b0, b1 = blocks * rank // world, blocks * (rank + 1) // world
+    x = ExactBfs(csr, depth_limit, interval=interval, device=device)
+    x.run(min(b0 * 4096, csr.n), min(b1 * 4096, csr.n))
+    return x.result()

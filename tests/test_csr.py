@@ -196,3 +196,13 @@ def test_partition_edge_balanced(parts):
     w = g.degrees.astype(np.int64) + 1
     loads = [int(w[int(b[i]):int(b[i + 1])].sum()) for i in range(parts)]
     assert max(loads) - min(loads) <= 2 * int(w.max())
+
+
+def test_hilbert_components_match_union_find():
+    """The reorder permutes components (first-occurrence ids in the new order) instead of
+    re-running UnionFind over every edge; both must agree."""
+    for args in ((40, 44, 30, 1, 6, 3, 0), (50, 50, 120, 1, 3, 9, 7 * 7)):
+        h = CompressedCsr.synth_grid(*args).hilbert_reorder()
+        uf = CompressedCsr.from_arrays(h.offsets, h.degrees, h.stream)
+        assert np.array_equal(h.component_id, uf.component_id)
+        assert np.array_equal(h.component_sizes, uf.component_sizes)

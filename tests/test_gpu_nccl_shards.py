@@ -128,3 +128,62 @@ def test_fused_p2p_exchange_bit_identical(world, mode):
     assert all(p.exitcode == 0 for p in ps), [p.exitcode for p in ps]
     same_t, same_sum, same_regs = q.get(timeout=10)
     assert same_t and same_sum and same_regs
+
+
+def _rank_widened(rank, world, port, q):
+    """Local metrics by node range and exact BFS by source range, summed over gloo."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import traceback
+    import torch
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        _widened_body(rank, world, q, torch, dist)
+    except Exception:
+        q.put(("error", rank, traceback.format_exc()))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+def _widened_body(rank, world, q, torch, dist):
+    if True:
+        from paper_2604_08374_b200 import CompressedCsr, DeviceGraph, exact_bfs_all
+        from paper_2604_08374_b200.distributed import (gather_to_root, shard_bounds, sharded_exact_bfs,
+                                                       sharded_local_metrics)
+        dev = rank % torch.cuda.device_count()
+        g = CompressedCsr.synth_grid(90, 100, 30, 2, 6, 21, 9 * 9)  # > 8192 nodes: 3 source blocks
+        b = shard_bounds(g, world)
+        lm = sharded_local_metrics(g, rank, world, dev, b)
+        clus = gather_to_root(lm["clustering"], b, rank, world)
+        ex = sharded_exact_bfs(g, rank, world, dev)
+        tot = {}
+        for k in ("sum_d", "sum_d2", "reach"):
+            t = torch.from_numpy(ex[k].astype(np.int64))
+            dist.all_reduce(t)
+            tot[k] = t.numpy()
+        if rank == 0:
+            ref_l = DeviceGraph(g).local_metrics()["clustering"]
+            ref_x = exact_bfs_all(g)
+            q.put(("ok", bool(np.array_equal(clus, ref_l, equal_nan=True)),
+                   all(bool(np.array_equal(tot[k], ref_x[k].astype(np.int64))) for k in tot)))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_widened_passes_shard_without_exchange(world):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    ps = [ctx.Process(target=_rank_widened, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(timeout=300)
+    for p in ps:
+        if p.is_alive():
+            p.kill()
+    res = q.get(timeout=10)
+    assert res[0] == "ok", res
+    assert all(p.exitcode == 0 for p in ps), [p.exitcode for p in ps]
+    assert res[1] and res[2]
