@@ -143,11 +143,21 @@ __global__ void __launch_bounds__(256) vis_rows_kernel(VisArgs a) {
             }
             *o = static_cast<uint8_t>(x);
           }
-          // emitted index j >= 1 -> column; its delta is 2 right after v itself
-          for (uint32_t j = 1 + lane; j < cnt; j += 32) {
-            const int cj = c_lo + static_cast<int>(j) + ((self_row && c_lo + static_cast<int>(j) >= cc) ? 1 : 0);
-            a.stream[pos + l0 + j - 1] = (self_row && cj == cc + 1 && cj - 2 >= c_lo) ? 2u : 1u;
+          // bytes [pos + l0, pos + l0 + cnt - 1): delta 1 everywhere except 2 right
+          // after v itself (when v has emitted cells on both sides); aligned words
+          // of 0x01010101 in the middle, single bytes at the ends.
+          const uint64_t b0 = pos + l0, len = cnt - 1u;
+          const uint64_t two = (self_row && cc > c_lo && cc < c_hi) ? b0 + (cc - c_lo - 1) : ~0ull;
+          const uint64_t mis = (4u - (b0 & 3u)) & 3u, head = len < mis ? len : mis;
+          const uint64_t nw = (len - head) / 4u, tail0 = b0 + head + 4u * nw;
+          if (lane < head) a.stream[b0 + lane] = (b0 + lane == two) ? 2u : 1u;
+          for (uint64_t k = lane; k < nw; k += 32) {
+            const uint64_t at = b0 + head + 4u * k;
+            uint32_t word = 0x01010101u;
+            if (two >= at && two < at + 4u) word += 1u << (8u * static_cast<uint32_t>(two - at));
+            *reinterpret_cast<uint32_t*>(a.stream + at) = word;
           }
+          if (lane < b0 + len - tail0) a.stream[tail0 + lane] = (tail0 + lane == two) ? 2u : 1u;
         }
         pos += l0 + cnt - 1;
         bytes += l0 + cnt - 1;
