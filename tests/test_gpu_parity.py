@@ -317,3 +317,13 @@ def test_gpu_cpp_facade_tool(oracle_best):
     line = [ln for ln in r.stdout.splitlines() if ln.startswith("mean MD")][0]
     assert f"iterations={ref['iterations']}" in r.stdout
     assert float(line.split("=")[1]) == pytest.approx(float(np.mean(md)), rel=1e-6)  # printed with %.6f
+
+
+def test_gpu_lockstep_c2_full_scale(oracle_best):
+    """BASELINE config C2 (212^2 grid, 60 obstacles, radius 44: 42,656 cells, 159 M edges,
+    9 iterations) bit-exact after every iteration against the compiled reference
+    primitives; C3 (236,196 cells, 4.79e9 edges) was checked the same way with
+    scripts/parity_at_scale.py (profiles/r01b_parity_c3_full.json)."""
+    g = CompressedCsr.synth_grid(212, 212, 60, 3, 10, 20261017, 44 * 44)
+    assert g.n == 42656
+    lockstep(g, 10, None, oracle_best)
