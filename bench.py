@@ -244,8 +244,9 @@ def pipeline_variant(args, P, device, hb_ref):
     r, c, k, a, b, seed, rad2, _ = CONFIGS[args.config]
     mask = grid_mask(r, c, k, a, b, seed)
     DeviceGraph.from_grid(grid_mask(16, 16, 0, 1, 1, 1), 9, device)  # warm the build kernels
-    out = {"input": f"{r}x{c} obstacle mask ({mask.size} B H2D)"}
-    for mode in ("interval", "dense"):
+    out = {"input": f"{r}x{c} obstacle mask ({mask.size} B H2D)",
+           "timing": "host wall clock per phase, best of 2 (synchronous C-ABI calls)"}
+    for mode in ("interval", "dense", "interval", "dense"):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         dg = DeviceGraph.from_grid(mask, rad2, device)
@@ -256,13 +257,21 @@ def pipeline_variant(args, P, device, hb_ref):
         met = h.metrics(dg.node_count_of_component(), dg.degrees())
         t3 = time.perf_counter()
         same = bool(np.array_equal(h.state().sum_d, hb_ref.state().sum_d))
-        out[mode] = {"build_s": t1 - t0, "hyperball_s": t2 - t1, "metrics_s": t3 - t2, "total_s": t3 - t0,
-                     "iterations": it, "sum_d_identical_to_uploaded_graph": same,
-                     "md_mean": float(np.nanmean(met["md"]))}
+        rec = {"build_s": t1 - t0, "hyperball_s": t2 - t1, "metrics_s": t3 - t2, "total_s": t3 - t0,
+               "iterations": it, "sum_d_identical_to_uploaded_graph": same,
+               "md_mean": float(np.nanmean(met["md"]))}
         if args.local:
             t4 = time.perf_counter()
             dg.local_metrics()
-            out[mode]["local_metrics_s"] = time.perf_counter() - t4
+            rec["local_metrics_s"] = time.perf_counter() - t4
+        if mode in out:  # keep the faster of the two runs per field (timings only)
+            prev = out[mode]
+            for k, v in rec.items():
+                if k.endswith("_s"):
+                    prev[k] = min(prev[k], v)
+            prev["sum_d_identical_to_uploaded_graph"] &= same
+        else:
+            out[mode] = rec
         del h, dg
     log(f"[bench] pipeline: {json.dumps(out)}")
     return out
