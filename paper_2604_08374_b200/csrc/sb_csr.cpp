@@ -749,15 +749,19 @@ int sb_depth_entropy(uint64_t n, const uint32_t* hist, uint32_t hist_cap, double
 // ---------------------------------------------------------------- CSV writer
 // cmd_analyze output: one row per node, NaN serialised "NaN",
 // doubles with 17 significant digits (round-trip exact, byte-deterministic).
-static void put_num(FILE* f, double x) {
-  if (std::isnan(x))
-    fputs("NaN", f);
-  else if (std::isinf(x))
-    fputs(x > 0 ? "inf" : "-inf", f);
-  else
-    fprintf(f, "%.17g", x);
+static void put_num(std::string& o, double x) {
+  if (std::isnan(x)) {
+    o += "NaN";
+  } else if (std::isinf(x)) {
+    o += x > 0 ? "inf" : "-inf";
+  } else {
+    char buf[32];
+    o.append(buf, static_cast<size_t>(snprintf(buf, sizeof buf, "%.17g", x)));
+  }
 }
 
+// Rows are formatted in parallel into per-block strings and written in order:
+// the bytes do not depend on the thread count.
 int sb_metrics_write_csv(const char* path, const sb_metric_table* t) {
   if (!path || !t) return cfail(SB_EINVAL, "sb_metrics_write_csv: NULL argument");
   FILE* f = fopen(path, "wb");
@@ -765,21 +769,34 @@ int sb_metrics_write_csv(const char* path, const sb_metric_table* t) {
   fputs("x,y,node_id,component_id,node_count,connectivity,visual_mean_depth,integration_hh,integration_tekl,"
         "integration_pv,control,controllability,clustering,entropy,rel_entropy,first_moment,second_moment\n", f);
   auto col = [](const double* c, uint64_t i) { return c ? c[i] : NAN; };
-  for (uint64_t i = 0; i < t->n; ++i) {
-    put_num(f, col(t->x, i));
-    fputc(',', f);
-    put_num(f, col(t->y, i));
-    fprintf(f, ",%llu,%u,%u,%u,", static_cast<unsigned long long>(t->node_id ? t->node_id[i] : i),
-            t->component_id ? t->component_id[i] : 0u, t->node_count ? t->node_count[i] : 0u,
-            t->connectivity ? t->connectivity[i] : 0u);
-    const double* cols[11] = {t->md, t->ihh, t->tekl, t->pv, t->control, t->controllability,
-                              t->clustering, t->entropy, t->rel_entropy, t->m1, t->m2};
-    for (int k = 0; k < 11; ++k) {
-      put_num(f, col(cols[k], i));
-      fputc(k == 10 ? '\n' : ',', f);
+  const double* cols[11] = {t->md, t->ihh, t->tekl, t->pv, t->control, t->controllability,
+                            t->clustering, t->entropy, t->rel_entropy, t->m1, t->m2};
+  const uint64_t blk = 256, nb = (t->n + blk - 1) / blk;  // parallel_for hands out >= 64 blocks per grab
+  std::vector<std::string> parts(nb);
+  parallel_for(nb, 0, [&](uint64_t b0, uint64_t b1) {
+    for (uint64_t b = b0; b < b1; ++b) {
+      std::string& o = parts[b];
+      o.reserve(blk * 280);
+      char buf[96];
+      for (uint64_t i = b * blk; i < std::min<uint64_t>(t->n, (b + 1) * blk); ++i) {
+        put_num(o, col(t->x, i));
+        o += ',';
+        put_num(o, col(t->y, i));
+        o.append(buf, static_cast<size_t>(snprintf(
+                          buf, sizeof buf, ",%llu,%u,%u,%u,",
+                          static_cast<unsigned long long>(t->node_id ? t->node_id[i] : i),
+                          t->component_id ? t->component_id[i] : 0u, t->node_count ? t->node_count[i] : 0u,
+                          t->connectivity ? t->connectivity[i] : 0u)));
+        for (int k = 0; k < 11; ++k) {
+          put_num(o, col(cols[k], i));
+          o += k == 10 ? '\n' : ',';
+        }
+      }
     }
-  }
-  const bool bad = ferror(f) != 0;
+  });
+  bool bad = false;
+  for (const auto& o : parts) bad |= fwrite(o.data(), 1, o.size(), f) != o.size();
+  bad |= ferror(f) != 0;
   if (fclose(f) != 0 || bad) return cfail(SB_ERUNTIME, "write error on %s", path);
   return SB_OK;
 }
