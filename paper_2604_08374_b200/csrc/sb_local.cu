@@ -205,10 +205,16 @@ __global__ void __launch_bounds__(256) local_kernel(LocalArgs a) {
     for (uint64_t r = r0; r < r1; ++r) {
       const uint32_t s = a.run_s[r], e = a.run_e[r];
       const uint64_t q0 = a.run_off[a.node_item[s]], q1 = a.run_off[a.node_item[e + 1]];
-      for (uint64_t q = q0 + threadIdx.x; q < q1; q += blockDim.x) {
-        const uint32_t cs = max(a.run_s[q], lo1), ce = min(a.run_e[q], hi1);
-        if (cs <= ce) among += rank1(rk, ce - lo1 + 1) - rank1(rk, cs - lo1);
+      const uint32_t* __restrict__ qs = a.run_s + q0;
+      const uint32_t* __restrict__ qe = a.run_e + q0;
+      const uint32_t cnt = static_cast<uint32_t>(q1 - q0);
+      uint32_t part = 0;  // < 2^32: at most the window size per slice
+      for (uint32_t k = threadIdx.x; k < cnt; k += 256) {
+        const uint32_t cs = max(qs[k], lo1), ce = min(qe[k], hi1);
+        const bool hit = cs <= ce;  // branch-free: an empty clip queries rank(0) twice
+        part += rank1(rk, hit ? ce - lo1 + 1 : 0u) - rank1(rk, hit ? cs - lo1 : 0u);
       }
+      among += part;
     }
 #pragma unroll
     for (int d = 16; d; d >>= 1) among += __shfl_xor_sync(FULL, among, d);

@@ -7,7 +7,7 @@ set -u
 export SB_SYNC_TIMEOUT_S=600 PYTHONUNBUFFERED=1
 what=${1:-all}
 mkdir -p gpurun_out
-run() { echo "== $*"; "$@"; echo "rc=$?"; }
+run() { echo "== $*" >> gpurun_out/evidence.log; "$@"; echo "rc=$? ($1 ${*: -1})" >> gpurun_out/evidence.log; }
 
 if [[ $what == tests || $what == all ]]; then
   run timeout 1500 python -u -m pytest tests -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; tail -3 gpurun_out/pytest_gpu.log
