@@ -508,7 +508,8 @@ __global__ void __launch_bounds__(256) run_index_kernel(RunIndexArgs a) {
 // registers, then runs are broadcast 4 at a time (8 sparse-table rows per
 // batch, tree-reduced).
 template <int P, bool OR>
-__device__ __forceinline__ void process_item_runs(const IntervalArgs& ia, uint64_t item, int slice, int lane) {
+__device__ __forceinline__ void process_item_runs(const IntervalArgs& ia, uint64_t item, int slice, int lane,
+                                                  const long long* lvl_off) {
   using G = Geo<P>;
   using IO = GrpIO<G::GB>;
   static_assert(G::SUB == 1, "interval mode maps one 512-byte slice per warp (p >= 10)");
@@ -521,8 +522,6 @@ __device__ __forceinline__ void process_item_runs(const IntervalArgs& ia, uint64
   const uint32_t nit = a.node_item[node + 1] - first;
   const uint64_t goff = static_cast<uint64_t>(slice) * G::SLICE_BYTES + static_cast<uint64_t>(gl) * G::GB;
   const uint8_t* curb = opaque(a.cur + goff);
-  const uint8_t* stb = curb + (ia.st - a.cur);
-  const uint64_t lvl = ia.n_global * G::ROW;
   Grp acc = (item == first) ? IO::ld(curb + v * G::ROW) : grp_zero();
   const uint64_t r0 = ia.run_off[item], r1 = ia.run_off[item + 1];
   const int K = ia.levels;
@@ -542,12 +541,12 @@ __device__ __forceinline__ void process_item_runs(const IntervalArgs& ia, uint64
         const uint32_t e = __shfl_sync(FULL, me, r);
         uint32_t L = e - s + 1;
         while (L >= (2u << K)) {  // longer than the table covers: peel 2^K blocks
-          combine<OR>(acc, IO::ld(stb + static_cast<uint64_t>(K - 1) * lvl + static_cast<uint64_t>(s) * G::ROW));
+          combine<OR>(acc, IO::ld(curb + lvl_off[K] + static_cast<uint64_t>(s) * G::ROW));
           s += 1u << K;
           L -= 1u << K;
         }
         const int k = 31 - __clz(L);
-        const uint8_t* lb = k == 0 ? curb : stb + static_cast<uint64_t>(k - 1) * lvl;
+        const uint8_t* lb = curb + lvl_off[k];  // level k's plane (k = 0: cur itself)
         x[2 * q] = IO::ld(lb + static_cast<uint64_t>(s) * G::ROW);
         x[2 * q + 1] = IO::ld(lb + static_cast<uint64_t>(e - (1u << k) + 1) * G::ROW);
       }
@@ -583,6 +582,13 @@ template <int P, bool OR>
 __global__ void __launch_bounds__(256, 4) union_interval_kernel(IntervalArgs ia) {
   using G = Geo<P>;
   __shared__ unsigned long long s_unit[2];
+  __shared__ long long s_lvl[12];  // byte offset of sparse-table level k from the cur plane
+  if (threadIdx.x < 12)
+    s_lvl[threadIdx.x] = threadIdx.x == 0 ? 0ll
+                                          : static_cast<long long>(ia.st - ia.u.cur) +
+                                                static_cast<long long>(threadIdx.x - 1) *
+                                                    static_cast<long long>(ia.n_global * G::ROW);
+  __syncthreads();
   const UnionArgs& a = ia.u;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -598,7 +604,7 @@ __global__ void __launch_bounds__(256, 4) union_interval_kernel(IntervalArgs ia)
     if (node < a.n_local) {
       const uint32_t first = a.node_item[node];
       if (q < a.node_item[node + 1] - first)
-        process_item_runs<P, OR>(ia, first + q, static_cast<int>(u % G::SLICES), lane);
+        process_item_runs<P, OR>(ia, first + q, static_cast<int>(u % G::SLICES), lane, s_lvl);
     }
   }
 }
