@@ -379,11 +379,13 @@ def main():
         log(f"[bench]   t={s['t']} union={s['union_ms']:.2f} ms est={s['estimate_ms']:.3f} ms "
             f"xchg={s['exchange_ms']:.3f} ms changed={s['changed_nodes']} max_inc={s['max_increase']:.3f}")
 
+    # passes executed (Alg. 1 stops one pass after the last change) vs last changing pass
+    last_changing = max_over_ranks(float(max([s["t"] for s in st if s["changed_nodes"] > 0], default=0)))
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * dev_s / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": workload_config(args, g, iters),
+        "config": dict(workload_config(args, g, iters), last_changing_pass=int(last_changing)),
         "hbm_gbs_algorithmic": bytes_iter * iters * args.steps / dev_s / 1e9,
         "end_to_end_s_device": dev_s / args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk, "unit": "GB/s", "frac": achieved / pk,
