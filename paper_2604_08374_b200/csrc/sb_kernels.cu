@@ -1,16 +1,22 @@
 // sb_kernels.cu -- sm_100a kernels of the HyperBall hot path.
 //
-//   sb_build_items   : validates the LEB128 delta-CSR once at upload and cuts
+//   build_items_kernel: validates the LEB128 delta-CSR once at upload and cuts
 //                      every row into work items of <= `chunk` neighbours
-//   sb_init          : hll_init: insert orig_id[v]
-//   sb_union   <P>   : fused decode-union (PAPER.md:469-475 replaced): warp per
-//                      work item, warp-cooperative LEB128 decode, 16-B coalesced
-//                      row gathers, bit-sliced register max, per-node changed flag
-//   sb_estimate<P>   : hll_cardinality + hll_accumulate:
+//   init_kernel<P>   : hll_init: insert orig_id[v]
+//   union_kernel<P>  : fused decode-union (PAPER.md:469-475 replaced): CTA tile
+//                      of 8 consecutive nodes x one work item each, warp-
+//                      cooperative LEB128 decode, 16-B coalesced row gathers,
+//                      bit-serial 9-way register max on bit-sliced rows, per-node
+//                      changed flag, optional P2P stores into peer replicas
+//   union_interval_kernel<P> + st_build_kernel<P> : the interval variant (runs of
+//                      consecutive ids folded through a per-iteration sparse table)
+//   run_index_kernel : runs of consecutive ids per work item, once per graph
+//   estimate_kernel<P>: hll_cardinality + hll_accumulate:
 //                      integer harmonic sum -> bit-exact estimate (hll.cpp:31-37),
 //                      sum_d/sum_d2 accumulation, global max increase
-//   sb_to_packed / sb_from_packed : export/import in the reference packed layout
-//   sb_metrics       : MD / IHH / Tekl / PV / moments
+//   exact_init / exact_count : exact mode (bitset rows, OR union)
+//   to_packed / from_packed : export/import in the reference packed layout
+//   metrics_kernel   : MD / IHH / Tekl / PV / moments
 #include <cstdio>
 #include <cstdlib>
 
@@ -506,7 +512,7 @@ __global__ void __launch_bounds__(256) run_index_kernel(RunIndexArgs a) {
 
 // Folds one work unit's runs: lane i stages run i of each 32-run chunk in
 // registers, then runs are broadcast 4 at a time (8 sparse-table rows per
-// batch, tree-reduced).
+// batch, folded by the bit-serial 9-way max, or OR in exact mode).
 template <int P, bool OR>
 __device__ __forceinline__ void process_item_runs(const IntervalArgs& ia, uint64_t item, int slice, int lane,
                                                   const long long* lvl_off) {
