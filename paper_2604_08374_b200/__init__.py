@@ -10,11 +10,11 @@ from .hyperball import (Comm, DeviceGraph, HllParams, HyperBall, HyperBallState,
                         check_convergence, run)
 from . import metrics  # noqa: F401
 from .exact import ExactBfs, depth_entropy, exact_bfs_all, neighbourhood_function  # noqa: F401
-from .analyze import analyze, metrics_from_sums, write_csv  # noqa: F401
+from .analyze import analyze, bench_depths, metrics_from_sums, validate_graph, write_csv  # noqa: F401
 from . import validate  # noqa: F401
 
 __all__ = ["CompressedCsr", "DeviceGraph", "HllParams", "HyperBall", "HyperBallState", "Comm",
            "check_convergence", "run", "metrics", "leb128_encode", "leb128_decode",
            "encode_neighbor_row", "lib", "ExactBfs",
            "exact_bfs_all", "depth_entropy", "neighbourhood_function", "analyze", "metrics_from_sums", "write_csv",
-           "validate", "grid_mask"]
+           "validate", "grid_mask", "bench_depths", "validate_graph"]

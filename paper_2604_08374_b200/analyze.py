@@ -105,3 +105,50 @@ def write_csv(path: str, cols: dict, n: int) -> None:
     for field in ("node_id", "component_id", "node_count", "connectivity"):
         put(field, field, np.uint32)
     check(lib().sb_metrics_write_csv(path.encode(), C.byref(t)))
+
+
+BENCH_HEADER = ("depth", "iterations", "last_changing_pass", "bfs_seconds", "union_ms", "mean_md", "max_increase")
+
+
+def bench_depths(csr: CompressedCsr, depths=(3, 5, 10, None), p: int = 10, out: str | None = None,
+                 device: int = 0, interval: bool = False) -> list[dict]:
+    """cmd_bench (paper Table 3 shape): one HyperBall run per depth limit
+    (None = unlimited) -> depth, iterations, BFS time (device, summed per-iteration
+    kernel + exchange time), mean MD as the accuracy proxy; optional CSV."""
+    dg = DeviceGraph(csr, device)
+    nv = np.ascontiguousarray(csr.node_count_of_component(), np.uint32)
+    deg = np.ascontiguousarray(csr.degrees, np.uint32)
+    rows = []
+    for d in depths:
+        hb = HyperBall(dg, p, d, interval=interval)
+        hb.run()  # warm
+        hb.reset()
+        it = hb.run()
+        st = hb.stats()
+        m = hb.metrics(nv, deg)
+        rows.append(dict(depth="unlimited" if d is None else int(d), iterations=it,
+                         last_changing_pass=max([s["t"] for s in st if s["changed_nodes"] > 0], default=0),
+                         bfs_seconds=sum(s["step_ms"] for s in st) / 1e3,
+                         union_ms=sum(s["union_ms"] for s in st), mean_md=float(np.nanmean(m["md"])),
+                         max_increase=st[-1]["max_increase"] if st else 0.0))
+    if out is not None:
+        import csv
+        with open(out, "w", newline="") as f:
+            w = csv.DictWriter(f, fieldnames=list(BENCH_HEADER))
+            w.writeheader()
+            for r in rows:
+                w.writerow(r)
+    return rows
+
+
+def validate_graph(csr: CompressedCsr, p: int = 10, depth_limit: int | None = None, out: str | None = None,
+                   device: int = 0) -> list[dict]:
+    """cmd_validate: both modes on the same graph, compare() report
+    (Pearson r, Spearman rho, median relative error per metric)."""
+    from . import validate
+    hb = analyze(csr, p, depth_limit, "hyperball", device=device, local=False)
+    ex = analyze(csr, p, depth_limit, "exact", device=device, local=False)
+    rows = validate.compare(hb, ex)
+    if out is not None:
+        validate.write_report(out, rows)
+    return rows

@@ -302,3 +302,30 @@ def test_gpu_exact_argument_errors():
     hist = np.zeros(10, np.uint32)
     with pytest.raises(ValueError):  # histogram capacity must exceed the max depth (9)
         check(lib().sb_exact_read(x._h, None, None, None, hist.ctypes.data, 1))
+
+
+@pytest.mark.gpu
+def test_gpu_cmd_bench_depth_sweep(tmp_path):
+    """cmd_bench: depth sweep on a diameter-8 graph; iterations follow
+    min(d, D + 1) (Alg. 1 observes convergence one pass after the last change) and the
+    BFS time grows with depth (paper Table 3 shape)."""
+    from paper_2604_08374_b200 import bench_depths
+    g = CompressedCsr.synth_grid(5, 5, 0, 1, 1, 1, 1)  # 4-neighbour 5x5 grid: diameter 8
+    out = tmp_path / "bench.csv"
+    rows = bench_depths(g, (3, 5, 10, None), out=str(out))
+    assert [r["iterations"] for r in rows] == [3, 5, 9, 9]
+    assert [r["last_changing_pass"] for r in rows] == [3, 5, 8, 8]  # the SPEC's [3, 5, 8, 8]
+    assert rows[0]["union_ms"] < rows[-1]["union_ms"]
+    lines = out.read_text().splitlines()
+    assert lines[0] == "depth,iterations,last_changing_pass,bfs_seconds,union_ms,mean_md,max_increase"
+    assert len(lines) == 5 and lines[-1].startswith("unlimited,9,8,")
+
+
+@pytest.mark.gpu
+def test_gpu_cmd_validate_report(tmp_path):
+    from paper_2604_08374_b200 import validate_graph
+    g = CompressedCsr.synth_grid(50, 50, 20, 2, 7, 100, 0)
+    rows = validate_graph(g, 12, out=str(tmp_path / "v.csv"))
+    md = {r["metric"]: r for r in rows}["md"]
+    assert md["pearson_r"] >= 0.995 and md["n"] == int((g.node_count_of_component() >= 2).sum())  # finite pairs
+    assert (tmp_path / "v.csv").read_text().startswith("metric,pearson_r,spearman_rho,median_rel_err,n")
