@@ -329,3 +329,25 @@ def test_gpu_cmd_validate_report(tmp_path):
     md = {r["metric"]: r for r in rows}["md"]
     assert md["pearson_r"] >= 0.995 and md["n"] == int((g.node_count_of_component() >= 2).sum())  # finite pairs
     assert (tmp_path / "v.csv").read_text().startswith("metric,pearson_r,spearman_rho,median_rel_err,n")
+
+
+@pytest.mark.gpu
+def test_gpu_tiny_graphs_through_every_entry_point(oracle_port):
+    """1-node, 2-node and edgeless graphs through HyperBall (all modes), exact BFS,
+    local metrics, analyze and the device grid build."""
+    from paper_2604_08374_b200 import grid_mask
+    for adj in ([[]], [[1], [0]], [[], [], []]):
+        g = CompressedCsr.from_adjacency(adj)
+        for kw in ({}, {"skip_unchanged": True}, {"interval": True}):
+            hb = HyperBall(g, 10, None, **kw)
+            assert hb.run() >= 1
+        ex = exact_bfs_all(g)
+        rx = oracle_port.exact_bfs(g)
+        assert np.array_equal(ex["sum_d"], rx["sum_d"]) and np.array_equal(ex["reach"], rx["reach"])
+        lm, rl = DeviceGraph(g).local_metrics(), oracle_port.local_metrics(g)
+        for k in rl:
+            assert np.array_equal(lm[k], rl[k], equal_nan=lm[k].dtype.kind == "f"), k
+        cols = analyze(g, 10, None, "exact")
+        assert cols["md"].shape == (g.n,)
+    dg = DeviceGraph.from_grid(grid_mask(1, 1), 0)
+    assert dg.n == 1 and HyperBall(dg, 10, None).run() == 1
