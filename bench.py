@@ -482,6 +482,8 @@ def main():
         try:
             line["cpu_baseline"] = run_cpu(g, args.p, args.cpu_sample_s, os.cpu_count() or 1)
             line["cpu_baseline"].pop("seconds", None)
+            one = run_cpu(g, args.p, min(5.0, args.cpu_sample_s), 1)  # per-core figure
+            line["cpu_baseline"]["per_core"] = {"value": one["value"], "cores": 1, "sample": one["sample"]}
         except Exception as e:  # the baseline is reported, never required
             line["cpu_baseline"] = {"value": None, "error": repr(e)}
     if rank == 0:
