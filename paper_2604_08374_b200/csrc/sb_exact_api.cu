@@ -215,15 +215,27 @@ int sb_local_metrics(sb_graph* g, uint64_t v0, uint64_t v1, double* control, dou
   if (rc) return rc;
   const uint64_t n = g->n, nl = v1 - v0;
   if (nl == 0) return SB_OK;
-  // |B(v, 2)| for every node: two OR-union iterations per 4096-source block
+  // |N2(v)|: depth-2 exact BFS over every source block (cost ~ blocks x runs, best
+  // for dense graphs) or per-node 2-hop bitmaps (cost ~ sum_w deg(w) runs(w),
+  // best for large sparse graphs).  Measured C3 rates: 62 ps per row-pair of
+  // the BFS, ~2.6 ps per range-OR -> bitmaps win when avg degree < 48 x blocks.
+  const uint64_t blocks = (n + 4095) / 4096;
+  bool n2_bitmap = static_cast<double>(g->edges_local) / static_cast<double>(n) < 48.0 * static_cast<double>(blocks);
+  if (const char* e = getenv("SB_LOCAL_N2")) {  // test / A-B override: "bfs" or "bitmap"
+    if (!strcmp(e, "bfs")) n2_bitmap = false;
+    if (!strcmp(e, "bitmap")) n2_bitmap = true;
+  }
   sb_exact* x = nullptr;
-  rc = sb_exact_create(g, 12, 2, SB_HB_INTERVAL, &x);
-  if (rc) return rc;
-  std::unique_ptr<sb_exact, void (*)(sb_exact*)> xg(x, sb_exact_destroy);
-  rc = sb_exact_run(x, 0, n, nullptr);
-  if (rc) return rc;
-  // [span_lo N | span_hi N | max 1] u32, [control | ctrl | clus] f64 nl, [among | n2 | work] u64
-  const uint64_t u32_words = 2 * n + 1;
+  std::unique_ptr<sb_exact, void (*)(sb_exact*)> xg(nullptr, sb_exact_destroy);
+  if (!n2_bitmap) {
+    rc = sb_exact_create(g, 12, 2, SB_HB_INTERVAL, &x);
+    if (rc) return rc;
+    xg.reset(x);
+    rc = sb_exact_run(x, 0, n, nullptr);
+    if (rc) return rc;
+  }
+  // [span_lo N | span_hi N | lo2 nl | hi2 nl | max 2] u32, [control | ctrl | clus] f64 nl, [among | n2 | work] u64
+  const uint64_t u32_words = 2 * n + 2 * nl + 2;
   const uint64_t bytes = ((u32_words * 4 + 7) & ~7ull) + 5 * nl * 8 + 8;
   uint8_t* blk = nullptr;
   CK(cudaMalloc(&blk, bytes));
@@ -242,11 +254,13 @@ int sb_local_metrics(sb_graph* g, uint64_t v0, uint64_t v1, double* control, dou
   a.run_off = g->d_run_off;
   a.run_s = g->d_run_s;
   a.run_e = g->d_run_e;
-  a.reach2 = x->d_reach;
+  a.reach2 = n2_bitmap ? nullptr : x->d_reach;
   uint32_t* u = reinterpret_cast<uint32_t*>(blk);
   a.span_lo = u;
   a.span_hi = u + n;
-  a.max_words = u + 2 * n;
+  a.lo2 = n2_bitmap ? u + 2 * n : nullptr;
+  a.hi2 = n2_bitmap ? u + 2 * n + nl : nullptr;
+  a.max_words = u + 2 * n + 2 * nl;
   double* f = reinterpret_cast<double*>(blk + ((u32_words * 4 + 7) & ~7ull));
   a.control = f;
   a.controllability = f + nl;
@@ -254,23 +268,24 @@ int sb_local_metrics(sb_graph* g, uint64_t v0, uint64_t v1, double* control, dou
   a.edges_among = reinterpret_cast<unsigned long long*>(f + 3 * nl);
   a.n2 = a.edges_among + nl;
   a.work = a.n2 + nl;
-  CK(cudaMemsetAsync(a.max_words, 0, 4, 0));
+  CK(cudaMemsetAsync(a.max_words, 0, 8, 0));
   CK(cudaMemsetAsync(a.work, 0, 8, 0));
   CK(sb::launch_local_spans(a, 0));
-  unsigned int mw = 0;
-  CK(cudaMemcpy(&mw, a.max_words, 4, cudaMemcpyDeviceToHost));
-  a.w1_words = std::max(mw, 1u);
-  a.stride_words = 2ull * (a.w1_words + 1);
+  unsigned int mw[2] = {0, 0};
+  CK(cudaMemcpy(mw, a.max_words, 8, cudaMemcpyDeviceToHost));
+  a.w1_words = std::max(mw[0], 1u);
+  a.stride_words = 2ull * (a.w1_words + 1) + (n2_bitmap ? std::max(mw[1], 1u) : 0u);
+  a.stride_words = (a.stride_words + 3) & ~3ull;  // 16-B aligned per-CTA regions (uint2 rank table)
   // SB_LOCAL_GLOBAL=1 forces the global-scratch bitmaps (test hook for wide windows)
   const char* force = getenv("SB_LOCAL_GLOBAL");
   const bool smem = a.stride_words * 4 <= sb::local_smem_limit() && !(force && atoi(force));
   if (!smem) {
     int grid = 0;
-    CK(sb::launch_local(a, false, &grid, 0));
+    CK(sb::launch_local(a, false, n2_bitmap, &grid, 0));
     CK(cudaMalloc(&scratch, static_cast<uint64_t>(grid) * a.stride_words * 4));
     a.scratch = scratch;
   }
-  CK(sb::launch_local(a, smem, nullptr, 0));
+  CK(sb::launch_local(a, smem, n2_bitmap, nullptr, 0));
   CK(sync_stream(0));
   if (control) CK(cudaMemcpy(control, a.control, nl * 8, cudaMemcpyDeviceToHost));
   if (controllability) CK(cudaMemcpy(controllability, a.controllability, nl * 8, cudaMemcpyDeviceToHost));

@@ -152,22 +152,24 @@ struct LocalArgs {
   const uint32_t* run_e;
   uint32_t* span_lo;           // N: first neighbour id (0xffffffff if none)
   uint32_t* span_hi;           // N: last neighbour id
-  const uint32_t* reach2;      // N: |B(v, 2)| from the exact BFS at depth 2
-  unsigned int* max_words;     // max 1-hop window words
+  const uint32_t* reach2;      // N: |B(v, 2)| from the exact BFS at depth 2 (BFS mode)
+  uint32_t* lo2;               // [v1 - v0]: 2-hop id window (bitmap mode; NULL in BFS mode)
+  uint32_t* hi2;
+  unsigned int* max_words;     // [0] max 1-hop window words, [1] max 2-hop window words
   double* control;             // [v1 - v0]
   double* controllability;
   double* clustering;
   unsigned long long* edges_among;  // optional
   unsigned long long* n2;           // optional
   uint32_t* scratch;           // global bitmaps (non-smem path): grid * stride_words
-  uint64_t stride_words;       // 2 * (w1_words + 1)
+  uint64_t stride_words;       // 2 * (w1_words + 1) [+ w2_words in bitmap mode]
   uint32_t w1_words;
   unsigned long long* work;
 };
 
 cudaError_t launch_local_spans(const LocalArgs& a, cudaStream_t s);
 // grid_out != NULL: only returns the grid the launch would use.
-cudaError_t launch_local(const LocalArgs& a, bool smem, int* grid_out, cudaStream_t s);
+cudaError_t launch_local(const LocalArgs& a, bool smem, bool n2_bitmap, int* grid_out, cudaStream_t s);
 size_t local_smem_limit();
 
 cudaError_t launch_build_items(const BuildArgs& a, cudaStream_t s);

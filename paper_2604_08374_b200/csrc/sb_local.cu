@@ -105,10 +105,15 @@ __global__ void __launch_bounds__(256) ctrl_kernel(LocalArgs a) {
     node_runs(a, v, r0, r1);
     U128 acc{0ull, 0ull};
     bool zero_deg = false;
+    uint32_t lo = a.span_lo[v], hi = a.span_hi[v];  // 2-hop window (bitmap mode)
     for (uint64_t r = r0; r < r1; ++r) {
       const uint32_t s = a.run_s[r], e = a.run_e[r];
       for (uint64_t w = s + lane; w <= e; w += 32) {
         const uint32_t dw = a.degrees[w];
+        if (a.lo2) {
+          lo = min(lo, a.span_lo[w]);
+          hi = max(hi, a.span_hi[w]);
+        }
         if (dw == 0) {
           zero_deg = true;  // only in an asymmetric graph: 1/0 = +inf
         } else {
@@ -118,10 +123,38 @@ __global__ void __launch_bounds__(256) ctrl_kernel(LocalArgs a) {
     }
     acc = warp_sum128(acc);
     zero_deg = __any_sync(FULL, zero_deg);
+    if (a.lo2) {
+#pragma unroll
+      for (int d = 16; d; d >>= 1) {
+        lo = min(lo, __shfl_xor_sync(FULL, lo, d));
+        hi = max(hi, __shfl_xor_sync(FULL, hi, d));
+      }
+    }
     if (lane == 0) {
       a.control[v - a.v0] = zero_deg ? INFINITY : fixed96_to_double(acc);
-      if (r1 > r0) atomicMax(a.max_words, (a.span_hi[v] - a.span_lo[v]) / 32 + 1);
+      if (r1 > r0) {
+        atomicMax(a.max_words, (a.span_hi[v] - a.span_lo[v]) / 32 + 1);
+        if (a.lo2) {
+          a.lo2[v - a.v0] = lo;
+          a.hi2[v - a.v0] = hi;
+          atomicMax(a.max_words + 1, (hi - lo) / 32 + 1);
+        }
+      }
     }
+  }
+}
+
+// Sets bits [s, e] (relative to the window) of bm.  Interior words are plain
+// all-ones stores (any concurrent OR of a subset leaves them all-ones).
+__device__ __forceinline__ void range_set(uint32_t* bm, uint32_t s, uint32_t e) {
+  const uint32_t ws = s >> 5, we = e >> 5;
+  const uint32_t ms = 0xffffffffu << (s & 31), me = 0xffffffffu >> (31 - (e & 31));
+  if (ws == we) {
+    atomicOr(bm + ws, ms & me);
+  } else {
+    atomicOr(bm + ws, ms);
+    for (uint32_t w = ws + 1; w < we; ++w) bm[w] = 0xffffffffu;
+    atomicOr(bm + we, me);
   }
 }
 
@@ -132,14 +165,18 @@ __device__ __forceinline__ uint32_t rank1(const uint2* rk, uint32_t i) {
   return x.x + __popc(x.y & ((1u << (i & 31)) - 1u));
 }
 
-template <bool SMEM>
+// N2BM: |N2(v)| from a per-node 2-hop bitmap (range-OR of every run of every
+// N(w) over the 2-hop window) instead of the depth-2 BFS counts in reach2 --
+// linear in sum_w deg(w) runs(w), the cheaper choice for large, low-degree graphs.
+template <bool SMEM, bool N2BM>
 __global__ void __launch_bounds__(256) local_kernel(LocalArgs a) {
   extern __shared__ uint2 dyn_s[];
   __shared__ unsigned long long s_node;
-  __shared__ unsigned long long s_red[8];
+  __shared__ unsigned long long s_red[8], s_reach[8];
   __shared__ uint32_t s_scan[8];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint2* rk = SMEM ? dyn_s : reinterpret_cast<uint2*>(a.scratch + blockIdx.x * a.stride_words);  // w1 + 1
+  uint32_t* bm2 = reinterpret_cast<uint32_t*>(rk + a.w1_words + 1);  // N2BM: w2 words
   for (;;) {
     if (threadIdx.x == 0) s_node = atomicAdd(a.work, 1ull);
     __syncthreads();
@@ -161,7 +198,11 @@ __global__ void __launch_bounds__(256) local_kernel(LocalArgs a) {
     }
     const uint32_t lo1 = a.span_lo[v], hi1 = a.span_hi[v];
     const uint32_t n1w = (hi1 - lo1) / 32 + 1;
+    const uint32_t lo2 = N2BM ? a.lo2[i] : 0u, hi2 = N2BM ? a.hi2[i] : 0u;
+    const uint32_t n2w = N2BM ? (hi2 - lo2) / 32 + 1 : 0u;
     for (uint32_t k = threadIdx.x; k <= n1w; k += blockDim.x) rk[k] = make_uint2(0u, 0u);
+    if (N2BM)
+      for (uint32_t k = threadIdx.x; k < n2w; k += blockDim.x) bm2[k] = 0u;
     __syncthreads();
     for (uint64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {  // runs of N(v) are disjoint
       const uint32_t s = a.run_s[r] - lo1, e = a.run_e[r] - lo1;
@@ -174,6 +215,7 @@ __global__ void __launch_bounds__(256) local_kernel(LocalArgs a) {
         for (uint32_t w = ws + 1; w < we; ++w) rk[w].y = 0xffffffffu;  // all-ones is OR-stable
         atomicOr(&rk[we].y, me);
       }
+      if (N2BM) range_set(bm2, s + lo1 - lo2, e + lo1 - lo2);  // N(v) itself is in N2(v)
     }
     __syncthreads();
     // exclusive prefix popcount of the words [0, n1w]
@@ -210,20 +252,39 @@ __global__ void __launch_bounds__(256) local_kernel(LocalArgs a) {
       const uint32_t cnt = static_cast<uint32_t>(q1 - q0);
       uint32_t part = 0;  // < 2^32: at most the window size per slice
       for (uint32_t k = threadIdx.x; k < cnt; k += 256) {
-        const uint32_t cs = max(qs[k], lo1), ce = min(qe[k], hi1);
+        const uint32_t qsk = qs[k], qek = qe[k];
+        const uint32_t cs = max(qsk, lo1), ce = min(qek, hi1);
         const bool hit = cs <= ce;  // branch-free: an empty clip queries rank(0) twice
         part += rank1(rk, hit ? ce - lo1 + 1 : 0u) - rank1(rk, hit ? cs - lo1 : 0u);
+        if (N2BM) range_set(bm2, qsk - lo2, qek - lo2);
       }
       among += part;
     }
+    unsigned long long reach = 0;
+    if (N2BM) {
+      __syncthreads();
+      for (uint32_t k = threadIdx.x; k < n2w; k += blockDim.x) reach += __popc(bm2[k]);
+#pragma unroll
+      for (int d = 16; d; d >>= 1) reach += __shfl_xor_sync(FULL, reach, d);
+    }
 #pragma unroll
     for (int d = 16; d; d >>= 1) among += __shfl_xor_sync(FULL, among, d);
-    if (lane == 0) s_red[warp] = among;
+    if (lane == 0) {
+      s_red[warp] = among;
+      s_reach[warp] = reach;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
-      unsigned long long tri = 0;
-      for (int q = 0; q < 8; ++q) tri += s_red[q];
-      const unsigned long long n2 = a.reach2[v] - 1ull;  // |B(v, 2)| minus v itself
+      unsigned long long tri = 0, n2 = 0;
+      for (int q = 0; q < 8; ++q) {
+        tri += s_red[q];
+        n2 += s_reach[q];
+      }
+      if (N2BM) {  // v itself is not in N2(v)
+        if (v >= lo2 && v <= hi2 && ((bm2[(v - lo2) >> 5] >> ((v - lo2) & 31)) & 1u)) --n2;
+      } else {
+        n2 = a.reach2[v] - 1ull;  // |B(v, 2)| minus v itself
+      }
       a.controllability[i] = n2 ? __ddiv_rn(static_cast<double>(deg), static_cast<double>(n2)) : NAN;
       a.clustering[i] = deg >= 2 ? __ddiv_rn(static_cast<double>(tri),
                                              __dmul_rn(static_cast<double>(deg), static_cast<double>(deg - 1)))
@@ -250,27 +311,28 @@ cudaError_t launch_local_spans(const LocalArgs& a, cudaStream_t s) {
 
 size_t local_smem_limit() { return 200 * 1024; }
 
-cudaError_t launch_local(const LocalArgs& a, bool smem, int* grid_out, cudaStream_t s) {
-  const size_t bytes = smem ? a.stride_words * 4 : 0;
+template <bool SMEM, bool N2BM>
+static cudaError_t launch_local_t(const LocalArgs& a, int* grid_out, cudaStream_t s) {
+  const size_t bytes = SMEM ? a.stride_words * 4 : 0;
   int per = 0;
-  if (smem) {
-    cudaError_t e = cudaFuncSetAttribute(local_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (SMEM) {
+    cudaError_t e = cudaFuncSetAttribute(local_kernel<SMEM, N2BM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(bytes));
     if (e != cudaSuccess) return e;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, local_kernel<true>, 256, bytes);
-  } else {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, local_kernel<false>, 256, 0);
   }
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, local_kernel<SMEM, N2BM>, 256, bytes);
   const int g = sm_count() * (per < 1 ? 1 : per);
   if (grid_out) {  // query only (global scratch sizing)
     *grid_out = g;
     return cudaSuccess;
   }
-  if (smem)
-    local_kernel<true><<<g, 256, bytes, s>>>(a);
-  else
-    local_kernel<false><<<g, 256, 0, s>>>(a);
+  local_kernel<SMEM, N2BM><<<g, 256, bytes, s>>>(a);
   return cudaGetLastError();
+}
+
+cudaError_t launch_local(const LocalArgs& a, bool smem, bool n2_bitmap, int* grid_out, cudaStream_t s) {
+  if (smem) return n2_bitmap ? launch_local_t<true, true>(a, grid_out, s) : launch_local_t<true, false>(a, grid_out, s);
+  return n2_bitmap ? launch_local_t<false, true>(a, grid_out, s) : launch_local_t<false, false>(a, grid_out, s);
 }
 
 }  // namespace sb

@@ -130,18 +130,25 @@ def test_gpu_local_metrics_needs_full_graph():
 
 
 @pytest.mark.gpu
-def test_gpu_local_metrics_global_scratch_path():
-    """SB_LOCAL_GLOBAL=1 forces the per-CTA global bitmaps (wide-window graphs)."""
+@pytest.mark.parametrize("n2", ["bfs", "bitmap"])
+@pytest.mark.parametrize("scratch", ["smem", "global"])
+def test_gpu_local_metrics_both_n2_methods(n2, scratch):
+    """|N2(v)| from the depth-2 BFS or from per-node 2-hop bitmaps (SB_LOCAL_N2), with the
+    bitmaps in shared memory or in the per-CTA global scratch (SB_LOCAL_GLOBAL=1)."""
     code = (
         "import sys; sys.path.insert(0, %r)\n"
         "import numpy as np, oracle\n"
         "from paper_2604_08374_b200 import CompressedCsr, DeviceGraph\n"
-        "g = CompressedCsr.synth_grid(32, 32, 8, 2, 5, 20261017, 0)\n"
-        "ref = oracle.port().local_metrics(g); got = DeviceGraph(g).local_metrics()\n"
-        "assert all(np.array_equal(got[k], ref[k], equal_nan=got[k].dtype.kind == 'f') for k in ref)\n"
+        "from tests.test_local_metrics import random_graph\n"
+        "for g in (CompressedCsr.synth_grid(32, 32, 8, 2, 5, 20261017, 0),\n"
+        "          CompressedCsr.synth_grid(60, 70, 40, 1, 5, 9, 7 * 7), random_graph(120, 0.05, 3)[1],\n"
+        "          CompressedCsr.from_adjacency([[1], [0, 2], [1], [], [5], [4], []])):\n"
+        "    ref = oracle.port().local_metrics(g); got = DeviceGraph(g).local_metrics()\n"
+        "    assert all(np.array_equal(got[k], ref[k], equal_nan=got[k].dtype.kind == 'f') for k in ref)\n"
         "print('ok')\n" % ROOT)
-    env = dict(os.environ, SB_LOCAL_GLOBAL="1")
-    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    env = dict(os.environ, SB_LOCAL_N2=n2, SB_LOCAL_GLOBAL="1" if scratch == "global" else "0")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300,
+                       cwd=ROOT)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
 
 
