@@ -1,8 +1,10 @@
-"""City-scale run (paper §5: 2.7 M-cell Valdivia analysis on one GPU): a
-1650 x 1650 raster (2.72 M cells) with building-like rectangular obstacles,
-visibility radius R cells, built on the device (sb_graph_build_grid) and
-analysed with HyperBall (interval and dense) at p = 10, plus exact local
-metrics on a node sample.  Prints one JSON object with the timings."""
+"""City-scale run (paper §5: 2.7 M-cell Valdivia analysis on one GPU):
+usage: python scripts/city_scale.py SIDE RADIUS RECTS [DEPTH]
+a SIDE x SIDE raster with RECTS building-like rectangular obstacles (4-16
+cells), visibility radius RADIUS cells, built on the device
+(sb_graph_build_grid), analysed with HyperBall (interval and dense) at p = 10
+to DEPTH (0 = convergence), plus exact local metrics for every node.
+Prints one JSON object with the timings."""
 import json
 import os
 import sys
@@ -16,17 +18,19 @@ from paper_2604_08374_b200 import DeviceGraph, HyperBall, grid_mask  # noqa: E40
 side = int(sys.argv[1]) if len(sys.argv) > 1 else 1650
 R = int(sys.argv[2]) if len(sys.argv) > 2 else 30
 rects = int(sys.argv[3]) if len(sys.argv) > 3 else 12000
+depth = int(sys.argv[4]) if len(sys.argv) > 4 and int(sys.argv[4]) > 0 else None
 mask = grid_mask(side, side, rects, 4, 16, 20261017)
 DeviceGraph.from_grid(grid_mask(8, 8), 4)  # context + module load
 t0 = time.perf_counter()
 dg = DeviceGraph.from_grid(mask, R * R)
 t_build = time.perf_counter() - t0
 nv = dg.node_count_of_component()
-out = {"grid": f"{side}x{side}", "blocked_cells": int(mask.sum()), "radius_cells": R, "nodes": dg.n,
+out = {"grid": f"{side}x{side}", "blocked_cells": int(mask.sum()), "radius_cells": R, "depth_limit": depth,
+       "nodes": dg.n,
        "edges": dg.edges, "stream_bytes": dg.stream_bytes_local, "components": int(len(np.unique(nv))),
        "build_s": t_build}
 for mode in ("interval", "dense"):
-    hb = HyperBall(dg, 10, None, interval=(mode == "interval"))
+    hb = HyperBall(dg, 10, depth, interval=(mode == "interval"))
     t0 = time.perf_counter()
     it = hb.run()
     t_run = time.perf_counter() - t0
