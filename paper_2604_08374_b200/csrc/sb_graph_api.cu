@@ -309,8 +309,12 @@ int sb_graph_build_grid(uint32_t rows, uint32_t cols, const uint8_t* blocked, ui
   g->cols = cols;
   uint8_t* d_mask = nullptr;
   uint32_t *d_pref = nullptr, *d_scan = nullptr, *d_noc = nullptr, *d_tmp = nullptr;
-  uint64_t* d_bytes = nullptr;
-  auto cleanup = [&] { dfree(d_mask); dfree(d_pref); dfree(d_scan); dfree(d_noc); dfree(d_tmp); dfree(d_bytes); };
+  uint64_t *d_bytes = nullptr, *d_steps = nullptr, *d_stepoff = nullptr;
+  uint32_t* d_masks = nullptr;
+  auto cleanup = [&] {
+    dfree(d_mask); dfree(d_pref); dfree(d_scan); dfree(d_noc); dfree(d_tmp); dfree(d_bytes);
+    dfree(d_steps); dfree(d_stepoff); dfree(d_masks);
+  };
   auto bail = [&](int rc) { cleanup(); delete g; return rc; };
 #define BK(x)                                                 \
   do {                                                        \
@@ -349,6 +353,24 @@ int sb_graph_build_grid(uint32_t rows, uint32_t cols, const uint8_t* blocked, ui
   } else {
     a.R = std::max(rows, cols);
   }
+  // Line-of-sight results of the count pass are kept (one mask word per warp
+  // step) so the write pass does not walk them again; skipped if HBM is short.
+  if (cudaMalloc(&d_steps, (n + 1) * 8) == cudaSuccess && cudaMalloc(&d_stepoff, (n + 1) * 8) == cudaSuccess) {
+    BK(cudaMemsetAsync(d_steps + n, 0, 8, s));
+    BK(sb::launch_vis_steps(a, d_steps, s));
+    BK(sb::launch_scan_u64(d_steps, d_stepoff, n + 1, s));
+    uint64_t words = 0;
+    BK(cudaMemcpy(&words, d_stepoff + n, 8, cudaMemcpyDeviceToHost));
+    if (cudaMalloc(&d_masks, std::max<uint64_t>(words, 1) * 4) == cudaSuccess) {
+      a.masks = d_masks;
+      a.step_off = d_stepoff;
+    } else {
+      cudaGetLastError();  // clear the allocation failure; the write pass recomputes instead
+    }
+  } else {
+    cudaGetLastError();
+  }
+  auto free_masks = [&] { dfree(d_masks); dfree(d_steps); dfree(d_stepoff); a.masks = nullptr; a.step_off = nullptr; };
   BK(cudaMalloc(&g->d_deg, n * 4));
   BK(cudaMalloc(&d_bytes, (n + 1) * 8));
   BK(cudaMemsetAsync(d_bytes + n, 0, 8, s));
@@ -365,6 +387,8 @@ int sb_graph_build_grid(uint32_t rows, uint32_t cols, const uint8_t* blocked, ui
   a.offsets = g->d_rowoff;
   a.stream = g->d_stream;
   BK(sb::launch_vis_rows(a, true, s));
+  BK(cudaStreamSynchronize(s));
+  free_masks();
   // components (the 2n scratch doubles as the union-find parent array + ranks)
   BK(cudaMalloc(&d_tmp, 3 * n * 4));
   BK(cudaMalloc(&g->d_comp, n * 4));

@@ -122,12 +122,15 @@ struct VisArgs {
   const uint64_t* offsets;     // pass 2
   uint8_t* stream;             // pass 2
   uint32_t* parent;            // components
+  uint32_t* masks;             // per-warp-step visibility masks (NULL: recompute in the write pass)
+  const uint64_t* step_off;    // first mask word per node (n + 1)
 };
 
 cudaError_t launch_vis_prepare(VisArgs& a, uint32_t* pref, uint32_t* tmp_scan, uint64_t* n_out, cudaStream_t s);
 cudaError_t launch_vis_maps(const VisArgs& a, const uint32_t* scan, uint32_t* node_of_cell, uint32_t* cell_of_node,
                             cudaStream_t s);
 cudaError_t launch_vis_rows(const VisArgs& a, bool write, cudaStream_t s);
+cudaError_t launch_vis_steps(const VisArgs& a, uint64_t* steps, cudaStream_t s);
 cudaError_t launch_scan_u64(const uint64_t* in, uint64_t* out, uint64_t count, cudaStream_t s);
 cudaError_t launch_vis_components(const VisArgs& a, uint32_t* comp, uint32_t* sizes, uint32_t* tmp2n,
                                   uint64_t* n_comp, cudaStream_t s);

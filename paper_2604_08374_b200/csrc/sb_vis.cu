@@ -108,6 +108,7 @@ __global__ void __launch_bounds__(256) vis_rows_kernel(VisArgs a) {
     const int r_hi = static_cast<int>(imin64(static_cast<int64_t>(a.rows) - 1, r + a.R));
     uint32_t deg = 0;
     uint64_t pos = WRITE ? a.offsets[v] : 0, bytes = 0;
+    uint64_t step = a.masks ? a.step_off[v] : 0;  // visibility-mask word of the current warp step
     bool have_prev = false;
     uint32_t prev = 0;
     for (int r2 = r_lo; r2 <= r_hi; ++r2) {
@@ -121,6 +122,7 @@ __global__ void __launch_bounds__(256) vis_rows_kernel(VisArgs a) {
       // (r, cc) and the row's column range: no obstacle in it -> all visible.
       const bool clear = !any_blocked(a, r, min(cc, c_lo), r2, max(cc, c_hi));
       if (clear) {
+        step += static_cast<uint64_t>(c_hi - c_lo + 32) / 32;  // no masks stored for clear rows
         // Obstacle-free row: its candidates are consecutive free cells, so their
         // node ids are consecutive (raster order) and every delta after the
         // row's first is 1 (2 across v itself): one varint + (count - 1) bytes.
@@ -170,11 +172,16 @@ __global__ void __launch_bounds__(256) vis_rows_kernel(VisArgs a) {
         const int c2 = base + lane;
         bool emit = false;
         uint32_t w = 0;
-        if (c2 <= c_hi && !(r2 == r && c2 == cc)) {
+        if (WRITE && a.masks) {  // the count pass stored this step's line-of-sight results
+          emit = (a.masks[step] >> lane) & 1u;
+          if (emit) w = a.node_of_cell[rowbase + c2];
+        } else if (c2 <= c_hi && !(r2 == r && c2 == cc)) {
           w = a.node_of_cell[rowbase + c2];
-          if (w != 0xffffffffu) emit = clear || visible(a, r, cc, r2, c2);
+          if (w != 0xffffffffu) emit = visible(a, r, cc, r2, c2);
         }
         const uint32_t mask = __ballot_sync(FULL, emit);
+        if (!WRITE && a.masks && lane == 0) a.masks[step] = mask;
+        ++step;
         if (!mask) continue;
         const uint32_t lower = mask & ltm;
         const uint32_t pw = __shfl_sync(FULL, w, lower ? 31 - __clz(lower) : 0);
@@ -208,6 +215,33 @@ __global__ void __launch_bounds__(256) vis_rows_kernel(VisArgs a) {
       a.bytes[v] = bytes;
     }
   }
+}
+
+// Warp steps (32 candidate columns of one grid row) per node: the count pass
+// stores one visibility mask per step so the write pass need not re-walk lines
+// of sight.
+__global__ void vis_steps_kernel(VisArgs a, uint64_t* steps) {
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < a.n; v += gridDim.x * (uint64_t)blockDim.x) {
+    const uint32_t cell = a.cell_of_node[v];
+    const int r = static_cast<int>(cell / a.cols), cc = static_cast<int>(cell % a.cols);
+    const int r_lo = static_cast<int>(imax64(0, r - a.R));
+    const int r_hi = static_cast<int>(imin64(static_cast<int64_t>(a.rows) - 1, r + a.R));
+    uint64_t n = 0;
+    for (int r2 = r_lo; r2 <= r_hi; ++r2) {
+      const int64_t dr = r2 - r;
+      int64_t span = a.cols;
+      if (a.radius2) span = static_cast<int64_t>(isqrt64_dev(a.radius2 - static_cast<uint64_t>(dr * dr)));
+      const int c_lo = static_cast<int>(imax64(0, cc - span));
+      const int c_hi = static_cast<int>(imin64(static_cast<int64_t>(a.cols) - 1, cc + span));
+      n += static_cast<uint64_t>(c_hi - c_lo + 32) / 32;
+    }
+    steps[v] = n;
+  }
+}
+
+cudaError_t launch_vis_steps(const VisArgs& a, uint64_t* steps, cudaStream_t s) {
+  vis_steps_kernel<<<(a.n + 255) / 256 < 148 * 16 ? (a.n + 255) / 256 : 148 * 16, 256, 0, s>>>(a, steps);
+  return cudaGetLastError();
 }
 
 // ---- grid preparation -------------------------------------------------------
