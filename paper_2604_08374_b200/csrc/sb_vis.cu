@@ -55,38 +55,36 @@ __device__ __forceinline__ bool any_blocked(const VisArgs& a, int r0, int c0, in
   return s != 0;
 }
 
-// Exact integer line of sight between the centres of (r1,c1) and (r2,c2).
+// Exact integer line of sight between the centres of (r1,c1) and (r2,c2):
+// walk the cells whose interior the open segment crosses, stepping in x when
+// (2k+1)*ay < (2j+1)*ax, in y when greater, diagonally on an exact corner
+// crossing -- the host generator's walk (sb_csr.cpp) with the two products
+// kept as running 32-bit sums (ax, ay < 2^15 for any grid side < 32768).
 __device__ bool visible(const VisArgs& a, int r1, int c1, int r2, int c2) {
   if (!any_blocked(a, r1, c1, r2, c2)) return true;
   const int dx = c2 - c1, dy = r2 - r1;
   const int sx = dx > 0 ? 1 : -1, sy = dy > 0 ? 1 : -1;
-  const int64_t ax = dx < 0 ? -dx : dx, ay = dy < 0 ? -dy : dy;
-  int x = c1, y = r1;
-  int64_t k = 0, j = 0;
+  const int ax = dx < 0 ? -dx : dx, ay = dy < 0 ? -dy : dy;
+  int x = c1, y = r1, k = 0, j = 0;
+  int lhs = ay, rhs = ax;  // (2k+1)*ay and (2j+1)*ax
+  const uint8_t* __restrict__ row = a.blocked + static_cast<uint64_t>(y) * a.cols;
+  const int64_t rstep = sy * static_cast<int64_t>(a.cols);
   while (k < ax || j < ay) {
-    if (k < ax && j < ay) {
-      const int64_t lhs = (2 * k + 1) * ay, rhs = (2 * j + 1) * ax;
-      if (lhs < rhs) {
-        x += sx;
-        ++k;
-      } else if (lhs > rhs) {
-        y += sy;
-        ++j;
-      } else {
-        x += sx;
-        y += sy;
-        ++k;
-        ++j;
-      }
-    } else if (k < ax) {
+    const bool mx = k < ax && (j >= ay || lhs <= rhs);
+    const bool my = j < ay && (k >= ax || lhs >= rhs);
+    if (mx) {
       x += sx;
       ++k;
-    } else {
+      lhs += 2 * ay;
+    }
+    if (my) {
       y += sy;
       ++j;
+      rhs += 2 * ax;
+      row += rstep;
     }
     if (x == c2 && y == r2) break;
-    if (a.blocked[static_cast<uint64_t>(y) * a.cols + x]) return false;
+    if (row[x]) return false;
   }
   return true;
 }
