@@ -168,12 +168,16 @@ __device__ __forceinline__ uint32_t rank1(const uint2* rk, uint32_t i) {
 // N2BM: |N2(v)| from a per-node 2-hop bitmap (range-OR of every run of every
 // N(w) over the 2-hop window) instead of the depth-2 BFS counts in reach2 --
 // linear in sum_w deg(w) runs(w), the cheaper choice for large, low-degree graphs.
-template <bool SMEM, bool N2BM>
-__global__ void __launch_bounds__(256) local_kernel(LocalArgs a) {
+// BS threads per CTA: 1024 when the per-node windows are so large (wide grids
+// in raster id space) that only one or two CTAs fit an SM, so a node's slice
+// loop still has 32 warps to hide latency with.
+template <bool SMEM, bool N2BM, int BS>
+__global__ void __launch_bounds__(BS) local_kernel(LocalArgs a) {
+  constexpr int NW = BS / 32;
   extern __shared__ uint2 dyn_s[];
   __shared__ unsigned long long s_node;
-  __shared__ unsigned long long s_red[8], s_reach[8];
-  __shared__ uint32_t s_scan[8];
+  __shared__ unsigned long long s_red[NW], s_reach[NW];
+  __shared__ uint32_t s_scan[NW];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint2* rk = SMEM ? dyn_s : reinterpret_cast<uint2*>(a.scratch + blockIdx.x * a.stride_words);  // w1 + 1
   uint32_t* bm2 = reinterpret_cast<uint32_t*>(rk + a.w1_words + 1);  // N2BM: w2 words
@@ -251,7 +255,7 @@ __global__ void __launch_bounds__(256) local_kernel(LocalArgs a) {
       const uint32_t* __restrict__ qe = a.run_e + q0;
       const uint32_t cnt = static_cast<uint32_t>(q1 - q0);
       uint32_t part = 0;  // < 2^32: at most the window size per slice
-      for (uint32_t k = threadIdx.x; k < cnt; k += 256) {
+      for (uint32_t k = threadIdx.x; k < cnt; k += BS) {
         const uint32_t qsk = qs[k], qek = qe[k];
         const uint32_t cs = max(qsk, lo1), ce = min(qek, hi1);
         const bool hit = cs <= ce;  // branch-free: an empty clip queries rank(0) twice
@@ -276,7 +280,7 @@ __global__ void __launch_bounds__(256) local_kernel(LocalArgs a) {
     __syncthreads();
     if (threadIdx.x == 0) {
       unsigned long long tri = 0, n2 = 0;
-      for (int q = 0; q < 8; ++q) {
+      for (int q = 0; q < NW; ++q) {
         tri += s_red[q];
         n2 += s_reach[q];
       }
@@ -311,28 +315,34 @@ cudaError_t launch_local_spans(const LocalArgs& a, cudaStream_t s) {
 
 size_t local_smem_limit() { return 200 * 1024; }
 
-template <bool SMEM, bool N2BM>
+template <bool SMEM, bool N2BM, int BS>
 static cudaError_t launch_local_t(const LocalArgs& a, int* grid_out, cudaStream_t s) {
   const size_t bytes = SMEM ? a.stride_words * 4 : 0;
   int per = 0;
   if (SMEM) {
-    cudaError_t e = cudaFuncSetAttribute(local_kernel<SMEM, N2BM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(local_kernel<SMEM, N2BM, BS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(bytes));
     if (e != cudaSuccess) return e;
   }
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, local_kernel<SMEM, N2BM>, 256, bytes);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, local_kernel<SMEM, N2BM, BS>, BS, bytes);
   const int g = sm_count() * (per < 1 ? 1 : per);
   if (grid_out) {  // query only (global scratch sizing)
     *grid_out = g;
     return cudaSuccess;
   }
-  local_kernel<SMEM, N2BM><<<g, 256, bytes, s>>>(a);
+  local_kernel<SMEM, N2BM, BS><<<g, BS, bytes, s>>>(a);
   return cudaGetLastError();
 }
 
+// 256 threads per CTA unless the shared windows exceed 56 KB (fewer than 4 CTAs/SM).
 cudaError_t launch_local(const LocalArgs& a, bool smem, bool n2_bitmap, int* grid_out, cudaStream_t s) {
-  if (smem) return n2_bitmap ? launch_local_t<true, true>(a, grid_out, s) : launch_local_t<true, false>(a, grid_out, s);
-  return n2_bitmap ? launch_local_t<false, true>(a, grid_out, s) : launch_local_t<false, false>(a, grid_out, s);
+  const bool wide = smem && a.stride_words * 4 > 56 * 1024;
+  if (smem) {
+    if (wide)
+      return n2_bitmap ? launch_local_t<true, true, 1024>(a, grid_out, s) : launch_local_t<true, false, 1024>(a, grid_out, s);
+    return n2_bitmap ? launch_local_t<true, true, 256>(a, grid_out, s) : launch_local_t<true, false, 256>(a, grid_out, s);
+  }
+  return n2_bitmap ? launch_local_t<false, true, 256>(a, grid_out, s) : launch_local_t<false, false, 256>(a, grid_out, s);
 }
 
 }  // namespace sb

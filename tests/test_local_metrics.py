@@ -167,3 +167,26 @@ def test_gpu_local_metrics_hilbert_equivariant(tmp_path):
         got = DeviceGraph(hh).local_metrics()
         for k in ref:
             assert same(got[k], ref[k][inv]), k
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n2", ["bfs", "bitmap"])
+def test_gpu_local_metrics_wide_windows_paths_agree(tmp_path, n2):
+    """A wide grid (raster ids make the per-node windows span whole grid rows): the
+    1024-thread shared-memory path and the 256-thread global-scratch path agree."""
+    code = (
+        "import sys; sys.path.insert(0, %r)\n"
+        "import numpy as np\n"
+        "from paper_2604_08374_b200 import DeviceGraph, grid_mask\n"
+        "dg = DeviceGraph.from_grid(grid_mask(40, 4000, 300, 2, 6, 5), 30 * 30)\n"
+        "m = dg.local_metrics(0, 4000)\n"
+        "np.savez(sys.argv[1], **m)\n" % ROOT)
+    outs = []
+    for glob in ("0", "1"):
+        f = str(tmp_path / f"m{glob}.npz")
+        env = dict(os.environ, SB_LOCAL_N2=n2, SB_LOCAL_GLOBAL=glob)
+        r = subprocess.run([sys.executable, "-c", code, f], env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(f))
+    for k in outs[0].files:
+        assert same(outs[0][k], outs[1][k]), k
