@@ -20,11 +20,16 @@
 //                 N(w): |run & N(v)| by two rank queries (clustering).  The
 //                 runs of all w in one run [s, e] of N(v) are one contiguous
 //                 range of the run index, strided over by the whole CTA.  The
-//                 bitmap lives in shared memory when the widest window fits,
-//                 else in a per-CTA global scratch (L2-resident).
-// |N2(v)| (controllability) is |B(v, 2)| - 1 from the exact bit-parallel BFS
-// at depth 2 (sb_exact_*, the same fused decode-union kernels with OR), run by
-// the caller; local_kernel only divides.
+//                 bitmap lives in shared memory when the widest window fits
+//                 (1024-thread CTAs for windows > 56 KB), else in a per-CTA
+//                 global scratch (L2-resident).
+// |N2(v)| (controllability), two methods chosen by the caller on cost:
+//   BFS mode    |B(v, 2)| - 1 from the exact bit-parallel BFS at depth 2
+//               (sb_exact_*, the fused decode-union kernels with OR); the
+//               kernel only divides
+//   bitmap mode local_kernel<., true, .> range-ORs every run of every N(w)
+//               into a per-node 2-hop bitmap over [lo2, hi2] (from
+//               ctrl_kernel) and popcounts it
 #include <cmath>
 
 #include "sb_device.cuh"
