@@ -24,4 +24,11 @@ for p in (6, 10, 12):
     h.registers()
 h = HyperBall(DeviceGraph(g, async_upload=True), 10, None, interval=True)
 h.run()
+# local metrics: both |N2| methods, shared / global scratch, the wide-window 1024-thread CTA
+import os as _os  # noqa: E402
+for n2 in ("bfs", "bitmap"):
+    _os.environ["SB_LOCAL_N2"] = n2
+    DeviceGraph(g).local_metrics()
+    DeviceGraph.from_grid(grid_mask(24, 3000, 200, 2, 6, 5), 20 * 20).local_metrics(0, 512)
+_os.environ.pop("SB_LOCAL_N2")
 print("ok")
