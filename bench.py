@@ -246,7 +246,8 @@ def pipeline_variant(args, P, device, hb_ref):
     DeviceGraph.from_grid(grid_mask(16, 16, 0, 1, 1, 1), 9, device)  # warm the build kernels
     out = {"input": f"{r}x{c} obstacle mask ({mask.size} B H2D)",
            "timing": "host wall clock per phase, best of 2 (synchronous C-ABI calls)"}
-    for mode in ("interval", "dense", "interval", "dense"):
+    modes = ("interval", "dense") if P.p >= 10 else ("dense",)  # interval mode needs p >= 10
+    for mode in modes + modes:
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         dg = DeviceGraph.from_grid(mask, rad2, device)
