@@ -72,3 +72,9 @@ def test_cpp_facade_tool_builds_and_reports_missing_gpu():
     assert r.returncode == 1 and "no CUDA device" in r.stderr
     r = subprocess.run([tool, "synth", "8", "8", "0", "1", "1", "1", "0", "3", "2"], capture_output=True, text=True)
     assert r.returncode in (1, 2)
+
+
+def test_version_and_last_error_strings():
+    from paper_2604_08374_b200 import lib
+    assert b"sm_100a" in lib().sb_version()
+    assert isinstance(lib().sb_last_error(), bytes)
