@@ -286,9 +286,21 @@ __device__ __forceinline__ Decode4 decode_step4(const uint8_t* __restrict__ stre
   const int lk = __shfl_sync(FULL, lastk, L);
   o.advance = 4 * L + lk + 1;
   o.last = __shfl_sync(FULL, sel4(id, lk), L);  // lk is warp-uniform
+  if (!SKIP) {
+    // Every wanted id is kept, and the wanted terminators are a prefix of the
+    // window's terminators: a terminator's rank is its slot, the last wanted
+    // id is the padding value -- no further ballots.
+    uint32_t slot = below;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (want[k]) buf[slot++] = id[k];
+    o.count = o.wanted;
+    if (lane < PAD) buf[o.wanted + lane] = o.last;
+    return o;
+  }
   bool keep[4];
 #pragma unroll
-  for (int k = 0; k < 4; ++k) keep[k] = want[k] && (!SKIP || changed[id[k]]);
+  for (int k = 0; k < 4; ++k) keep[k] = want[k] && changed[id[k]];
   uint32_t kb = 0, kn = 0;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {

@@ -13,6 +13,7 @@ int build_run_index(sb_graph* g) {
   if (g->d_run_off || g->n_items == 0) return SB_OK;
   sb::RunIndexArgs a{};
   a.stream = g->d_stream;
+  a.stream_len = g->stream_local;
   a.item_off = g->d_item_off;
   a.item_base = g->d_item_base;
   a.item_count = g->d_item_count;

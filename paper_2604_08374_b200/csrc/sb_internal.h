@@ -65,6 +65,7 @@ struct IntervalArgs {
 // Run index, derived once at upload from the LEB128 stream (decode_runs4).
 struct RunIndexArgs {
   const uint8_t* stream;
+  uint64_t stream_len;         // bytes (prefetch bound)
   const uint64_t* item_off;
   const uint32_t* item_base;
   const uint32_t* item_count;

@@ -26,8 +26,20 @@
 namespace sb {
 
 // ------------------------------------------------------------------ build
+// Upload-time validation and work-item cutting: one warp per row, 128-byte
+// windows at 4 bytes per lane (the decode_step4 arithmetic), the next lines
+// prefetched into L2 -- the pass is a latency-bound stream (one dependent
+// window per warp at a time), so keeping lines in flight is what sets its
+// speed.  Bytes at or past the row end read as continuation bytes, so they
+// never form a terminator: a truncated row runs out of terminators and a
+// longer one leaves trailing bytes, both reported.  Checks (leb128.hpp:28-39,
+// SPEC.md:174-177): varint <= 5 bytes and < 2^32, id < N, ids strictly
+// increasing (no zero delta, no 32-bit wrap), exactly deg ids, no trailing bytes.
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
 __global__ void __launch_bounds__(256) build_items_kernel(BuildArgs a) {
   const int lane = threadIdx.x & 31;
+  const uint32_t ltm = (1u << lane) - 1u;
   const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = (gridDim.x * (uint64_t)blockDim.x) >> 5;
   const uint64_t node_end = a.node_end ? a.node_end : a.n_local;
@@ -45,45 +57,106 @@ __global__ void __launch_bounds__(256) build_items_kernel(BuildArgs a) {
     uint32_t rem = deg, base = 0, k0 = 0, run_start = 0, maxrun = 0;
     bool bad = false;
     while (rem > 0) {
-      const DecodeOut d = decode_step<true>(a.stream, pos, end, rem, base, lane);
-      if (d.count == 0) {  // truncated row or varint longer than the window
-        bad = true;
-        break;
+      if (lane < 2 && pos + 256 + 128 * lane < end) prefetch_l2(a.stream + pos + 256 + 128 * lane);
+      const uint8_t* al = a.stream + (pos & ~3ull) + 4 * lane;
+      const uint32_t w0 = ld_stream_word(al);
+      const uint32_t w1 = ld_stream_word(al + 4);
+      uint32_t w = __funnelshift_r(w0, w1, static_cast<uint32_t>(pos & 3) * 8);
+      const int64_t q = static_cast<int64_t>(end - pos) - 4 * lane;  // row bytes left at this lane
+      if (q < 4) w |= q <= 0 ? 0x80808080u : (0x80808080u << (8 * q));
+      uint32_t wp = __shfl_up_sync(FULL, w, 1), wpp = __shfl_up_sync(FULL, w, 2);
+      if (lane < 1) wp = 0;  // the window starts on a varint boundary
+      if (lane < 2) wpp = 0;
+      const uint32_t F = w & 0x80808080u, Fp = wp & 0x80808080u, Fpp = wpp & 0x80808080u;
+      const uint32_t m1 = __funnelshift_l(Fp, F, 8);
+      const uint32_t m2 = m1 & __funnelshift_l(Fp, F, 16);
+      const uint32_t m3 = m2 & __funnelshift_l(Fp, F, 24);
+      const uint32_t m4 = m3 & Fp;
+      const uint32_t m5 = m4 & __funnelshift_l(Fpp, Fp, 8);  // >= 5 continuation bytes: too long
+      const uint32_t D = (m1 >> 7) + (m2 >> 7) + (m3 >> 7) + (m4 >> 7);
+      uint32_t c[4], dk[4], vl[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        dk[k] = (D >> (8 * k)) & 0xffu;
+        c[k] = ((w >> (8 * k)) & 0x7fu) << (7 * dk[k]);
+        vl[k] = c[k] + ((k >= 1 && dk[k] >= 1) ? vl[k > 0 ? k - 1 : 0] : 0u);
       }
-      const bool want = (d.mask >> lane) & 1u;
-      const uint32_t up = __shfl_up_sync(FULL, d.id, 1);  // every lane must execute the shuffle
-      const uint32_t prev = lane > 0 ? up : base;
-      const uint32_t rank = __popc(d.mask & ((1u << lane) - 1u));
-      const uint32_t j = k0 + rank;  // neighbour index within the row
-      bool lane_bad = d.bad;
-      if (want) {
-        if (d.id >= a.n_global) lane_bad = true;
-        if (j > 0 && !(d.id > prev)) lane_bad = true;  // strictly increasing
-        if ((j + 1) % a.chunk == 0 && j + 1 < deg) {
-          const uint32_t it = i0 + (j + 1) / a.chunk;
-          a.item_off[it] = pos + lane + 1;
-          a.item_base[it] = d.id;
-          a.item_count[it] = (deg - (j + 1)) < a.chunk ? deg - (j + 1) : a.chunk;
-          a.item_node[it] = static_cast<uint32_t>(node);
+      uint32_t vp3 = __shfl_up_sync(FULL, vl[3], 1);
+      if (lane == 0) vp3 = 0;
+      const uint32_t p1 = c[0] + c[1], p2 = p1 + c[2], lane_sum = p2 + c[3];
+      uint32_t incl = lane_sum;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL, incl, d);
+        if (lane >= d) incl += y;
+      }
+      const uint32_t excl = base + incl - lane_sum;
+      const uint32_t id[4] = {excl + c[0], excl + p1, excl + p2, excl + lane_sum};
+      const uint32_t T = ~w & 0x80808080u;
+      uint32_t below = 0, tot = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t B = __ballot_sync(FULL, (T >> (8 * k + 7)) & 1u);
+        below += __popc(B & ltm);
+        tot += __popc(B);
+      }
+      uint32_t r = below, jj[4];
+      bool start[4], lane_bad = false;
+      int lastk = -1;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const bool t = (T >> (8 * k + 7)) & 1u;
+        const bool want = t && r < rem;
+        jj[k] = k0 + r;  // neighbour index within the row
+        start[k] = false;
+        if (want) {
+          const uint32_t v = vl[k] + (dk[k] > static_cast<uint32_t>(k) ? vp3 : 0u);  // this varint's value
+          if (((m5 >> (8 * k + 7)) & 1u) || (dk[k] == 4 && ((w >> (8 * k)) & 0x7fu) > 0x0fu)) lane_bad = true;
+          if (id[k] >= a.n_global) lane_bad = true;
+          if (jj[k] > 0 && (v == 0 || id[k] < v)) lane_bad = true;  // zero delta or 32-bit wrap
+          if ((jj[k] + 1) % a.chunk == 0 && jj[k] + 1 < deg) {
+            const uint32_t it = i0 + (jj[k] + 1) / a.chunk;
+            a.item_off[it] = pos + 4 * lane + k + 1;
+            a.item_base[it] = id[k];
+            a.item_count[it] = (deg - (jj[k] + 1)) < a.chunk ? deg - (jj[k] + 1) : a.chunk;
+            a.item_node[it] = static_cast<uint32_t>(node);
+          }
+          start[k] = jj[k] == 0 || v != 1u;  // a delta of 1 continues the run of consecutive ids
+          lastk = k;
         }
+        r += t;
       }
-      if (__any_sync(FULL, lane_bad)) {
+      const uint32_t anyw = __ballot_sync(FULL, lastk >= 0);
+      if (__any_sync(FULL, lane_bad) || anyw == 0) {  // anyw == 0: the row ran out of bytes
         bad = true;
         break;
       }
       // longest run of consecutive ids (sizes the interval-mode sparse table)
-      const bool st = want && (j == 0 || d.id != prev + 1);
-      const uint32_t S = __ballot_sync(FULL, st);
-      const uint32_t sb = S & ((1u << lane) - 1u);
-      const int pl = sb ? 31 - __clz(sb) : -1;
-      const uint32_t pj = __shfl_sync(FULL, j, pl < 0 ? 0 : pl);
-      const uint32_t prev_start = pl < 0 ? run_start : pj;
-      if (st && j > 0) maxrun = max(maxrun, j - prev_start);
-      if (S) run_start = __shfl_sync(FULL, j, 31 - __clz(S));
-      pos += d.last + 1;
-      rem -= d.count;
-      base = __shfl_sync(FULL, d.id, d.last);
-      k0 += d.count;
+      int hs = -1;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (start[k]) hs = k;
+      const uint32_t A = __ballot_sync(FULL, hs >= 0);
+      const uint32_t lastSj = sel4(jj, hs);
+      const uint32_t Ab = A & ltm;
+      const uint32_t pj = __shfl_sync(FULL, lastSj, Ab ? 31 - __clz(Ab) : 0);
+      bool have = Ab ? true : k0 > 0;
+      uint32_t ps = Ab ? pj : run_start;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (start[k]) {
+          if (have) maxrun = max(maxrun, jj[k] - ps);
+          have = true;
+          ps = jj[k];
+        }
+      if (A) run_start = __shfl_sync(FULL, lastSj, 31 - __clz(A));
+      const int L = 31 - __clz(anyw);
+      const int lk = __shfl_sync(FULL, lastk, L);
+      const uint32_t wanted = tot < rem ? tot : rem;
+      base = __shfl_sync(FULL, sel4(id, lk), L);
+      pos += 4 * L + lk + 1;
+      rem -= wanted;
+      k0 += wanted;
     }
     if (!bad && pos != end) bad = true;  // trailing bytes in the row
     if (bad && lane == 0) atomicMin(a.err_node, static_cast<unsigned long long>(node));
@@ -473,6 +546,7 @@ __global__ void __launch_bounds__(256) run_index_kernel(RunIndexArgs a) {
     uint64_t out = FILL ? a.run_off[item] : 0;
     int nr = 0;
     while (rem > 0) {
+      if (lane < 2 && pos + 256 + 128 * lane < a.stream_len) prefetch_l2(a.stream + pos + 256 + 128 * lane);
       __syncwarp();
       const RunWindow o = decode_runs4(a.stream, pos, rem, base, open, ostart, rs, re, nr, lane);
       if (o.advance == 0) break;
