@@ -68,6 +68,11 @@ typedef struct sb_comm sb_comm;   /* NCCL communicator for node-range sharding *
 const char* sb_last_error(void);
 const char* sb_version(void);
 int sb_device_count(int* n);
+/* Device buffers come from the device's default stream-ordered memory pool,
+ * which keeps freed blocks so repeated graph / HyperBall create-destroy cycles
+ * reuse them (buffers shared over CUDA IPC excepted).  This returns the cached
+ * blocks of `device` to the driver (after a device synchronise). */
+int sb_release_cached_memory(int device);
 
 /* ---------------- host CompressedCsr ---------------- */
 typedef struct {

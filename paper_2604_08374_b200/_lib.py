@@ -66,6 +66,7 @@ _SIGS = {
     "sb_last_error": (C.c_char_p, []),
     "sb_version": (C.c_char_p, []),
     "sb_device_count": (_i, [C.POINTER(_i)]),
+    "sb_release_cached_memory": (_i, [_i]),
     "sb_check_convergence": (_i, [C.c_double]),
     "sb_csr_synth_grid": (_i, [_u32, _u32, _u32, _u32, _u32, _u64, _u64, C.c_uint, _pp]),
     "sb_csr_from_adjacency": (_i, [_u64, _vp, _vp, _pp]),

@@ -21,7 +21,7 @@ static int exact_grow_hist(sb_exact* x, uint32_t need) {
   while (cap <= need) cap *= 2;
   const uint64_t n = x->g->n;
   uint32_t* nh = nullptr;
-  CK(cudaMalloc(&nh, n * cap * 4));
+  CK(dalloc(&nh, n * cap * 4));
   CK(cudaMemsetAsync(nh, 0, n * cap * 4, x->stream));
   if (x->d_hist)
     CK(cudaMemcpy2DAsync(nh, cap * 4, x->d_hist, x->hist_cap * 4, x->hist_cap * 4, n, cudaMemcpyDeviceToDevice,
@@ -60,22 +60,22 @@ int sb_exact_create(sb_graph* g, unsigned log2_block, uint32_t depth_limit, uint
   XK(cudaStreamCreateWithFlags(&x->stream, cudaStreamNonBlocking));
   for (auto& e : x->ev) XK(cudaEventCreate(&e));
   const uint64_t n = g->n, plane = n * x->row;
-  for (int i = 0; i < 2; ++i) XK(cudaMalloc(&x->d_plane[i], plane + 64));
-  XK(cudaMalloc(&x->d_changed, n));
-  XK(cudaMalloc(&x->d_scratch, std::max<uint64_t>(g->n_items, 1) * x->slices * 512));
-  XK(cudaMalloc(&x->d_counter, n * x->slices * 4));
+  for (int i = 0; i < 2; ++i) XK(dalloc(&x->d_plane[i], plane + 64));
+  XK(dalloc(&x->d_changed, n));
+  XK(dalloc(&x->d_scratch, std::max<uint64_t>(g->n_items, 1) * x->slices * 512));
+  XK(dalloc(&x->d_counter, n * x->slices * 4));
   XK(cudaMemset(x->d_counter, 0, n * x->slices * 4));
-  XK(cudaMalloc(&x->d_pop, n * 4));
-  XK(cudaMalloc(&x->d_reach, n * 4));
+  XK(dalloc(&x->d_pop, n * 4));
+  XK(dalloc(&x->d_reach, n * 4));
   XK(cudaMemset(x->d_reach, 0, n * 4));
-  XK(cudaMalloc(&x->d_sum, 2 * n * 8));
+  XK(dalloc(&x->d_sum, 2 * n * 8));
   XK(cudaMemset(x->d_sum, 0, 2 * n * 8));
-  XK(cudaMalloc(&x->d_misc, 2 * 8));
+  XK(dalloc(&x->d_misc, 2 * 8));
   if (flags & SB_HB_INTERVAL) {
     int K = 0;
     while (K < 10 && (2u << K) <= g->max_run) ++K;
     x->levels = K;
-    if (K) XK(cudaMalloc(&x->d_st, static_cast<uint64_t>(K) * plane + 64));
+    if (K) XK(dalloc(&x->d_st, static_cast<uint64_t>(K) * plane + 64));
     const int rc = build_run_index(g);
     if (rc) return bail(rc);
   }
@@ -238,12 +238,16 @@ int sb_local_metrics(sb_graph* g, uint64_t v0, uint64_t v1, double* control, dou
   const uint64_t u32_words = 2 * n + 2 * nl + 2;
   const uint64_t bytes = ((u32_words * 4 + 7) & ~7ull) + 5 * nl * 8 + 8;
   uint8_t* blk = nullptr;
-  CK(cudaMalloc(&blk, bytes));
+  CK(dalloc(&blk, bytes));
   uint32_t* scratch = nullptr;
   struct Free {
     uint8_t*& p;
     uint32_t*& q;
-    ~Free() { if (p) cudaFree(p); if (q) cudaFree(q); }
+    ~Free() {
+      cudaStreamSynchronize(0);  // error paths: kernels on the legacy stream may still run
+      dfree(p);
+      dfree(q);
+    }
   } fr{blk, scratch};
   sb::LocalArgs a{};
   a.n = n;
@@ -282,7 +286,7 @@ int sb_local_metrics(sb_graph* g, uint64_t v0, uint64_t v1, double* control, dou
   if (!smem) {
     int grid = 0;
     CK(sb::launch_local(a, false, n2_bitmap, &grid, 0));
-    CK(cudaMalloc(&scratch, static_cast<uint64_t>(grid) * a.stride_words * 4));
+    CK(dalloc(&scratch, static_cast<uint64_t>(grid) * a.stride_words * 4));
     a.scratch = scratch;
   }
   CK(sb::launch_local(a, smem, n2_bitmap, nullptr, 0));

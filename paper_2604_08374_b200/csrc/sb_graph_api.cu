@@ -19,19 +19,19 @@ int build_run_index(sb_graph* g) {
   a.item_count = g->d_item_count;
   a.n_items = g->n_items;
   uint64_t* d_cnt = nullptr;
-  CK(cudaMalloc(&d_cnt, g->n_items * 8));
+  CK(dalloc(&d_cnt, g->n_items * 8));
   a.run_count = d_cnt;
   CK(sb::launch_run_index(a, false, 0));
   CK(sync_stream(0));
   std::vector<uint64_t> off(g->n_items + 1, 0);
   CK(cudaMemcpy(off.data() + 1, d_cnt, g->n_items * 8, cudaMemcpyDeviceToHost));
-  cudaFree(d_cnt);
+  dfree(d_cnt);
   for (uint64_t i = 0; i < g->n_items; ++i) off[i + 1] += off[i];
   g->n_runs = off[g->n_items];
-  CK(cudaMalloc(&g->d_run_off, off.size() * 8));
+  CK(dalloc(&g->d_run_off, off.size() * 8));
   CK(cudaMemcpy(g->d_run_off, off.data(), off.size() * 8, cudaMemcpyHostToDevice));
-  CK(cudaMalloc(&g->d_run_s, std::max<uint64_t>(g->n_runs, 1) * 4));
-  CK(cudaMalloc(&g->d_run_e, std::max<uint64_t>(g->n_runs, 1) * 4));
+  CK(dalloc(&g->d_run_s, std::max<uint64_t>(g->n_runs, 1) * 4));
+  CK(dalloc(&g->d_run_e, std::max<uint64_t>(g->n_runs, 1) * 4));
   a.run_off = g->d_run_off;
   a.run_s = g->d_run_s;
   a.run_e = g->d_run_e;
@@ -54,6 +54,18 @@ int sb_device_count(int* n) {
     return cuda_fail(e, "cudaGetDeviceCount");
   }
   *n = c;
+  return SB_OK;
+}
+
+int sb_release_cached_memory(int device) {
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
+    return fail(SB_EINVAL, "bad device %d", device);
+  DeviceGuard dg(device);
+  CK(cudaDeviceSynchronize());
+  cudaMemPool_t pool;
+  CK(cudaDeviceGetDefaultMemPool(&pool, device));
+  CK(cudaMemPoolTrimTo(pool, 0));
   return SB_OK;
 }
 
@@ -94,20 +106,20 @@ static int graph_setup_host(sb_graph* g, const uint32_t* deg_local) {
     }
   }
   g->n_tiles = tn0.size();
-  CK(cudaMalloc(&g->d_tile_node0, std::max<size_t>(tn0.size(), 1) * 4));
-  CK(cudaMalloc(&g->d_tile_q, std::max<size_t>(tq.size(), 1) * 4));
+  CK(dalloc(&g->d_tile_node0, std::max<size_t>(tn0.size(), 1) * 4));
+  CK(dalloc(&g->d_tile_q, std::max<size_t>(tq.size(), 1) * 4));
   if (!tn0.empty()) {
     CK(cudaMemcpy(g->d_tile_node0, tn0.data(), tn0.size() * 4, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(g->d_tile_q, tq.data(), tq.size() * 4, cudaMemcpyHostToDevice));
   }
-  CK(cudaMalloc(&g->d_node_item, node_item.size() * 4));
+  CK(dalloc(&g->d_node_item, node_item.size() * 4));
   CK(cudaMemcpy(g->d_node_item, node_item.data(), node_item.size() * 4, cudaMemcpyHostToDevice));
   const uint64_t ni = std::max<uint64_t>(items, 1);
-  CK(cudaMalloc(&g->d_item_off, ni * 8));
-  CK(cudaMalloc(&g->d_item_base, ni * 4));
-  CK(cudaMalloc(&g->d_item_count, ni * 4));
-  CK(cudaMalloc(&g->d_item_node, ni * 4));
-  CK(cudaMalloc(&g->d_err, 16));
+  CK(dalloc(&g->d_item_off, ni * 8));
+  CK(dalloc(&g->d_item_base, ni * 4));
+  CK(dalloc(&g->d_item_count, ni * 4));
+  CK(dalloc(&g->d_item_node, ni * 4));
+  CK(dalloc(&g->d_err, 16));
   CK(cudaMemset(g->d_err, 0xff, 8));
   CK(cudaMemset(reinterpret_cast<uint8_t*>(g->d_err) + 8, 0, 8));
   return SB_OK;
@@ -207,18 +219,18 @@ static int graph_create(uint64_t n, const uint64_t* offsets, const uint32_t* deg
     if (e_ != cudaSuccess) return bail(cuda_fail(e_, #x));    \
   } while (0)
   // 256 B of zero padding: the decoder reads whole 128-byte windows (+8 for alignment).
-  GK(cudaMalloc(&g->d_stream, g->stream_local + 256));
+  GK(dalloc(&g->d_stream, g->stream_local + 256));
   GK(cudaMemset(g->d_stream + g->stream_local, 0, 256));
   if (g->stream_local && !async)
     GK(cudaMemcpy(g->d_stream, stream + b0, g->stream_local, cudaMemcpyHostToDevice));
   std::vector<uint64_t> ro(g->n_local + 1);
   for (uint64_t i = 0; i <= g->n_local; ++i) ro[i] = offsets[node_begin + i] - b0;
-  GK(cudaMalloc(&g->d_rowoff, ro.size() * 8));
+  GK(dalloc(&g->d_rowoff, ro.size() * 8));
   GK(cudaMemcpy(g->d_rowoff, ro.data(), ro.size() * 8, cudaMemcpyHostToDevice));
-  GK(cudaMalloc(&g->d_deg, std::max<uint64_t>(g->n_local, 1) * 4));
+  GK(dalloc(&g->d_deg, std::max<uint64_t>(g->n_local, 1) * 4));
   if (g->n_local) GK(cudaMemcpy(g->d_deg, degrees + node_begin, g->n_local * 4, cudaMemcpyHostToDevice));
   if (orig_id) {
-    GK(cudaMalloc(&g->d_orig, n * 4));
+    GK(dalloc(&g->d_orig, n * 4));
     GK(cudaMemcpy(g->d_orig, orig_id, n * 4, cudaMemcpyHostToDevice));
   }
   if (!async) {
@@ -323,10 +335,10 @@ int sb_graph_build_grid(uint32_t rows, uint32_t cols, const uint8_t* blocked, ui
     if (e_ != cudaSuccess) return bail(cuda_fail(e_, #x));    \
   } while (0)
   cudaStream_t s = 0;
-  BK(cudaMalloc(&d_mask, cells));
+  BK(dalloc(&d_mask, cells));
   BK(cudaMemcpy(d_mask, blocked, cells, cudaMemcpyHostToDevice));
-  BK(cudaMalloc(&d_pref, static_cast<uint64_t>(rows + 1) * (cols + 1) * 4));
-  BK(cudaMalloc(&d_scan, 2 * cells * 4));
+  BK(dalloc(&d_pref, static_cast<uint64_t>(rows + 1) * (cols + 1) * 4));
+  BK(dalloc(&d_scan, 2 * cells * 4));
   sb::VisArgs a{};
   a.rows = rows;
   a.cols = cols;
@@ -340,8 +352,8 @@ int sb_graph_build_grid(uint32_t rows, uint32_t cols, const uint8_t* blocked, ui
   g->v0 = 0;
   g->v1 = n;
   g->n_local = n;
-  BK(cudaMalloc(&d_noc, cells * 4));
-  BK(cudaMalloc(&g->d_cell, n * 4));
+  BK(dalloc(&d_noc, cells * 4));
+  BK(dalloc(&g->d_cell, n * 4));
   BK(sb::launch_vis_maps(a, d_scan, d_noc, g->d_cell, s));
   a.node_of_cell = d_noc;
   a.cell_of_node = g->d_cell;
@@ -356,13 +368,13 @@ int sb_graph_build_grid(uint32_t rows, uint32_t cols, const uint8_t* blocked, ui
   }
   // Line-of-sight results of the count pass are kept (one mask word per warp
   // step) so the write pass does not walk them again; skipped if HBM is short.
-  if (cudaMalloc(&d_steps, (n + 1) * 8) == cudaSuccess && cudaMalloc(&d_stepoff, (n + 1) * 8) == cudaSuccess) {
+  if (dalloc(&d_steps, (n + 1) * 8) == cudaSuccess && dalloc(&d_stepoff, (n + 1) * 8) == cudaSuccess) {
     BK(cudaMemsetAsync(d_steps + n, 0, 8, s));
     BK(sb::launch_vis_steps(a, d_steps, s));
     BK(sb::launch_scan_u64(d_steps, d_stepoff, n + 1, s));
     uint64_t words = 0;
     BK(cudaMemcpy(&words, d_stepoff + n, 8, cudaMemcpyDeviceToHost));
-    if (cudaMalloc(&d_masks, std::max<uint64_t>(words, 1) * 4) == cudaSuccess) {
+    if (dalloc(&d_masks, std::max<uint64_t>(words, 1) * 4) == cudaSuccess) {
       a.masks = d_masks;
       a.step_off = d_stepoff;
     } else {
@@ -372,18 +384,18 @@ int sb_graph_build_grid(uint32_t rows, uint32_t cols, const uint8_t* blocked, ui
     cudaGetLastError();
   }
   auto free_masks = [&] { dfree(d_masks); dfree(d_steps); dfree(d_stepoff); a.masks = nullptr; a.step_off = nullptr; };
-  BK(cudaMalloc(&g->d_deg, n * 4));
-  BK(cudaMalloc(&d_bytes, (n + 1) * 8));
+  BK(dalloc(&g->d_deg, n * 4));
+  BK(dalloc(&d_bytes, (n + 1) * 8));
   BK(cudaMemsetAsync(d_bytes + n, 0, 8, s));
   a.deg = g->d_deg;
   a.bytes = d_bytes;
   BK(sb::launch_vis_rows(a, false, s));
-  BK(cudaMalloc(&g->d_rowoff, (n + 1) * 8));
+  BK(dalloc(&g->d_rowoff, (n + 1) * 8));
   BK(sb::launch_scan_u64(d_bytes, g->d_rowoff, n + 1, s));
   uint64_t total = 0;
   BK(cudaMemcpy(&total, g->d_rowoff + n, 8, cudaMemcpyDeviceToHost));
   g->stream_local = total;
-  BK(cudaMalloc(&g->d_stream, total + 256));
+  BK(dalloc(&g->d_stream, total + 256));
   BK(cudaMemsetAsync(g->d_stream + total, 0, 256, s));
   a.offsets = g->d_rowoff;
   a.stream = g->d_stream;
@@ -391,9 +403,9 @@ int sb_graph_build_grid(uint32_t rows, uint32_t cols, const uint8_t* blocked, ui
   BK(cudaStreamSynchronize(s));
   free_masks();
   // components (the 2n scratch doubles as the union-find parent array + ranks)
-  BK(cudaMalloc(&d_tmp, 3 * n * 4));
-  BK(cudaMalloc(&g->d_comp, n * 4));
-  BK(cudaMalloc(&g->d_comp_sizes, n * 4));
+  BK(dalloc(&d_tmp, 3 * n * 4));
+  BK(dalloc(&g->d_comp, n * 4));
+  BK(dalloc(&g->d_comp_sizes, n * 4));
   a.parent = d_tmp;
   BK(sb::launch_vis_components(a, g->d_comp, g->d_comp_sizes, d_tmp + n, &g->n_comp, s));
   std::vector<uint32_t> deg(n);

@@ -9,6 +9,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -48,8 +49,61 @@ struct DeviceGuard {
   }
 };
 
+// Device memory comes from the device's default stream-ordered pool, told to
+// keep what is freed (release threshold = all): repeated create / destroy
+// cycles -- a service analysing many grids, the end-to-end bench -- then reuse
+// the multi-GB stream and plane buffers instead of paying the driver's
+// map / unmap (and cudaFree's device-wide sync) every time, the way torch's
+// caching allocator does.  sb_release_cached_memory() hands it back.  Owners
+// synchronise their streams before dfree.  Buffers shared with peer processes
+// over CUDA IPC (HyperBall planes and changed flags) stay on cudaMalloc.
+inline cudaError_t keep_pool(int dev) {
+  static std::once_flag once[128];
+  if (dev < 0 || dev >= 128) return cudaErrorInvalidDevice;
+  cudaError_t e = cudaSuccess;
+  std::call_once(once[dev], [&] {
+    cudaMemPool_t pool;
+    e = cudaDeviceGetDefaultMemPool(&pool, dev);
+    uint64_t keep = ~0ull;
+    if (e == cudaSuccess) e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  });
+  return e;
+}
+
+template <class T>
+inline cudaError_t dalloc(T** p, size_t bytes) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = keep_pool(dev);
+  if (e != cudaSuccess) return e;
+  void* q = nullptr;
+  e = cudaMallocAsync(&q, bytes, cudaStreamPerThread);
+  if (e == cudaErrorMemoryAllocation) {  // return cached blocks to the driver once, then retry
+    cudaGetLastError();
+    cudaMemPool_t pool;
+    cudaDeviceGetDefaultMemPool(&pool, dev);
+    cudaDeviceSynchronize();
+    cudaMemPoolTrimTo(pool, 0);
+    e = cudaMallocAsync(&q, bytes, cudaStreamPerThread);
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(cudaStreamPerThread);
+  if (e == cudaSuccess) *p = static_cast<T*>(q);
+  return e;
+}
+
 template <class T>
 inline void dfree(T*& p) {
+  if (p) cudaFreeAsync(p, cudaStreamPerThread);
+  p = nullptr;
+}
+
+template <class T>
+inline cudaError_t dalloc_ipc(T** p, size_t bytes) {
+  return cudaMalloc(p, bytes);
+}
+
+template <class T>
+inline void dfree_ipc(T*& p) {
   if (p) cudaFree(p);
   p = nullptr;
 }
@@ -86,7 +140,10 @@ using sb::fail;
 using sb::rt::cuda_fail;
 using sb::rt::DeviceGuard;
 using sb::rt::decode_ord;
+using sb::rt::dalloc;
+using sb::rt::dalloc_ipc;
 using sb::rt::dfree;
+using sb::rt::dfree_ipc;
 using sb::rt::sync_stream;
 
 struct sb_graph {
@@ -128,13 +185,13 @@ struct sb_graph {
   std::vector<uint64_t> chunk_node, chunk_tile;
   ~sb_graph() {
     DeviceGuard dg(device);
+    if (up_stream) cudaStreamSynchronize(up_stream);
+    if (val_stream) cudaStreamSynchronize(val_stream);
     dfree(d_stream); dfree(d_rowoff); dfree(d_deg); dfree(d_orig); dfree(d_node_item);
     dfree(d_item_off); dfree(d_item_base); dfree(d_item_count); dfree(d_item_node);
     dfree(d_tile_node0); dfree(d_tile_q);
     dfree(d_run_off); dfree(d_run_s); dfree(d_run_e);
     dfree(d_cell); dfree(d_comp); dfree(d_comp_sizes);
-    if (up_stream) cudaStreamSynchronize(up_stream);
-    if (val_stream) cudaStreamSynchronize(val_stream);
     for (auto e : val_ev) cudaEventDestroy(e);
     if (up_stream) cudaStreamDestroy(up_stream);
     if (val_stream) cudaStreamDestroy(val_stream);
@@ -187,9 +244,10 @@ struct sb_hb {
   uint8_t** d_peer_chg[2] = {nullptr, nullptr};
   ~sb_hb() {
     DeviceGuard dg(g ? g->device : 0);
+    if (stream) cudaStreamSynchronize(stream);
     for (void* q : ipc_opened) cudaIpcCloseMemHandle(q);
     for (int i = 0; i < 2; ++i) { dfree(d_peer_plane[i]); dfree(d_peer_chg[i]); }
-    for (int i = 0; i < 2; ++i) { dfree(d_plane[i]); dfree(d_changed[i]); dfree(d_c[i]); }
+    for (int i = 0; i < 2; ++i) { dfree_ipc(d_plane[i]); dfree_ipc(d_changed[i]); dfree(d_c[i]); }
     dfree(d_sum_d); dfree(d_sum_d2); dfree(d_lc); dfree(d_scratch); dfree(d_counter);
     dfree(d_misc); dfree(d_tmp); dfree(d_st);
     if (h_misc) cudaFreeHost(h_misc);
@@ -223,6 +281,7 @@ struct sb_exact {
   cudaEvent_t ev[2] = {nullptr, nullptr};
   ~sb_exact() {
     DeviceGuard dg(g ? g->device : 0);
+    if (stream) cudaStreamSynchronize(stream);
     for (int i = 0; i < 2; ++i) dfree(d_plane[i]);
     dfree(d_changed); dfree(d_scratch); dfree(d_counter); dfree(d_st); dfree(d_pop);
     dfree(d_reach); dfree(d_sum); dfree(d_hist); dfree(d_misc);

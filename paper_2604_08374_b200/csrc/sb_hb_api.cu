@@ -79,30 +79,30 @@ int sb_hb_create(sb_graph* g, unsigned p, uint32_t depth_limit, uint32_t flags, 
   const uint64_t plane = g->n * h->row;
   const uint64_t nl = std::max<uint64_t>(g->n_local, 1);
   for (int i = 0; i < 2; ++i) {
-    HK(cudaMalloc(&h->d_plane[i], plane + 64));
-    HK(cudaMalloc(&h->d_changed[i], g->n));
-    HK(cudaMalloc(&h->d_c[i], nl * 8));
+    HK(dalloc_ipc(&h->d_plane[i], plane + 64));
+    HK(dalloc_ipc(&h->d_changed[i], g->n));
+    HK(dalloc(&h->d_c[i], nl * 8));
   }
-  HK(cudaMalloc(&h->d_sum_d, nl * 8));
-  HK(cudaMalloc(&h->d_sum_d2, nl * 8));
+  HK(dalloc(&h->d_sum_d, nl * 8));
+  HK(dalloc(&h->d_sum_d2, nl * 8));
   // Linear-counting table lc[z] = m * log(m / z) built with the host libm, so
   // the device never evaluates log (hll.cpp:35).
   std::vector<double> lc(m + 1, 0.0);
   const double md = static_cast<double>(m);
   for (uint32_t z = 1; z <= m; ++z) lc[z] = md * std::log(md / static_cast<double>(z));
-  HK(cudaMalloc(&h->d_lc, lc.size() * 8));
+  HK(dalloc(&h->d_lc, lc.size() * 8));
   HK(cudaMemcpy(h->d_lc, lc.data(), lc.size() * 8, cudaMemcpyHostToDevice));
   const uint64_t slice_bytes = std::min<uint64_t>(h->row, 512);
-  HK(cudaMalloc(&h->d_scratch, std::max<uint64_t>(g->n_items, 1) * h->slices * slice_bytes));
-  HK(cudaMalloc(&h->d_counter, nl * h->slices * 4));
-  HK(cudaMalloc(&h->d_misc, 4 * 8));
+  HK(dalloc(&h->d_scratch, std::max<uint64_t>(g->n_items, 1) * h->slices * slice_bytes));
+  HK(dalloc(&h->d_counter, nl * h->slices * 4));
+  HK(dalloc(&h->d_misc, 4 * 8));
   if (flags & SB_HB_INTERVAL) {
     if (const int rc = graph_wait(g)) return bail(rc);  // max_run comes from the validation pass
     // levels K = floor(log2(longest run)), capped at 10 (longer runs peel 2^K blocks)
     int K = 0;
     while (K < 10 && (2u << K) <= g->max_run) ++K;
     h->levels = K;
-    if (K) HK(cudaMalloc(&h->d_st, static_cast<uint64_t>(K) * plane + 64));
+    if (K) HK(dalloc(&h->d_st, static_cast<uint64_t>(K) * plane + 64));
     const int rc = build_run_index(g);
     if (rc) return bail(rc);
   }
@@ -363,7 +363,7 @@ static int ensure_tmp(sb_hb* h, uint64_t bytes) {
   if (h->tmp_bytes >= bytes) return SB_OK;
   dfree(h->d_tmp);
   h->tmp_bytes = 0;
-  CK(cudaMalloc(&h->d_tmp, bytes));
+  CK(dalloc(&h->d_tmp, bytes));
   h->tmp_bytes = bytes;
   return SB_OK;
 }
@@ -564,8 +564,8 @@ int sb_hb_attach_peers(sb_hb* h, int nranks, int rank, const void* handles, cons
   }
   const int np = nranks - 1;
   for (int i = 0; i < 2; ++i) {
-    CK(cudaMalloc(&h->d_peer_plane[i], std::max(np, 1) * sizeof(uint8_t*)));
-    CK(cudaMalloc(&h->d_peer_chg[i], std::max(np, 1) * sizeof(uint8_t*)));
+    CK(dalloc(&h->d_peer_plane[i], std::max(np, 1) * sizeof(uint8_t*)));
+    CK(dalloc(&h->d_peer_chg[i], std::max(np, 1) * sizeof(uint8_t*)));
     if (np) {
       CK(cudaMemcpy(h->d_peer_plane[i], pl[i].data(), np * sizeof(uint8_t*), cudaMemcpyHostToDevice));
       CK(cudaMemcpy(h->d_peer_chg[i], ch[i].data(), np * sizeof(uint8_t*), cudaMemcpyHostToDevice));

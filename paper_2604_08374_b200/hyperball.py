@@ -35,6 +35,11 @@ class HllParams:
         return f"HllParams(p={self.p})"
 
 
+def release_cached_memory(device: int = 0) -> None:
+    """Return the device memory cached by freed graphs / HyperBall states to the driver."""
+    check(lib().sb_release_cached_memory(device))
+
+
 def check_convergence(max_increase: float) -> bool:
     """True iff max_increase <= 0.5 (inclusive)."""
     return bool(lib().sb_check_convergence(float(max_increase)))

@@ -286,6 +286,28 @@ def test_gpu_determinism_and_reset(c1):
     assert np.array_equal(a.registers, b.registers) and np.array_equal(a.sum_d, b.sum_d)
 
 
+def test_gpu_pool_reuse_and_release(c1):
+    """Freed graph / HyperBall buffers are cached in the stream-ordered pool and reused
+    by the next create (same results every cycle); release_cached_memory trims it."""
+    from paper_2604_08374_b200 import release_cached_memory
+    ref = None
+    for cycle in range(4):
+        dg = DeviceGraph(c1, async_upload=cycle % 2 == 1)
+        hb = HyperBall(dg, HllParams(10), None)
+        hb.run()
+        sd, regs = hb.state().sum_d, hb.registers()
+        del hb, dg
+        if ref is None:
+            ref = (sd, regs)
+        assert np.array_equal(sd, ref[0]) and np.array_equal(regs, ref[1]), cycle
+    release_cached_memory(0)
+    with pytest.raises(ValueError):
+        release_cached_memory(1 << 20)
+    hb = HyperBall(c1, 10, None)  # allocations after a trim
+    hb.run()
+    assert np.array_equal(hb.state().sum_d, ref[0])
+
+
 def test_gpu_hilbert_permutation_equivariance(c1):
     """Hashing original ids makes reordering layout-only."""
     h = c1.hilbert_reorder()
