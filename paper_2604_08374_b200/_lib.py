@@ -123,6 +123,22 @@ EXPORTED = tuple(_SIGS)
 _lib = None
 
 
+def _preload_torch_nccl() -> None:
+    """Load the NCCL that torch ships (the nvidia-nccl wheel) before this library, so
+    both bind one libnccl.so.2 whichever is imported first.  Otherwise loading this
+    library first binds the system NCCL and a later `import torch` fails on symbols
+    only the wheel's newer NCCL has."""
+    try:
+        import nvidia.nccl as nn
+    except ImportError:
+        return
+    for d in getattr(nn, "__path__", []):
+        so = os.path.join(d, "lib", "libnccl.so.2")
+        if os.path.exists(so):
+            C.CDLL(so, mode=C.RTLD_GLOBAL)
+            return
+
+
 def lib() -> C.CDLL:
     """Load the in-tree shared object (fails loudly if it was not built)."""
     global _lib
@@ -131,6 +147,7 @@ def lib() -> C.CDLL:
             raise ImportError(
                 f"{LIB_PATH} is missing: build it with `make` or __graft_entry__.build(); "
                 "the HyperBall path has no CPU fallback")
+        _preload_torch_nccl()
         L = C.CDLL(LIB_PATH)
         for name, (res, args) in _SIGS.items():
             f = getattr(L, name)

@@ -72,12 +72,12 @@ int sb_exact_create(sb_graph* g, unsigned log2_block, uint32_t depth_limit, uint
   XK(cudaMemset(x->d_sum, 0, 2 * n * 8));
   XK(dalloc(&x->d_misc, 2 * 8));
   if (flags & SB_HB_INTERVAL) {
+    const int rc = build_run_index(g);  // sets max_run
+    if (rc) return bail(rc);
     int K = 0;
     while (K < 10 && (2u << K) <= g->max_run) ++K;
     x->levels = K;
     if (K) XK(dalloc(&x->d_st, static_cast<uint64_t>(K) * plane + 64));
-    const int rc = build_run_index(g);
-    if (rc) return bail(rc);
   }
 #undef XK
   const int rc = exact_grow_hist(x, 15);

@@ -9,8 +9,12 @@
 #include "sb_device.cuh"
 #include "sb_handles.h"
 
+// Also sets g->max_run (longest run within a work item; sizes the interval
+// mode's sparse table).
 int build_run_index(sb_graph* g) {
   if (g->d_run_off || g->n_items == 0) return SB_OK;
+  if (const int rc = graph_wait(g)) return rc;
+  if (reinterpret_cast<uintptr_t>(g->d_stream) & 15) return fail(SB_ERUNTIME, "internal: stream not 16-B aligned");
   sb::RunIndexArgs a{};
   a.stream = g->d_stream;
   a.stream_len = g->stream_local;
@@ -19,10 +23,13 @@ int build_run_index(sb_graph* g) {
   a.item_count = g->d_item_count;
   a.n_items = g->n_items;
   uint64_t* d_cnt = nullptr;
-  CK(dalloc(&d_cnt, g->n_items * 8));
+  CK(dalloc(&d_cnt, g->n_items * 8 + 8));
   a.run_count = d_cnt;
+  a.max_run = reinterpret_cast<unsigned int*>(d_cnt + g->n_items);
+  CK(cudaMemsetAsync(a.max_run, 0, 4, 0));
   CK(sb::launch_run_index(a, false, 0));
   CK(sync_stream(0));
+  CK(cudaMemcpy(&g->max_run, a.max_run, 4, cudaMemcpyDeviceToHost));
   std::vector<uint64_t> off(g->n_items + 1, 0);
   CK(cudaMemcpy(off.data() + 1, d_cnt, g->n_items * 8, cudaMemcpyDeviceToHost));
   dfree(d_cnt);
@@ -129,6 +136,7 @@ static int graph_setup_host(sb_graph* g, const uint32_t* deg_local) {
 // increasing ids < n, exactly degrees[v] ids) + work items; errors land in d_err.
 static cudaError_t launch_validate(sb_graph* g, uint64_t n0, uint64_t n1, cudaStream_t s) {
   if (n1 <= n0) return cudaSuccess;
+  if (reinterpret_cast<uintptr_t>(g->d_stream) & 15) return cudaErrorMisalignedAddress;  // 16-B window loads
   sb::BuildArgs a{};
   a.stream = g->d_stream;
   a.row_off = g->d_rowoff;
@@ -144,14 +152,12 @@ static cudaError_t launch_validate(sb_graph* g, uint64_t n0, uint64_t n1, cudaSt
   a.item_count = g->d_item_count;
   a.item_node = g->d_item_node;
   a.err_node = g->d_err;
-  a.max_run = reinterpret_cast<unsigned int*>(g->d_err + 1);
   return sb::launch_build_items(a, s);
 }
 
 static int graph_check(sb_graph* g) {
   unsigned long long err = 0;
   CK(cudaMemcpy(&err, g->d_err, 8, cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(&g->max_run, g->d_err + 1, 4, cudaMemcpyDeviceToHost));
   if (err != ~0ull) {
     g->broken = 1;
     return fail(SB_ERUNTIME, "cgraph: malformed compressed row at node %llu (bad varint, "
@@ -239,16 +245,18 @@ static int graph_create(uint64_t n, const uint64_t* offsets, const uint32_t* deg
     *out = g;
     return SB_OK;
   }
-  // Asynchronous: K chunks of ~equal stream bytes on 8-node (tile group)
-  // boundaries; copy k on up_stream, validation k on val_stream after copy k.
+  // Asynchronous: a small first chunk (1/64 of the bytes, so the first union
+  // tiles start early) then K-1 chunks of ~equal stream bytes, on 8-node (tile
+  // group) boundaries; copy k on up_stream, validation k on val_stream after copy k.
   const int rc = graph_setup_host(g, degrees + node_begin);
   if (rc) return bail(rc);
   GK(cudaStreamCreateWithFlags(&g->up_stream, cudaStreamNonBlocking));
   GK(cudaStreamCreateWithFlags(&g->val_stream, cudaStreamNonBlocking));
   const int K = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(16, g->n_local / 64)));
+  const uint64_t first = K > 1 ? g->stream_local / 64 : 0;
   g->chunk_node.assign(1, 0);
   for (int k = 1; k < K; ++k) {
-    const uint64_t goal = b0 + g->stream_local * k / K;
+    const uint64_t goal = b0 + first + (g->stream_local - first) * (k - 1) / (K - 1);
     uint64_t v = std::lower_bound(offsets + node_begin, offsets + node_end, goal) - (offsets + node_begin);
     v = std::min<uint64_t>(v & ~7ull, g->n_local);
     if (v > g->chunk_node.back()) g->chunk_node.push_back(v);

@@ -233,6 +233,11 @@ struct sb_hb {
   double alpha = 0.0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  // first pass over a graph still uploading: second stream + per-chunk work counters
+  cudaStream_t stream2 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  unsigned long long* d_chunk_work = nullptr;
+  size_t chunk_work_n = 0;
   std::vector<sb_iter_stats> stats;
   sb_iter_stats cur_stats{};
   sb_comm* comm = nullptr;
@@ -245,14 +250,18 @@ struct sb_hb {
   ~sb_hb() {
     DeviceGuard dg(g ? g->device : 0);
     if (stream) cudaStreamSynchronize(stream);
+    if (stream2) cudaStreamSynchronize(stream2);
     for (void* q : ipc_opened) cudaIpcCloseMemHandle(q);
     for (int i = 0; i < 2; ++i) { dfree(d_peer_plane[i]); dfree(d_peer_chg[i]); }
     for (int i = 0; i < 2; ++i) { dfree_ipc(d_plane[i]); dfree_ipc(d_changed[i]); dfree(d_c[i]); }
     dfree(d_sum_d); dfree(d_sum_d2); dfree(d_lc); dfree(d_scratch); dfree(d_counter);
-    dfree(d_misc); dfree(d_tmp); dfree(d_st);
+    dfree(d_misc); dfree(d_tmp); dfree(d_st); dfree(d_chunk_work);
     if (h_misc) cudaFreeHost(h_misc);
     for (auto& e : ev) if (e) cudaEventDestroy(e);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
     if (stream) cudaStreamDestroy(stream);
+    if (stream2) cudaStreamDestroy(stream2);
   }
 };
 

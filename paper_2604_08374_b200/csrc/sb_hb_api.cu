@@ -97,14 +97,13 @@ int sb_hb_create(sb_graph* g, unsigned p, uint32_t depth_limit, uint32_t flags, 
   HK(dalloc(&h->d_counter, nl * h->slices * 4));
   HK(dalloc(&h->d_misc, 4 * 8));
   if (flags & SB_HB_INTERVAL) {
-    if (const int rc = graph_wait(g)) return bail(rc);  // max_run comes from the validation pass
+    const int rc = build_run_index(g);  // waits for an asynchronous upload; sets max_run
+    if (rc) return bail(rc);
     // levels K = floor(log2(longest run)), capped at 10 (longer runs peel 2^K blocks)
     int K = 0;
     while (K < 10 && (2u << K) <= g->max_run) ++K;
     h->levels = K;
     if (K) HK(dalloc(&h->d_st, static_cast<uint64_t>(K) * plane + 64));
-    const int rc = build_run_index(g);
-    if (rc) return bail(rc);
   }
   HK(cudaMallocHost(&h->h_misc, 4 * 8));
 #undef HK
@@ -190,17 +189,37 @@ int sb_hb_step_compute(sb_hb* h, double* local_max) {
     } else if (g->pending) {
       // First pass over a graph still streaming in: chunk k's tiles start as
       // soon as its bytes are copied and validated (overlaps PCIe with compute).
-      for (size_t k = 0; k + 1 < g->chunk_node.size(); ++k) {
+      // Consecutive chunks alternate between two streams (own work counters),
+      // so chunk k+1's CTAs fill the SMs chunk k's last tiles leave idle.
+      const size_t nk = g->chunk_node.size() - 1;
+      if (!h->stream2) {
+        CK(cudaStreamCreateWithFlags(&h->stream2, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
+      }
+      if (h->chunk_work_n < nk) {
+        dfree(h->d_chunk_work);
+        h->chunk_work_n = 0;
+        CK(dalloc(&h->d_chunk_work, nk * 8));
+        h->chunk_work_n = nk;
+      }
+      CK(cudaMemsetAsync(h->d_chunk_work, 0, nk * 8, h->stream));
+      CK(cudaEventRecord(h->ev_fork, h->stream));
+      CK(cudaStreamWaitEvent(h->stream2, h->ev_fork, 0));
+      for (size_t k = 0; k < nk; ++k) {
         const uint64_t t0 = g->chunk_tile[k], t1 = g->chunk_tile[k + 1];
         if (t1 == t0) continue;
-        CK(cudaStreamWaitEvent(h->stream, g->val_ev[k], 0));
-        CK(cudaMemsetAsync(h->d_misc, 0, 8, h->stream));  // work counter
+        cudaStream_t sk = (k & 1) ? h->stream2 : h->stream;
+        CK(cudaStreamWaitEvent(sk, g->val_ev[k], 0));
         sb::UnionArgs uk = u;
+        uk.work = h->d_chunk_work + k;
         uk.tile_node0 = g->d_tile_node0 + t0;
         uk.tile_q = g->d_tile_q + t0;
         uk.n_tiles = t1 - t0;
-        CK(sb::launch_union(static_cast<int>(h->p), skip, uk, h->stream));
+        CK(sb::launch_union(static_cast<int>(h->p), skip, uk, sk));
       }
+      CK(cudaEventRecord(h->ev_join, h->stream2));
+      CK(cudaStreamWaitEvent(h->stream, h->ev_join, 0));
     } else {
       CK(sb::launch_union(static_cast<int>(h->p), skip, u, h->stream));
     }

@@ -19,7 +19,6 @@ struct BuildArgs {
   uint32_t* item_count;
   uint32_t* item_node;
   unsigned long long* err_node;  // min local node with a malformed row (~0 = none)
-  unsigned int* max_run;         // longest run of consecutive neighbour ids (interval mode)
 };
 
 struct UnionArgs {
@@ -71,6 +70,7 @@ struct RunIndexArgs {
   const uint32_t* item_count;
   uint64_t n_items;
   uint64_t* run_count;         // count pass: runs per item
+  unsigned int* max_run;       // count pass: longest run within an item
   const uint64_t* run_off;     // fill pass: offsets (n_items + 1)
   uint32_t* run_s;
   uint32_t* run_e;

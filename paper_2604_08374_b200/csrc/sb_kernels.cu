@@ -26,144 +26,192 @@
 namespace sb {
 
 // ------------------------------------------------------------------ build
-// Upload-time validation and work-item cutting: one warp per row, 128-byte
-// windows at 4 bytes per lane (the decode_step4 arithmetic), the next lines
-// prefetched into L2 -- the pass is a latency-bound stream (one dependent
-// window per warp at a time), so keeping lines in flight is what sets its
-// speed.  Bytes at or past the row end read as continuation bytes, so they
-// never form a terminator: a truncated row runs out of terminators and a
-// longer one leaves trailing bytes, both reported.  Checks (leb128.hpp:28-39,
-// SPEC.md:174-177): varint <= 5 bytes and < 2^32, id < N, ids strictly
-// increasing (no zero delta, no 32-bit wrap), exactly deg ids, no trailing bytes.
+// Upload-time validation and work-item cutting (leb128.hpp:28-39, SPEC.md:
+// 174-177, restricted to 32-bit ids).  A row is valid iff
+//   * no varint is longer than 5 bytes,
+//   * it holds exactly deg varints and ends on a terminator (no truncation,
+//     no trailing bytes),
+//   * no varint after the first has value 0 (ids strictly increasing),
+//   * the sum of its varints -- the last id -- is < N (so no id is >= N and no
+//     32-bit wrap: every delta is >= 1).
+// All four are reductions over the row's bytes, so one warp streams a row in
+// 512-byte windows (16 bytes per lane, byte-parallel SWAR on 32-bit words)
+// and reduces across lanes once per row; only the windows holding an item cut
+// (rows with deg > chunk) run a warp scan to place the cut and its base id.
+// The previous 8 bytes of the window come from the neighbour lane (or the
+// previous window), since a varint's value depends on up to 4 bytes before its
+// terminator.  Bytes outside the row read as 0x00: counted nowhere, and as
+// look-back they look like a terminator, i.e. the row starts on a varint boundary.
 __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 
-__global__ void __launch_bounds__(256) build_items_kernel(BuildArgs a) {
+// 0x80 in every byte of x whose low 7 bits are zero.
+__device__ __forceinline__ uint32_t zero_payload(uint32_t x) {
+  return ~((x & 0x7f7f7f7fu) + 0x7f7f7f7fu) & 0x80808080u;
+}
+
+__global__ void __launch_bounds__(256, 3) build_items_kernel(BuildArgs a) {
   const int lane = threadIdx.x & 31;
-  const uint32_t ltm = (1u << lane) - 1u;
   const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = (gridDim.x * (uint64_t)blockDim.x) >> 5;
   const uint64_t node_end = a.node_end ? a.node_end : a.n_local;
   for (uint64_t node = a.node_begin + gw; node < node_end; node += nw) {
-    uint64_t pos = a.row_off[node];
+    const uint64_t pos0 = a.row_off[node];
     const uint64_t end = a.row_off[node + 1];
     const uint32_t deg = a.degrees[node];
     const uint32_t i0 = a.node_item[node];
     if (lane == 0) {
-      a.item_off[i0] = pos;
+      a.item_off[i0] = pos0;
       a.item_base[i0] = 0;
       a.item_count[i0] = deg < a.chunk ? deg : a.chunk;
       a.item_node[i0] = static_cast<uint32_t>(node);
     }
-    uint32_t rem = deg, base = 0, k0 = 0, run_start = 0, maxrun = 0;
-    bool bad = false;
-    while (rem > 0) {
-      if (lane < 2 && pos + 256 + 128 * lane < end) prefetch_l2(a.stream + pos + 256 + 128 * lane);
-      const uint8_t* al = a.stream + (pos & ~3ull) + 4 * lane;
-      const uint32_t w0 = ld_stream_word(al);
-      const uint32_t w1 = ld_stream_word(al + 4);
-      uint32_t w = __funnelshift_r(w0, w1, static_cast<uint32_t>(pos & 3) * 8);
-      const int64_t q = static_cast<int64_t>(end - pos) - 4 * lane;  // row bytes left at this lane
-      if (q < 4) w |= q <= 0 ? 0x80808080u : (0x80808080u << (8 * q));
-      uint32_t wp = __shfl_up_sync(FULL, w, 1), wpp = __shfl_up_sync(FULL, w, 2);
-      if (lane < 1) wp = 0;  // the window starts on a varint boundary
-      if (lane < 2) wpp = 0;
-      const uint32_t F = w & 0x80808080u, Fp = wp & 0x80808080u, Fpp = wpp & 0x80808080u;
-      const uint32_t m1 = __funnelshift_l(Fp, F, 8);
-      const uint32_t m2 = m1 & __funnelshift_l(Fp, F, 16);
-      const uint32_t m3 = m2 & __funnelshift_l(Fp, F, 24);
-      const uint32_t m4 = m3 & Fp;
-      const uint32_t m5 = m4 & __funnelshift_l(Fpp, Fp, 8);  // >= 5 continuation bytes: too long
-      const uint32_t D = (m1 >> 7) + (m2 >> 7) + (m3 >> 7) + (m4 >> 7);
-      uint32_t c[4], dk[4], vl[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        dk[k] = (D >> (8 * k)) & 0xffu;
-        c[k] = ((w >> (8 * k)) & 0x7fu) << (7 * dk[k]);
-        vl[k] = c[k] + ((k >= 1 && dk[k] >= 1) ? vl[k > 0 ? k - 1 : 0] : 0u);
-      }
-      uint32_t vp3 = __shfl_up_sync(FULL, vl[3], 1);
-      if (lane == 0) vp3 = 0;
-      const uint32_t p1 = c[0] + c[1], p2 = p1 + c[2], lane_sum = p2 + c[3];
-      uint32_t incl = lane_sum;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t y = __shfl_up_sync(FULL, incl, d);
-        if (lane >= d) incl += y;
-      }
-      const uint32_t excl = base + incl - lane_sum;
-      const uint32_t id[4] = {excl + c[0], excl + p1, excl + p2, excl + lane_sum};
-      const uint32_t T = ~w & 0x80808080u;
-      uint32_t below = 0, tot = 0;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const uint32_t B = __ballot_sync(FULL, (T >> (8 * k + 7)) & 1u);
-        below += __popc(B & ltm);
-        tot += __popc(B);
-      }
-      uint32_t r = below, jj[4];
-      bool start[4], lane_bad = false;
-      int lastk = -1;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const bool t = (T >> (8 * k + 7)) & 1u;
-        const bool want = t && r < rem;
-        jj[k] = k0 + r;  // neighbour index within the row
-        start[k] = false;
-        if (want) {
-          const uint32_t v = vl[k] + (dk[k] > static_cast<uint32_t>(k) ? vp3 : 0u);  // this varint's value
-          if (((m5 >> (8 * k + 7)) & 1u) || (dk[k] == 4 && ((w >> (8 * k)) & 0x7fu) > 0x0fu)) lane_bad = true;
-          if (id[k] >= a.n_global) lane_bad = true;
-          if (jj[k] > 0 && (v == 0 || id[k] < v)) lane_bad = true;  // zero delta or 32-bit wrap
-          if ((jj[k] + 1) % a.chunk == 0 && jj[k] + 1 < deg) {
-            const uint32_t it = i0 + (jj[k] + 1) / a.chunk;
-            a.item_off[it] = pos + 4 * lane + k + 1;
-            a.item_base[it] = id[k];
-            a.item_count[it] = (deg - (jj[k] + 1)) < a.chunk ? deg - (jj[k] + 1) : a.chunk;
-            a.item_node[it] = static_cast<uint32_t>(node);
-          }
-          start[k] = jj[k] == 0 || v != 1u;  // a delta of 1 continues the run of consecutive ids
-          lastk = k;
-        }
-        r += t;
-      }
-      const uint32_t anyw = __ballot_sync(FULL, lastk >= 0);
-      if (__any_sync(FULL, lane_bad) || anyw == 0) {  // anyw == 0: the row ran out of bytes
-        bad = true;
-        break;
-      }
-      // longest run of consecutive ids (sizes the interval-mode sparse table)
-      int hs = -1;
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-        if (start[k]) hs = k;
-      const uint32_t A = __ballot_sync(FULL, hs >= 0);
-      const uint32_t lastSj = sel4(jj, hs);
-      const uint32_t Ab = A & ltm;
-      const uint32_t pj = __shfl_sync(FULL, lastSj, Ab ? 31 - __clz(Ab) : 0);
-      bool have = Ab ? true : k0 > 0;
-      uint32_t ps = Ab ? pj : run_start;
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-        if (start[k]) {
-          if (have) maxrun = max(maxrun, jj[k] - ps);
-          have = true;
-          ps = jj[k];
-        }
-      if (A) run_start = __shfl_sync(FULL, lastSj, 31 - __clz(A));
-      const int L = 31 - __clz(anyw);
-      const int lk = __shfl_sync(FULL, lastk, L);
-      const uint32_t wanted = tot < rem ? tot : rem;
-      base = __shfl_sync(FULL, sel4(id, lk), L);
-      pos += 4 * L + lk + 1;
-      rem -= wanted;
-      k0 += wanted;
+    if (deg == 0 || end <= pos0) {
+      if (lane == 0 && (deg != 0 || end != pos0)) atomicMin(a.err_node, static_cast<unsigned long long>(node));
+      continue;
     }
-    if (!bad && pos != end) bad = true;  // trailing bytes in the row
-    if (bad && lane == 0) atomicMin(a.err_node, static_cast<unsigned long long>(node));
-    if (deg > 0) maxrun = max(maxrun, deg - run_start);
+    uint32_t cnt = 0, zeros = 0, bad = 0;  // per lane
+    unsigned long long sum = 0;            // per lane: sum of its varint contributions
+    uint32_t px2 = 0, px3 = 0;             // words 2, 3 of the previous window's lane 31
+    uint32_t done = 0;                     // terminators before this window (cut rows only)
+    unsigned long long done_sum = 0;       // their contributions
+    uint32_t next_cut = a.chunk;           // row index of the next item's first id
+    for (uint64_t wb = pos0 & ~15ull; wb < end; wb += 512) {
+      if (lane < 4 && wb + 1024 + 128 * lane < end) prefetch_l2(a.stream + wb + 1024 + 128 * lane);
+      const uint64_t lb = wb + 16 * lane;  // this lane's first byte
+      uint32_t x[4] = {0u, 0u, 0u, 0u};
+      if (lb < end) {
+        const uint4 q = __ldg(reinterpret_cast<const uint4*>(a.stream + lb));
+        x[0] = q.x;
+        x[1] = q.y;
+        x[2] = q.z;
+        x[3] = q.w;
+      }
+      // valid-byte flags (0x80 per byte in [pos0, end)); invalid bytes -> 0x00
+      uint32_t vm[4];
 #pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) maxrun = max(maxrun, __shfl_xor_sync(FULL, maxrun, o));
-    if (lane == 0 && maxrun) atomicMax(a.max_run, maxrun);
+      for (int i = 0; i < 4; ++i) {
+        const int64_t lo = static_cast<int64_t>(pos0) - static_cast<int64_t>(lb + 4 * i);  // bytes below pos0
+        const int64_t hi = static_cast<int64_t>(end) - static_cast<int64_t>(lb + 4 * i);   // bytes below end
+        uint32_t m = 0x80808080u;
+        if (lo > 0) m = lo >= 4 ? 0u : m << (8 * lo);
+        if (hi < 4) m &= hi <= 0 ? 0u : 0x80808080u >> (8 * (4 - hi));
+        vm[i] = m;
+        x[i] &= (m >> 7) * 0xffu;
+      }
+      uint32_t p3 = __shfl_up_sync(FULL, x[3], 1), p2 = __shfl_up_sync(FULL, x[2], 1);
+      if (lane == 0) {
+        p3 = px3;
+        p2 = px2;
+      }
+      px3 = __shfl_sync(FULL, x[3], 31);
+      px2 = __shfl_sync(FULL, x[2], 31);
+      uint32_t lcnt = 0, tw[4];
+      unsigned long long lsum = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t w = x[i];
+        const uint32_t wp = i >= 1 ? x[i - 1] : p3;
+        const uint32_t wpp = i >= 2 ? x[i - 2] : (i == 1 ? p3 : p2);
+        const uint32_t F = w & 0x80808080u, Fp = wp & 0x80808080u, Fpp = wpp & 0x80808080u;
+        const uint32_t m1 = __funnelshift_l(Fp, F, 8);
+        const uint32_t m2 = m1 & __funnelshift_l(Fp, F, 16);
+        const uint32_t m3 = m2 & __funnelshift_l(Fp, F, 24);
+        const uint32_t m4 = m3 & Fp;
+        const uint32_t m5 = m4 & __funnelshift_l(Fpp, Fp, 8);
+        bad |= m5 & vm[i];  // a varint longer than 5 bytes
+        const uint32_t T = ~w & 0x80808080u & vm[i];
+        tw[i] = T;
+        lcnt += __popc(T);
+        // zero-valued varint: terminator whose payload and whole look-back chain are zero
+        const uint32_t z = zero_payload(w), zp = zero_payload(wp);
+        const uint32_t z1 = __funnelshift_l(zp, z, 8), z2 = __funnelshift_l(zp, z, 16);
+        const uint32_t z3 = __funnelshift_l(zp, z, 24), z4 = zp;
+        zeros += __popc(T & z & (~m1 | z1) & (~m2 | z2) & (~m3 | z3) & (~m4 | z4));
+        const uint32_t D = (m1 >> 7) + (m2 >> 7) + (m3 >> 7) + (m4 >> 7);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t dk = (D >> (8 * k)) & 0xffu;
+          lsum += static_cast<unsigned long long>((w >> (8 * k)) & 0x7fu) << (7 * dk);
+        }
+      }
+      cnt += lcnt;
+      sum += lsum;
+      if (next_cut < deg) {  // warp-uniform: this row is cut into several items
+        uint32_t incl = lcnt;
+        unsigned long long sincl = lsum;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const uint32_t y = __shfl_up_sync(FULL, incl, d);
+          const unsigned long long ys = __shfl_up_sync(FULL, sincl, d);
+          if (lane >= d) {
+            incl += y;
+            sincl += ys;
+          }
+        }
+        const uint32_t excl = incl - lcnt;
+        const uint32_t want = next_cut - 1 - done;  // window rank of the last id before the cut
+        if (done + incl > next_cut - 1 && want >= excl && want < incl) {
+          // this lane holds it: walk its bytes in order
+          uint32_t r = excl;
+          unsigned long long part = done_sum + (sincl - lsum);
+          bool found = false;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const uint32_t w = x[i];
+            const uint32_t wp = i >= 1 ? x[i - 1] : p3;
+            const uint32_t F = w & 0x80808080u, Fp = wp & 0x80808080u;
+            const uint32_t m1 = __funnelshift_l(Fp, F, 8);
+            const uint32_t m2 = m1 & __funnelshift_l(Fp, F, 16);
+            const uint32_t m3 = m2 & __funnelshift_l(Fp, F, 24);
+            const uint32_t m4 = m3 & Fp;
+            const uint32_t D = (m1 >> 7) + (m2 >> 7) + (m3 >> 7) + (m4 >> 7);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              if (!found) {
+                const uint32_t dk = (D >> (8 * k)) & 0xffu;
+                part += static_cast<unsigned long long>((w >> (8 * k)) & 0x7fu) << (7 * dk);
+                if ((tw[i] >> (8 * k + 7)) & 1u) {
+                  if (r == want) {
+                    found = true;
+                    const uint32_t it = i0 + next_cut / a.chunk;
+                    a.item_off[it] = lb + 4 * i + k + 1;
+                    a.item_base[it] = static_cast<uint32_t>(part);
+                    a.item_count[it] = (deg - next_cut) < a.chunk ? deg - next_cut : a.chunk;
+                    a.item_node[it] = static_cast<uint32_t>(node);
+                  }
+                  ++r;
+                }
+              }
+            }
+          }
+        }
+        const uint32_t wtot = __shfl_sync(FULL, incl, 31);
+        if (done + wtot >= next_cut) next_cut += a.chunk;  // at most one cut per window (chunk >= 512)
+        done += wtot;
+        done_sum += __shfl_sync(FULL, sincl, 31);
+      }
+    }
+    // row totals
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      cnt += __shfl_xor_sync(FULL, cnt, o);
+      zeros += __shfl_xor_sync(FULL, zeros, o);
+      bad |= __shfl_xor_sync(FULL, bad, o);
+      sum += __shfl_xor_sync(FULL, sum, o);
+    }
+    if (lane == 0) {
+      // the first varint (the absolute first id) may be 0
+      bool first_zero = true;
+      for (uint64_t b = pos0; b < end; ++b) {
+        const uint8_t c = a.stream[b];
+        if (c & 0x7fu) first_zero = false;
+        if (!(c & 0x80u)) break;
+      }
+      const bool ends_on_terminator = !(a.stream[end - 1] & 0x80u);
+      const bool ok = !bad && cnt == deg && ends_on_terminator && zeros == (first_zero ? 1u : 0u) &&
+                      sum < a.n_global;
+      if (!ok) atomicMin(a.err_node, static_cast<unsigned long long>(node));
+    }
   }
 }
 
@@ -545,6 +593,7 @@ __global__ void __launch_bounds__(256) run_index_kernel(RunIndexArgs a) {
     uint32_t ostart = 0;
     uint64_t out = FILL ? a.run_off[item] : 0;
     int nr = 0;
+    uint32_t longest = 0;  // count pass: longest run (sizes the interval-mode sparse table)
     while (rem > 0) {
       if (lane < 2 && pos + 256 + 128 * lane < a.stream_len) prefetch_l2(a.stream + pos + 256 + 128 * lane);
       __syncwarp();
@@ -556,6 +605,8 @@ __global__ void __launch_bounds__(256) run_index_kernel(RunIndexArgs a) {
       nr += o.emitted;
       if (nr >= 32) {
         __syncwarp();
+        if (!FILL)
+          for (int i = lane; i < nr; i += 32) longest = max(longest, re[i] - rs[i] + 1u);
         if (FILL)
           for (int i = lane; i < nr; i += 32) {
             a.run_s[out + i] = rs[i];
@@ -580,7 +631,15 @@ __global__ void __launch_bounds__(256) run_index_kernel(RunIndexArgs a) {
         a.run_e[out + i] = re[i];
       }
     out += nr;
-    if (!FILL && lane == 0) a.run_count[item] = out;
+    if (!FILL) {
+      for (int i = lane; i < nr; i += 32) longest = max(longest, re[i] - rs[i] + 1u);
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) longest = max(longest, __shfl_xor_sync(FULL, longest, o));
+      if (lane == 0) {
+        a.run_count[item] = out;
+        if (longest) atomicMax(a.max_run, longest);
+      }
+    }
   }
 }
 

@@ -78,3 +78,15 @@ def test_version_and_last_error_strings():
     from paper_2604_08374_b200 import lib
     assert b"sm_100a" in lib().sb_version()
     assert isinstance(lib().sb_last_error(), bytes)
+
+
+def test_library_then_torch_import_order():
+    """Loading libsieveball_cuda before torch must not pin the system NCCL under torch."""
+    import subprocess
+    import sys
+    code = ("import paper_2604_08374_b200 as P; P.lib()\n"
+            "import torch, torch.distributed\n"
+            "print('ok')\n")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
