@@ -328,127 +328,4 @@ __device__ __forceinline__ Decode4 decode_step4(const uint8_t* __restrict__ stre
   return o;
 }
 
-// ---- 128-byte LEB128 decode straight to runs of consecutive ids ----------
-// Same window arithmetic as decode_step4, plus the varint value of every
-// terminator: v_k = sum of this varint's byte contributions (a segmented sum
-// over <= 5 bytes, at most one lane back).  A terminator CONTINUES the open run
-// iff its value is exactly 1; otherwise it starts a run and closes the
-// previous one at id - v (the preceding id).  Closed runs [s, e] are appended
-// to rs/re[nr..]; the open run (ostart) is carried across windows.
-struct RunWindow {
-  int wanted;     // terminators consumed
-  int advance;    // bytes consumed
-  uint32_t last;  // last wanted id
-  int emitted;    // runs appended
-};
-
-__device__ __forceinline__ RunWindow decode_runs4(const uint8_t* __restrict__ stream, uint64_t pos,
-                                                  uint32_t remaining, uint32_t base, bool& open,
-                                                  uint32_t& ostart, uint32_t* rs, uint32_t* re, int nr,
-                                                  int lane) {
-  const uint8_t* al = stream + (pos & ~3ull) + 4 * lane;
-  const uint32_t w0 = ld_stream_word(al);
-  const uint32_t w1 = ld_stream_word(al + 4);
-  const uint32_t w = __funnelshift_r(w0, w1, static_cast<uint32_t>(pos & 3) * 8);
-  uint32_t wp = __shfl_up_sync(FULL, w, 1);
-  if (lane == 0) wp = 0;
-  const uint32_t F = w & 0x80808080u, Fp = wp & 0x80808080u;
-  const uint32_t m1 = __funnelshift_l(Fp, F, 8);
-  const uint32_t m2 = m1 & __funnelshift_l(Fp, F, 16);
-  const uint32_t m3 = m2 & __funnelshift_l(Fp, F, 24);
-  const uint32_t m4 = m3 & Fp;
-  const uint32_t D = (m1 >> 7) + (m2 >> 7) + (m3 >> 7) + (m4 >> 7);
-  uint32_t c[4], dk[4], vl[4];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    dk[k] = (D >> (8 * k)) & 0xffu;
-    c[k] = ((w >> (8 * k)) & 0x7fu) << (7 * dk[k]);
-    vl[k] = c[k] + ((k >= 1 && dk[k] >= 1) ? vl[k > 0 ? k - 1 : 0] : 0u);
-  }
-  uint32_t vp3 = __shfl_up_sync(FULL, vl[3], 1);
-  if (lane == 0) vp3 = 0;
-  const uint32_t p1 = c[0] + c[1], p2 = p1 + c[2], lane_sum = p2 + c[3];
-  uint32_t incl = lane_sum;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const uint32_t y = __shfl_up_sync(FULL, incl, d);
-    if (lane >= d) incl += y;
-  }
-  const uint32_t excl = base + incl - lane_sum;
-  const uint32_t id[4] = {excl + c[0], excl + p1, excl + p2, excl + lane_sum};
-  const uint32_t T = ~w & 0x80808080u;
-  const uint32_t ltm = (1u << lane) - 1u;
-  uint32_t below = 0, tot = 0;
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const uint32_t B = __ballot_sync(FULL, (T >> (8 * k + 7)) & 1u);
-    below += __popc(B & ltm);
-    tot += __popc(B);
-  }
-  bool want[4], start[4];
-  uint32_t r = below;
-  int lastk = -1;
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const bool t = (T >> (8 * k + 7)) & 1u;
-    want[k] = t && r < remaining;
-    const uint32_t v = vl[k] + (dk[k] > static_cast<uint32_t>(k) ? vp3 : 0u);
-    start[k] = want[k] && (v != 1u || (!open && r == 0));
-    r += t;
-    if (want[k]) lastk = k;
-  }
-  RunWindow o;
-  o.wanted = static_cast<int>(tot < remaining ? tot : remaining);
-  o.advance = 0;
-  o.last = base;
-  o.emitted = 0;
-  const uint32_t anyw = __ballot_sync(FULL, lastk >= 0);
-  if (anyw == 0) return o;
-  const int L = 31 - __clz(anyw);
-  const int lk = __shfl_sync(FULL, lastk, L);
-  o.advance = 4 * L + lk + 1;
-  // start ranks and the previous start's id
-  uint32_t sbelow = 0, stot = 0;
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const uint32_t B = __ballot_sync(FULL, start[k]);
-    sbelow += __popc(B & ltm);
-    stot += __popc(B);
-  }
-  int hs = -1;  // this lane's last start
-#pragma unroll
-  for (int k = 0; k < 4; ++k)
-    if (start[k]) hs = k;
-  const uint32_t A = __ballot_sync(FULL, hs >= 0);
-  const uint32_t lastS = sel4(id, hs);
-  const uint32_t Ab = A & ltm;
-  const int pls = Ab ? 31 - __clz(Ab) : 0;
-  const uint32_t pstart = __shfl_sync(FULL, lastS, pls);
-  bool have = Ab ? true : open;
-  uint32_t ps = Ab ? pstart : ostart;
-  const int skip1 = open ? 0 : 1;  // the item's first start closes nothing
-  uint32_t srank = sbelow;         // global rank of the next start in this lane
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    if (start[k]) {
-      if (have) {
-        const uint32_t v = vl[k] + (dk[k] > static_cast<uint32_t>(k) ? vp3 : 0u);
-        const uint32_t slot = nr + srank - skip1;
-        rs[slot] = ps;
-        re[slot] = id[k] - v;
-      }
-      ++srank;
-      have = true;
-      ps = id[k];
-    }
-  }
-  o.last = __shfl_sync(FULL, sel4(id, lk), L);
-  if (stot) {
-    o.emitted = static_cast<int>(stot) - skip1;
-    ostart = __shfl_sync(FULL, lastS, 31 - __clz(A));
-    open = true;
-  }
-  return o;
-}
-
 }  // namespace sb

@@ -574,69 +574,169 @@ __global__ void st_build_kernel(const uint8_t* __restrict__ src, uint8_t* __rest
   }
 }
 
-// Run index: one warp per work item decodes its LEB128 bytes straight to runs
-// of consecutive ids (decode_runs4); pass 1 counts, pass 2 writes them at the
-// item's offset.  Built once per graph, used by every interval iteration.
+// Run index: one warp per work item streams the item's bytes (items tile the
+// stream: item i ends where item i+1 starts) in 512-byte windows, 16 bytes per
+// lane with the validation kernel's SWAR arithmetic.  The stream is validated,
+// so 32-bit sums are exact: the id after byte j is a warp prefix sum of byte
+// contributions, and a terminator's varint value is its segmented sum (the
+// chain of continuation bytes may start in the neighbour lane).  A terminator
+// starts a run unless its value is 1 (the item's first always starts one) and
+// closes the previous run at (its id - its value).  Count pass: runs per item
+// and the longest run; fill pass: run starts / ends at the item's offset.
 template <bool FILL>
-__global__ void __launch_bounds__(256) run_index_kernel(RunIndexArgs a) {
-  __shared__ uint32_t rb_s[8][2 * 160];
+__global__ void __launch_bounds__(256, FILL ? 2 : 3) run_index_kernel(RunIndexArgs a) {
   const int lane = threadIdx.x & 31;
-  uint32_t* rs = rb_s[threadIdx.x >> 5];
-  uint32_t* re = rs + 160;
+  const uint32_t ltm = (1u << lane) - 1u;
   const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = (gridDim.x * (uint64_t)blockDim.x) >> 5;
   for (uint64_t item = gw; item < a.n_items; item += nw) {
-    uint64_t pos = a.item_off[item];
-    uint32_t rem = a.item_count[item];
-    uint32_t base = a.item_base[item];
-    bool open = false;
-    uint32_t ostart = 0;
-    uint64_t out = FILL ? a.run_off[item] : 0;
-    int nr = 0;
-    uint32_t longest = 0;  // count pass: longest run (sizes the interval-mode sparse table)
-    while (rem > 0) {
-      if (lane < 2 && pos + 256 + 128 * lane < a.stream_len) prefetch_l2(a.stream + pos + 256 + 128 * lane);
-      __syncwarp();
-      const RunWindow o = decode_runs4(a.stream, pos, rem, base, open, ostart, rs, re, nr, lane);
-      if (o.advance == 0) break;
-      pos += o.advance;
-      rem -= o.wanted;
-      base = o.last;
-      nr += o.emitted;
-      if (nr >= 32) {
-        __syncwarp();
-        if (!FILL)
-          for (int i = lane; i < nr; i += 32) longest = max(longest, re[i] - rs[i] + 1u);
-        if (FILL)
-          for (int i = lane; i < nr; i += 32) {
-            a.run_s[out + i] = rs[i];
-            a.run_e[out + i] = re[i];
+    const uint64_t pos0 = a.item_off[item];
+    const uint64_t end = item + 1 < a.n_items ? a.item_off[item + 1] : a.stream_len;
+    const uint64_t out = FILL ? a.run_off[item] : 0;
+    uint32_t id_before = a.item_base[item];  // warp-uniform: id after the previous window
+    uint32_t nruns = 0;                       // warp-uniform: runs started so far
+    uint32_t open_start = 0;                  // first id of the open run
+    uint32_t longest = 0;
+    uint32_t c3 = 0, ctail = 0;               // previous window's lane 31: word 3, trailing chain value
+    for (uint64_t wb = pos0 & ~15ull; wb < end; wb += 512) {
+      if (lane < 4 && wb + 1024 + 128 * lane < end) prefetch_l2(a.stream + wb + 1024 + 128 * lane);
+      const uint64_t lb = wb + 16 * lane;
+      uint32_t x[4] = {0u, 0u, 0u, 0u};
+      if (lb < end) {
+        const uint4 q = __ldg(reinterpret_cast<const uint4*>(a.stream + lb));
+        x[0] = q.x;
+        x[1] = q.y;
+        x[2] = q.z;
+        x[3] = q.w;
+      }
+      uint32_t T[4], D[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int64_t lo = static_cast<int64_t>(pos0) - static_cast<int64_t>(lb + 4 * i);
+        const int64_t hi = static_cast<int64_t>(end) - static_cast<int64_t>(lb + 4 * i);
+        uint32_t m = 0x80808080u;
+        if (lo > 0) m = lo >= 4 ? 0u : m << (8 * lo);
+        if (hi < 4) m &= hi <= 0 ? 0u : 0x80808080u >> (8 * (4 - hi));
+        x[i] &= (m >> 7) * 0xffu;  // bytes outside the item read as 0x00 (terminators, not counted)
+        T[i] = ~x[i] & m;
+      }
+      uint32_t wp3 = __shfl_up_sync(FULL, x[3], 1);
+      if (lane == 0) wp3 = c3;
+      c3 = __shfl_sync(FULL, x[3], 31);
+      // pass A: continuation depths, lane sum, trailing chain value
+      uint32_t lane_sum = 0, vl = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t w = x[i], wp = i ? x[i - 1] : wp3;
+        const uint32_t F = w & 0x80808080u, Fp = wp & 0x80808080u;
+        const uint32_t m1 = __funnelshift_l(Fp, F, 8);
+        const uint32_t m2 = m1 & __funnelshift_l(Fp, F, 16);
+        const uint32_t m3 = m2 & __funnelshift_l(Fp, F, 24);
+        const uint32_t m4 = m3 & Fp;
+        D[i] = (m1 >> 7) + (m2 >> 7) + (m3 >> 7) + (m4 >> 7);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t c = ((w >> (8 * k)) & 0x7fu) << (7 * ((D[i] >> (8 * k)) & 0xffu));
+          lane_sum += c;
+          vl = ((F >> (8 * k + 7)) & 1u) ? vl + c : 0u;  // value of the chain still open after this byte
+        }
+      }
+      // vl: value of the lane's trailing (unterminated) chain; the next lane continues it
+      uint32_t tail = __shfl_up_sync(FULL, vl, 1);
+      if (lane == 0) tail = ctail;
+      ctail = __shfl_sync(FULL, vl, 31);
+      uint32_t incl = lane_sum;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL, incl, d);
+        if (lane >= d) incl += y;
+      }
+      const uint32_t excl = id_before + incl - lane_sum;
+      const uint32_t anyT = __ballot_sync(FULL, (T[0] | T[1] | T[2] | T[3]) != 0);
+      bool first = nruns == 0 && (anyT & ltm) == 0;  // the item's first terminator is in this lane
+      // pass B: ids, varint values, run starts
+      uint32_t id = excl, seg = tail, ns = 0, lastS = 0, firstPrev = 0, prevS = 0;
+      bool haveS = false;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t w = x[i];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t c = ((w >> (8 * k)) & 0x7fu) << (7 * ((D[i] >> (8 * k)) & 0xffu));
+          id += c;
+          seg += c;
+          if ((T[i] >> (8 * k + 7)) & 1u) {
+            const uint32_t val = seg, prev = id - val;
+            if (val != 1u || first) {
+              if (!FILL) {
+                if (haveS) longest = max(longest, prev - prevS + 1u);
+                if (!haveS) firstPrev = prev;
+              }
+              prevS = id;
+              lastS = id;
+              haveS = true;
+              ++ns;
+            }
+            first = false;
+            seg = 0;
+          } else if (!((w >> (8 * k + 7)) & 1u)) {
+            seg = 0;  // a byte outside the item (0x00): no chain crosses it
           }
-        out += nr;
-        nr = 0;
+        }
       }
+      uint32_t sincl = ns;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL, sincl, d);
+        if (lane >= d) sincl += y;
+      }
+      const uint32_t A = __ballot_sync(FULL, ns != 0);
+      if (FILL && ns) {  // pass C: write this lane's runs
+        uint32_t slot = nruns + sincl - ns;
+        uint32_t id2 = excl, seg2 = tail;
+        bool first2 = nruns == 0 && (anyT & ltm) == 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const uint32_t w = x[i];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint32_t c = ((w >> (8 * k)) & 0x7fu) << (7 * ((D[i] >> (8 * k)) & 0xffu));
+            id2 += c;
+            seg2 += c;
+            if ((T[i] >> (8 * k + 7)) & 1u) {
+              if (seg2 != 1u || first2) {
+                a.run_s[out + slot] = id2;
+                if (slot) a.run_e[out + slot - 1] = id2 - seg2;
+                ++slot;
+              }
+              first2 = false;
+              seg2 = 0;
+            } else if (!((w >> (8 * k + 7)) & 1u)) {
+              seg2 = 0;
+            }
+          }
+        }
+      }
+      if (!FILL) {
+        // close the run open at this lane's first start: its first id is the last
+        // start of the nearest lower lane with starts (or of an earlier window)
+        const uint32_t Ab = A & ltm;
+        const uint32_t pl = __shfl_sync(FULL, lastS, Ab ? 31 - __clz(Ab) : 0);
+        if (ns && (Ab || nruns)) longest = max(longest, firstPrev - (Ab ? pl : open_start) + 1u);
+      }
+      if (A) open_start = __shfl_sync(FULL, lastS, 31 - __clz(A));
+      nruns += __shfl_sync(FULL, sincl, 31);
+      id_before = __shfl_sync(FULL, excl + lane_sum, 31);
     }
-    __syncwarp();
-    if (open) {
-      if (lane == 0) {
-        rs[nr] = ostart;
-        re[nr] = base;
-      }
-      ++nr;
+    if (nruns) {  // the open run ends at the item's last id
+      if (FILL && lane == 0) a.run_e[out + nruns - 1] = id_before;
+      if (!FILL) longest = max(longest, id_before - open_start + 1u);
     }
-    __syncwarp();
-    if (FILL)
-      for (int i = lane; i < nr; i += 32) {
-        a.run_s[out + i] = rs[i];
-        a.run_e[out + i] = re[i];
-      }
-    out += nr;
     if (!FILL) {
-      for (int i = lane; i < nr; i += 32) longest = max(longest, re[i] - rs[i] + 1u);
 #pragma unroll
       for (int o = 16; o >= 1; o >>= 1) longest = max(longest, __shfl_xor_sync(FULL, longest, o));
       if (lane == 0) {
-        a.run_count[item] = out;
+        a.run_count[item] = nruns;
         if (longest) atomicMax(a.max_run, longest);
       }
     }

@@ -13,6 +13,8 @@ against the oracle (so the work items and the longest-run bound were right).
 import numpy as np
 import pytest
 
+import oracle
+
 from paper_2604_08374_b200 import CompressedCsr, DeviceGraph, HyperBall
 from paper_2604_08374_b200.cgraph import encode_neighbor_row
 
@@ -161,6 +163,15 @@ def test_gpu_validation_matches_python(seed, oracle_best):
             ref = oracle_best.hb_run(csr, 10, 3)
             assert np.array_equal(hb.registers(), ref["registers"]), (seed, case)
             assert np.array_equal(hb.state().sum_d, ref["sum_d"]), (seed, case)
+            # the run index (interval mode, local metrics) over the same rows and work items
+            hi = HyperBall(csr, 10, 3, interval=True)
+            hi.run()
+            assert np.array_equal(hi.registers(), ref["registers"]), (seed, case)
+            if case % 4 == 0:
+                lm = DeviceGraph(csr).local_metrics()
+                lo = oracle.port().local_metrics(csr)
+                for k in lo:
+                    assert np.array_equal(lm[k], lo[k], equal_nan=lm[k].dtype.kind == "f"), (seed, case, k)
     assert rejected > 10
 
 
