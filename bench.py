@@ -83,9 +83,16 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
-    def stop(self):
+    def stop(self, keep_busy=None):
+        """keep_busy: for timed regions shorter than nvidia-smi's first sample (small
+        configs), the same workload keeps running untimed until one sample exists."""
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        extended = False
+        t0 = time.perf_counter()
+        while keep_busy is not None and not self.lines and time.perf_counter() - t0 < 5.0:
+            keep_busy()
+            extended = True
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -105,8 +112,11 @@ class ClockSampler:
             for nm, v in zip(names, parts[2:6]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        out = {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+               "reasons": sorted(reasons), "samples": len(sm)}
+        if extended:
+            out["note"] = "timed region shorter than the first nvidia-smi sample; sampled while the same runs continued untimed"
+        return out
 
 
 def build_graph(cfg, threads=0):
@@ -361,7 +371,8 @@ def main():
     ev1.record(stream)
     ev1.synchronize()
     barrier()
-    clock_info = clocks.stop()
+    # (single process only: extra runs on one rank would desynchronise the collectives)
+    clock_info = clocks.stop(keep_busy=(lambda: (one_run(hb), torch.cuda.synchronize())) if world == 1 else None)
     dev_s = max_over_ranks(ev0.elapsed_time(ev1) / 1e3)
     st = hb.stats()
     total_updates = args.steps * iters * g.edges * m
