@@ -410,6 +410,7 @@ def main():
         "binding": binding_from_profile(args.config, args.p),
         "per_iteration_ms": [round(s["step_ms"], 3) for s in st],
         "exchange_ms": [round(s["exchange_ms"], 4) for s in st] if world > 1 else None,
+        "exchange": getattr(hb, "exchange_mode", None) if world > 1 else None,
         "clocks": clock_info,
         "gpu_launches": args.steps * (2 + 2 * iters),
     }

@@ -48,12 +48,37 @@ def sharded_hyperball(csr: CompressedCsr, params: HllParams | int, depth_limit: 
     """This rank's HyperBall over its node range, wired to the communicator.
     fused_p2p: rows travel as P2P stores from the union kernel (NCCL only
     carries the 8-byte max / barrier); otherwise grouped ncclBroadcast."""
+    import os
     b = shard_bounds(csr, world) if bounds is None else bounds
     v0, v1 = int(b[rank]), int(b[rank + 1])
-    hb = HyperBall(DeviceGraph(csr, device, (v0, v1)), params, depth_limit, skip_unchanged=skip_unchanged,
-                   interval=interval)
-    if world > 1 and fused_p2p:
-        attach_peers(hb, rank, world, b)
+
+    def make():
+        return HyperBall(DeviceGraph(csr, device, (v0, v1)), params, depth_limit, skip_unchanged=skip_unchanged,
+                         interval=interval)
+
+    hb = make()
+    hb.exchange_mode = "single"
+    if world > 1:
+        hb.exchange_mode = "nccl-broadcast"
+        if fused_p2p and os.environ.get("SB_P2P", "1") != "0":
+            # Every rank must agree: a rank whose CUDA IPC attach fails (no peer
+            # access, IPC blocked by the container) sends all ranks back to the
+            # grouped-broadcast exchange.
+            import torch.distributed as dist
+            err = None
+            try:
+                attach_peers(hb, rank, world, b)
+            except Exception as e:  # noqa: BLE001 -- reported, then agreed on
+                err = f"{type(e).__name__}: {e}"
+            errs = [None] * world
+            dist.all_gather_object(errs, err)
+            if any(errs):
+                if err is None:  # peers attached here but not everywhere: start over without them
+                    hb.close()
+                    hb = make()
+                hb.exchange_mode = "nccl-broadcast (fused P2P unavailable: " + next(e for e in errs if e) + ")"
+            else:
+                hb.exchange_mode = "fused-p2p"
     if comm is not None:
         hb.attach_comm(comm, b)
     return hb

@@ -85,3 +85,58 @@ def test_sharded_hyperball_gloo_bit_identical(world):
     assert all(pr.exitcode == 0 for pr in procs), [pr.exitcode for pr in procs]
     same_t, same_sum, same_regs = q.get(timeout=5)
     assert same_t and same_sum and same_regs
+
+
+def _p2p_fallback_worker(rank, world, port, fail_rank, q):
+    """sharded_hyperball's agreement on the exchange: one rank's CUDA IPC attach
+    fails -> every rank ends on the grouped-broadcast exchange, and ranks whose
+    attach had succeeded rebuild their state without peers."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2604_08374_b200.distributed as D
+        from paper_2604_08374_b200 import CompressedCsr
+        made = []
+
+        class FakeHB:
+            def __init__(self, *a, **k):
+                self.peers = False
+                self.closed = False
+                made.append(self)
+
+            def close(self):
+                self.closed = True
+
+        def fake_attach(hb, r, w, b):
+            if r == fail_rank:
+                raise RuntimeError("cudaIpcOpenMemHandle: peer access not supported")
+            hb.peers = True
+
+        D.HyperBall, D.DeviceGraph, D.attach_peers = FakeHB, (lambda *a, **k: None), fake_attach
+        g = CompressedCsr.synth_grid(12, 12, 0, 1, 1, 1, 0)
+        hb = D.sharded_hyperball(g, 10, None, rank, world, 0, None)
+        q.put((rank, hb.exchange_mode, hb.peers, len(made), made[0].closed))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("fail_rank", [1, None])
+def test_fused_p2p_fallback_agreement(fail_rank):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    world = 3
+    procs = [ctx.Process(target=_p2p_fallback_worker, args=(r, world, port, fail_rank, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    for pr in procs:
+        pr.join(timeout=240)
+    assert all(pr.exitcode == 0 for pr in procs), [pr.exitcode for pr in procs]
+    res = sorted(q.get(timeout=5) for _ in range(world))
+    for rank, mode, peers, n_made, first_closed in res:
+        if fail_rank is None:
+            assert mode == "fused-p2p" and peers and n_made == 1
+        else:
+            assert mode.startswith("nccl-broadcast (fused P2P unavailable: RuntimeError: cudaIpcOpenMemHandle")
+            assert not peers
+            assert n_made == (1 if rank == fail_rank else 2) and first_closed == (rank != fail_rank)
