@@ -108,6 +108,58 @@ inline void dfree_ipc(T*& p) {
   p = nullptr;
 }
 
+// 32-byte page-locked host slots (each HyperBall handle's per-iteration
+// read-back) carved from one process-wide slab: cudaMallocHost / cudaFreeHost
+// per handle cost milliseconds, more than a whole small-graph run.
+constexpr int kPinnedSlot = 32, kPinnedSlots = 4096;
+struct PinnedSlab {
+  std::mutex mu;
+  uint8_t* base = nullptr;
+  std::vector<int> free_slots;
+  bool failed = false;
+};
+inline PinnedSlab& pinned_slab() {
+  static PinnedSlab* s = new PinnedSlab();  // never destroyed: slots may outlive static teardown
+  return *s;
+}
+// Returns a slot, or a private cudaMallocHost block when the slab is exhausted
+// (*owned = true: release with cudaFreeHost).
+inline cudaError_t pinned_get(unsigned long long** out, bool* owned) {
+  PinnedSlab& s = pinned_slab();
+  {
+    std::lock_guard<std::mutex> lk(s.mu);
+    if (!s.base && !s.failed) {
+      void* p = nullptr;
+      if (cudaHostAlloc(&p, static_cast<size_t>(kPinnedSlot) * kPinnedSlots, cudaHostAllocPortable) == cudaSuccess) {
+        s.base = static_cast<uint8_t*>(p);
+        for (int i = kPinnedSlots - 1; i >= 0; --i) s.free_slots.push_back(i);
+      } else {
+        cudaGetLastError();
+        s.failed = true;
+      }
+    }
+    if (!s.free_slots.empty()) {
+      const int i = s.free_slots.back();
+      s.free_slots.pop_back();
+      *out = reinterpret_cast<unsigned long long*>(s.base + static_cast<size_t>(i) * kPinnedSlot);
+      *owned = false;
+      return cudaSuccess;
+    }
+  }
+  *owned = true;
+  return cudaMallocHost(reinterpret_cast<void**>(out), kPinnedSlot);
+}
+inline void pinned_put(unsigned long long* p, bool owned) {
+  if (!p) return;
+  if (owned) {
+    cudaFreeHost(p);
+    return;
+  }
+  PinnedSlab& s = pinned_slab();
+  std::lock_guard<std::mutex> lk(s.mu);
+  s.free_slots.push_back(static_cast<int>((reinterpret_cast<uint8_t*>(p) - s.base) / kPinnedSlot));
+}
+
 // Stream sync with an optional watchdog: SB_SYNC_TIMEOUT_S=<seconds> turns a
 // device hang into an SB_ECUDA error instead of a blocked host thread.
 inline cudaError_t sync_stream(cudaStream_t s) {
@@ -144,6 +196,8 @@ using sb::rt::dalloc;
 using sb::rt::dalloc_ipc;
 using sb::rt::dfree;
 using sb::rt::dfree_ipc;
+using sb::rt::pinned_get;
+using sb::rt::pinned_put;
 using sb::rt::sync_stream;
 
 struct sb_graph {
@@ -222,7 +276,9 @@ struct sb_hb {
   uint8_t* d_scratch = nullptr;
   uint32_t* d_counter = nullptr;
   unsigned long long* d_misc = nullptr;  // [0] work, [1] max_ord, [2] changed count
-  unsigned long long* h_misc = nullptr;  // pinned
+  unsigned long long* h_misc = nullptr;  // pinned (slab slot unless h_misc_owned)
+  bool h_misc_owned = false;
+  bool planes_ipc = false;               // planes / changed flags re-allocated for CUDA IPC export
   uint8_t* d_tmp = nullptr;              // packed export buffer
   uint8_t* d_st = nullptr;               // interval mode: sparse-table levels 1..levels
   int levels = 0;
@@ -253,10 +309,19 @@ struct sb_hb {
     if (stream2) cudaStreamSynchronize(stream2);
     for (void* q : ipc_opened) cudaIpcCloseMemHandle(q);
     for (int i = 0; i < 2; ++i) { dfree(d_peer_plane[i]); dfree(d_peer_chg[i]); }
-    for (int i = 0; i < 2; ++i) { dfree_ipc(d_plane[i]); dfree_ipc(d_changed[i]); dfree(d_c[i]); }
+    for (int i = 0; i < 2; ++i) {
+      if (planes_ipc) {
+        dfree_ipc(d_plane[i]);
+        dfree_ipc(d_changed[i]);
+      } else {
+        dfree(d_plane[i]);
+        dfree(d_changed[i]);
+      }
+      dfree(d_c[i]);
+    }
     dfree(d_sum_d); dfree(d_sum_d2); dfree(d_lc); dfree(d_scratch); dfree(d_counter);
     dfree(d_misc); dfree(d_tmp); dfree(d_st); dfree(d_chunk_work);
-    if (h_misc) cudaFreeHost(h_misc);
+    pinned_put(h_misc, h_misc_owned);
     for (auto& e : ev) if (e) cudaEventDestroy(e);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);

@@ -79,8 +79,8 @@ int sb_hb_create(sb_graph* g, unsigned p, uint32_t depth_limit, uint32_t flags, 
   const uint64_t plane = g->n * h->row;
   const uint64_t nl = std::max<uint64_t>(g->n_local, 1);
   for (int i = 0; i < 2; ++i) {
-    HK(dalloc_ipc(&h->d_plane[i], plane + 64));
-    HK(dalloc_ipc(&h->d_changed[i], g->n));
+    HK(dalloc(&h->d_plane[i], plane + 64));
+    HK(dalloc(&h->d_changed[i], g->n));
     HK(dalloc(&h->d_c[i], nl * 8));
   }
   HK(dalloc(&h->d_sum_d, nl * 8));
@@ -105,7 +105,7 @@ int sb_hb_create(sb_graph* g, unsigned p, uint32_t depth_limit, uint32_t flags, 
     h->levels = K;
     if (K) HK(dalloc(&h->d_st, static_cast<uint64_t>(K) * plane + 64));
   }
-  HK(cudaMallocHost(&h->h_misc, 4 * 8));
+  HK(pinned_get(&h->h_misc, &h->h_misc_owned));
 #undef HK
   const int rc = hb_init(h);
   if (rc != SB_OK) return bail(rc);
@@ -545,11 +545,38 @@ int sb_hb_attach_comm(sb_hb* h, sb_comm* c, const uint64_t* bounds) {
 void sb_comm_destroy(sb_comm* c) { delete c; }
 
 // ------------------------------------------------------------------ fused P2P exchange
-int sb_hb_ipc_handles(const sb_hb* h, void* out, size_t cap) {
+// Pool memory cannot be exported with cudaIpcGetMemHandle: on first export the
+// planes and changed flags move to cudaMalloc blocks (contents copied).
+static int make_planes_ipc(sb_hb* h) {
+  if (h->planes_ipc) return SB_OK;
+  const uint64_t sizes[2] = {h->g->n * h->row + 64, h->g->n};
+  uint8_t** bufs[4] = {&h->d_plane[0], &h->d_plane[1], &h->d_changed[0], &h->d_changed[1]};
+  uint8_t* fresh[4] = {nullptr, nullptr, nullptr, nullptr};
+  for (int k = 0; k < 4; ++k) {
+    const cudaError_t e = dalloc_ipc(&fresh[k], sizes[k / 2]);
+    if (e != cudaSuccess) {
+      for (auto& f : fresh) dfree_ipc(f);
+      return cuda_fail(e, "cudaMalloc (IPC-exportable planes)");
+    }
+  }
+  for (int k = 0; k < 4; ++k) CK(cudaMemcpyAsync(fresh[k], *bufs[k], sizes[k / 2], cudaMemcpyDeviceToDevice, h->stream));
+  CK(sync_stream(h->stream));
+  for (int k = 0; k < 4; ++k) {
+    dfree(*bufs[k]);
+    *bufs[k] = fresh[k];
+  }
+  h->planes_ipc = true;
+  return SB_OK;
+}
+
+int sb_hb_ipc_handles(const sb_hb* hc, void* out, size_t cap) {
+  sb_hb* h = const_cast<sb_hb*>(hc);
   if (!h || !out) return fail(SB_EINVAL, "NULL argument");
   if (cap < SB_IPC_HANDLE_BYTES) return fail(SB_EINVAL, "handle buffer too small (%d bytes needed)", SB_IPC_HANDLE_BYTES);
   static_assert(sizeof(cudaIpcMemHandle_t) * 4 == SB_IPC_HANDLE_BYTES, "ipc handle size");
   DeviceGuard dg(h->g->device);
+  if (h->computed) return fail(SB_EINVAL, "ipc_handles during a step");
+  if (const int rc = make_planes_ipc(h)) return rc;
   cudaIpcMemHandle_t hs[4];
   CK(cudaIpcGetMemHandle(&hs[0], h->d_plane[0]));
   CK(cudaIpcGetMemHandle(&hs[1], h->d_plane[1]));
