@@ -106,7 +106,42 @@ int sb_exact_run(sb_exact* x, uint64_t src_begin, uint64_t src_end, uint32_t* ma
     e.s0 = s0;
     e.s1 = s1;
     CK(sb::launch_exact_init(x->P, e, x->stream));
-    for (uint32_t t = 1;; ++t) {
+    uint32_t t0 = 1;
+    if (g->d_run_off) {
+      // Depth 1 straight from the run index (the rows the first OR pass would
+      // produce) -- one union pass fewer per block.
+      int rc = exact_grow_hist(x, 1);
+      if (rc) return rc;
+      e.hist = x->d_hist;
+      e.hist_cap = x->hist_cap;
+      e.node_item = g->d_node_item;
+      e.run_off = g->d_run_off;
+      e.run_s = g->d_run_s;
+      e.run_e = g->d_run_e;
+      e.plane = x->d_plane[1];
+      CK(cudaMemsetAsync(x->d_misc, 0, 16, x->stream));
+      CK(cudaEventRecord(x->ev[0], x->stream));
+      CK(sb::launch_exact_init1(x->P, e, x->stream));
+      CK(cudaEventRecord(x->ev[1], x->stream));
+      e.t = 1;
+      CK(sb::launch_exact_count(x->P, e, x->stream));
+      unsigned long long changed = 0;
+      CK(cudaMemcpyAsync(&changed, x->d_misc + 1, 8, cudaMemcpyDeviceToHost, x->stream));
+      CK(sync_stream(x->stream));
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, x->ev[0], x->ev[1]);
+      x->union_ms += ms;
+      x->union_launches += 1;
+      if (changed == 0 || (x->depth && x->depth == 1)) {
+        if (changed) x->max_depth = std::max(x->max_depth, 1u);
+        x->sources_done += s1 - s0;
+        continue;
+      }
+      x->max_depth = std::max(x->max_depth, 1u);
+      L = 1;
+      t0 = 2;
+    }
+    for (uint32_t t = t0;; ++t) {
       int rc = exact_grow_hist(x, t);
       if (rc) return rc;
       e.hist = x->d_hist;

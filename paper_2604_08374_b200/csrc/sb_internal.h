@@ -106,6 +106,11 @@ struct ExactArgs {
   uint32_t hist_cap;
   uint32_t t;
   unsigned long long* changed_count;
+  // exact_init1 (rows at depth 1 straight from the run index)
+  const uint32_t* node_item;
+  const uint64_t* run_off;
+  const uint32_t* run_s;
+  const uint32_t* run_e;
 };
 
 // On-device grid visibility graph construction (sb_vis.cu).
@@ -184,6 +189,7 @@ cudaError_t launch_st_build(int p, const uint8_t* cur, uint8_t* st, uint64_t n, 
 cudaError_t launch_union_interval(int p, const IntervalArgs& a, cudaStream_t s, bool orop = false);
 cudaError_t launch_union_or(int p, const UnionArgs& a, cudaStream_t s);
 cudaError_t launch_exact_init(int p, const ExactArgs& a, cudaStream_t s);
+cudaError_t launch_exact_init1(int p, const ExactArgs& a, cudaStream_t s);
 cudaError_t launch_exact_count(int p, const ExactArgs& a, cudaStream_t s);
 cudaError_t launch_run_index(const RunIndexArgs& a, bool fill, cudaStream_t s);
 cudaError_t launch_estimate(int p, int mode, const EstArgs& a, cudaStream_t s);

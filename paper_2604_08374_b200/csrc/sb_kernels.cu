@@ -1023,6 +1023,48 @@ __global__ void __launch_bounds__(256) exact_init_kernel(ExactArgs a) {
   }
 }
 
+// Depth-1 rows without a union pass: row v = ({v} U N(v)) & [s0, s1) -- what
+// the first OR pass over the source rows produces -- written from v's runs
+// (runs are sorted; each clipped run is a bit range: interior words plain
+// stores, boundary words atomicOr, since two runs can share only a boundary word).
+template <int P>
+__global__ void __launch_bounds__(256) exact_init1_kernel(ExactArgs a) {
+  using G = Geo<P>;
+  constexpr uint32_t WORDS = G::ROW / 4;
+  const int lane = threadIdx.x & 31;
+  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = (gridDim.x * (uint64_t)blockDim.x) >> 5;
+  const uint32_t s0 = static_cast<uint32_t>(a.s0), s1 = static_cast<uint32_t>(a.s1);
+  for (uint64_t v = gw; v < a.n; v += nw) {
+    uint32_t* row = reinterpret_cast<uint32_t*>(a.plane + v * G::ROW);
+    for (uint32_t k = lane; k < WORDS; k += 32) row[k] = 0u;
+    __syncwarp();
+    if (lane == 0 && v >= s0 && v < s1) atomicOr(row + (v - s0) / 32, 1u << ((v - s0) % 32));
+    const uint64_t r0 = a.run_off[a.node_item[v]], r1 = a.run_off[a.node_item[v + 1]];
+    for (uint64_t r = r0; r < r1; r += 32) {
+      uint32_t rs = 0xffffffffu, re = 0u;
+      if (r + lane < r1) {
+        rs = a.run_s[r + lane];
+        re = a.run_e[r + lane];
+      }
+      const uint32_t cs = max(rs, s0), ce = min(re, s1 - 1u);
+      if (rs != 0xffffffffu && cs <= ce) {
+        const uint32_t b0 = cs - s0, b1 = ce - s0;
+        const uint32_t w0 = b0 / 32, w1 = b1 / 32;
+        const uint32_t m0 = 0xffffffffu << (b0 % 32), m1 = 0xffffffffu >> (31 - b1 % 32);
+        if (w0 == w1) {
+          atomicOr(row + w0, m0 & m1);
+        } else {
+          atomicOr(row + w0, m0);
+          for (uint32_t w = w0 + 1; w < w1; ++w) row[w] = 0xffffffffu;
+          atomicOr(row + w1, m1);
+        }
+      }
+      if (__all_sync(FULL, rs >= s1)) break;  // sorted runs: the rest start past the block
+    }
+  }
+}
+
 template <int P>
 __global__ void __launch_bounds__(256) exact_count_kernel(ExactArgs a) {
   using G = Geo<P>;
@@ -1232,6 +1274,25 @@ cudaError_t launch_exact_init(int p, const ExactArgs& a, cudaStream_t s) {
   {                                                                                     \
     const int g = grid_for(reinterpret_cast<const void*>(exact_init_kernel<P>), 256);   \
     exact_init_kernel<P><<<g, 256, 0, s>>>(a);                                          \
+    break;                                                                              \
+  }
+  switch (p) {
+    case 10: SB_L(10)
+    case 11: SB_L(11)
+    case 12: SB_L(12)
+    case 13: SB_L(13)
+    case 14: SB_L(14)
+    default: return cudaErrorInvalidValue;
+  }
+#undef SB_L
+  return cudaGetLastError();
+}
+
+cudaError_t launch_exact_init1(int p, const ExactArgs& a, cudaStream_t s) {
+#define SB_L(P)                                                                         \
+  {                                                                                     \
+    const int g = grid_for(reinterpret_cast<const void*>(exact_init1_kernel<P>), 256);  \
+    exact_init1_kernel<P><<<g, 256, 0, s>>>(a);                                         \
     break;                                                                              \
   }
   switch (p) {
