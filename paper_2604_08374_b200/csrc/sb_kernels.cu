@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(256, 3) build_items_kernel(BuildArgs a) {
     if (lane == 0) {
       // the first varint (the absolute first id) may be 0
       bool first_zero = true;
-      for (uint64_t b = pos0; b < end; ++b) {
+      for (uint64_t b = pos0; b < end && b < pos0 + 5; ++b) {  // a longer first varint is flagged anyway
         const uint8_t c = a.stream[b];
         if (c & 0x7fu) first_zero = false;
         if (!(c & 0x80u)) break;
