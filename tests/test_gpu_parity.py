@@ -308,6 +308,26 @@ def test_gpu_pool_reuse_and_release(c1):
     assert np.array_equal(hb.state().sum_d, ref[0])
 
 
+def test_gpu_many_handles_pinned_slab_overflow():
+    """More live HyperBall handles than the pinned read-back slab has slots (4096):
+    the overflow handles fall back to private pinned blocks; every handle still
+    steps correctly, and slots are reused after destruction."""
+    g = csr_of([[1, 2], [0, 2], [0, 1], []])
+    dg = DeviceGraph(g)
+    ref = HyperBall(dg, 4, 2)
+    ref.run()
+    want = ref.state().sum_d
+    hs = [HyperBall(dg, 4, 2) for _ in range(4200)]
+    for h in hs[::97] + hs[-5:]:
+        h.run()
+        assert np.array_equal(h.state().sum_d, want)
+    del hs[:2000]
+    more = [HyperBall(dg, 4, 2) for _ in range(100)]
+    for h in more[::9]:
+        h.run()
+        assert np.array_equal(h.state().sum_d, want)
+
+
 def test_gpu_hilbert_permutation_equivariance(c1):
     """Hashing original ids makes reordering layout-only."""
     h = c1.hilbert_reorder()
