@@ -61,7 +61,7 @@ struct IntervalArgs {
   const uint32_t* run_e;       // run end ids (inclusive)
 };
 
-// Run index, derived once at upload from the LEB128 stream (decode_runs4).
+// Run index, derived once per graph from the LEB128 stream (run_index_kernel).
 struct RunIndexArgs {
   const uint8_t* stream;
   uint64_t stream_len;         // bytes (prefetch bound)
