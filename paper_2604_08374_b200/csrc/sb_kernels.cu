@@ -342,30 +342,53 @@ __device__ __forceinline__ void tree_max(Grp& acc, Grp (&x)[U]) {
 // its bits so far equal the maximum's; M_k = OR of b_k over the alive values.
 // With the AND folded into the OR-accumulate (one LOP3 each) this is
 // ceil((K-1)/2) + 6K LOP3 (58 for K = 9) instead of 8U (64) for the tree.
+// Written as explicit lop3 so ptxas keeps exactly that count: left to itself
+// it turned each M_k accumulation into a tree over (b_k & alive) terms with
+// the alive masks recomputed beside it (62 LOP3 per batch on the ALU pipe the
+// kernel is bound by); the serial accumulate's latency is hidden by the 8
+// warps per scheduler.
+template <uint32_t LUT>
+__device__ __forceinline__ uint32_t lop3(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, %4;" : "=r"(r) : "r"(a), "r"(b), "r"(c), "n"(LUT));
+  return r;
+}
+constexpr uint32_t kOr3 = 0xfe;      // a | b | c
+constexpr uint32_t kOrNot = 0xf3;    // a | ~b
+constexpr uint32_t kAnd = 0xc0;      // a & b
+constexpr uint32_t kOrAnd = 0xf8;    // a | (b & c)
+constexpr uint32_t kAndOrNot = 0xd0; // a & (b | ~c)
+
 template <int U>
 __device__ __forceinline__ void kway_max(Grp& acc, const Grp (&x)[U]) {
+  // M3: OR of the K b3 planes, three at a time
   uint32_t m3 = acc.b3;
+  int q0 = 0;
+  if (U % 2 == 1) {
+    m3 |= x[0].b3;  // odd U: one plain OR first, then pairs
+    q0 = 1;
+  }
 #pragma unroll
-  for (int q = 0; q < U; ++q) m3 |= x[q].b3;
+  for (int q = q0; q + 1 < U; q += 2) m3 = lop3<kOr3>(m3, x[q].b3, x[q + 1].b3);
   uint32_t al[U + 1];
-  al[U] = acc.b3 | ~m3;
+  al[U] = lop3<kOrNot>(acc.b3, m3, 0u);
 #pragma unroll
-  for (int q = 0; q < U; ++q) al[q] = x[q].b3 | ~m3;
-  uint32_t m2 = al[U] & acc.b2;
+  for (int q = 0; q < U; ++q) al[q] = lop3<kOrNot>(x[q].b3, m3, 0u);
+  uint32_t m2 = lop3<kAnd>(al[U], acc.b2, 0u);
 #pragma unroll
-  for (int q = 0; q < U; ++q) m2 |= al[q] & x[q].b2;
-  al[U] &= acc.b2 | ~m2;
+  for (int q = 0; q < U; ++q) m2 = lop3<kOrAnd>(m2, al[q], x[q].b2);
+  al[U] = lop3<kAndOrNot>(al[U], acc.b2, m2);
 #pragma unroll
-  for (int q = 0; q < U; ++q) al[q] &= x[q].b2 | ~m2;
-  uint32_t m1 = al[U] & acc.b1;
+  for (int q = 0; q < U; ++q) al[q] = lop3<kAndOrNot>(al[q], x[q].b2, m2);
+  uint32_t m1 = lop3<kAnd>(al[U], acc.b1, 0u);
 #pragma unroll
-  for (int q = 0; q < U; ++q) m1 |= al[q] & x[q].b1;
-  al[U] &= acc.b1 | ~m1;
+  for (int q = 0; q < U; ++q) m1 = lop3<kOrAnd>(m1, al[q], x[q].b1);
+  al[U] = lop3<kAndOrNot>(al[U], acc.b1, m1);
 #pragma unroll
-  for (int q = 0; q < U; ++q) al[q] &= x[q].b1 | ~m1;
-  uint32_t m0 = al[U] & acc.b0;
+  for (int q = 0; q < U; ++q) al[q] = lop3<kAndOrNot>(al[q], x[q].b1, m1);
+  uint32_t m0 = lop3<kAnd>(al[U], acc.b0, 0u);
 #pragma unroll
-  for (int q = 0; q < U; ++q) m0 |= al[q] & x[q].b0;
+  for (int q = 0; q < U; ++q) m0 = lop3<kOrAnd>(m0, al[q], x[q].b0);
   acc = Grp{m0, m1, m2, m3};
 }
 
