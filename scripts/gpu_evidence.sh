@@ -17,6 +17,9 @@ if [[ $what == bench || $what == all ]]; then
   run timeout 900 python -u bench.py --local > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.log
   run timeout 600 python -u bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.log
   run timeout 600 python -u scripts/e2e_breakdown.py > gpurun_out/e2e_breakdown.txt 2>&1
+  run timeout 600 python -u scripts/e2e_small.py > gpurun_out/e2e_small_graphs.txt 2>&1
+  run timeout 600 python -u bench.py --config c2 > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.log
+  run timeout 600 python -u bench.py --config c1 > gpurun_out/bench_c1.json 2> gpurun_out/bench_c1.log
   run timeout 600 python -u scripts/step_overhead.py > gpurun_out/step_overhead.json 2>/dev/null
 fi
 if [[ $what == ncu || $what == all ]]; then
