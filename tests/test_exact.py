@@ -141,12 +141,15 @@ def test_gpu_exact_bfs_bit_exact(oracle_port, name, g, interval):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("interval", [False, True], ids=["dense", "interval"])
 @pytest.mark.parametrize("depth", [1, 2, 3])
-@pytest.mark.parametrize("log2_block", [12, 13])
-def test_gpu_exact_depth_limit_and_block_size(oracle_port, depth, log2_block):
+@pytest.mark.parametrize("log2_block", [12, 13, 16])
+def test_gpu_exact_depth_limit_and_block_size(oracle_port, depth, log2_block, interval):
+    """Interval mode writes the depth-1 rows from the run index (exact_init1)
+    instead of a union pass; every row geometry (p = log2_block - 2) and depth."""
     g = CompressedCsr.synth_grid(70, 70, 20, 2, 6, 5, 8 * 8)
     ref = oracle_port.exact_bfs(g, depth_limit=depth)
-    x = ExactBfs(g, depth, log2_block=log2_block)
+    x = ExactBfs(g, depth, log2_block=log2_block, interval=interval)
     x.run()
     got = x.result()
     for k in ("sum_d", "sum_d2", "reach"):
