@@ -1046,7 +1046,8 @@ __global__ void __launch_bounds__(256) exact_init_kernel(ExactArgs a) {
   }
 }
 
-// Depth-1 rows without a union pass: row v = ({v} U N(v)) & [s0, s1) -- what
+// Depth-1 rows without a union pass (exact BFS): row v =
+// ({v} U N(v)) & [s0, s1) -- what
 // the first OR pass over the source rows produces -- written from v's runs
 // (runs are sorted; each clipped run is a bit range: interior words plain
 // stores, boundary words atomicOr, since two runs can share only a boundary word).
