@@ -40,6 +40,8 @@ CONFIGS = {
     "c2": (212, 212, 60, 3, 10, 20261017, 44 * 44, "C2 212x212 grid, 60 rectangles (3-10 cells), radius 44 cells"),
     "c3": (486, 486, 0, 1, 1, 20261017, 87 * 87, "C3 open 486x486 grid, radius 87 cells"),
 }
+# BASELINE.json configs: C1 is quoted at depth limit 3, C2 / C3 at full depth.
+DEFAULT_DEPTH = {"c1": 3}
 METRIC = "HyperBall edge-register updates/s"
 UNIT = "edge-register updates/s"
 
@@ -297,7 +299,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--p", type=int, default=10)
-    ap.add_argument("--depth", type=int, default=0)
+    ap.add_argument("--depth", type=int, default=None,
+                    help="depth limit d (0 = unbounded); default: the config's (C1: 3, C2/C3: full depth)")
     ap.add_argument("--cpu-sample-s", type=float, default=15.0)
     ap.add_argument("--cpu-step-s", type=float, default=6.0)
     ap.add_argument("--no-cpu", action="store_true")
@@ -307,6 +310,8 @@ def main():
     ap.add_argument("--no-pipeline", action="store_true", help="skip the grid -> device graph -> HyperBall pipeline")
     ap.add_argument("--local", action="store_true", help="also time the exact local metrics (slow on c3)")
     args = ap.parse_args()
+    if args.depth is None:
+        args.depth = DEFAULT_DEPTH.get(args.config, 0)
     if args.impl == "reference":
         return reference_arm(args)
 
