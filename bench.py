@@ -258,7 +258,7 @@ def pipeline_variant(args, P, device, hb_ref):
     DeviceGraph.from_grid(grid_mask(16, 16, 0, 1, 1, 1), 9, device)  # warm the build kernels
     out = {"input": f"{r}x{c} obstacle mask ({mask.size} B H2D)",
            "timing": "host wall clock per phase, best of 2 (synchronous C-ABI calls)"}
-    modes = ("interval", "dense") if P.p >= 10 else ("dense",)  # interval mode needs p >= 10
+    modes = ("interval", "dense")
     for mode in modes + modes:
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -472,7 +472,7 @@ def main():
             "per_iteration_union_ms": [round(s["union_ms"], 3) for s in hs.stats()],
             "note": "gathers only neighbours whose registers changed last iteration; not used for value/roofline"}}
         del hs
-        if args.p >= 10:
+        if True:
             hi = sharded_hyperball(g, P, args.depth or None, rank, world, local, comm, False, bounds, interval=True)
             one_run(hi)
             barrier()

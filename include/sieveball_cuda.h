@@ -54,7 +54,7 @@ enum {
 #define SB_HB_SKIP_UNCHANGED 1u /* gather only neighbours whose registers changed last iteration (bit-exact) */
 #define SB_HB_SCHEDULE_WARP 2u  /* per-warp work-item schedule instead of the default 8-node CTA tiles */
 #define SB_HB_INTERVAL 4u       /* variant: fold runs of consecutive ids via a per-iteration sparse table
-                                   (bit-exact; p >= 10; not combinable with SKIP_UNCHANGED) */
+                                   (bit-exact; any p; not combinable with SKIP_UNCHANGED) */
 
 /* sb_hb_read_registers `which` */
 #define SB_REGS_LATEST 0   /* registers after the last executed iteration (c_t) */

@@ -46,8 +46,8 @@ int sb_hb_create(sb_graph* g, unsigned p, uint32_t depth_limit, uint32_t flags, 
   *out = nullptr;
   if (!g) return fail(SB_EINVAL, "sb_hb_create: NULL graph");
   if (p < 4 || p > 16) return fail(SB_EINVAL, "hll: precision must be in [4, 16]");
-  if ((flags & SB_HB_INTERVAL) && (p < 10 || (flags & SB_HB_SKIP_UNCHANGED)))
-    return fail(SB_EINVAL, "interval mode needs p >= 10 and excludes SB_HB_SKIP_UNCHANGED");
+  if ((flags & SB_HB_INTERVAL) && (flags & SB_HB_SKIP_UNCHANGED))
+    return fail(SB_EINVAL, "interval mode excludes SB_HB_SKIP_UNCHANGED");
   DeviceGuard dg(g->device);
   auto* h = new sb_hb();
   h->g = g;

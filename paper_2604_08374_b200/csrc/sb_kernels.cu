@@ -774,9 +774,11 @@ __device__ __forceinline__ void process_item_runs(const IntervalArgs& ia, uint64
                                                   const long long* lvl_off) {
   using G = Geo<P>;
   using IO = GrpIO<G::GB>;
-  static_assert(G::SUB == 1, "interval mode maps one 512-byte slice per warp (p >= 10)");
+  // p < 10: a row is LPR < 32 lanes wide, so the warp's SUB lane groups fold
+  // different runs and are merged by xor-shuffles at the end (as the dense kernel)
   const UnionArgs& a = ia.u;
-  const int gl = lane;
+  const int sub = lane / G::LPR;
+  const int gl = lane % G::LPR;
   const uint64_t u = item * G::SLICES + slice;
   const uint32_t node = a.item_node[item];
   const uint64_t v = a.node_begin + node;
@@ -794,11 +796,11 @@ __device__ __forceinline__ void process_item_runs(const IntervalArgs& ia, uint64
       ms = ia.run_s[c + lane];
       me = ia.run_e[c + lane];
     }
-    for (int q0 = 0; q0 < cnt; q0 += 4) {
+    for (int q0 = 0; q0 < cnt; q0 += 4 * G::SUB) {
       Grp x[8];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const int r = min(q0 + q, cnt - 1);
+        const int r = min(q0 + q * G::SUB + sub, cnt - 1);  // tail repeats are harmless (max is idempotent)
         uint32_t s = __shfl_sync(FULL, ms, r);
         const uint32_t e = __shfl_sync(FULL, me, r);
         uint32_t L = e - s + 1;
@@ -818,10 +820,14 @@ __device__ __forceinline__ void process_item_runs(const IntervalArgs& ia, uint64
         kway_max<8>(acc, x);
     }
   }
+  if (G::SUB > 1) {
+#pragma unroll
+    for (int m = G::LPR; m < 32; m <<= 1) combine<OR>(acc, grp_shfl_xor(acc, m));
+  }
   uint8_t* nextb = a.next + goff + v * G::ROW;
   bool finish = nit == 1;
   if (!finish) {
-    IO::st(a.scratch + u * G::SLICE_BYTES + static_cast<uint64_t>(gl) * G::GB, acc);
+    if (lane < G::LPR) IO::st(a.scratch + u * G::SLICE_BYTES + static_cast<uint64_t>(gl) * G::GB, acc);
     __threadfence();
     uint32_t prev = 0;
     if (lane == 0) prev = atomicAdd(&a.node_counter[static_cast<uint64_t>(node) * G::SLICES + slice], 1u);
@@ -1257,6 +1263,12 @@ cudaError_t launch_union_interval(int p, const IntervalArgs& a, cudaStream_t s, 
     break;                                                                                          \
   }
   switch (p) {
+    case 4: SB_LI(4)
+    case 5: SB_LI(5)
+    case 6: SB_LI(6)
+    case 7: SB_LI(7)
+    case 8: SB_LI(8)
+    case 9: SB_LI(9)
     case 10: SB_LI(10)
     case 11: SB_LI(11)
     case 12: SB_LI(12)

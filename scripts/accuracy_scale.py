@@ -26,7 +26,7 @@ for cfg in sys.argv[1:] or ["c2", "c3"]:
     rows = {}
     for p in (8, 10, 12):
         t0 = time.perf_counter()
-        hb = HyperBall(dg, p, None, interval=p >= 10)
+        hb = HyperBall(dg, p, None, interval=True)
         it = hb.run()
         m = hb.metrics(nv, deg)
         t_hb = time.perf_counter() - t0

@@ -30,8 +30,6 @@ for case in range(n_cases):
     p = int(rng.integers(4, 17)) if rng.random() < 0.5 else 10
     depth = None if rng.random() < 0.5 else int(rng.integers(1, 6))
     mode = rng.choice(["dense", "skip", "interval", "shards"])
-    if mode == "interval" and p < 10:
-        mode = "dense"
     params = dict(rows=rows, cols=cols, rects=rects, rmin=rmin, rmax=rmax, radius2=radius2, seed=seed, p=p,
                   depth=depth, mode=str(mode))
     try:

@@ -56,8 +56,7 @@ def main():
     res["c4_graph"] = {"nodes": g2.n, "edges": g2.edges, "stream_bytes": g2.stream_len}
     for p in (4, 6, 8, 10, 12, 14):
         res["c4"].append(point(g2, dg2, p, None, False))
-        if p >= 10:
-            res["c4"].append(point(g2, dg2, p, None, True))
+        res["c4"].append(point(g2, dg2, p, None, True))
     del dg2
     g3 = build_graph("c3")
     dg3 = DeviceGraph(g3, 0)

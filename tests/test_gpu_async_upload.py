@@ -20,8 +20,6 @@ def graphs():
 @pytest.mark.parametrize("p", [6, 10, 12])
 @pytest.mark.parametrize("name,g", list(graphs()), ids=[n for n, _ in graphs()])
 def test_async_upload_bit_identical(name, g, p, flags):
-    if flags.get("interval") and p < 10:
-        pytest.skip("interval mode needs p >= 10")
     ref = HyperBall(g, p, None, **flags)
     ref.run()
     hb = HyperBall(DeviceGraph(g, async_upload=True), p, None, **flags)
