@@ -252,10 +252,13 @@ int sb_local_metrics(sb_graph* g, uint64_t v0, uint64_t v1, double* control, dou
   if (nl == 0) return SB_OK;
   // |N2(v)|: depth-2 exact BFS over every source block (cost ~ blocks x runs, best
   // for dense graphs) or per-node 2-hop bitmaps (cost ~ sum_w deg(w) runs(w),
-  // best for large sparse graphs).  Measured C3 rates: 62 ps per row-pair of
-  // the BFS, ~2.6 ps per range-OR -> bitmaps win when avg degree < 48 x blocks.
+  // best for large sparse graphs).  Crossover measured with the one-pass BFS
+  // (depth-1 rows from the run index) on a 49,632-node grid, 13 blocks:
+  // bitmap 6.3 vs BFS 8.2 ms at mean degree 898, 14.1 vs 11.5 ms at 1,536 ->
+  // bitmaps win when avg degree < ~88 x blocks (C3, 350 x: BFS 2.2x faster;
+  // city grid, 2.3 x: bitmap).
   const uint64_t blocks = (n + 4095) / 4096;
-  bool n2_bitmap = static_cast<double>(g->edges_local) / static_cast<double>(n) < 48.0 * static_cast<double>(blocks);
+  bool n2_bitmap = static_cast<double>(g->edges_local) / static_cast<double>(n) < 88.0 * static_cast<double>(blocks);
   if (const char* e = getenv("SB_LOCAL_N2")) {  // test / A-B override: "bfs" or "bitmap"
     if (!strcmp(e, "bfs")) n2_bitmap = false;
     if (!strcmp(e, "bitmap")) n2_bitmap = true;
