@@ -472,49 +472,48 @@ def main():
             "per_iteration_union_ms": [round(s["union_ms"], 3) for s in hs.stats()],
             "note": "gathers only neighbours whose registers changed last iteration; not used for value/roofline"}}
         del hs
-        if True:
-            hi = sharded_hyperball(g, P, args.depth or None, rank, world, local, comm, False, bounds, interval=True)
-            one_run(hi)
-            barrier()
-            s3 = torch.cuda.ExternalStream(hi.stream_handle())
-            e0.record(s3)
-            iti = one_run(hi)
-            e1.record(s3)
-            e1.synchronize()
-            ti = max_over_ranks(e0.elapsed_time(e1) / 1e3)
-            line["variants"]["interval"] = {
-                "seconds_per_run": ti, "iterations": iti, "dense_equivalent_updates_per_s": iti * g.edges * m / ti,
-                "sum_d_identical_to_dense": bool(np.array_equal(hi.state().sum_d, hb.state().sum_d)),
-                "per_iteration_union_ms": [round(s["union_ms"], 3) for s in hi.stats()],
-                "note": "runs of consecutive ids folded with 2 sparse-table rows (per-iteration table build "
-                        "included); bit-exact; reported separately from value/roofline"}
-            del hi
-            if not args.no_e2e and world == 1:
-                # the same end-to-end path as `e2e` (host CSR -> HBM -> run -> read-back) in interval
-                # mode: the run index needs the whole stream, so the upload is not hidden here
-                g.pin(True)
+        hi = sharded_hyperball(g, P, args.depth or None, rank, world, local, comm, False, bounds, interval=True)
+        one_run(hi)
+        barrier()
+        s3 = torch.cuda.ExternalStream(hi.stream_handle())
+        e0.record(s3)
+        iti = one_run(hi)
+        e1.record(s3)
+        e1.synchronize()
+        ti = max_over_ranks(e0.elapsed_time(e1) / 1e3)
+        line["variants"]["interval"] = {
+            "seconds_per_run": ti, "iterations": iti, "dense_equivalent_updates_per_s": iti * g.edges * m / ti,
+            "sum_d_identical_to_dense": bool(np.array_equal(hi.state().sum_d, hb.state().sum_d)),
+            "per_iteration_union_ms": [round(s["union_ms"], 3) for s in hi.stats()],
+            "note": "runs of consecutive ids folded with 2 sparse-table rows (per-iteration table build "
+                    "included); bit-exact; reported separately from value/roofline"}
+        del hi
+        if not args.no_e2e and world == 1:
+            # the same end-to-end path as `e2e` (host CSR -> HBM -> run -> read-back) in interval
+            # mode: the run index needs the whole stream, so the upload is not hidden here
+            g.pin(True)
 
-                def e2e_interval():
-                    t = time.perf_counter()
-                    dg = DeviceGraph(g, local, (v0, v1), async_upload=True)
-                    h = HyperBall(dg, P, args.depth or None, interval=True)
-                    it = h.run()
-                    sd = h.state().sum_d
-                    torch.cuda.synchronize()
-                    dt = time.perf_counter() - t
-                    del h, dg
-                    return dt, it, sd
+            def e2e_interval():
+                t = time.perf_counter()
+                dg = DeviceGraph(g, local, (v0, v1), async_upload=True)
+                h = HyperBall(dg, P, args.depth or None, interval=True)
+                it = h.run()
+                sd = h.state().sum_d
+                torch.cuda.synchronize()
+                dt = time.perf_counter() - t
+                del h, dg
+                return dt, it, sd
 
-                e2e_interval()
-                ts = [e2e_interval() for _ in range(max(args.steps, 3))]
-                es = statistics.mean(t for t, _, _ in ts)
-                line["variants"]["interval"]["e2e"] = {
-                    "seconds_per_step": es, "dense_equivalent_updates_per_s": ts[-1][1] * g.edges * m / es,
-                    "sum_d_identical_to_dense": bool(np.array_equal(ts[-1][2], hb.state().sum_d)),
-                    "h2d_bytes_per_step": g.stream_len + 8 * (g.n + 1) + 4 * g.n,
-                    "path": "sb_graph_create_async + sb_hb_create(SB_HB_INTERVAL) (waits for the upload, builds "
-                            "the run index) + sb_hb_run + sb_hb_read_state"}
-                g.pin(False)
+            e2e_interval()
+            ts = [e2e_interval() for _ in range(max(args.steps, 3))]
+            es = statistics.mean(t for t, _, _ in ts)
+            line["variants"]["interval"]["e2e"] = {
+                "seconds_per_step": es, "dense_equivalent_updates_per_s": ts[-1][1] * g.edges * m / es,
+                "sum_d_identical_to_dense": bool(np.array_equal(ts[-1][2], hb.state().sum_d)),
+                "h2d_bytes_per_step": g.stream_len + 8 * (g.n + 1) + 4 * g.n,
+                "path": "sb_graph_create_async + sb_hb_create(SB_HB_INTERVAL) (waits for the upload, builds "
+                        "the run index) + sb_hb_run + sb_hb_read_state"}
+            g.pin(False)
 
     # ---- paper pipeline on the device: raster obstacle mask -> visibility graph built in HBM
     # (sb_graph_build_grid) -> HyperBall -> BFS metrics; the only H2D copy is the mask.
