@@ -130,6 +130,29 @@ def build_graph(cfg, threads=0):
     return g
 
 
+def build_graph_reference(cfg, threads=0):
+    """The same graph from the oracle's own generator (oracle/sb_synth.c, byte-identical:
+    tests/test_oracle_synth.py), so the reference arm never maps the product library."""
+    import oracle
+    r, c, k, a, b, seed, rad2, _ = CONFIGS[cfg]
+    t0 = time.perf_counter()
+    g = oracle.SynthCsr(r, c, k, a, b, seed, rad2, threads)
+    log(f"[bench] generated {cfg} (oracle generator): {g} in {time.perf_counter() - t0:.1f} s")
+    return g
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
 def alg_bytes_per_iter(n, edges, stream_len, p):
     """CSR (stream + 8(N+1) + 4N) + |E| m/2 + N m/2 (own) + N m/2 (write)."""
     row = (1 << p) // 2
@@ -199,19 +222,25 @@ def run_cpu(g, p, target_s, threads, reps=1):
     m = 1 << p
     return {
         "value": edges * m / statistics.median(times), "unit": UNIT, "cores": threads, "kind": O.kind,
-        "sample": f"iterate_once (t=1) over nodes [{v0},{v1}) = {v1 - v0} nodes / {edges} edges of the same "
-                  f"graph, p={p}, {threads} threads, median of {reps} ({statistics.median(times):.2f} s)",
+        "cpu_model": cpu_model(), "nproc": os.cpu_count(),
+        "sample": sample_text(v0, v1, edges, p, threads) + f", median of {reps} ({statistics.median(times):.2f} s)",
         "seconds": times,
     }
+
+
+def sample_text(v0, v1, edges, p, threads):
+    return (f"iterate_once (t=1) over nodes [{v0},{v1}) = {v1 - v0} nodes / {edges} edges of the same graph, "
+            f"p={p}, {threads} threads (parallel_ranges). Representative of every pass: the reference's "
+            f"iterate_once unions all neighbour rows whatever t is (SPEC.md:427-435), so its time per "
+            f"edge does not depend on the iteration")
 
 
 def reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    g = build_graph(args.config)
     threads = os.cpu_count() or 1
-    import oracle
+    g = build_graph_reference(args.config, threads)
     O, (v0, v1), edges, bufs = cpu_sample(g, args.p, args.cpu_step_s, threads)
     cur, nxt, c0, c1, sd, sd2 = bufs
     for _ in range(args.warmup):
@@ -223,29 +252,47 @@ def reference_arm(args):
         times.append(time.perf_counter() - t0)
     m = 1 << args.p
     v = edges * m / statistics.mean(times)
-    cb = {"value": v, "unit": UNIT, "cores": threads, "kind": O.kind,
-          "sample": f"iterate_once (t=1) over nodes [{v0},{v1}) ({v1 - v0} nodes, {edges} edges) of {args.config}"}
+    cb = {"value": v, "unit": UNIT, "cores": threads, "kind": O.kind, "cpu_model": cpu_model(),
+          "nproc": os.cpu_count(), "sample": sample_text(v0, v1, edges, args.p, threads)}
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(times),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
-        "data": "synthetic", "config": dict(workload_config(args, g, None),
-                                            register_layout="reference packed 4-bit (hll.hpp:31-32)",
-                                            parallelism=f"{threads} host threads (parallel_ranges)"),
+        "data": "synthetic", "config": workload_config(args, g),
+        "run": {"register_layout": "reference packed 4-bit (hll.hpp:31-32)",
+                "parallelism": f"{threads} host threads (parallel_ranges)",
+                "graph_generator": "oracle/sb_synth.c (byte-identical to the product generator)",
+                "ops": O._opsname().decode() if O.kind == "reference" else "port"},
         "cpu_baseline": cb, "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    line["run"]["repo_libraries_mapped"] = repo_libraries_mapped()
     print(json.dumps(line), flush=True)
     return 0
 
 
-def workload_config(args, g, iters):
+def repo_libraries_mapped():
+    """Shared objects under this repository mapped by this process (the reference arm
+    must show only oracle/ ones)."""
+    out = set()
+    try:
+        with open("/proc/self/maps") as f:
+            for ln in f:
+                path = ln.split()[-1] if ln.rstrip().endswith(".so") else ""
+                if path.startswith(ROOT):
+                    out.add(os.path.relpath(path, ROOT))
+    except OSError:
+        pass
+    return sorted(out)
+
+
+def workload_config(args, g):
+    """Identical in both arms: only what defines the workload."""
     return {
         "workload": CONFIGS[args.config][7] + f", p={args.p}, depth {'unbounded' if not args.depth else args.depth}",
         "config": args.config, "nodes": g.n, "edges": g.edges, "stream_bytes": g.stream_len, "p": args.p,
-        "depth_limit": args.depth or None, "iterations": iters,
-        "register_layout": "4-bit bit-sliced (reference density m/2 B per row)",
+        "depth_limit": args.depth or None,
         "l2": "inputs larger than L2 (4.8 GB CSR stream read every iteration; 121 MB plane)" if args.config == "c3"
-        else "small graph", "parallelism": f"node-range shards x{args.gpus}",
+        else "small graph",
     }
 
 
@@ -318,14 +365,24 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_2604_08374_b200 import DeviceGraph, HllParams, HyperBall
-    from paper_2604_08374_b200.distributed import init_comm, sharded_hyperball
+    from paper_2604_08374_b200.distributed import (attach_peers, init_comm, reset_external_barrier,
+                                                   run_external_barrier, sharded_hyperball)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    ndev = max(torch.cuda.device_count(), 1)
+    local = local_rank % ndev
+    # More ranks than GPUs (a functional run of the sharded path on a 1-GPU lease):
+    # NCCL refuses two ranks on one device, so the rows travel as fused P2P stores
+    # over CUDA IPC and a gloo all-reduce of the max increase is the iteration barrier.
+    shared = world > ndev
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     g = build_graph(args.config, threads=max(1, (os.cpu_count() or 1) // max(world, 1)))
     P = HllParams(args.p)
     m = P.m
@@ -340,14 +397,15 @@ def main():
     def max_over_ranks(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if shared else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    comm = init_comm(rank, world, local)
+    comm = None if shared else init_comm(rank, world, local)
 
     def make_hb(skip=False):
-        return sharded_hyperball(g, P, args.depth or None, rank, world, local, comm, skip, bounds)
+        return sharded_hyperball(g, P, args.depth or None, rank, world, local, comm, skip, bounds,
+                                 external_barrier=shared)
 
     t0 = time.perf_counter()
     hb = make_hb()
@@ -356,6 +414,9 @@ def main():
     stream = torch.cuda.ExternalStream(hb.stream_handle())
 
     def one_run(h):
+        if shared:
+            reset_external_barrier(h)
+            return run_external_barrier(h)
         h.reset()
         return h.run()
 
@@ -402,7 +463,10 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * dev_s / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": dict(workload_config(args, g, iters), last_changing_pass=int(last_changing)),
+        "config": workload_config(args, g),
+        "run": {"iterations": iters, "last_changing_pass": int(last_changing),
+                "register_layout": "4-bit bit-sliced (reference density m/2 B per row)",
+                "parallelism": f"node-range shards x{world}"},
         "hbm_gbs_algorithmic": bytes_iter * iters * args.steps / dev_s / 1e9,
         "end_to_end_s_device": dev_s / args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk, "unit": "GB/s", "frac": achieved / pk,
@@ -416,6 +480,8 @@ def main():
         "per_iteration_ms": [round(s["step_ms"], 3) for s in st],
         "exchange_ms": [round(s["exchange_ms"], 4) for s in st] if world > 1 else None,
         "exchange": getattr(hb, "exchange_mode", None) if world > 1 else None,
+        "shared_device": ({"ranks": world, "gpus": ndev, "note": "functional run of the sharded path: ranks share "
+                           "a GPU, so this is not a scaling point"} if shared else None),
         "clocks": clock_info,
         "gpu_launches": args.steps * (2 + 2 * iters),
     }
@@ -429,12 +495,18 @@ def main():
             t = time.perf_counter()
             dg = DeviceGraph(g, local, (v0, v1), async_upload=True)
             h = HyperBall(dg, P, args.depth or None)
-            if comm is not None:
-                h.attach_comm(comm, bounds)
-            it = h.run()
+            if shared:
+                attach_peers(h, rank, world, bounds)
+                it = run_external_barrier(h)
+            else:
+                if comm is not None:
+                    h.attach_comm(comm, bounds)
+                it = h.run()
             s = h.state()  # D2H c_t, c_(t-1), sum_d, sum_d2, changed
             torch.cuda.synchronize()
             dt = time.perf_counter() - t
+            if shared:
+                dist.barrier()  # no peer still holds this rank's IPC-exported planes
             del h, dg, s
             return dt, it
         e2e_once()
@@ -472,7 +544,8 @@ def main():
             "per_iteration_union_ms": [round(s["union_ms"], 3) for s in hs.stats()],
             "note": "gathers only neighbours whose registers changed last iteration; not used for value/roofline"}}
         del hs
-        hi = sharded_hyperball(g, P, args.depth or None, rank, world, local, comm, False, bounds, interval=True)
+        hi = sharded_hyperball(g, P, args.depth or None, rank, world, local, comm, False, bounds, interval=True,
+                               external_barrier=shared)
         one_run(hi)
         barrier()
         s3 = torch.cuda.ExternalStream(hi.stream_handle())

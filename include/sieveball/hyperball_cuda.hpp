@@ -326,13 +326,13 @@ inline double diamond(double k) {
   return 2.0 * (k * (std::log2((k + 2.0) / 3.0) - 1.0) + 1.0) / ((k - 1.0) * (k - 2.0));
 }
 inline double integration_hh(double md, uint32_t nv) {
-  if (nv < 3 || std::isnan(md) || md == 1.0) return NAN;
+  if (nv < 3 || std::isnan(md) || !(md > 1.0)) return NAN;  // pre: MD > 1
   return 1.0 / (relative_asymmetry(md, nv) / diamond(nv));
 }
 inline double integration_pv(double md, uint32_t nv) {
   if (nv < 3 || std::isnan(md)) return NAN;
   const double x = 1.0 - relative_asymmetry(md, nv);
-  return x > 0.0 ? x : 0.0;
+  return x > 0.0 ? (x < 1.0 ? x : 1.0) : 0.0;  // in [0, 1]
 }
 }  // namespace metrics
 

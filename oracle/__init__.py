@@ -246,6 +246,41 @@ class Oracle:
         return float(self._sum_recip(d, d.size))
 
 
+class SynthCsr:
+    """The benchmark grid graph built by the oracle's own generator (sb_synth.c):
+    the CSR arrays of SPEC.md:174-177 as zero-copy numpy views of C buffers.
+    Duck-types CompressedCsr for Oracle.hb_iterate / hb_run."""
+
+    def __init__(self, rows, cols, n_rects, rect_min, rect_max, seed, radius2, threads=0):
+        import weakref
+        L = port()._L
+        f = L.sbo_synth_grid
+        f.restype = C.c_int
+        f.argtypes = [C.c_uint32] * 5 + [C.c_uint64, C.c_uint64, C.c_uint] + [C.c_void_p] * 5
+        n, off, deg, st, sl = C.c_uint64(), C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_uint64()
+        rc = f(rows, cols, n_rects, rect_min, rect_max, seed, radius2, threads or os.cpu_count() or 1,
+               C.byref(n), C.byref(off), C.byref(deg), C.byref(st), C.byref(sl))
+        if rc:
+            raise RuntimeError(f"sbo_synth_grid failed ({rc})")
+        L.sbo_synth_free.argtypes = [C.c_void_p]
+        for p in (off, deg, st):
+            weakref.finalize(self, L.sbo_synth_free, p.value)
+        self.n = n.value
+        self.stream_len = sl.value
+        view = lambda p, cnt, ct, dt: np.ctypeslib.as_array(C.cast(p, C.POINTER(ct)), (cnt,)).view(dt)  # noqa: E731
+        self.offsets = view(off, self.n + 1, C.c_uint64, np.uint64)
+        self.degrees = view(deg, self.n, C.c_uint32, np.uint32)
+        self._stream_padded = view(st, self.stream_len + 256, C.c_uint8, np.uint8)
+        self.stream = self._stream_padded[: self.stream_len]
+        self.edges = int(self.degrees.sum(dtype=np.uint64))
+
+    def stream_padded(self) -> np.ndarray:
+        return self._stream_padded
+
+    def __repr__(self) -> str:
+        return f"SynthCsr(N={self.n}, |E|={self.edges}, stream={self.stream_len} B)"
+
+
 _cache: dict = {}
 
 

@@ -340,8 +340,8 @@ void sbo_metrics(uint64_t n, const double* sum_d, const double* sum_d2, const ui
       if (nv[v] >= 3) {
         const double RA = 2.0 * (MD - 1.0) / (N - 2.0); /* SPEC.md:497 */
         const double pvv = 1.0 - RA;                    /* SPEC.md:515-516 */
-        PV = pvv > 0.0 ? pvv : 0.0;
-        if (MD != 1.0) {                                /* MD=1 -> NaN (SPEC.md:554) */
+        PV = pvv > 0.0 ? (pvv < 1.0 ? pvv : 1.0) : 0.0; /* in [0, 1] (SPEC.md:481, 551) */
+        if (MD > 1.0) {                                 /* pre MD > 1, else NaN */
           const double RRA = RA / diamond(N);
           IHH = 1.0 / RRA;
         }

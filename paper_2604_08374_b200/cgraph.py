@@ -36,7 +36,7 @@ def leb128_decode(data: bytes, pos: int = 0) -> tuple[int, int]:
             raise RuntimeError("leb128: truncated varint")
         b = data[pos]
         pos += 1
-        value |= (b & 0x7F) << shift
+        value = (value | ((b & 0x7F) << shift)) & 0xFFFFFFFFFFFFFFFF  # uint64_t, as the reference
         if not b & 0x80:
             return value, pos
         shift += 7

@@ -138,61 +138,6 @@ __device__ __host__ __forceinline__ unsigned long long dbl_to_ord(double x) {
   return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
 }
 
-// ---- warp-cooperative LEB128 decode -----------------------------------
-// One step consumes the 32-byte window at `pos` up to its last wanted varint
-// terminator (bit 7 clear).  Each terminator lane assembles its varint from
-// itself and up to four preceding bytes (shfl_up), a warp inclusive scan turns
-// deltas into absolute ids (first id of a row is absolute: base 0), and the
-// window always starts on a varint boundary so no carry crosses steps.
-// Returns the ballot of lanes holding a decoded id in *idmask and the id in *id.
-struct DecodeOut {
-  uint32_t mask;  // lanes holding a wanted id
-  uint32_t id;    // this lane's absolute id (valid iff mask bit set); for other
-                  // lanes the id of the closest wanted lane below (or base)
-  int count;      // popc(mask)
-  int last;       // lane of the last wanted id (-1 if none)
-  bool bad;       // (CHECK only) this lane's varint is > 5 bytes or exceeds 32 bits
-};
-
-template <bool CHECK>
-__device__ __forceinline__ DecodeOut decode_step(const uint8_t* __restrict__ stream, uint64_t pos,
-                                                 uint64_t end, uint32_t remaining, uint32_t base,
-                                                 int lane) {
-  const uint64_t at = pos + static_cast<uint64_t>(lane);
-  const uint32_t b = at < end ? static_cast<uint32_t>(__ldg(stream + at)) : 0x80u;
-  const bool term = (b & 0x80u) == 0;
-  const uint32_t T = __ballot_sync(FULL, term);
-  const uint32_t lt = (1u << lane) - 1u;
-  const uint32_t rank = __popc(T & lt);
-  const bool want = term && rank < remaining;
-  const uint32_t W = __ballot_sync(FULL, want);
-  const uint32_t b1 = __shfl_up_sync(FULL, b, 1);
-  const uint32_t b2 = __shfl_up_sync(FULL, b, 2);
-  const uint32_t b3 = __shfl_up_sync(FULL, b, 3);
-  const uint32_t b4 = __shfl_up_sync(FULL, b, 4);
-  const uint32_t below = T & lt;
-  const int start = below ? 32 - __clz(below) : 0;
-  const int k = lane - start;  // continuation bytes preceding this terminator
-  uint32_t v = b & 0x7fu;
-  if (k >= 1) v = (v << 7) | (b1 & 0x7fu);
-  if (k >= 2) v = (v << 7) | (b2 & 0x7fu);
-  if (k >= 3) v = (v << 7) | (b3 & 0x7fu);
-  if (k >= 4) v = (v << 7) | (b4 & 0x7fu);
-  if (!want) v = 0;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const uint32_t y = __shfl_up_sync(FULL, v, d);
-    if (lane >= d) v += y;
-  }
-  DecodeOut o;
-  o.mask = W;
-  o.id = base + v;
-  o.count = __popc(W);
-  o.last = W ? 31 - __clz(W) : -1;
-  o.bad = CHECK ? (want && (k > 4 || (k == 4 && (b & 0x7fu) > 0x0fu))) : false;
-  return o;
-}
-
 // ---- 4-bytes-per-lane LEB128 decode (hot path) ------------------------
 // A 128-byte window at `pos` (a varint boundary); lane L holds bytes
 // 4L..4L+3.  Because every byte's payload lands in exactly one delta, the
@@ -200,8 +145,10 @@ __device__ __forceinline__ DecodeOut decode_step(const uint8_t* __restrict__ str
 //     base + sum_{k <= j} (b_k & 0x7f) << (7 * d_k),
 // d_k = number of continuation bytes immediately preceding byte k -- a plain
 // prefix sum over bytes, no segmented reduction.  d_k needs at most 4 bytes
-// of look-back (ids < 2^32 -> varints <= 5 bytes), i.e. the previous lane's
-// word.  Only the first `remaining` terminators are taken; the window's
+// of look-back (ids < 2^32 -> at most 5 payload-carrying bytes; the bytes of a
+// non-canonical varint beyond the 5th carry zero payload on a validated
+// stream, so capping d_k at 4 leaves their contribution 0), i.e. the previous
+// lane's word.  Only the first `remaining` terminators are taken; the window's
 // trailing partial varint is re-read by the next step.
 struct Decode4 {
   int wanted;     // terminators consumed from the item in this window

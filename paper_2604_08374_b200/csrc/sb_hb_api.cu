@@ -54,10 +54,6 @@ int sb_hb_create(sb_graph* g, unsigned p, uint32_t depth_limit, uint32_t flags, 
   h->p = p;
   h->depth = depth_limit;
   h->flags = flags;
-  if (const char* e = getenv("SB_UNION_SCHEDULE")) {  // A/B override for benchmarking
-    if (!strcmp(e, "warp")) h->flags |= SB_HB_SCHEDULE_WARP;
-    if (!strcmp(e, "tile")) h->flags &= ~SB_HB_SCHEDULE_WARP;
-  }
   const uint32_t m = 1u << p;
   h->row = m / 2;
   h->slices = sb::union_slices(static_cast<int>(p));
@@ -218,6 +214,7 @@ int sb_hb_step_compute(sb_hb* h, double* local_max) {
         cudaStream_t sk = (k & 1) ? h->stream2 : h->stream;
         CK(cudaStreamWaitEvent(sk, g->val_ev[k], 0));
         sb::UnionArgs uk = u;
+        uk.err = g->d_err;  // stop at once if this or an earlier chunk failed validation
         uk.work = h->d_chunk_work + k;
         uk.tile_node0 = g->d_tile_node0 + t0;
         uk.tile_q = g->d_tile_q + t0;
@@ -360,7 +357,7 @@ int sb_hb_step(sb_hb* h, double* max_increase, int* converged, int* finished) {
   double mx = 0.0;
   int rc = sb_hb_step_compute(h, &mx);
   if (rc) return rc;
-  if (h->comm && h->comm->nranks > 1) {
+  if (h->comm) {  // any attached communicator, a 1-rank one included: same code path at every N
     DeviceGuard dg(h->g->device);
     rc = exchange_nccl(h, &mx);
     if (rc) {

@@ -37,6 +37,11 @@ struct UnionArgs {
   uint8_t* changed_out;        // global-indexed, 1 = registers changed this iteration
   const uint8_t* changed_in;   // global-indexed, previous iteration (skip mode)
   unsigned long long* work;    // dynamic work counter (zeroed per launch)
+  // Upload-time validation verdict (min bad local node, ~0 = clean; NULL once
+  // the upload is complete).  During the pipelined first pass a chunk's union
+  // starts right after its validation: CTAs stop fetching work once it is set,
+  // so ids from a malformed row are never used as row addresses.
+  const unsigned long long* err;
   // CTA tile schedule (n_tiles == 0 -> per-warp item schedule)
   uint64_t n_tiles;
   uint64_t n_local;

@@ -28,12 +28,18 @@ namespace sb {
 // ------------------------------------------------------------------ build
 // Upload-time validation and work-item cutting (leb128.hpp:28-39, SPEC.md:
 // 174-177, restricted to 32-bit ids).  A row is valid iff
-//   * no varint is longer than 5 bytes,
 //   * it holds exactly deg varints and ends on a terminator (no truncation,
-//     no trailing bytes),
+//     no trailing bytes), none longer than 10 bytes (leb128.hpp:38),
 //   * no varint after the first has value 0 (ids strictly increasing),
 //   * the sum of its varints -- the last id -- is < N (so no id is >= N and no
 //     32-bit wrap: every delta is >= 1).
+// Canonical varints of ids < 2^32 are at most 5 bytes.  The reference decoder
+// also accepts non-canonical encodings of up to 10 bytes (zero-payload
+// continuation bytes, leb128.hpp:28-39); a row holding a byte with >= 5
+// continuation bytes before it is re-checked by a scalar decode with exactly
+// the reference's semantics (long_row_ok) -- rare, so the SWAR fast path below
+// stays 5-byte only.  On an accepted row every byte at depth >= 5 has zero
+// payload, so the device decoders' 4-byte look-back is exact for it.
 // All four are reductions over the row's bytes, so one warp streams a row in
 // 512-byte windows (16 bytes per lane, byte-parallel SWAR on 32-bit words)
 // and reduces across lanes once per row; only the windows holding an item cut
@@ -47,6 +53,32 @@ __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefe
 // 0x80 in every byte of x whose low 7 bits are zero.
 __device__ __forceinline__ uint32_t zero_payload(uint32_t x) {
   return ~((x & 0x7f7f7f7fu) + 0x7f7f7f7fu) & 0x80808080u;
+}
+
+// Scalar decode of one row with the reference's semantics: leb128_decode
+// (leb128.hpp:28-39: truncation or > 10 bytes -> error) per varint, id =
+// first or prev + delta, id < N, delta != 0 after the first, no trailing bytes.
+// Deltas >= 2^32 are rejected (the u64 sum could wrap below prev: a
+// non-increasing row).
+__device__ bool long_row_ok(const uint8_t* stream, uint64_t pos, uint64_t end, uint32_t deg, uint64_t n) {
+  uint64_t prev = 0;
+  for (uint32_t k = 0; k < deg; ++k) {
+    uint64_t x = 0;
+    unsigned shift = 0;
+    bool term = false;
+    for (int i = 0; i < 10 && !term; ++i) {
+      if (pos >= end) return false;
+      const uint8_t b = stream[pos++];
+      if (shift < 64) x |= static_cast<uint64_t>(b & 0x7fu) << shift;
+      term = !(b & 0x80u);
+      shift += 7;
+    }
+    if (!term || x >= (1ull << 32)) return false;
+    const uint64_t id = k ? prev + x : x;
+    if (id >= n || (k && x == 0)) return false;
+    prev = id;
+  }
+  return pos == end;
 }
 
 __global__ void __launch_bounds__(256, 3) build_items_kernel(BuildArgs a) {
@@ -69,7 +101,7 @@ __global__ void __launch_bounds__(256, 3) build_items_kernel(BuildArgs a) {
       if (lane == 0 && (deg != 0 || end != pos0)) atomicMin(a.err_node, static_cast<unsigned long long>(node));
       continue;
     }
-    uint32_t cnt = 0, zeros = 0, bad = 0;  // per lane
+    uint32_t cnt = 0, zeros = 0, lng = 0;  // per lane (lng: a byte at varint depth >= 5)
     unsigned long long sum = 0;            // per lane: sum of its varint contributions
     uint32_t px2 = 0, px3 = 0;             // words 2, 3 of the previous window's lane 31
     uint32_t done = 0;                     // terminators before this window (cut rows only)
@@ -118,7 +150,7 @@ __global__ void __launch_bounds__(256, 3) build_items_kernel(BuildArgs a) {
         const uint32_t m3 = m2 & __funnelshift_l(Fp, F, 24);
         const uint32_t m4 = m3 & Fp;
         const uint32_t m5 = m4 & __funnelshift_l(Fpp, Fp, 8);
-        bad |= m5 & vm[i];  // a varint longer than 5 bytes
+        lng |= m5 & vm[i];  // a varint longer than 5 bytes: the scalar check decides
         const uint32_t T = ~w & 0x80808080u & vm[i];
         tw[i] = T;
         lcnt += __popc(T);
@@ -196,7 +228,7 @@ __global__ void __launch_bounds__(256, 3) build_items_kernel(BuildArgs a) {
     for (int o = 16; o >= 1; o >>= 1) {
       cnt += __shfl_xor_sync(FULL, cnt, o);
       zeros += __shfl_xor_sync(FULL, zeros, o);
-      bad |= __shfl_xor_sync(FULL, bad, o);
+      lng |= __shfl_xor_sync(FULL, lng, o);
       sum += __shfl_xor_sync(FULL, sum, o);
     }
     if (lane == 0) {
@@ -208,8 +240,8 @@ __global__ void __launch_bounds__(256, 3) build_items_kernel(BuildArgs a) {
         if (!(c & 0x80u)) break;
       }
       const bool ends_on_terminator = !(a.stream[end - 1] & 0x80u);
-      const bool ok = !bad && cnt == deg && ends_on_terminator && zeros == (first_zero ? 1u : 0u) &&
-                      sum < a.n_global;
+      const bool ok = lng ? long_row_ok(a.stream, pos0, end, deg, a.n_global)
+                          : cnt == deg && ends_on_terminator && zeros == (first_zero ? 1u : 0u) && sum < a.n_global;
       if (!ok) atomicMin(a.err_node, static_cast<unsigned long long>(node));
     }
   }
@@ -534,6 +566,10 @@ __device__ __forceinline__ void process_item(const UnionArgs& a, uint64_t item, 
   if (finish) publish_row<P>(a, curb, nextb, goff, v, acc, lane);
 }
 
+__device__ __forceinline__ bool upload_failed(const UnionArgs& a) {
+  return a.err && *reinterpret_cast<const volatile unsigned long long*>(a.err) != ~0ull;
+}
+
 // Fused decode-union kernel.  Two schedules over the same work units:
 //  TILE=false: each warp grabs the next (item, slice) from a global counter.
 //  TILE=true : each CTA grabs a tile = (8 consecutive nodes, chunk index q,
@@ -553,7 +589,7 @@ __global__ void __launch_bounds__(256, C::MINB) union_kernel(UnionArgs a) {
     const uint64_t total = a.n_items * G::SLICES;
     for (;;) {
       unsigned long long u = 0;
-      if (lane == 0) u = atomicAdd(a.work, 1ull);
+      if (lane == 0) u = upload_failed(a) ? total : atomicAdd(a.work, 1ull);
       u = __shfl_sync(FULL, u, 0);
       if (u >= total) break;
       process_item<P, SKIP, C>(a, u / G::SLICES, static_cast<int>(u % G::SLICES), lane, buf);
@@ -561,7 +597,7 @@ __global__ void __launch_bounds__(256, C::MINB) union_kernel(UnionArgs a) {
   } else {
     const uint64_t total = a.n_tiles * G::SLICES;
     for (int k = 0;; ++k) {
-      if (threadIdx.x == 0) s_unit[k & 1] = atomicAdd(a.work, 1ull);
+      if (threadIdx.x == 0) s_unit[k & 1] = upload_failed(a) ? total : atomicAdd(a.work, 1ull);
       __syncthreads();
       const unsigned long long u = s_unit[k & 1];
       if (u >= total) break;
@@ -1006,8 +1042,10 @@ __global__ void metrics_kernel(MetricArgs a) {
       if (nv >= 3) {
         const double RA = 2.0 * (MD - 1.0) / (N - 2.0);
         const double pv = 1.0 - RA;
-        PV = pv > 0.0 ? pv : 0.0;
-        if (MD != 1.0) {
+        // integration_pv in [0, 1]: an HLL estimate can put
+        // MD below 1 (RA < 0), so both ends are clamped
+        PV = pv > 0.0 ? (pv < 1.0 ? pv : 1.0) : 0.0;
+        if (MD > 1.0) {  // integration_hh pre: MD > 1, else NaN
           const double Dk = 2.0 * (N * (log2((N + 2.0) / 3.0) - 1.0) + 1.0) / ((N - 1.0) * (N - 2.0));
           IHH = 1.0 / (RA / Dk);
         }
@@ -1173,48 +1211,12 @@ cudaError_t launch_init(int p, uint8_t* plane, uint64_t n, const uint32_t* orig,
 
 int union_slices(int p) { return p > 10 ? 1 << (p - 10) : 1; }
 
-// p=10 dense tile kernel variants for A/B runs (SB_UNION_VARIANT=0..9);
-// 0 = DefaultCfg (8-row single buffer, bit-serial 9-way max, 4 CTAs/SM).
-// C3 union ms/iter on one B200 (profiles/r01b_union_variants.txt): tree max
-// 97.9; 5: 94.7; 6: 95.8; 7: 99.2; 8: 106.8.
-using V10_1 = UCfg<8, true, 2, false>;   // 8-row double buffer (round-1 first design)
-using V10_2 = UCfg<4, false, 6, false>;  // 4-row single buffer, 6 CTAs/SM
-using V10_3 = UCfg<6, false, 5, false>;  // 6-row single buffer, 5 CTAs/SM
-using V10_4 = UCfg<12, false, 3, false>; // 12-row single buffer, 3 CTAs/SM
-using V10_5 = UCfg<8, false, 4, false, false>;  // 8-row single buffer, pairwise tree max (round-1 default)
-using V10_6 = UCfg<12, false, 3, false, true>;  // 12-row, bit-serial 13-way max
-using V10_7 = UCfg<16, false, 2, false, true>;  // 16-row, bit-serial 17-way max
-using V10_8 = UCfg<6, false, 5, false, true>;   // 6-row, bit-serial 7-way max
-using V10_9 = UCfg<16, false, 3, false, true>;  // 16-row, bit-serial 17-way max, 3 CTAs/SM
-
-static int union_variant() {
-  static const int v = [] {
-    const char* e = getenv("SB_UNION_VARIANT");
-    return e ? atoi(e) : 0;
-  }();
-  return v;
-}
-
 cudaError_t launch_union(int p, bool skip, const UnionArgs& a, cudaStream_t s) {
   const bool tile = a.n_tiles != 0;
 #define SB_UL(P, SK, TL, ...)                                                                        \
   {                                                                                                  \
     static int g = grid_for(reinterpret_cast<const void*>(union_kernel<P, SK, TL, ##__VA_ARGS__>), 256); \
     union_kernel<P, SK, TL, ##__VA_ARGS__><<<g, 256, 0, s>>>(a);                                     \
-  }
-  if (p == 10 && !skip && tile && union_variant() != 0) {
-    switch (union_variant()) {
-      case 1: SB_UL(10, false, true, V10_1) break;
-      case 2: SB_UL(10, false, true, V10_2) break;
-      case 3: SB_UL(10, false, true, V10_3) break;
-      case 4: SB_UL(10, false, true, V10_4) break;
-      case 5: SB_UL(10, false, true, V10_5) break;
-      case 6: SB_UL(10, false, true, V10_6) break;
-      case 7: SB_UL(10, false, true, V10_7) break;
-      case 8: SB_UL(10, false, true, V10_8) break;
-      default: SB_UL(10, false, true, V10_9) break;
-    }
-    return cudaGetLastError();
   }
 #define SB_L(P)                                                     \
   {                                                                 \

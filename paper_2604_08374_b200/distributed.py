@@ -44,10 +44,12 @@ def attach_peers(hb: HyperBall, rank: int, world: int, bounds: np.ndarray) -> No
 def sharded_hyperball(csr: CompressedCsr, params: HllParams | int, depth_limit: int | None, rank: int,
                       world: int, device: int, comm: Comm | None, skip_unchanged: bool = False,
                       bounds: np.ndarray | None = None, interval: bool = False,
-                      fused_p2p: bool = True) -> HyperBall:
+                      fused_p2p: bool = True, external_barrier: bool = False) -> HyperBall:
     """This rank's HyperBall over its node range, wired to the communicator.
     fused_p2p: rows travel as P2P stores from the union kernel (NCCL only
-    carries the 8-byte max / barrier); otherwise grouped ncclBroadcast."""
+    carries the 8-byte max / barrier); otherwise grouped ncclBroadcast.
+    external_barrier: no NCCL at all (ranks sharing a GPU): fused P2P rows, and
+    the caller runs the iterations with run_external_barrier."""
     import os
     b = shard_bounds(csr, world) if bounds is None else bounds
     v0, v1 = int(b[rank]), int(b[rank + 1])
@@ -58,6 +60,10 @@ def sharded_hyperball(csr: CompressedCsr, params: HllParams | int, depth_limit: 
 
     hb = make()
     hb.exchange_mode = "single"
+    if world > 1 and external_barrier:  # no NCCL (ranks share a device): fused P2P + external barrier only
+        attach_peers(hb, rank, world, b)
+        hb.exchange_mode = "fused-p2p (external torch.distributed barrier)"
+        return hb
     if world > 1:
         hb.exchange_mode = "nccl-broadcast"
         if fused_p2p and os.environ.get("SB_P2P", "1") != "0":
@@ -82,6 +88,29 @@ def sharded_hyperball(csr: CompressedCsr, params: HllParams | int, depth_limit: 
     if comm is not None:
         hb.attach_comm(comm, b)
     return hb
+
+
+def run_external_barrier(hb: HyperBall) -> int:
+    """Alg. 1 for a rank whose rows travel as fused P2P stores but whose ranks
+    share no NCCL communicator (e.g. several ranks on one GPU, which NCCL
+    refuses): step_compute (returns after this rank's union kernel, and so its
+    peer stores, completed), then a torch.distributed all-reduce of the local
+    max increase -- the iteration barrier -- then step_finish."""
+    import torch
+    import torch.distributed as dist
+    while True:
+        mx = torch.tensor([hb.step_compute()], dtype=torch.float64)
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        if hb.step_finish(float(mx.item()))[1]:
+            return hb.t
+
+
+def reset_external_barrier(hb: HyperBall) -> None:
+    """sb_hb_reset + the barrier that keeps peers from storing into a replica that
+    is still being re-initialised (the in-library NCCL barrier's role)."""
+    import torch.distributed as dist
+    hb.reset()
+    dist.barrier()
 
 
 def gather_to_root(local: np.ndarray, bounds: np.ndarray, rank: int, world: int) -> np.ndarray | None:

@@ -23,8 +23,8 @@ def diamond(k: float) -> float:
 
 
 def integration_hh(md: float, n_v: int) -> float:
-    """1 / RRA; NaN if N_v < 3 or MD == 1 (SPEC.md:494-502, :554)."""
-    if n_v < 3 or math.isnan(md) or md == 1.0:
+    """1 / RRA; NaN unless N_v >= 3 and MD > 1."""
+    if n_v < 3 or math.isnan(md) or not md > 1.0:
         return float("nan")
     return 1.0 / (relative_asymmetry(md, n_v) / diamond(n_v))
 
@@ -35,10 +35,11 @@ def integration_tekl(md: float) -> float:
 
 
 def integration_pv(md: float, n_v: int) -> float:
-    """max(0, 1 - RA) (SPEC.md:512-520)."""
+    """max(0, 1 - RA), clamped to [0, 1]: an HLL
+    estimate can put MD below 1."""
     if n_v < 3 or math.isnan(md):
         return float("nan")
-    return max(0.0, 1.0 - relative_asymmetry(md, n_v))
+    return min(1.0, max(0.0, 1.0 - relative_asymmetry(md, n_v)))
 
 
 def moments(md: float, deg: int, sum_d2: float, n_v: int) -> tuple[float, float]:

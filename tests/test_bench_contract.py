@@ -29,6 +29,12 @@ def test_reference_arm_json_line():
     cb = d["cpu_baseline"]
     assert cb["value"] == d["value"] and cb["cores"] >= 1 and cb["kind"] in ("reference", "port") and cb["sample"]
     assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+    # the reference arm builds its graph with the oracle's generator: the product library is never mapped
+    libs = d["run"]["repo_libraries_mapped"]
+    assert libs and all(x.startswith("oracle" + os.sep) for x in libs), libs
+    assert cb["cpu_model"] and cb["nproc"] >= 1
+    # config holds only the workload, so both arms' configs compare equal
+    assert set(d["config"]) == {"workload", "config", "nodes", "edges", "stream_bytes", "p", "depth_limit", "l2"}
 
 
 def test_reference_arm_other_ranks_exit_quietly():

@@ -53,12 +53,32 @@ def _raw(n, offsets, degrees, stream):
     return CompressedCsr.from_arrays(offsets, degrees, bytes(stream))
 
 
+def _cut_row(n, deg, bad_at, kind):
+    """Node 0 -> ids 1..deg (cut into 512-id work items), malformed at neighbour
+    `bad_at`: a zero delta, or a delta that jumps far past N; other rows empty."""
+    from paper_2604_08374_b200.cgraph import leb128_encode
+    row = bytearray(leb128_encode(1))
+    for k in range(1, deg):
+        d = 1
+        if k == bad_at:
+            d = 0 if kind == "zero" else (1 << 31)
+        row += leb128_encode(d)
+    offs = [0, len(row)] + [len(row)] * (n - 1)
+    return n, offs, [deg] + [0] * (n - 1), list(row)
+
+
 @pytest.mark.parametrize("bad", [
     (2, [0, 1, 2], [1, 1], [0x81, 0x80]),                  # truncated varint
     (3, [0, 2, 3, 4], [1, 1, 1], [1, 1, 0, 1]),             # degree mismatch
     (2, [0, 1, 2], [1, 1], [5, 0]),                         # id out of range
-], ids=["truncated", "degree", "range"])
+    (2, [0, 5, 6], [1, 1], [0x80, 0x80, 0x80, 0x80, 0x08, 0]),  # id 2^31: far outside the plane
+    _cut_row(1600, 1500, 1000, "zero"),                     # zero delta inside the row's 2nd work item
+    _cut_row(1600, 1500, 700, "huge"),                      # id jump of 2^31 inside a cut row
+], ids=["truncated", "degree", "range", "range_huge", "cut_zero", "cut_huge"])
 def test_async_upload_reports_malformed_stream(bad):
+    """A malformed row surfaces as RuntimeError (sticky), and the pipelined first
+    pass never dereferences its ids: the union CTAs stop once validation has
+    flagged the chunk, so the CUDA context stays healthy (the next graph runs)."""
     g = _raw(*bad)
     dg = DeviceGraph(g, async_upload=True)
     hb = HyperBall(dg, 10, None)
@@ -68,3 +88,9 @@ def test_async_upload_reports_malformed_stream(bad):
         hb.iterate_once()
     with pytest.raises(RuntimeError):
         DeviceGraph(g, async_upload=True).wait()
+    ok = CompressedCsr.from_adjacency([[1], [0, 2], [1], []])
+    h = HyperBall(DeviceGraph(ok, async_upload=True), 10, None)
+    h.run()
+    ref = HyperBall(ok, 10, None)
+    ref.run()
+    assert np.array_equal(h.registers(), ref.registers())

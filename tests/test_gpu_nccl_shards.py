@@ -80,6 +80,31 @@ def test_nccl_sharded_bit_identical(world, interval):
     assert xms > 0.0  # the exchange actually ran
 
 
+@pytest.mark.parametrize("interval", [False, True])
+def test_nccl_exchange_one_rank_communicator(interval):
+    """The in-library exchange (grouped ncclBroadcast of the shard rows + 8-byte
+    ncclAllReduce(max), sb_hb_api.cu exchange_nccl) runs for ANY attached
+    communicator, a 1-rank one included, so it executes on a 1-GPU box: every
+    iteration goes through it and the result stays bit-identical."""
+    from paper_2604_08374_b200 import CompressedCsr, HyperBall
+    from paper_2604_08374_b200.hyperball import Comm
+    g = CompressedCsr.synth_grid(64, 64, 20, 2, 9, 20261017, 0)
+    ref = HyperBall(g, 10, None, interval=interval)
+    ref.run()
+    comm = Comm(1, 0, Comm.unique_id(), 0)
+    hb = HyperBall(g, 10, None, interval=interval)
+    hb.attach_comm(comm, [0, g.n])
+    for _ in range(2):  # run, reset, run again
+        hb.run()
+        st = hb.stats()
+        assert len(st) == ref.t and all(s["exchange_ms"] > 0.0 for s in st)
+        assert np.array_equal(hb.registers(), ref.registers())
+        assert np.array_equal(hb.state().sum_d, ref.state().sum_d)
+        hb.reset()
+    del hb
+    comm.close()
+
+
 def _rank_p2p(rank, world, port, q, mode):
     """Two+ processes, fused P2P row stores over CUDA IPC, gloo barrier + max."""
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))

@@ -265,9 +265,12 @@ def test_gpu_errors():
     # id out of range
     with pytest.raises(RuntimeError):
         DeviceGraph.from_raw(2, [0, 1, 2], [1, 1], [5, 0])
-    # varint longer than 5 bytes
+    # varint longer than 10 bytes (leb128.hpp:38)
     with pytest.raises(RuntimeError):
-        DeviceGraph.from_raw(2, [0, 6, 7], [1, 1], [0x81, 0x80, 0x80, 0x80, 0x80, 0x00, 0x00])
+        DeviceGraph.from_raw(2, [0, 11, 12], [1, 1], [0x81] + [0x80] * 9 + [0x00, 0x00])
+    # 6-byte varint whose payload beyond 32 bits is non-zero: id >= N
+    with pytest.raises(RuntimeError):
+        DeviceGraph.from_raw(2, [0, 6, 7], [1, 1], [0x81, 0x80, 0x80, 0x80, 0x80, 0x01, 0x00])
     hb = HyperBall(g, 10, 1)
     hb.run()
     with pytest.raises(ValueError):
@@ -360,11 +363,118 @@ def test_gpu_cpp_facade_tool(oracle_best):
     assert float(line.split("=")[1]) == pytest.approx(float(np.mean(md)), rel=1e-6)  # printed with %.6f
 
 
-def test_gpu_lockstep_c2_full_scale(oracle_best):
+def test_gpu_lockstep_c2_full_scale(c2, oracle_best):
     """BASELINE config C2 (212^2 grid, 60 obstacles, radius 44: 42,656 cells, 159 M edges,
     9 iterations) bit-exact after every iteration against the compiled reference
-    primitives; C3 (236,196 cells, 4.79e9 edges) was checked the same way with
-    scripts/parity_at_scale.py (profiles/r01b_parity_c3_full.json)."""
-    g = CompressedCsr.synth_grid(212, 212, 60, 3, 10, 20261017, 44 * 44)
+    primitives; C3 is checked against committed reference hashes below."""
+    lockstep(c2, 10, None, oracle_best)
+
+
+# ---------------------------------------------------------------- non-canonical LEB128 (leb128.hpp:28-39)
+def noncanonical(csr, rng, frac):
+    """Re-encodes csr with a fraction `frac` of its varints padded by zero-payload
+    continuation bytes to 6..10 bytes: the same ids, streams the reference decoder
+    accepts (it only rejects truncation and > 10 bytes)."""
+    from paper_2604_08374_b200.cgraph import leb128_encode
+    rows, offs = [], [0]
+    for v in range(csr.n):
+        out = bytearray()
+        prev = None
+        for w in csr.neighbors(v):
+            b = bytearray(leb128_encode(int(w) if prev is None else int(w) - prev))
+            prev = int(w)
+            if rng.random() < frac:
+                extra = int(rng.integers(6, 11)) - len(b)
+                b[-1] |= 0x80
+                b += b"\x80" * (extra - 1) + b"\x00"
+            out += b
+        rows.append(bytes(out))
+        offs.append(offs[-1] + len(out))
+    return CompressedCsr.from_arrays(np.array(offs, np.uint64), csr.degrees.copy(), b"".join(rows))
+
+
+@pytest.mark.parametrize("frac", [0.02, 1.0])
+def test_gpu_noncanonical_varints_match_reference(c1, oracle_best, frac):
+    """6..10-byte varints decode like the reference (acceptance AND values): registers,
+    c and sum_d after every iteration equal the oracle's on the re-encoded stream,
+    and the final state equals the canonical stream's.  C1 rows (degree up to ~3,000)
+    are cut into 512-id work items, so long varints also sit at item cuts."""
+    g = noncanonical(c1, np.random.default_rng(7), frac)
+    assert g.stream_len > c1.stream_len
+    assert lockstep(g, 10, None, oracle_best) >= 3
+    a, b = HyperBall(g, 10, None), HyperBall(c1, 10, None)
+    a.run(), b.run()
+    assert np.array_equal(a.registers(), b.registers()) and np.array_equal(a.state().sum_d, b.state().sum_d)
+    h = HyperBall(DeviceGraph(g, async_upload=True), 10, None)  # pipelined first pass
+    h.run()
+    assert np.array_equal(h.registers(), b.registers())
+    hi = HyperBall(g, 10, None, interval=True)  # run index from the same stream
+    hi.run()
+    assert np.array_equal(hi.registers(), b.registers())
+
+
+def test_gpu_six_byte_varint_accepted_like_reference(oracle_best):
+    """`81 80 80 80 80 00` is the 6-byte encoding of 1: the reference converges on
+    [[1], [0]] so written; so must the device."""
+    raw = CompressedCsr.from_arrays(np.array([0, 6, 7], np.uint64), np.array([1, 1], np.uint32),
+                                    bytes([0x81, 0x80, 0x80, 0x80, 0x80, 0x00, 0x00]))
+    ref = oracle_best.hb_run(raw, 10)
+    hb = HyperBall(raw, 10, None)
+    hb.run()
+    st = hb.state()
+    assert st.t == ref["iterations"] and np.array_equal(hb.registers(), ref["registers"])
+    assert np.array_equal(st.sum_d, ref["sum_d"])
+
+
+# ---------------------------------------------------------------- BASELINE configs at full size
+SCALE = os.path.join(os.path.dirname(__file__), "golden", "scale_reference.json")
+
+
+def _sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+@pytest.fixture(scope="module")
+def c3():
+    from bench import build_graph
+    return build_graph("c3", threads=os.cpu_count() or 1)
+
+
+@pytest.mark.parametrize("mode", ["dense", "skip", "interval"])
+def test_gpu_c3_matches_reference_hashes(c3, mode):
+    """BASELINE headline config C3 (open 486^2 grid, radius 87: 236,196 cells, 4.79e9
+    edges, p=10, full depth): after EVERY iteration the register plane (reference
+    packed layout), c_t and the max increase hash-equal the reference CPU path's
+    (oracle/_ref, tests/golden/make_scale_golden.py c3); final sum_d / sum_d2 too."""
+    gold = json.load(open(SCALE))["c3_p10"]
+    gh = gold["graph"]
+    assert (c3.n, c3.edges, c3.stream_len) == (gh["nodes"], gh["edges"], gh["stream_bytes"])
+    assert _sha(c3.offsets) == gh["offsets_sha256"] and _sha(c3.degrees) == gh["degrees_sha256"]
+    assert _sha(c3.stream) == gh["stream_sha256"]
+    hb = HyperBall(c3, HllParams(10), None, skip_unchanged=mode == "skip", interval=mode == "interval")
+    t = 0
+    while not hb.finished:
+        mx = hb.iterate_once()
+        want = gold["per_iteration"][t]
+        t += 1
+        assert _sha(hb.registers()) == want["registers_sha256"], f"registers at t={t}"
+        assert _sha(hb.state().c_curr) == want["c_sha256"], f"c_t at t={t}"
+        assert mx == f64(want["max_increase"]), f"max increase at t={t}"
+    st = hb.state()
+    assert st.t == gold["iterations"] and st.converged == gold["converged"]
+    assert _sha(st.sum_d) == gold["sum_d_sha256"] and _sha(st.sum_d2) == gold["sum_d2_sha256"]
+
+
+@pytest.fixture(scope="module")
+def c2():
+    from bench import build_graph
+    g = build_graph("c2", threads=os.cpu_count() or 1)
     assert g.n == 42656
-    lockstep(g, 10, None, oracle_best)
+    return g
+
+
+@pytest.mark.parametrize("p,depth", [(4, None), (6, None), (8, None), (12, None), (14, 2)])
+def test_gpu_c4_precision_sweep_lockstep(c2, oracle_best, p, depth):
+    """BASELINE C4: the p sweep on the C2 graph, bit-exact after every iteration
+    against the reference CPU path (p=10 is test_gpu_lockstep_c2_full_scale)."""
+    lockstep(c2, p, depth, oracle_best)

@@ -217,6 +217,21 @@ def test_spec_metrics_kats():
     assert math.isnan(m["md"][5])
 
 
+def test_metrics_md_below_one():
+    """An HLL under-estimate can give MD < 1 (RA < 0): integration_pv stays in
+    [0, 1] and integration_hh is NaN (pre MD > 1),
+    in the port, the scalar Python forms and the C++ facade's closed forms alike."""
+    from paper_2604_08374_b200 import metrics as M
+    P = oracle.port()
+    nv = np.array([10, 10, 10], np.uint32)
+    sd = np.array([8.1, 9.0, 9.9])                              # MD = 0.9, 1.0, 1.1
+    m = P.metrics(sd, np.zeros(3), nv, np.ones(3, np.uint32))
+    assert m["pv"][0] == 1.0 and m["pv"][1] == 1.0 and 0.0 < m["pv"][2] < 1.0
+    assert math.isnan(m["ihh"][0]) and math.isnan(m["ihh"][1]) and m["ihh"][2] > 0
+    assert M.integration_pv(0.9, 10) == 1.0 and math.isnan(M.integration_hh(0.9, 10))
+    assert M.integration_hh(1.1, 10) == pytest.approx(m["ihh"][2])
+
+
 @pytest.mark.skipif(not oracle.reference_available(), reason="reference build absent")
 def test_port_equals_reference_random():
     P, R = oracle.port(), oracle.reference()
