@@ -21,6 +21,7 @@ config and prints its own line.
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
 import statistics
@@ -459,12 +460,15 @@ def main():
 
     # passes executed (Alg. 1 stops one pass after the last change) vs last changing pass
     last_changing = max_over_ranks(float(max([s["t"] for s in st if s["changed_nodes"] > 0], default=0)))
+    from paper_2604_08374_b200.distributed import gather_to_root
+    sd_all = gather_to_root(hb.state().sum_d, bounds, rank, world)  # identical for every N
+    sum_d_sha = hashlib.sha256(sd_all.tobytes()).hexdigest() if rank == 0 else None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * dev_s / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
         "config": workload_config(args, g),
-        "run": {"iterations": iters, "last_changing_pass": int(last_changing),
+        "run": {"iterations": iters, "last_changing_pass": int(last_changing), "sum_d_sha256": sum_d_sha,
                 "register_layout": "4-bit bit-sliced (reference density m/2 B per row)",
                 "parallelism": f"node-range shards x{world}"},
         "hbm_gbs_algorithmic": bytes_iter * iters * args.steps / dev_s / 1e9,

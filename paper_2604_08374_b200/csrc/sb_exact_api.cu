@@ -148,14 +148,7 @@ int sb_exact_run(sb_exact* x, uint64_t src_begin, uint64_t src_end, uint32_t* ma
       e.hist_cap = x->hist_cap;
       CK(cudaMemsetAsync(x->d_misc, 0, 16, x->stream));
       sb::UnionArgs u{};
-      u.stream = g->d_stream;
-      u.item_off = g->d_item_off;
-      u.item_base = g->d_item_base;
-      u.item_count = g->d_item_count;
-      u.item_node = g->d_item_node;
-      u.node_item = g->d_node_item;
-      u.n_items = g->n_items;
-      u.node_begin = 0;
+      graph_union_args(g, u);
       u.cur = x->d_plane[L];
       u.next = x->d_plane[1 - L];
       u.scratch = x->d_scratch;
@@ -163,10 +156,6 @@ int sb_exact_run(sb_exact* x, uint64_t src_begin, uint64_t src_end, uint32_t* ma
       u.changed_out = x->d_changed;
       u.changed_in = x->d_changed;
       u.work = x->d_misc;
-      u.n_local = n;
-      u.n_tiles = g->n_tiles;
-      u.tile_node0 = g->d_tile_node0;
-      u.tile_q = g->d_tile_q;
       CK(cudaEventRecord(x->ev[0], x->stream));
       if (x->flags & SB_HB_INTERVAL) {
         if (x->levels) CK(sb::launch_st_build(x->P, x->d_plane[L], x->d_st, n, x->levels, x->stream, true));

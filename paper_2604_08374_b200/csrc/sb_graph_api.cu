@@ -126,6 +126,8 @@ static int graph_setup_host(sb_graph* g, const uint32_t* deg_local) {
   CK(dalloc(&g->d_item_base, ni * 4));
   CK(dalloc(&g->d_item_count, ni * 4));
   CK(dalloc(&g->d_item_node, ni * 4));
+  CK(dalloc(&g->d_node_lo, std::max<uint64_t>(g->n_local, 1) * 4));
+  CK(dalloc(&g->d_node_hi, std::max<uint64_t>(g->n_local, 1) * 4));
   CK(dalloc(&g->d_err, 16));
   CK(cudaMemset(g->d_err, 0xff, 8));
   CK(cudaMemset(reinterpret_cast<uint8_t*>(g->d_err) + 8, 0, 8));
@@ -151,8 +153,34 @@ static cudaError_t launch_validate(sb_graph* g, uint64_t n0, uint64_t n1, cudaSt
   a.item_base = g->d_item_base;
   a.item_count = g->d_item_count;
   a.item_node = g->d_item_node;
+  a.node_lo = g->d_node_lo;
+  a.node_hi = g->d_node_hi;
   a.err_node = g->d_err;
   return sb::launch_build_items(a, s);
+}
+
+void graph_union_args(const sb_graph* g, sb::UnionArgs& u) {
+  u.stream = g->d_stream;
+  u.item_off = g->d_item_off;
+  u.item_base = g->d_item_base;
+  u.item_count = g->d_item_count;
+  u.item_node = g->d_item_node;
+  u.node_item = g->d_node_item;
+  u.n_items = g->n_items;
+  u.node_begin = g->v0;
+  u.n_local = g->n_local;
+  u.n_tiles = g->n_tiles;
+  u.tile_node0 = g->d_tile_node0;
+  u.tile_q = g->d_tile_q;
+  u.row_off = g->d_rowoff;
+  u.degrees = g->d_deg;
+  u.node_lo = g->d_node_lo;
+  u.node_hi = g->d_node_hi;
+  // A group tile is one CTA's work: beyond ~1/(2 x SMs) of the slice's edges
+  // it would unbalance the launch, so such groups take the per-node items.
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
+  u.shared_max_edges = std::max<uint64_t>(1ull << 15, g->edges_local / (2ull * sms));
 }
 
 static int graph_check(sb_graph* g) {

@@ -214,6 +214,8 @@ struct sb_graph {
   uint32_t* d_item_base = nullptr;
   uint32_t* d_item_count = nullptr;
   uint32_t* d_item_node = nullptr;
+  uint32_t* d_node_lo = nullptr;      // first / last neighbour id per local node (validation pass)
+  uint32_t* d_node_hi = nullptr;
   uint32_t max_run = 0;               // longest run of consecutive neighbour ids
   uint64_t n_runs = 0;                // interval-mode run index (built on first use)
   uint64_t* d_run_off = nullptr;
@@ -243,6 +245,7 @@ struct sb_graph {
     if (val_stream) cudaStreamSynchronize(val_stream);
     dfree(d_stream); dfree(d_rowoff); dfree(d_deg); dfree(d_orig); dfree(d_node_item);
     dfree(d_item_off); dfree(d_item_base); dfree(d_item_count); dfree(d_item_node);
+    dfree(d_node_lo); dfree(d_node_hi);
     dfree(d_tile_node0); dfree(d_tile_q);
     dfree(d_run_off); dfree(d_run_s); dfree(d_run_e);
     dfree(d_cell); dfree(d_comp); dfree(d_comp_sizes);
@@ -366,5 +369,8 @@ struct sb_exact {
 
 // Internal graph helpers (sb_graph_api.cu).
 int graph_setup(sb_graph* g, const uint32_t* deg_local);
+// Union arguments shared by HyperBall and exact mode: CSR slice, work items,
+// CTA tiles and the group path of union_kernel.
+void graph_union_args(const sb_graph* g, sb::UnionArgs& u);
 int graph_wait(sb_graph* g);
 int build_run_index(sb_graph* g);

@@ -153,14 +153,7 @@ int sb_hb_step_compute(sb_hb* h, double* local_max) {
   if (g->n_local) {
     CK(cudaMemsetAsync(h->d_changed[N] + g->v0, 0, g->n_local, h->stream));
     sb::UnionArgs u{};
-    u.stream = g->d_stream;
-    u.item_off = g->d_item_off;
-    u.item_base = g->d_item_base;
-    u.item_count = g->d_item_count;
-    u.item_node = g->d_item_node;
-    u.node_item = g->d_node_item;
-    u.n_items = g->n_items;
-    u.node_begin = g->v0;
+    graph_union_args(g, u);
     u.cur = h->d_plane[L];
     u.next = h->d_plane[N];
     u.scratch = h->d_scratch;
@@ -168,10 +161,7 @@ int sb_hb_step_compute(sb_hb* h, double* local_max) {
     u.changed_out = h->d_changed[N];
     u.changed_in = h->d_changed[L];
     u.work = h->d_misc;
-    u.n_local = g->n_local;
-    u.n_tiles = (h->flags & SB_HB_SCHEDULE_WARP) ? 0 : g->n_tiles;
-    u.tile_node0 = g->d_tile_node0;
-    u.tile_q = g->d_tile_q;
+    if (h->flags & SB_HB_SCHEDULE_WARP) u.n_tiles = 0;
     u.npeers = h->npeers;
     u.peer_next = h->d_peer_plane[N];
     u.peer_changed = h->d_peer_chg[N];

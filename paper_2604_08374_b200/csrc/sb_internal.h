@@ -18,6 +18,8 @@ struct BuildArgs {
   uint32_t* item_base;
   uint32_t* item_count;
   uint32_t* item_node;
+  uint32_t* node_lo;           // first / last neighbour id per local node (empty row: ~0 / 0)
+  uint32_t* node_hi;
   unsigned long long* err_node;  // min local node with a malformed row (~0 = none)
 };
 
@@ -47,6 +49,14 @@ struct UnionArgs {
   uint64_t n_local;
   const uint32_t* tile_node0;  // first local node of the 8-node group
   const uint32_t* tile_q;      // chunk index within each node of the group
+  // Tile-shared gathers (union_kernel's group path): whole rows of the group's
+  // 8 nodes, decoded from their row offsets; the group takes the path when its
+  // id span is dense in edges and it holds <= shared_max_edges (else per-node items).
+  const uint64_t* row_off;     // local byte offsets (n_local + 1)
+  const uint32_t* degrees;     // local degrees
+  const uint32_t* node_lo;     // first / last neighbour id per local node (NULL: path off)
+  const uint32_t* node_hi;
+  uint64_t shared_max_edges;
   // Fused shard exchange: every finished row (and its changed flag) is also
   // stored straight into each peer GPU's replica (CUDA IPC / NVLink P2P).
   uint8_t* const* peer_next;     // [npeers] peers' `next` planes

@@ -60,7 +60,8 @@ __device__ __forceinline__ uint32_t zero_payload(uint32_t x) {
 // first or prev + delta, id < N, delta != 0 after the first, no trailing bytes.
 // Deltas >= 2^32 are rejected (the u64 sum could wrap below prev: a
 // non-increasing row).
-__device__ bool long_row_ok(const uint8_t* stream, uint64_t pos, uint64_t end, uint32_t deg, uint64_t n) {
+__device__ bool long_row_ok(const uint8_t* stream, uint64_t pos, uint64_t end, uint32_t deg, uint64_t n,
+                            uint32_t* lo) {
   uint64_t prev = 0;
   for (uint32_t k = 0; k < deg; ++k) {
     uint64_t x = 0;
@@ -76,6 +77,7 @@ __device__ bool long_row_ok(const uint8_t* stream, uint64_t pos, uint64_t end, u
     if (!term || x >= (1ull << 32)) return false;
     const uint64_t id = k ? prev + x : x;
     if (id >= n || (k && x == 0)) return false;
+    if (!k) *lo = static_cast<uint32_t>(id);
     prev = id;
   }
   return pos == end;
@@ -98,7 +100,11 @@ __global__ void __launch_bounds__(256, 3) build_items_kernel(BuildArgs a) {
       a.item_node[i0] = static_cast<uint32_t>(node);
     }
     if (deg == 0 || end <= pos0) {
-      if (lane == 0 && (deg != 0 || end != pos0)) atomicMin(a.err_node, static_cast<unsigned long long>(node));
+      if (lane == 0) {
+        if (deg != 0 || end != pos0) atomicMin(a.err_node, static_cast<unsigned long long>(node));
+        a.node_lo[node] = 0xffffffffu;
+        a.node_hi[node] = 0u;
+      }
       continue;
     }
     uint32_t cnt = 0, zeros = 0, lng = 0;  // per lane (lng: a byte at varint depth >= 5)
@@ -233,16 +239,19 @@ __global__ void __launch_bounds__(256, 3) build_items_kernel(BuildArgs a) {
     }
     if (lane == 0) {
       // the first varint (the absolute first id) may be 0
-      bool first_zero = true;
-      for (uint64_t b = pos0; b < end && b < pos0 + 5; ++b) {  // a longer first varint is flagged anyway
+      uint32_t first = 0;
+      for (uint64_t b = pos0, sh = 0; b < end && b < pos0 + 5; ++b, sh += 7) {  // longer: the scalar check
         const uint8_t c = a.stream[b];
-        if (c & 0x7fu) first_zero = false;
+        first |= static_cast<uint32_t>(c & 0x7fu) << sh;
         if (!(c & 0x80u)) break;
       }
+      const bool first_zero = first == 0;
       const bool ends_on_terminator = !(a.stream[end - 1] & 0x80u);
-      const bool ok = lng ? long_row_ok(a.stream, pos0, end, deg, a.n_global)
+      const bool ok = lng ? long_row_ok(a.stream, pos0, end, deg, a.n_global, &first)
                           : cnt == deg && ends_on_terminator && zeros == (first_zero ? 1u : 0u) && sum < a.n_global;
       if (!ok) atomicMin(a.err_node, static_cast<unsigned long long>(node));
+      a.node_lo[node] = first;
+      a.node_hi[node] = static_cast<uint32_t>(sum);
     }
   }
 }
@@ -566,6 +575,285 @@ __device__ __forceinline__ void process_item(const UnionArgs& a, uint64_t item, 
   if (finish) publish_row<P>(a, curb, nextb, goff, v, acc, lane);
 }
 
+// ------------------------------------------------------------------ tile-shared gathers
+// A CTA takes a group of 8 consecutive nodes (whole rows, one 512-B row slice)
+// and sweeps the union of their neighbour lists in id windows of SH_W ids:
+//   A  warp w decodes node w's LEB128 row (decode_step4) and sets the node's
+//      membership bitmap for the window (bit per id; one shared atomicOr per
+//      run of ids sharing a word: __match_any + __reduce_or);
+//   B1 the 8 bitmaps are ANDed / ORed word by word: F = ids in EVERY active
+//      node's list, P = ids in some but not all.  Warp w gathers the rows of
+//      the F ids of its 16-word block ONCE and folds them into a group
+//      accumulator (bit-serial 9-way max over 8-row batches);
+//   B2 warp w folds the P ids of its own node (P & own bitmap) into the node's
+//      accumulator.
+// At the end next[v] = max(cur[v], own partials, group accumulator) -- max is
+// associative, commutative and idempotent, so the grouping is exact
+// (PAPER.md:358-360 unchanged).  On a visibility graph 8 consecutive raster
+// nodes see nearly the same cells: every row is fetched once per group
+// instead of once per edge, and the F rows (~90 %) are max-reduced once
+// instead of 8 times.
+constexpr int SH_W = 4096;             // ids per window
+constexpr int SH_WW = SH_W / 32;       // bitmap words per node
+constexpr int SH_WPW = SH_WW / 8;      // words per warp in B1
+constexpr int SH_BUF = 128;            // ids of one 128-byte decode window
+constexpr unsigned SH_MIN_EDGES_PER_WINDOW = 128;
+
+struct SharedSmem {
+  uint32_t bm[8][SH_WW];
+  uint32_t buf[8][SH_BUF];
+  uint32_t sF[SH_WW], sP[SH_WW];
+  uint16_t plist[SH_WW];
+  uint32_t pcount[2];
+  uint32_t next[2][8];
+  uint4 red[8][32];  // per-warp group accumulators (<= 32 lanes x 16 B)
+};
+
+// Per-warp cursor over one node's row (warp-uniform state).
+template <bool SKIP>
+struct RowCursor {
+  uint64_t pos;
+  uint32_t rem, base;
+  int n, i;
+  // Next undecoded-and-unconsumed id (0xffffffff: row exhausted); refills the
+  // buffer from the stream when it is empty.
+  __device__ __forceinline__ uint32_t peek(const UnionArgs& a, uint32_t* buf, int lane) {
+    while (i >= n) {
+      if (rem == 0) return 0xffffffffu;
+      __syncwarp();  // every lane is done with the previous window's ids
+      const Decode4 d = decode_step4<SKIP, 0>(a.stream, pos, rem, base, a.changed_in, buf, lane);
+      if (d.advance == 0) {  // unreachable on a validated stream
+        rem = 0;
+        return 0xffffffffu;
+      }
+      pos += d.advance;
+      rem -= d.wanted;
+      base = d.last;
+      n = d.count;
+      i = 0;
+      __syncwarp();
+    }
+    return buf[i];
+  }
+};
+
+// acc <- max(acc, rows of the candidate bits) over `nw` bitmap words: id of
+// bit b of word j = id0 + 32 j + b.  Batches of U * SUB candidates; a lane
+// group loads its candidates' row slices (0 for a clear bit: the identity of
+// the max) and folds them with the bit-serial (U+1)-way max.
+template <int P, class C>
+__device__ __forceinline__ void fold_bits(Grp& acc, const uint32_t* words, int nw, uint32_t id0,
+                                          const uint8_t* curb, int sub) {
+  using G = Geo<P>;
+  using IO = GrpIO<G::GB>;
+  constexpr int U = C::U;
+  constexpr int BATCH = U * G::SUB;
+  if constexpr (BATCH <= 32) {
+    for (int j = 0; j < nw; ++j) {
+      const uint32_t w = words[j];
+      if (!w) continue;
+      const uint8_t* rb = curb + static_cast<uint64_t>(id0 + 32u * j) * G::ROW;
+#pragma unroll 1
+      for (int c0 = 0; c0 < 32; c0 += BATCH) {
+        const uint32_t bits = BATCH == 32 ? w : (w >> c0) & ((1u << (BATCH & 31)) - 1u);
+        if (!bits) continue;
+        Grp x[U];
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+          const int b = q * G::SUB + sub;
+          x[q] = ((bits >> b) & 1u) ? IO::ld(rb + static_cast<uint64_t>(c0 + b) * G::ROW) : grp_zero();
+        }
+        batch_max<C, U>(acc, x);
+      }
+    }
+  } else {
+    constexpr int K = BATCH / 32;  // words per batch (p <= 7)
+    for (int j = 0; j < nw; j += K) {
+      uint32_t any = 0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) any |= words[j + k];
+      if (!any) continue;
+      Grp x[U];
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        const int c = q * G::SUB + sub;
+        const uint32_t w = words[j + (c >> 5)];
+        x[q] = ((w >> (c & 31)) & 1u) ? IO::ld(curb + static_cast<uint64_t>(id0 + 32u * j + c) * G::ROW)
+                                      : grp_zero();
+      }
+      batch_max<C, U>(acc, x);
+    }
+  }
+}
+
+// One word of candidates (the partial rows of one node).
+template <int P, class C>
+__device__ __forceinline__ void fold_word(Grp& acc, uint32_t w, uint32_t id0, const uint8_t* curb, int sub) {
+  using G = Geo<P>;
+  using IO = GrpIO<G::GB>;
+  constexpr int QW = 32 / G::SUB;  // candidate slots per lane in one word
+  constexpr int U = C::U < QW ? C::U : QW;
+  constexpr int BATCH = U * G::SUB;
+  const uint8_t* rb = curb + static_cast<uint64_t>(id0) * G::ROW;
+#pragma unroll 1
+  for (int c0 = 0; c0 < 32; c0 += BATCH) {
+    const uint32_t bits = BATCH == 32 ? w : (w >> c0) & ((1u << (BATCH & 31)) - 1u);
+    if (!bits) continue;
+    Grp x[U];
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      const int b = q * G::SUB + sub;
+      x[q] = ((bits >> b) & 1u) ? IO::ld(rb + static_cast<uint64_t>(c0 + b) * G::ROW) : grp_zero();
+    }
+    batch_max<C, U>(acc, x);
+  }
+}
+
+// Group decision (warp 0): take the shared path iff >= 2 nodes have
+// neighbours, the group averages >= SH_MIN_EDGES_PER_WINDOW edges per window
+// of its id span (sparse, scattered rows would pay the window sweep for
+// nothing) and the group is small enough not to unbalance the launch.
+// Returns the mask of nodes with neighbours | 0x100 for the shared path, else 0.
+__device__ __forceinline__ uint32_t group_mode(const UnionArgs& a, uint32_t g0, int lane) {
+  const uint32_t node = g0 + lane;
+  const bool ex = lane < 8 && node < a.n_local;
+  const uint32_t deg = ex ? a.degrees[node] : 0u;
+  uint32_t lo = deg ? a.node_lo[node] : 0xffffffffu;
+  uint32_t hi = deg ? a.node_hi[node] : 0u;
+  unsigned long long sum = deg;
+#pragma unroll
+  for (int o = 4; o >= 1; o >>= 1) {  // lanes 0..7
+    sum += __shfl_xor_sync(FULL, sum, o);
+    lo = min(lo, __shfl_xor_sync(FULL, lo, o));
+    hi = max(hi, __shfl_xor_sync(FULL, hi, o));
+  }
+  const uint32_t act = __ballot_sync(FULL, deg != 0) & 0xffu;
+  if (__popc(act) < 2 || sum > a.shared_max_edges) return 0u;
+  const unsigned long long windows = (hi - lo) / SH_W + 1ull;
+  return sum >= SH_MIN_EDGES_PER_WINDOW * windows ? (act | 0x100u) : 0u;
+}
+
+template <int P, bool SKIP, class C0>
+__device__ __forceinline__ void process_group_shared(const UnionArgs& a, uint32_t g0, int slice, int lane, int warp,
+                                                     uint32_t act, SharedSmem& S) {
+  using G = Geo<P>;
+  using IO = GrpIO<G::GB>;
+  // 8 candidate rows per lane per batch at every p (the per-node feeder is tied
+  // to U * SUB <= one 128-id decode window; the bitmap sweep is not)
+  using C = UCfg<8, false, C0::MINB, false, C0::KWAY, C0::OR>;
+  const int sub = lane / G::LPR;
+  const int gl = lane % G::LPR;
+  const uint32_t node = g0 + warp;
+  const bool exists = node < a.n_local;
+  const bool mine = (act >> warp) & 1u;
+  const uint64_t v = a.node_begin + node;
+  const uint64_t goff = static_cast<uint64_t>(slice) * G::SLICE_BYTES + static_cast<uint64_t>(gl) * G::GB;
+  const uint8_t* curb = opaque(a.cur + goff);
+  Grp acc = exists ? IO::ld(curb + v * G::ROW) : grp_zero();  // next[v] <- cur[v]
+  Grp all = grp_zero();
+  RowCursor<SKIP> c;
+  c.pos = mine ? a.row_off[node] : 0;
+  c.rem = mine ? a.degrees[node] : 0u;
+  c.base = 0;
+  c.n = c.i = 0;
+  uint32_t* buf = S.buf[warp];
+  uint32_t* bm = S.bm[warp];
+  uint32_t nx = c.peek(a, buf, lane);
+  if (lane == 0) S.next[0][warp] = nx;
+  if (threadIdx.x == 0) S.pcount[0] = 0;
+  __syncthreads();
+  for (int r = 0;; ++r) {
+    uint32_t B = 0xffffffffu;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) B = min(B, S.next[r & 1][k]);
+    if (B == 0xffffffffu) break;  // every row exhausted (CTA-uniform)
+    B &= ~31u;
+    // A: this node's ids in [B, B + SH_W) -> own bitmap
+#pragma unroll
+    for (int k = lane; k < SH_WW; k += 32) bm[k] = 0u;
+    __syncwarp();
+    for (;;) {
+      const uint32_t x = c.peek(a, buf, lane);
+      if (x == 0xffffffffu || x - B >= static_cast<uint32_t>(SH_W)) break;
+      const int e = c.i + lane;
+      const uint32_t off = (e < c.n ? buf[e] : 0xffffffffu) - B;
+      const bool in = e < c.n && off < static_cast<uint32_t>(SH_W);
+      const unsigned inm = __ballot_sync(FULL, in);
+      if (in) {
+        const unsigned peers = __match_any_sync(inm, off >> 5);
+        const unsigned bits = __reduce_or_sync(peers, 1u << (off & 31));
+        if (lane == __ffs(peers) - 1) atomicOr(bm + (off >> 5), bits);
+      }
+      c.i += __popc(inm);
+    }
+    nx = c.peek(a, buf, lane);
+    if (lane == 0) S.next[(r + 1) & 1][warp] = nx;
+    __syncthreads();
+    // B1: F / P of this warp's word block; F rows -> group accumulator
+    if (threadIdx.x == 0) S.pcount[(r + 1) & 1] = 0;  // every warp is past round r-1's B2
+    uint32_t Pw = 0;
+    if (lane < SH_WPW) {
+      const int j = warp * SH_WPW + lane;
+      uint32_t Uw = 0, F = 0xffffffffu;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t w = S.bm[k][j];
+        Uw |= w;
+        if ((act >> k) & 1u) F &= w;
+      }
+      Pw = Uw & ~F;
+      S.sF[j] = F;
+      S.sP[j] = Pw;
+    }
+    const unsigned pm = __ballot_sync(FULL, Pw != 0u);
+    if (pm) {
+      uint32_t at = 0;
+      if (lane == 0) at = atomicAdd(&S.pcount[r & 1], static_cast<uint32_t>(__popc(pm)));
+      at = __shfl_sync(FULL, at, 0);
+      if (Pw) S.plist[at + __popc(pm & ((1u << lane) - 1u))] = static_cast<uint16_t>(warp * SH_WPW + lane);
+    }
+    __syncwarp();
+    fold_bits<P, C>(all, S.sF + warp * SH_WPW, SH_WPW, B + 32u * warp * SH_WPW, curb, sub);
+    __syncthreads();
+    // B2: this node's partial rows
+    if (mine) {
+      const int np = static_cast<int>(S.pcount[r & 1]);
+      for (int k = 0; k < np; ++k) {
+        const int j = S.plist[k];
+        const uint32_t w = S.sP[j] & bm[j];
+        if (w) fold_word<P, C>(acc, w, B + 32u * j, curb, sub);
+      }
+    }
+  }
+  if (G::SUB > 1) {
+#pragma unroll
+    for (int m = G::LPR; m < 32; m <<= 1) {
+      combine<C::OR>(acc, grp_shfl_xor(acc, m));
+      combine<C::OR>(all, grp_shfl_xor(all, m));
+    }
+  }
+  // every warp's F rows (its word blocks), whatever its own node: all eight fold in
+  if (lane < G::LPR) IO::st(reinterpret_cast<uint8_t*>(&S.red[warp][0]) + gl * G::GB, all);
+  __syncthreads();
+  if (exists) {
+    if (mine) {
+      Grp x[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint8_t* p = reinterpret_cast<const uint8_t*>(&S.red[k][0]) + gl * G::GB;
+        if constexpr (G::GB == 16) {
+          const uint4 q = *reinterpret_cast<const uint4*>(p);
+          x[k] = Grp{q.x, q.y, q.z, q.w};
+        } else {
+          x[k] = GrpIO<8>::unpack(*reinterpret_cast<const uint2*>(p));
+        }
+      }
+      batch_max<C, 8>(acc, x);
+    }
+    publish_row<P>(a, curb, a.next + goff + v * G::ROW, goff, v, acc, lane);
+  }
+}
+
 __device__ __forceinline__ bool upload_failed(const UnionArgs& a) {
   return a.err && *reinterpret_cast<const volatile unsigned long long*>(a.err) != ~0ull;
 }
@@ -580,11 +868,14 @@ __device__ __forceinline__ bool upload_failed(const UnionArgs& a) {
 template <int P, bool SKIP, bool TILE, class C = DefaultCfg<P>>
 __global__ void __launch_bounds__(256, C::MINB) union_kernel(UnionArgs a) {
   using G = Geo<P>;
-  __shared__ uint32_t ids_s[8][Feeder<P, SKIP, C::U>::BUF];
+  constexpr size_t kIds = sizeof(uint32_t) * 8 * Feeder<P, SKIP, C::U>::BUF;
+  constexpr size_t kSmem = kIds > sizeof(SharedSmem) ? kIds : sizeof(SharedSmem);
+  __shared__ __align__(16) unsigned char smem[kSmem];  // per-node feeders or the group path
   __shared__ unsigned long long s_unit[2];
+  __shared__ uint32_t s_mode;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  uint32_t* buf = ids_s[warp];
+  uint32_t* buf = reinterpret_cast<uint32_t*>(smem) + warp * Feeder<P, SKIP, C::U>::BUF;
   if (!TILE) {
     const uint64_t total = a.n_items * G::SLICES;
     for (;;) {
@@ -602,8 +893,23 @@ __global__ void __launch_bounds__(256, C::MINB) union_kernel(UnionArgs a) {
       const unsigned long long u = s_unit[k & 1];
       if (u >= total) break;
       const uint64_t t = u / G::SLICES;
-      const uint32_t node = a.tile_node0[t] + warp;
+      const uint32_t g0 = a.tile_node0[t];
       const uint32_t q = a.tile_q[t];
+      if (a.node_lo) {  // group path when the group's rows overlap densely
+        if (warp == 0) {
+          const uint32_t m = group_mode(a, g0, lane);
+          if (lane == 0) s_mode = m;
+        }
+        __syncthreads();
+        const uint32_t m = s_mode;
+        if (m) {
+          if (q == 0)
+            process_group_shared<P, SKIP, C>(a, g0, static_cast<int>(u % G::SLICES), lane, warp, m & 0xffu,
+                                             *reinterpret_cast<SharedSmem*>(smem));
+          continue;
+        }
+      }
+      const uint32_t node = g0 + warp;
       if (node < a.n_local) {
         const uint32_t first = a.node_item[node];
         if (q < a.node_item[node + 1] - first)
