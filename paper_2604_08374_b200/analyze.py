@@ -74,8 +74,11 @@ def analyze(csr: CompressedCsr, p: int = 10, depth_limit: int | None = None, mod
         timings["local_s"] = time.perf_counter() - t0
         cols.update(control=lm["control"], controllability=lm["controllability"], clustering=lm["clustering"])
     x, y = csr.coordinates()
+    # node_id is the ORIGINAL id: a Hilbert-reordered graph maps each row back
+    # through hilbert_inverse, otherwise the row index.
+    node_id = csr.hilbert_inverse if csr.hilbert_inverse is not None else np.arange(csr.n, dtype=np.uint32)
     cols.update(x=np.ascontiguousarray(x, np.float64), y=np.ascontiguousarray(y, np.float64),
-                component_id=np.ascontiguousarray(csr.component_id, np.uint32), node_count=nv, connectivity=deg)
+                node_id=np.ascontiguousarray(node_id, np.uint32), component_id=np.ascontiguousarray(csr.component_id, np.uint32), node_count=nv, connectivity=deg)
     if out is not None:
         t0 = time.perf_counter()
         write_csv(out, cols, csr.n)

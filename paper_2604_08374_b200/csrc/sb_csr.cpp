@@ -4,6 +4,7 @@
 // Hilbert renumbering and edge-balanced partitions.
 #include <cuda_runtime_api.h>
 #include <zlib.h>
+#include <sys/stat.h>
 
 #include <algorithm>
 #include <atomic>
@@ -652,9 +653,21 @@ int sb_vgacsr_save(const sb_csr* c, const char* path) {
   return SB_OK;
 }
 
+static int vgacsr_load(const char* path, sb_csr** out);
+
 int sb_vgacsr_load(const char* path, sb_csr** out) {
   if (!path || !out) return cfail(SB_EINVAL, "NULL argument");
   *out = nullptr;
+  try {  // no C++ exception crosses the C ABI
+    return vgacsr_load(path, out);
+  } catch (const std::bad_alloc&) {
+    return cfail(SB_ENOMEM, "vgacsr: out of host memory loading %s", path);
+  } catch (const std::exception& e) {
+    return cfail(SB_ERUNTIME, "vgacsr: %s", e.what());
+  }
+}
+
+static int vgacsr_load(const char* path, sb_csr** out) {
   FILE* f = fopen(path, "rb");
   if (!f) return cfail(SB_ERUNTIME, "vgacsr: cannot open %s", path);
   std::unique_ptr<FILE, int (*)(FILE*)> guard(f, fclose);
@@ -672,6 +685,16 @@ int sb_vgacsr_load(const char* path, sb_csr** out) {
     return cfail(SB_ERUNTIME, "vgacsr: truncated header");
   if (c->n == 0 || c->n > 0xffffffffull) return cfail(SB_ERUNTIME, "vgacsr: bad node count");
   const uint64_t n = c->n;
+  // The header's sizes must fit the file before anything is allocated from them
+  // (a truncated or corrupt header must not drive multi-GB allocations).
+  struct stat sbuf;
+  if (fstat(fileno(f), &sbuf) != 0) return cfail(SB_ERUNTIME, "vgacsr: cannot stat %s", path);
+  const uint64_t fsize = static_cast<uint64_t>(sbuf.st_size);
+  constexpr uint64_t kHeader = 8 + 4 + 8 + 8 + 8 + 24 + 8;
+  const uint64_t fixed = kHeader + n * 4 + (n + 1) * 8 + n * 4 + 4 + n * 4 + ((flags & 1u) ? n * 4 : 0) + 4;
+  if (slen > fsize || fixed > fsize || fixed + slen > fsize)
+    return cfail(SB_ERUNTIME, "vgacsr: truncated file (header sizes exceed its %llu bytes)", (unsigned long long)fsize);
+  const uint64_t comp_bytes = fsize - fixed - slen;  // what is left for sizes[C]
   c->cell_of_node.resize(n);
   c->offsets.resize(n + 1);
   c->degrees.resize(n);
@@ -683,6 +706,8 @@ int sb_vgacsr_load(const char* path, sb_csr** out) {
   if (!r.get(c->stream, slen)) return cfail(SB_ERUNTIME, "vgacsr: truncated stream");
   uint32_t C = 0;
   if (!r.get(&C, 4)) return cfail(SB_ERUNTIME, "vgacsr: truncated components");
+  if (static_cast<uint64_t>(C) * 4 != comp_bytes || C == 0 || C > n)
+    return cfail(SB_ERUNTIME, "vgacsr: component count %u does not match the file", C);
   c->comp_id.resize(n);
   c->comp_sizes.resize(C);
   if (!r.get(c->comp_id.data(), n * 4) || !r.get(c->comp_sizes.data(), static_cast<uint64_t>(C) * 4))
@@ -698,6 +723,13 @@ int sb_vgacsr_load(const char* path, sb_csr** out) {
   uint64_t e = 0;
   for (uint64_t v = 0; v < n; ++v) e += c->degrees[v];
   if (e != c->edges) return cfail(SB_ERUNTIME, "vgacsr: edge count mismatch");
+  std::vector<uint64_t> seen(C, 0);
+  for (uint64_t v = 0; v < n; ++v) {
+    if (c->comp_id[v] >= C) return cfail(SB_ERUNTIME, "vgacsr: component id out of range");
+    ++seen[c->comp_id[v]];
+  }
+  for (uint32_t k = 0; k < C; ++k)
+    if (seen[k] != c->comp_sizes[k]) return cfail(SB_ERUNTIME, "vgacsr: component sizes do not match the ids");
   *out = c.release();
   return SB_OK;
 }

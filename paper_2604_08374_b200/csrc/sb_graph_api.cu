@@ -176,11 +176,13 @@ void graph_union_args(const sb_graph* g, sb::UnionArgs& u) {
   u.degrees = g->d_deg;
   u.node_lo = g->d_node_lo;
   u.node_hi = g->d_node_hi;
-  // A group tile is one CTA's work: beyond ~1/(2 x SMs) of the slice's edges
-  // it would unbalance the launch, so such groups take the per-node items.
+  // A group tile is one CTA's work: above half a resident CTA's fair share of
+  // the slice's edges (SMs x 4 CTAs) it would stretch the launch's tail, so
+  // such groups -- and every group of a small graph, where the per-node items
+  // are what fills the machine -- take the per-node items.
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
-  u.shared_max_edges = std::max<uint64_t>(1ull << 15, g->edges_local / (2ull * sms));
+  u.shared_max_edges = g->edges_local / (2ull * 4ull * static_cast<uint64_t>(sms));
 }
 
 static int graph_check(sb_graph* g) {

@@ -48,6 +48,10 @@ int sb_hb_create(sb_graph* g, unsigned p, uint32_t depth_limit, uint32_t flags, 
   if (p < 4 || p > 16) return fail(SB_EINVAL, "hll: precision must be in [4, 16]");
   if ((flags & SB_HB_INTERVAL) && (flags & SB_HB_SKIP_UNCHANGED))
     return fail(SB_EINVAL, "interval mode excludes SB_HB_SKIP_UNCHANGED");
+  if ((flags & SB_HB_SCHEDULE_GROUP) && (flags & SB_HB_SCHEDULE_WARP))
+    return fail(SB_EINVAL, "SB_HB_SCHEDULE_GROUP excludes SB_HB_SCHEDULE_WARP");
+  if (flags & ~(SB_HB_SKIP_UNCHANGED | SB_HB_SCHEDULE_WARP | SB_HB_INTERVAL | SB_HB_SCHEDULE_GROUP))
+    return fail(SB_EINVAL, "sb_hb_create: unknown flags 0x%x", flags);
   DeviceGuard dg(g->device);
   auto* h = new sb_hb();
   h->g = g;
@@ -162,6 +166,7 @@ int sb_hb_step_compute(sb_hb* h, double* local_max) {
     u.changed_in = h->d_changed[L];
     u.work = h->d_misc;
     if (h->flags & SB_HB_SCHEDULE_WARP) u.n_tiles = 0;
+    if (h->flags & SB_HB_SCHEDULE_GROUP) u.shared_max_edges = ~0ull;
     u.npeers = h->npeers;
     u.peer_next = h->d_peer_plane[N];
     u.peer_changed = h->d_peer_chg[N];

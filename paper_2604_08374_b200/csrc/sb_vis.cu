@@ -59,14 +59,14 @@ __device__ __forceinline__ bool any_blocked(const VisArgs& a, int r0, int c0, in
 // walk the cells whose interior the open segment crosses, stepping in x when
 // (2k+1)*ay < (2j+1)*ax, in y when greater, diagonally on an exact corner
 // crossing -- the host generator's walk (sb_csr.cpp) with the two products
-// kept as running 32-bit sums (ax, ay < 2^15 for any grid side < 32768).
+// kept as running 64-bit sums (2*ax*ay reaches 2^33 on a 2^32-cell grid).
 __device__ bool visible(const VisArgs& a, int r1, int c1, int r2, int c2) {
   if (!any_blocked(a, r1, c1, r2, c2)) return true;
   const int dx = c2 - c1, dy = r2 - r1;
   const int sx = dx > 0 ? 1 : -1, sy = dy > 0 ? 1 : -1;
   const int ax = dx < 0 ? -dx : dx, ay = dy < 0 ? -dy : dy;
   int x = c1, y = r1, k = 0, j = 0;
-  int lhs = ay, rhs = ax;  // (2k+1)*ay and (2j+1)*ax
+  int64_t lhs = ay, rhs = ax;  // (2k+1)*ay and (2j+1)*ax
   const uint8_t* __restrict__ row = a.blocked + static_cast<uint64_t>(y) * a.cols;
   const int64_t rstep = sy * static_cast<int64_t>(a.cols);
   while (k < ax || j < ay) {
@@ -75,12 +75,12 @@ __device__ bool visible(const VisArgs& a, int r1, int c1, int r2, int c2) {
     if (mx) {
       x += sx;
       ++k;
-      lhs += 2 * ay;
+      lhs += 2 * static_cast<int64_t>(ay);
     }
     if (my) {
       y += sy;
       ++j;
-      rhs += 2 * ax;
+      rhs += 2 * static_cast<int64_t>(ax);
       row += rstep;
     }
     if (x == c2 && y == r2) break;

@@ -1,0 +1,46 @@
+#!/usr/bin/env bash
+# Round-2 evidence on one B200 (outputs under gpurun_out/; copy what is kept to profiles/r02/):
+#   gpurun --timeout 3000 -- bash scripts/gpu_r02.sh [tests|bench|ncu|ncu_sweep|dist|all]...
+# Each step has its own timeout; no number printed under ncu is a bench value.
+set -u
+export SB_SYNC_TIMEOUT_S=600 PYTHONUNBUFFERED=1
+mkdir -p gpurun_out
+run() { echo "== $*" >> gpurun_out/r02.log; "$@"; echo "rc=$? ($1 ${*: -1})" >> gpurun_out/r02.log; }
+(nproc; lscpu | grep 'Model name'; nvidia-smi -L) > gpurun_out/host.txt 2>&1
+NCU="ncu --set full --clock-control none --import-source on"
+for what in "${@:-all}"; do
+if [[ $what == tests || $what == all ]]; then
+  run timeout 2400 python -u -m pytest tests -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; tail -3 gpurun_out/pytest_gpu.log
+  run timeout 300 python -u -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
+fi
+if [[ $what == bench || $what == all ]]; then
+  run timeout 900 python -u bench.py > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.log
+  run timeout 600 python -u bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.log
+  run timeout 600 python -u bench.py --config c2 --no-cpu > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.log
+  run timeout 600 python -u bench.py --config c1 --no-cpu > gpurun_out/bench_c1.json 2> gpurun_out/bench_c1.log
+fi
+if [[ $what == ncu || $what == all ]]; then
+  run timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+      --log-file gpurun_out/launches_c3.csv python -u bench.py --profile --no-cpu --no-e2e --no-variants --no-pipeline
+  run timeout 900 $NCU -k regex:union_kernel -s 3 -c 1 -o gpurun_out/prof_c3_p10 \
+      python -u bench.py --profile --no-cpu --no-e2e --no-variants --no-pipeline
+fi
+if [[ $what == ncu_sweep || $what == all ]]; then
+  for cfg in "c1 10" "c2 10" "c2 4" "c2 6" "c2 14"; do
+    set -- $cfg
+    run timeout 600 $NCU -k regex:union_kernel -s 2 -c 1 -o gpurun_out/prof_$1_p$2 \
+        python -u bench.py --config $1 --p $2 --profile --no-cpu --no-e2e --no-variants --no-pipeline
+  done
+  run timeout 600 $NCU -k regex:union_interval -s 3 -c 1 -o gpurun_out/prof_c3_interval \
+      python -u scripts/pipeline_profile.py c3
+fi
+if [[ $what == dist || $what == all ]]; then
+  # the sharded bench path (2 ranks sharing the one GPU: fused P2P + gloo barrier) vs N=1
+  run timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 \
+      --master-port 29533 bench.py --gpus 2 --config c3 --steps 3 --warmup 3 --no-cpu --no-variants --no-pipeline \
+      > gpurun_out/bench_c3_w2_shared.json 2> gpurun_out/bench_c3_w2_shared.log
+fi
+if [[ $what == sweeps || $what == all ]]; then
+  run timeout 900 python -u scripts/sweep.py > gpurun_out/sweeps.json 2> gpurun_out/sweeps.log
+fi
+done

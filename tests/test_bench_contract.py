@@ -40,3 +40,19 @@ def test_reference_arm_json_line():
 def test_reference_arm_other_ranks_exit_quietly():
     r = run_bench("--impl", "reference", "--gpus", "2", env={"RANK": "1", "WORLD_SIZE": "2"})
     assert r.returncode == 0 and r.stdout.strip() == ""
+
+
+def test_roofline_is_a_fraction_of_the_binding_unit():
+    """The union kernel's roofline is reported on the unit that binds it (SM
+    instruction issue, from the committed ncu summary), so frac <= 1; the
+    SURVEY 8(d) HBM-algorithmic ratio (> 1) lives in its own key."""
+    sys.path.insert(0, ROOT)
+    import bench
+    e = bench.profile_entry("c3", 10)
+    assert e and e["warp_instructions_issued"] > 0
+    launch_s = e["duration_ms"] / 1e3
+    roof, alg = bench.roofline_of("c3", 10, launch_s, 2.457e12, 1965.0)
+    assert roof["bound"] == "issue" and 0 < roof["frac"] <= 1.0
+    assert roof["traffic"] == e["dram_bytes_per_launch"] and 0 < roof["dram_frac"] < 1.0
+    assert not roof["profile_stale"]
+    assert alg["ratio_to_hbm_peak"] > 1.0

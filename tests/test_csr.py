@@ -163,6 +163,30 @@ def test_vgacsr_roundtrip_and_errors(tmp_path):
     with pytest.raises(RuntimeError, match="truncated"):
         CompressedCsr.load_vgacsr(str(bad))
 
+    def with_crc(body: bytes) -> bytes:
+        return body + zlib.crc32(body).to_bytes(4, "little")
+
+    # a corrupt header claiming 2^32-1 nodes is rejected before any allocation
+    huge = bytearray(raw)
+    huge[12:20] = (0xFFFFFFFF).to_bytes(8, "little")
+    bad.write_bytes(bytes(huge))
+    with pytest.raises(RuntimeError, match="truncated"):
+        CompressedCsr.load_vgacsr(str(bad))
+    # component ids are checked against C and the sizes against the ids (CRC kept valid)
+    n = g.n
+    comp_at = len(raw) - 4 - 4 * g.component_sizes.size - 4 * n
+    body = bytearray(raw[:-4])
+    body[comp_at:comp_at + 4] = (g.component_sizes.size + 7).to_bytes(4, "little")
+    bad.write_bytes(with_crc(bytes(body)))
+    with pytest.raises(RuntimeError, match="component id"):
+        CompressedCsr.load_vgacsr(str(bad))
+    body = bytearray(raw[:-4])
+    sz_at = len(raw) - 4 - 4 * g.component_sizes.size
+    body[sz_at:sz_at + 4] = (int(g.component_sizes[0]) + 1).to_bytes(4, "little")
+    bad.write_bytes(with_crc(bytes(body)))
+    with pytest.raises(RuntimeError, match="component sizes"):
+        CompressedCsr.load_vgacsr(str(bad))
+
 
 def test_hilbert_reorder_is_a_relabelling(tmp_path):
     g = CompressedCsr.synth_grid(20, 24, 8, 1, 4, 9, 0)

@@ -29,9 +29,9 @@ def csr_of(adj):
     return CompressedCsr.from_adjacency(adj)
 
 
-def lockstep(csr, p, depth, O, skip=False, threads=0, interval=False):
+def lockstep(csr, p, depth, O, skip=False, threads=0, interval=False, schedule="auto"):
     """Run GPU and oracle side by side; assert bit-exact state after every iteration."""
-    hb = HyperBall(csr, HllParams(p), depth, skip_unchanged=skip, interval=interval)
+    hb = HyperBall(csr, HllParams(p), depth, skip_unchanged=skip, interval=interval, schedule=schedule)
     n = csr.n
     cur, c_prev = O.hb_init(n, p)
     assert np.array_equal(hb.registers(), cur), "init registers"
@@ -73,11 +73,12 @@ def c1():
 
 
 # ---------------------------------------------------------------- golden (reference-generated) fixtures
+@pytest.mark.parametrize("schedule", ["auto", "group", "items"])
 @pytest.mark.parametrize("case", range(len(GOLD["hyperball"])))
-def test_gpu_matches_reference_golden(case):
+def test_gpu_matches_reference_golden(case, schedule):
     c = GOLD["hyperball"][case]
     csr = csr_of(GOLD["graphs"][c["graph"]])
-    hb = HyperBall(csr, HllParams(c["p"]), c["depth"] or None)
+    hb = HyperBall(csr, HllParams(c["p"]), c["depth"] or None, schedule=schedule)
     hashes, maxes = [], []
     while not hb.finished:
         maxes.append(hb.iterate_once())
@@ -95,19 +96,22 @@ def test_gpu_matches_reference_golden(case):
 
 
 # ---------------------------------------------------------------- lockstep vs oracle
+@pytest.mark.parametrize("schedule", ["auto", "group"])
 @pytest.mark.parametrize("p", [4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14])
-def test_gpu_lockstep_c1_depth3(c1, oracle_best, p):
-    assert lockstep(c1, p, 3, oracle_best) == 3
+def test_gpu_lockstep_c1_depth3(c1, oracle_best, p, schedule):
+    assert lockstep(c1, p, 3, oracle_best, schedule=schedule) == 3
 
 
+@pytest.mark.parametrize("schedule", ["auto", "group", "items"])
 @pytest.mark.parametrize("depth", [1, 2, None])
-def test_gpu_lockstep_c1_p10(c1, oracle_best, depth):
-    lockstep(c1, 10, depth, oracle_best)
+def test_gpu_lockstep_c1_p10(c1, oracle_best, depth, schedule):
+    lockstep(c1, 10, depth, oracle_best, schedule=schedule)
 
 
+@pytest.mark.parametrize("schedule", ["auto", "group"])
 @pytest.mark.parametrize("p", [8, 10, 12])
-def test_gpu_skip_unchanged_bit_exact(c1, oracle_best, p):
-    lockstep(c1, p, None, oracle_best, skip=True)
+def test_gpu_skip_unchanged_bit_exact(c1, oracle_best, p, schedule):
+    lockstep(c1, p, None, oracle_best, skip=True, schedule=schedule)
 
 
 @pytest.mark.parametrize("p", [15, 16])
@@ -116,17 +120,28 @@ def test_gpu_lockstep_large_p(oracle_best, p):
     lockstep(g, p, 2, oracle_best)
 
 
-def test_gpu_lockstep_radius_and_obstacles(oracle_best):
+@pytest.mark.parametrize("schedule", ["auto", "group"])
+def test_gpu_lockstep_radius_and_obstacles(oracle_best, schedule):
     g = CompressedCsr.synth_grid(90, 70, 40, 2, 8, 99, 15 * 15)
-    lockstep(g, 10, None, oracle_best)
+    lockstep(g, 10, None, oracle_best, schedule=schedule)
 
 
-def test_gpu_edge_cases(oracle_best):
+@pytest.mark.parametrize("schedule", ["auto", "group", "items"])
+def test_gpu_edge_cases(oracle_best, schedule):
     # isolated nodes, empty rows mixed with a clique, a star
     adj = [[], [2, 3, 4], [1, 3, 4], [1, 2, 4], [1, 2, 3], [], [7], [6]]
     for p in (4, 10, 16):
-        lockstep(csr_of(adj), p, None, oracle_best)
-    lockstep(csr_of([[]]), 10, None, oracle_best)
+        lockstep(csr_of(adj), p, None, oracle_best, schedule=schedule)
+    lockstep(csr_of([[]]), 10, None, oracle_best, schedule=schedule)
+    # a dense 300-clique: one group path window holds every id of 8 identical-but-self rows
+    clique = [[w for w in range(300) if w != v] for v in range(300)]
+    lockstep(csr_of(clique), 10, 2, oracle_best, schedule=schedule)
+
+
+def test_gpu_schedule_flags_rejected():
+    g = csr_of([[1], [0]])
+    with pytest.raises(ValueError):
+        HyperBall(g, 10, schedule="bogus")
 
 
 # ---------------------------------------------------------------- interval (sparse-table) variant
@@ -186,14 +201,15 @@ def test_gpu_interval_random_registers(oracle_best, p):
 
 
 # ---------------------------------------------------------------- random registers (all nibble values)
+@pytest.mark.parametrize("schedule", ["auto", "group"])
 @pytest.mark.parametrize("p", list(range(4, 17)))
-def test_gpu_random_registers_one_step(oracle_best, p):
+def test_gpu_random_registers_one_step(oracle_best, p, schedule):
     g = CompressedCsr.synth_grid(20, 20, 4, 2, 4, p, 0)
     n, rb = g.n, (1 << p) // 2
     rng = np.random.default_rng(p)
     regs = rng.integers(0, 256, n * rb, dtype=np.uint8)
     regs[rng.random(regs.size) < 0.3] = 0
-    hb = HyperBall(g, p, None)
+    hb = HyperBall(g, p, None, schedule=schedule)
     hb.set_registers(regs)
     assert np.array_equal(hb.registers(), regs), "packed <-> bit-sliced round trip"
     c_prev = np.array([oracle_best.estimate(regs[v * rb:(v + 1) * rb].copy(), p) for v in range(n)])
@@ -393,16 +409,17 @@ def noncanonical(csr, rng, frac):
     return CompressedCsr.from_arrays(np.array(offs, np.uint64), csr.degrees.copy(), b"".join(rows))
 
 
+@pytest.mark.parametrize("schedule", ["auto", "group"])
 @pytest.mark.parametrize("frac", [0.02, 1.0])
-def test_gpu_noncanonical_varints_match_reference(c1, oracle_best, frac):
+def test_gpu_noncanonical_varints_match_reference(c1, oracle_best, frac, schedule):
     """6..10-byte varints decode like the reference (acceptance AND values): registers,
     c and sum_d after every iteration equal the oracle's on the re-encoded stream,
     and the final state equals the canonical stream's.  C1 rows (degree up to ~3,000)
     are cut into 512-id work items, so long varints also sit at item cuts."""
     g = noncanonical(c1, np.random.default_rng(7), frac)
     assert g.stream_len > c1.stream_len
-    assert lockstep(g, 10, None, oracle_best) >= 3
-    a, b = HyperBall(g, 10, None), HyperBall(c1, 10, None)
+    assert lockstep(g, 10, None, oracle_best, schedule=schedule) >= 3
+    a, b = HyperBall(g, 10, None, schedule=schedule), HyperBall(c1, 10, None)
     a.run(), b.run()
     assert np.array_equal(a.registers(), b.registers()) and np.array_equal(a.state().sum_d, b.state().sum_d)
     h = HyperBall(DeviceGraph(g, async_upload=True), 10, None)  # pipelined first pass
@@ -440,7 +457,7 @@ def c3():
     return build_graph("c3", threads=os.cpu_count() or 1)
 
 
-@pytest.mark.parametrize("mode", ["dense", "skip", "interval"])
+@pytest.mark.parametrize("mode", ["dense", "skip", "interval", "items"])
 def test_gpu_c3_matches_reference_hashes(c3, mode):
     """BASELINE headline config C3 (open 486^2 grid, radius 87: 236,196 cells, 4.79e9
     edges, p=10, full depth): after EVERY iteration the register plane (reference
@@ -451,7 +468,8 @@ def test_gpu_c3_matches_reference_hashes(c3, mode):
     assert (c3.n, c3.edges, c3.stream_len) == (gh["nodes"], gh["edges"], gh["stream_bytes"])
     assert _sha(c3.offsets) == gh["offsets_sha256"] and _sha(c3.degrees) == gh["degrees_sha256"]
     assert _sha(c3.stream) == gh["stream_sha256"]
-    hb = HyperBall(c3, HllParams(10), None, skip_unchanged=mode == "skip", interval=mode == "interval")
+    hb = HyperBall(c3, HllParams(10), None, skip_unchanged=mode == "skip", interval=mode == "interval",
+                   schedule="items" if mode == "items" else "auto")
     t = 0
     while not hb.finished:
         mx = hb.iterate_once()
