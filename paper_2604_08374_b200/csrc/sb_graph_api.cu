@@ -276,8 +276,8 @@ static int graph_create(uint64_t n, const uint64_t* offsets, const uint32_t* deg
     return SB_OK;
   }
   // Asynchronous: a small first chunk (1/64 of the bytes, so the first union
-  // tiles start early) then K-1 chunks of ~equal stream bytes, on 8-node (tile
-  // group) boundaries; copy k on up_stream, validation k on val_stream after copy k.
+  // tiles start early) then K-1 chunks of ~equal stream bytes, on 16-node
+  // (group path) boundaries; copy k on up_stream, validation k on val_stream after copy k.
   const int rc = graph_setup_host(g, degrees + node_begin);
   if (rc) return bail(rc);
   GK(cudaStreamCreateWithFlags(&g->up_stream, cudaStreamNonBlocking));
@@ -288,11 +288,11 @@ static int graph_create(uint64_t n, const uint64_t* offsets, const uint32_t* deg
   for (int k = 1; k < K; ++k) {
     const uint64_t goal = b0 + first + (g->stream_local - first) * (k - 1) / (K - 1);
     uint64_t v = std::lower_bound(offsets + node_begin, offsets + node_end, goal) - (offsets + node_begin);
-    v = std::min<uint64_t>(v & ~7ull, g->n_local);
+    v = std::min<uint64_t>(v & ~15ull, g->n_local);  // whole 16-node groups per chunk
     if (v > g->chunk_node.back()) g->chunk_node.push_back(v);
   }
   if (g->chunk_node.back() != g->n_local) g->chunk_node.push_back(g->n_local);
-  // tile ranges: tiles are ordered by 8-node group
+  // tile ranges: tiles are ordered by 8-node group (chunks hold whole 16-node groups)
   std::vector<uint32_t> tn0(g->n_tiles);
   if (g->n_tiles) GK(cudaMemcpy(tn0.data(), g->d_tile_node0, g->n_tiles * 4, cudaMemcpyDeviceToHost));
   g->chunk_tile.clear();

@@ -576,65 +576,41 @@ __device__ __forceinline__ void process_item(const UnionArgs& a, uint64_t item, 
 }
 
 // ------------------------------------------------------------------ tile-shared gathers
-// A CTA takes a group of 8 consecutive nodes (whole rows, one 512-B row slice)
-// and sweeps the union of their neighbour lists in id windows of SH_W ids:
-//   A  warp w decodes node w's LEB128 row (decode_step4) and sets the node's
-//      membership bitmap for the window (bit per id; one shared atomicOr per
-//      run of ids sharing a word: __match_any + __reduce_or);
-//   B1 the 8 bitmaps are ANDed / ORed word by word: F = ids in EVERY active
-//      node's list, P = ids in some but not all.  Warp w gathers the rows of
-//      the F ids of its 16-word block ONCE and folds them into a group
-//      accumulator (bit-serial 9-way max over 8-row batches);
-//   B2 warp w folds the P ids of its own node (P & own bitmap) into the node's
-//      accumulator.
-// At the end next[v] = max(cur[v], own partials, group accumulator) -- max is
-// associative, commutative and idempotent, so the grouping is exact
-// (PAPER.md:358-360 unchanged).  On a visibility graph 8 consecutive raster
-// nodes see nearly the same cells: every row is fetched once per group
-// instead of once per edge, and the F rows (~90 %) are max-reduced once
-// instead of 8 times.
-constexpr int SH_W = 4096;             // ids per window
-constexpr int SH_WW = SH_W / 32;       // bitmap words per node
-constexpr int SH_WPW = SH_WW / 8;      // words per warp in B1
-constexpr int SH_BUF = 128;            // ids of one 128-byte decode window
-constexpr unsigned SH_MIN_EDGES_PER_WINDOW = 128;
+// A CTA takes a group of GN = 16 consecutive nodes (whole rows, one row slice)
+// and sweeps the union of their neighbour lists in windows of GW_IDS ids:
+//   A  warp w decodes the LEB128 rows of nodes 2w and 2w+1 straight into their
+//      membership bitmaps for the window (bit per id, one shared atomicOr per
+//      lane and word; a row's decode stops at the first id past the window and
+//      resumes there in the next one).
+//   B0 per bitmap word: the AND of every aligned block of nodes -- 8 pairs, 4
+//      quads, 2 octets and the root (all 16; nodes without neighbours count as
+//      holding every id).
+//   B1 every id is folded into the blocks of the canonical cover of its member
+//      set: block b takes the ids held by all of b but not by all of b's parent
+//      (C_b = A_b & ~A_parent).  The root's ids (held by every node, ~90 % on a
+//      visibility graph) are split over the 8 warps by word range; the 30 other
+//      block accumulators are split over the warps by tree level.
+// At the end node k's row is max(cur[k], root, k's leaf, pair, quad, octet):
+// max is associative, commutative and idempotent and the covers partition each
+// id's member set, so every id of N(k) is folded into exactly the blocks on
+// k's path and no other id is (PAPER.md:358-360 unchanged).  Each row is
+// gathered once per block of its cover -- about once per group for the root
+// ids and ~2 times for the ids at the rim of the visibility disks -- instead of
+// once per edge.
+constexpr int GN = 16;                  // nodes per group
+constexpr int GW_IDS = 8192;            // ids per window
+constexpr int GW = GW_IDS / 32;         // bitmap words per node (= threads per CTA)
+constexpr int GBLK = 2 * GN - 2;        // non-root blocks: 16 leaves, 8 pairs, 4 quads, 2 octets
+constexpr unsigned GMIN_EDGES_PER_WINDOW = 1024;
 
-struct SharedSmem {
-  uint32_t bm[8][SH_WW];
-  uint32_t buf[8][SH_BUF];
-  uint32_t sF[SH_WW], sP[SH_WW];
-  uint16_t plist[SH_WW];
-  uint32_t pcount[2];
-  uint32_t next[2][8];
-  uint4 red[8][32];  // per-warp group accumulators (<= 32 lanes x 16 B)
-};
-
-// Per-warp cursor over one node's row (warp-uniform state).
-template <bool SKIP>
-struct RowCursor {
-  uint64_t pos;
-  uint32_t rem, base;
-  int n, i;
-  // Next undecoded-and-unconsumed id (0xffffffff: row exhausted); refills the
-  // buffer from the stream when it is empty.
-  __device__ __forceinline__ uint32_t peek(const UnionArgs& a, uint32_t* buf, int lane) {
-    while (i >= n) {
-      if (rem == 0) return 0xffffffffu;
-      __syncwarp();  // every lane is done with the previous window's ids
-      const Decode4 d = decode_step4<SKIP, 0>(a.stream, pos, rem, base, a.changed_in, buf, lane);
-      if (d.advance == 0) {  // unreachable on a validated stream
-        rem = 0;
-        return 0xffffffffu;
-      }
-      pos += d.advance;
-      rem -= d.wanted;
-      base = d.last;
-      n = d.count;
-      i = 0;
-      __syncwarp();
-    }
-    return buf[i];
-  }
+struct GroupSmem {
+  uint32_t bm[GN][GW];          // membership bitmaps of the window
+  uint32_t A[GN - 1][GW];       // block ANDs: pairs 0..7, quads 8..11, octets 12..13, root 14
+  uint4 blk[GBLK][32];          // block accumulators (per lane; leaves 0..15, pairs 16..23, quads 24..27, octets 28..29)
+  uint4 root[8][32];            // per-warp root partials (end of group)
+  uint32_t next[2][GN];         // next undecoded id per node (~0: row exhausted)
+  unsigned long long pos[GN];   // row cursors: byte position, ids left, last id
+  uint32_t rem[GN], base[GN];
 };
 
 // acc <- max(acc, rows of the candidate bits) over `nw` bitmap words: id of
@@ -709,149 +685,311 @@ __device__ __forceinline__ void fold_word(Grp& acc, uint32_t w, uint32_t id0, co
   }
 }
 
-// Group decision (warp 0): take the shared path iff >= 2 nodes have
-// neighbours, the group averages >= SH_MIN_EDGES_PER_WINDOW edges per window
-// of its id span (sparse, scattered rows would pay the window sweep for
-// nothing) and the group is small enough not to unbalance the launch.
-// Returns the mask of nodes with neighbours | 0x100 for the shared path, else 0.
-__device__ __forceinline__ uint32_t group_mode(const UnionArgs& a, uint32_t g0, int lane) {
+__device__ __forceinline__ uint4 grp_u4(const Grp& g) { return make_uint4(g.b0, g.b1, g.b2, g.b3); }
+__device__ __forceinline__ Grp u4_grp(const uint4& v) { return Grp{v.x, v.y, v.z, v.w}; }
+
+// Per-node cursor over its LEB128 row (warp-uniform).
+struct RowPos {
+  uint64_t pos;
+  uint32_t rem, base;
+};
+
+// Decodes node row `c` from its cursor into bitmap `bm` (ids in [B, B + GW_IDS))
+// and returns the first id not consumed (~0 when the row is exhausted).  128
+// bytes per step, the decode_step4 arithmetic; the terminators of the row whose
+// id falls in the window are a prefix of the step's, so the cursor advances to
+// just past the last one and the rest are decoded again by the next window.
+template <bool SKIP>
+__device__ __forceinline__ uint32_t decode_to_bitmap(const UnionArgs& a, RowPos& c, uint32_t B, uint32_t* bm,
+                                                     int lane) {
+  const uint32_t ltm = (1u << lane) - 1u;
+  while (c.rem) {
+    const uint8_t* al = a.stream + (c.pos & ~3ull) + 4 * lane;
+    const uint32_t w0 = ld_stream_word(al);
+    const uint32_t w1 = ld_stream_word(al + 4);
+    const uint32_t w = __funnelshift_r(w0, w1, static_cast<uint32_t>(c.pos & 3) * 8);
+    uint32_t wp = __shfl_up_sync(FULL, w, 1);
+    if (lane == 0) wp = 0;  // the cursor sits on a varint boundary
+    const uint32_t F = w & 0x80808080u, Fp = wp & 0x80808080u;
+    const uint32_t m1 = __funnelshift_l(Fp, F, 8);
+    const uint32_t m2 = m1 & __funnelshift_l(Fp, F, 16);
+    const uint32_t m3 = m2 & __funnelshift_l(Fp, F, 24);
+    const uint32_t m4 = m3 & Fp;
+    const uint32_t D = (m1 >> 7) + (m2 >> 7) + (m3 >> 7) + (m4 >> 7);
+    uint32_t cb[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) cb[k] = ((w >> (8 * k)) & 0x7fu) << (7 * ((D >> (8 * k)) & 0xffu));
+    const uint32_t p1 = cb[0] + cb[1], p2 = p1 + cb[2], lane_sum = p2 + cb[3];
+    uint32_t incl = lane_sum;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(FULL, incl, d);
+      if (lane >= d) incl += y;
+    }
+    const uint32_t excl = c.base + incl - lane_sum;
+    const uint32_t id[4] = {excl + cb[0], excl + p1, excl + p2, excl + lane_sum};
+    const uint32_t T = ~w & 0x80808080u;
+    uint32_t below = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) below += __popc(__ballot_sync(FULL, (T >> (8 * k + 7)) & 1u) & ltm);
+    // wanted: a terminator of this row; in: wanted and inside the window
+    bool in[4], out[4];
+    uint32_t r = below;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const bool want = ((T >> (8 * k + 7)) & 1u) && r < c.rem;
+      r += (T >> (8 * k + 7)) & 1u;
+      in[k] = want && id[k] - B < static_cast<uint32_t>(GW_IDS);
+      out[k] = want && !in[k];
+    }
+    // bitmap: OR the lane's bits word by word (one atomic per distinct word)
+    uint32_t cw = 0xffffffffu, cm = 0u;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      bool keep = in[k];
+      if (SKIP && keep) keep = a.changed_in[id[k]] != 0;
+      if (keep) {
+        const uint32_t off = id[k] - B;
+        const uint32_t wd = off >> 5;
+        if (wd != cw) {
+          if (cm) atomicOr(bm + cw, cm);
+          cw = wd;
+          cm = 0u;
+        }
+        cm |= 1u << (off & 31);
+      }
+    }
+    if (cm) atomicOr(bm + cw, cm);
+    // last in-window terminator -> new cursor; first out-of-window one -> next id
+    int lastk = -1, firstk = -1;
+#pragma unroll
+    for (int k = 3; k >= 0; --k) {
+      if (in[k] && lastk < 0) lastk = k;
+      if (out[k]) firstk = k;
+    }
+    uint32_t nin = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) nin += __popc(__ballot_sync(FULL, in[k]));
+    const uint32_t anyin = __ballot_sync(FULL, lastk >= 0);
+    const uint32_t anyout = __ballot_sync(FULL, firstk >= 0);
+    if (anyin) {
+      const int L = 31 - __clz(anyin);
+      const int lk = __shfl_sync(FULL, lastk, L);
+      c.pos += 4 * L + lk + 1;
+      c.base = __shfl_sync(FULL, sel4(id, lk), L);
+      c.rem -= nin;
+    }
+    if (anyout) {
+      const int L = __ffs(anyout) - 1;
+      const int fk = __shfl_sync(FULL, firstk, L);
+      return __shfl_sync(FULL, sel4(id, fk), L);
+    }
+    if (!anyin) {  // unreachable on a validated stream (a step always holds a terminator)
+      c.rem = 0;
+      break;
+    }
+  }
+  return 0xffffffffu;
+}
+
+// acc <- max(acc, rows of the set bits of the warp-uniform word cw): ids
+// id0 + bit.  p >= 10 (one row slice per warp step): the set bits are taken 4
+// at a time (one 4-row bit-serial max, 8 LOP3 per row also for sparse words);
+// p < 10: batches over bit positions (fold_word).
+template <int P, class C>
+__device__ __forceinline__ void fold_set_bits(Grp& acc, uint32_t cw, uint32_t id0, const uint8_t* curb, int sub) {
+  using G = Geo<P>;
+  using IO = GrpIO<G::GB>;
+  if constexpr (G::SUB == 1) {
+    const uint8_t* rb = curb + static_cast<uint64_t>(id0) * G::ROW;
+    while (cw) {
+      Grp x[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (cw) {
+          const int b = __ffs(cw) - 1;
+          cw &= cw - 1u;
+          x[q] = IO::ld(rb + static_cast<uint64_t>(b) * G::ROW);
+        } else {
+          x[q] = grp_zero();
+        }
+      }
+      batch_max<C, 4>(acc, x);
+    }
+  } else {
+    fold_word<P, C>(acc, cw, id0, curb, sub);
+  }
+}
+
+// Non-root blocks by owner warp, balanced per tree level: warps 0/1 the octets,
+// 2/3 two quads each, 4/5 four pairs each, 6/7 eight leaves each.
+__device__ __forceinline__ void owned_blocks(int warp, int& first, int& count) {
+  const int level = warp >> 1;            // 0 octets, 1 quads, 2 pairs, 3 leaves
+  count = 1 << level;
+  first = 32 - (4 << level) + (warp & 1) * count;
+}
+
+// Node mask of block b (leaves 0..15, pairs 16..23, quads 24..27, octets 28..29).
+__device__ __forceinline__ uint32_t block_nodes(int b) {
+  if (b < 16) return 1u << b;
+  if (b < 24) return 0x3u << (2 * (b - 16));
+  if (b < 28) return 0xfu << (4 * (b - 24));
+  return 0xffu << (8 * (b - 28));
+}
+
+// C_b for word j: ids held by every node of block b but not by every node of its parent.
+__device__ __forceinline__ uint32_t block_cover_word(const GroupSmem& S, int b, int j, uint32_t act) {
+  if (b < 16) {  // leaf: own bitmap minus the pair's AND
+    const uint32_t own = S.bm[b][j];
+    return own & ~S.A[b >> 1][j];
+  }
+  if (b < 24) return S.A[b - 16][j] & ~S.A[8 + ((b - 16) >> 1)][j];
+  if (b < 28) return S.A[b - 16][j] & ~S.A[12 + ((b - 24) >> 1)][j];
+  return S.A[b - 16][j] & ~S.A[14][j];
+}
+
+template <int P, bool SKIP, class C0>
+__device__ __forceinline__ void process_group16(const UnionArgs& a, uint32_t g0, int slice, int lane, int warp,
+                                                uint32_t act, GroupSmem& S) {
+  using G = Geo<P>;
+  using IO = GrpIO<G::GB>;
+  using C = UCfg<8, false, C0::MINB, false, C0::KWAY, C0::OR>;
+  const int sub = lane / G::LPR;
+  const int gl = lane % G::LPR;
+  const uint64_t goff = static_cast<uint64_t>(slice) * G::SLICE_BYTES + static_cast<uint64_t>(gl) * G::GB;
+  const uint8_t* curb = opaque(a.cur + goff);
+  // cursors of this warp's two nodes (kept in shared memory between windows)
+  if (lane < 2) {
+    const int k = 2 * warp + lane;
+    const uint32_t node = g0 + k;
+    const bool mine = (act >> k) & 1u;
+    S.pos[k] = mine ? a.row_off[node] : 0ull;
+    S.rem[k] = mine ? a.degrees[node] : 0u;
+    S.base[k] = 0u;
+    S.next[0][k] = mine ? a.node_lo[node] : 0xffffffffu;
+  }
+  for (int i = threadIdx.x; i < GBLK * 32; i += blockDim.x) (&S.blk[0][0])[i] = make_uint4(0u, 0u, 0u, 0u);
+  Grp all = grp_zero();  // this warp's share of the root
+  int bfirst, bcount;
+  owned_blocks(warp, bfirst, bcount);
+  __syncthreads();
+  for (int r = 0;; ++r) {
+    uint32_t B = 0xffffffffu;
+#pragma unroll
+    for (int k = 0; k < GN; ++k) B = min(B, S.next[r & 1][k]);
+    if (B == 0xffffffffu) break;  // every row exhausted (CTA-uniform)
+    B &= ~31u;
+    // A: this warp's two rows -> bitmaps
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int k = 2 * warp + h;
+      uint32_t* bm = S.bm[k];
+#pragma unroll
+      for (int i = lane; i < GW; i += 32) bm[i] = 0u;
+      __syncwarp();
+      uint32_t nx = S.next[r & 1][k];
+      if (nx - B < static_cast<uint32_t>(GW_IDS)) {
+        RowPos c{S.pos[k], S.rem[k], S.base[k]};
+        nx = decode_to_bitmap<SKIP>(a, c, B, bm, lane);
+        __syncwarp();
+        if (lane == 0) {
+          S.pos[k] = c.pos;
+          S.rem[k] = c.rem;
+          S.base[k] = c.base;
+        }
+      }
+      if (lane == 0) S.next[(r + 1) & 1][k] = nx;
+    }
+    __syncthreads();
+    // B0: block ANDs of word j = threadIdx.x (nodes without neighbours hold every id)
+    {
+      const int j = threadIdx.x;
+      uint32_t x[GN];
+#pragma unroll
+      for (int k = 0; k < GN; ++k) x[k] = ((act >> k) & 1u) ? S.bm[k][j] : 0xffffffffu;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) S.A[i][j] = x[2 * i] & x[2 * i + 1];
+      uint32_t q[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) S.A[8 + i][j] = q[i] = x[4 * i] & x[4 * i + 1] & x[4 * i + 2] & x[4 * i + 3];
+      const uint32_t o0 = q[0] & q[1], o1 = q[2] & q[3];
+      S.A[12][j] = o0;
+      S.A[13][j] = o1;
+      S.A[14][j] = o0 & o1;
+    }
+    __syncthreads();
+    // B1: root ids of this warp's word range, then the owned blocks' covers
+    fold_bits<P, C>(all, S.A[14] + 32 * warp, 32, B + 32u * 32u * warp, curb, sub);
+    for (int bi = 0; bi < bcount; ++bi) {
+      const int b = bfirst + bi;
+      if (!(act & block_nodes(b))) continue;  // no node of this block has neighbours
+      Grp acc = u4_grp(S.blk[b][lane]);
+      bool touched = false;
+#pragma unroll 1
+      for (int j0 = 0; j0 < GW; j0 += 32) {
+        const uint32_t cword = block_cover_word(S, b, j0 + lane, act);
+        uint32_t nz = __ballot_sync(FULL, cword != 0u);
+        touched |= nz != 0u;
+        while (nz) {
+          const int src = __ffs(nz) - 1;
+          nz &= nz - 1u;
+          const uint32_t cw = __shfl_sync(FULL, cword, src);
+          fold_set_bits<P, C>(acc, cw, B + 32u * (j0 + src), curb, sub);
+        }
+      }
+      if (touched) S.blk[b][lane] = grp_u4(acc);
+    }
+    __syncthreads();  // bitmaps and block ANDs are rewritten by the next window
+  }
+  // node k = max(cur[k], root partials, its leaf / pair / quad / octet)
+  S.root[warp][lane] = grp_u4(all);
+  __syncthreads();
+#pragma unroll 1
+  for (int h = 0; h < 2; ++h) {
+    const int k = 2 * warp + h;
+    const uint32_t node = g0 + k;
+    if (node >= a.n_local) break;  // warp-uniform
+    const uint64_t v = a.node_begin + node;
+    Grp acc = IO::ld(curb + v * G::ROW);  // next[v] <- cur[v]
+    if ((act >> k) & 1u) {
+      Grp x[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) x[q] = u4_grp(S.root[q][lane]);
+      batch_max<C, 8>(acc, x);
+      Grp y[4] = {u4_grp(S.blk[k][lane]), u4_grp(S.blk[16 + (k >> 1)][lane]), u4_grp(S.blk[24 + (k >> 2)][lane]),
+                  u4_grp(S.blk[28 + (k >> 3)][lane])};
+      batch_max<C, 4>(acc, y);
+    }
+    if (G::SUB > 1) {
+#pragma unroll
+      for (int m = G::LPR; m < 32; m <<= 1) combine<C::OR>(acc, grp_shfl_xor(acc, m));
+    }
+    publish_row<P>(a, curb, a.next + goff + v * G::ROW, goff, v, acc, lane);
+  }
+}
+
+// Group decision (warp 0) for the 16-node group at g0: the shared path iff >= 2
+// nodes have neighbours, the group holds <= shared_max_edges edges (load
+// balance) and its id span is dense in edges (>= GMIN_EDGES_PER_WINDOW per
+// window: the window sweep costs per window, not per edge).  Returns the mask
+// of nodes with neighbours | 0x10000 for the shared path, else 0.
+__device__ __forceinline__ uint32_t group_mode16(const UnionArgs& a, uint32_t g0, int lane) {
   const uint32_t node = g0 + lane;
-  const bool ex = lane < 8 && node < a.n_local;
+  const bool ex = lane < GN && node < a.n_local;
   const uint32_t deg = ex ? a.degrees[node] : 0u;
   uint32_t lo = deg ? a.node_lo[node] : 0xffffffffu;
   uint32_t hi = deg ? a.node_hi[node] : 0u;
   unsigned long long sum = deg;
 #pragma unroll
-  for (int o = 4; o >= 1; o >>= 1) {  // lanes 0..7
+  for (int o = 8; o >= 1; o >>= 1) {  // lanes 0..15
     sum += __shfl_xor_sync(FULL, sum, o);
     lo = min(lo, __shfl_xor_sync(FULL, lo, o));
     hi = max(hi, __shfl_xor_sync(FULL, hi, o));
   }
-  const uint32_t act = __ballot_sync(FULL, deg != 0) & 0xffu;
+  const uint32_t act = __ballot_sync(FULL, deg != 0) & 0xffffu;
   if (__popc(act) < 2 || sum > a.shared_max_edges) return 0u;
-  const unsigned long long windows = (hi - lo) / SH_W + 1ull;
-  return sum >= SH_MIN_EDGES_PER_WINDOW * windows ? (act | 0x100u) : 0u;
-}
-
-template <int P, bool SKIP, class C0>
-__device__ __forceinline__ void process_group_shared(const UnionArgs& a, uint32_t g0, int slice, int lane, int warp,
-                                                     uint32_t act, SharedSmem& S) {
-  using G = Geo<P>;
-  using IO = GrpIO<G::GB>;
-  // 8 candidate rows per lane per batch at every p (the per-node feeder is tied
-  // to U * SUB <= one 128-id decode window; the bitmap sweep is not)
-  using C = UCfg<8, false, C0::MINB, false, C0::KWAY, C0::OR>;
-  const int sub = lane / G::LPR;
-  const int gl = lane % G::LPR;
-  const uint32_t node = g0 + warp;
-  const bool exists = node < a.n_local;
-  const bool mine = (act >> warp) & 1u;
-  const uint64_t v = a.node_begin + node;
-  const uint64_t goff = static_cast<uint64_t>(slice) * G::SLICE_BYTES + static_cast<uint64_t>(gl) * G::GB;
-  const uint8_t* curb = opaque(a.cur + goff);
-  Grp acc = exists ? IO::ld(curb + v * G::ROW) : grp_zero();  // next[v] <- cur[v]
-  Grp all = grp_zero();
-  RowCursor<SKIP> c;
-  c.pos = mine ? a.row_off[node] : 0;
-  c.rem = mine ? a.degrees[node] : 0u;
-  c.base = 0;
-  c.n = c.i = 0;
-  uint32_t* buf = S.buf[warp];
-  uint32_t* bm = S.bm[warp];
-  uint32_t nx = c.peek(a, buf, lane);
-  if (lane == 0) S.next[0][warp] = nx;
-  if (threadIdx.x == 0) S.pcount[0] = 0;
-  __syncthreads();
-  for (int r = 0;; ++r) {
-    uint32_t B = 0xffffffffu;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) B = min(B, S.next[r & 1][k]);
-    if (B == 0xffffffffu) break;  // every row exhausted (CTA-uniform)
-    B &= ~31u;
-    // A: this node's ids in [B, B + SH_W) -> own bitmap
-#pragma unroll
-    for (int k = lane; k < SH_WW; k += 32) bm[k] = 0u;
-    __syncwarp();
-    for (;;) {
-      const uint32_t x = c.peek(a, buf, lane);
-      if (x == 0xffffffffu || x - B >= static_cast<uint32_t>(SH_W)) break;
-      const int e = c.i + lane;
-      const uint32_t off = (e < c.n ? buf[e] : 0xffffffffu) - B;
-      const bool in = e < c.n && off < static_cast<uint32_t>(SH_W);
-      const unsigned inm = __ballot_sync(FULL, in);
-      if (in) {
-        const unsigned peers = __match_any_sync(inm, off >> 5);
-        const unsigned bits = __reduce_or_sync(peers, 1u << (off & 31));
-        if (lane == __ffs(peers) - 1) atomicOr(bm + (off >> 5), bits);
-      }
-      c.i += __popc(inm);
-    }
-    nx = c.peek(a, buf, lane);
-    if (lane == 0) S.next[(r + 1) & 1][warp] = nx;
-    __syncthreads();
-    // B1: F / P of this warp's word block; F rows -> group accumulator
-    if (threadIdx.x == 0) S.pcount[(r + 1) & 1] = 0;  // every warp is past round r-1's B2
-    uint32_t Pw = 0;
-    if (lane < SH_WPW) {
-      const int j = warp * SH_WPW + lane;
-      uint32_t Uw = 0, F = 0xffffffffu;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const uint32_t w = S.bm[k][j];
-        Uw |= w;
-        if ((act >> k) & 1u) F &= w;
-      }
-      Pw = Uw & ~F;
-      S.sF[j] = F;
-      S.sP[j] = Pw;
-    }
-    const unsigned pm = __ballot_sync(FULL, Pw != 0u);
-    if (pm) {
-      uint32_t at = 0;
-      if (lane == 0) at = atomicAdd(&S.pcount[r & 1], static_cast<uint32_t>(__popc(pm)));
-      at = __shfl_sync(FULL, at, 0);
-      if (Pw) S.plist[at + __popc(pm & ((1u << lane) - 1u))] = static_cast<uint16_t>(warp * SH_WPW + lane);
-    }
-    __syncwarp();
-    fold_bits<P, C>(all, S.sF + warp * SH_WPW, SH_WPW, B + 32u * warp * SH_WPW, curb, sub);
-    __syncthreads();
-    // B2: this node's partial rows
-    if (mine) {
-      const int np = static_cast<int>(S.pcount[r & 1]);
-      for (int k = 0; k < np; ++k) {
-        const int j = S.plist[k];
-        const uint32_t w = S.sP[j] & bm[j];
-        if (w) fold_word<P, C>(acc, w, B + 32u * j, curb, sub);
-      }
-    }
-  }
-  if (G::SUB > 1) {
-#pragma unroll
-    for (int m = G::LPR; m < 32; m <<= 1) {
-      combine<C::OR>(acc, grp_shfl_xor(acc, m));
-      combine<C::OR>(all, grp_shfl_xor(all, m));
-    }
-  }
-  // every warp's F rows (its word blocks), whatever its own node: all eight fold in
-  if (lane < G::LPR) IO::st(reinterpret_cast<uint8_t*>(&S.red[warp][0]) + gl * G::GB, all);
-  __syncthreads();
-  if (exists) {
-    if (mine) {
-      Grp x[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const uint8_t* p = reinterpret_cast<const uint8_t*>(&S.red[k][0]) + gl * G::GB;
-        if constexpr (G::GB == 16) {
-          const uint4 q = *reinterpret_cast<const uint4*>(p);
-          x[k] = Grp{q.x, q.y, q.z, q.w};
-        } else {
-          x[k] = GrpIO<8>::unpack(*reinterpret_cast<const uint2*>(p));
-        }
-      }
-      batch_max<C, 8>(acc, x);
-    }
-    publish_row<P>(a, curb, a.next + goff + v * G::ROW, goff, v, acc, lane);
-  }
+  const unsigned long long windows = (hi - lo) / GW_IDS + 1ull;
+  return sum >= GMIN_EDGES_PER_WINDOW * windows ? (act | 0x10000u) : 0u;
 }
 
 __device__ __forceinline__ bool upload_failed(const UnionArgs& a) {
@@ -865,12 +1003,16 @@ __device__ __forceinline__ bool upload_failed(const UnionArgs& a) {
 //              nodes see almost the same neighbour ids at the same stream
 //              position, so the CTA's 8 warps re-read each row from L1
 //              instead of L2.
+template <int P, bool SKIP, class C>
+constexpr size_t union_smem_bytes() {
+  constexpr size_t ids = sizeof(uint32_t) * 8 * Feeder<P, SKIP, C::U>::BUF;
+  return ids > sizeof(GroupSmem) ? ids : sizeof(GroupSmem);
+}
+
 template <int P, bool SKIP, bool TILE, class C = DefaultCfg<P>>
 __global__ void __launch_bounds__(256, C::MINB) union_kernel(UnionArgs a) {
   using G = Geo<P>;
-  constexpr size_t kIds = sizeof(uint32_t) * 8 * Feeder<P, SKIP, C::U>::BUF;
-  constexpr size_t kSmem = kIds > sizeof(SharedSmem) ? kIds : sizeof(SharedSmem);
-  __shared__ __align__(16) unsigned char smem[kSmem];  // per-node feeders or the group path
+  extern __shared__ __align__(16) unsigned char smem[];  // per-node feeders or the group path
   __shared__ unsigned long long s_unit[2];
   __shared__ uint32_t s_mode;
   const int lane = threadIdx.x & 31;
@@ -895,17 +1037,18 @@ __global__ void __launch_bounds__(256, C::MINB) union_kernel(UnionArgs a) {
       const uint64_t t = u / G::SLICES;
       const uint32_t g0 = a.tile_node0[t];
       const uint32_t q = a.tile_q[t];
-      if (a.node_lo) {  // group path when the group's rows overlap densely
+      if (a.node_lo) {  // 16-node group path when the group's rows overlap densely
+        const uint32_t g16 = g0 & ~15u;
         if (warp == 0) {
-          const uint32_t m = group_mode(a, g0, lane);
+          const uint32_t m = group_mode16(a, g16, lane);
           if (lane == 0) s_mode = m;
         }
         __syncthreads();
         const uint32_t m = s_mode;
-        if (m) {
-          if (q == 0)
-            process_group_shared<P, SKIP, C>(a, g0, static_cast<int>(u % G::SLICES), lane, warp, m & 0xffu,
-                                             *reinterpret_cast<SharedSmem*>(smem));
+        if (m) {  // the group's first tile does the whole group; its other tiles have nothing to do
+          if (q == 0 && g0 == g16)
+            process_group16<P, SKIP, C>(a, g16, static_cast<int>(u % G::SLICES), lane, warp, m & 0xffffu,
+                                        *reinterpret_cast<GroupSmem*>(smem));
           continue;
         }
       }
@@ -1517,12 +1660,20 @@ cudaError_t launch_init(int p, uint8_t* plane, uint64_t n, const uint32_t* orig,
 
 int union_slices(int p) { return p > 10 ? 1 << (p - 10) : 1; }
 
+// Dynamic shared memory above the 48 KB default (the group path's bitmaps and
+// block accumulators), then the persistent grid for that footprint.
+static int prep_union(const void* fn, size_t smem) {
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  return grid_for(fn, 256, smem);
+}
+
 cudaError_t launch_union(int p, bool skip, const UnionArgs& a, cudaStream_t s) {
   const bool tile = a.n_tiles != 0;
-#define SB_UL(P, SK, TL, ...)                                                                        \
-  {                                                                                                  \
-    static int g = grid_for(reinterpret_cast<const void*>(union_kernel<P, SK, TL, ##__VA_ARGS__>), 256); \
-    union_kernel<P, SK, TL, ##__VA_ARGS__><<<g, 256, 0, s>>>(a);                                     \
+#define SB_UL(P, SK, TL)                                                                          \
+  {                                                                                               \
+    constexpr size_t sm = union_smem_bytes<P, SK, DefaultCfg<P>>();                               \
+    static int g = prep_union(reinterpret_cast<const void*>(union_kernel<P, SK, TL>), sm);        \
+    union_kernel<P, SK, TL><<<g, 256, sm, s>>>(a);                                                \
   }
 #define SB_L(P)                                                     \
   {                                                                 \
@@ -1597,8 +1748,9 @@ using OrCfg = UCfg<8, false, 4, false, false, true>;
 cudaError_t launch_union_or(int p, const UnionArgs& a, cudaStream_t s) {
 #define SB_LO(P)                                                                                         \
   {                                                                                                      \
-    static int g = grid_for(reinterpret_cast<const void*>(union_kernel<P, false, true, OrCfg<P>>), 256); \
-    union_kernel<P, false, true, OrCfg<P>><<<g, 256, 0, s>>>(a);                                        \
+    constexpr size_t sm = union_smem_bytes<P, false, OrCfg<P>>();                                        \
+    static int g = prep_union(reinterpret_cast<const void*>(union_kernel<P, false, true, OrCfg<P>>), sm); \
+    union_kernel<P, false, true, OrCfg<P>><<<g, 256, sm, s>>>(a);                                       \
     break;                                                                                               \
   }
   switch (p) {

@@ -8,7 +8,20 @@ mkdir -p gpurun_out
 run() { echo "== $*" >> gpurun_out/r02.log; "$@"; echo "rc=$? ($1 ${*: -1})" >> gpurun_out/r02.log; }
 (nproc; lscpu | grep 'Model name'; nvidia-smi -L) > gpurun_out/host.txt 2>&1
 NCU="ncu --set full --clock-control none --import-source on"
+# keep gpurun_out small (it must stay under 64 MiB to come back): text exports + summary, no .ncu-rep
+export_rep() {  # $1 = summary key, $2 = report basename (without .ncu-rep)
+  [[ -f gpurun_out/$2.ncu-rep ]] || return
+  ncu -i gpurun_out/$2.ncu-rep --page details > gpurun_out/$2_details.txt 2>&1
+  python -u scripts/ncu_summary.py --out gpurun_out/ncu_summary.json $1 gpurun_out/$2.ncu-rep > /dev/null
+  rm -f gpurun_out/$2.ncu-rep
+}
 for what in "${@:-all}"; do
+if [[ $what == parity ]]; then
+  run timeout 1800 python -u -m pytest tests/test_gpu_parity.py -q -x > gpurun_out/pytest_parity.log 2>&1; tail -3 gpurun_out/pytest_parity.log
+fi
+if [[ $what == quick ]]; then
+  run timeout 600 python -u bench.py --no-cpu --no-variants --no-pipeline --no-e2e > gpurun_out/bench_c3_quick.json 2> gpurun_out/bench_c3_quick.log
+fi
 if [[ $what == tests || $what == all ]]; then
   run timeout 2400 python -u -m pytest tests -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; tail -3 gpurun_out/pytest_gpu.log
   run timeout 300 python -u -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
@@ -24,15 +37,18 @@ if [[ $what == ncu || $what == all ]]; then
       --log-file gpurun_out/launches_c3.csv python -u bench.py --profile --no-cpu --no-e2e --no-variants --no-pipeline
   run timeout 900 $NCU -k regex:union_kernel -s 3 -c 1 -o gpurun_out/prof_c3_p10 \
       python -u bench.py --profile --no-cpu --no-e2e --no-variants --no-pipeline
+  export_rep c3_p10 prof_c3_p10
 fi
 if [[ $what == ncu_sweep || $what == all ]]; then
   for cfg in "c1 10" "c2 10" "c2 4" "c2 6" "c2 14"; do
     set -- $cfg
     run timeout 600 $NCU -k regex:union_kernel -s 2 -c 1 -o gpurun_out/prof_$1_p$2 \
         python -u bench.py --config $1 --p $2 --profile --no-cpu --no-e2e --no-variants --no-pipeline
+    export_rep $1_p$2 prof_$1_p$2
   done
   run timeout 600 $NCU -k regex:union_interval -s 3 -c 1 -o gpurun_out/prof_c3_interval \
       python -u scripts/pipeline_profile.py c3
+  export_rep c3_p10_interval prof_c3_interval
 fi
 if [[ $what == dist || $what == all ]]; then
   # the sharded bench path (2 ranks sharing the one GPU: fused P2P + gloo barrier) vs N=1

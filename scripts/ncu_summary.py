@@ -85,11 +85,16 @@ def summarise(rep: str, kernel: str | None) -> dict:
         if m and row[i] not in ("", "n/a"):
             stalls[m.group(1)] = float(row[i])
     out["stalls_per_issue"] = dict(sorted(stalls.items(), key=lambda kv: -kv[1])[:6])
-    out["source"] = os.path.relpath(rep, ROOT) + " (ncu --set full --clock-control none)"
+    out["source"] = os.path.basename(rep).replace(".ncu-rep", "") + " (ncu --set full --clock-control none)"
     return out
 
 
 def main(argv):
+    global OUT
+    if "--out" in argv:
+        i = argv.index("--out")
+        OUT = argv[i + 1]
+        argv = argv[:i] + argv[i + 2:]
     kernel = None
     if "--kernel" in argv:
         i = argv.index("--kernel")
