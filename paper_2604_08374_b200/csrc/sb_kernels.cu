@@ -608,6 +608,8 @@ struct GroupSmem {
   uint32_t A[GN - 1][GW];       // block ANDs: pairs 0..7, quads 8..11, octets 12..13, root 14
   uint4 blk[GBLK][32];          // block accumulators (per lane; leaves 0..15, pairs 16..23, quads 24..27, octets 28..29)
   uint4 root[8][32];            // per-warp root partials (end of group)
+  uint32_t rpre[GW];            // root bits: inclusive popcount prefix within each 32-word block
+  uint32_t rsum[8];             // root bits per 32-word block
   uint32_t next[2][GN];         // next undecoded id per node (~0: row exhausted)
   unsigned long long pos[GN];   // row cursors: byte position, ids left, last id
   uint32_t rem[GN], base[GN];
@@ -742,47 +744,71 @@ __device__ __forceinline__ uint32_t decode_to_bitmap(const UnionArgs& a, RowPos&
       in[k] = want && id[k] - B < static_cast<uint32_t>(GW_IDS);
       out[k] = want && !in[k];
     }
-    // bitmap: OR the lane's bits word by word (one atomic per distinct word)
-    uint32_t cw = 0xffffffffu, cm = 0u;
+    // the lane's in-window ids: first / last / count; its last in-window
+    // terminator (-> new cursor) and first out-of-window one (-> next id)
+    int lastk = -1, nl = 0;
+    uint32_t lo_id = 0, hi_id = 0, out_id = 0;
+    bool have_out = false;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      bool keep = in[k];
-      if (SKIP && keep) keep = a.changed_in[id[k]] != 0;
-      if (keep) {
-        const uint32_t off = id[k] - B;
-        const uint32_t wd = off >> 5;
-        if (wd != cw) {
-          if (cm) atomicOr(bm + cw, cm);
-          cw = wd;
-          cm = 0u;
-        }
-        cm |= 1u << (off & 31);
+      if (in[k]) {
+        if (nl == 0) lo_id = id[k];
+        hi_id = id[k];
+        lastk = k;
+        ++nl;
+      }
+      if (out[k] && !have_out) {
+        out_id = id[k];
+        have_out = true;
       }
     }
-    if (cm) atomicOr(bm + cw, cm);
-    // last in-window terminator -> new cursor; first out-of-window one -> next id
-    int lastk = -1, firstk = -1;
+    // bitmap: the lane's ids OR-ed in word by word (one shared atomic per word)
+    if (!SKIP && nl && hi_id - lo_id == static_cast<uint32_t>(nl - 1)) {
+      // consecutive ids (a run of deltas of 1, the common case): one bit range
+      const uint32_t olo = lo_id - B, ohi = hi_id - B;
+      const uint32_t mlo = 0xffffffffu << (olo & 31), mhi = 0xffffffffu >> (31 - (ohi & 31));
+      if ((olo >> 5) == (ohi >> 5)) {
+        atomicOr(bm + (olo >> 5), mlo & mhi);
+      } else {
+        atomicOr(bm + (olo >> 5), mlo);
+        atomicOr(bm + (ohi >> 5), mhi);
+      }
+    } else if (nl) {
+      uint32_t cw = 0xffffffffu, cm = 0u;
 #pragma unroll
-    for (int k = 3; k >= 0; --k) {
-      if (in[k] && lastk < 0) lastk = k;
-      if (out[k]) firstk = k;
+      for (int k = 0; k < 4; ++k) {
+        bool keep = in[k];
+        if (SKIP && keep) keep = a.changed_in[id[k]] != 0;
+        if (keep) {
+          const uint32_t off = id[k] - B;
+          const uint32_t wd = off >> 5;
+          if (wd != cw) {
+            if (cm) atomicOr(bm + cw, cm);
+            cw = wd;
+            cm = 0u;
+          }
+          cm |= 1u << (off & 31);
+        }
+      }
+      if (cm) atomicOr(bm + cw, cm);
     }
     uint32_t nin = 0;
 #pragma unroll
     for (int k = 0; k < 4; ++k) nin += __popc(__ballot_sync(FULL, in[k]));
-    const uint32_t anyin = __ballot_sync(FULL, lastk >= 0);
-    const uint32_t anyout = __ballot_sync(FULL, firstk >= 0);
+    const uint32_t anyin = __ballot_sync(FULL, nl != 0);
+    const uint32_t anyout = __ballot_sync(FULL, have_out);
     if (anyin) {
       const int L = 31 - __clz(anyin);
       const int lk = __shfl_sync(FULL, lastk, L);
       c.pos += 4 * L + lk + 1;
-      c.base = __shfl_sync(FULL, sel4(id, lk), L);
+      c.base = __shfl_sync(FULL, hi_id, L);
       c.rem -= nin;
     }
     if (anyout) {
-      const int L = __ffs(anyout) - 1;
-      const int fk = __shfl_sync(FULL, firstk, L);
-      return __shfl_sync(FULL, sel4(id, fk), L);
+      // the next window resumes here: pull its bytes into L2 now (the row's
+      // decode is a chain of dependent 128-byte steps)
+      if (lane < 16) prefetch_l2(a.stream + c.pos + 128 * lane);
+      return __shfl_sync(FULL, out_id, __ffs(anyout) - 1);
     }
     if (!anyin) {  // unreachable on a validated stream (a step always holds a terminator)
       c.rem = 0;
@@ -819,6 +845,63 @@ __device__ __forceinline__ void fold_set_bits(Grp& acc, uint32_t cw, uint32_t id
   } else {
     fold_word<P, C>(acc, cw, id0, curb, sub);
   }
+}
+
+// acc <- max(acc, rows of the set bits of w) for p >= 10: a full word as four
+// unconditional 8-row batches, a partial one 8 set bits at a time.
+template <int P, class C>
+__device__ __forceinline__ void fold_word_rows(Grp& acc, uint32_t w, uint32_t id0, const uint8_t* curb) {
+  using G = Geo<P>;
+  using IO = GrpIO<G::GB>;
+  const uint8_t* rb = curb + static_cast<uint64_t>(id0) * G::ROW;
+  if (w == 0xffffffffu) {
+#pragma unroll 1
+    for (int c0 = 0; c0 < 32; c0 += 8) {
+      Grp x[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) x[q] = IO::ld(rb + static_cast<uint64_t>(c0 + q) * G::ROW);
+      batch_max<C, 8>(acc, x);
+    }
+    return;
+  }
+  while (w) {
+    Grp x[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      if (w) {
+        const int b = __ffs(w) - 1;
+        w &= w - 1u;
+        x[q] = IO::ld(rb + static_cast<uint64_t>(b) * G::ROW);
+      } else {
+        x[q] = grp_zero();
+      }
+    }
+    batch_max<C, 8>(acc, x);
+  }
+}
+
+// acc <- max(acc, rows of the first n (<= K) queued ids; lane q holds id q).
+template <int P, class C, int K>
+__device__ __forceinline__ void fold_queue(Grp& acc, uint32_t qv, int n, const uint8_t* curb) {
+  using G = Geo<P>;
+  using IO = GrpIO<G::GB>;
+  Grp x[K];
+#pragma unroll
+  for (int q = 0; q < K; ++q) {
+    const uint32_t idq = __shfl_sync(FULL, qv, q);
+    x[q] = q < n ? IO::ld(curb + static_cast<uint64_t>(idq) * G::ROW) : grp_zero();
+  }
+  batch_max<C, K>(acc, x);
+}
+
+// Bits of w whose rank among its set bits is in [r0, r1).
+__device__ __forceinline__ uint32_t rank_range(uint32_t w, uint32_t r0, uint32_t r1) {
+  if (r1 < static_cast<uint32_t>(__popc(w))) w &= (1u << __fns(w, 0, static_cast<int>(r1) + 1)) - 1u;
+  if (r0 > 0) {
+    const uint32_t p = __fns(w, 0, static_cast<int>(r0));
+    w &= p >= 31 ? 0u : ~((2u << p) - 1u);
+  }
+  return w;
 }
 
 // Non-root blocks by owner warp, balanced per tree level: warps 0/1 the octets,
@@ -915,16 +998,65 @@ __device__ __forceinline__ void process_group16(const UnionArgs& a, uint32_t g0,
       const uint32_t o0 = q[0] & q[1], o1 = q[2] & q[3];
       S.A[12][j] = o0;
       S.A[13][j] = o1;
-      S.A[14][j] = o0 & o1;
+      const uint32_t rw = o0 & o1;
+      S.A[14][j] = rw;
+      uint32_t incl = __popc(rw);
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL, incl, d);
+        if (lane >= d) incl += y;
+      }
+      S.rpre[j] = incl;
+      if (lane == 31) S.rsum[warp] = incl;
     }
     __syncthreads();
-    // B1: root ids of this warp's word range, then the owned blocks' covers
-    fold_bits<P, C>(all, S.A[14] + 32 * warp, 32, B + 32u * 32u * warp, curb, sub);
+    // B1: this warp's eighth of the root ids, then the owned blocks' covers
+    if constexpr (G::SUB == 1) {
+      // split by id count (root ids cluster in runs, so equal word ranges would not balance)
+      uint32_t bs = lane < 8 ? S.rsum[lane] : 0u, bincl = bs;
+#pragma unroll
+      for (int d = 1; d < 8; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL, bincl, d);
+        if (lane >= d) bincl += y;
+      }
+      const uint32_t total = __shfl_sync(FULL, bincl, 7);
+      const uint32_t lo = static_cast<uint32_t>((static_cast<uint64_t>(total) * warp) >> 3);
+      const uint32_t hi = static_cast<uint32_t>((static_cast<uint64_t>(total) * (warp + 1)) >> 3);
+      if (lo < hi) {
+        // first word whose inclusive prefix exceeds x: the block by a ballot over
+        // the 8 block sums, the word by a ballot inside the block
+        auto locate = [&](uint32_t x, uint32_t& excl) -> int {
+          const int blk = __ffs(__ballot_sync(FULL, lane < 8 && bincl > x)) - 1;
+          const uint32_t bex = __shfl_sync(FULL, bincl - bs, blk);
+          const int jw = __ffs(__ballot_sync(FULL, bex + S.rpre[32 * blk + lane] > x)) - 1;
+          const int jj = 32 * blk + jw;
+          excl = bex + S.rpre[jj] - __popc(S.A[14][jj]);
+          return jj;
+        };
+        uint32_t ex0, ex1;
+        const int j0 = locate(lo, ex0), j1 = locate(hi - 1, ex1);
+#pragma unroll 1
+        for (int j = j0; j <= j1; ++j) {
+          uint32_t w = S.A[14][j];
+          if (j == j0 || j == j1) {
+            const uint32_t ex = j == j0 ? ex0 : ex1;
+            w = rank_range(w, j == j0 ? lo - ex : 0u, j == j1 ? hi - ex : 32u);
+          }
+          fold_word_rows<P, C>(all, w, B + 32u * j, curb);
+        }
+      }
+    } else {
+      fold_bits<P, C>(all, S.A[14] + 32 * warp, 32, B + 32u * 32u * warp, curb, sub);
+    }
     for (int bi = 0; bi < bcount; ++bi) {
       const int b = bfirst + bi;
       if (!(act & block_nodes(b))) continue;  // no node of this block has neighbours
       Grp acc = u4_grp(S.blk[b][lane]);
       bool touched = false;
+      // p >= 10: the cover's ids are sparse (the rims of the disks), so they are
+      // queued across words -- lane q holds queued id q -- and folded 8 at a time
+      uint32_t qv = 0u;
+      int qn = 0;
 #pragma unroll 1
       for (int j0 = 0; j0 < GW; j0 += 32) {
         const uint32_t cword = block_cover_word(S, b, j0 + lane, act);
@@ -933,10 +1065,28 @@ __device__ __forceinline__ void process_group16(const UnionArgs& a, uint32_t g0,
         while (nz) {
           const int src = __ffs(nz) - 1;
           nz &= nz - 1u;
-          const uint32_t cw = __shfl_sync(FULL, cword, src);
-          fold_set_bits<P, C>(acc, cw, B + 32u * (j0 + src), curb, sub);
+          uint32_t cw = __shfl_sync(FULL, cword, src);
+          const uint32_t id0 = B + 32u * (j0 + src);
+          if constexpr (G::SUB == 1) {
+            if (cw == 0xffffffffu) {
+              fold_word_rows<P, C>(acc, cw, id0, curb);
+              continue;
+            }
+            while (cw) {
+              const int bp = __ffs(cw) - 1;
+              cw &= cw - 1u;
+              if (lane == qn) qv = id0 + bp;
+              if (++qn == 8) {
+                fold_queue<P, C, 8>(acc, qv, 8, curb);
+                qn = 0;
+              }
+            }
+          } else {
+            fold_set_bits<P, C>(acc, cw, id0, curb, sub);
+          }
         }
       }
+      if (G::SUB == 1 && qn) fold_queue<P, C, 8>(acc, qv, qn, curb);
       if (touched) S.blk[b][lane] = grp_u4(acc);
     }
     __syncthreads();  // bitmaps and block ANDs are rewritten by the next window

@@ -13,6 +13,7 @@ export_rep() {  # $1 = summary key, $2 = report basename (without .ncu-rep)
   [[ -f gpurun_out/$2.ncu-rep ]] || return
   ncu -i gpurun_out/$2.ncu-rep --page details > gpurun_out/$2_details.txt 2>&1
   python -u scripts/ncu_summary.py --out gpurun_out/ncu_summary.json $1 gpurun_out/$2.ncu-rep > /dev/null
+  python -u scripts/ncu_lines.py gpurun_out/$2.ncu-rep > gpurun_out/$2_lines.txt 2>&1
   rm -f gpurun_out/$2.ncu-rep
 }
 for what in "${@:-all}"; do
