@@ -611,8 +611,8 @@ struct GroupSmem {
   uint32_t rpre[GW];            // root bits: inclusive popcount prefix within each 32-word block
   uint32_t rsum[8];             // root bits per 32-word block
   uint32_t next[2][GN];         // next undecoded id per node (~0: row exhausted)
-  unsigned long long pos[GN];   // row cursors: byte position, ids left, last id
-  uint32_t rem[GN], base[GN];
+  unsigned long long pos[GN], end[GN];  // row cursors: next byte, row end, last id
+  uint32_t base[GN];
 };
 
 // acc <- max(acc, rows of the candidate bits) over `nw` bitmap words: id of
@@ -690,22 +690,23 @@ __device__ __forceinline__ void fold_word(Grp& acc, uint32_t w, uint32_t id0, co
 __device__ __forceinline__ uint4 grp_u4(const Grp& g) { return make_uint4(g.b0, g.b1, g.b2, g.b3); }
 __device__ __forceinline__ Grp u4_grp(const uint4& v) { return Grp{v.x, v.y, v.z, v.w}; }
 
-// Per-node cursor over its LEB128 row (warp-uniform).
+// Per-node cursor over its LEB128 row (warp-uniform): next byte, row end, last id.
 struct RowPos {
-  uint64_t pos;
-  uint32_t rem, base;
+  uint64_t pos, end;
+  uint32_t base;
 };
 
 // Decodes node row `c` from its cursor into bitmap `bm` (ids in [B, B + GW_IDS))
 // and returns the first id not consumed (~0 when the row is exhausted).  128
-// bytes per step, the decode_step4 arithmetic; the terminators of the row whose
-// id falls in the window are a prefix of the step's, so the cursor advances to
-// just past the last one and the rest are decoded again by the next window.
+// bytes per step, the decode_step4 arithmetic; a byte belongs to the row iff it
+// lies before the row's end offset (no terminator ranks needed), and the
+// terminators whose id falls in the window are a prefix of the step's, so the
+// cursor advances to just past the last one and the rest are decoded again by
+// the next window.
 template <bool SKIP>
 __device__ __forceinline__ uint32_t decode_to_bitmap(const UnionArgs& a, RowPos& c, uint32_t B, uint32_t* bm,
                                                      int lane) {
-  const uint32_t ltm = (1u << lane) - 1u;
-  while (c.rem) {
+  while (c.pos < c.end) {
     const uint8_t* al = a.stream + (c.pos & ~3ull) + 4 * lane;
     const uint32_t w0 = ld_stream_word(al);
     const uint32_t w1 = ld_stream_word(al + 4);
@@ -730,42 +731,23 @@ __device__ __forceinline__ uint32_t decode_to_bitmap(const UnionArgs& a, RowPos&
     }
     const uint32_t excl = c.base + incl - lane_sum;
     const uint32_t id[4] = {excl + cb[0], excl + p1, excl + p2, excl + lane_sum};
-    const uint32_t T = ~w & 0x80808080u;
-    uint32_t below = 0;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) below += __popc(__ballot_sync(FULL, (T >> (8 * k + 7)) & 1u) & ltm);
-    // wanted: a terminator of this row; in: wanted and inside the window
-    bool in[4], out[4];
-    uint32_t r = below;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const bool want = ((T >> (8 * k + 7)) & 1u) && r < c.rem;
-      r += (T >> (8 * k + 7)) & 1u;
-      in[k] = want && id[k] - B < static_cast<uint32_t>(GW_IDS);
-      out[k] = want && !in[k];
-    }
-    // the lane's in-window ids: first / last / count; its last in-window
-    // terminator (-> new cursor) and first out-of-window one (-> next id)
-    int lastk = -1, nl = 0;
-    uint32_t lo_id = 0, hi_id = 0, out_id = 0;
-    bool have_out = false;
+    // terminators of this row: bytes before the row end
+    const int64_t left = static_cast<int64_t>(c.end) - static_cast<int64_t>(c.pos + 4 * lane);
+    const uint32_t vmask = left >= 4 ? 0x80808080u : left <= 0 ? 0u : 0x80808080u >> (8 * (4 - left));
+    const uint32_t T = ~w & vmask;
+    // in: a terminator whose id falls in the window (a prefix of the row's terminators)
+    uint32_t inm = 0u, outm = 0u;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      if (in[k]) {
-        if (nl == 0) lo_id = id[k];
-        hi_id = id[k];
-        lastk = k;
-        ++nl;
-      }
-      if (out[k] && !have_out) {
-        out_id = id[k];
-        have_out = true;
-      }
+      const uint32_t tk = (T >> (8 * k + 7)) & 1u;
+      const uint32_t ik = tk & (id[k] - B < static_cast<uint32_t>(GW_IDS) ? 1u : 0u);
+      inm |= ik << k;
+      outm |= (tk & ~ik) << k;
     }
     // bitmap: the lane's ids OR-ed in word by word (one shared atomic per word)
-    if (!SKIP && nl && hi_id - lo_id == static_cast<uint32_t>(nl - 1)) {
-      // consecutive ids (a run of deltas of 1, the common case): one bit range
-      const uint32_t olo = lo_id - B, ohi = hi_id - B;
+    if (!SKIP && w == 0x01010101u && lane_sum == 4u && inm == 0xfu) {
+      // four deltas of 1 (a run, the common case): one bit range
+      const uint32_t olo = excl + 1u - B, ohi = excl + 4u - B;
       const uint32_t mlo = 0xffffffffu << (olo & 31), mhi = 0xffffffffu >> (31 - (ohi & 31));
       if ((olo >> 5) == (ohi >> 5)) {
         atomicOr(bm + (olo >> 5), mlo & mhi);
@@ -773,11 +755,11 @@ __device__ __forceinline__ uint32_t decode_to_bitmap(const UnionArgs& a, RowPos&
         atomicOr(bm + (olo >> 5), mlo);
         atomicOr(bm + (ohi >> 5), mhi);
       }
-    } else if (nl) {
+    } else if (inm) {
       uint32_t cw = 0xffffffffu, cm = 0u;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        bool keep = in[k];
+        bool keep = (inm >> k) & 1u;
         if (SKIP && keep) keep = a.changed_in[id[k]] != 0;
         if (keep) {
           const uint32_t off = id[k] - B;
@@ -792,26 +774,24 @@ __device__ __forceinline__ uint32_t decode_to_bitmap(const UnionArgs& a, RowPos&
       }
       if (cm) atomicOr(bm + cw, cm);
     }
-    uint32_t nin = 0;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) nin += __popc(__ballot_sync(FULL, in[k]));
-    const uint32_t anyin = __ballot_sync(FULL, nl != 0);
-    const uint32_t anyout = __ballot_sync(FULL, have_out);
-    if (anyin) {
+    const uint32_t anyin = __ballot_sync(FULL, inm != 0u);
+    const uint32_t anyout = __ballot_sync(FULL, outm != 0u);
+    if (anyin) {  // advance past the last in-window terminator
       const int L = 31 - __clz(anyin);
-      const int lk = __shfl_sync(FULL, lastk, L);
+      const int lk = 31 - __clz(__shfl_sync(FULL, inm, L));
+      c.base = __shfl_sync(FULL, sel4(id, lk), L);
       c.pos += 4 * L + lk + 1;
-      c.base = __shfl_sync(FULL, hi_id, L);
-      c.rem -= nin;
     }
     if (anyout) {
       // the next window resumes here: pull its bytes into L2 now (the row's
       // decode is a chain of dependent 128-byte steps)
       if (lane < 16) prefetch_l2(a.stream + c.pos + 128 * lane);
-      return __shfl_sync(FULL, out_id, __ffs(anyout) - 1);
+      const int L = __ffs(anyout) - 1;
+      const int fk = __ffs(__shfl_sync(FULL, outm, L)) - 1;
+      return __shfl_sync(FULL, sel4(id, fk), L);
     }
     if (!anyin) {  // unreachable on a validated stream (a step always holds a terminator)
-      c.rem = 0;
+      c.pos = c.end;
       break;
     }
   }
@@ -947,7 +927,7 @@ __device__ __forceinline__ void process_group16(const UnionArgs& a, uint32_t g0,
     const uint32_t node = g0 + k;
     const bool mine = (act >> k) & 1u;
     S.pos[k] = mine ? a.row_off[node] : 0ull;
-    S.rem[k] = mine ? a.degrees[node] : 0u;
+    S.end[k] = mine ? a.row_off[node + 1] : 0ull;
     S.base[k] = 0u;
     S.next[0][k] = mine ? a.node_lo[node] : 0xffffffffu;
   }
@@ -972,12 +952,11 @@ __device__ __forceinline__ void process_group16(const UnionArgs& a, uint32_t g0,
       __syncwarp();
       uint32_t nx = S.next[r & 1][k];
       if (nx - B < static_cast<uint32_t>(GW_IDS)) {
-        RowPos c{S.pos[k], S.rem[k], S.base[k]};
+        RowPos c{S.pos[k], S.end[k], S.base[k]};
         nx = decode_to_bitmap<SKIP>(a, c, B, bm, lane);
         __syncwarp();
         if (lane == 0) {
           S.pos[k] = c.pos;
-          S.rem[k] = c.rem;
           S.base[k] = c.base;
         }
       }
@@ -1035,6 +1014,10 @@ __device__ __forceinline__ void process_group16(const UnionArgs& a, uint32_t g0,
         };
         uint32_t ex0, ex1;
         const int j0 = locate(lo, ex0), j1 = locate(hi - 1, ex1);
+        // full words: 4 unconditional 8-row batches; the bits of partial words
+        // (run ends) are queued across words and folded 8 at a time
+        uint32_t qv = 0u;
+        int qn = 0;
 #pragma unroll 1
         for (int j = j0; j <= j1; ++j) {
           uint32_t w = S.A[14][j];
@@ -1042,8 +1025,21 @@ __device__ __forceinline__ void process_group16(const UnionArgs& a, uint32_t g0,
             const uint32_t ex = j == j0 ? ex0 : ex1;
             w = rank_range(w, j == j0 ? lo - ex : 0u, j == j1 ? hi - ex : 32u);
           }
-          fold_word_rows<P, C>(all, w, B + 32u * j, curb);
+          if (w == 0xffffffffu) {
+            fold_word_rows<P, C>(all, w, B + 32u * j, curb);
+            continue;
+          }
+          while (w) {
+            const int bp = __ffs(w) - 1;
+            w &= w - 1u;
+            if (lane == qn) qv = B + 32u * j + bp;
+            if (++qn == 8) {
+              fold_queue<P, C, 8>(all, qv, 8, curb);
+              qn = 0;
+            }
+          }
         }
+        if (qn) fold_queue<P, C, 8>(all, qv, qn, curb);
       }
     } else {
       fold_bits<P, C>(all, S.A[14] + 32 * warp, 32, B + 32u * 32u * warp, curb, sub);
