@@ -48,8 +48,17 @@ $(TOOL): tools/sb_hyperball.cpp include/sieveball/hyperball_cuda.hpp $(LIB)
 oracle:
 	$(MAKE) -s -C oracle
 
+# Instrumented build for scripts/group_stats.py (per-phase cycles of the group
+# path); loaded with SB_LIBRARY=$(STATS_LIB), never by default.
+STATS_LIB := $(PKG)/libsieveball_cuda_stats.so
+stats: $(STATS_LIB)
+$(BUILD)/sb_kernels_stats.o: $(CSRC)/sb_kernels.cu $(HDRS) | $(BUILD)
+	$(NVCC) $(NVFLAGS) -DSB_GROUP_STATS -c $< -o $@ 2> $(BUILD)/ptxas_kernels_stats.txt || (cat $(BUILD)/ptxas_kernels_stats.txt; false)
+$(STATS_LIB): $(BUILD)/sb_kernels_stats.o $(filter-out $(BUILD)/sb_kernels.o,$(OBJS))
+	$(NVCC) $(ARCH) -shared -o $@ $^ -lnccl -lz -lpthread
+
 clean:
-	rm -rf $(BUILD) $(LIB) $(TOOL)
+	rm -rf $(BUILD) $(LIB) $(TOOL) $(STATS_LIB)
 	$(MAKE) -C oracle clean
 
-.PHONY: all oracle clean
+.PHONY: all oracle clean stats

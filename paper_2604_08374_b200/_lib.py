@@ -141,15 +141,18 @@ def _preload_torch_nccl() -> None:
 
 
 def lib() -> C.CDLL:
-    """Load the in-tree shared object (fails loudly if it was not built)."""
+    """Load the in-tree shared object (fails loudly if it was not built).
+    SB_LIBRARY may name another build of the same sources (the instrumented
+    `make stats` build used by scripts/group_stats.py)."""
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB_PATH):
+        path = os.environ.get("SB_LIBRARY", LIB_PATH)
+        if not os.path.exists(path):
             raise ImportError(
-                f"{LIB_PATH} is missing: build it with `make` or __graft_entry__.build(); "
+                f"{path} is missing: build it with `make` or __graft_entry__.build(); "
                 "the HyperBall path has no CPU fallback")
         _preload_torch_nccl()
-        L = C.CDLL(LIB_PATH)
+        L = C.CDLL(path)
         for name, (res, args) in _SIGS.items():
             f = getattr(L, name)
             f.restype = res

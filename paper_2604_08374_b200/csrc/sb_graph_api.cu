@@ -13,7 +13,7 @@
 // mode's sparse table).
 int build_run_index(sb_graph* g) {
   if (g->d_run_off || g->n_items == 0) return SB_OK;
-  if (const int rc = graph_wait(g)) return rc;
+  if (g->broken) return fail(SB_ERUNTIME, "cgraph: the graph failed validation at upload");
   if (reinterpret_cast<uintptr_t>(g->d_stream) & 15) return fail(SB_ERUNTIME, "internal: stream not 16-B aligned");
   sb::RunIndexArgs a{};
   a.stream = g->d_stream;
@@ -22,13 +22,48 @@ int build_run_index(sb_graph* g) {
   a.item_base = g->d_item_base;
   a.item_count = g->d_item_count;
   a.n_items = g->n_items;
+  a.item_begin = 0;
+  a.item_end = g->n_items;
+  a.range_end_byte = g->stream_local;
   uint64_t* d_cnt = nullptr;
   CK(dalloc(&d_cnt, g->n_items * 8 + 8));
   a.run_count = d_cnt;
   a.max_run = reinterpret_cast<unsigned int*>(d_cnt + g->n_items);
   CK(cudaMemsetAsync(a.max_run, 0, 4, 0));
-  CK(sb::launch_run_index(a, false, 0));
-  CK(sync_stream(0));
+  if (g->pending && g->chunk_item.size() > 2) {
+    // still uploading: count chunk k's runs as soon as chunk k is validated,
+    // so the count pass hides under the remaining PCIe copies
+    cudaStream_t s = nullptr;
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    CK(sync_stream(0));  // the max_run reset
+    a.err = g->d_err;
+    for (size_t k = 0; k + 1 < g->chunk_item.size(); ++k) {
+      a.item_begin = g->chunk_item[k];
+      a.item_end = g->chunk_item[k + 1];
+      a.range_end_byte = g->chunk_byte[k + 1];  // the next chunk's items are not cut yet
+      if (a.item_end == a.item_begin) continue;
+      CK(cudaStreamWaitEvent(s, g->val_ev[k], 0));
+      CK(sb::launch_run_index(a, false, s));
+    }
+    const int rc = graph_wait(g);
+    CK(sync_stream(s));
+    cudaStreamDestroy(s);
+    if (rc) {
+      dfree(d_cnt);
+      return rc;
+    }
+    a.err = nullptr;
+    a.item_begin = 0;
+    a.item_end = g->n_items;
+    a.range_end_byte = g->stream_local;
+  } else {
+    if (const int rc = graph_wait(g)) {
+      dfree(d_cnt);
+      return rc;
+    }
+    CK(sb::launch_run_index(a, false, 0));
+    CK(sync_stream(0));
+  }
   CK(cudaMemcpy(&g->max_run, a.max_run, 4, cudaMemcpyDeviceToHost));
   std::vector<uint64_t> off(g->n_items + 1, 0);
   CK(cudaMemcpy(off.data() + 1, d_cnt, g->n_items * 8, cudaMemcpyDeviceToHost));
@@ -121,6 +156,7 @@ static int graph_setup_host(sb_graph* g, const uint32_t* deg_local) {
   }
   CK(dalloc(&g->d_node_item, node_item.size() * 4));
   CK(cudaMemcpy(g->d_node_item, node_item.data(), node_item.size() * 4, cudaMemcpyHostToDevice));
+  g->h_node_item = std::move(node_item);
   const uint64_t ni = std::max<uint64_t>(items, 1);
   CK(dalloc(&g->d_item_off, ni * 8));
   CK(dalloc(&g->d_item_base, ni * 4));
@@ -299,6 +335,12 @@ static int graph_create(uint64_t n, const uint64_t* offsets, const uint32_t* deg
   for (uint64_t cn : g->chunk_node)
     g->chunk_tile.push_back(std::lower_bound(tn0.begin(), tn0.end(), static_cast<uint32_t>(std::min<uint64_t>(cn, 0xffffffffull))) - tn0.begin());
   g->chunk_tile.back() = g->n_tiles;
+  g->chunk_item.clear();
+  g->chunk_byte.clear();
+  for (uint64_t cn : g->chunk_node) {
+    g->chunk_item.push_back(g->h_node_item[cn]);
+    g->chunk_byte.push_back(offsets[node_begin + cn] - b0);  // slice-relative start of the chunk's bytes
+  }
   const size_t nk = g->chunk_node.size() - 1;
   g->val_ev.resize(nk, nullptr);
   for (size_t k = 0; k < nk; ++k) {

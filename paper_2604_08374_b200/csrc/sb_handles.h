@@ -238,7 +238,8 @@ struct sb_graph {
   unsigned long long* d_err = nullptr;  // [0] min bad node, [1] max run
   cudaStream_t up_stream = nullptr, val_stream = nullptr;
   std::vector<cudaEvent_t> val_ev;
-  std::vector<uint64_t> chunk_node, chunk_tile;
+  std::vector<uint64_t> chunk_node, chunk_tile, chunk_item, chunk_byte;
+  std::vector<uint32_t> h_node_item;  // local node -> first work item (host copy)
   ~sb_graph() {
     DeviceGuard dg(device);
     if (up_stream) cudaStreamSynchronize(up_stream);

@@ -84,6 +84,9 @@ struct RunIndexArgs {
   const uint32_t* item_base;
   const uint32_t* item_count;
   uint64_t n_items;
+  uint64_t item_begin, item_end;  // items this launch covers (an upload chunk, or all)
+  uint64_t range_end_byte;        // end of item_end - 1 (the next item may not exist yet)
+  const unsigned long long* err;  // upload validation verdict (~0 = clean; NULL: validated)
   uint64_t* run_count;         // count pass: runs per item
   unsigned int* max_run;       // count pass: longest run within an item
   const uint64_t* run_off;     // fill pass: offsets (n_items + 1)

@@ -113,17 +113,16 @@ __global__ void __launch_bounds__(256, 3) build_items_kernel(BuildArgs a) {
     uint32_t done = 0;                     // terminators before this window (cut rows only)
     unsigned long long done_sum = 0;       // their contributions
     uint32_t next_cut = a.chunk;           // row index of the next item's first id
+    // software pipeline: the next window's 16 bytes per lane are in flight
+    // while this one is reduced (plus an L2 prefetch two windows ahead)
+    uint4 qn = make_uint4(0u, 0u, 0u, 0u);
+    if ((pos0 & ~15ull) + 16 * lane < end) qn = __ldg(reinterpret_cast<const uint4*>(a.stream + (pos0 & ~15ull) + 16 * lane));
     for (uint64_t wb = pos0 & ~15ull; wb < end; wb += 512) {
       if (lane < 4 && wb + 1024 + 128 * lane < end) prefetch_l2(a.stream + wb + 1024 + 128 * lane);
       const uint64_t lb = wb + 16 * lane;  // this lane's first byte
-      uint32_t x[4] = {0u, 0u, 0u, 0u};
-      if (lb < end) {
-        const uint4 q = __ldg(reinterpret_cast<const uint4*>(a.stream + lb));
-        x[0] = q.x;
-        x[1] = q.y;
-        x[2] = q.z;
-        x[3] = q.w;
-      }
+      uint32_t x[4] = {qn.x, qn.y, qn.z, qn.w};
+      qn = make_uint4(0u, 0u, 0u, 0u);
+      if (lb + 512 < end) qn = __ldg(reinterpret_cast<const uint4*>(a.stream + lb + 512));
       // valid-byte flags (0x80 per byte in [pos0, end)); invalid bytes -> 0x00
       uint32_t vm[4];
 #pragma unroll
@@ -311,8 +310,10 @@ struct UCfg {
   static constexpr bool KWAY = KWAY_;
   static constexpr bool OR = OR_;
 };
+// U rows in flight per lane: 8 (a batch of 8 * SUB ids), at most one 128-id
+// decode window per batch -- p=4/5 (32 rows per warp step) take 4 per lane.
 template <int P>
-using DefaultCfg = UCfg<((32 / Geo<P>::SUB) < 8 ? (32 / Geo<P>::SUB) : 8), false, 4, false, true>;
+using DefaultCfg = UCfg<((128 / Geo<P>::SUB) < 8 ? (128 / Geo<P>::SUB) : 8), false, 4, false, true>;
 
 // Per-warp id feeder: decodes one 128-byte window of the item's LEB128 stream
 // at a time (decode_step4) into a shared buffer (compacted; tail padded with
@@ -603,6 +604,21 @@ constexpr int GW = GW_IDS / 32;         // bitmap words per node (= threads per 
 constexpr int GBLK = 2 * GN - 2;        // non-root blocks: 16 leaves, 8 pairs, 4 quads, 2 octets
 constexpr unsigned GMIN_EDGES_PER_WINDOW = 1024;
 
+// Instrumented build only (make stats, -DSB_GROUP_STATS): per-phase cycles and
+// work counts of the group path, summed over warps (scripts/group_stats.py).
+#ifdef SB_GROUP_STATS
+__device__ unsigned long long g_group_stats[16];
+#define SB_ST_DECL unsigned long long stc[16] = {}; long long stt = clock64();
+#define SB_ST_ADD(i, v) stc[i] += (v)
+#define SB_ST_LAP(i) do { const long long t_ = clock64(); stc[i] += t_ - stt; stt = t_; } while (0)
+#define SB_ST_FLUSH() do { if (lane == 0) for (int i_ = 0; i_ < 16; ++i_) atomicAdd(&g_group_stats[i_], stc[i_]); } while (0)
+#else
+#define SB_ST_DECL
+#define SB_ST_ADD(i, v) do { } while (0)
+#define SB_ST_LAP(i) do { } while (0)
+#define SB_ST_FLUSH() do { } while (0)
+#endif
+
 struct GroupSmem {
   uint32_t bm[GN][GW];          // membership bitmaps of the window
   uint32_t A[GN - 1][GW];       // block ANDs: pairs 0..7, quads 8..11, octets 12..13, root 14
@@ -705,8 +721,9 @@ struct RowPos {
 // the next window.
 template <bool SKIP>
 __device__ __forceinline__ uint32_t decode_to_bitmap(const UnionArgs& a, RowPos& c, uint32_t B, uint32_t* bm,
-                                                     int lane) {
+                                                     int lane, unsigned& steps) {
   while (c.pos < c.end) {
+    ++steps;
     const uint8_t* al = a.stream + (c.pos & ~3ull) + 4 * lane;
     const uint32_t w0 = ld_stream_word(al);
     const uint32_t w1 = ld_stream_word(al + 4);
@@ -935,8 +952,10 @@ __device__ __forceinline__ void process_group16(const UnionArgs& a, uint32_t g0,
   Grp all = grp_zero();  // this warp's share of the root
   int bfirst, bcount;
   owned_blocks(warp, bfirst, bcount);
+  SB_ST_DECL
   __syncthreads();
   for (int r = 0;; ++r) {
+    SB_ST_ADD(0, 1);
     uint32_t B = 0xffffffffu;
 #pragma unroll
     for (int k = 0; k < GN; ++k) B = min(B, S.next[r & 1][k]);
@@ -953,7 +972,9 @@ __device__ __forceinline__ void process_group16(const UnionArgs& a, uint32_t g0,
       uint32_t nx = S.next[r & 1][k];
       if (nx - B < static_cast<uint32_t>(GW_IDS)) {
         RowPos c{S.pos[k], S.end[k], S.base[k]};
-        nx = decode_to_bitmap<SKIP>(a, c, B, bm, lane);
+        unsigned steps = 0;
+        nx = decode_to_bitmap<SKIP>(a, c, B, bm, lane, steps);
+        SB_ST_ADD(1, steps);
         __syncwarp();
         if (lane == 0) {
           S.pos[k] = c.pos;
@@ -962,7 +983,9 @@ __device__ __forceinline__ void process_group16(const UnionArgs& a, uint32_t g0,
       }
       if (lane == 0) S.next[(r + 1) & 1][k] = nx;
     }
+    SB_ST_LAP(8);
     __syncthreads();
+    SB_ST_LAP(9);
     // B0: block ANDs of word j = threadIdx.x (nodes without neighbours hold every id)
     {
       const int j = threadIdx.x;
@@ -988,7 +1011,9 @@ __device__ __forceinline__ void process_group16(const UnionArgs& a, uint32_t g0,
       S.rpre[j] = incl;
       if (lane == 31) S.rsum[warp] = incl;
     }
+    SB_ST_LAP(10);
     __syncthreads();
+    SB_ST_LAP(11);
     // B1: this warp's eighth of the root ids, then the owned blocks' covers
     if constexpr (G::SUB == 1) {
       // split by id count (root ids cluster in runs, so equal word ranges would not balance)
@@ -1040,10 +1065,12 @@ __device__ __forceinline__ void process_group16(const UnionArgs& a, uint32_t g0,
           }
         }
         if (qn) fold_queue<P, C, 8>(all, qv, qn, curb);
+        SB_ST_ADD(2, hi - lo);
       }
     } else {
       fold_bits<P, C>(all, S.A[14] + 32 * warp, 32, B + 32u * 32u * warp, curb, sub);
     }
+    SB_ST_LAP(12);
     for (int bi = 0; bi < bcount; ++bi) {
       const int b = bfirst + bi;
       if (!(act & block_nodes(b))) continue;  // no node of this block has neighbours
@@ -1064,6 +1091,7 @@ __device__ __forceinline__ void process_group16(const UnionArgs& a, uint32_t g0,
           uint32_t cw = __shfl_sync(FULL, cword, src);
           const uint32_t id0 = B + 32u * (j0 + src);
           if constexpr (G::SUB == 1) {
+            SB_ST_ADD(3, __popc(cw));
             if (cw == 0xffffffffu) {
               fold_word_rows<P, C>(acc, cw, id0, curb);
               continue;
@@ -1084,8 +1112,11 @@ __device__ __forceinline__ void process_group16(const UnionArgs& a, uint32_t g0,
       }
       if (G::SUB == 1 && qn) fold_queue<P, C, 8>(acc, qv, qn, curb);
       if (touched) S.blk[b][lane] = grp_u4(acc);
+      SB_ST_ADD(4, 1);
     }
+    SB_ST_LAP(13);
     __syncthreads();  // bitmaps and block ANDs are rewritten by the next window
+    SB_ST_LAP(14);
   }
   // node k = max(cur[k], root partials, its leaf / pair / quad / octet)
   S.root[warp][lane] = grp_u4(all);
@@ -1112,6 +1143,9 @@ __device__ __forceinline__ void process_group16(const UnionArgs& a, uint32_t g0,
     }
     publish_row<P>(a, curb, a.next + goff + v * G::ROW, goff, v, acc, lane);
   }
+  SB_ST_LAP(15);
+  SB_ST_ADD(5, 1);
+  SB_ST_FLUSH();
 }
 
 // Group decision (warp 0) for the 16-node group at g0: the shared path iff >= 2
@@ -1149,13 +1183,15 @@ __device__ __forceinline__ bool upload_failed(const UnionArgs& a) {
 //              nodes see almost the same neighbour ids at the same stream
 //              position, so the CTA's 8 warps re-read each row from L1
 //              instead of L2.
-template <int P, bool SKIP, class C>
+template <int P, bool SKIP, class C, bool GRP>
 constexpr size_t union_smem_bytes() {
   constexpr size_t ids = sizeof(uint32_t) * 8 * Feeder<P, SKIP, C::U>::BUF;
-  return ids > sizeof(GroupSmem) ? ids : sizeof(GroupSmem);
+  return GRP && sizeof(GroupSmem) > ids ? sizeof(GroupSmem) : ids;
 }
 
-template <int P, bool SKIP, bool TILE, class C = DefaultCfg<P>>
+// GRP: the 16-node group path is compiled in (launched when the graph's
+// node_lo is set); without it the per-node item path keeps its registers.
+template <int P, bool SKIP, bool TILE, class C = DefaultCfg<P>, bool GRP = true>
 __global__ void __launch_bounds__(256, C::MINB) union_kernel(UnionArgs a) {
   using G = Geo<P>;
   extern __shared__ __align__(16) unsigned char smem[];  // per-node feeders or the group path
@@ -1183,7 +1219,7 @@ __global__ void __launch_bounds__(256, C::MINB) union_kernel(UnionArgs a) {
       const uint64_t t = u / G::SLICES;
       const uint32_t g0 = a.tile_node0[t];
       const uint32_t q = a.tile_q[t];
-      if (a.node_lo) {  // 16-node group path when the group's rows overlap densely
+      if (GRP && a.node_lo) {  // 16-node group path when the group's rows overlap densely
         const uint32_t g16 = g0 & ~15u;
         if (warp == 0) {
           const uint32_t m = group_mode16(a, g16, lane);
@@ -1243,26 +1279,25 @@ __global__ void __launch_bounds__(256, FILL ? 2 : 3) run_index_kernel(RunIndexAr
   const uint32_t ltm = (1u << lane) - 1u;
   const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = (gridDim.x * (uint64_t)blockDim.x) >> 5;
-  for (uint64_t item = gw; item < a.n_items; item += nw) {
+  for (uint64_t item = a.item_begin + gw; item < a.item_end; item += nw) {
+    // a malformed upload: its items' offsets are not trustworthy addresses
+    if (a.err && *reinterpret_cast<const volatile unsigned long long*>(a.err) != ~0ull) break;
     const uint64_t pos0 = a.item_off[item];
-    const uint64_t end = item + 1 < a.n_items ? a.item_off[item + 1] : a.stream_len;
+    const uint64_t end = item + 1 < a.item_end ? a.item_off[item + 1] : a.range_end_byte;
     const uint64_t out = FILL ? a.run_off[item] : 0;
     uint32_t id_before = a.item_base[item];  // warp-uniform: id after the previous window
     uint32_t nruns = 0;                       // warp-uniform: runs started so far
     uint32_t open_start = 0;                  // first id of the open run
     uint32_t longest = 0;
     uint32_t c3 = 0, ctail = 0;               // previous window's lane 31: word 3, trailing chain value
+    uint4 qn = make_uint4(0u, 0u, 0u, 0u);  // next window in flight (as in build_items_kernel)
+    if ((pos0 & ~15ull) + 16 * lane < end) qn = __ldg(reinterpret_cast<const uint4*>(a.stream + (pos0 & ~15ull) + 16 * lane));
     for (uint64_t wb = pos0 & ~15ull; wb < end; wb += 512) {
       if (lane < 4 && wb + 1024 + 128 * lane < end) prefetch_l2(a.stream + wb + 1024 + 128 * lane);
       const uint64_t lb = wb + 16 * lane;
-      uint32_t x[4] = {0u, 0u, 0u, 0u};
-      if (lb < end) {
-        const uint4 q = __ldg(reinterpret_cast<const uint4*>(a.stream + lb));
-        x[0] = q.x;
-        x[1] = q.y;
-        x[2] = q.z;
-        x[3] = q.w;
-      }
+      uint32_t x[4] = {qn.x, qn.y, qn.z, qn.w};
+      qn = make_uint4(0u, 0u, 0u, 0u);
+      if (lb + 512 < end) qn = __ldg(reinterpret_cast<const uint4*>(a.stream + lb + 512));
       uint32_t T[4], D[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
@@ -1815,11 +1850,16 @@ static int prep_union(const void* fn, size_t smem) {
 
 cudaError_t launch_union(int p, bool skip, const UnionArgs& a, cudaStream_t s) {
   const bool tile = a.n_tiles != 0;
-#define SB_UL(P, SK, TL)                                                                          \
-  {                                                                                               \
-    constexpr size_t sm = union_smem_bytes<P, SK, DefaultCfg<P>>();                               \
-    static int g = prep_union(reinterpret_cast<const void*>(union_kernel<P, SK, TL>), sm);        \
-    union_kernel<P, SK, TL><<<g, 256, sm, s>>>(a);                                                \
+#define SB_UG(P, SK, TL, GR)                                                                                 \
+  {                                                                                                          \
+    constexpr size_t sm = union_smem_bytes<P, SK, DefaultCfg<P>, GR>();                                      \
+    static int g = prep_union(reinterpret_cast<const void*>(union_kernel<P, SK, TL, DefaultCfg<P>, GR>), sm); \
+    union_kernel<P, SK, TL, DefaultCfg<P>, GR><<<g, 256, sm, s>>>(a);                                        \
+  }
+#define SB_UL(P, SK, TL)                      \
+  {                                           \
+    if (TL && a.node_lo) SB_UG(P, SK, TL, true) \
+    else SB_UG(P, SK, TL, false)              \
   }
 #define SB_L(P)                                                     \
   {                                                                 \
@@ -1894,7 +1934,7 @@ using OrCfg = UCfg<8, false, 4, false, false, true>;
 cudaError_t launch_union_or(int p, const UnionArgs& a, cudaStream_t s) {
 #define SB_LO(P)                                                                                         \
   {                                                                                                      \
-    constexpr size_t sm = union_smem_bytes<P, false, OrCfg<P>>();                                        \
+    constexpr size_t sm = union_smem_bytes<P, false, OrCfg<P>, true>();                                  \
     static int g = prep_union(reinterpret_cast<const void*>(union_kernel<P, false, true, OrCfg<P>>), sm); \
     union_kernel<P, false, true, OrCfg<P>><<<g, 256, sm, s>>>(a);                                       \
     break;                                                                                               \
@@ -2021,6 +2061,18 @@ cudaError_t launch_from_packed(int p, const uint8_t* packed, uint8_t* bits, uint
 #undef SB_L
   return cudaGetLastError();
 }
+
+#ifdef SB_GROUP_STATS
+extern "C" int sb_debug_group_stats(unsigned long long* out16, int reset) {
+  cudaDeviceSynchronize();
+  if (cudaMemcpyFromSymbol(out16, g_group_stats, sizeof(unsigned long long) * 16) != cudaSuccess) return 3;
+  if (reset) {
+    static const unsigned long long zero[16] = {};
+    cudaMemcpyToSymbol(g_group_stats, zero, sizeof(zero));
+  }
+  return 0;
+}
+#endif
 
 cudaError_t launch_metrics(const MetricArgs& a, cudaStream_t s) {
   const int g = static_cast<int>(a.n / 256 + 1 < 65535 ? a.n / 256 + 1 : 65535);

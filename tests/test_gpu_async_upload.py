@@ -94,3 +94,20 @@ def test_async_upload_reports_malformed_stream(bad):
     ref = HyperBall(ok, 10, None)
     ref.run()
     assert np.array_equal(h.registers(), ref.registers())
+
+
+@pytest.mark.parametrize("bad", [_cut_row(1600, 1500, 1000, "zero"), _cut_row(1600, 1500, 700, "huge")],
+                         ids=["cut_zero", "cut_huge"])
+def test_async_upload_interval_malformed_stream(bad):
+    """Interval mode counts the run index per upload chunk while the copies are
+    still in flight; a malformed chunk stops the count kernels (they never follow
+    its item offsets) and surfaces as RuntimeError at create."""
+    g = _raw(*bad)
+    with pytest.raises(RuntimeError):
+        HyperBall(DeviceGraph(g, async_upload=True), 10, None, interval=True)
+    ok = CompressedCsr.synth_grid(40, 40, 6, 2, 5, 11, 0)
+    h = HyperBall(DeviceGraph(ok, async_upload=True), 10, None, interval=True)
+    h.run()
+    ref = HyperBall(ok, 10, None)
+    ref.run()
+    assert np.array_equal(h.registers(), ref.registers())
