@@ -242,7 +242,8 @@ __device__ __forceinline__ Decode4 decode_step4(const uint8_t* __restrict__ stre
     for (int k = 0; k < 4; ++k)
       if (want[k]) buf[slot++] = id[k];
     o.count = o.wanted;
-    if (lane < PAD) buf[o.wanted + lane] = o.last;
+#pragma unroll
+    for (int k = lane; k < PAD; k += 32) buf[o.wanted + k] = o.last;
     return o;
   }
   bool keep[4];
@@ -270,7 +271,8 @@ __device__ __forceinline__ Decode4 decode_step4(const uint8_t* __restrict__ stre
     const int KL = 31 - __clz(anyk);
     const int kk = __shfl_sync(FULL, hk, KL);
     const uint32_t lastkept = __shfl_sync(FULL, sel4(id, kk), KL);
-    if (lane < PAD) buf[kn + lane] = lastkept;
+#pragma unroll
+    for (int k = lane; k < PAD; k += 32) buf[kn + k] = lastkept;
   }
   return o;
 }

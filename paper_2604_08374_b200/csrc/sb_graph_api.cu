@@ -290,9 +290,10 @@ static int graph_create(uint64_t n, const uint64_t* offsets, const uint32_t* deg
     cudaError_t e_ = (x);                                     \
     if (e_ != cudaSuccess) return bail(cuda_fail(e_, #x));    \
   } while (0)
-  // 256 B of zero padding: the decoder reads whole 128-byte windows (+8 for alignment).
-  GK(dalloc(&g->d_stream, g->stream_local + 256));
-  GK(cudaMemset(g->d_stream + g->stream_local, 0, 256));
+  // zero padding: the decoders read whole windows past a row's end (512-byte
+  // steps + the next lane's word + alignment)
+  GK(dalloc(&g->d_stream, g->stream_local + sb::kStreamPad));
+  GK(cudaMemset(g->d_stream + g->stream_local, 0, sb::kStreamPad));
   if (g->stream_local && !async)
     GK(cudaMemcpy(g->d_stream, stream + b0, g->stream_local, cudaMemcpyHostToDevice));
   std::vector<uint64_t> ro(g->n_local + 1);
@@ -475,8 +476,8 @@ int sb_graph_build_grid(uint32_t rows, uint32_t cols, const uint8_t* blocked, ui
   uint64_t total = 0;
   BK(cudaMemcpy(&total, g->d_rowoff + n, 8, cudaMemcpyDeviceToHost));
   g->stream_local = total;
-  BK(dalloc(&g->d_stream, total + 256));
-  BK(cudaMemsetAsync(g->d_stream + total, 0, 256, s));
+  BK(dalloc(&g->d_stream, total + sb::kStreamPad));
+  BK(cudaMemsetAsync(g->d_stream + total, 0, sb::kStreamPad, s));
   a.offsets = g->d_rowoff;
   a.stream = g->d_stream;
   BK(sb::launch_vis_rows(a, true, s));

@@ -23,6 +23,10 @@ struct BuildArgs {
   unsigned long long* err_node;  // min local node with a malformed row (~0 = none)
 };
 
+// Zero bytes after every device stream slice: the decoders read whole windows
+// past a row's end (decode16_to_bitmap: 512 bytes + 4 + alignment).
+constexpr uint64_t kStreamPad = 1024;
+
 struct UnionArgs {
   const uint8_t* stream;
   const uint64_t* item_off;

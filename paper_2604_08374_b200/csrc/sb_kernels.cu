@@ -815,6 +815,108 @@ __device__ __forceinline__ uint32_t decode_to_bitmap(const UnionArgs& a, RowPos&
   return 0xffffffffu;
 }
 
+// Same contract as decode_to_bitmap, 512 bytes per step (16 per lane): the
+// per-step costs -- the warp prefix sum, the votes, the cursor update -- are
+// paid once per 512 bytes instead of once per 128.  Every in-window id sets
+// its bit with its own shared atomicOr (lanes 16 ids apart: 2-way conflicts).
+template <bool SKIP>
+__device__ __forceinline__ uint32_t decode16_to_bitmap(const UnionArgs& a, RowPos& c, uint32_t B, uint32_t* bm,
+                                                       int lane, unsigned& steps) {
+  while (c.pos < c.end) {
+    ++steps;
+    // this lane's 16 bytes [pos + 16 lane, +16): 4 aligned words + the next lane's first
+    const uint8_t* al = a.stream + (c.pos & ~3ull) + 16 * lane;
+    uint32_t A[5];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) A[i] = ld_stream_word(al + 4 * i);
+    A[4] = __shfl_down_sync(FULL, A[0], 1);
+    if (lane == 31) A[4] = ld_stream_word(al + 16);
+    const uint32_t sh = static_cast<uint32_t>(c.pos & 3) * 8;
+    uint32_t x[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) x[i] = __funnelshift_r(A[i], A[i + 1], sh);
+    uint32_t prev = __shfl_up_sync(FULL, x[3], 1);
+    if (lane == 0) prev = 0;  // the cursor sits on a varint boundary
+    // per byte: payload << 7 * (continuation bytes just before it, <= 4)
+    uint32_t cb[16];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t w = x[i], wp = i ? x[i - 1] : prev;
+      const uint32_t F = w & 0x80808080u, Fp = wp & 0x80808080u;
+      const uint32_t m1 = __funnelshift_l(Fp, F, 8);
+      const uint32_t m2 = m1 & __funnelshift_l(Fp, F, 16);
+      const uint32_t m3 = m2 & __funnelshift_l(Fp, F, 24);
+      const uint32_t m4 = m3 & Fp;
+      const uint32_t D = (m1 >> 7) + (m2 >> 7) + (m3 >> 7) + (m4 >> 7);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) cb[4 * i + k] = ((w >> (8 * k)) & 0x7fu) << (7 * ((D >> (8 * k)) & 0xffu));
+    }
+    uint32_t pre[16];
+    pre[0] = cb[0];
+#pragma unroll
+    for (int j = 1; j < 16; ++j) pre[j] = pre[j - 1] + cb[j];
+    const uint32_t lane_sum = pre[15];
+    uint32_t incl = lane_sum;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(FULL, incl, d);
+      if (lane >= d) incl += y;
+    }
+    const uint32_t excl = c.base + incl - lane_sum;
+    // terminators of this row (bytes before its end), 16-bit mask
+    const int64_t left = static_cast<int64_t>(c.end) - static_cast<int64_t>(c.pos + 16 * lane);
+    uint32_t tm = 0u;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t T = ~x[i] & 0x80808080u;
+      tm |= ((T >> 7) & 1u | (T >> 14) & 2u | (T >> 21) & 4u | (T >> 28) & 8u) << (4 * i);
+    }
+    tm &= left >= 16 ? 0xffffu : left <= 0 ? 0u : (1u << left) - 1u;
+    // in-window terminators: all of them unless the window ends inside this step
+    uint32_t inm = tm;
+    if (!__all_sync(FULL, excl + lane_sum - B < static_cast<uint32_t>(GW_IDS))) {
+      inm = 0u;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) inm |= (excl + pre[j] - B < static_cast<uint32_t>(GW_IDS) ? 1u : 0u) << j;
+      inm &= tm;
+    }
+    const uint32_t outm = tm & ~inm;
+    // bitmap bits, last in-window id, first out-of-window id
+    uint32_t last_in = 0u, first_out = 0u;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const uint32_t idj = excl + pre[j];
+      if ((inm >> j) & 1u) {
+        bool keep = true;
+        if (SKIP) keep = a.changed_in[idj] != 0;
+        const uint32_t off = idj - B;
+        if (keep) atomicOr(bm + (off >> 5), 1u << (off & 31));
+        last_in = idj;
+      }
+    }
+#pragma unroll
+    for (int j = 15; j >= 0; --j)
+      if ((outm >> j) & 1u) first_out = excl + pre[j];
+    const uint32_t anyin = __ballot_sync(FULL, inm != 0u);
+    const uint32_t anyout = __ballot_sync(FULL, outm != 0u);
+    if (anyin) {  // advance past the last in-window terminator
+      const int L = 31 - __clz(anyin);
+      const int lk = 31 - __clz(__shfl_sync(FULL, inm, L));
+      c.base = __shfl_sync(FULL, last_in, L);
+      c.pos += 16 * L + lk + 1;
+    }
+    if (anyout) {
+      if (lane < 16) prefetch_l2(a.stream + c.pos + 128 * lane);
+      return __shfl_sync(FULL, first_out, __ffs(anyout) - 1);
+    }
+    if (!anyin) {  // unreachable on a validated stream (a step always holds a terminator)
+      c.pos = c.end;
+      break;
+    }
+  }
+  return 0xffffffffu;
+}
+
 // acc <- max(acc, rows of the set bits of the warp-uniform word cw): ids
 // id0 + bit.  p >= 10 (one row slice per warp step): the set bits are taken 4
 // at a time (one 4-row bit-serial max, 8 LOP3 per row also for sparse words);
@@ -973,7 +1075,7 @@ __device__ __forceinline__ void process_group16(const UnionArgs& a, uint32_t g0,
       if (nx - B < static_cast<uint32_t>(GW_IDS)) {
         RowPos c{S.pos[k], S.end[k], S.base[k]};
         unsigned steps = 0;
-        nx = decode_to_bitmap<SKIP>(a, c, B, bm, lane, steps);
+        nx = decode16_to_bitmap<SKIP>(a, c, B, bm, lane, steps);
         SB_ST_ADD(1, steps);
         __syncwarp();
         if (lane == 0) {

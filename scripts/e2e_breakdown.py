@@ -1,4 +1,5 @@
-"""Phase breakdown of the end-to-end C-ABI path on C3 (host CSR -> HBM -> run -> read-back)."""
+"""Phase breakdown of the end-to-end C-ABI path on C3 (host CSR -> HBM -> run -> read-back),
+dense (sync / async upload) and interval (async upload: the run index is counted per upload chunk)."""
 import os
 import sys
 import time
@@ -12,17 +13,19 @@ from paper_2604_08374_b200 import DeviceGraph, HllParams, HyperBall  # noqa: E40
 g = build_graph("c3")
 g.pin(True)
 P = HllParams(10)
-for rep in range(6):
+for rep in range(9):
+    interval = rep >= 6
     t0 = time.perf_counter()
     dg = DeviceGraph(g, 0, async_upload=rep >= 3)
     t1 = time.perf_counter()
-    h = HyperBall(dg, P, None)
+    h = HyperBall(dg, P, None, interval=interval)
     t2 = time.perf_counter()
     it = h.run()
     t3 = time.perf_counter()
     s = h.state()
     torch.cuda.synchronize()
     t4 = time.perf_counter()
-    print(f"rep {rep}: graph_create {t1 - t0:.3f} s, hb_create {t2 - t1:.3f} s, run {t3 - t2:.3f} s ({it} it), "
-          f"read_state {t4 - t3:.3f} s, total {t4 - t0:.3f} s", flush=True)
+    mode = "interval async" if interval else ("dense async" if rep >= 3 else "dense sync")
+    print(f"rep {rep} ({mode}): graph_create {t1 - t0:.3f} s, hb_create {t2 - t1:.3f} s, run {t3 - t2:.3f} s "
+          f"({it} it), read_state {t4 - t3:.3f} s, total {t4 - t0:.3f} s", flush=True)
     del h, dg, s

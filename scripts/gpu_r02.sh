@@ -57,6 +57,21 @@ if [[ $what == dist || $what == all ]]; then
       --master-port 29533 bench.py --gpus 2 --config c3 --steps 3 --warmup 3 --no-cpu --no-variants --no-pipeline \
       > gpurun_out/bench_c3_w2_shared.json 2> gpurun_out/bench_c3_w2_shared.log
 fi
+if [[ $what == stats ]]; then
+  for c in "c3 10" "c2 10"; do
+    SB_LIBRARY=paper_2604_08374_b200/libsieveball_cuda_stats.so timeout 600 python -u scripts/group_stats.py $c \
+        >> gpurun_out/group_stats.txt 2>&1
+  done
+fi
+if [[ $what == async ]]; then
+  run timeout 900 python -u -m pytest tests/test_gpu_async_upload.py -q -x > gpurun_out/pytest_async.log 2>&1; tail -2 gpurun_out/pytest_async.log
+fi
+if [[ $what == setup ]]; then
+  # setup kernels (validation/work items at upload, run index) and the interval end to end
+  run timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+      --log-file gpurun_out/launches_pipeline.csv python -u scripts/pipeline_profile.py c3
+  run timeout 600 python -u scripts/e2e_breakdown.py > gpurun_out/e2e_breakdown.txt 2>&1
+fi
 if [[ $what == sweeps || $what == all ]]; then
   run timeout 900 python -u scripts/sweep.py > gpurun_out/sweeps.json 2> gpurun_out/sweeps.log
 fi
