@@ -626,6 +626,7 @@ struct GroupSmem {
   uint4 root[8][32];            // per-warp root partials (end of group)
   uint32_t rpre[GW];            // root bits: inclusive popcount prefix within each 32-word block
   uint32_t rsum[8];             // root bits per 32-word block
+  uint32_t unit;                // B1 work-unit counter of the window
   uint32_t next[2][GN];         // next undecoded id per node (~0: row exhausted)
   unsigned long long pos[GN], end[GN];  // row cursors: next byte, row end, last id
   uint32_t base[GN];
@@ -1003,12 +1004,15 @@ __device__ __forceinline__ uint32_t rank_range(uint32_t w, uint32_t r0, uint32_t
   return w;
 }
 
-// Non-root blocks by owner warp, balanced per tree level: warps 0/1 the octets,
-// 2/3 two quads each, 4/5 four pairs each, 6/7 eight leaves each.
-__device__ __forceinline__ void owned_blocks(int warp, int& first, int& count) {
-  const int level = warp >> 1;            // 0 octets, 1 quads, 2 pairs, 3 leaves
-  count = 1 << level;
-  first = 32 - (4 << level) + (warp & 1) * count;
+// B1 work units, taken by the warps from a shared counter in this order: the
+// 30 non-root blocks coarse levels first (octets 28..29, quads 24..27, pairs
+// 16..23, leaves 0..15; one warp per block, which owns its accumulator for the
+// window), then GRC slices of the root ids of equal size.  Cover sizes differ
+// per block and window, so a static split leaves warps idle at the window's
+// closing barrier (ncu: 22 % of the stall samples there with 8 fixed shares).
+constexpr int GRC = 16;
+__device__ __forceinline__ int unit_block(int u) {
+  return u < 2 ? 28 + u : u < 6 ? 24 + (u - 2) : u < 14 ? 16 + (u - 6) : u - 14;
 }
 
 // Node mask of block b (leaves 0..15, pairs 16..23, quads 24..27, octets 28..29).
@@ -1052,8 +1056,6 @@ __device__ __forceinline__ void process_group16(const UnionArgs& a, uint32_t g0,
   }
   for (int i = threadIdx.x; i < GBLK * 32; i += blockDim.x) (&S.blk[0][0])[i] = make_uint4(0u, 0u, 0u, 0u);
   Grp all = grp_zero();  // this warp's share of the root
-  int bfirst, bcount;
-  owned_blocks(warp, bfirst, bcount);
   SB_ST_DECL
   __syncthreads();
   for (int r = 0;; ++r) {
@@ -1112,111 +1114,127 @@ __device__ __forceinline__ void process_group16(const UnionArgs& a, uint32_t g0,
       }
       S.rpre[j] = incl;
       if (lane == 31) S.rsum[warp] = incl;
+      if (j == 0) S.unit = 0u;
     }
     SB_ST_LAP(10);
     __syncthreads();
     SB_ST_LAP(11);
-    // B1: this warp's eighth of the root ids, then the owned blocks' covers
-    if constexpr (G::SUB == 1) {
-      // split by id count (root ids cluster in runs, so equal word ranges would not balance)
-      uint32_t bs = lane < 8 ? S.rsum[lane] : 0u, bincl = bs;
+    // B1: work units from the shared counter (blocks, then root slices)
+    {
+      uint32_t bs = 0u, bincl = 0u, total = 0u;
+      if constexpr (G::SUB == 1) {
+        bs = lane < 8 ? S.rsum[lane] : 0u;
+        bincl = bs;
 #pragma unroll
-      for (int d = 1; d < 8; d <<= 1) {
-        const uint32_t y = __shfl_up_sync(FULL, bincl, d);
-        if (lane >= d) bincl += y;
+        for (int d = 1; d < 8; d <<= 1) {
+          const uint32_t y = __shfl_up_sync(FULL, bincl, d);
+          if (lane >= d) bincl += y;
+        }
+        total = __shfl_sync(FULL, bincl, 7);
       }
-      const uint32_t total = __shfl_sync(FULL, bincl, 7);
-      const uint32_t lo = static_cast<uint32_t>((static_cast<uint64_t>(total) * warp) >> 3);
-      const uint32_t hi = static_cast<uint32_t>((static_cast<uint64_t>(total) * (warp + 1)) >> 3);
-      if (lo < hi) {
-        // first word whose inclusive prefix exceeds x: the block by a ballot over
-        // the 8 block sums, the word by a ballot inside the block
-        auto locate = [&](uint32_t x, uint32_t& excl) -> int {
-          const int blk = __ffs(__ballot_sync(FULL, lane < 8 && bincl > x)) - 1;
-          const uint32_t bex = __shfl_sync(FULL, bincl - bs, blk);
-          const int jw = __ffs(__ballot_sync(FULL, bex + S.rpre[32 * blk + lane] > x)) - 1;
-          const int jj = 32 * blk + jw;
-          excl = bex + S.rpre[jj] - __popc(S.A[14][jj]);
-          return jj;
-        };
-        uint32_t ex0, ex1;
-        const int j0 = locate(lo, ex0), j1 = locate(hi - 1, ex1);
-        // full words: 4 unconditional 8-row batches; the bits of partial words
-        // (run ends) are queued across words and folded 8 at a time
+      constexpr int NRC = G::SUB == 1 ? GRC : 8;  // root slices (p < 10: 8 ranges of 32 words)
+      for (;;) {
+        uint32_t u = 0u;
+        if (lane == 0) u = atomicAdd(&S.unit, 1u);
+        u = __shfl_sync(FULL, u, 0);
+        if (u >= static_cast<uint32_t>(GBLK + NRC)) break;
+        if (u >= static_cast<uint32_t>(GBLK)) {
+          const int c = static_cast<int>(u) - GBLK;
+          if constexpr (G::SUB == 1) {
+            // root slice c of equal id count (root ids cluster in runs, so equal
+            // word ranges would not balance)
+            const uint32_t lo = static_cast<uint32_t>((static_cast<uint64_t>(total) * c) / NRC);
+            const uint32_t hi = static_cast<uint32_t>((static_cast<uint64_t>(total) * (c + 1)) / NRC);
+            if (lo < hi) {
+              // first word whose inclusive prefix exceeds x: the block by a ballot over
+              // the 8 block sums, the word by a ballot inside the block
+              auto locate = [&](uint32_t x, uint32_t& excl) -> int {
+                const int blk = __ffs(__ballot_sync(FULL, lane < 8 && bincl > x)) - 1;
+                const uint32_t bex = __shfl_sync(FULL, bincl - bs, blk);
+                const int jw = __ffs(__ballot_sync(FULL, bex + S.rpre[32 * blk + lane] > x)) - 1;
+                const int jj = 32 * blk + jw;
+                excl = bex + S.rpre[jj] - __popc(S.A[14][jj]);
+                return jj;
+              };
+              uint32_t ex0, ex1;
+              const int j0 = locate(lo, ex0), j1 = locate(hi - 1, ex1);
+              // full words: 4 unconditional 8-row batches; the bits of partial words
+              // (run ends) are queued across words and folded 8 at a time
+              uint32_t qv = 0u;
+              int qn = 0;
+#pragma unroll 1
+              for (int j = j0; j <= j1; ++j) {
+                uint32_t w = S.A[14][j];
+                if (j == j0 || j == j1) {
+                  const uint32_t ex = j == j0 ? ex0 : ex1;
+                  w = rank_range(w, j == j0 ? lo - ex : 0u, j == j1 ? hi - ex : 32u);
+                }
+                if (w == 0xffffffffu) {
+                  fold_word_rows<P, C>(all, w, B + 32u * j, curb);
+                  continue;
+                }
+                while (w) {
+                  const int bp = __ffs(w) - 1;
+                  w &= w - 1u;
+                  if (lane == qn) qv = B + 32u * j + bp;
+                  if (++qn == 8) {
+                    fold_queue<P, C, 8>(all, qv, 8, curb);
+                    qn = 0;
+                  }
+                }
+              }
+              if (qn) fold_queue<P, C, 8>(all, qv, qn, curb);
+              SB_ST_ADD(2, hi - lo);
+            }
+          } else {
+            fold_bits<P, C>(all, S.A[14] + 32 * c, 32, B + 32u * 32u * c, curb, sub);
+          }
+          continue;
+        }
+        const int b = unit_block(static_cast<int>(u));
+        if (!(act & block_nodes(b))) continue;  // no node of this block has neighbours
+        Grp acc = u4_grp(S.blk[b][lane]);
+        bool touched = false;
+        // p >= 10: the cover's ids are sparse (the rims of the disks), so they are
+        // queued across words -- lane q holds queued id q -- and folded 8 at a time
         uint32_t qv = 0u;
         int qn = 0;
 #pragma unroll 1
-        for (int j = j0; j <= j1; ++j) {
-          uint32_t w = S.A[14][j];
-          if (j == j0 || j == j1) {
-            const uint32_t ex = j == j0 ? ex0 : ex1;
-            w = rank_range(w, j == j0 ? lo - ex : 0u, j == j1 ? hi - ex : 32u);
-          }
-          if (w == 0xffffffffu) {
-            fold_word_rows<P, C>(all, w, B + 32u * j, curb);
-            continue;
-          }
-          while (w) {
-            const int bp = __ffs(w) - 1;
-            w &= w - 1u;
-            if (lane == qn) qv = B + 32u * j + bp;
-            if (++qn == 8) {
-              fold_queue<P, C, 8>(all, qv, 8, curb);
-              qn = 0;
+        for (int j0 = 0; j0 < GW; j0 += 32) {
+          const uint32_t cword = block_cover_word(S, b, j0 + lane, act);
+          uint32_t nz = __ballot_sync(FULL, cword != 0u);
+          touched |= nz != 0u;
+          while (nz) {
+            const int src = __ffs(nz) - 1;
+            nz &= nz - 1u;
+            uint32_t cw = __shfl_sync(FULL, cword, src);
+            const uint32_t id0 = B + 32u * (j0 + src);
+            if constexpr (G::SUB == 1) {
+              SB_ST_ADD(3, __popc(cw));
+              if (cw == 0xffffffffu) {
+                fold_word_rows<P, C>(acc, cw, id0, curb);
+                continue;
+              }
+              while (cw) {
+                const int bp = __ffs(cw) - 1;
+                cw &= cw - 1u;
+                if (lane == qn) qv = id0 + bp;
+                if (++qn == 8) {
+                  fold_queue<P, C, 8>(acc, qv, 8, curb);
+                  qn = 0;
+                }
+              }
+            } else {
+              fold_set_bits<P, C>(acc, cw, id0, curb, sub);
             }
           }
         }
-        if (qn) fold_queue<P, C, 8>(all, qv, qn, curb);
-        SB_ST_ADD(2, hi - lo);
+        if (G::SUB == 1 && qn) fold_queue<P, C, 8>(acc, qv, qn, curb);
+        if (touched) S.blk[b][lane] = grp_u4(acc);
+        SB_ST_ADD(4, 1);
       }
-    } else {
-      fold_bits<P, C>(all, S.A[14] + 32 * warp, 32, B + 32u * 32u * warp, curb, sub);
     }
     SB_ST_LAP(12);
-    for (int bi = 0; bi < bcount; ++bi) {
-      const int b = bfirst + bi;
-      if (!(act & block_nodes(b))) continue;  // no node of this block has neighbours
-      Grp acc = u4_grp(S.blk[b][lane]);
-      bool touched = false;
-      // p >= 10: the cover's ids are sparse (the rims of the disks), so they are
-      // queued across words -- lane q holds queued id q -- and folded 8 at a time
-      uint32_t qv = 0u;
-      int qn = 0;
-#pragma unroll 1
-      for (int j0 = 0; j0 < GW; j0 += 32) {
-        const uint32_t cword = block_cover_word(S, b, j0 + lane, act);
-        uint32_t nz = __ballot_sync(FULL, cword != 0u);
-        touched |= nz != 0u;
-        while (nz) {
-          const int src = __ffs(nz) - 1;
-          nz &= nz - 1u;
-          uint32_t cw = __shfl_sync(FULL, cword, src);
-          const uint32_t id0 = B + 32u * (j0 + src);
-          if constexpr (G::SUB == 1) {
-            SB_ST_ADD(3, __popc(cw));
-            if (cw == 0xffffffffu) {
-              fold_word_rows<P, C>(acc, cw, id0, curb);
-              continue;
-            }
-            while (cw) {
-              const int bp = __ffs(cw) - 1;
-              cw &= cw - 1u;
-              if (lane == qn) qv = id0 + bp;
-              if (++qn == 8) {
-                fold_queue<P, C, 8>(acc, qv, 8, curb);
-                qn = 0;
-              }
-            }
-          } else {
-            fold_set_bits<P, C>(acc, cw, id0, curb, sub);
-          }
-        }
-      }
-      if (G::SUB == 1 && qn) fold_queue<P, C, 8>(acc, qv, qn, curb);
-      if (touched) S.blk[b][lane] = grp_u4(acc);
-      SB_ST_ADD(4, 1);
-    }
-    SB_ST_LAP(13);
     __syncthreads();  // bitmaps and block ANDs are rewritten by the next window
     SB_ST_LAP(14);
   }

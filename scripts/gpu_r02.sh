@@ -76,3 +76,14 @@ if [[ $what == sweeps || $what == all ]]; then
   run timeout 900 python -u scripts/sweep.py > gpurun_out/sweeps.json 2> gpurun_out/sweeps.log
 fi
 done
+for what in "$@"; do
+if [[ $what == ncusass ]]; then
+  # per-SASS-instruction executed counts and stall samples of the C3 union (kept as csv)
+  run timeout 900 $NCU -k regex:union_kernel -s 3 -c 1 -o gpurun_out/prof_sass \
+      python -u bench.py --profile --no-cpu --no-e2e --no-variants --no-pipeline
+  ncu -i gpurun_out/prof_sass.ncu-rep --page source --csv --print-source sass > gpurun_out/sass.csv 2>&1
+  ncu -i gpurun_out/prof_sass.ncu-rep --page details > gpurun_out/prof_sass_details.txt 2>&1
+  ls -la gpurun_out/prof_sass.ncu-rep
+  rm -f gpurun_out/prof_sass.ncu-rep
+fi
+done

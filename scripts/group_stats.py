@@ -32,7 +32,7 @@ hb.run()   # one union pass (depth 1)
 f(buf, 0)
 st = list(buf)
 names = {8: "A decode->bitmaps", 9: "barrier 1 wait", 10: "B0 block ANDs", 11: "barrier 2 wait",
-         12: "B1 root folds", 13: "B1 block folds", 14: "barrier 3 wait", 15: "end of group"}
+         12: "B1 folds (blocks, root slices)", 13: "(unused)", 14: "barrier 3 wait", 15: "end of group"}
 tot = sum(st[i] for i in names)
 print(f"{cfg} p={p}: groups={st[5] // 8} windows={st[0] // 8} windows/group={st[0] / max(st[5], 1):.2f} "
       f"decode steps={st[1]} root rows={st[2]} block rows={st[3]} block passes={st[4]}")
