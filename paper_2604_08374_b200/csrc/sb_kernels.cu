@@ -630,6 +630,90 @@ struct GroupSmem {
   uint32_t next[2][GN];         // next undecoded id per node (~0: row exhausted)
   unsigned long long pos[GN], end[GN];  // row cursors: next byte, row end, last id
   uint32_t base[GN];
+  alignas(16) uint32_t q[8][64];  // per-warp id queues of the B1 folds (IdQueue)
+};
+
+// Per-warp ring of queued row ids in shared memory for the sparse B1 folds
+// (p >= 10, one row slice per warp step): set bits are pushed lane-parallel --
+// a lane per bitmap word, or a lane per bit of one word -- each at its rank,
+// and folded 8 at a time (two broadcast LDS.128 for the ids, then one 9-way
+// bit-serial max).  Replaces a warp-uniform loop over the set bits (~10
+// instructions per id, 23 % of the kernel's instructions at C3).
+template <int P, class C>
+struct IdQueue {
+  uint32_t* q;          // 64 entries
+  uint32_t head, tail;  // warp-uniform; tail - head < 8 between pushes
+  const uint8_t* curb;
+
+  __device__ __forceinline__ void drain(Grp& acc) {
+    using G = Geo<P>;
+    using IO = GrpIO<G::GB>;
+    __syncwarp();
+    while (tail - head >= 8) {
+      const uint4 i0 = *reinterpret_cast<const uint4*>(q + (head & 63));
+      const uint4 i1 = *reinterpret_cast<const uint4*>(q + (head & 63) + 4);
+      const uint32_t id[8] = {i0.x, i0.y, i0.z, i0.w, i1.x, i1.y, i1.z, i1.w};
+      Grp x[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) x[k] = IO::ld(curb + static_cast<uint64_t>(id[k]) * G::ROW);
+      batch_max<C, 8>(acc, x);
+      head += 8;
+    }
+  }
+  // The last < 8 queued ids (absent rows read as 0, the identity of the max).
+  __device__ __forceinline__ void flush(Grp& acc) {
+    using G = Geo<P>;
+    using IO = GrpIO<G::GB>;
+    const uint32_t n = tail - head;
+    if (!n) return;
+    __syncwarp();
+    const uint4 i0 = *reinterpret_cast<const uint4*>(q + (head & 63));
+    const uint4 i1 = *reinterpret_cast<const uint4*>(q + (head & 63) + 4);
+    const uint32_t id[8] = {i0.x, i0.y, i0.z, i0.w, i1.x, i1.y, i1.z, i1.w};
+    Grp x[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = k < static_cast<int>(n) ? IO::ld(curb + static_cast<uint64_t>(id[k]) * G::ROW) : grp_zero();
+    batch_max<C, 8>(acc, x);
+    head = tail;
+  }
+  // One warp-uniform word w: ids id0 + bit, lane b pushes bit b.
+  __device__ __forceinline__ void push_word(Grp& acc, uint32_t w, uint32_t id0, int lane) {
+    __syncwarp();
+    if ((w >> lane) & 1u) q[(tail + __popc(w & ((1u << lane) - 1u))) & 63] = id0 + lane;
+    tail += __popc(w);
+    drain(acc);
+  }
+  // Every lane's word cw: ids idb + bit (lane-parallel when the ids fit the ring).
+  __device__ __forceinline__ void push_lanes(Grp& acc, uint32_t cw, uint32_t idb, int lane) {
+    const uint32_t n = __popc(cw);
+    uint32_t incl = n;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(FULL, incl, d);
+      if (lane >= d) incl += y;
+    }
+    const uint32_t T = __shfl_sync(FULL, incl, 31);
+    if (!T) return;
+    if (tail - head + T <= 64u) {
+      __syncwarp();
+      uint32_t pos = tail + incl - n;
+      while (cw) {
+        const int b = __ffs(cw) - 1;
+        cw &= cw - 1u;
+        q[pos & 63] = idb + b;
+        ++pos;
+      }
+      tail += T;
+      drain(acc);
+      return;
+    }
+    uint32_t nz = __ballot_sync(FULL, cw != 0u);
+    while (nz) {
+      const int src = __ffs(nz) - 1;
+      nz &= nz - 1u;
+      push_word(acc, __shfl_sync(FULL, cw, src), __shfl_sync(FULL, idb, src), lane);
+    }
+  }
 };
 
 // acc <- max(acc, rows of the candidate bits) over `nw` bitmap words: id of
@@ -980,20 +1064,6 @@ __device__ __forceinline__ void fold_word_rows(Grp& acc, uint32_t w, uint32_t id
   }
 }
 
-// acc <- max(acc, rows of the first n (<= K) queued ids; lane q holds id q).
-template <int P, class C, int K>
-__device__ __forceinline__ void fold_queue(Grp& acc, uint32_t qv, int n, const uint8_t* curb) {
-  using G = Geo<P>;
-  using IO = GrpIO<G::GB>;
-  Grp x[K];
-#pragma unroll
-  for (int q = 0; q < K; ++q) {
-    const uint32_t idq = __shfl_sync(FULL, qv, q);
-    x[q] = q < n ? IO::ld(curb + static_cast<uint64_t>(idq) * G::ROW) : grp_zero();
-  }
-  batch_max<C, K>(acc, x);
-}
-
 // Bits of w whose rank among its set bits is in [r0, r1).
 __device__ __forceinline__ uint32_t rank_range(uint32_t w, uint32_t r0, uint32_t r1) {
   if (r1 < static_cast<uint32_t>(__popc(w))) w &= (1u << __fns(w, 0, static_cast<int>(r1) + 1)) - 1u;
@@ -1158,32 +1228,23 @@ __device__ __forceinline__ void process_group16(const UnionArgs& a, uint32_t g0,
               };
               uint32_t ex0, ex1;
               const int j0 = locate(lo, ex0), j1 = locate(hi - 1, ex1);
-              // full words: 4 unconditional 8-row batches; the bits of partial words
-              // (run ends) are queued across words and folded 8 at a time
-              uint32_t qv = 0u;
-              int qn = 0;
+              // 32 words per pass, a word per lane: full words as 4 unconditional
+              // 8-row batches, the set bits of partial ones (run ends) queued
+              IdQueue<P, C> Q{S.q[warp], 0u, 0u, curb};
 #pragma unroll 1
-              for (int j = j0; j <= j1; ++j) {
-                uint32_t w = S.A[14][j];
-                if (j == j0 || j == j1) {
-                  const uint32_t ex = j == j0 ? ex0 : ex1;
-                  w = rank_range(w, j == j0 ? lo - ex : 0u, j == j1 ? hi - ex : 32u);
+              for (int jb = j0; jb <= j1; jb += 32) {
+                const int j = jb + lane;
+                uint32_t w = j <= j1 ? S.A[14][j] : 0u;
+                if (j == j0 || j == j1) w = rank_range(w, j == j0 ? lo - ex0 : 0u, j == j1 ? hi - ex1 : 32u);
+                uint32_t fm = __ballot_sync(FULL, w == 0xffffffffu);
+                while (fm) {
+                  const int src = __ffs(fm) - 1;
+                  fm &= fm - 1u;
+                  fold_word_rows<P, C>(all, 0xffffffffu, B + 32u * (jb + src), curb);
                 }
-                if (w == 0xffffffffu) {
-                  fold_word_rows<P, C>(all, w, B + 32u * j, curb);
-                  continue;
-                }
-                while (w) {
-                  const int bp = __ffs(w) - 1;
-                  w &= w - 1u;
-                  if (lane == qn) qv = B + 32u * j + bp;
-                  if (++qn == 8) {
-                    fold_queue<P, C, 8>(all, qv, 8, curb);
-                    qn = 0;
-                  }
-                }
+                Q.push_lanes(all, w == 0xffffffffu ? 0u : w, B + 32u * j, lane);
               }
-              if (qn) fold_queue<P, C, 8>(all, qv, qn, curb);
+              Q.flush(all);
               SB_ST_ADD(2, hi - lo);
             }
           } else {
@@ -1195,41 +1256,33 @@ __device__ __forceinline__ void process_group16(const UnionArgs& a, uint32_t g0,
         if (!(act & block_nodes(b))) continue;  // no node of this block has neighbours
         Grp acc = u4_grp(S.blk[b][lane]);
         bool touched = false;
-        // p >= 10: the cover's ids are sparse (the rims of the disks), so they are
-        // queued across words -- lane q holds queued id q -- and folded 8 at a time
-        uint32_t qv = 0u;
-        int qn = 0;
+        // p >= 10: the cover's ids are sparse (the rims of the disks): a word per
+        // lane, full words as 8-row batches, the other set bits queued
+        IdQueue<P, C> Q{S.q[warp], 0u, 0u, curb};
 #pragma unroll 1
         for (int j0 = 0; j0 < GW; j0 += 32) {
-          const uint32_t cword = block_cover_word(S, b, j0 + lane, act);
-          uint32_t nz = __ballot_sync(FULL, cword != 0u);
-          touched |= nz != 0u;
-          while (nz) {
-            const int src = __ffs(nz) - 1;
-            nz &= nz - 1u;
-            uint32_t cw = __shfl_sync(FULL, cword, src);
-            const uint32_t id0 = B + 32u * (j0 + src);
-            if constexpr (G::SUB == 1) {
-              SB_ST_ADD(3, __popc(cw));
-              if (cw == 0xffffffffu) {
-                fold_word_rows<P, C>(acc, cw, id0, curb);
-                continue;
-              }
-              while (cw) {
-                const int bp = __ffs(cw) - 1;
-                cw &= cw - 1u;
-                if (lane == qn) qv = id0 + bp;
-                if (++qn == 8) {
-                  fold_queue<P, C, 8>(acc, qv, 8, curb);
-                  qn = 0;
-                }
-              }
-            } else {
-              fold_set_bits<P, C>(acc, cw, id0, curb, sub);
+          uint32_t cword = block_cover_word(S, b, j0 + lane, act);
+          const uint32_t id0l = B + 32u * (j0 + lane);
+          touched |= __any_sync(FULL, cword != 0u);
+          if constexpr (G::SUB == 1) {
+            SB_ST_ADD(3, __reduce_add_sync(FULL, __popc(cword)));
+            uint32_t fm = __ballot_sync(FULL, cword == 0xffffffffu);
+            while (fm) {
+              const int src = __ffs(fm) - 1;
+              fm &= fm - 1u;
+              fold_word_rows<P, C>(acc, 0xffffffffu, B + 32u * (j0 + src), curb);
+            }
+            Q.push_lanes(acc, cword == 0xffffffffu ? 0u : cword, id0l, lane);
+          } else {
+            uint32_t nz = __ballot_sync(FULL, cword != 0u);
+            while (nz) {
+              const int src = __ffs(nz) - 1;
+              nz &= nz - 1u;
+              fold_set_bits<P, C>(acc, __shfl_sync(FULL, cword, src), B + 32u * (j0 + src), curb, sub);
             }
           }
         }
-        if (G::SUB == 1 && qn) fold_queue<P, C, 8>(acc, qv, qn, curb);
+        if (G::SUB == 1) Q.flush(acc);
         if (touched) S.blk[b][lane] = grp_u4(acc);
         SB_ST_ADD(4, 1);
       }
