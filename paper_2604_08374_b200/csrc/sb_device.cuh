@@ -277,4 +277,94 @@ __device__ __forceinline__ Decode4 decode_step4(const uint8_t* __restrict__ stre
   return o;
 }
 
+// ---- 16-bytes-per-lane LEB128 decode of the per-node feeder (p < 9) ------
+// A 512-byte window at `pos` (a varint boundary); lane L holds bytes
+// 16L..16L+15, decode_step4's prefix-sum arithmetic.  No compaction: slot
+// buf[17 L + j] gets the id of byte j's terminator if it is one of the item's
+// wanted terminators (the first `remaining`), else the window's last wanted id
+// -- a neighbour of the same node, and folding a row twice changes nothing
+// (max is idempotent).  Stride 17 keeps the stores conflict-free and the batch
+// loads at 2-way.  Needs the stream padded by >= 516 B.
+struct Decode16 {
+  int wanted;     // terminators consumed from the item in this window
+  int advance;    // bytes consumed (through the last wanted terminator)
+  uint32_t last;  // id of the last wanted terminator (next base)
+};
+
+__device__ __forceinline__ Decode16 decode_step16(const uint8_t* __restrict__ stream, uint64_t pos,
+                                                  uint32_t remaining, uint32_t base, uint32_t* buf, int lane) {
+  const uint8_t* al = stream + (pos & ~3ull) + 16 * lane;
+  uint32_t A[5];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) A[i] = ld_stream_word(al + 4 * i);
+  A[4] = __shfl_down_sync(FULL, A[0], 1);
+  if (lane == 31) A[4] = ld_stream_word(al + 16);
+  const uint32_t sh = static_cast<uint32_t>(pos & 3) * 8;
+  uint32_t x[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) x[i] = __funnelshift_r(A[i], A[i + 1], sh);
+  uint32_t prev = __shfl_up_sync(FULL, x[3], 1);
+  if (lane == 0) prev = 0;  // the window starts on a varint boundary
+  uint32_t pre[16];
+  uint32_t tm = 0u;  // terminator bytes, 16-bit mask
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t w = x[i], wp = i ? x[i - 1] : prev;
+    const uint32_t F = w & 0x80808080u, Fp = wp & 0x80808080u;
+    const uint32_t m1 = __funnelshift_l(Fp, F, 8);
+    const uint32_t m2 = m1 & __funnelshift_l(Fp, F, 16);
+    const uint32_t m3 = m2 & __funnelshift_l(Fp, F, 24);
+    const uint32_t m4 = m3 & Fp;
+    const uint32_t D = (m1 >> 7) + (m2 >> 7) + (m3 >> 7) + (m4 >> 7);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t c = ((w >> (8 * k)) & 0x7fu) << (7 * ((D >> (8 * k)) & 0xffu));
+      pre[4 * i + k] = (4 * i + k) ? pre[4 * i + k - 1] + c : c;
+    }
+    const uint32_t T = ~w & 0x80808080u;
+    tm |= ((T >> 7) & 1u | (T >> 14) & 2u | (T >> 21) & 4u | (T >> 28) & 8u) << (4 * i);
+  }
+  const uint32_t lane_sum = pre[15];
+  uint32_t incl = lane_sum;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(FULL, incl, d);
+    if (lane >= d) incl += y;
+  }
+  const uint32_t excl = base + incl - lane_sum;
+  const uint32_t tc = __popc(tm);
+  const uint32_t ttot = __reduce_add_sync(FULL, tc);
+  uint32_t wm = tm;  // wanted terminators
+  if (ttot > remaining) {  // warp-uniform: the item ends inside this window
+    uint32_t tinc = tc;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(FULL, tinc, d);
+      if (lane >= d) tinc += y;
+    }
+    const uint32_t below = tinc - tc;
+    if (below >= remaining)
+      wm = 0u;
+    else if (remaining - below < tc)
+      wm = tm & ((2u << __fns(tm, 0, static_cast<int>(remaining - below))) - 1u);
+  }
+  Decode16 o;
+  o.wanted = static_cast<int>(ttot < remaining ? ttot : remaining);
+  o.advance = 0;
+  o.last = base;
+  const uint32_t anyw = __ballot_sync(FULL, wm != 0u);
+  if (anyw == 0) return o;
+  uint32_t mylast = 0u;
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    if ((wm >> j) & 1u) mylast = excl + pre[j];
+  const int L = 31 - __clz(anyw);
+  o.advance = 16 * L + (31 - __clz(__shfl_sync(FULL, wm, L))) + 1;
+  o.last = __shfl_sync(FULL, mylast, L);
+  uint32_t* b = buf + 17 * lane;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) b[j] = ((wm >> j) & 1u) ? excl + pre[j] : o.last;
+  return o;
+}
+
 }  // namespace sb

@@ -301,7 +301,8 @@ __global__ void __launch_bounds__(256) init_kernel(uint8_t* plane, uint64_t n, c
 //   ACC2 two accumulators alternating between batches (shorter dependency chain)
 //   KWAY bit-serial (U+1)-way max instead of the pairwise tree (kway_max)
 //   OR   exact mode: rows are reachability bitsets, the union is a plain OR
-template <int U_, bool DB_, int MINB_, bool ACC2_, bool KWAY_ = false, bool OR_ = false>
+//   D16  per-node feeder decodes 512-byte steps into uncompacted slots (decode_step16)
+template <int U_, bool DB_, int MINB_, bool ACC2_, bool KWAY_ = false, bool OR_ = false, bool D16_ = false>
 struct UCfg {
   static constexpr int U = U_;
   static constexpr bool DB = DB_;
@@ -309,21 +310,26 @@ struct UCfg {
   static constexpr bool ACC2 = ACC2_;
   static constexpr bool KWAY = KWAY_;
   static constexpr bool OR = OR_;
+  static constexpr bool D16 = D16_;
 };
-// U rows in flight per lane: 8 (a batch of 8 * SUB ids), at most one 128-id
-// decode window per batch -- p=4/5 (32 rows per warp step) take 4 per lane.
+// U rows in flight per lane: 8 (a batch of 8 * SUB ids).  p >= 9: 128-byte
+// decode windows, at most one per batch.  p < 9 (rows of <= 128 B, where the
+// decode is most of the per-edge work): 512-byte decode steps (D16), 2..16
+// batches per step.
 template <int P>
-using DefaultCfg = UCfg<((128 / Geo<P>::SUB) < 8 ? (128 / Geo<P>::SUB) : 8), false, 4, false, true>;
+using DefaultCfg = UCfg<8, false, 4, false, true, false, (P < 9)>;
 
 // Per-warp id feeder: decodes one 128-byte window of the item's LEB128 stream
 // at a time (decode_step4) into a shared buffer (compacted; tail padded with
 // the last id, harmless because max is idempotent) and hands out batches of
-// BATCH = U * SUB ids.
-template <int P, bool SKIP, int U>
+// BATCH = U * SUB ids.  D16: 512-byte steps (decode_step16), one slot per byte
+// in a lane-major layout of stride 17, batches up to the step's last id.
+template <int P, bool SKIP, int U, bool D16 = false>
 struct Feeder {
   using G = Geo<P>;
   static constexpr int BATCH = U * G::SUB;
-  static constexpr int BUF = 128 + BATCH;  // one 128-byte window of ids + padding
+  static constexpr int BUF = D16 ? 17 * 32 : 128 + BATCH;  // one decode step of ids + padding
+  static_assert(!D16 || (!SKIP && BATCH % 16 == 0 && 512 % BATCH == 0), "D16 feeder shape");
   uint32_t* buf;
   uint64_t pos;
   uint32_t rem, base;
@@ -334,19 +340,44 @@ struct Feeder {
     while (i >= n) {
       if (rem == 0) return false;
       __syncwarp();  // every lane finished reading the previous window's ids
-      const Decode4 d = decode_step4<SKIP, BATCH>(a.stream, pos, rem, base, a.changed_in, buf, lane);
-      if (d.advance == 0) {  // unreachable on a validated stream
-        rem = 0;
-        return false;
+      if constexpr (D16) {
+        const Decode16 d = decode_step16(a.stream, pos, rem, base, buf, lane);
+        if (d.advance == 0) {  // unreachable on a validated stream
+          rem = 0;
+          return false;
+        }
+        pos += d.advance;
+        rem -= d.wanted;
+        base = d.last;
+        n = (d.advance + BATCH - 1) / BATCH * BATCH;  // slots past the last id repeat it
+      } else {
+        const Decode4 d = decode_step4<SKIP, BATCH>(a.stream, pos, rem, base, a.changed_in, buf, lane);
+        if (d.advance == 0) {  // unreachable on a validated stream
+          rem = 0;
+          return false;
+        }
+        pos += d.advance;
+        rem -= d.wanted;
+        base = d.last;
+        n = d.count;
       }
-      pos += d.advance;
-      rem -= d.wanted;
-      base = d.last;
-      n = d.count;
       i = 0;
       __syncwarp();
     }
     return true;
+  }
+
+  // Row id of slot i + q * SUB + sub (q compile-time after unrolling).
+  __device__ __forceinline__ uint32_t id(int q, int sub) const {
+    if constexpr (D16) {
+      const uint32_t* b = buf + 17 * (i >> 4);
+      if constexpr (G::SUB >= 16)
+        return b[17 * (q * (G::SUB >> 4)) + 17 * (sub >> 4) + (sub & 15)];
+      else
+        return b[17 * ((q * G::SUB) >> 4) + ((q * G::SUB) & 15) + sub];
+    } else {
+      return buf[i + q * G::SUB + sub];
+    }
   }
 };
 
@@ -359,12 +390,12 @@ __device__ __forceinline__ const uint8_t* opaque(const uint8_t* p) {
   return p;
 }
 
-template <int P, int U>
-__device__ __forceinline__ void load_batch(Grp (&x)[U], const uint8_t* curb, const uint32_t* buf, int i, int sub) {
+template <int P, int U, class F>
+__device__ __forceinline__ void load_batch(Grp (&x)[U], const uint8_t* curb, const F& f, int sub) {
   using G = Geo<P>;
   using IO = GrpIO<G::GB>;
 #pragma unroll
-  for (int q = 0; q < U; ++q) x[q] = IO::ld(curb + static_cast<uint64_t>(buf[i + q * G::SUB + sub]) * G::ROW);
+  for (int q = 0; q < U; ++q) x[q] = IO::ld(curb + static_cast<uint64_t>(f.id(q, sub)) * G::ROW);
 }
 
 // acc <- max(acc, x[0..U)) as a balanced tree: depth log2(U)+1 maxes instead
@@ -497,8 +528,9 @@ __device__ __forceinline__ void process_item(const UnionArgs& a, uint64_t item, 
                                              uint32_t* buf) {
   using G = Geo<P>;
   using IO = GrpIO<G::GB>;
-  constexpr int U = C::U;
-  using F = Feeder<P, SKIP, U>;
+  // 128-byte decode windows feed at most 128 ids per batch
+  constexpr int U = (C::D16 && !SKIP) || C::U * G::SUB <= 128 ? C::U : 128 / G::SUB;
+  using F = Feeder<P, SKIP, U, C::D16 && !SKIP>;
   const int sub = lane / G::LPR;
   const int gl = lane % G::LPR;
   const uint64_t u = item * G::SLICES + slice;
@@ -523,20 +555,20 @@ __device__ __forceinline__ void process_item(const UnionArgs& a, uint64_t item, 
     Grp xa[U], xb[U];
     bool ha = f.next(a, lane);
     if (ha) {
-      load_batch<P, U>(xa, curb, f.buf, f.i, sub);
+      load_batch<P, U>(xa, curb, f, sub);
       f.i += F::BATCH;
     }
     while (ha) {
       const bool hb = f.next(a, lane);
       if (hb) {
-        load_batch<P, U>(xb, curb, f.buf, f.i, sub);
+        load_batch<P, U>(xb, curb, f, sub);
         f.i += F::BATCH;
       }
       batch_max<C, U>(acc, xa);
       if (!hb) break;
       ha = f.next(a, lane);
       if (ha) {
-        load_batch<P, U>(xa, curb, f.buf, f.i, sub);
+        load_batch<P, U>(xa, curb, f, sub);
         f.i += F::BATCH;
       }
       batch_max<C, U>(C::ACC2 ? acc2 : acc, xb);
@@ -544,7 +576,7 @@ __device__ __forceinline__ void process_item(const UnionArgs& a, uint64_t item, 
   } else {
     Grp x[U];
     while (f.next(a, lane)) {
-      load_batch<P, U>(x, curb, f.buf, f.i, sub);
+      load_batch<P, U>(x, curb, f, sub);
       f.i += F::BATCH;
       batch_max<C, U>(acc, x);
     }
@@ -1358,7 +1390,7 @@ __device__ __forceinline__ bool upload_failed(const UnionArgs& a) {
 //              instead of L2.
 template <int P, bool SKIP, class C, bool GRP>
 constexpr size_t union_smem_bytes() {
-  constexpr size_t ids = sizeof(uint32_t) * 8 * Feeder<P, SKIP, C::U>::BUF;
+  constexpr size_t ids = sizeof(uint32_t) * 8 * Feeder<P, SKIP, C::U, C::D16 && !SKIP>::BUF;
   return GRP && sizeof(GroupSmem) > ids ? sizeof(GroupSmem) : ids;
 }
 
@@ -1372,7 +1404,7 @@ __global__ void __launch_bounds__(256, C::MINB) union_kernel(UnionArgs a) {
   __shared__ uint32_t s_mode;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  uint32_t* buf = reinterpret_cast<uint32_t*>(smem) + warp * Feeder<P, SKIP, C::U>::BUF;
+  uint32_t* buf = reinterpret_cast<uint32_t*>(smem) + warp * Feeder<P, SKIP, C::U, C::D16 && !SKIP>::BUF;
   if (!TILE) {
     const uint64_t total = a.n_items * G::SLICES;
     for (;;) {
