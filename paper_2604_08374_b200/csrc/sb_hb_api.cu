@@ -168,9 +168,12 @@ int sb_hb_step_compute(sb_hb* h, double* local_max) {
     if (h->flags & SB_HB_SCHEDULE_WARP) u.n_tiles = 0;
     if (h->flags & SB_HB_SCHEDULE_GROUP) {
       u.shared_max_edges = ~0ull;
-    } else if (h->p < 9) {
-      // rows of <= 128 B: the gathers the group path saves are cheap, and the
-      // per-node decode + fold is faster (C2: p=4 0.56 vs 1.18 ms, p=8 1.12 vs 1.97 ms)
+    } else if (h->p < 9 && g->edges_local < 6000ull * g->n_local) {
+      // rows of <= 128 B on graphs of moderate degree: the gathers the group
+      // path saves are cheap, and the per-node decode + fold is faster (C2,
+      // mean degree 3,730: p=6 0.44 vs 0.80 ms, p=8 1.07 vs 1.56 ms); at C3
+      // (mean degree 20,278) the shared gathers win also at p=8 (22.0 vs 29.2 ms;
+      // profiles/r02/group_threshold.json)
       u.node_lo = nullptr;
     }
     u.npeers = h->npeers;

@@ -398,6 +398,21 @@ __device__ __forceinline__ void load_batch(Grp (&x)[U], const uint8_t* curb, con
   for (int q = 0; q < U; ++q) x[q] = IO::ld(curb + static_cast<uint64_t>(f.id(q, sub)) * G::ROW);
 }
 
+// p = 4 (8-byte rows of four 16-bit planes): two rows per 32-bit plane word --
+// row 2k in the low halves, row 2k+1 in the high ones (one PRMT per plane) --
+// so one bit-serial max covers two rows; the halves are merged once per item.
+template <int P, int U, class F>
+__device__ __forceinline__ void load_batch_pairs(Grp (&x)[U / 2], const uint8_t* curb, const F& f, int sub) {
+  using G = Geo<P>;
+#pragma unroll
+  for (int q = 0; q < U / 2; ++q) {
+    const uint2 r0 = __ldg(reinterpret_cast<const uint2*>(curb + static_cast<uint64_t>(f.id(2 * q, sub)) * G::ROW));
+    const uint2 r1 = __ldg(reinterpret_cast<const uint2*>(curb + static_cast<uint64_t>(f.id(2 * q + 1, sub)) * G::ROW));
+    x[q] = Grp{__byte_perm(r0.x, r1.x, 0x5410), __byte_perm(r0.x, r1.x, 0x7632), __byte_perm(r0.y, r1.y, 0x5410),
+               __byte_perm(r0.y, r1.y, 0x7632)};
+  }
+}
+
 // acc <- max(acc, x[0..U)) as a balanced tree: depth log2(U)+1 maxes instead
 // of a U-long serial chain through acc (the ripple LOP3s are latency-bound).
 template <int U>
@@ -573,6 +588,16 @@ __device__ __forceinline__ void process_item(const UnionArgs& a, uint64_t item, 
       }
       batch_max<C, U>(C::ACC2 ? acc2 : acc, xb);
     }
+  } else if constexpr (G::GB == 8 && !C::OR && U % 2 == 0) {
+    Grp x[U / 2];
+    while (f.next(a, lane)) {
+      load_batch_pairs<P, U>(x, curb, f, sub);
+      f.i += F::BATCH;
+      batch_max<C, U / 2>(acc, x);
+    }
+    Grp hi{acc.b0 >> 16, acc.b1 >> 16, acc.b2 >> 16, acc.b3 >> 16};
+    acc = Grp{acc.b0 & 0xffffu, acc.b1 & 0xffffu, acc.b2 & 0xffffu, acc.b3 & 0xffffu};
+    bsmax(acc, hi);
   } else {
     Grp x[U];
     while (f.next(a, lane)) {

@@ -87,3 +87,19 @@ if [[ $what == ncusass ]]; then
   rm -f gpurun_out/prof_sass.ncu-rep
 fi
 done
+for what in "$@"; do
+if [[ $what == ncu_lowp ]]; then
+  for cfg in "c2 4" "c2 6" "c2 8"; do
+    set -- $cfg
+    run timeout 600 $NCU -k regex:union_kernel -s 2 -c 1 -o gpurun_out/prof_$1_p$2 \
+        python -u bench.py --config $1 --p $2 --profile --no-cpu --no-e2e --no-variants --no-pipeline
+    ncu -i gpurun_out/prof_$1_p$2.ncu-rep --page source --csv --print-source sass > gpurun_out/sass_$1_p$2.csv 2>&1
+    export_rep $1_p$2 prof_$1_p$2
+  done
+fi
+done
+for what in "$@"; do
+if [[ $what == gthr ]]; then
+  run timeout 900 python -u scripts/group_threshold.py > gpurun_out/group_threshold.log 2>&1
+fi
+done
