@@ -177,7 +177,7 @@ def roofline_of(cfg, p, launch_s, bytes_launch, sm_mhz):
     """Roofline of the dominant kernel (the dense union) on the unit that binds it.
 
     The union's 2.46 TB of SURVEY 8(d) algorithmic row bytes per C3 launch never
-    reach DRAM: each 8-node group gathers a row once and L1/L2 serve the rest, so
+    reach DRAM: each 16-node group gathers a row once per block of its cover and L2 serves it, so
     the ncu DRAM traffic is ~5 GB per launch (the stream + the planes) and an
     HBM "roofline" on algorithmic bytes reads > 1.  What bounds the kernel is the
     SM's instruction issue (ncu: issue slots ~77 % busy, ALU pipe ~70 %).  So:
@@ -192,7 +192,7 @@ def roofline_of(cfg, p, launch_s, bytes_launch, sm_mhz):
     alg = {"bytes_per_launch": bytes_launch, "achieved_gbs": bytes_launch / launch_s / 1e9,
            "ratio_to_hbm_peak": bytes_launch / launch_s / 1e9 / hbm,
            "note": "SURVEY 8(d) algorithmic bytes (every edge's packed m/2-byte row) per launch / launch time; "
-                   "> 1 because rows are shared within 8-node groups and served on-chip -- not a roofline"}
+                   "> 1 because each row is gathered once per block of its 16-node group cover and served from L2 -- not a roofline"}
     if not e or not e.get("warp_instructions_issued"):
         return {"bound": "hbm", "achieved": None, "peak": hbm, "unit": "GB/s", "frac": None, "traffic": None,
                 "note": "no committed ncu summary for this config (profiles/union_ncu_summary.json)"}, alg
@@ -465,10 +465,10 @@ def main():
     ev0.record(stream)
     for _ in range(args.steps):
         iters = one_run(hb)
-        union_ms += [s["union_ms"] for s in hb.stats()]
     ev1.record(stream)
     ev1.synchronize()
     barrier()
+    union_ms = [s["union_ms"] for s in hb.stats()]  # the last timed run (every run is identical)
     # (single process only: extra runs on one rank would desynchronise the collectives)
     clock_info = clocks.stop(keep_busy=(lambda: (one_run(hb), torch.cuda.synchronize())) if world == 1 else None)
     dev_s = max_over_ranks(ev0.elapsed_time(ev1) / 1e3)

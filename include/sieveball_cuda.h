@@ -55,9 +55,10 @@ enum {
 #define SB_HB_SCHEDULE_WARP 2u  /* per-warp work-item schedule instead of the default 8-node CTA tiles */
 #define SB_HB_INTERVAL 4u       /* variant: fold runs of consecutive ids via a per-iteration sparse table
                                    (bit-exact; any p; not combinable with SKIP_UNCHANGED) */
-#define SB_HB_SCHEDULE_GROUP 8u /* 8-node shared-gather groups wherever the rows overlap densely, also on graphs
-                                   too small to fill the device (default: only groups within half a resident
-                                   CTA's share of the edges); not combinable with SCHEDULE_WARP */
+#define SB_HB_SCHEDULE_GROUP 8u /* 16-node shared-gather groups wherever the rows overlap densely, at every p and
+                                   also on graphs too small to fill the device (default: p >= 9 or mean degree
+                                   >= 6000, >= 16 x 4 x SMs nodes, groups within half a resident CTA's share of
+                                   the edges); not combinable with SCHEDULE_WARP */
 
 /* sb_hb_read_registers `which` */
 #define SB_REGS_LATEST 0   /* registers after the last executed iteration (c_t) */

@@ -219,6 +219,9 @@ void graph_union_args(const sb_graph* g, sb::UnionArgs& u) {
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
   u.shared_max_edges = g->edges_local / (2ull * 4ull * static_cast<uint64_t>(sms));
+  // fewer 16-node groups than resident CTAs: no group can qualify, so launch
+  // the kernel without the group path (no per-tile group test; C1)
+  if (g->n_local < 16ull * 4ull * static_cast<uint64_t>(sms)) u.node_lo = nullptr;
 }
 
 static int graph_check(sb_graph* g) {

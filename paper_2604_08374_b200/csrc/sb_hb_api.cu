@@ -166,7 +166,8 @@ int sb_hb_step_compute(sb_hb* h, double* local_max) {
     u.changed_in = h->d_changed[L];
     u.work = h->d_misc;
     if (h->flags & SB_HB_SCHEDULE_WARP) u.n_tiles = 0;
-    if (h->flags & SB_HB_SCHEDULE_GROUP) {
+    if (h->flags & SB_HB_SCHEDULE_GROUP) {  // every dense-enough group takes the group path
+      u.node_lo = g->d_node_lo;
       u.shared_max_edges = ~0ull;
     } else if (h->p < 9 && g->edges_local < 6000ull * g->n_local) {
       // rows of <= 128 B on graphs of moderate degree: the gathers the group

@@ -103,3 +103,10 @@ if [[ $what == gthr ]]; then
   run timeout 900 python -u scripts/group_threshold.py > gpurun_out/group_threshold.log 2>&1
 fi
 done
+for what in "$@"; do
+if [[ $what == small ]]; then
+  run timeout 600 python -u bench.py --config c2 --no-cpu > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.log
+  run timeout 600 python -u bench.py --config c1 --no-cpu > gpurun_out/bench_c1.json 2> gpurun_out/bench_c1.log
+  run timeout 600 python -u scripts/step_overhead.py > gpurun_out/step_overhead.json 2> gpurun_out/step_overhead.log
+fi
+done
