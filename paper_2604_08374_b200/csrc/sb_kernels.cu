@@ -989,9 +989,10 @@ __device__ __forceinline__ uint32_t decode16_to_bitmap(const UnionArgs& a, RowPo
       const uint32_t m2 = m1 & __funnelshift_l(Fp, F, 16);
       const uint32_t m3 = m2 & __funnelshift_l(Fp, F, 24);
       const uint32_t m4 = m3 & Fp;
-      const uint32_t D = (m1 >> 7) + (m2 >> 7) + (m3 >> 7) + (m4 >> 7);
+      // 7 * d per byte (<= 28: no carries between bytes)
+      const uint32_t D7 = ((m1 >> 7) + (m2 >> 7) + (m3 >> 7) + (m4 >> 7)) * 7u;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) cb[4 * i + k] = ((w >> (8 * k)) & 0x7fu) << (7 * ((D >> (8 * k)) & 0xffu));
+      for (int k = 0; k < 4; ++k) cb[4 * i + k] = ((w >> (8 * k)) & 0x7fu) << ((D7 >> (8 * k)) & 0xffu);
     }
     uint32_t pre[16];
     pre[0] = cb[0];
@@ -1004,7 +1005,8 @@ __device__ __forceinline__ uint32_t decode16_to_bitmap(const UnionArgs& a, RowPo
       const uint32_t y = __shfl_up_sync(FULL, incl, d);
       if (lane >= d) incl += y;
     }
-    const uint32_t excl = c.base + incl - lane_sum;
+    // window offset of the id after this lane's preceding bytes: byte j's id is B + E + pre[j]
+    const uint32_t E = c.base + incl - lane_sum - B;
     // terminators of this row (bytes before its end), 16-bit mask
     const int64_t left = static_cast<int64_t>(c.end) - static_cast<int64_t>(c.pos + 16 * lane);
     uint32_t tm = 0u;
@@ -1016,40 +1018,40 @@ __device__ __forceinline__ uint32_t decode16_to_bitmap(const UnionArgs& a, RowPo
     tm &= left >= 16 ? 0xffffu : left <= 0 ? 0u : (1u << left) - 1u;
     // in-window terminators: all of them unless the window ends inside this step
     uint32_t inm = tm;
-    if (!__all_sync(FULL, excl + lane_sum - B < static_cast<uint32_t>(GW_IDS))) {
+    if (!__all_sync(FULL, E + lane_sum < static_cast<uint32_t>(GW_IDS))) {
       inm = 0u;
 #pragma unroll
-      for (int j = 0; j < 16; ++j) inm |= (excl + pre[j] - B < static_cast<uint32_t>(GW_IDS) ? 1u : 0u) << j;
+      for (int j = 0; j < 16; ++j) inm |= (E + pre[j] < static_cast<uint32_t>(GW_IDS) ? 1u : 0u) << j;
       inm &= tm;
     }
     const uint32_t outm = tm & ~inm;
-    // bitmap bits, last in-window id, first out-of-window id
-    uint32_t last_in = 0u, first_out = 0u;
+    // bitmap bits and the last in-window offset
+    uint32_t last_off = 0u;
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-      const uint32_t idj = excl + pre[j];
+      const uint32_t off = E + pre[j];
       if ((inm >> j) & 1u) {
         bool keep = true;
-        if (SKIP) keep = a.changed_in[idj] != 0;
-        const uint32_t off = idj - B;
+        if (SKIP) keep = a.changed_in[B + off] != 0;
         if (keep) atomicOr(bm + (off >> 5), 1u << (off & 31));
-        last_in = idj;
+        last_off = off;
       }
     }
-#pragma unroll
-    for (int j = 15; j >= 0; --j)
-      if ((outm >> j) & 1u) first_out = excl + pre[j];
     const uint32_t anyin = __ballot_sync(FULL, inm != 0u);
     const uint32_t anyout = __ballot_sync(FULL, outm != 0u);
     if (anyin) {  // advance past the last in-window terminator
       const int L = 31 - __clz(anyin);
       const int lk = 31 - __clz(__shfl_sync(FULL, inm, L));
-      c.base = __shfl_sync(FULL, last_in, L);
+      c.base = B + __shfl_sync(FULL, last_off, L);
       c.pos += 16 * L + lk + 1;
     }
-    if (anyout) {
+    if (anyout) {  // once per row and window: the first id past the window
+      uint32_t first_out = 0u;
+#pragma unroll
+      for (int j = 15; j >= 0; --j)
+        if ((outm >> j) & 1u) first_out = E + pre[j];
       if (lane < 16) prefetch_l2(a.stream + c.pos + 128 * lane);
-      return __shfl_sync(FULL, first_out, __ffs(anyout) - 1);
+      return B + __shfl_sync(FULL, first_out, __ffs(anyout) - 1);
     }
     if (!anyin) {  // unreachable on a validated stream (a step always holds a terminator)
       c.pos = c.end;
