@@ -742,6 +742,7 @@ struct IdQueue {
   }
   // Every lane's word cw: ids idb + bit (lane-parallel when the ids fit the ring).
   __device__ __forceinline__ void push_lanes(Grp& acc, uint32_t cw, uint32_t idb, int lane) {
+    if (!__any_sync(FULL, cw != 0u)) return;
     const uint32_t n = __popc(cw);
     uint32_t incl = n;
 #pragma unroll
@@ -1321,8 +1322,9 @@ __device__ __forceinline__ void process_group16(const UnionArgs& a, uint32_t g0,
 #pragma unroll 1
         for (int j0 = 0; j0 < GW; j0 += 32) {
           uint32_t cword = block_cover_word(S, b, j0 + lane, act);
+          if (!__any_sync(FULL, cword != 0u)) continue;
           const uint32_t id0l = B + 32u * (j0 + lane);
-          touched |= __any_sync(FULL, cword != 0u);
+          touched = true;
           if constexpr (G::SUB == 1) {
             SB_ST_ADD(3, __reduce_add_sync(FULL, __popc(cword)));
             uint32_t fm = __ballot_sync(FULL, cword == 0xffffffffu);
