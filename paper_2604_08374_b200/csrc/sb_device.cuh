@@ -281,10 +281,11 @@ __device__ __forceinline__ Decode4 decode_step4(const uint8_t* __restrict__ stre
 // A 512-byte window at `pos` (a varint boundary); lane L holds bytes
 // 16L..16L+15, decode_step4's prefix-sum arithmetic.  No compaction: slot
 // buf[17 L + j] gets the id of byte j's terminator if it is one of the item's
-// wanted terminators (the first `remaining`), else the window's last wanted id
-// -- a neighbour of the same node, and folding a row twice changes nothing
-// (max is idempotent).  Stride 17 keeps the stores conflict-free and the batch
-// loads at 2-way.  Needs the stream padded by >= 516 B.
+// wanted terminators (the first `remaining`); any other slot keeps what it
+// held -- an id of an earlier step of the same item, or the fill the feeder
+// writes at the item's start (the node itself): folding a row twice changes
+// nothing (max is idempotent).  Stride 17 keeps the stores conflict-free and
+// the batch loads at 2-way.  Needs the stream padded by >= 516 B.
 struct Decode16 {
   int wanted;     // terminators consumed from the item in this window
   int advance;    // bytes consumed (through the last wanted terminator)
@@ -363,7 +364,8 @@ __device__ __forceinline__ Decode16 decode_step16(const uint8_t* __restrict__ st
   o.last = __shfl_sync(FULL, mylast, L);
   uint32_t* b = buf + 17 * lane;
 #pragma unroll
-  for (int j = 0; j < 16; ++j) b[j] = ((wm >> j) & 1u) ? excl + pre[j] : o.last;
+  for (int j = 0; j < 16; ++j)
+    if ((wm >> j) & 1u) b[j] = excl + pre[j];
   return o;
 }
 

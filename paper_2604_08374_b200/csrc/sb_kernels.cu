@@ -367,6 +367,16 @@ struct Feeder {
     return true;
   }
 
+  // D16: every slot holds an id of this item's node before the first decode
+  // (decode_step16 only overwrites the slots of wanted terminators).
+  __device__ __forceinline__ void prefill(uint32_t id, int lane) {
+    if constexpr (D16) {
+      __syncwarp();  // the previous item's batches are read
+#pragma unroll
+      for (int k = 0; k < 17; ++k) buf[32 * k + lane] = id;
+    }
+  }
+
   // Row id of slot i + q * SUB + sub (q compile-time after unrolling).
   __device__ __forceinline__ uint32_t id(int q, int sub) const {
     if constexpr (D16) {
@@ -564,6 +574,7 @@ __device__ __forceinline__ void process_item(const UnionArgs& a, uint64_t item, 
   f.base = a.item_base[item];
   f.n = 0;
   f.i = 0;
+  f.prefill(static_cast<uint32_t>(v), lane);
   if (C::DB) {
     // software pipeline: batch k+1's loads (and the next window decode when
     // needed) are in flight while batch k is reduced.
