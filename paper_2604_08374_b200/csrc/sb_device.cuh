@@ -277,6 +277,23 @@ __device__ __forceinline__ Decode4 decode_step4(const uint8_t* __restrict__ stre
   return o;
 }
 
+// Byte k of x, zero-extended (one PRMT).
+__device__ __forceinline__ uint32_t byte_of(uint32_t x, int k) { return __byte_perm(x, 0u, 0x4440u + k); }
+
+// Per byte of w: payload << 7 * (continuation bytes just before it, <= 4), the
+// continuation run read from the flag bytes of w and of the previous word wp.
+__device__ __forceinline__ void varint_contrib(uint32_t w, uint32_t wp, uint32_t (&c)[4]) {
+  const uint32_t F = w & 0x80808080u, Fp = wp & 0x80808080u;
+  const uint32_t m1 = __funnelshift_l(Fp, F, 8);
+  const uint32_t m2 = m1 & __funnelshift_l(Fp, F, 16);
+  const uint32_t m3 = m2 & __funnelshift_l(Fp, F, 24);
+  const uint32_t m4 = m3 & Fp;
+  const uint32_t D7 = ((m1 >> 7) + (m2 >> 7) + (m3 >> 7) + (m4 >> 7)) * 7u;  // 7 d per byte, <= 28
+  const uint32_t P = w & 0x7f7f7f7fu;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) c[k] = byte_of(P, k) << byte_of(D7, k);
+}
+
 // ---- 16-bytes-per-lane LEB128 decode of the per-node feeder (p < 9) ------
 // A 512-byte window at `pos` (a varint boundary); lane L holds bytes
 // 16L..16L+15, decode_step4's prefix-sum arithmetic.  No compaction: slot
@@ -310,18 +327,11 @@ __device__ __forceinline__ Decode16 decode_step16(const uint8_t* __restrict__ st
   uint32_t tm = 0u;  // terminator bytes, 16-bit mask
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const uint32_t w = x[i], wp = i ? x[i - 1] : prev;
-    const uint32_t F = w & 0x80808080u, Fp = wp & 0x80808080u;
-    const uint32_t m1 = __funnelshift_l(Fp, F, 8);
-    const uint32_t m2 = m1 & __funnelshift_l(Fp, F, 16);
-    const uint32_t m3 = m2 & __funnelshift_l(Fp, F, 24);
-    const uint32_t m4 = m3 & Fp;
-    const uint32_t D = (m1 >> 7) + (m2 >> 7) + (m3 >> 7) + (m4 >> 7);
+    const uint32_t w = x[i];
+    uint32_t c[4];
+    varint_contrib(w, i ? x[i - 1] : prev, c);
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const uint32_t c = ((w >> (8 * k)) & 0x7fu) << (7 * ((D >> (8 * k)) & 0xffu));
-      pre[4 * i + k] = (4 * i + k) ? pre[4 * i + k - 1] + c : c;
-    }
+    for (int k = 0; k < 4; ++k) pre[4 * i + k] = (4 * i + k) ? pre[4 * i + k - 1] + c[k] : c[k];
     const uint32_t T = ~w & 0x80808080u;
     tm |= ((T >> 7) & 1u | (T >> 14) & 2u | (T >> 21) & 4u | (T >> 28) & 8u) << (4 * i);
   }
@@ -355,17 +365,15 @@ __device__ __forceinline__ Decode16 decode_step16(const uint8_t* __restrict__ st
   o.last = base;
   const uint32_t anyw = __ballot_sync(FULL, wm != 0u);
   if (anyw == 0) return o;
-  uint32_t mylast = 0u;
-#pragma unroll
-  for (int j = 0; j < 16; ++j)
-    if ((wm >> j) & 1u) mylast = excl + pre[j];
   const int L = 31 - __clz(anyw);
-  o.advance = 16 * L + (31 - __clz(__shfl_sync(FULL, wm, L))) + 1;
-  o.last = __shfl_sync(FULL, mylast, L);
+  const int lk = 31 - __clz(__shfl_sync(FULL, wm, L));
+  o.advance = 16 * L + lk + 1;
   uint32_t* b = buf + 17 * lane;
 #pragma unroll
   for (int j = 0; j < 16; ++j)
     if ((wm >> j) & 1u) b[j] = excl + pre[j];
+  __syncwarp();
+  o.last = buf[17 * L + lk];  // the last wanted id, as just stored by lane L
   return o;
 }
 

@@ -992,24 +992,14 @@ __device__ __forceinline__ uint32_t decode16_to_bitmap(const UnionArgs& a, RowPo
     uint32_t prev = __shfl_up_sync(FULL, x[3], 1);
     if (lane == 0) prev = 0;  // the cursor sits on a varint boundary
     // per byte: payload << 7 * (continuation bytes just before it, <= 4)
-    uint32_t cb[16];
+    uint32_t pre[16];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      const uint32_t w = x[i], wp = i ? x[i - 1] : prev;
-      const uint32_t F = w & 0x80808080u, Fp = wp & 0x80808080u;
-      const uint32_t m1 = __funnelshift_l(Fp, F, 8);
-      const uint32_t m2 = m1 & __funnelshift_l(Fp, F, 16);
-      const uint32_t m3 = m2 & __funnelshift_l(Fp, F, 24);
-      const uint32_t m4 = m3 & Fp;
-      // 7 * d per byte (<= 28: no carries between bytes)
-      const uint32_t D7 = ((m1 >> 7) + (m2 >> 7) + (m3 >> 7) + (m4 >> 7)) * 7u;
+      uint32_t cb[4];
+      varint_contrib(x[i], i ? x[i - 1] : prev, cb);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) cb[4 * i + k] = ((w >> (8 * k)) & 0x7fu) << ((D7 >> (8 * k)) & 0xffu);
+      for (int k = 0; k < 4; ++k) pre[4 * i + k] = (4 * i + k) ? pre[4 * i + k - 1] + cb[k] : cb[k];
     }
-    uint32_t pre[16];
-    pre[0] = cb[0];
-#pragma unroll
-    for (int j = 1; j < 16; ++j) pre[j] = pre[j - 1] + cb[j];
     const uint32_t lane_sum = pre[15];
     uint32_t incl = lane_sum;
 #pragma unroll
