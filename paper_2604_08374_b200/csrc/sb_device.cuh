@@ -138,6 +138,23 @@ __device__ __host__ __forceinline__ unsigned long long dbl_to_ord(double x) {
   return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
 }
 
+// Byte k of x, zero-extended (one PRMT).
+__device__ __forceinline__ uint32_t byte_of(uint32_t x, int k) { return __byte_perm(x, 0u, 0x4440u + k); }
+
+// Per byte of w: payload << 7 * (continuation bytes just before it, <= 4), the
+// continuation run read from the flag bytes of w and of the previous word wp.
+__device__ __forceinline__ void varint_contrib(uint32_t w, uint32_t wp, uint32_t (&c)[4]) {
+  const uint32_t F = w & 0x80808080u, Fp = wp & 0x80808080u;
+  const uint32_t m1 = __funnelshift_l(Fp, F, 8);
+  const uint32_t m2 = m1 & __funnelshift_l(Fp, F, 16);
+  const uint32_t m3 = m2 & __funnelshift_l(Fp, F, 24);
+  const uint32_t m4 = m3 & Fp;
+  const uint32_t D7 = ((m1 >> 7) + (m2 >> 7) + (m3 >> 7) + (m4 >> 7)) * 7u;  // 7 d per byte, <= 28
+  const uint32_t P = w & 0x7f7f7f7fu;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) c[k] = byte_of(P, k) << byte_of(D7, k);
+}
+
 // ---- 4-bytes-per-lane LEB128 decode (hot path) ------------------------
 // A 128-byte window at `pos` (a varint boundary); lane L holds bytes
 // 4L..4L+3.  Because every byte's payload lands in exactly one delta, the
@@ -180,16 +197,8 @@ __device__ __forceinline__ Decode4 decode_step4(const uint8_t* __restrict__ stre
   const uint32_t w = __funnelshift_r(w0, w1, static_cast<uint32_t>(pos & 3) * 8);
   uint32_t wp = __shfl_up_sync(FULL, w, 1);
   if (lane == 0) wp = 0;  // the window starts on a varint boundary
-  const uint32_t F = w & 0x80808080u, Fp = wp & 0x80808080u;
-  // run of continuation flags before each byte of w (1..4 bytes back)
-  const uint32_t m1 = __funnelshift_l(Fp, F, 8);
-  const uint32_t m2 = m1 & __funnelshift_l(Fp, F, 16);
-  const uint32_t m3 = m2 & __funnelshift_l(Fp, F, 24);
-  const uint32_t m4 = m3 & Fp;
-  const uint32_t D = (m1 >> 7) + (m2 >> 7) + (m3 >> 7) + (m4 >> 7);  // per-byte d_k in 0..4
-  uint32_t c[4];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) c[k] = ((w >> (8 * k)) & 0x7fu) << (7 * ((D >> (8 * k)) & 0xffu));
+  uint32_t c[4];  // per byte: payload << 7 * (run of continuation flags before it, 0..4)
+  varint_contrib(w, wp, c);
   const uint32_t p1 = c[0] + c[1], p2 = p1 + c[2], lane_sum = p2 + c[3];
   uint32_t incl = lane_sum;
 #pragma unroll
@@ -275,23 +284,6 @@ __device__ __forceinline__ Decode4 decode_step4(const uint8_t* __restrict__ stre
     for (int k = lane; k < PAD; k += 32) buf[kn + k] = lastkept;
   }
   return o;
-}
-
-// Byte k of x, zero-extended (one PRMT).
-__device__ __forceinline__ uint32_t byte_of(uint32_t x, int k) { return __byte_perm(x, 0u, 0x4440u + k); }
-
-// Per byte of w: payload << 7 * (continuation bytes just before it, <= 4), the
-// continuation run read from the flag bytes of w and of the previous word wp.
-__device__ __forceinline__ void varint_contrib(uint32_t w, uint32_t wp, uint32_t (&c)[4]) {
-  const uint32_t F = w & 0x80808080u, Fp = wp & 0x80808080u;
-  const uint32_t m1 = __funnelshift_l(Fp, F, 8);
-  const uint32_t m2 = m1 & __funnelshift_l(Fp, F, 16);
-  const uint32_t m3 = m2 & __funnelshift_l(Fp, F, 24);
-  const uint32_t m4 = m3 & Fp;
-  const uint32_t D7 = ((m1 >> 7) + (m2 >> 7) + (m3 >> 7) + (m4 >> 7)) * 7u;  // 7 d per byte, <= 28
-  const uint32_t P = w & 0x7f7f7f7fu;
-#pragma unroll
-  for (int k = 0; k < 4; ++k) c[k] = byte_of(P, k) << byte_of(D7, k);
 }
 
 // ---- 16-bytes-per-lane LEB128 decode of the per-node feeder (p < 9) ------

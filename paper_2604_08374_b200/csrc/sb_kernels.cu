@@ -164,12 +164,10 @@ __global__ void __launch_bounds__(256, 3) build_items_kernel(BuildArgs a) {
         const uint32_t z1 = __funnelshift_l(zp, z, 8), z2 = __funnelshift_l(zp, z, 16);
         const uint32_t z3 = __funnelshift_l(zp, z, 24), z4 = zp;
         zeros += __popc(T & z & (~m1 | z1) & (~m2 | z2) & (~m3 | z3) & (~m4 | z4));
-        const uint32_t D = (m1 >> 7) + (m2 >> 7) + (m3 >> 7) + (m4 >> 7);
+        const uint32_t D7 = ((m1 >> 7) + (m2 >> 7) + (m3 >> 7) + (m4 >> 7)) * 7u;
+        const uint32_t P = w & 0x7f7f7f7fu;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const uint32_t dk = (D >> (8 * k)) & 0xffu;
-          lsum += static_cast<unsigned long long>((w >> (8 * k)) & 0x7fu) << (7 * dk);
-        }
+        for (int k = 0; k < 4; ++k) lsum += static_cast<unsigned long long>(byte_of(P, k)) << byte_of(D7, k);
       }
       cnt += lcnt;
       sum += lsum;
@@ -867,111 +865,13 @@ struct RowPos {
 };
 
 // Decodes node row `c` from its cursor into bitmap `bm` (ids in [B, B + GW_IDS))
-// and returns the first id not consumed (~0 when the row is exhausted).  128
-// bytes per step, the decode_step4 arithmetic; a byte belongs to the row iff it
-// lies before the row's end offset (no terminator ranks needed), and the
-// terminators whose id falls in the window are a prefix of the step's, so the
-// cursor advances to just past the last one and the rest are decoded again by
-// the next window.
-template <bool SKIP>
-__device__ __forceinline__ uint32_t decode_to_bitmap(const UnionArgs& a, RowPos& c, uint32_t B, uint32_t* bm,
-                                                     int lane, unsigned& steps) {
-  while (c.pos < c.end) {
-    ++steps;
-    const uint8_t* al = a.stream + (c.pos & ~3ull) + 4 * lane;
-    const uint32_t w0 = ld_stream_word(al);
-    const uint32_t w1 = ld_stream_word(al + 4);
-    const uint32_t w = __funnelshift_r(w0, w1, static_cast<uint32_t>(c.pos & 3) * 8);
-    uint32_t wp = __shfl_up_sync(FULL, w, 1);
-    if (lane == 0) wp = 0;  // the cursor sits on a varint boundary
-    const uint32_t F = w & 0x80808080u, Fp = wp & 0x80808080u;
-    const uint32_t m1 = __funnelshift_l(Fp, F, 8);
-    const uint32_t m2 = m1 & __funnelshift_l(Fp, F, 16);
-    const uint32_t m3 = m2 & __funnelshift_l(Fp, F, 24);
-    const uint32_t m4 = m3 & Fp;
-    const uint32_t D = (m1 >> 7) + (m2 >> 7) + (m3 >> 7) + (m4 >> 7);
-    uint32_t cb[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) cb[k] = ((w >> (8 * k)) & 0x7fu) << (7 * ((D >> (8 * k)) & 0xffu));
-    const uint32_t p1 = cb[0] + cb[1], p2 = p1 + cb[2], lane_sum = p2 + cb[3];
-    uint32_t incl = lane_sum;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t y = __shfl_up_sync(FULL, incl, d);
-      if (lane >= d) incl += y;
-    }
-    const uint32_t excl = c.base + incl - lane_sum;
-    const uint32_t id[4] = {excl + cb[0], excl + p1, excl + p2, excl + lane_sum};
-    // terminators of this row: bytes before the row end
-    const int64_t left = static_cast<int64_t>(c.end) - static_cast<int64_t>(c.pos + 4 * lane);
-    const uint32_t vmask = left >= 4 ? 0x80808080u : left <= 0 ? 0u : 0x80808080u >> (8 * (4 - left));
-    const uint32_t T = ~w & vmask;
-    // in: a terminator whose id falls in the window (a prefix of the row's terminators)
-    uint32_t inm = 0u, outm = 0u;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const uint32_t tk = (T >> (8 * k + 7)) & 1u;
-      const uint32_t ik = tk & (id[k] - B < static_cast<uint32_t>(GW_IDS) ? 1u : 0u);
-      inm |= ik << k;
-      outm |= (tk & ~ik) << k;
-    }
-    // bitmap: the lane's ids OR-ed in word by word (one shared atomic per word)
-    if (!SKIP && w == 0x01010101u && lane_sum == 4u && inm == 0xfu) {
-      // four deltas of 1 (a run, the common case): one bit range
-      const uint32_t olo = excl + 1u - B, ohi = excl + 4u - B;
-      const uint32_t mlo = 0xffffffffu << (olo & 31), mhi = 0xffffffffu >> (31 - (ohi & 31));
-      if ((olo >> 5) == (ohi >> 5)) {
-        atomicOr(bm + (olo >> 5), mlo & mhi);
-      } else {
-        atomicOr(bm + (olo >> 5), mlo);
-        atomicOr(bm + (ohi >> 5), mhi);
-      }
-    } else if (inm) {
-      uint32_t cw = 0xffffffffu, cm = 0u;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        bool keep = (inm >> k) & 1u;
-        if (SKIP && keep) keep = a.changed_in[id[k]] != 0;
-        if (keep) {
-          const uint32_t off = id[k] - B;
-          const uint32_t wd = off >> 5;
-          if (wd != cw) {
-            if (cm) atomicOr(bm + cw, cm);
-            cw = wd;
-            cm = 0u;
-          }
-          cm |= 1u << (off & 31);
-        }
-      }
-      if (cm) atomicOr(bm + cw, cm);
-    }
-    const uint32_t anyin = __ballot_sync(FULL, inm != 0u);
-    const uint32_t anyout = __ballot_sync(FULL, outm != 0u);
-    if (anyin) {  // advance past the last in-window terminator
-      const int L = 31 - __clz(anyin);
-      const int lk = 31 - __clz(__shfl_sync(FULL, inm, L));
-      c.base = __shfl_sync(FULL, sel4(id, lk), L);
-      c.pos += 4 * L + lk + 1;
-    }
-    if (anyout) {
-      // the next window resumes here: pull its bytes into L2 now (the row's
-      // decode is a chain of dependent 128-byte steps)
-      if (lane < 16) prefetch_l2(a.stream + c.pos + 128 * lane);
-      const int L = __ffs(anyout) - 1;
-      const int fk = __ffs(__shfl_sync(FULL, outm, L)) - 1;
-      return __shfl_sync(FULL, sel4(id, fk), L);
-    }
-    if (!anyin) {  // unreachable on a validated stream (a step always holds a terminator)
-      c.pos = c.end;
-      break;
-    }
-  }
-  return 0xffffffffu;
-}
-
-// Same contract as decode_to_bitmap, 512 bytes per step (16 per lane): the
-// per-step costs -- the warp prefix sum, the votes, the cursor update -- are
-// paid once per 512 bytes instead of once per 128.  Every in-window id sets
+// and returns the first id not consumed (~0 when the row is exhausted).  512
+// bytes per step, 16 per lane, the decode_step4 arithmetic (the per-step
+// costs -- the warp prefix sum, the votes, the cursor update -- paid once per
+// 512 bytes); a byte belongs to the row iff it lies before the row's end
+// offset, and the terminators whose id falls in the window are a prefix of the
+// step's, so the cursor advances to just past the last one and the rest are
+// decoded again by the next window.  Every in-window id sets
 // its bit with its own shared atomicOr (lanes 16 ids apart: 2-way conflicts).
 template <bool SKIP>
 __device__ __forceinline__ uint32_t decode16_to_bitmap(const UnionArgs& a, RowPos& c, uint32_t B, uint32_t* bm,
@@ -1557,10 +1457,10 @@ __global__ void __launch_bounds__(256, FILL ? 2 : 3) run_index_kernel(RunIndexAr
         const uint32_t m2 = m1 & __funnelshift_l(Fp, F, 16);
         const uint32_t m3 = m2 & __funnelshift_l(Fp, F, 24);
         const uint32_t m4 = m3 & Fp;
-        D[i] = (m1 >> 7) + (m2 >> 7) + (m3 >> 7) + (m4 >> 7);
+        D[i] = ((m1 >> 7) + (m2 >> 7) + (m3 >> 7) + (m4 >> 7)) * 7u;  // 7 d per byte
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          const uint32_t c = ((w >> (8 * k)) & 0x7fu) << (7 * ((D[i] >> (8 * k)) & 0xffu));
+          const uint32_t c = byte_of(w & 0x7f7f7f7fu, k) << byte_of(D[i], k);
           lane_sum += c;
           vl = ((F >> (8 * k + 7)) & 1u) ? vl + c : 0u;  // value of the chain still open after this byte
         }
@@ -1586,7 +1486,7 @@ __global__ void __launch_bounds__(256, FILL ? 2 : 3) run_index_kernel(RunIndexAr
         const uint32_t w = x[i];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          const uint32_t c = ((w >> (8 * k)) & 0x7fu) << (7 * ((D[i] >> (8 * k)) & 0xffu));
+          const uint32_t c = byte_of(w & 0x7f7f7f7fu, k) << byte_of(D[i], k);
           id += c;
           seg += c;
           if ((T[i] >> (8 * k + 7)) & 1u) {
@@ -1624,7 +1524,7 @@ __global__ void __launch_bounds__(256, FILL ? 2 : 3) run_index_kernel(RunIndexAr
           const uint32_t w = x[i];
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            const uint32_t c = ((w >> (8 * k)) & 0x7fu) << (7 * ((D[i] >> (8 * k)) & 0xffu));
+            const uint32_t c = byte_of(w & 0x7f7f7f7fu, k) << byte_of(D[i], k);
             id2 += c;
             seg2 += c;
             if ((T[i] >> (8 * k + 7)) & 1u) {
