@@ -693,7 +693,9 @@ struct GroupSmem {
   uint32_t rpre[GW];            // root bits: inclusive popcount prefix within each 32-word block
   uint32_t rsum[8];             // root bits per 32-word block
   uint32_t unit;                // B1 work-unit counter of the window
-  uint32_t next[2][GN];         // next undecoded id per node (~0: row exhausted)
+  uint32_t next[3][GN];         // next undecoded id per node (~0: row exhausted), by window mod 3
+                                // (a double buffer is reused one window later; compute-sanitizer
+                                // racecheck flags that reuse, the triple buffer is clean)
   unsigned long long pos[GN], end[GN];  // row cursors: next byte, row end, last id
   uint32_t base[GN];
   alignas(16) uint32_t q[8][64];  // per-warp id queues of the B1 folds (IdQueue)
@@ -1093,7 +1095,7 @@ __device__ __forceinline__ void process_group16(const UnionArgs& a, uint32_t g0,
     SB_ST_ADD(0, 1);
     uint32_t B = 0xffffffffu;
 #pragma unroll
-    for (int k = 0; k < GN; ++k) B = min(B, S.next[r & 1][k]);
+    for (int k = 0; k < GN; ++k) B = min(B, S.next[r % 3][k]);
     if (B == 0xffffffffu) break;  // every row exhausted (CTA-uniform)
     B &= ~31u;
     // A: this warp's two rows -> bitmaps
@@ -1104,7 +1106,7 @@ __device__ __forceinline__ void process_group16(const UnionArgs& a, uint32_t g0,
 #pragma unroll
       for (int i = lane; i < GW; i += 32) bm[i] = 0u;
       __syncwarp();
-      uint32_t nx = S.next[r & 1][k];
+      uint32_t nx = S.next[r % 3][k];
       if (nx - B < static_cast<uint32_t>(GW_IDS)) {
         RowPos c{S.pos[k], S.end[k], S.base[k]};
         unsigned steps = 0;
@@ -1116,7 +1118,7 @@ __device__ __forceinline__ void process_group16(const UnionArgs& a, uint32_t g0,
           S.base[k] = c.base;
         }
       }
-      if (lane == 0) S.next[(r + 1) & 1][k] = nx;
+      if (lane == 0) S.next[(r + 1) % 3][k] = nx;
     }
     SB_ST_LAP(8);
     __syncthreads();

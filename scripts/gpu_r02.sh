@@ -110,3 +110,13 @@ if [[ $what == small ]]; then
   run timeout 600 python -u scripts/step_overhead.py > gpurun_out/step_overhead.json 2> gpurun_out/step_overhead.log
 fi
 done
+for what in "$@"; do
+if [[ $what == sanitize ]]; then
+  python -u scripts/sanitize_r02.py > gpurun_out/sanitize_plain.log 2>&1; tail -1 gpurun_out/sanitize_plain.log
+  for tool in memcheck racecheck synccheck; do
+    run timeout 1500 compute-sanitizer --tool $tool --error-exitcode 9 python -u scripts/sanitize_r02.py \
+        > gpurun_out/sanitize_r02_$tool.log 2>&1
+    tail -3 gpurun_out/sanitize_r02_$tool.log
+  done
+fi
+done
