@@ -346,6 +346,7 @@ static int graph_create(uint64_t n, const uint64_t* offsets, const uint32_t* deg
     g->chunk_byte.push_back(offsets[node_begin + cn] - b0);  // slice-relative start of the chunk's bytes
   }
   const size_t nk = g->chunk_node.size() - 1;
+  GK(dalloc(&g->d_chunk_rng, nk * 2 * 4));
   g->val_ev.resize(nk, nullptr);
   for (size_t k = 0; k < nk; ++k) {
     cudaEvent_t copied = nullptr;
@@ -357,6 +358,8 @@ static int graph_create(uint64_t n, const uint64_t* offsets, const uint32_t* deg
     GK(cudaStreamWaitEvent(g->val_stream, copied, 0));
     cudaEventDestroy(copied);  // released once the wait is enqueued
     GK(launch_validate(g, g->chunk_node[k], g->chunk_node[k + 1], g->val_stream));
+    GK(sb::launch_chunk_range(g->d_node_lo, g->d_node_hi, g->chunk_node[k], g->chunk_node[k + 1],
+                              g->d_chunk_rng + 2 * k, g->val_stream));
     GK(cudaEventRecord(g->val_ev[k], g->val_stream));
   }
   g->pending = true;

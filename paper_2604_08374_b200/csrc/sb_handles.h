@@ -238,6 +238,7 @@ struct sb_graph {
   unsigned long long* d_err = nullptr;  // [0] min bad node, [1] max run
   cudaStream_t up_stream = nullptr, val_stream = nullptr;
   std::vector<cudaEvent_t> val_ev;
+  uint32_t* d_chunk_rng = nullptr;      // per chunk: min first / max last neighbour id (after val_ev[k])
   std::vector<uint64_t> chunk_node, chunk_tile, chunk_item, chunk_byte;
   std::vector<uint32_t> h_node_item;  // local node -> first work item (host copy)
   ~sb_graph() {
@@ -246,7 +247,7 @@ struct sb_graph {
     if (val_stream) cudaStreamSynchronize(val_stream);
     dfree(d_stream); dfree(d_rowoff); dfree(d_deg); dfree(d_orig); dfree(d_node_item);
     dfree(d_item_off); dfree(d_item_base); dfree(d_item_count); dfree(d_item_node);
-    dfree(d_node_lo); dfree(d_node_hi);
+    dfree(d_node_lo); dfree(d_node_hi); dfree(d_chunk_rng);
     dfree(d_tile_node0); dfree(d_tile_q);
     dfree(d_run_off); dfree(d_run_s); dfree(d_run_e);
     dfree(d_cell); dfree(d_comp); dfree(d_comp_sizes);
@@ -298,6 +299,13 @@ struct sb_hb {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   unsigned long long* d_chunk_work = nullptr;
   size_t chunk_work_n = 0;
+  // wavefront first run (pipelined_run): a plane + changed flags per pass >= 2,
+  // a stream per pass, an event per (pass, chunk), pass start / end events
+  std::vector<uint8_t*> d_xplane, d_xchg;
+  std::vector<cudaStream_t> pstream;
+  std::vector<cudaEvent_t> pev, pev_t;
+  unsigned long long* d_pwork = nullptr;
+  size_t pwork_n = 0;
   std::vector<sb_iter_stats> stats;
   sb_iter_stats cur_stats{};
   sb_comm* comm = nullptr;
@@ -324,7 +332,13 @@ struct sb_hb {
       dfree(d_c[i]);
     }
     dfree(d_sum_d); dfree(d_sum_d2); dfree(d_lc); dfree(d_scratch); dfree(d_counter);
-    dfree(d_misc); dfree(d_tmp); dfree(d_st); dfree(d_chunk_work);
+    for (cudaStream_t ps : pstream) cudaStreamSynchronize(ps);
+    dfree(d_misc); dfree(d_tmp); dfree(d_st); dfree(d_chunk_work); dfree(d_pwork);
+    for (uint8_t* x : d_xplane) dfree(x);
+    for (uint8_t* x : d_xchg) dfree(x);
+    for (cudaEvent_t e : pev) cudaEventDestroy(e);
+    for (cudaEvent_t e : pev_t) cudaEventDestroy(e);
+    for (cudaStream_t ps : pstream) cudaStreamDestroy(ps);
     pinned_put(h_misc, h_misc_owned);
     for (auto& e : ev) if (e) cudaEventDestroy(e);
     if (ev_fork) cudaEventDestroy(ev_fork);

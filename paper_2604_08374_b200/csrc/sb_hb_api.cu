@@ -37,8 +37,27 @@ static int hb_init(sb_hb* h) {
   return SB_OK;
 }
 
-// Interval mode: runs of consecutive ids per work item, decoded once from the
-// device-resident LEB128 stream (count pass, host scan, fill pass).
+// Union arguments of this HyperBall: the graph's CSR / items / tiles / group
+// path plus the handle's scratch, with the schedule rules applied.
+static void hb_union_args(const sb_hb* h, sb::UnionArgs& u) {
+  const sb_graph* g = h->g;
+  graph_union_args(g, u);
+  u.scratch = h->d_scratch;
+  u.node_counter = h->d_counter;
+  if (h->flags & SB_HB_SCHEDULE_WARP) u.n_tiles = 0;
+  if (h->flags & SB_HB_SCHEDULE_GROUP) {  // every dense-enough group takes the group path
+    u.node_lo = g->d_node_lo;
+    u.shared_max_edges = ~0ull;
+  } else if (h->p < 9 && g->edges_local < 6000ull * g->n_local) {
+    // rows of <= 128 B on graphs of moderate degree: the gathers the group
+    // path saves are cheap, and the per-node decode + fold is faster (C2,
+    // mean degree 3,730: p=6 0.44 vs 0.80 ms, p=8 1.07 vs 1.56 ms); at C3
+    // (mean degree 20,278) the shared gathers win also at p=8 (22.0 vs 29.2 ms;
+    // profiles/r02/group_threshold.json)
+    u.node_lo = nullptr;
+  }
+}
+
 extern "C" {
 
 int sb_hb_create(sb_graph* g, unsigned p, uint32_t depth_limit, uint32_t flags, sb_hb** out) {
@@ -157,26 +176,12 @@ int sb_hb_step_compute(sb_hb* h, double* local_max) {
   if (g->n_local) {
     CK(cudaMemsetAsync(h->d_changed[N] + g->v0, 0, g->n_local, h->stream));
     sb::UnionArgs u{};
-    graph_union_args(g, u);
+    hb_union_args(h, u);
     u.cur = h->d_plane[L];
     u.next = h->d_plane[N];
-    u.scratch = h->d_scratch;
-    u.node_counter = h->d_counter;
     u.changed_out = h->d_changed[N];
     u.changed_in = h->d_changed[L];
     u.work = h->d_misc;
-    if (h->flags & SB_HB_SCHEDULE_WARP) u.n_tiles = 0;
-    if (h->flags & SB_HB_SCHEDULE_GROUP) {  // every dense-enough group takes the group path
-      u.node_lo = g->d_node_lo;
-      u.shared_max_edges = ~0ull;
-    } else if (h->p < 9 && g->edges_local < 6000ull * g->n_local) {
-      // rows of <= 128 B on graphs of moderate degree: the gathers the group
-      // path saves are cheap, and the per-node decode + fold is faster (C2,
-      // mean degree 3,730: p=6 0.44 vs 0.80 ms, p=8 1.07 vs 1.56 ms); at C3
-      // (mean degree 20,278) the shared gathers win also at p=8 (22.0 vs 29.2 ms;
-      // profiles/r02/group_threshold.json)
-      u.node_lo = nullptr;
-    }
     u.npeers = h->npeers;
     u.peer_next = h->d_peer_plane[N];
     u.peer_changed = h->d_peer_chg[N];
@@ -374,8 +379,228 @@ int sb_hb_step(sb_hb* h, double* max_increase, int* converged, int* finished) {
   return sb_hb_step_finish(h, mx, converged, finished);
 }
 
+}  // extern "C"
+
+// First run over a graph still uploading (sb_graph_create_async), dense mode,
+// one unsharded graph: a wavefront over the upload chunks instead of one pass
+// after another.  Pass p of chunk k reads pass p-1 of every chunk its rows
+// reference -- the chunk's neighbour-id range, reduced at validation -- so
+// passes 2, 3, ... start on the first chunks while later chunks still cross
+// PCIe.  Every pass of the wavefront writes its own plane and changed flags
+// (overlapping passes never overwrite what another still reads), on its own
+// stream (higher priority for earlier passes), each chunk launch waiting on
+// the events of the chunk-passes it reads.  Estimates run on h->stream in pass
+// order once a pass is complete; a pass counts only if the previous one did
+// not finish the run, and the state handed back is exactly the stepped run's
+// (bit-identical: each row is the same max over the same rows).
+// Sets *done when the run finished inside the wavefront; otherwise the caller
+// continues with ordinary steps from the state left in d_plane[latest].
+static int pipelined_run(sb_hb* h, bool* done) {
+  *done = false;
+  sb_graph* g = h->g;
+  if (!g->pending || !g->d_chunk_rng || g->chunk_node.size() < 3 || h->t != 0 || h->finished || h->computed)
+    return SB_OK;
+  if ((h->flags & (SB_HB_INTERVAL | SB_HB_SKIP_UNCHANGED | SB_HB_SCHEDULE_WARP)) || h->npeers || h->comm)
+    return SB_OK;
+  if (g->v0 != 0 || g->n_local != g->n) return SB_OK;
+  DeviceGuard dg(g->device);
+  const int nk = static_cast<int>(g->chunk_node.size() - 1);
+  const uint64_t plane = g->n * h->row;
+  // passes that may overlap the upload: a plane each, within a quarter of free HBM
+  int P = 12;
+  if (h->depth) P = std::min<int>(P, static_cast<int>(h->depth));
+  size_t fr = 0, tot = 0;
+  CK(cudaMemGetInfo(&fr, &tot));
+  while (P > 2 && static_cast<uint64_t>(P - 1) * (plane + 64 + g->n) > fr / 4) --P;
+  if (P < 2) return SB_OK;
+  // resources (kept on the handle: the next first run reuses them)
+  while (static_cast<int>(h->d_xplane.size()) < P - 1) {
+    uint8_t* x = nullptr;
+    uint8_t* c = nullptr;
+    CK(dalloc(&x, plane + 64));
+    h->d_xplane.push_back(x);
+    CK(dalloc(&c, g->n));
+    h->d_xchg.push_back(c);
+  }
+  while (static_cast<int>(h->pstream.size()) < P) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);  // hi is the numerically smaller, higher priority
+    const int pr = std::max(hi, std::min(lo, hi + static_cast<int>(h->pstream.size())));
+    cudaStream_t st = nullptr;
+    CK(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, pr));
+    h->pstream.push_back(st);
+  }
+  while (static_cast<int>(h->pev.size()) < P * nk) {
+    cudaEvent_t e = nullptr;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    h->pev.push_back(e);
+  }
+  while (static_cast<int>(h->pev_t.size()) < 2 * P) {
+    cudaEvent_t e = nullptr;
+    CK(cudaEventCreate(&e));
+    h->pev_t.push_back(e);
+  }
+  if (h->pwork_n < static_cast<size_t>(P * nk)) {
+    dfree(h->d_pwork);
+    h->pwork_n = 0;
+    CK(dalloc(&h->d_pwork, static_cast<size_t>(P * nk) * 8));
+    h->pwork_n = static_cast<size_t>(P * nk);
+  }
+  // pass p's registers / changed flags: p = 0 the initialised plane, p = 1
+  // the second plane, p >= 2 the extra ones
+  auto pl = [&](int p) { return p == 0 ? h->d_plane[0] : p == 1 ? h->d_plane[1] : h->d_xplane[p - 2]; };
+  auto cg = [&](int p) { return p == 0 ? h->d_changed[0] : p == 1 ? h->d_changed[1] : h->d_xchg[p - 2]; };
+  CK(cudaMemsetAsync(h->d_pwork, 0, static_cast<size_t>(P * nk) * 8, h->stream));
+  CK(cudaEventRecord(h->ev[0], h->stream));  // init + counters done before any pass starts
+  for (int p = 0; p < P; ++p) CK(cudaStreamWaitEvent(h->pstream[p], h->ev[0], 0));
+  sb::UnionArgs base{};
+  hb_union_args(h, base);
+  base.err = g->d_err;  // every CTA stops if a chunk failed validation
+  std::vector<int> dlo(nk, 0), dhi(nk, -1), next(P + 1, 0);
+  auto chunk_of = [&](uint64_t id) {
+    const int k = static_cast<int>(std::upper_bound(g->chunk_node.begin(), g->chunk_node.end(), id) -
+                                   g->chunk_node.begin()) - 1;
+    return std::min(std::max(k, 0), nk - 1);
+  };
+  auto launch = [&](int p, int k) -> int {  // pass p (1-based) of chunk k
+    cudaStream_t st = h->pstream[p - 1];
+    if (k == 0) CK(cudaEventRecord(h->pev_t[2 * (p - 1)], st));
+    if (p == 1) {
+      CK(cudaStreamWaitEvent(st, g->val_ev[k], 0));
+    } else {
+      // the chunks its rows reference, and always the chunk itself (its items'
+      // partial rows and arrival counters are reused by the next pass)
+      if (k < dlo[k] || k > dhi[k]) CK(cudaStreamWaitEvent(st, h->pev[(p - 2) * nk + k], 0));
+      for (int j = dlo[k]; j <= dhi[k]; ++j) CK(cudaStreamWaitEvent(st, h->pev[(p - 2) * nk + j], 0));
+    }
+    const uint64_t n0 = g->chunk_node[k], n1 = g->chunk_node[k + 1];
+    CK(cudaMemsetAsync(cg(p) + n0, 0, n1 - n0, st));
+    const uint64_t t0 = g->chunk_tile[k], t1 = g->chunk_tile[k + 1];
+    if (t1 > t0) {
+      sb::UnionArgs u = base;
+      u.cur = pl(p - 1);
+      u.next = pl(p);
+      u.changed_in = cg(p - 1);
+      u.changed_out = cg(p);
+      u.work = h->d_pwork + (p - 1) * nk + k;
+      u.tile_node0 = g->d_tile_node0 + t0;
+      u.tile_q = g->d_tile_q + t0;
+      u.n_tiles = t1 - t0;
+      CK(sb::launch_union(static_cast<int>(h->p), false, u, st));
+    }
+    CK(cudaEventRecord(h->pev[(p - 1) * nk + k], st));
+    if (k == nk - 1) CK(cudaEventRecord(h->pev_t[2 * (p - 1) + 1], st));
+    return SB_OK;
+  };
+  int rc = SB_OK;
+  // pass 1 of every chunk waits only for its upload + validation
+  for (int k = 0; k < nk && !rc; ++k) rc = launch(1, k);
+  next[1] = nk;
+  int P_enq = 1;
+  // as each chunk lands: its neighbour range, then -- while later chunks are
+  // still uploading -- every chunk-pass whose inputs are all enqueued (in chunk
+  // order per pass).  Passes are started only while the upload is in flight:
+  // that work fills time the GPU would otherwise wait; once the last chunk is
+  // in, the started passes are completed and the rest run one by one, so no
+  // pass beyond the converging one is computed unless it overlapped the upload.
+  for (int k = 0; k < nk && !rc; ++k) {
+    CK(cudaEventSynchronize(g->val_ev[k]));
+    uint32_t r[2] = {0u, 0u};
+    CK(cudaMemcpy(r, g->d_chunk_rng + 2 * k, 8, cudaMemcpyDeviceToHost));
+    if (r[0] <= r[1]) {
+      dlo[k] = chunk_of(r[0]);
+      dhi[k] = chunk_of(r[1]);
+    }
+    if (k == nk - 1) break;
+    for (int p = 2; p <= P && !rc; ++p) {
+      while (next[p] <= k && !rc && std::max(dhi[next[p]], next[p]) < next[p - 1]) {
+        rc = launch(p, next[p]++);
+        P_enq = std::max(P_enq, p);
+      }
+    }
+  }
+  auto drain = [&] {  // every launched chunk-pass done (scratch / counters are shared)
+    for (int p = 0; p < P_enq; ++p) cudaStreamSynchronize(h->pstream[p]);
+  };
+  if (rc) {
+    drain();
+    return rc;
+  }
+  rc = graph_wait(g);  // upload complete: a malformed stream is reported here
+  if (rc) {
+    drain();
+    return rc;
+  }
+  // complete the passes already started
+  for (int p = 2; p <= P_enq && !rc; ++p)
+    while (next[p] < nk && !rc) rc = launch(p, next[p]++);
+  if (rc) {
+    drain();
+    return rc;
+  }
+  // estimates in pass order (Alg. 1: union -> estimate -> accumulate -> test)
+  int last = 0;
+  for (int p = 1; p <= P_enq; ++p) {
+    h->t = static_cast<uint32_t>(p);
+    h->cur_stats = sb_iter_stats{};
+    h->cur_stats.t = h->t;
+    CK(cudaMemsetAsync(h->d_misc, 0, 4 * 8, h->stream));
+    CK(cudaStreamWaitEvent(h->stream, h->pev_t[2 * (p - 1) + 1], 0));
+    CK(cudaEventRecord(h->ev[2], h->stream));
+    sb::EstArgs e{};
+    e.plane = pl(p);
+    e.node_begin = g->v0;
+    e.n_local = g->n_local;
+    e.lc = h->d_lc;
+    e.alpha = h->alpha;
+    e.m = static_cast<double>(1u << h->p);
+    e.c_prev = h->d_c[(p - 1) & 1];
+    e.c_cur = h->d_c[p & 1];
+    e.sum_d = h->d_sum_d;
+    e.sum_d2 = h->d_sum_d2;
+    e.changed = cg(p);
+    e.t = h->t;
+    e.max_ord = h->d_misc + 1;
+    e.changed_count = h->d_misc + 2;
+    CK(sb::launch_estimate(static_cast<int>(h->p), 1, e, h->stream));
+    CK(cudaEventRecord(h->ev[3], h->stream));
+    CK(cudaMemcpyAsync(h->h_misc, h->d_misc, 4 * 8, cudaMemcpyDeviceToHost, h->stream));
+    CK(sync_stream(h->stream));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, h->pev_t[2 * (p - 1)], h->pev_t[2 * (p - 1) + 1]);
+    h->cur_stats.union_ms = ms;  // span of the pass's chunk launches (they overlap other passes)
+    cudaEventElapsedTime(&ms, h->ev[2], h->ev[3]);
+    h->cur_stats.estimate_ms = ms;
+    cudaEventElapsedTime(&ms, h->pev_t[2 * (p - 1)], h->ev[3]);
+    h->cur_stats.step_ms = ms;
+    h->cur_stats.changed_nodes = h->h_misc[2];
+    const double mx = decode_ord(h->h_misc[1]);
+    h->converged = sb_check_convergence(mx) != 0;
+    h->finished = h->converged || (h->depth != 0 && h->t == h->depth);
+    h->cur_stats.max_increase = mx;
+    h->stats.push_back(h->cur_stats);
+    last = p;
+    if (h->finished) break;
+  }
+  // hand over to the two-plane stepping: d_plane[last & 1] holds pass `last`,
+  // the other plane pass last - 1 (the "previous" registers), as after `last` steps
+  for (int p = 0; p < P_enq; ++p) CK(cudaStreamWaitEvent(h->stream, h->pev_t[2 * p + 1], 0));
+  for (int p = std::max(last - 1, 0); p <= last; ++p) {
+    if (pl(p) != h->d_plane[p & 1]) CK(cudaMemcpyAsync(h->d_plane[p & 1], pl(p), plane, cudaMemcpyDeviceToDevice, h->stream));
+    if (cg(p) != h->d_changed[p & 1]) CK(cudaMemcpyAsync(h->d_changed[p & 1], cg(p), g->n, cudaMemcpyDeviceToDevice, h->stream));
+  }
+  CK(sync_stream(h->stream));
+  h->latest = last & 1;
+  *done = h->finished;
+  return SB_OK;
+}
+
+extern "C" {
+
 int sb_hb_run(sb_hb* h, uint32_t* iterations, int* converged) {
   if (!h) return fail(SB_EINVAL, "NULL handle");
+  bool done = false;
+  if (const int rc = pipelined_run(h, &done)) return rc;
   int conv = 0, fin = h->finished ? 1 : 0;
   while (!fin) {
     const int rc = sb_hb_step(h, nullptr, &conv, &fin);

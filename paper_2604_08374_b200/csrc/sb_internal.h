@@ -204,6 +204,8 @@ cudaError_t launch_local(const LocalArgs& a, bool smem, bool n2_bitmap, int* gri
 size_t local_smem_limit();
 
 cudaError_t launch_build_items(const BuildArgs& a, cudaStream_t s);
+cudaError_t launch_chunk_range(const uint32_t* lo, const uint32_t* hi, uint64_t n0, uint64_t n1, uint32_t* out,
+                               cudaStream_t s);
 cudaError_t launch_init(int p, uint8_t* plane, uint64_t n, const uint32_t* orig, cudaStream_t s);
 cudaError_t launch_union(int p, bool skip, const UnionArgs& a, cudaStream_t s);
 cudaError_t launch_st_build(int p, const uint8_t* cur, uint8_t* st, uint64_t n, int levels, cudaStream_t s,

@@ -1959,6 +1959,41 @@ static int grid_for(const void* fn, int block, size_t smem = 0) {
     default: return cudaErrorInvalidValue; \
   }
 
+// Neighbour-id range of nodes [n0, n1) from the validation output: out[0] =
+// min first id, out[1] = max last id (rows without neighbours hold ~0 / 0, the
+// neutral elements; a chunk without edges gets out[0] > out[1]).
+__global__ void __launch_bounds__(256) chunk_range_kernel(const uint32_t* __restrict__ lo,
+                                                          const uint32_t* __restrict__ hi, uint64_t n0, uint64_t n1,
+                                                          uint32_t* out) {
+  __shared__ uint32_t smn[8], smx[8];
+  uint32_t mn = 0xffffffffu, mx = 0u;
+  for (uint64_t v = n0 + threadIdx.x; v < n1; v += blockDim.x) {
+    mn = min(mn, lo[v]);
+    mx = max(mx, hi[v]);
+  }
+  mn = __reduce_min_sync(FULL, mn);
+  mx = __reduce_max_sync(FULL, mx);
+  if ((threadIdx.x & 31) == 0) {
+    smn[threadIdx.x >> 5] = mn;
+    smx[threadIdx.x >> 5] = mx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w) {
+      mn = min(mn, smn[w]);
+      mx = max(mx, smx[w]);
+    }
+    out[0] = mn;
+    out[1] = mx;
+  }
+}
+
+cudaError_t launch_chunk_range(const uint32_t* lo, const uint32_t* hi, uint64_t n0, uint64_t n1, uint32_t* out,
+                               cudaStream_t s) {
+  chunk_range_kernel<<<1, 256, 0, s>>>(lo, hi, n0, n1, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_build_items(const BuildArgs& a, cudaStream_t s) {
   const int g = grid_for(reinterpret_cast<const void*>(build_items_kernel), 256);
   build_items_kernel<<<g, 256, 0, s>>>(a);

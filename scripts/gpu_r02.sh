@@ -120,3 +120,10 @@ if [[ $what == sanitize ]]; then
   done
 fi
 done
+for what in "$@"; do
+if [[ $what == wave ]]; then
+  run timeout 1500 python -u -m pytest tests/test_gpu_async_upload.py -q -x > gpurun_out/pytest_async.log 2>&1; tail -2 gpurun_out/pytest_async.log
+  run timeout 600 python -u -m pytest tests/test_gpu_parity.py -q -x -k "c3_pipelined or c3_matches" > gpurun_out/pytest_c3.log 2>&1; tail -2 gpurun_out/pytest_c3.log
+  run timeout 600 python -u scripts/e2e_breakdown.py > gpurun_out/e2e_breakdown.txt 2>&1
+fi
+done

@@ -111,3 +111,87 @@ def test_async_upload_interval_malformed_stream(bad):
     ref = HyperBall(ok, 10, None)
     ref.run()
     assert np.array_equal(h.registers(), ref.registers())
+
+
+# ---------------------------------------------------------------- wavefront first run
+# sb_hb_run over a graph still uploading runs passes 2, 3, ... on the first
+# chunks while later chunks cross PCIe (pipelined_run, sb_hb_api.cu).  Graphs
+# whose rows reference only nearby ids (grids with a radius) engage it; the
+# result must equal the stepped run on the synchronously uploaded graph in
+# every observable: registers (latest and previous), c, sum_d, sum_d2, t,
+# convergence, the per-iteration max increases and changed counts.
+def wave_graphs():
+    yield "grid_r6", CompressedCsr.synth_grid(150, 150, 30, 2, 6, 5, 6 * 6)       # deps +-1-2 chunks
+    yield "strip_r3", CompressedCsr.synth_grid(400, 40, 10, 1, 4, 9, 3 * 3)        # long diameter: many passes
+    yield "open_r12", CompressedCsr.synth_grid(120, 120, 0, 1, 1, 1, 12 * 12)      # denser rows, group path at p>=9
+    yield "global", CompressedCsr.synth_grid(40, 40, 6, 2, 4, 3, 0)                # unlimited radius: every chunk depends on all
+
+
+def _same_run(a, b):
+    assert np.array_equal(a.registers(), b.registers())
+    assert np.array_equal(a.registers("previous"), b.registers("previous"))
+    sa, sb = a.state(), b.state()
+    assert (sa.t, sa.converged, sa.finished) == (sb.t, sb.converged, sb.finished)
+    assert np.array_equal(sa.c_curr, sb.c_curr) and np.array_equal(sa.c_prev, sb.c_prev)
+    assert np.array_equal(sa.sum_d, sb.sum_d) and np.array_equal(sa.sum_d2, sb.sum_d2)
+    ka, kb = a.stats(), b.stats()
+    assert [x["max_increase"] for x in ka] == [x["max_increase"] for x in kb]
+    assert [x["changed_nodes"] for x in ka] == [x["changed_nodes"] for x in kb]
+
+
+@pytest.mark.parametrize("depth", [None, 2, 3, 5])
+@pytest.mark.parametrize("p", [4, 6, 10, 12])
+@pytest.mark.parametrize("name,g", list(wave_graphs()), ids=[n for n, _ in wave_graphs()])
+def test_pipelined_first_run_bit_identical(name, g, p, depth):
+    ref = HyperBall(g, p, depth)
+    ref.run()
+    hb = HyperBall(DeviceGraph(g, async_upload=True), p, depth)
+    hb.run()
+    _same_run(hb, ref)
+    # the handle keeps working: reset and a second (device-resident) run
+    hb.reset()
+    hb.run()
+    _same_run(hb, ref)
+
+
+@pytest.mark.parametrize("sched", ["group", "items"])
+def test_pipelined_first_run_schedules(sched):
+    g = CompressedCsr.synth_grid(150, 150, 30, 2, 6, 5, 6 * 6)
+    ref = HyperBall(g, 10, None)
+    ref.run()
+    hb = HyperBall(DeviceGraph(g, async_upload=True), 10, None, schedule=sched)
+    hb.run()
+    _same_run(hb, ref)
+
+
+def _corrupt_middle_row(kind):
+    """A valid radius grid (16 upload chunks) with one bad varint in a row of the
+    9th chunk: a zero delta, or a delta of 2^31 (ids far outside the plane)."""
+    g = CompressedCsr.synth_grid(150, 150, 30, 2, 6, 5, 6 * 6)
+    offs, deg, st = g.offsets.copy(), g.degrees.copy(), bytearray(g.stream.tobytes())
+    v = g.n * 9 // 16
+    a, b = int(offs[v]), int(offs[v + 1])
+    row = st[a:b]
+    k = len(row) // 2
+    while row[k] & 0x80 or row[k - 1] & 0x80:  # a one-byte varint in the middle
+        k += 1
+    if kind == "zero":
+        st[a + k] = 0
+        return CompressedCsr.from_arrays(offs, deg, bytes(st))
+    new = bytes(st[:a + k]) + bytes([0x80, 0x80, 0x80, 0x80, 0x08]) + bytes(st[a + k + 1:])
+    offs[v + 1:] += 4
+    return CompressedCsr.from_arrays(offs, deg, new)
+
+
+@pytest.mark.parametrize("kind", ["zero", "huge"])
+def test_pipelined_first_run_reports_malformed_stream(kind):
+    g = _corrupt_middle_row(kind)
+    hb = HyperBall(DeviceGraph(g, async_upload=True), 10, None)
+    with pytest.raises(RuntimeError):
+        hb.run()
+    ok = CompressedCsr.synth_grid(60, 70, 20, 2, 6, 3, 9 * 9)
+    h = HyperBall(DeviceGraph(ok, async_upload=True), 10, None)
+    h.run()
+    ref = HyperBall(ok, 10, None)
+    ref.run()
+    assert np.array_equal(h.registers(), ref.registers())
