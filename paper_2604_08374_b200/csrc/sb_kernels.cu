@@ -124,16 +124,18 @@ __global__ void __launch_bounds__(256, 3) build_items_kernel(BuildArgs a) {
       qn = make_uint4(0u, 0u, 0u, 0u);
       if (lb + 512 < end) qn = __ldg(reinterpret_cast<const uint4*>(a.stream + lb + 512));
       // valid-byte flags (0x80 per byte in [pos0, end)); invalid bytes -> 0x00
-      uint32_t vm[4];
+      uint32_t vm[4] = {0x80808080u, 0x80808080u, 0x80808080u, 0x80808080u};
+      if (wb < pos0 || wb + 512 > end) {  // warp-uniform: only a row's first / last window is partial
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int64_t lo = static_cast<int64_t>(pos0) - static_cast<int64_t>(lb + 4 * i);  // bytes below pos0
-        const int64_t hi = static_cast<int64_t>(end) - static_cast<int64_t>(lb + 4 * i);   // bytes below end
-        uint32_t m = 0x80808080u;
-        if (lo > 0) m = lo >= 4 ? 0u : m << (8 * lo);
-        if (hi < 4) m &= hi <= 0 ? 0u : 0x80808080u >> (8 * (4 - hi));
-        vm[i] = m;
-        x[i] &= (m >> 7) * 0xffu;
+        for (int i = 0; i < 4; ++i) {
+          const int64_t lo = static_cast<int64_t>(pos0) - static_cast<int64_t>(lb + 4 * i);  // bytes below pos0
+          const int64_t hi = static_cast<int64_t>(end) - static_cast<int64_t>(lb + 4 * i);   // bytes below end
+          uint32_t m = 0x80808080u;
+          if (lo > 0) m = lo >= 4 ? 0u : m << (8 * lo);
+          if (hi < 4) m &= hi <= 0 ? 0u : 0x80808080u >> (8 * (4 - hi));
+          vm[i] = m;
+          x[i] &= (m >> 7) * 0xffu;
+        }
       }
       uint32_t p3 = __shfl_up_sync(FULL, x[3], 1), p2 = __shfl_up_sync(FULL, x[2], 1);
       if (lane == 0) {
@@ -1436,16 +1438,21 @@ __global__ void __launch_bounds__(256, FILL ? 2 : 3) run_index_kernel(RunIndexAr
       qn = make_uint4(0u, 0u, 0u, 0u);
       if (lb + 512 < end) qn = __ldg(reinterpret_cast<const uint4*>(a.stream + lb + 512));
       uint32_t T[4], D[4];
+      uint32_t vm[4] = {0x80808080u, 0x80808080u, 0x80808080u, 0x80808080u};
+      if (wb < pos0 || wb + 512 > end) {  // warp-uniform: only an item's first / last window is partial
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int64_t lo = static_cast<int64_t>(pos0) - static_cast<int64_t>(lb + 4 * i);
-        const int64_t hi = static_cast<int64_t>(end) - static_cast<int64_t>(lb + 4 * i);
-        uint32_t m = 0x80808080u;
-        if (lo > 0) m = lo >= 4 ? 0u : m << (8 * lo);
-        if (hi < 4) m &= hi <= 0 ? 0u : 0x80808080u >> (8 * (4 - hi));
-        x[i] &= (m >> 7) * 0xffu;  // bytes outside the item read as 0x00 (terminators, not counted)
-        T[i] = ~x[i] & m;
+        for (int i = 0; i < 4; ++i) {
+          const int64_t lo = static_cast<int64_t>(pos0) - static_cast<int64_t>(lb + 4 * i);
+          const int64_t hi = static_cast<int64_t>(end) - static_cast<int64_t>(lb + 4 * i);
+          uint32_t m = 0x80808080u;
+          if (lo > 0) m = lo >= 4 ? 0u : m << (8 * lo);
+          if (hi < 4) m &= hi <= 0 ? 0u : 0x80808080u >> (8 * (4 - hi));
+          x[i] &= (m >> 7) * 0xffu;  // bytes outside the item read as 0x00 (terminators, not counted)
+          vm[i] = m;
+        }
       }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) T[i] = ~x[i] & vm[i];
       uint32_t wp3 = __shfl_up_sync(FULL, x[3], 1);
       if (lane == 0) wp3 = c3;
       c3 = __shfl_sync(FULL, x[3], 31);

@@ -127,3 +127,17 @@ if [[ $what == wave ]]; then
   run timeout 600 python -u scripts/e2e_breakdown.py > gpurun_out/e2e_breakdown.txt 2>&1
 fi
 done
+for what in "$@"; do
+if [[ $what == ncu_setup ]]; then
+  run timeout 600 $NCU -k regex:build_items -c 1 -o gpurun_out/prof_build_items \
+      python -u bench.py --profile --no-cpu --no-e2e --no-variants --no-pipeline
+  export_rep c3_build_items prof_build_items
+  run timeout 600 $NCU -k regex:run_index -c 2 -o gpurun_out/prof_run_index python -u scripts/pipeline_profile.py c3
+  export_rep c3_run_index prof_run_index
+fi
+done
+for what in "$@"; do
+if [[ $what == setupcheck ]]; then
+  run timeout 1500 python -u -m pytest tests/test_gpu_validation_fuzz.py tests/test_gpu_async_upload.py tests/test_gpu_parity.py -q -x -k "validation or async or interval or malformed or errors or varint or pipelined" > gpurun_out/pytest_setup.log 2>&1; tail -2 gpurun_out/pytest_setup.log
+fi
+done
