@@ -413,15 +413,22 @@ static int pipelined_run(sb_hb* h, bool* done) {
   CK(cudaMemGetInfo(&fr, &tot));
   while (P > 2 && static_cast<uint64_t>(P - 1) * (plane + 64 + g->n) > fr / 4) --P;
   if (P < 2) return SB_OK;
-  // resources (kept on the handle: the next first run reuses them)
-  while (static_cast<int>(h->d_xplane.size()) < P - 1) {
-    uint8_t* x = nullptr;
-    uint8_t* c = nullptr;
-    CK(dalloc(&x, plane + 64));
-    h->d_xplane.push_back(x);
-    CK(dalloc(&c, g->n));
-    h->d_xchg.push_back(c);
-  }
+  // resources (kept on the handle: the next first run reuses them).  The
+  // planes of passes 2..5 up front -- a graph's first pool growth maps new
+  // memory (slow, and stalls the wavefront if done inside it); passes beyond 5
+  // only start on graphs whose rows reach few chunks, and get theirs on demand
+  auto more_planes = [&](int count) -> int {
+    while (static_cast<int>(h->d_xplane.size()) < count) {
+      uint8_t* x = nullptr;
+      uint8_t* c = nullptr;
+      CK(dalloc(&x, plane + 64));
+      h->d_xplane.push_back(x);
+      CK(dalloc(&c, g->n));
+      h->d_xchg.push_back(c);
+    }
+    return SB_OK;
+  };
+  if (const int rc0 = more_planes(std::min(P - 1, 4))) return rc0;
   while (static_cast<int>(h->pstream.size()) < P) {
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);  // hi is the numerically smaller, higher priority
@@ -463,6 +470,7 @@ static int pipelined_run(sb_hb* h, bool* done) {
     return std::min(std::max(k, 0), nk - 1);
   };
   auto launch = [&](int p, int k) -> int {  // pass p (1-based) of chunk k
+    if (const int rc0 = more_planes(p - 1)) return rc0;
     cudaStream_t st = h->pstream[p - 1];
     if (k == 0) CK(cudaEventRecord(h->pev_t[2 * (p - 1)], st));
     if (p == 1) {
