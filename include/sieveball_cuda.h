@@ -60,6 +60,10 @@ enum {
                                    >= 6000, >= 16 x 4 x SMs nodes, groups within half a resident CTA's share of
                                    the edges); not combinable with SCHEDULE_WARP */
 
+#define SB_HB_WAVEFRONT 16u     /* first sb_hb_run over an sb_graph_create_async graph: run the wavefront
+                                   over the upload chunks whatever the stream size (default: streams
+                                   >= 1 GB; dense mode, one shard; bit-identical either way) */
+
 /* sb_hb_read_registers `which` */
 #define SB_REGS_LATEST 0   /* registers after the last executed iteration (c_t) */
 #define SB_REGS_PREVIOUS 1 /* registers before it (c_{t-1}) */

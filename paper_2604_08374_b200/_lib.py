@@ -16,6 +16,7 @@ SB_HB_SKIP_UNCHANGED = 1
 SB_HB_SCHEDULE_WARP = 2
 SB_HB_INTERVAL = 4
 SB_HB_SCHEDULE_GROUP = 8
+SB_HB_WAVEFRONT = 16
 SB_REGS_LATEST, SB_REGS_PREVIOUS = 0, 1
 SB_COMM_ID_BYTES = 128
 SB_IPC_HANDLE_BYTES = 256

@@ -69,7 +69,7 @@ int sb_hb_create(sb_graph* g, unsigned p, uint32_t depth_limit, uint32_t flags, 
     return fail(SB_EINVAL, "interval mode excludes SB_HB_SKIP_UNCHANGED");
   if ((flags & SB_HB_SCHEDULE_GROUP) && (flags & SB_HB_SCHEDULE_WARP))
     return fail(SB_EINVAL, "SB_HB_SCHEDULE_GROUP excludes SB_HB_SCHEDULE_WARP");
-  if (flags & ~(SB_HB_SKIP_UNCHANGED | SB_HB_SCHEDULE_WARP | SB_HB_INTERVAL | SB_HB_SCHEDULE_GROUP))
+  if (flags & ~(SB_HB_SKIP_UNCHANGED | SB_HB_SCHEDULE_WARP | SB_HB_INTERVAL | SB_HB_SCHEDULE_GROUP | SB_HB_WAVEFRONT))
     return fail(SB_EINVAL, "sb_hb_create: unknown flags 0x%x", flags);
   DeviceGuard dg(g->device);
   auto* h = new sb_hb();
@@ -403,6 +403,9 @@ static int pipelined_run(sb_hb* h, bool* done) {
   if ((h->flags & (SB_HB_INTERVAL | SB_HB_SKIP_UNCHANGED | SB_HB_SCHEDULE_WARP)) || h->npeers || h->comm)
     return SB_OK;
   if (g->v0 != 0 || g->n_local != g->n) return SB_OK;
+  // worth its fixed cost (a stream per pass, events, extra planes) only when
+  // the upload is long: >= 1 GB is >= 18 ms of PCIe (C3: 4.8 GB, 95 ms)
+  if (g->stream_local < (1ull << 30) && !(h->flags & SB_HB_WAVEFRONT)) return SB_OK;
   DeviceGuard dg(g->device);
   const int nk = static_cast<int>(g->chunk_node.size() - 1);
   const uint64_t plane = g->n * h->row;

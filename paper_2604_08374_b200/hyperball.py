@@ -14,7 +14,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from ._lib import (SB_COMM_ID_BYTES, SB_HB_INTERVAL, SB_HB_SCHEDULE_GROUP, SB_HB_SCHEDULE_WARP,
+from ._lib import (SB_COMM_ID_BYTES, SB_HB_INTERVAL, SB_HB_SCHEDULE_GROUP, SB_HB_SCHEDULE_WARP, SB_HB_WAVEFRONT,
                    SB_HB_SKIP_UNCHANGED, SB_IPC_HANDLE_BYTES, SB_REGS_LATEST, SB_REGS_PREVIOUS, check, lib, ptr, sb_iter_stats)
 from .cgraph import CompressedCsr
 
@@ -201,10 +201,13 @@ class HyperBall:
 
     def __init__(self, graph: CompressedCsr | DeviceGraph, params: HllParams | int,
                  depth_limit: int | None = None, device: int = 0, skip_unchanged: bool = False,
-                 node_range: tuple[int, int] | None = None, interval: bool = False, schedule: str = "auto"):
-        """schedule: "auto" (8-node shared-gather groups sized to the device, per-node work
+                 node_range: tuple[int, int] | None = None, interval: bool = False, schedule: str = "auto",
+                 wavefront: bool = False):
+        """schedule: "auto" (16-node shared-gather groups sized to the device, per-node work
         items elsewhere), "group" (groups wherever rows overlap densely, any graph size) or
-        "items" (per-warp work items only).  Every schedule gives identical results."""
+        "items" (per-warp work items only).  wavefront: run the first run() over an
+        asynchronously uploading graph as a wavefront over the upload chunks whatever its
+        size (default: streams >= 1 GB).  Every choice gives identical results."""
         self.params = params if isinstance(params, HllParams) else HllParams(params)
         self.graph = graph if isinstance(graph, DeviceGraph) else DeviceGraph(graph, device, node_range)
         self.depth_limit = depth_limit
@@ -212,7 +215,7 @@ class HyperBall:
         if schedule not in SCHEDULES:
             raise ValueError(f"schedule must be one of {sorted(SCHEDULES)}")
         flags = ((SB_HB_SKIP_UNCHANGED if skip_unchanged else 0) | (SB_HB_INTERVAL if interval else 0)
-                 | SCHEDULES[schedule])
+                 | SCHEDULES[schedule] | (SB_HB_WAVEFRONT if wavefront else 0))
         check(lib().sb_hb_create(self.graph._h, self.params.p, int(depth_limit or 0), flags, C.byref(self._h)))
         self._comm = None
 

@@ -145,7 +145,7 @@ def _same_run(a, b):
 def test_pipelined_first_run_bit_identical(name, g, p, depth):
     ref = HyperBall(g, p, depth)
     ref.run()
-    hb = HyperBall(DeviceGraph(g, async_upload=True), p, depth)
+    hb = HyperBall(DeviceGraph(g, async_upload=True), p, depth, wavefront=True)
     hb.run()
     _same_run(hb, ref)
     # the handle keeps working: reset and a second (device-resident) run
@@ -159,7 +159,7 @@ def test_pipelined_first_run_schedules(sched):
     g = CompressedCsr.synth_grid(150, 150, 30, 2, 6, 5, 6 * 6)
     ref = HyperBall(g, 10, None)
     ref.run()
-    hb = HyperBall(DeviceGraph(g, async_upload=True), 10, None, schedule=sched)
+    hb = HyperBall(DeviceGraph(g, async_upload=True), 10, None, schedule=sched, wavefront=True)
     hb.run()
     _same_run(hb, ref)
 
@@ -186,7 +186,7 @@ def _corrupt_middle_row(kind):
 @pytest.mark.parametrize("kind", ["zero", "huge"])
 def test_pipelined_first_run_reports_malformed_stream(kind):
     g = _corrupt_middle_row(kind)
-    hb = HyperBall(DeviceGraph(g, async_upload=True), 10, None)
+    hb = HyperBall(DeviceGraph(g, async_upload=True), 10, None, wavefront=True)
     with pytest.raises(RuntimeError):
         hb.run()
     ok = CompressedCsr.synth_grid(60, 70, 20, 2, 6, 3, 9 * 9)
