@@ -56,6 +56,11 @@ static void hb_union_args(const sb_hb* h, sb::UnionArgs& u) {
     // profiles/r02/group_threshold.json)
     u.node_lo = nullptr;
   }
+  // Without the group path the per-warp item schedule balances better than
+  // 8-node CTA tiles (C2 p=4 0.246 vs 0.260 ms, p=6 0.356 vs 0.379, C1 p=10
+  // 0.140 vs 0.155; profiles/r02/group_threshold.json) -- except over a graph
+  // still uploading, whose chunks are cut into tile ranges.
+  if (!u.node_lo && !(h->flags & SB_HB_SCHEDULE_GROUP) && !g->pending) u.n_tiles = 0;
 }
 
 extern "C" {

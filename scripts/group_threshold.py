@@ -18,7 +18,7 @@ from scripts.sweep import time_runs  # noqa: E402
 def main():
     torch.cuda.set_device(0)
     out = []
-    for cfg, ps in (("c1", (6, 7, 8, 9, 10)), ("c2", (6, 7, 8, 9, 10)), ("c3", (8, 9))):
+    for cfg, ps in (("c1", (4, 6, 8, 10)), ("c2", (4, 5, 6, 7, 8, 9, 10)), ("c3", (8, 9))):
         g = build_graph(cfg)
         dg = DeviceGraph(g, 0)
         for p in ps:
