@@ -154,6 +154,22 @@ def test_pipelined_first_run_bit_identical(name, g, p, depth):
     _same_run(hb, ref)
 
 
+def test_pipelined_first_run_converges_inside_the_wavefront():
+    """Many small cliques of consecutive ids: every chunk reads only itself, so the
+    wavefront starts passes 2..12 while the upload is in flight, but the run
+    converges at pass 2.  The speculative passes must leave no trace."""
+    k, c = 2000, 8
+    adj = [[b * c + j for j in range(c) if j != i] for b in range(k) for i in range(c)]
+    g = CompressedCsr.from_adjacency(adj)
+    for p in (4, 10):
+        ref = HyperBall(g, p, None)
+        ref.run()
+        hb = HyperBall(DeviceGraph(g, async_upload=True), p, None, wavefront=True)
+        hb.run()
+        assert ref.state().t <= 3
+        _same_run(hb, ref)
+
+
 @pytest.mark.parametrize("sched", ["group", "items"])
 def test_pipelined_first_run_schedules(sched):
     g = CompressedCsr.synth_grid(150, 150, 30, 2, 6, 5, 6 * 6)
