@@ -1346,7 +1346,9 @@ __global__ void __launch_bounds__(256, C::MINB) union_kernel(UnionArgs a) {
       if (lane == 0) u = upload_failed(a) ? total : atomicAdd(a.work, 1ull);
       u = __shfl_sync(FULL, u, 0);
       if (u >= total) break;
-      process_item<P, SKIP, C>(a, u / G::SLICES, static_cast<int>(u % G::SLICES), lane, buf);
+      // slice-major: the warps in flight share one 512-byte slice of the plane
+      // (p >= 11: a slice of every row stays in L2, the whole plane would not)
+      process_item<P, SKIP, C>(a, u % a.n_items, static_cast<int>(u / a.n_items), lane, buf);
     }
   } else {
     const uint64_t total = a.n_tiles * G::SLICES;
@@ -1355,7 +1357,8 @@ __global__ void __launch_bounds__(256, C::MINB) union_kernel(UnionArgs a) {
       __syncthreads();
       const unsigned long long u = s_unit[k & 1];
       if (u >= total) break;
-      const uint64_t t = u / G::SLICES;
+      const uint64_t t = u % a.n_tiles;  // slice-major (see the item schedule)
+      const int slice = static_cast<int>(u / a.n_tiles);
       const uint32_t g0 = a.tile_node0[t];
       const uint32_t q = a.tile_q[t];
       if (GRP && a.node_lo) {  // 16-node group path when the group's rows overlap densely
@@ -1368,7 +1371,7 @@ __global__ void __launch_bounds__(256, C::MINB) union_kernel(UnionArgs a) {
         const uint32_t m = s_mode;
         if (m) {  // the group's first tile does the whole group; its other tiles have nothing to do
           if (q == 0 && g0 == g16)
-            process_group16<P, SKIP, C>(a, g16, static_cast<int>(u % G::SLICES), lane, warp, m & 0xffffu,
+            process_group16<P, SKIP, C>(a, g16, slice, lane, warp, m & 0xffffu,
                                         *reinterpret_cast<GroupSmem*>(smem));
           continue;
         }
@@ -1377,7 +1380,7 @@ __global__ void __launch_bounds__(256, C::MINB) union_kernel(UnionArgs a) {
       if (node < a.n_local) {
         const uint32_t first = a.node_item[node];
         if (q < a.node_item[node + 1] - first)
-          process_item<P, SKIP, C>(a, first + q, static_cast<int>(u % G::SLICES), lane, buf);
+          process_item<P, SKIP, C>(a, first + q, slice, lane, buf);
       }
     }
   }
@@ -1676,13 +1679,14 @@ __global__ void __launch_bounds__(256, 4) union_interval_kernel(IntervalArgs ia)
     __syncthreads();
     const unsigned long long u = s_unit[k & 1];
     if (u >= total) break;
-    const uint64_t t = u / G::SLICES;
+    const uint64_t t = u % a.n_tiles;  // slice-major (see union_kernel)
+    const int slice = static_cast<int>(u / a.n_tiles);
     const uint32_t node = a.tile_node0[t] + warp;
     const uint32_t q = a.tile_q[t];
     if (node < a.n_local) {
       const uint32_t first = a.node_item[node];
       if (q < a.node_item[node + 1] - first)
-        process_item_runs<P, OR>(ia, first + q, static_cast<int>(u % G::SLICES), lane, s_lvl);
+        process_item_runs<P, OR>(ia, first + q, slice, lane, s_lvl);
     }
   }
 }
