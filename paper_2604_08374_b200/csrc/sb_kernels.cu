@@ -712,37 +712,43 @@ struct GroupSmem {
 template <int P, class C>
 struct IdQueue {
   uint32_t* q;          // 64 entries
-  uint32_t head, tail;  // warp-uniform; tail - head < 8 between pushes
+  uint32_t head, tail;  // warp-uniform; tail - head < QB between pushes
   const uint8_t* curb;
+  int sub;              // p = 9: the half-warp (row group) of this lane
+  // ids folded per batch: 8 per lane, lane halves taking different ids at p = 9
+  static constexpr uint32_t QB = 8u * Geo<P>::SUB;
 
   __device__ __forceinline__ void drain(Grp& acc) {
     using G = Geo<P>;
     using IO = GrpIO<G::GB>;
     __syncwarp();
-    while (tail - head >= 8) {
-      const uint4 i0 = *reinterpret_cast<const uint4*>(q + (head & 63));
-      const uint4 i1 = *reinterpret_cast<const uint4*>(q + (head & 63) + 4);
+    while (tail - head >= QB) {
+      const uint32_t* b = q + ((head + 8u * sub) & 63);
+      const uint4 i0 = *reinterpret_cast<const uint4*>(b);
+      const uint4 i1 = *reinterpret_cast<const uint4*>(b + 4);
       const uint32_t id[8] = {i0.x, i0.y, i0.z, i0.w, i1.x, i1.y, i1.z, i1.w};
       Grp x[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) x[k] = IO::ld(curb + static_cast<uint64_t>(id[k]) * G::ROW);
       batch_max<C, 8>(acc, x);
-      head += 8;
+      head += QB;
     }
   }
-  // The last < 8 queued ids (absent rows read as 0, the identity of the max).
+  // The last < QB queued ids (absent rows read as 0, the identity of the max).
   __device__ __forceinline__ void flush(Grp& acc) {
     using G = Geo<P>;
     using IO = GrpIO<G::GB>;
     const uint32_t n = tail - head;
     if (!n) return;
     __syncwarp();
-    const uint4 i0 = *reinterpret_cast<const uint4*>(q + (head & 63));
-    const uint4 i1 = *reinterpret_cast<const uint4*>(q + (head & 63) + 4);
+    const int mine = static_cast<int>(n) - 8 * sub;  // this half's ids
+    const uint32_t* b = q + ((head + 8u * sub) & 63);
+    const uint4 i0 = *reinterpret_cast<const uint4*>(b);
+    const uint4 i1 = *reinterpret_cast<const uint4*>(b + 4);
     const uint32_t id[8] = {i0.x, i0.y, i0.z, i0.w, i1.x, i1.y, i1.z, i1.w};
     Grp x[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) x[k] = k < static_cast<int>(n) ? IO::ld(curb + static_cast<uint64_t>(id[k]) * G::ROW) : grp_zero();
+    for (int k = 0; k < 8; ++k) x[k] = k < mine ? IO::ld(curb + static_cast<uint64_t>(id[k]) * G::ROW) : grp_zero();
     batch_max<C, 8>(acc, x);
     head = tail;
   }
@@ -996,35 +1002,19 @@ __device__ __forceinline__ void fold_set_bits(Grp& acc, uint32_t cw, uint32_t id
   }
 }
 
-// acc <- max(acc, rows of the set bits of w) for p >= 10: a full word as four
-// unconditional 8-row batches, a partial one 8 set bits at a time.
+// acc <- max(acc, rows of the full word at id0) for p >= 9: 8 rows per lane per
+// batch (lane halves take different rows at p = 9).
 template <int P, class C>
-__device__ __forceinline__ void fold_word_rows(Grp& acc, uint32_t w, uint32_t id0, const uint8_t* curb) {
+__device__ __forceinline__ void fold_word_rows(Grp& acc, uint32_t id0, const uint8_t* curb, int sub) {
   using G = Geo<P>;
   using IO = GrpIO<G::GB>;
-  const uint8_t* rb = curb + static_cast<uint64_t>(id0) * G::ROW;
-  if (w == 0xffffffffu) {
+  static_assert(G::SUB <= 2, "full-word folds serve p >= 9");
+  const uint8_t* rb = curb + static_cast<uint64_t>(id0 + 8 * sub) * G::ROW;
 #pragma unroll 1
-    for (int c0 = 0; c0 < 32; c0 += 8) {
-      Grp x[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) x[q] = IO::ld(rb + static_cast<uint64_t>(c0 + q) * G::ROW);
-      batch_max<C, 8>(acc, x);
-    }
-    return;
-  }
-  while (w) {
+  for (int c0 = 0; c0 < 32; c0 += 8 * G::SUB) {
     Grp x[8];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      if (w) {
-        const int b = __ffs(w) - 1;
-        w &= w - 1u;
-        x[q] = IO::ld(rb + static_cast<uint64_t>(b) * G::ROW);
-      } else {
-        x[q] = grp_zero();
-      }
-    }
+    for (int q = 0; q < 8; ++q) x[q] = IO::ld(rb + static_cast<uint64_t>(c0 + q) * G::ROW);
     batch_max<C, 8>(acc, x);
   }
 }
@@ -1157,7 +1147,7 @@ __device__ __forceinline__ void process_group16(const UnionArgs& a, uint32_t g0,
     // B1: work units from the shared counter (blocks, then root slices)
     {
       uint32_t bs = 0u, bincl = 0u, total = 0u;
-      if constexpr (G::SUB == 1) {
+      if constexpr (G::SUB <= 2) {
         bs = lane < 8 ? S.rsum[lane] : 0u;
         bincl = bs;
 #pragma unroll
@@ -1167,7 +1157,7 @@ __device__ __forceinline__ void process_group16(const UnionArgs& a, uint32_t g0,
         }
         total = __shfl_sync(FULL, bincl, 7);
       }
-      constexpr int NRC = G::SUB == 1 ? GRC : 8;  // root slices (p < 10: 8 ranges of 32 words)
+      constexpr int NRC = G::SUB <= 2 ? GRC : 8;  // root slices (p < 9: 8 ranges of 32 words)
       for (;;) {
         uint32_t u = 0u;
         if (lane == 0) u = atomicAdd(&S.unit, 1u);
@@ -1175,7 +1165,7 @@ __device__ __forceinline__ void process_group16(const UnionArgs& a, uint32_t g0,
         if (u >= static_cast<uint32_t>(GBLK + NRC)) break;
         if (u >= static_cast<uint32_t>(GBLK)) {
           const int c = static_cast<int>(u) - GBLK;
-          if constexpr (G::SUB == 1) {
+          if constexpr (G::SUB <= 2) {
             // root slice c of equal id count (root ids cluster in runs, so equal
             // word ranges would not balance)
             const uint32_t lo = static_cast<uint32_t>((static_cast<uint64_t>(total) * c) / NRC);
@@ -1195,7 +1185,7 @@ __device__ __forceinline__ void process_group16(const UnionArgs& a, uint32_t g0,
               const int j0 = locate(lo, ex0), j1 = locate(hi - 1, ex1);
               // 32 words per pass, a word per lane: full words as 4 unconditional
               // 8-row batches, the set bits of partial ones (run ends) queued
-              IdQueue<P, C> Q{S.q[warp], 0u, 0u, curb};
+              IdQueue<P, C> Q{S.q[warp], 0u, 0u, curb, sub};
 #pragma unroll 1
               for (int jb = j0; jb <= j1; jb += 32) {
                 const int j = jb + lane;
@@ -1205,7 +1195,7 @@ __device__ __forceinline__ void process_group16(const UnionArgs& a, uint32_t g0,
                 while (fm) {
                   const int src = __ffs(fm) - 1;
                   fm &= fm - 1u;
-                  fold_word_rows<P, C>(all, 0xffffffffu, B + 32u * (jb + src), curb);
+                  fold_word_rows<P, C>(all, B + 32u * (jb + src), curb, sub);
                 }
                 Q.push_lanes(all, w == 0xffffffffu ? 0u : w, B + 32u * j, lane);
               }
@@ -1221,22 +1211,22 @@ __device__ __forceinline__ void process_group16(const UnionArgs& a, uint32_t g0,
         if (!(act & block_nodes(b))) continue;  // no node of this block has neighbours
         Grp acc = u4_grp(S.blk[b][lane]);
         bool touched = false;
-        // p >= 10: the cover's ids are sparse (the rims of the disks): a word per
+        // p >= 9: the cover's ids are sparse (the rims of the disks): a word per
         // lane, full words as 8-row batches, the other set bits queued
-        IdQueue<P, C> Q{S.q[warp], 0u, 0u, curb};
+        IdQueue<P, C> Q{S.q[warp], 0u, 0u, curb, sub};
 #pragma unroll 1
         for (int j0 = 0; j0 < GW; j0 += 32) {
           uint32_t cword = block_cover_word(S, b, j0 + lane, act);
           if (!__any_sync(FULL, cword != 0u)) continue;
           const uint32_t id0l = B + 32u * (j0 + lane);
           touched = true;
-          if constexpr (G::SUB == 1) {
+          if constexpr (G::SUB <= 2) {
             SB_ST_ADD(3, __reduce_add_sync(FULL, __popc(cword)));
             uint32_t fm = __ballot_sync(FULL, cword == 0xffffffffu);
             while (fm) {
               const int src = __ffs(fm) - 1;
               fm &= fm - 1u;
-              fold_word_rows<P, C>(acc, 0xffffffffu, B + 32u * (j0 + src), curb);
+              fold_word_rows<P, C>(acc, B + 32u * (j0 + src), curb, sub);
             }
             Q.push_lanes(acc, cword == 0xffffffffu ? 0u : cword, id0l, lane);
           } else {
@@ -1248,7 +1238,7 @@ __device__ __forceinline__ void process_group16(const UnionArgs& a, uint32_t g0,
             }
           }
         }
-        if (G::SUB == 1) Q.flush(acc);
+        if (G::SUB <= 2) Q.flush(acc);
         if (touched) S.blk[b][lane] = grp_u4(acc);
         SB_ST_ADD(4, 1);
       }
