@@ -48,12 +48,12 @@ static void hb_union_args(const sb_hb* h, sb::UnionArgs& u) {
   if (h->flags & SB_HB_SCHEDULE_GROUP) {  // every dense-enough group takes the group path
     u.node_lo = g->d_node_lo;
     u.shared_max_edges = ~0ull;
-  } else if (h->p < 9 && g->edges_local < 6000ull * g->n_local) {
-    // rows of <= 128 B on graphs of moderate degree: the gathers the group
-    // path saves are cheap, and the per-node decode + fold is faster (C2,
-    // mean degree 3,730: p=6 0.44 vs 0.80 ms, p=8 1.07 vs 1.56 ms); at C3
-    // (mean degree 20,278) the shared gathers win also at p=8 (22.0 vs 29.2 ms;
-    // profiles/r02/group_threshold.json)
+  } else if (h->p < 8 && g->edges_local < 6000ull * g->n_local) {
+    // rows of <= 64 B on graphs of moderate degree: the gathers the group path
+    // saves are cheap, and the per-node decode + fold is faster (C2, mean
+    // degree 3,730: p=6 0.36 vs 0.81 ms, p=7 0.55 vs 1.02 ms; from p = 8 the
+    // group path folds through the id ring: p=8 0.68 vs 0.96 ms); at C3 (mean
+    // degree 20,278) the shared gathers win at every p (profiles/r02/group_threshold.json)
     u.node_lo = nullptr;
   }
   // Without the group path the per-warp item schedule balances better than

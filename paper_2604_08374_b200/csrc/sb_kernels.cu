@@ -1008,7 +1008,7 @@ template <int P, class C>
 __device__ __forceinline__ void fold_word_rows(Grp& acc, uint32_t id0, const uint8_t* curb, int sub) {
   using G = Geo<P>;
   using IO = GrpIO<G::GB>;
-  static_assert(G::SUB <= 2, "full-word folds serve p >= 9");
+  static_assert(G::SUB <= 4, "full-word folds serve p >= 8");
   const uint8_t* rb = curb + static_cast<uint64_t>(id0 + 8 * sub) * G::ROW;
 #pragma unroll 1
   for (int c0 = 0; c0 < 32; c0 += 8 * G::SUB) {
@@ -1147,7 +1147,7 @@ __device__ __forceinline__ void process_group16(const UnionArgs& a, uint32_t g0,
     // B1: work units from the shared counter (blocks, then root slices)
     {
       uint32_t bs = 0u, bincl = 0u, total = 0u;
-      if constexpr (G::SUB <= 2) {
+      if constexpr (G::SUB <= 4) {
         bs = lane < 8 ? S.rsum[lane] : 0u;
         bincl = bs;
 #pragma unroll
@@ -1157,7 +1157,7 @@ __device__ __forceinline__ void process_group16(const UnionArgs& a, uint32_t g0,
         }
         total = __shfl_sync(FULL, bincl, 7);
       }
-      constexpr int NRC = G::SUB <= 2 ? GRC : 8;  // root slices (p < 9: 8 ranges of 32 words)
+      constexpr int NRC = G::SUB <= 4 ? GRC : 8;  // root slices (p < 8: 8 ranges of 32 words)
       for (;;) {
         uint32_t u = 0u;
         if (lane == 0) u = atomicAdd(&S.unit, 1u);
@@ -1165,7 +1165,7 @@ __device__ __forceinline__ void process_group16(const UnionArgs& a, uint32_t g0,
         if (u >= static_cast<uint32_t>(GBLK + NRC)) break;
         if (u >= static_cast<uint32_t>(GBLK)) {
           const int c = static_cast<int>(u) - GBLK;
-          if constexpr (G::SUB <= 2) {
+          if constexpr (G::SUB <= 4) {
             // root slice c of equal id count (root ids cluster in runs, so equal
             // word ranges would not balance)
             const uint32_t lo = static_cast<uint32_t>((static_cast<uint64_t>(total) * c) / NRC);
@@ -1220,7 +1220,7 @@ __device__ __forceinline__ void process_group16(const UnionArgs& a, uint32_t g0,
           if (!__any_sync(FULL, cword != 0u)) continue;
           const uint32_t id0l = B + 32u * (j0 + lane);
           touched = true;
-          if constexpr (G::SUB <= 2) {
+          if constexpr (G::SUB <= 4) {
             SB_ST_ADD(3, __reduce_add_sync(FULL, __popc(cword)));
             uint32_t fm = __ballot_sync(FULL, cword == 0xffffffffu);
             while (fm) {
@@ -1238,7 +1238,7 @@ __device__ __forceinline__ void process_group16(const UnionArgs& a, uint32_t g0,
             }
           }
         }
-        if (G::SUB <= 2) Q.flush(acc);
+        if (G::SUB <= 4) Q.flush(acc);
         if (touched) S.blk[b][lane] = grp_u4(acc);
         SB_ST_ADD(4, 1);
       }
