@@ -141,3 +141,16 @@ if [[ $what == setupcheck ]]; then
   run timeout 1500 python -u -m pytest tests/test_gpu_validation_fuzz.py tests/test_gpu_async_upload.py tests/test_gpu_parity.py -q -x -k "validation or async or interval or malformed or errors or varint or pipelined" > gpurun_out/pytest_setup.log 2>&1; tail -2 gpurun_out/pytest_setup.log
 fi
 done
+for what in "$@"; do
+if [[ $what == widened ]]; then
+  for a in "c2 dense 12" "c2 interval 12" "c3 dense 12" "c3 interval 12"; do
+    run timeout 900 python -u scripts/exact_bench.py $a > "gpurun_out/exact_${a// /_}.json" 2>/dev/null
+  done
+  run timeout 600 python -u scripts/local_metrics_bench.py c3 > gpurun_out/local_c3.json 2>/dev/null
+  for tool in memcheck racecheck synccheck; do
+    run timeout 900 compute-sanitizer --tool $tool --error-exitcode 9 python -u scripts/sanitize_widened.py \
+        > gpurun_out/sanitizer_widened_$tool.log 2>&1
+    tail -1 gpurun_out/sanitizer_widened_$tool.log
+  done
+fi
+done
