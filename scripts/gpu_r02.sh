@@ -154,3 +154,24 @@ if [[ $what == widened ]]; then
   done
 fi
 done
+for what in "$@"; do
+if [[ $what == city ]]; then
+  run timeout 900 python -u scripts/city_scale.py 1650 30 12000 0 > gpurun_out/city_scale.json 2> gpurun_out/city_scale.log
+  run timeout 900 python -u scripts/city_scale.py 1800 80 6500 3 > gpurun_out/city_valdivia_like.json 2> gpurun_out/city_valdivia.log
+  ( time ./tools/sb_hyperball analyze 1800 1800 6500 4 16 20261017 6400 10 3 hyperball /tmp/v.csv ) \
+      > gpurun_out/valdivia_like_cpp_analyze.txt 2>&1
+  rm -f /tmp/v.csv
+fi
+done
+for what in "$@"; do
+if [[ $what == citysched ]]; then
+  run timeout 900 python -u scripts/city_sched.py > gpurun_out/city_sched.json 2> gpurun_out/city_sched.log
+fi
+done
+for what in "$@"; do
+if [[ $what == cppanalyze ]]; then
+  ( time ./tools/sb_hyperball analyze 1800 1800 6500 4 16 20261017 6400 10 3 hyperball /tmp/v.csv ) \
+      > gpurun_out/valdivia_like_cpp_analyze.txt 2>&1
+  ls -la /tmp/v.csv >> gpurun_out/valdivia_like_cpp_analyze.txt 2>&1; rm -f /tmp/v.csv
+fi
+done
