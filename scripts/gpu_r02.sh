@@ -175,3 +175,8 @@ if [[ $what == cppanalyze ]]; then
   ls -la /tmp/v.csv >> gpurun_out/valdivia_like_cpp_analyze.txt 2>&1; rm -f /tmp/v.csv
 fi
 done
+for what in "$@"; do
+if [[ $what == fuzz ]]; then
+  run timeout 3000 python -u scripts/parity_fuzz.py 2500 2026 > gpurun_out/parity_fuzz_2500_seed2026.json 2> gpurun_out/parity_fuzz.log
+fi
+done

@@ -1,7 +1,9 @@
 """Randomised parity campaign: random grid graphs (size, obstacles, radius),
 random p in [4, 16], random depth limit, random mode (dense / skip / interval /
-sharded), GPU vs the oracle after EVERY iteration; plus exact local metrics and
-the exact BFS on the same graph.  usage: python scripts/parity_fuzz.py [n_cases] [seed]
+sharded / asynchronous upload with the wavefront first run) and schedule (auto /
+group / items), GPU vs the oracle after EVERY iteration (the wavefront run: its
+final state and every max increase); plus exact local metrics and the exact BFS
+on the same graph.  usage: python scripts/parity_fuzz.py [n_cases] [seed]
 Prints one JSON summary (cases, failures with their parameters)."""
 import json
 import os
@@ -29,9 +31,10 @@ for case in range(n_cases):
     seed = int(rng.integers(1, 2**31))
     p = int(rng.integers(4, 17)) if rng.random() < 0.5 else 10
     depth = None if rng.random() < 0.5 else int(rng.integers(1, 6))
-    mode = rng.choice(["dense", "skip", "interval", "shards"])
+    mode = rng.choice(["dense", "skip", "interval", "shards", "async"])
+    sched = str(rng.choice(["auto", "group", "items"])) if mode in ("dense", "skip") else "auto"
     params = dict(rows=rows, cols=cols, rects=rects, rmin=rmin, rmax=rmax, radius2=radius2, seed=seed, p=p,
-                  depth=depth, mode=str(mode))
+                  depth=depth, mode=str(mode), schedule=sched)
     try:
         g = CompressedCsr.synth_grid(rows, cols, rects, rmin, rmax, seed, radius2)
     except RuntimeError:
@@ -41,12 +44,24 @@ for case in range(n_cases):
         cur, c_prev = O.hb_init(n, p)
         nxt = np.zeros_like(cur)
         c_cur, sd, sd2 = np.zeros(n), np.zeros(n), np.zeros(n)
+        if mode == "async":
+            h = HyperBall(DeviceGraph(g, async_upload=True), p, depth, wavefront=True)
+            h.run()
+            ref = O.hb_run(g, p, depth_limit=depth)
+            st = h.state()
+            ok = st.t == ref["iterations"] and np.array_equal(h.registers(), ref["registers"])
+            ok &= np.array_equal(st.sum_d, ref["sum_d"]) and np.array_equal(st.c_curr, ref["c"])
+            if not ok:
+                raise AssertionError("wavefront run mismatch")
+            done += 1
+            continue
         if mode == "shards":
             k = int(rng.integers(2, 5))
             b = g.partition(k)
             hs = [HyperBall(g, p, depth, node_range=(int(b[r]), int(b[r + 1]))) for r in range(k)]
         else:
-            hs = [HyperBall(g, p, depth, skip_unchanged=(mode == "skip"), interval=(mode == "interval"))]
+            hs = [HyperBall(g, p, depth, skip_unchanged=(mode == "skip"), interval=(mode == "interval"),
+                            schedule=sched)]
         t = 0
         while True:
             t += 1
