@@ -9,7 +9,8 @@ cells: 236,196 cells, 4.79e9 directed edges, 4.83 GB LEB128 stream), p=10.
            counters resident in HBM, device time (CUDA events on the
            library's stream), max over ranks.
   e2e      same metric through the public C-ABI with HOST buffers: CSR upload
-           (pinned H2D) + validation + run + read-back of c / sum_d / sum_d2.
+           (pinned H2D, chunked, validated per chunk) + run (its first run a
+           wavefront over the upload chunks) + read-back of c / sum_d / sum_d2.
   roofline the fused decode-union kernel against the unit that binds it (SM
            instruction issue): ncu's warp-instructions per launch / the live
            CUDA-event launch time vs 1 instr/cycle/SMSP at the sampled clock;
@@ -638,7 +639,7 @@ def main():
             line["cpu_baseline"] = {"value": None, "error": repr(e)}
     line["roofline"], line["hbm_algorithmic"] = roofline_of(args.config, args.p, avg_union_s, bytes_launch,
                                                             clock_info.get("sm_mhz"))
-    line["roofline"]["kernel"] = f"sb::union_kernel<{args.p}> (fused decode-union, tile-shared gathers)"
+    line["roofline"]["kernel"] = f"sb::union_kernel<{args.p}> (fused decode-union, 16-node group path)"
     line["hbm_algorithmic"]["whole_run_gbs"] = bytes_iter * iters * args.steps / dev_s / 1e9
     if rank == 0:
         print(json.dumps(line), flush=True)
