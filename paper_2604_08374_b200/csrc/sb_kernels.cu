@@ -186,44 +186,47 @@ __global__ void __launch_bounds__(256, 3) build_items_kernel(BuildArgs a) {
           }
         }
         const uint32_t excl = incl - lcnt;
-        const uint32_t want = next_cut - 1 - done;  // window rank of the last id before the cut
-        if (done + incl > next_cut - 1 && want >= excl && want < incl) {
-          // this lane holds it: walk its bytes in order
-          uint32_t r = excl;
-          unsigned long long part = done_sum + (sincl - lsum);
-          bool found = false;
+        const uint32_t wtot = __shfl_sync(FULL, incl, 31);
+        // every cut whose last id before it falls in this window (several when
+        // chunk < 512 ids): the lane holding that id walks its bytes in order
+        while (next_cut < deg && done + wtot >= next_cut) {  // warp-uniform
+          const uint32_t want = next_cut - 1 - done;  // window rank of the last id before the cut
+          if (want >= excl && want < incl) {
+            uint32_t r = excl;
+            unsigned long long part = done_sum + (sincl - lsum);
+            bool found = false;
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const uint32_t w = x[i];
-            const uint32_t wp = i >= 1 ? x[i - 1] : p3;
-            const uint32_t F = w & 0x80808080u, Fp = wp & 0x80808080u;
-            const uint32_t m1 = __funnelshift_l(Fp, F, 8);
-            const uint32_t m2 = m1 & __funnelshift_l(Fp, F, 16);
-            const uint32_t m3 = m2 & __funnelshift_l(Fp, F, 24);
-            const uint32_t m4 = m3 & Fp;
-            const uint32_t D = (m1 >> 7) + (m2 >> 7) + (m3 >> 7) + (m4 >> 7);
+            for (int i = 0; i < 4; ++i) {
+              const uint32_t w = x[i];
+              const uint32_t wp = i >= 1 ? x[i - 1] : p3;
+              const uint32_t F = w & 0x80808080u, Fp = wp & 0x80808080u;
+              const uint32_t m1 = __funnelshift_l(Fp, F, 8);
+              const uint32_t m2 = m1 & __funnelshift_l(Fp, F, 16);
+              const uint32_t m3 = m2 & __funnelshift_l(Fp, F, 24);
+              const uint32_t m4 = m3 & Fp;
+              const uint32_t D = (m1 >> 7) + (m2 >> 7) + (m3 >> 7) + (m4 >> 7);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              if (!found) {
-                const uint32_t dk = (D >> (8 * k)) & 0xffu;
-                part += static_cast<unsigned long long>((w >> (8 * k)) & 0x7fu) << (7 * dk);
-                if ((tw[i] >> (8 * k + 7)) & 1u) {
-                  if (r == want) {
-                    found = true;
-                    const uint32_t it = i0 + next_cut / a.chunk;
-                    a.item_off[it] = lb + 4 * i + k + 1;
-                    a.item_base[it] = static_cast<uint32_t>(part);
-                    a.item_count[it] = (deg - next_cut) < a.chunk ? deg - next_cut : a.chunk;
-                    a.item_node[it] = static_cast<uint32_t>(node);
+              for (int k = 0; k < 4; ++k) {
+                if (!found) {
+                  const uint32_t dk = (D >> (8 * k)) & 0xffu;
+                  part += static_cast<unsigned long long>((w >> (8 * k)) & 0x7fu) << (7 * dk);
+                  if ((tw[i] >> (8 * k + 7)) & 1u) {
+                    if (r == want) {
+                      found = true;
+                      const uint32_t it = i0 + next_cut / a.chunk;
+                      a.item_off[it] = lb + 4 * i + k + 1;
+                      a.item_base[it] = static_cast<uint32_t>(part);
+                      a.item_count[it] = (deg - next_cut) < a.chunk ? deg - next_cut : a.chunk;
+                      a.item_node[it] = static_cast<uint32_t>(node);
+                    }
+                    ++r;
                   }
-                  ++r;
                 }
               }
             }
           }
+          next_cut += a.chunk;
         }
-        const uint32_t wtot = __shfl_sync(FULL, incl, 31);
-        if (done + wtot >= next_cut) next_cut += a.chunk;  // at most one cut per window (chunk >= 512)
         done += wtot;
         done_sum += __shfl_sync(FULL, sincl, 31);
       }
