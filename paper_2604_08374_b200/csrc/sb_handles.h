@@ -111,7 +111,7 @@ inline void dfree_ipc(T*& p) {
 // 32-byte page-locked host slots (each HyperBall handle's per-iteration
 // read-back) carved from one process-wide slab: cudaMallocHost / cudaFreeHost
 // per handle cost milliseconds, more than a whole small-graph run.
-constexpr int kPinnedSlot = 32, kPinnedSlots = 4096;
+constexpr int kPinnedSlot = 256, kPinnedSlots = 4096;  // per handle: step read-back / batched-run records
 struct PinnedSlab {
   std::mutex mu;
   uint8_t* base = nullptr;
@@ -304,6 +304,11 @@ struct sb_hb {
   std::vector<uint8_t*> d_xplane, d_xchg;
   std::vector<cudaStream_t> pstream;
   std::vector<cudaEvent_t> pev, pev_t;
+  // back-to-back passes (batched_run): device flags [stop, last pass, converged],
+  // per-pass [max increase, changed count], pinned read-back, timing events
+  unsigned int* d_bflags = nullptr;
+  unsigned long long* d_brec = nullptr;
+  std::vector<cudaEvent_t> bev;
   unsigned long long* d_pwork = nullptr;
   size_t pwork_n = 0;
   std::vector<sb_iter_stats> stats;
@@ -338,6 +343,8 @@ struct sb_hb {
     for (uint8_t* x : d_xchg) dfree(x);
     for (cudaEvent_t e : pev) cudaEventDestroy(e);
     for (cudaEvent_t e : pev_t) cudaEventDestroy(e);
+    for (cudaEvent_t e : bev) cudaEventDestroy(e);
+    dfree(d_bflags); dfree(d_brec);
     for (cudaStream_t ps : pstream) cudaStreamDestroy(ps);
     pinned_put(h_misc, h_misc_owned);
     for (auto& e : ev) if (e) cudaEventDestroy(e);

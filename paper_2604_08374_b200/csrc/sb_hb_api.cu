@@ -33,7 +33,10 @@ static int hb_init(sb_hb* h) {
     CK(sb::launch_estimate(static_cast<int>(h->p), 0, e, h->stream));
   }
   if (h->d_counter) CK(cudaMemsetAsync(h->d_counter, 0, std::max<uint64_t>(g->n_local, 1) * h->slices * 4, h->stream));
-  CK(sync_stream(h->stream));
+  // Everything that follows on this handle is ordered behind the stream; only
+  // peers writing into this replica over P2P (and the caller's barrier after a
+  // reset) need the initialisation complete before returning.
+  if (h->npeers || h->comm) CK(sync_stream(h->stream));
   return SB_OK;
 }
 
@@ -611,12 +614,113 @@ static int pipelined_run(sb_hb* h, bool* done) {
   return SB_OK;
 }
 
+// Back-to-back passes on one GPU (dense mode, no shards, graph resident): up
+// to kBatch passes are enqueued at once and Alg. 1's test runs on the device
+// after each (decide_kernel), turning the passes after the last one into
+// no-ops -- one host round trip per batch instead of per pass.  Same kernels,
+// same order of operations, bit-identical state and statistics.
+static constexpr int kBatch = 8;
+static int batched_run(sb_hb* h) {
+  sb_graph* g = h->g;
+  DeviceGuard dg(g->device);
+  static_assert((kBatch * 2 + 2) * 8 <= sb::rt::kPinnedSlot, "batch records fit the pinned read-back slot");
+  if (!h->d_bflags) {
+    CK(dalloc(&h->d_bflags, 4 * 4));
+    CK(dalloc(&h->d_brec, kBatch * 2 * 8));
+  }
+  unsigned long long* rec = h->h_misc;  // the handle's pinned slot
+  while (static_cast<int>(h->bev.size()) < 2 * kBatch + 1) {
+    cudaEvent_t e = nullptr;
+    CK(cudaEventCreate(&e));
+    h->bev.push_back(e);
+  }
+  sb::UnionArgs base{};
+  hb_union_args(h, base);
+  base.stop = h->d_bflags;
+  while (!h->finished) {
+    int K = kBatch;
+    if (h->depth) K = std::min<int>(K, static_cast<int>(h->depth - h->t));
+    CK(cudaMemsetAsync(h->d_bflags, 0, 4 * 4, h->stream));
+    CK(cudaMemsetAsync(h->d_misc, 0, 4 * 8, h->stream));
+    CK(cudaEventRecord(h->bev[2 * kBatch], h->stream));
+    int L = h->latest;
+    for (int i = 0; i < K; ++i) {
+      const int N = 1 - L;
+      const uint32_t t = h->t + 1 + i;
+      CK(sb::launch_clear_flags(h->d_bflags, h->d_changed[N] + g->v0, g->n_local, h->stream));
+      CK(cudaEventRecord(h->bev[2 * i], h->stream));
+      if (g->n_local) {
+        sb::UnionArgs u = base;
+        u.cur = h->d_plane[L];
+        u.next = h->d_plane[N];
+        u.changed_out = h->d_changed[N];
+        u.changed_in = h->d_changed[L];
+        u.work = h->d_misc;
+        CK(sb::launch_union(static_cast<int>(h->p), false, u, h->stream));
+      }
+      CK(cudaEventRecord(h->bev[2 * i + 1], h->stream));
+      if (g->n_local) {
+        sb::EstArgs e{};
+        e.plane = h->d_plane[N];
+        e.node_begin = g->v0;
+        e.n_local = g->n_local;
+        e.lc = h->d_lc;
+        e.alpha = h->alpha;
+        e.m = static_cast<double>(1u << h->p);
+        e.c_prev = h->d_c[L];
+        e.c_cur = h->d_c[N];
+        e.sum_d = h->d_sum_d;
+        e.sum_d2 = h->d_sum_d2;
+        e.changed = h->d_changed[N];
+        e.t = t;
+        e.max_ord = h->d_misc + 1;
+        e.changed_count = h->d_misc + 2;
+        e.stop = h->d_bflags;
+        CK(sb::launch_estimate(static_cast<int>(h->p), 1, e, h->stream));
+      }
+      CK(sb::launch_clear_flags(h->d_bflags, h->d_changed[L], g->n, h->stream));  // consumed flags
+      CK(sb::launch_decide(h->d_misc, h->d_bflags, h->d_brec + 2 * i, t, h->depth, h->stream));
+      L = N;
+    }
+    CK(cudaMemcpyAsync(rec, h->d_brec, K * 2 * 8, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaMemcpyAsync(rec + 2 * kBatch, h->d_bflags, 4 * 4, cudaMemcpyDeviceToHost, h->stream));
+    CK(sync_stream(h->stream));
+    const unsigned int* fl = reinterpret_cast<const unsigned int*>(rec + 2 * kBatch);
+    const int ran = fl[0] ? static_cast<int>(fl[1] - h->t) : K;
+    for (int i = 0; i < ran; ++i) {
+      sb_iter_stats st{};
+      st.t = h->t + 1 + i;
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, h->bev[2 * i], h->bev[2 * i + 1]);
+      st.union_ms = ms;
+      if (i + 1 < K) {
+        cudaEventElapsedTime(&ms, h->bev[2 * i + 1], h->bev[2 * i + 2]);
+        st.estimate_ms = ms;
+      }
+      cudaEventElapsedTime(&ms, i ? h->bev[2 * i - 1] : h->bev[2 * kBatch], h->bev[2 * i + 1]);
+      st.step_ms = ms;
+      st.changed_nodes = rec[2 * i + 1];
+      st.max_increase = decode_ord(rec[2 * i]);
+      h->stats.push_back(st);
+    }
+    h->t += static_cast<uint32_t>(ran);
+    h->latest = (h->latest + ran) & 1;
+    h->converged = fl[0] && fl[2];
+    h->finished = fl[0] != 0;
+  }
+  return SB_OK;
+}
+
 extern "C" {
 
 int sb_hb_run(sb_hb* h, uint32_t* iterations, int* converged) {
   if (!h) return fail(SB_EINVAL, "NULL handle");
   bool done = false;
   if (const int rc = pipelined_run(h, &done)) return rc;
+  if (!h->finished && !h->computed && !h->comm && !h->npeers && !h->g->pending && !h->g->broken &&
+      !(h->flags & (SB_HB_INTERVAL | SB_HB_SKIP_UNCHANGED))) {
+    if (const int rc = batched_run(h)) return rc;
+  }
   int conv = 0, fin = h->finished ? 1 : 0;
   while (!fin) {
     const int rc = sb_hb_step(h, nullptr, &conv, &fin);
@@ -686,6 +790,7 @@ int sb_hb_read_state(const sb_hb* h, double* c_latest, double* c_previous, doubl
   if (!h) return fail(SB_EINVAL, "NULL handle");
   const sb_graph* g = h->g;
   DeviceGuard dg(g->device);
+  CK(sync_stream(h->stream));  // work still queued on the handle (e.g. a reset)
   const uint64_t nb = g->n_local * 8;
   if (g->n_local) {
     if (c_latest) CK(cudaMemcpy(c_latest, h->d_c[h->latest], nb, cudaMemcpyDeviceToHost));

@@ -61,6 +61,9 @@ struct UnionArgs {
   const uint32_t* node_lo;     // first / last neighbour id per local node (NULL: path off)
   const uint32_t* node_hi;
   uint64_t shared_max_edges;
+  // Back-to-back passes (sb_hb_run without a per-pass host test): every CTA
+  // returns at once when the run already finished on the device (NULL: off)
+  const unsigned int* stop;
   // Fused shard exchange: every finished row (and its changed flag) is also
   // stored straight into each peer GPU's replica (CUDA IPC / NVLink P2P).
   uint8_t* const* peer_next;     // [npeers] peers' `next` planes
@@ -113,6 +116,7 @@ struct EstArgs {
   uint32_t t;
   unsigned long long* max_ord; // ordered-encoded max increase
   unsigned long long* changed_count;
+  const unsigned int* stop;    // NULL, or the device-side "run finished" flag (the pass is a no-op)
 };
 
 // Exact mode (bit-parallel BFS over blocks of 2^(P+2) sources).
@@ -220,6 +224,11 @@ cudaError_t launch_estimate(int p, int mode, const EstArgs& a, cudaStream_t s);
 cudaError_t launch_to_packed(int p, const uint8_t* bits, uint8_t* packed, uint64_t rows, cudaStream_t s);
 cudaError_t launch_from_packed(int p, const uint8_t* packed, uint8_t* bits, uint64_t rows, cudaStream_t s);
 cudaError_t launch_metrics(const MetricArgs& a, cudaStream_t s);
+// Device-side Alg. 1 test after pass t (flags[0] = stop, [1] = last pass, [2] = converged)
+// and a flag clear that is skipped once the run stopped.
+cudaError_t launch_decide(unsigned long long* misc, unsigned int* flags, unsigned long long* rec, uint32_t t,
+                          uint32_t depth, cudaStream_t s);
+cudaError_t launch_clear_flags(const unsigned int* flags, uint8_t* bytes, uint64_t n, cudaStream_t s);
 int union_slices(int p);
 
 }  // namespace sb

@@ -1332,6 +1332,7 @@ __global__ void __launch_bounds__(256, C::MINB) union_kernel(UnionArgs a) {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   uint32_t* buf = reinterpret_cast<uint32_t*>(smem) + warp * Feeder<P, SKIP, C::U, C::D16 && !SKIP>::BUF;
+  if (a.stop && *reinterpret_cast<const volatile unsigned int*>(a.stop)) return;  // run finished on the device
   if (!TILE) {
     const uint64_t total = a.n_items * G::SLICES;
     for (;;) {
@@ -1694,6 +1695,7 @@ __global__ void __launch_bounds__(256) estimate_kernel(EstArgs a) {
   const int lane = threadIdx.x & 31;
   const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = (gridDim.x * (uint64_t)blockDim.x) >> 5;
+  if (a.stop && *reinterpret_cast<const volatile unsigned int*>(a.stop)) return;  // run finished on the device
   unsigned long long wmax = 0ull;  // ordered encoding; 0 < every encoded value
   unsigned long long nchanged = 0ull;
   const double m = a.m;
@@ -1995,6 +1997,49 @@ __global__ void __launch_bounds__(256) chunk_range_kernel(const uint32_t* __rest
 cudaError_t launch_chunk_range(const uint32_t* lo, const uint32_t* hi, uint64_t n0, uint64_t n1, uint32_t* out,
                                cudaStream_t s) {
   chunk_range_kernel<<<1, 256, 0, s>>>(lo, hi, n0, n1, out);
+  return cudaGetLastError();
+}
+
+// Alg. 1's test on the device after pass
+// t of back-to-back passes: keeps the pass's max increase and changed count
+// for the host, stops the run when max increase <= 0.5 (inclusive) or t is the
+// depth limit, and resets the per-pass counters for the next pass.
+__global__ void decide_kernel(unsigned long long* misc, unsigned int* flags, unsigned long long* rec, uint32_t t,
+                              uint32_t depth) {
+  if (flags[0]) return;
+  const unsigned long long mo = misc[1];
+  rec[0] = mo;
+  rec[1] = misc[2];
+  double mx = -INFINITY;  // no node contributed
+  if (mo) {
+    const unsigned long long u = (mo >> 63) ? (mo & 0x7fffffffffffffffull) : ~mo;
+    mx = __longlong_as_double(static_cast<long long>(u));
+  }
+  const bool conv = mx <= 0.5;
+  if (conv || (depth != 0 && t == depth)) {
+    flags[1] = t;
+    flags[2] = conv ? 1u : 0u;
+    flags[0] = 1u;
+  }
+  misc[0] = misc[1] = misc[2] = misc[3] = 0ull;
+}
+
+__global__ void clear_flags_kernel(const unsigned int* flags, uint8_t* bytes, uint64_t n) {
+  if (*flags) return;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    bytes[i] = 0;
+}
+
+cudaError_t launch_decide(unsigned long long* misc, unsigned int* flags, unsigned long long* rec, uint32_t t,
+                          uint32_t depth, cudaStream_t s) {
+  decide_kernel<<<1, 1, 0, s>>>(misc, flags, rec, t, depth);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_clear_flags(const unsigned int* flags, uint8_t* bytes, uint64_t n, cudaStream_t s) {
+  const uint64_t blocks = (n + 255) / 256;
+  clear_flags_kernel<<<static_cast<unsigned>(blocks < 1184 ? (blocks ? blocks : 1) : 1184), 256, 0, s>>>(flags, bytes, n);
   return cudaGetLastError();
 }
 
