@@ -26,59 +26,114 @@ int build_run_index(sb_graph* g) {
   a.item_end = g->n_items;
   a.range_end_byte = g->stream_local;
   uint64_t* d_cnt = nullptr;
+  unsigned long long* d_aux = nullptr;  // [0] run total, [1] overflow flag
   CK(dalloc(&d_cnt, g->n_items * 8 + 8));
+  CK(dalloc(&d_aux, 2 * 8));
+  auto bail = [&](int rc) {
+    dfree(d_cnt);
+    dfree(d_aux);
+    dfree(g->d_run_off);
+    dfree(g->d_run_s);
+    dfree(g->d_run_e);
+    g->n_runs = 0;
+    return rc;
+  };
+#define RK(x)                                                 \
+  do {                                                        \
+    cudaError_t e_ = (x);                                     \
+    if (e_ != cudaSuccess) return bail(cuda_fail(e_, #x));    \
+  } while (0)
   a.run_count = d_cnt;
   a.max_run = reinterpret_cast<unsigned int*>(d_cnt + g->n_items);
-  CK(cudaMemsetAsync(a.max_run, 0, 4, 0));
+  RK(cudaMemsetAsync(a.max_run, 0, 4, 0));
+  RK(cudaMemsetAsync(d_aux, 0, 16, 0));
+  RK(dalloc(&g->d_run_off, (g->n_items + 1) * 8));
+  bool exact = true;  // run storage sized from the final total (else from an estimate)
   if (g->pending && g->chunk_item.size() > 2) {
-    // still uploading: count chunk k's runs as soon as chunk k is validated,
-    // so the count pass hides under the remaining PCIe copies
+    // Still uploading: chunk k's runs are counted, offset and written as soon
+    // as chunk k is validated, so the whole index hides under the remaining
+    // PCIe copies.  The run storage is sized before the total is known, from
+    // the runs per stream byte of the first full-size chunk (x 1.25 + slack);
+    // an item that would not fit is skipped and flagged, and the index is then
+    // rebuilt with exact storage after the upload.
     cudaStream_t s = nullptr;
-    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    CK(sync_stream(0));  // the max_run reset
+    RK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    RK(sync_stream(0));  // the resets above
     a.err = g->d_err;
-    for (size_t k = 0; k + 1 < g->chunk_item.size(); ++k) {
+    const size_t nk = g->chunk_item.size() - 1;
+    const size_t probe = std::min<size_t>(1, nk - 1);  // chunk 0 is the small 1/64 one
+    uint64_t cap = 0;
+    int rc = SB_OK;
+    for (size_t k = 0; k < nk && !rc; ++k) {
       a.item_begin = g->chunk_item[k];
       a.item_end = g->chunk_item[k + 1];
       a.range_end_byte = g->chunk_byte[k + 1];  // the next chunk's items are not cut yet
       if (a.item_end == a.item_begin) continue;
-      CK(cudaStreamWaitEvent(s, g->val_ev[k], 0));
-      CK(sb::launch_run_index(a, false, s));
+      RK(cudaStreamWaitEvent(s, g->val_ev[k], 0));
+      RK(sb::launch_run_index(a, false, s));
+      RK(sb::launch_run_offsets(d_cnt, g->d_run_off, a.item_begin, a.item_end, d_aux, s));
+      if (k == probe || (cap == 0 && k + 1 == nk)) {
+        unsigned long long tot = 0;
+        RK(cudaMemcpyAsync(&tot, d_aux, 8, cudaMemcpyDeviceToHost, s));
+        RK(sync_stream(s));
+        const uint64_t bytes = std::max<uint64_t>(g->chunk_byte[k + 1], 1);
+        cap = static_cast<uint64_t>(static_cast<double>(tot) / static_cast<double>(bytes) *
+                                    static_cast<double>(g->stream_local) * 1.25) + g->n_items + 1024;
+        RK(dalloc(&g->d_run_s, cap * 4));
+        RK(dalloc(&g->d_run_e, cap * 4));
+        exact = false;
+        // the chunks counted so far are written now
+        sb::RunIndexArgs f = a;
+        f.item_begin = g->chunk_item[0];
+        f.item_end = g->chunk_item[k + 1];
+        f.run_off = g->d_run_off;
+        f.run_s = g->d_run_s;
+        f.run_e = g->d_run_e;
+        f.run_cap = cap;
+        f.overflow = reinterpret_cast<unsigned int*>(d_aux + 1);
+        RK(sb::launch_run_index(f, true, s));
+      } else if (cap) {
+        sb::RunIndexArgs f = a;
+        f.run_off = g->d_run_off;
+        f.run_s = g->d_run_s;
+        f.run_e = g->d_run_e;
+        f.run_cap = cap;
+        f.overflow = reinterpret_cast<unsigned int*>(d_aux + 1);
+        RK(sb::launch_run_index(f, true, s));
+      }
     }
-    const int rc = graph_wait(g);
-    CK(sync_stream(s));
+    rc = graph_wait(g);
+    RK(sync_stream(s));
     cudaStreamDestroy(s);
-    if (rc) {
-      dfree(d_cnt);
-      return rc;
-    }
+    if (rc) return bail(rc);
     a.err = nullptr;
     a.item_begin = 0;
     a.item_end = g->n_items;
     a.range_end_byte = g->stream_local;
   } else {
-    if (const int rc = graph_wait(g)) {
-      dfree(d_cnt);
-      return rc;
-    }
-    CK(sb::launch_run_index(a, false, 0));
-    CK(sync_stream(0));
+    if (const int rc = graph_wait(g)) return bail(rc);
+    RK(sb::launch_run_index(a, false, 0));
+    RK(sb::launch_run_offsets(d_cnt, g->d_run_off, 0, g->n_items, d_aux, 0));
   }
-  CK(cudaMemcpy(&g->max_run, a.max_run, 4, cudaMemcpyDeviceToHost));
-  std::vector<uint64_t> off(g->n_items + 1, 0);
-  CK(cudaMemcpy(off.data() + 1, d_cnt, g->n_items * 8, cudaMemcpyDeviceToHost));
+  unsigned long long aux[2] = {0, 0};
+  RK(cudaMemcpy(aux, d_aux, 16, cudaMemcpyDeviceToHost));
+  RK(cudaMemcpy(&g->max_run, a.max_run, 4, cudaMemcpyDeviceToHost));
+  g->n_runs = aux[0];
+  RK(cudaMemcpy(g->d_run_off + g->n_items, &aux[0], 8, cudaMemcpyHostToDevice));
+  if (exact || aux[1]) {  // storage from the total (the estimate was too small: rebuild)
+    dfree(g->d_run_s);
+    dfree(g->d_run_e);
+    RK(dalloc(&g->d_run_s, std::max<uint64_t>(g->n_runs, 1) * 4));
+    RK(dalloc(&g->d_run_e, std::max<uint64_t>(g->n_runs, 1) * 4));
+    a.run_off = g->d_run_off;
+    a.run_s = g->d_run_s;
+    a.run_e = g->d_run_e;
+    RK(sb::launch_run_index(a, true, 0));
+  }
+  RK(sync_stream(0));
   dfree(d_cnt);
-  for (uint64_t i = 0; i < g->n_items; ++i) off[i + 1] += off[i];
-  g->n_runs = off[g->n_items];
-  CK(dalloc(&g->d_run_off, off.size() * 8));
-  CK(cudaMemcpy(g->d_run_off, off.data(), off.size() * 8, cudaMemcpyHostToDevice));
-  CK(dalloc(&g->d_run_s, std::max<uint64_t>(g->n_runs, 1) * 4));
-  CK(dalloc(&g->d_run_e, std::max<uint64_t>(g->n_runs, 1) * 4));
-  a.run_off = g->d_run_off;
-  a.run_s = g->d_run_s;
-  a.run_e = g->d_run_e;
-  CK(sb::launch_run_index(a, true, 0));
-  CK(sync_stream(0));
+  dfree(d_aux);
+#undef RK
   return SB_OK;
 }
 

@@ -99,6 +99,8 @@ struct RunIndexArgs {
   const uint64_t* run_off;     // fill pass: offsets (n_items + 1)
   uint32_t* run_s;
   uint32_t* run_e;
+  uint64_t run_cap;            // fill pass: entries of run_s / run_e; an item past it is
+  unsigned int* overflow;      // skipped and flags *overflow (NULL: exact allocation)
 };
 
 struct EstArgs {
@@ -220,6 +222,9 @@ cudaError_t launch_exact_init(int p, const ExactArgs& a, cudaStream_t s);
 cudaError_t launch_exact_init1(int p, const ExactArgs& a, cudaStream_t s);
 cudaError_t launch_exact_count(int p, const ExactArgs& a, cudaStream_t s);
 cudaError_t launch_run_index(const RunIndexArgs& a, bool fill, cudaStream_t s);
+// run_off[i] = *total + exclusive prefix of run_count over items [i0, i1); *total += their sum.
+cudaError_t launch_run_offsets(const uint64_t* run_count, uint64_t* run_off, uint64_t i0, uint64_t i1,
+                               unsigned long long* total, cudaStream_t s);
 cudaError_t launch_estimate(int p, int mode, const EstArgs& a, cudaStream_t s);
 cudaError_t launch_to_packed(int p, const uint8_t* bits, uint8_t* packed, uint64_t rows, cudaStream_t s);
 cudaError_t launch_from_packed(int p, const uint8_t* packed, uint8_t* bits, uint64_t rows, cudaStream_t s);

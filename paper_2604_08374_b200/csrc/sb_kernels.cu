@@ -1421,6 +1421,10 @@ __global__ void __launch_bounds__(256, FILL ? 2 : 3) run_index_kernel(RunIndexAr
     const uint64_t pos0 = a.item_off[item];
     const uint64_t end = item + 1 < a.item_end ? a.item_off[item + 1] : a.range_end_byte;
     const uint64_t out = FILL ? a.run_off[item] : 0;
+    if (FILL && a.overflow && out + a.run_count[item] > a.run_cap) {  // storage sized from an estimate
+      if (lane == 0) *a.overflow = 1u;
+      continue;
+    }
     uint32_t id_before = a.item_base[item];  // warp-uniform: id after the previous window
     uint32_t nruns = 0;                       // warp-uniform: runs started so far
     uint32_t open_start = 0;                  // first id of the open run
@@ -2226,6 +2230,53 @@ cudaError_t launch_exact_count(int p, const ExactArgs& a, cudaStream_t s) {
     default: return cudaErrorInvalidValue;
   }
 #undef SB_L
+  return cudaGetLastError();
+}
+
+// Exclusive scan of one upload chunk's run counts into run offsets, carried
+// from the chunks before it (*total), one CTA: each thread scans a contiguous
+// span, the span sums are scanned across the block.
+__global__ void __launch_bounds__(1024) run_offsets_kernel(const uint64_t* __restrict__ cnt, uint64_t* off,
+                                                           uint64_t i0, uint64_t i1, unsigned long long* total) {
+  __shared__ unsigned long long wsum[32];
+  const uint64_t n = i1 - i0;
+  const uint64_t per = (n + blockDim.x - 1) / blockDim.x;
+  const uint64_t b = i0 + threadIdx.x * per, e = b + per < i1 ? b + per : i1;
+  unsigned long long mine = 0;
+  for (uint64_t i = b; i < e; ++i) mine += cnt[i];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned long long incl = mine;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const unsigned long long y = __shfl_up_sync(FULL, incl, d);
+    if (lane >= d) incl += y;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    unsigned long long w = lane < static_cast<int>(blockDim.x >> 5) ? wsum[lane] : 0ull, wi = w;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const unsigned long long y = __shfl_up_sync(FULL, wi, d);
+      if (lane >= d) wi += y;
+    }
+    wsum[lane] = wi - w;  // exclusive over warps
+  }
+  __syncthreads();
+  const unsigned long long base = *total;
+  unsigned long long run = base + wsum[warp] + incl - mine;
+  for (uint64_t i = b; i < e; ++i) {
+    off[i] = run;
+    run += cnt[i];
+  }
+  __syncthreads();
+  if (threadIdx.x == blockDim.x - 1) *total = run;  // the last thread's span ends the chunk
+}
+
+cudaError_t launch_run_offsets(const uint64_t* run_count, uint64_t* run_off, uint64_t i0, uint64_t i1,
+                               unsigned long long* total, cudaStream_t s) {
+  if (i1 <= i0) return cudaSuccess;
+  run_offsets_kernel<<<1, 1024, 0, s>>>(run_count, run_off, i0, i1, total);
   return cudaGetLastError();
 }
 
