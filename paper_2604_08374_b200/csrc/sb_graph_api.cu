@@ -9,13 +9,35 @@
 #include "sb_device.cuh"
 #include "sb_handles.h"
 
-// Also sets g->max_run (longest run within a work item; sizes the interval
-// mode's sparse table).
-int build_run_index(sb_graph* g) {
-  if (g->d_run_off || g->n_items == 0) return SB_OK;
-  if (g->broken) return fail(SB_ERUNTIME, "cgraph: the graph failed validation at upload");
+// ------------------------------------------------------------------ run index
+// Runs of consecutive ids per work item (interval mode, exact mode, local
+// metrics), decoded once from the device-resident stream: count pass, device
+// scan of offsets, fill pass.  Also sets g->max_run (longest run within a work
+// item; sizes the interval mode's sparse table).
+static void rix_free(RunIndexJob& j) {
+  dfree(j.d_cnt);
+  dfree(j.d_aux);
+  for (cudaEvent_t e : j.ready) cudaEventDestroy(e);
+  j.ready.clear();
+  if (j.s) {
+    cudaStreamSynchronize(j.s);
+    cudaStreamDestroy(j.s);
+    j.s = nullptr;
+  }
+}
+
+void rix_abort(sb_graph* g, RunIndexJob& j) {
+  rix_free(j);
+  dfree(g->d_run_off);
+  dfree(g->d_run_s);
+  dfree(g->d_run_e);
+  g->n_runs = 0;
+}
+
+static int rix_setup(sb_graph* g, RunIndexJob& j) {
   if (reinterpret_cast<uintptr_t>(g->d_stream) & 15) return fail(SB_ERUNTIME, "internal: stream not 16-B aligned");
-  sb::RunIndexArgs a{};
+  sb::RunIndexArgs& a = j.a;
+  a = sb::RunIndexArgs{};
   a.stream = g->d_stream;
   a.stream_len = g->stream_local;
   a.item_off = g->d_item_off;
@@ -25,116 +47,131 @@ int build_run_index(sb_graph* g) {
   a.item_begin = 0;
   a.item_end = g->n_items;
   a.range_end_byte = g->stream_local;
-  uint64_t* d_cnt = nullptr;
-  unsigned long long* d_aux = nullptr;  // [0] run total, [1] overflow flag
-  CK(dalloc(&d_cnt, g->n_items * 8 + 8));
-  CK(dalloc(&d_aux, 2 * 8));
-  auto bail = [&](int rc) {
-    dfree(d_cnt);
-    dfree(d_aux);
-    dfree(g->d_run_off);
-    dfree(g->d_run_s);
-    dfree(g->d_run_e);
-    g->n_runs = 0;
-    return rc;
-  };
-#define RK(x)                                                 \
-  do {                                                        \
-    cudaError_t e_ = (x);                                     \
-    if (e_ != cudaSuccess) return bail(cuda_fail(e_, #x));    \
-  } while (0)
-  a.run_count = d_cnt;
-  a.max_run = reinterpret_cast<unsigned int*>(d_cnt + g->n_items);
-  RK(cudaMemsetAsync(a.max_run, 0, 4, 0));
-  RK(cudaMemsetAsync(d_aux, 0, 16, 0));
-  RK(dalloc(&g->d_run_off, (g->n_items + 1) * 8));
-  bool exact = true;  // run storage sized from the final total (else from an estimate)
-  if (g->pending && g->chunk_item.size() > 2) {
-    // Still uploading: chunk k's runs are counted, offset and written as soon
-    // as chunk k is validated, so the whole index hides under the remaining
-    // PCIe copies.  The run storage is sized before the total is known, from
-    // the runs per stream byte of the first full-size chunk (x 1.25 + slack);
-    // an item that would not fit is skipped and flagged, and the index is then
-    // rebuilt with exact storage after the upload.
-    cudaStream_t s = nullptr;
-    RK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    RK(sync_stream(0));  // the resets above
-    a.err = g->d_err;
-    const size_t nk = g->chunk_item.size() - 1;
-    const size_t probe = std::min<size_t>(1, nk - 1);  // chunk 0 is the small 1/64 one
-    uint64_t cap = 0;
-    int rc = SB_OK;
-    for (size_t k = 0; k < nk && !rc; ++k) {
-      a.item_begin = g->chunk_item[k];
-      a.item_end = g->chunk_item[k + 1];
-      a.range_end_byte = g->chunk_byte[k + 1];  // the next chunk's items are not cut yet
-      if (a.item_end == a.item_begin) continue;
-      RK(cudaStreamWaitEvent(s, g->val_ev[k], 0));
-      RK(sb::launch_run_index(a, false, s));
-      RK(sb::launch_run_offsets(d_cnt, g->d_run_off, a.item_begin, a.item_end, d_aux, s));
-      if (k == probe || (cap == 0 && k + 1 == nk)) {
-        unsigned long long tot = 0;
-        RK(cudaMemcpyAsync(&tot, d_aux, 8, cudaMemcpyDeviceToHost, s));
-        RK(sync_stream(s));
-        const uint64_t bytes = std::max<uint64_t>(g->chunk_byte[k + 1], 1);
-        cap = static_cast<uint64_t>(static_cast<double>(tot) / static_cast<double>(bytes) *
-                                    static_cast<double>(g->stream_local) * 1.25) + g->n_items + 1024;
-        RK(dalloc(&g->d_run_s, cap * 4));
-        RK(dalloc(&g->d_run_e, cap * 4));
-        exact = false;
-        // the chunks counted so far are written now
-        sb::RunIndexArgs f = a;
-        f.item_begin = g->chunk_item[0];
-        f.item_end = g->chunk_item[k + 1];
-        f.run_off = g->d_run_off;
-        f.run_s = g->d_run_s;
-        f.run_e = g->d_run_e;
-        f.run_cap = cap;
-        f.overflow = reinterpret_cast<unsigned int*>(d_aux + 1);
-        RK(sb::launch_run_index(f, true, s));
-      } else if (cap) {
-        sb::RunIndexArgs f = a;
-        f.run_off = g->d_run_off;
-        f.run_s = g->d_run_s;
-        f.run_e = g->d_run_e;
-        f.run_cap = cap;
-        f.overflow = reinterpret_cast<unsigned int*>(d_aux + 1);
-        RK(sb::launch_run_index(f, true, s));
-      }
-    }
-    rc = graph_wait(g);
-    RK(sync_stream(s));
-    cudaStreamDestroy(s);
-    if (rc) return bail(rc);
-    a.err = nullptr;
-    a.item_begin = 0;
-    a.item_end = g->n_items;
-    a.range_end_byte = g->stream_local;
-  } else {
-    if (const int rc = graph_wait(g)) return bail(rc);
-    RK(sb::launch_run_index(a, false, 0));
-    RK(sb::launch_run_offsets(d_cnt, g->d_run_off, 0, g->n_items, d_aux, 0));
-  }
-  unsigned long long aux[2] = {0, 0};
-  RK(cudaMemcpy(aux, d_aux, 16, cudaMemcpyDeviceToHost));
-  RK(cudaMemcpy(&g->max_run, a.max_run, 4, cudaMemcpyDeviceToHost));
-  g->n_runs = aux[0];
-  RK(cudaMemcpy(g->d_run_off + g->n_items, &aux[0], 8, cudaMemcpyHostToDevice));
-  if (exact || aux[1]) {  // storage from the total (the estimate was too small: rebuild)
-    dfree(g->d_run_s);
-    dfree(g->d_run_e);
-    RK(dalloc(&g->d_run_s, std::max<uint64_t>(g->n_runs, 1) * 4));
-    RK(dalloc(&g->d_run_e, std::max<uint64_t>(g->n_runs, 1) * 4));
-    a.run_off = g->d_run_off;
-    a.run_s = g->d_run_s;
-    a.run_e = g->d_run_e;
-    RK(sb::launch_run_index(a, true, 0));
-  }
-  RK(sync_stream(0));
-  dfree(d_cnt);
-  dfree(d_aux);
-#undef RK
+  CK(dalloc(&j.d_cnt, g->n_items * 8 + 8));
+  CK(dalloc(&j.d_aux, 2 * 8));
+  CK(dalloc(&g->d_run_off, (g->n_items + 1) * 8));
+  a.run_count = j.d_cnt;
+  a.max_run = reinterpret_cast<unsigned int*>(j.d_cnt + g->n_items);
+  CK(cudaMemsetAsync(a.max_run, 0, 4, 0));
+  CK(cudaMemsetAsync(j.d_aux, 0, 16, 0));
+  CK(sync_stream(0));
   return SB_OK;
+}
+
+int rix_begin(sb_graph* g, RunIndexJob& j) {
+  if (const int rc = rix_setup(g, j)) return rc;
+  CK(cudaStreamCreateWithFlags(&j.s, cudaStreamNonBlocking));
+  j.a.err = g->d_err;
+  const size_t nk = g->chunk_item.size() - 1;
+  j.probe = std::min<size_t>(1, nk - 1);  // chunk 0 is the small 1/64 one
+  j.ready.assign(nk, nullptr);
+  for (auto& e : j.ready) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  return SB_OK;
+}
+
+static int rix_fill(sb_graph* g, RunIndexJob& j, size_t k_end) {  // fills chunks [filled, k_end)
+  if (k_end <= j.filled) return SB_OK;
+  sb::RunIndexArgs f = j.a;
+  f.item_begin = g->chunk_item[j.filled];
+  f.item_end = g->chunk_item[k_end];
+  f.range_end_byte = g->chunk_byte[k_end];  // the next chunk's items are not cut yet
+  f.run_off = g->d_run_off;
+  f.run_s = g->d_run_s;
+  f.run_e = g->d_run_e;
+  f.run_cap = j.cap;
+  f.overflow = reinterpret_cast<unsigned int*>(j.d_aux + 1);
+  if (f.item_end > f.item_begin) CK(sb::launch_run_index(f, true, j.s));
+  for (size_t k = j.filled; k < k_end; ++k) CK(cudaEventRecord(j.ready[k], j.s));
+  j.filled = k_end;
+  return SB_OK;
+}
+
+// Chunk k (after its validation): count + offsets; the first full-size chunk
+// sizes the run storage from its runs per stream byte (x 1.25 + slack) and
+// the chunks so far are written; later chunks are written at once.
+int rix_chunk(sb_graph* g, RunIndexJob& j, size_t k) {
+  sb::RunIndexArgs& a = j.a;
+  const size_t nk = g->chunk_item.size() - 1;
+  a.item_begin = g->chunk_item[k];
+  a.item_end = g->chunk_item[k + 1];
+  a.range_end_byte = g->chunk_byte[k + 1];
+  CK(cudaStreamWaitEvent(j.s, g->val_ev[k], 0));
+  if (a.item_end > a.item_begin) {
+    CK(sb::launch_run_index(a, false, j.s));
+    CK(sb::launch_run_offsets(j.d_cnt, g->d_run_off, a.item_begin, a.item_end, j.d_aux, j.s));
+  }
+  if (!j.cap && (k >= j.probe || k + 1 == nk)) {
+    unsigned long long tot = 0;
+    CK(cudaMemcpyAsync(&tot, j.d_aux, 8, cudaMemcpyDeviceToHost, j.s));
+    CK(sync_stream(j.s));
+    const uint64_t bytes = std::max<uint64_t>(g->chunk_byte[k + 1], 1);
+    j.cap = static_cast<uint64_t>(static_cast<double>(tot) / static_cast<double>(bytes) *
+                                  static_cast<double>(g->stream_local) * 1.25) + g->n_items + 1024;
+    CK(dalloc(&g->d_run_s, j.cap * 4));
+    CK(dalloc(&g->d_run_e, j.cap * 4));
+  }
+  if (j.cap) return rix_fill(g, j, k + 1);
+  return SB_OK;
+}
+
+int rix_finish(sb_graph* g, RunIndexJob& j, bool* overflow) {
+  *overflow = false;
+  CK(sync_stream(j.s));
+  unsigned long long aux[2] = {0, 0};
+  CK(cudaMemcpy(aux, j.d_aux, 16, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(&g->max_run, j.a.max_run, 4, cudaMemcpyDeviceToHost));
+  g->n_runs = aux[0];
+  CK(cudaMemcpy(g->d_run_off + g->n_items, &aux[0], 8, cudaMemcpyHostToDevice));
+  *overflow = aux[1] != 0 || j.filled + 1 < g->chunk_item.size();
+  rix_free(j);
+  return SB_OK;
+}
+
+int build_run_index(sb_graph* g) {
+  if (g->d_run_off || g->n_items == 0) return SB_OK;
+  if (g->broken) return fail(SB_ERUNTIME, "cgraph: the graph failed validation at upload");
+  RunIndexJob j;
+  if (g->pending && g->chunk_item.size() > 2) {
+    // still uploading: the index is built chunk by chunk under the PCIe copies
+    int rc = rix_begin(g, j);
+    for (size_t k = 0; k + 1 < g->chunk_item.size() && !rc; ++k) rc = rix_chunk(g, j, k);
+    if (!rc) rc = graph_wait(g);
+    bool overflow = false;
+    if (!rc) rc = rix_finish(g, j, &overflow);
+    if (rc) {
+      rix_abort(g, j);
+      return rc;
+    }
+    if (!overflow) return SB_OK;
+    rix_abort(g, j);  // storage estimate too small: rebuild with exact storage
+  }
+  if (const int rc = graph_wait(g)) return rc;
+  int rc = rix_setup(g, j);
+  sb::RunIndexArgs& a = j.a;
+  auto done = [&](int r) {
+    if (r) rix_abort(g, j);
+    else rix_free(j);
+    return r;
+  };
+  if (rc) return done(rc);
+  cudaError_t e = sb::launch_run_index(a, false, 0);
+  if (e == cudaSuccess) e = sb::launch_run_offsets(j.d_cnt, g->d_run_off, 0, g->n_items, j.d_aux, 0);
+  unsigned long long tot = 0;
+  if (e == cudaSuccess) e = cudaMemcpy(&tot, j.d_aux, 8, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(&g->max_run, a.max_run, 4, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return done(cuda_fail(e, "run index count"));
+  g->n_runs = tot;
+  e = cudaMemcpy(g->d_run_off + g->n_items, &tot, 8, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = dalloc(&g->d_run_s, std::max<uint64_t>(g->n_runs, 1) * 4);
+  if (e == cudaSuccess) e = dalloc(&g->d_run_e, std::max<uint64_t>(g->n_runs, 1) * 4);
+  if (e != cudaSuccess) return done(cuda_fail(e, "run index storage"));
+  a.run_off = g->d_run_off;
+  a.run_s = g->d_run_s;
+  a.run_e = g->d_run_e;
+  e = sb::launch_run_index(a, true, 0);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(0);
+  if (e != cudaSuccess) return done(cuda_fail(e, "run index fill"));
+  return done(SB_OK);
 }
 
 

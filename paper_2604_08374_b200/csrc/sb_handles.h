@@ -396,3 +396,21 @@ int graph_setup(sb_graph* g, const uint32_t* deg_local);
 void graph_union_args(const sb_graph* g, sb::UnionArgs& u);
 int graph_wait(sb_graph* g);
 int build_run_index(sb_graph* g);
+// The run index built incrementally over an asynchronous upload: chunk k is
+// counted, offset and (once the storage is sized) written after its
+// validation; ready[k] fires when chunk k's runs are in place.
+struct RunIndexJob {
+  sb::RunIndexArgs a{};
+  uint64_t* d_cnt = nullptr;
+  unsigned long long* d_aux = nullptr;  // [0] run total, [1] overflow flag
+  uint64_t cap = 0;                     // run storage entries (0: not yet allocated)
+  size_t probe = 0, filled = 0;         // chunks [0, filled) have their fill enqueued
+  cudaStream_t s = nullptr;
+  std::vector<cudaEvent_t> ready;
+};
+int rix_begin(sb_graph* g, RunIndexJob& j);
+int rix_chunk(sb_graph* g, RunIndexJob& j, size_t k);
+// After the upload: totals, last offset, max run; *overflow: the estimate was
+// too small (the index must be rebuilt: rix_abort + build_run_index).
+int rix_finish(sb_graph* g, RunIndexJob& j, bool* overflow);
+void rix_abort(sb_graph* g, RunIndexJob& j);

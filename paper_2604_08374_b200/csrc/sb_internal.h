@@ -217,6 +217,9 @@ cudaError_t launch_union(int p, bool skip, const UnionArgs& a, cudaStream_t s);
 cudaError_t launch_st_build(int p, const uint8_t* cur, uint8_t* st, uint64_t n, int levels, cudaStream_t s,
                             bool orop = false);
 cudaError_t launch_union_interval(int p, const IntervalArgs& a, cudaStream_t s, bool orop = false);
+// Sparse-table levels 1..levels for rows [r0, r1) (each level over the rows the next one reads).
+cudaError_t launch_st_build_rows(int p, const uint8_t* cur, uint8_t* st, uint64_t n, int levels, uint64_t r0,
+                                 uint64_t r1, cudaStream_t s);
 cudaError_t launch_union_or(int p, const UnionArgs& a, cudaStream_t s);
 cudaError_t launch_exact_init(int p, const ExactArgs& a, cudaStream_t s);
 cudaError_t launch_exact_init1(int p, const ExactArgs& a, cudaStream_t s);

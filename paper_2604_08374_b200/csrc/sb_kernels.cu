@@ -1400,6 +1400,23 @@ __global__ void st_build_kernel(const uint8_t* __restrict__ src, uint8_t* __rest
   }
 }
 
+// The same level step over rows [r0, r1) only (the wavefront builds each
+// upload chunk's table rows as soon as the rows they read are final).
+template <int P, bool OR>
+__global__ void st_build_rows_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, uint64_t n,
+                                     uint64_t half, uint64_t r0, uint64_t r1) {
+  using G = Geo<P>;
+  using IO = GrpIO<G::GB>;
+  const uint64_t g0 = r0 * G::GROUPS, g1 = r1 * G::GROUPS;
+  for (uint64_t i = g0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < g1;
+       i += gridDim.x * (uint64_t)blockDim.x) {
+    const uint64_t j = i / G::GROUPS;
+    Grp x = IO::ld(src + i * G::GB);
+    if (j + half < n) combine<OR>(x, IO::ld(src + (i + half * G::GROUPS) * G::GB));
+    IO::st(dst + i * G::GB, x);
+  }
+}
+
 // Run index: one warp per work item streams the item's bytes (items tile the
 // stream: item i ends where item i+1 starts) in 512-byte windows, 16 bytes per
 // lane with the validation kernel's SWAR arithmetic.  The stream is validated,
@@ -1673,7 +1690,7 @@ __global__ void __launch_bounds__(256, 4) union_interval_kernel(IntervalArgs ia)
   const int warp = threadIdx.x >> 5;
   const uint64_t total = a.n_tiles * G::SLICES;
   for (int k = 0;; ++k) {
-    if (threadIdx.x == 0) s_unit[k & 1] = atomicAdd(a.work, 1ull);
+    if (threadIdx.x == 0) s_unit[k & 1] = upload_failed(a) ? total : atomicAdd(a.work, 1ull);
     __syncthreads();
     const unsigned long long u = s_unit[k & 1];
     if (u >= total) break;
@@ -2114,6 +2131,29 @@ cudaError_t launch_st_build(int p, const uint8_t* cur, uint8_t* st, uint64_t n, 
       else                                                                                       \
         st_build_kernel<P, false><<<g, 256, 0, s>>>(src, st + static_cast<uint64_t>(k - 1) * rowb, n, 1ull << (k - 1)); \
     }                                                                                            \
+  }
+  SB_DISPATCH_P(p, SB_L)
+#undef SB_L
+  return cudaGetLastError();
+}
+
+cudaError_t launch_st_build_rows(int p, const uint8_t* cur, uint8_t* st, uint64_t n, int levels, uint64_t r0,
+                                 uint64_t r1, cudaStream_t s) {
+  // level k of rows [r0, r1) reads level k-1 up to 2^(k-1) rows further: build
+  // level k over [r0, r1 + 2^K - 2^k), so the top level covers exactly [r0, r1)
+#define SB_L(P)                                                                                       \
+  {                                                                                                   \
+    const uint64_t rowb = n * Geo<P>::ROW;                                                            \
+    for (int k = 1; k <= levels; ++k) {                                                               \
+      const uint64_t e = r1 + (1ull << levels) - (1ull << k);                                         \
+      const uint64_t hi = e < n ? e : n;                                                              \
+      if (hi <= r0) continue;                                                                         \
+      const uint64_t groups = (hi - r0) * Geo<P>::GROUPS;                                             \
+      const int g = static_cast<int>(groups / 256 + 1 < 148 * 8 ? groups / 256 + 1 : 148 * 8);        \
+      const uint8_t* src = k == 1 ? cur : st + static_cast<uint64_t>(k - 2) * rowb;                   \
+      st_build_rows_kernel<P, false><<<g, 256, 0, s>>>(src, st + static_cast<uint64_t>(k - 1) * rowb, n, \
+                                                        1ull << (k - 1), r0, hi);                     \
+    }                                                                                                 \
   }
   SB_DISPATCH_P(p, SB_L)
 #undef SB_L
