@@ -302,6 +302,9 @@ struct sb_hb {
   // wavefront first run (pipelined_run): a plane + changed flags per pass >= 2,
   // a stream per pass, an event per (pass, chunk), pass start / end events
   std::vector<uint8_t*> d_xplane, d_xchg;
+  std::vector<uint8_t*> d_xst;            // interval mode: a sparse table per wavefront pass
+  std::vector<cudaEvent_t> sev;            // interval mode: sparse-table rows of (pass, chunk) ready
+  bool index_ready = true;                 // interval mode: run index + sparse table allocated
   std::vector<cudaStream_t> pstream;
   std::vector<cudaEvent_t> pev, pev_t;
   // back-to-back passes (batched_run): device flags [stop, last pass, converged],
@@ -341,6 +344,8 @@ struct sb_hb {
     dfree(d_misc); dfree(d_tmp); dfree(d_st); dfree(d_chunk_work); dfree(d_pwork);
     for (uint8_t* x : d_xplane) dfree(x);
     for (uint8_t* x : d_xchg) dfree(x);
+    for (uint8_t* x : d_xst) dfree(x);
+    for (cudaEvent_t e : sev) cudaEventDestroy(e);
     for (cudaEvent_t e : pev) cudaEventDestroy(e);
     for (cudaEvent_t e : pev_t) cudaEventDestroy(e);
     for (cudaEvent_t e : bev) cudaEventDestroy(e);

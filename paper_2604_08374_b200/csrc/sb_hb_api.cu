@@ -66,6 +66,33 @@ static void hb_union_args(const sb_hb* h, sb::UnionArgs& u) {
   if (!u.node_lo && !(h->flags & SB_HB_SCHEDULE_GROUP) && !g->pending) u.n_tiles = 0;
 }
 
+// Whether the first sb_hb_run over this handle's graph can be the wavefront of
+// pipelined_run (a long asynchronous upload of one unsharded graph).
+static bool wave_ok(const sb_hb* h) {
+  const sb_graph* g = h->g;
+  if (!g->pending || !g->d_chunk_rng || g->chunk_node.size() < 3) return false;
+  if ((h->flags & (SB_HB_SKIP_UNCHANGED | SB_HB_SCHEDULE_WARP)) || h->npeers || h->comm) return false;
+  if (g->v0 != 0 || g->n_local != g->n) return false;
+  return g->stream_local >= (1ull << 30) || (h->flags & SB_HB_WAVEFRONT);
+}
+
+// Interval mode: the run index (built on first use; waits for an upload) and
+// the sparse table, K = floor(log2(longest run)) levels, capped at 10 (longer
+// runs peel 2^K blocks).
+static int ensure_interval_ready(sb_hb* h) {
+  if (!(h->flags & SB_HB_INTERVAL) || h->index_ready) return SB_OK;
+  sb_graph* g = h->g;
+  DeviceGuard dg(g->device);
+  if (const int rc = build_run_index(g)) return rc;
+  int K = 0;
+  while (K < 10 && (2u << K) <= g->max_run) ++K;
+  h->levels = K;
+  dfree(h->d_st);
+  if (K) CK(dalloc(&h->d_st, static_cast<uint64_t>(K) * g->n * h->row + 64));
+  h->index_ready = true;
+  return SB_OK;
+}
+
 extern "C" {
 
 int sb_hb_create(sb_graph* g, unsigned p, uint32_t depth_limit, uint32_t flags, sb_hb** out) {
@@ -124,13 +151,13 @@ int sb_hb_create(sb_graph* g, unsigned p, uint32_t depth_limit, uint32_t flags, 
   HK(dalloc(&h->d_counter, nl * h->slices * 4));
   HK(dalloc(&h->d_misc, 4 * 8));
   if (flags & SB_HB_INTERVAL) {
-    const int rc = build_run_index(g);  // waits for an asynchronous upload; sets max_run
-    if (rc) return bail(rc);
-    // levels K = floor(log2(longest run)), capped at 10 (longer runs peel 2^K blocks)
-    int K = 0;
-    while (K < 10 && (2u << K) <= g->max_run) ++K;
-    h->levels = K;
-    if (K) HK(dalloc(&h->d_st, static_cast<uint64_t>(K) * plane + 64));
+    // over a long asynchronous upload the run index is built inside the first
+    // run's wavefront (pipelined_run); otherwise now (waits for the upload)
+    h->index_ready = false;
+    if (!wave_ok(h)) {
+      const int rc = ensure_interval_ready(h);
+      if (rc) return bail(rc);
+    }
   }
   HK(pinned_get(&h->h_misc, &h->h_misc_owned));
 #undef HK
@@ -164,6 +191,7 @@ int sb_hb_step_compute(sb_hb* h, double* local_max) {
   sb_graph* g = h->g;
   DeviceGuard dg(g->device);
   if (g->broken) return fail(SB_ERUNTIME, "cgraph: the graph failed validation at upload");
+  if (const int rc = ensure_interval_ready(h)) return rc;
   if (g->pending && (h->flags & SB_HB_SCHEDULE_WARP)) {  // the chunk pipeline needs the tile schedule
     const int rc = graph_wait(g);
     if (rc) return rc;
@@ -406,23 +434,22 @@ int sb_hb_step(sb_hb* h, double* max_increase, int* converged, int* finished) {
 static int pipelined_run(sb_hb* h, bool* done) {
   *done = false;
   sb_graph* g = h->g;
-  if (!g->pending || !g->d_chunk_rng || g->chunk_node.size() < 3 || h->t != 0 || h->finished || h->computed)
-    return SB_OK;
-  if ((h->flags & (SB_HB_INTERVAL | SB_HB_SKIP_UNCHANGED | SB_HB_SCHEDULE_WARP)) || h->npeers || h->comm)
-    return SB_OK;
-  if (g->v0 != 0 || g->n_local != g->n) return SB_OK;
-  // worth its fixed cost (a stream per pass, events, extra planes) only when
-  // the upload is long: >= 1 GB is >= 18 ms of PCIe (C3: 4.8 GB, 95 ms)
-  if (g->stream_local < (1ull << 30) && !(h->flags & SB_HB_WAVEFRONT)) return SB_OK;
+  if (h->t != 0 || h->finished || h->computed || !wave_ok(h)) return SB_OK;
+  const bool iv = (h->flags & SB_HB_INTERVAL) != 0;
+  if (iv && (h->index_ready || g->d_run_off)) return SB_OK;  // interval: the index is built in here
   DeviceGuard dg(g->device);
   const int nk = static_cast<int>(g->chunk_node.size() - 1);
   const uint64_t plane = g->n * h->row;
-  // passes that may overlap the upload: a plane each, within a quarter of free HBM
+  // interval mode: the sparse table of every pass, at the largest level count
+  // (the longest run is only known once every chunk is counted)
+  const int K = iv ? 10 : 0;
+  const uint64_t per_pass = plane + 64 + g->n + (iv ? static_cast<uint64_t>(K) * plane + 64 : 0);
+  // passes that may overlap the upload: a plane (+ table) each, within a quarter of free HBM
   int P = 12;
   if (h->depth) P = std::min<int>(P, static_cast<int>(h->depth));
   size_t fr = 0, tot = 0;
   CK(cudaMemGetInfo(&fr, &tot));
-  while (P > 2 && static_cast<uint64_t>(P - 1) * (plane + 64 + g->n) > fr / 4) --P;
+  while (P > 2 && static_cast<uint64_t>(P) * per_pass > fr / 4) --P;
   if (P < 2) return SB_OK;
   // resources (kept on the handle: the next first run reuses them).  The
   // planes of passes 2..5 up front -- a graph's first pool growth maps new
@@ -439,7 +466,16 @@ static int pipelined_run(sb_hb* h, bool* done) {
     }
     return SB_OK;
   };
+  auto more_tables = [&](int count) -> int {  // interval: tables of passes 0 .. count-1
+    while (iv && static_cast<int>(h->d_xst.size()) < count) {
+      uint8_t* x = nullptr;
+      CK(dalloc(&x, static_cast<uint64_t>(K) * plane + 64));
+      h->d_xst.push_back(x);
+    }
+    return SB_OK;
+  };
   if (const int rc0 = more_planes(std::min(P - 1, 4))) return rc0;
+  if (const int rc0 = more_tables(std::min(P, 5))) return rc0;
   while (static_cast<int>(h->pstream.size()) < P) {
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);  // hi is the numerically smaller, higher priority
@@ -448,16 +484,18 @@ static int pipelined_run(sb_hb* h, bool* done) {
     CK(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, pr));
     h->pstream.push_back(st);
   }
-  while (static_cast<int>(h->pev.size()) < P * nk) {
-    cudaEvent_t e = nullptr;
-    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    h->pev.push_back(e);
-  }
-  while (static_cast<int>(h->pev_t.size()) < 2 * P) {
-    cudaEvent_t e = nullptr;
-    CK(cudaEventCreate(&e));
-    h->pev_t.push_back(e);
-  }
+  auto more_events = [&](std::vector<cudaEvent_t>& v, size_t count, unsigned flags) -> int {
+    while (v.size() < count) {
+      cudaEvent_t e = nullptr;
+      CK(cudaEventCreateWithFlags(&e, flags));
+      v.push_back(e);
+    }
+    return SB_OK;
+  };
+  if (const int rc0 = more_events(h->pev, static_cast<size_t>(P) * nk, cudaEventDisableTiming)) return rc0;
+  if (const int rc0 = more_events(h->pev_t, 2 * static_cast<size_t>(P), cudaEventDefault)) return rc0;
+  if (iv)
+    if (const int rc0 = more_events(h->sev, static_cast<size_t>(P) * nk, cudaEventDisableTiming)) return rc0;
   if (h->pwork_n < static_cast<size_t>(P * nk)) {
     dfree(h->d_pwork);
     h->pwork_n = 0;
@@ -465,32 +503,45 @@ static int pipelined_run(sb_hb* h, bool* done) {
     h->pwork_n = static_cast<size_t>(P * nk);
   }
   // pass p's registers / changed flags: p = 0 the initialised plane, p = 1
-  // the second plane, p >= 2 the extra ones
+  // the second plane, p >= 2 the extra ones; interval: table of pass p's plane
   auto pl = [&](int p) { return p == 0 ? h->d_plane[0] : p == 1 ? h->d_plane[1] : h->d_xplane[p - 2]; };
   auto cg = [&](int p) { return p == 0 ? h->d_changed[0] : p == 1 ? h->d_changed[1] : h->d_xchg[p - 2]; };
+  auto stp = [&](int p) { return h->d_xst[p]; };
+  RunIndexJob job;
+  if (iv) {
+    if (const int rc0 = rix_begin(g, job)) {
+      rix_abort(g, job);
+      return rc0;
+    }
+    CK(sb::launch_st_build(static_cast<int>(h->p), pl(0), stp(0), g->n, K, h->stream));  // the initial plane's table
+  }
   CK(cudaMemsetAsync(h->d_pwork, 0, static_cast<size_t>(P * nk) * 8, h->stream));
-  CK(cudaEventRecord(h->ev[0], h->stream));  // init + counters done before any pass starts
+  CK(cudaEventRecord(h->ev[0], h->stream));  // init + counters (+ table 0) done before any pass starts
   for (int p = 0; p < P; ++p) CK(cudaStreamWaitEvent(h->pstream[p], h->ev[0], 0));
   sb::UnionArgs base{};
   hb_union_args(h, base);
-  base.err = g->d_err;  // every CTA stops if a chunk failed validation
-  std::vector<int> dlo(nk, 0), dhi(nk, -1), next(P + 1, 0);
+  base.err = g->d_err;    // every CTA stops if a chunk failed validation
+  base.stop = nullptr;
+  std::vector<int> dlo(nk, 0), dhi(nk, -1), next(P + 1, 0), next_st(P + 1, 0);
   auto chunk_of = [&](uint64_t id) {
     const int k = static_cast<int>(std::upper_bound(g->chunk_node.begin(), g->chunk_node.end(), id) -
                                    g->chunk_node.begin()) - 1;
     return std::min(std::max(k, 0), nk - 1);
   };
+  // interval: the last chunk whose plane rows table (p, k) reads (2^K - 1 rows past k)
+  auto kst = [&](int k) { return chunk_of(std::min<uint64_t>(g->n - 1, g->chunk_node[k + 1] + (1ull << K) - 2)); };
   auto launch = [&](int p, int k) -> int {  // pass p (1-based) of chunk k
     if (const int rc0 = more_planes(p - 1)) return rc0;
     cudaStream_t st = h->pstream[p - 1];
     if (k == 0) CK(cudaEventRecord(h->pev_t[2 * (p - 1)], st));
     if (p == 1) {
-      CK(cudaStreamWaitEvent(st, g->val_ev[k], 0));
+      CK(cudaStreamWaitEvent(st, iv ? job.ready[k] : g->val_ev[k], 0));
     } else {
-      // the chunks its rows reference, and always the chunk itself (its items'
-      // partial rows and arrival counters are reused by the next pass)
-      if (k < dlo[k] || k > dhi[k]) CK(cudaStreamWaitEvent(st, h->pev[(p - 2) * nk + k], 0));
-      for (int j = dlo[k]; j <= dhi[k]; ++j) CK(cudaStreamWaitEvent(st, h->pev[(p - 2) * nk + j], 0));
+      // the chunks its rows reference (interval: their table rows), and always
+      // the chunk itself (its items' partial rows and arrival counters are reused)
+      const std::vector<cudaEvent_t>& dep = iv ? h->sev : h->pev;
+      CK(cudaStreamWaitEvent(st, h->pev[(p - 2) * nk + k], 0));
+      for (int j = dlo[k]; j <= dhi[k]; ++j) CK(cudaStreamWaitEvent(st, dep[(p - 2) * nk + j], 0));
     }
     const uint64_t n0 = g->chunk_node[k], n1 = g->chunk_node[k + 1];
     CK(cudaMemsetAsync(cg(p) + n0, 0, n1 - n0, st));
@@ -505,20 +556,70 @@ static int pipelined_run(sb_hb* h, bool* done) {
       u.tile_node0 = g->d_tile_node0 + t0;
       u.tile_q = g->d_tile_q + t0;
       u.n_tiles = t1 - t0;
-      CK(sb::launch_union(static_cast<int>(h->p), false, u, st));
+      if (iv) {
+        sb::IntervalArgs ia{};
+        ia.u = u;
+        ia.st = stp(p - 1);
+        ia.n_global = g->n;
+        ia.levels = K;
+        ia.run_off = g->d_run_off;
+        ia.run_s = g->d_run_s;
+        ia.run_e = g->d_run_e;
+        CK(sb::launch_union_interval(static_cast<int>(h->p), ia, st));
+      } else {
+        CK(sb::launch_union(static_cast<int>(h->p), false, u, st));
+      }
     }
     CK(cudaEventRecord(h->pev[(p - 1) * nk + k], st));
     if (k == nk - 1) CK(cudaEventRecord(h->pev_t[2 * (p - 1) + 1], st));
     return SB_OK;
   };
+  auto launch_st = [&](int p, int k) -> int {  // table of pass p, rows of chunk k (after union(p) to kst(k))
+    if (const int rc0 = more_tables(p + 1)) return rc0;
+    cudaStream_t st = h->pstream[p - 1];
+    CK(sb::launch_st_build_rows(static_cast<int>(h->p), pl(p), stp(p), g->n, K, g->chunk_node[k],
+                                g->chunk_node[k + 1], st));
+    CK(cudaEventRecord(h->sev[(p - 1) * nk + k], st));
+    return SB_OK;
+  };
+  int P_enq = 1, known = 0;
+  // enqueue every chunk-pass (and table) whose inputs are enqueued, in chunk
+  // order per pass; `fresh`: passes may still start (the upload is in flight)
+  auto pump = [&](bool fresh) -> int {
+    for (bool progress = true; progress;) {
+      progress = false;
+      const int ready1 = iv ? static_cast<int>(job.filled) : nk;
+      while (next[1] < ready1) {
+        if (const int rc0 = launch(1, next[1]++)) return rc0;
+        progress = true;
+      }
+      for (int p = 1; p <= P; ++p) {
+        if (p >= 2) {
+          const int* have = iv ? next_st.data() : next.data();
+          while (next[p] < known && std::max(dhi[next[p]], next[p]) < have[p - 1] && (fresh || p <= P_enq)) {
+            if (const int rc0 = launch(p, next[p]++)) return rc0;
+            P_enq = std::max(P_enq, p);
+            progress = true;
+          }
+        }
+        if (iv && p < P && (fresh || p < P_enq)) {
+          while (next_st[p] < nk && next[p] > kst(next_st[p]) && next[p] > 0) {
+            if (const int rc0 = launch_st(p, next_st[p]++)) return rc0;
+            progress = true;
+          }
+        }
+      }
+    }
+    return SB_OK;
+  };
   int rc = SB_OK;
-  // pass 1 of every chunk waits only for its upload + validation
-  for (int k = 0; k < nk && !rc; ++k) rc = launch(1, k);
-  next[1] = nk;
-  int P_enq = 1;
-  // as each chunk lands: its neighbour range, then -- while later chunks are
-  // still uploading -- every chunk-pass whose inputs are all enqueued (in chunk
-  // order per pass).  Passes are started only while the upload is in flight:
+  if (!iv) {  // pass 1 of every chunk waits only for its upload + validation
+    for (int k = 0; k < nk && !rc; ++k) rc = launch(1, k);
+    next[1] = nk;
+  }
+  // as each chunk lands: its neighbour range (interval: its runs), then --
+  // while later chunks are still uploading -- every chunk-pass whose inputs
+  // are all enqueued.  Passes are started only while the upload is in flight:
   // that work fills time the GPU would otherwise wait; once the last chunk is
   // in, the started passes are completed and the rest run one by one, so no
   // pass beyond the converging one is computed unless it overlapped the upload.
@@ -530,32 +631,31 @@ static int pipelined_run(sb_hb* h, bool* done) {
       dlo[k] = chunk_of(r[0]);
       dhi[k] = chunk_of(r[1]);
     }
-    if (k == nk - 1) break;
-    for (int p = 2; p <= P && !rc; ++p) {
-      while (next[p] <= k && !rc && std::max(dhi[next[p]], next[p]) < next[p - 1]) {
-        rc = launch(p, next[p]++);
-        P_enq = std::max(P_enq, p);
-      }
-    }
+    known = k + 1;
+    if (iv) rc = rix_chunk(g, job, static_cast<size_t>(k));
+    if (!rc) rc = pump(k < nk - 1);
   }
   auto drain = [&] {  // every launched chunk-pass done (scratch / counters are shared)
-    for (int p = 0; p < P_enq; ++p) cudaStreamSynchronize(h->pstream[p]);
+    for (int p = 0; p < P; ++p) cudaStreamSynchronize(h->pstream[p]);
   };
+  if (!rc) rc = graph_wait(g);  // upload complete: a malformed stream is reported here
+  bool overflow = false;
+  if (iv && !rc) rc = rix_finish(g, job, &overflow);
+  if (rc || overflow) {
+    drain();
+    if (iv) rix_abort(g, job);
+    return rc;  // overflow: nothing was accounted; the caller runs the ordinary passes
+  }
+  rc = pump(false);  // complete the passes already started
   if (rc) {
     drain();
     return rc;
   }
-  rc = graph_wait(g);  // upload complete: a malformed stream is reported here
-  if (rc) {
-    drain();
-    return rc;
-  }
-  // complete the passes already started
-  for (int p = 2; p <= P_enq && !rc; ++p)
-    while (next[p] < nk && !rc) rc = launch(p, next[p]++);
-  if (rc) {
-    drain();
-    return rc;
+  if (iv) {  // the handed-over state steps with the table the longest run needs
+    if (const int rc0 = ensure_interval_ready(h)) {
+      drain();
+      return rc0;
+    }
   }
   // estimates in pass order (Alg. 1: union -> estimate -> accumulate -> test)
   int last = 0;
@@ -604,6 +704,8 @@ static int pipelined_run(sb_hb* h, bool* done) {
   // hand over to the two-plane stepping: d_plane[last & 1] holds pass `last`,
   // the other plane pass last - 1 (the "previous" registers), as after `last` steps
   for (int p = 0; p < P_enq; ++p) CK(cudaStreamWaitEvent(h->stream, h->pev_t[2 * p + 1], 0));
+  for (int p = 0; p + 1 < P && iv; ++p)  // tables built for passes that did not start
+    if (next_st[p + 1]) CK(cudaStreamWaitEvent(h->stream, h->sev[p * nk + next_st[p + 1] - 1], 0));
   for (int p = std::max(last - 1, 0); p <= last; ++p) {
     if (pl(p) != h->d_plane[p & 1]) CK(cudaMemcpyAsync(h->d_plane[p & 1], pl(p), plane, cudaMemcpyDeviceToDevice, h->stream));
     if (cg(p) != h->d_changed[p & 1]) CK(cudaMemcpyAsync(h->d_changed[p & 1], cg(p), g->n, cudaMemcpyDeviceToDevice, h->stream));
@@ -717,6 +819,7 @@ int sb_hb_run(sb_hb* h, uint32_t* iterations, int* converged) {
   if (!h) return fail(SB_EINVAL, "NULL handle");
   bool done = false;
   if (const int rc = pipelined_run(h, &done)) return rc;
+  if (const int rc = ensure_interval_ready(h)) return rc;
   if (!h->finished && !h->computed && !h->comm && !h->npeers && !h->g->pending && !h->g->broken &&
       !(h->flags & (SB_HB_INTERVAL | SB_HB_SKIP_UNCHANGED))) {
     if (const int rc = batched_run(h)) return rc;

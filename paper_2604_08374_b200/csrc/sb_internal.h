@@ -225,7 +225,8 @@ cudaError_t launch_exact_init(int p, const ExactArgs& a, cudaStream_t s);
 cudaError_t launch_exact_init1(int p, const ExactArgs& a, cudaStream_t s);
 cudaError_t launch_exact_count(int p, const ExactArgs& a, cudaStream_t s);
 cudaError_t launch_run_index(const RunIndexArgs& a, bool fill, cudaStream_t s);
-// run_off[i] = *total + exclusive prefix of run_count over items [i0, i1); *total += their sum.
+// run_off[i] = *total + exclusive prefix of run_count over items [i0, i1], i.e. run_off[i1] is the
+// end of item i1 - 1; *total += their sum.
 cudaError_t launch_run_offsets(const uint64_t* run_count, uint64_t* run_off, uint64_t i0, uint64_t i1,
                                unsigned long long* total, cudaStream_t s);
 cudaError_t launch_estimate(int p, int mode, const EstArgs& a, cudaStream_t s);

@@ -2310,7 +2310,10 @@ __global__ void __launch_bounds__(1024) run_offsets_kernel(const uint64_t* __res
     run += cnt[i];
   }
   __syncthreads();
-  if (threadIdx.x == blockDim.x - 1) *total = run;  // the last thread's span ends the chunk
+  if (threadIdx.x == blockDim.x - 1) {  // the last thread's span ends the chunk
+    *total = run;
+    off[i1] = run;  // the end of the chunk's last item (the next chunk's scan writes the same)
+  }
 }
 
 cudaError_t launch_run_offsets(const uint64_t* run_count, uint64_t* run_off, uint64_t i0, uint64_t i1,

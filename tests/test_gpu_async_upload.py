@@ -139,13 +139,16 @@ def _same_run(a, b):
     assert [x["changed_nodes"] for x in ka] == [x["changed_nodes"] for x in kb]
 
 
+@pytest.mark.parametrize("interval", [False, True], ids=["dense", "interval"])
 @pytest.mark.parametrize("depth", [None, 2, 3, 5])
 @pytest.mark.parametrize("p", [4, 6, 10, 12])
 @pytest.mark.parametrize("name,g", list(wave_graphs()), ids=[n for n, _ in wave_graphs()])
-def test_pipelined_first_run_bit_identical(name, g, p, depth):
+def test_pipelined_first_run_bit_identical(name, g, p, depth, interval):
+    """interval: the wavefront also builds the run index chunk by chunk and a
+    sparse table per pass and chunk."""
     ref = HyperBall(g, p, depth)
     ref.run()
-    hb = HyperBall(DeviceGraph(g, async_upload=True), p, depth, wavefront=True)
+    hb = HyperBall(DeviceGraph(g, async_upload=True), p, depth, wavefront=True, interval=interval)
     hb.run()
     _same_run(hb, ref)
     # the handle keeps working: reset and a second (device-resident) run
@@ -164,10 +167,11 @@ def test_pipelined_first_run_converges_inside_the_wavefront():
     for p in (4, 10):
         ref = HyperBall(g, p, None)
         ref.run()
-        hb = HyperBall(DeviceGraph(g, async_upload=True), p, None, wavefront=True)
-        hb.run()
-        assert ref.state().t <= 3
-        _same_run(hb, ref)
+        for interval in (False, True):
+            hb = HyperBall(DeviceGraph(g, async_upload=True), p, None, wavefront=True, interval=interval)
+            hb.run()
+            assert ref.state().t <= 3
+            _same_run(hb, ref)
 
 
 @pytest.mark.parametrize("sched", ["group", "items"])
@@ -199,10 +203,11 @@ def _corrupt_middle_row(kind):
     return CompressedCsr.from_arrays(offs, deg, new)
 
 
+@pytest.mark.parametrize("interval", [False, True], ids=["dense", "interval"])
 @pytest.mark.parametrize("kind", ["zero", "huge"])
-def test_pipelined_first_run_reports_malformed_stream(kind):
+def test_pipelined_first_run_reports_malformed_stream(kind, interval):
     g = _corrupt_middle_row(kind)
-    hb = HyperBall(DeviceGraph(g, async_upload=True), 10, None, wavefront=True)
+    hb = HyperBall(DeviceGraph(g, async_upload=True), 10, None, wavefront=True, interval=interval)
     with pytest.raises(RuntimeError):
         hb.run()
     ok = CompressedCsr.synth_grid(60, 70, 20, 2, 6, 3, 9 * 9)

@@ -483,13 +483,14 @@ def test_gpu_c3_matches_reference_hashes(c3, mode):
     assert _sha(st.sum_d) == gold["sum_d_sha256"] and _sha(st.sum_d2) == gold["sum_d2_sha256"]
 
 
-def test_gpu_c3_pipelined_async_run_matches_reference_hashes(c3):
+@pytest.mark.parametrize("interval", [False, True], ids=["dense", "interval"])
+def test_gpu_c3_pipelined_async_run_matches_reference_hashes(c3, interval):
     """The end-to-end call at C3: sb_graph_create_async + sb_hb_run, whose first
     run is the wavefront over the upload chunks (passes 2.. start while later
     chunks cross PCIe).  Final registers, the previous iteration's registers,
     c_t, sum_d, sum_d2 and every max increase equal the reference CPU path's."""
     gold = json.load(open(SCALE))["c3_p10"]
-    hb = HyperBall(DeviceGraph(c3, async_upload=True), HllParams(10), None)
+    hb = HyperBall(DeviceGraph(c3, async_upload=True), HllParams(10), None, interval=interval)
     hb.run()
     st = hb.state()
     assert st.t == gold["iterations"] and st.converged == gold["converged"]
