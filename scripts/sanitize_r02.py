@@ -1,8 +1,9 @@
 """Small runs of the round-2 union paths for compute-sanitizer (memcheck /
 racecheck / synccheck): the 16-node group path (forced `group` schedule) at
 p = 9 / 10 / 12 incl. skip mode and a 2-window id span, the per-node D16 feeder
-at p = 4 / 5 / 6 / 8 (paired p = 4 rows), the p >= 9 per-node items, and the
-asynchronous chunked upload feeding the group path.  Results are checked against
+at p = 4 / 5 / 6 / 8 (paired p = 4 rows), the p >= 9 per-node items, the
+asynchronous chunked upload feeding the group path, and the wavefront first
+run in dense and interval mode.  Results are checked against
 the plain schedule so a silent corruption also fails the run."""
 import os
 import sys
@@ -29,4 +30,12 @@ for graph in (g, wide):
 h = HyperBall(DeviceGraph(g, async_upload=True), 10, None, schedule="group")
 h.run()
 h.registers()
+# the wavefront first run (dense and interval: run index per chunk, tables per pass and chunk)
+w = CompressedCsr.synth_grid(150, 150, 30, 2, 6, 5, 6 * 6)
+for interval in (False, True):
+    ref = HyperBall(w, 10, None)
+    ref.run()
+    h = HyperBall(DeviceGraph(w, async_upload=True), 10, None, wavefront=True, interval=interval)
+    h.run()
+    assert np.array_equal(h.registers(), ref.registers()), interval
 print("ok")
