@@ -2,6 +2,7 @@
 // on-device grid build), their validation, work items and run index.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <memory>
 #include <string>
 #include <vector>
@@ -28,6 +29,7 @@ static void rix_free(RunIndexJob& j) {
 
 void rix_abort(sb_graph* g, RunIndexJob& j) {
   rix_free(j);
+  g->free_retired_runs();
   dfree(g->d_run_off);
   dfree(g->d_run_s);
   dfree(g->d_run_e);
@@ -86,9 +88,14 @@ static int rix_fill(sb_graph* g, RunIndexJob& j, size_t k_end) {  // fills chunk
   return SB_OK;
 }
 
-// Chunk k (after its validation): count + offsets; the first full-size chunk
-// sizes the run storage from its runs per stream byte (x 1.25 + slack) and
-// the chunks so far are written; later chunks are written at once.
+// Chunk k (after its validation): count + offsets, then the run total so far
+// is read back (the count of one chunk is short; the host is waiting for the
+// next chunk's copy anyway).  The first full-size chunk sizes the run storage
+// from the runs per stream byte so far (x 1.25 + slack) and the chunks so far
+// are written; a later chunk that would not fit grows it (runs written so far
+// are copied over on j.s, and the chunks' ready events re-recorded after the
+// copy, so a pass launched later reads the new storage only once it holds
+// them; the old storage stays alive for the passes already launched on it).
 int rix_chunk(sb_graph* g, RunIndexJob& j, size_t k) {
   sb::RunIndexArgs& a = j.a;
   const size_t nk = g->chunk_item.size() - 1;
@@ -100,18 +107,43 @@ int rix_chunk(sb_graph* g, RunIndexJob& j, size_t k) {
     CK(sb::launch_run_index(a, false, j.s));
     CK(sb::launch_run_offsets(j.d_cnt, g->d_run_off, a.item_begin, a.item_end, j.d_aux, j.s));
   }
-  if (!j.cap && (k >= j.probe || k + 1 == nk)) {
-    unsigned long long tot = 0;
-    CK(cudaMemcpyAsync(&tot, j.d_aux, 8, cudaMemcpyDeviceToHost, j.s));
-    CK(sync_stream(j.s));
-    const uint64_t bytes = std::max<uint64_t>(g->chunk_byte[k + 1], 1);
-    j.cap = static_cast<uint64_t>(static_cast<double>(tot) / static_cast<double>(bytes) *
-                                  static_cast<double>(g->stream_local) * 1.25) + g->n_items + 1024;
-    CK(dalloc(&g->d_run_s, j.cap * 4));
-    CK(dalloc(&g->d_run_e, j.cap * 4));
+  if (j.failed || (!j.cap && k < j.probe && k + 1 < nk)) return SB_OK;
+  unsigned long long tot = 0, err = 0;
+  CK(cudaMemcpyAsync(&tot, j.d_aux, 8, cudaMemcpyDeviceToHost, j.s));
+  CK(cudaMemcpyAsync(&err, g->d_err, 8, cudaMemcpyDeviceToHost, j.s));  // validation of chunks <= k is done
+  CK(sync_stream(j.s));
+  // a malformed chunk: the count pass stopped early, so the totals are garbage;
+  // write nothing more (the upload reports the error, the index is discarded).
+  // A valid stream never holds more runs than bytes.
+  if (err != ~0ull || tot > g->stream_local + g->n_items) {
+    j.failed = true;
+    return SB_OK;
   }
-  if (j.cap) return rix_fill(g, j, k + 1);
-  return SB_OK;
+  if (tot > j.cap) {
+    const uint64_t bytes = std::max<uint64_t>(g->chunk_byte[k + 1], 1);
+    uint64_t cap = static_cast<uint64_t>(static_cast<double>(tot) / static_cast<double>(bytes) *
+                                         static_cast<double>(g->stream_local) * 1.25) + g->n_items + 1024;
+    if (j.cap) cap = std::max<uint64_t>(cap, 2 * j.cap);
+    uint32_t* s = nullptr;
+    uint32_t* e = nullptr;
+    CK(dalloc(&s, cap * 4));
+    if (const cudaError_t ce = dalloc(&e, cap * 4)) {
+      dfree(s);
+      CK(ce);
+    }
+    if (j.cap) {  // a grown store: the runs written so far move over
+      CK(cudaMemcpyAsync(s, g->d_run_s, j.cap * 4, cudaMemcpyDeviceToDevice, j.s));
+      CK(cudaMemcpyAsync(e, g->d_run_e, j.cap * 4, cudaMemcpyDeviceToDevice, j.s));
+      for (size_t kk = 0; kk < j.filled; ++kk) CK(cudaEventRecord(j.ready[kk], j.s));
+      g->retired_runs.push_back(g->d_run_s);
+      g->retired_runs.push_back(g->d_run_e);
+      ++j.grown;
+    }
+    g->d_run_s = s;
+    g->d_run_e = e;
+    j.cap = cap;
+  }
+  return rix_fill(g, j, k + 1);
 }
 
 int rix_finish(sb_graph* g, RunIndexJob& j, bool* overflow) {
@@ -142,7 +174,10 @@ int build_run_index(sb_graph* g) {
       rix_abort(g, j);
       return rc;
     }
-    if (!overflow) return SB_OK;
+    if (!overflow) {
+      g->free_retired_runs();  // no pass reads the outgrown storage here
+      return SB_OK;
+    }
     rix_abort(g, j);  // storage estimate too small: rebuild with exact storage
   }
   if (const int rc = graph_wait(g)) return rc;
@@ -414,7 +449,9 @@ static int graph_create(uint64_t n, const uint64_t* offsets, const uint32_t* deg
   if (rc) return bail(rc);
   GK(cudaStreamCreateWithFlags(&g->up_stream, cudaStreamNonBlocking));
   GK(cudaStreamCreateWithFlags(&g->val_stream, cudaStreamNonBlocking));
-  const int K = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(16, g->n_local / 64)));
+  uint64_t kmax = 16;
+  if (const char* e = getenv("SB_UPLOAD_CHUNKS")) kmax = std::max(1, std::min(256, atoi(e)));  // A-B override
+  const int K = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(kmax, g->n_local / 64)));
   const uint64_t first = K > 1 ? g->stream_local / 64 : 0;
   g->chunk_node.assign(1, 0);
   for (int k = 1; k < K; ++k) {

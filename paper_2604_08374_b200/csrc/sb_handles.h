@@ -241,6 +241,12 @@ struct sb_graph {
   uint32_t* d_chunk_rng = nullptr;      // per chunk: min first / max last neighbour id (after val_ev[k])
   std::vector<uint64_t> chunk_node, chunk_tile, chunk_item, chunk_byte;
   std::vector<uint32_t> h_node_item;  // local node -> first work item (host copy)
+  // run storage outgrown while a wavefront still reads it (freed once its passes are done)
+  std::vector<uint32_t*> retired_runs;
+  void free_retired_runs() {
+    for (uint32_t*& r : retired_runs) dfree(r);
+    retired_runs.clear();
+  }
   ~sb_graph() {
     DeviceGuard dg(device);
     if (up_stream) cudaStreamSynchronize(up_stream);
@@ -250,6 +256,7 @@ struct sb_graph {
     dfree(d_node_lo); dfree(d_node_hi); dfree(d_chunk_rng);
     dfree(d_tile_node0); dfree(d_tile_q);
     dfree(d_run_off); dfree(d_run_s); dfree(d_run_e);
+    free_retired_runs();
     dfree(d_cell); dfree(d_comp); dfree(d_comp_sizes);
     for (auto e : val_ev) cudaEventDestroy(e);
     if (up_stream) cudaStreamDestroy(up_stream);
@@ -410,12 +417,14 @@ struct RunIndexJob {
   unsigned long long* d_aux = nullptr;  // [0] run total, [1] overflow flag
   uint64_t cap = 0;                     // run storage entries (0: not yet allocated)
   size_t probe = 0, filled = 0;         // chunks [0, filled) have their fill enqueued
+  int grown = 0;                        // times the run storage grew
+  bool failed = false;                  // a chunk failed validation: nothing more is written
   cudaStream_t s = nullptr;
   std::vector<cudaEvent_t> ready;
 };
 int rix_begin(sb_graph* g, RunIndexJob& j);
 int rix_chunk(sb_graph* g, RunIndexJob& j, size_t k);
-// After the upload: totals, last offset, max run; *overflow: the estimate was
-// too small (the index must be rebuilt: rix_abort + build_run_index).
+// After the upload: totals, last offset, max run; *overflow: the run storage
+// could not be allocated (the index must be rebuilt: rix_abort + build_run_index).
 int rix_finish(sb_graph* g, RunIndexJob& j, bool* overflow);
 void rix_abort(sb_graph* g, RunIndexJob& j);

@@ -541,6 +541,7 @@ static int pipelined_run(sb_hb* h, bool* done) {
       // the chunk itself (its items' partial rows and arrival counters are reused)
       const std::vector<cudaEvent_t>& dep = iv ? h->sev : h->pev;
       CK(cudaStreamWaitEvent(st, h->pev[(p - 2) * nk + k], 0));
+      if (iv) CK(cudaStreamWaitEvent(st, job.ready[k], 0));  // re-recorded if the run storage grew
       for (int j = dlo[k]; j <= dhi[k]; ++j) CK(cudaStreamWaitEvent(st, dep[(p - 2) * nk + j], 0));
     }
     const uint64_t n0 = g->chunk_node[k], n1 = g->chunk_node[k + 1];
@@ -565,6 +566,7 @@ static int pipelined_run(sb_hb* h, bool* done) {
         ia.run_off = g->d_run_off;
         ia.run_s = g->d_run_s;
         ia.run_e = g->d_run_e;
+        ia.run_cap = job.cap;  // the index is filled with estimated storage
         CK(sb::launch_union_interval(static_cast<int>(h->p), ia, st));
       } else {
         CK(sb::launch_union(static_cast<int>(h->p), false, u, st));
@@ -711,6 +713,7 @@ static int pipelined_run(sb_hb* h, bool* done) {
     if (cg(p) != h->d_changed[p & 1]) CK(cudaMemcpyAsync(h->d_changed[p & 1], cg(p), g->n, cudaMemcpyDeviceToDevice, h->stream));
   }
   CK(sync_stream(h->stream));
+  g->free_retired_runs();  // every launched pass is done
   h->latest = last & 1;
   *done = h->finished;
   return SB_OK;

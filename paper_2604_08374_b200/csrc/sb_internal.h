@@ -81,6 +81,8 @@ struct IntervalArgs {
   const uint64_t* run_off;     // per item: first run (n_items + 1)
   const uint32_t* run_s;       // run start ids
   const uint32_t* run_e;       // run end ids (inclusive)
+  uint64_t run_cap;            // != 0: runs stored below this (an index still being filled
+                               // with estimated storage: items past it were not written)
 };
 
 // Run index, derived once per graph from the LEB128 stream (run_index_kernel).

@@ -1615,7 +1615,11 @@ __device__ __forceinline__ void process_item_runs(const IntervalArgs& ia, uint64
   const uint64_t goff = static_cast<uint64_t>(slice) * G::SLICE_BYTES + static_cast<uint64_t>(gl) * G::GB;
   const uint8_t* curb = opaque(a.cur + goff);
   Grp acc = (item == first) ? IO::ld(curb + v * G::ROW) : grp_zero();
-  const uint64_t r0 = ia.run_off[item], r1 = ia.run_off[item + 1];
+  const uint64_t r0 = ia.run_off[item];
+  uint64_t r1 = ia.run_off[item + 1];
+  // an item the estimated storage could not hold was not written: its runs are
+  // skipped (the index overflowed, so the caller discards this pass and reruns it)
+  if (ia.run_cap && r1 > ia.run_cap) r1 = r0;
   const int K = ia.levels;
   for (uint64_t c = r0; c < r1; c += 32) {
     const int cnt = static_cast<int>(r1 - c < 32 ? r1 - c : 32);

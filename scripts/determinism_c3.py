@@ -1,5 +1,5 @@
 """Run-to-run determinism at C3: R full HyperBall runs per mode (dense tile
-schedule, dense warp schedule, skip-unchanged, interval, async upload), SHA-256
+schedule, dense warp schedule, skip-unchanged, interval, async upload, wavefront first run dense/interval), SHA-256
 of the final registers and of sum_d must be identical across all runs and modes."""
 import hashlib
 import json
@@ -35,6 +35,12 @@ hb = HyperBall(DeviceGraph(g, async_upload=True), 10, None)
 hb.run()
 hashes["async_upload"] = [(hashlib.sha256(hb.registers().tobytes()).hexdigest(),
                            hashlib.sha256(hb.state().sum_d.tobytes()).hexdigest())]
+for name, kw in {"async_wavefront": {}, "async_wavefront_interval": {"interval": True}}.items():
+    hb = HyperBall(DeviceGraph(g, async_upload=True), 10, None, wavefront=True, **kw)
+    hb.run()
+    hashes[name] = [(hashlib.sha256(hb.registers().tobytes()).hexdigest(),
+                     hashlib.sha256(hb.state().sum_d.tobytes()).hexdigest())]
+    del hb
 distinct = {h for v in hashes.values() for h in v}
 print(json.dumps(dict(runs_per_mode=R, modes=list(hashes), distinct_results=len(distinct),
                       deterministic=len(distinct) == 1, hash=sorted(distinct)[0]), indent=1))

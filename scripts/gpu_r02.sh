@@ -180,3 +180,44 @@ if [[ $what == fuzz ]]; then
   run timeout 3000 python -u scripts/parity_fuzz.py 2500 2026 > gpurun_out/parity_fuzz_2500_seed2026.json 2> gpurun_out/parity_fuzz.log
 fi
 done
+for what in "$@"; do
+if [[ $what == final_checks ]]; then
+  run timeout 3000 python -u scripts/parity_fuzz.py 2500 7 > gpurun_out/parity_fuzz_2500_seed7.json 2> gpurun_out/parity_fuzz7.log
+  run timeout 1500 python -u scripts/determinism_c3.py > gpurun_out/determinism_c3.json 2> gpurun_out/determinism_c3.log
+fi
+done
+for what in "$@"; do
+if [[ $what == chunksweep ]]; then
+  run timeout 1200 python -u scripts/chunk_sweep.py ${CHUNKS:-16 24 32 48 64} > gpurun_out/chunk_sweep.jsonl 2> gpurun_out/chunk_sweep.log
+fi
+done
+for what in "$@"; do
+if [[ $what == wavebug ]]; then
+  run timeout 600 compute-sanitizer --tool memcheck --show-backtrace device python -u scripts/wave_fuzz.py 1 0 43 30 34 3 7 186 1218590505 10 5 > gpurun_out/wavebug_memcheck.log 2>&1
+  run timeout 900 python -u scripts/wave_fuzz.py 400 11 > gpurun_out/wave_fuzz_400.log 2>&1
+fi
+done
+for what in "$@"; do
+if [[ $what == wavefix ]]; then
+  run timeout 900 python -m pytest -q -x tests/test_gpu_async_upload.py > gpurun_out/pytest_async.log 2>&1
+  run timeout 900 compute-sanitizer --tool memcheck python -m pytest -q -x tests/test_gpu_async_upload.py -k "overflow or fuzz_case" > gpurun_out/wavefix_memcheck.log 2>&1
+  run timeout 900 python -u scripts/wave_fuzz.py 400 11 > gpurun_out/wave_fuzz_400.log 2>&1
+  run timeout 3000 python -u scripts/parity_fuzz.py 2500 7 > gpurun_out/parity_fuzz_2500_seed7.json 2> gpurun_out/parity_fuzz7.log
+fi
+done
+for what in "$@"; do
+if [[ $what == e2e ]]; then
+  run timeout 600 python -u scripts/e2e_breakdown.py > gpurun_out/e2e_breakdown.txt 2>&1
+fi
+done
+for what in "$@"; do
+if [[ $what == wavebig ]]; then
+  run timeout 1500 python -u scripts/wave_fuzz.py 300 23 big > gpurun_out/wave_fuzz_big300.log 2>&1
+fi
+done
+for what in "$@"; do
+if [[ $what == e2e2 ]]; then
+  run timeout 600 python -u scripts/e2e_breakdown.py > gpurun_out/e2e_breakdown.txt 2>&1
+  run timeout 600 python -u scripts/e2e_breakdown.py > gpurun_out/e2e_breakdown_b.txt 2>&1
+fi
+done

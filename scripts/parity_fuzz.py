@@ -45,7 +45,8 @@ for case in range(n_cases):
         nxt = np.zeros_like(cur)
         c_cur, sd, sd2 = np.zeros(n), np.zeros(n), np.zeros(n)
         if mode == "async":
-            h = HyperBall(DeviceGraph(g, async_upload=True), p, depth, wavefront=True)
+            h = HyperBall(DeviceGraph(g, async_upload=True), p, depth, wavefront=True,
+                          interval=bool(rng.random() < 0.5))
             h.run()
             ref = O.hb_run(g, p, depth_limit=depth)
             st = h.state()

@@ -174,6 +174,51 @@ def test_pipelined_first_run_converges_inside_the_wavefront():
             _same_run(hb, ref)
 
 
+def _run_storage_overflow_graph():
+    """Single-run rows first, then rows of every other id: the run storage sized
+    from the first chunks' runs per byte is far too small for the rest."""
+    n, w = 6000, 200
+    adj = []
+    for v in range(n):
+        if v < 1000:
+            lo = min(max(v - w // 2, 0), n - w - 1)
+            adj.append([u for u in range(lo, lo + w + 1) if u != v])
+        else:
+            lo = min(max(v - w, 0), n - 2 * w - 1)
+            adj.append([u for u in range(lo, lo + 2 * w, 2) if u != v])
+    return CompressedCsr.from_adjacency(adj)
+
+
+@pytest.mark.parametrize("p", [6, 10])
+def test_pipelined_interval_run_storage_overflow(p):
+    """The wavefront's interval passes read a run index filled chunk by chunk
+    into storage sized from the first chunks' runs per byte; here the later
+    chunks need ~60x more, so the storage grows while passes already run on
+    the old one -- same result as the stepped run, also after a reset."""
+    g = _run_storage_overflow_graph()
+    ref = HyperBall(g, p, None)
+    ref.run()
+    hb = HyperBall(DeviceGraph(g, async_upload=True), p, None, wavefront=True, interval=True)
+    hb.run()
+    _same_run(hb, ref)
+    hb.reset()
+    hb.run()
+    _same_run(hb, ref)
+
+
+def test_pipelined_interval_fuzz_case_43x30():
+    """The randomised campaign's case (seed 7) whose wavefront read past the
+    estimated run storage (before it could grow)."""
+    g = CompressedCsr.synth_grid(43, 30, 34, 3, 7, 1218590505, 186)
+    for depth in (5, None):
+        ref = HyperBall(g, 10, depth)
+        ref.run()
+        for interval in (True, False):
+            hb = HyperBall(DeviceGraph(g, async_upload=True), 10, depth, wavefront=True, interval=interval)
+            hb.run()
+            _same_run(hb, ref)
+
+
 @pytest.mark.parametrize("sched", ["group", "items"])
 def test_pipelined_first_run_schedules(sched):
     g = CompressedCsr.synth_grid(150, 150, 30, 2, 6, 5, 6 * 6)
