@@ -221,3 +221,11 @@ if [[ $what == e2e2 ]]; then
   run timeout 600 python -u scripts/e2e_breakdown.py > gpurun_out/e2e_breakdown_b.txt 2>&1
 fi
 done
+for what in "$@"; do
+if [[ $what == wave3 ]]; then
+  run timeout 900 python -m pytest -q -x tests/test_gpu_async_upload.py > gpurun_out/pytest_async.log 2>&1
+  run timeout 900 compute-sanitizer --tool memcheck python -m pytest -q -x tests/test_gpu_async_upload.py -k "growth or overflow or fuzz_case" > gpurun_out/wavefix_memcheck.log 2>&1
+  run timeout 900 python -u scripts/wave_fuzz.py 400 11 > gpurun_out/wave_fuzz_400.log 2>&1
+  run timeout 1500 python -u scripts/wave_fuzz.py 300 23 big > gpurun_out/wave_fuzz_big300.log 2>&1
+fi
+done

@@ -11,7 +11,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 
 import oracle  # noqa: E402  (parity checker: test infrastructure)
-from paper_2604_08374_b200 import CompressedCsr, DeviceGraph, HyperBall  # noqa: E402
+from paper_2604_08374_b200 import CompressedCsr, DeviceGraph, ExactBfs, HyperBall  # noqa: E402
 
 O = oracle.reference() if oracle.reference_available() else oracle.port()
 n_cases, rng = int(sys.argv[1]), np.random.default_rng(int(sys.argv[2]))
@@ -55,4 +55,16 @@ for case in range(n_cases):
             print(json.dumps(dict(rows=rows, cols=cols, rects=rects, rmin=rmin, rmax=rmax, radius2=radius2,
                                   seed=gseed, p=p, depth=depth, interval=interval, n=g.n)), flush=True)
         del h
+    if case % 3 == 0:  # the run index's other users over an asynchronous upload
+        ra, rb = DeviceGraph(g, async_upload=True).local_metrics(), DeviceGraph(g).local_metrics()
+        ok = all(np.array_equal(ra[k], rb[k], equal_nan=ra[k].dtype.kind == "f") for k in rb)
+        xa, xb = ExactBfs(DeviceGraph(g, async_upload=True), depth, interval=True), ExactBfs(DeviceGraph(g), depth)
+        xa.run()
+        xb.run()
+        ea, eb = xa.result(), xb.result()
+        ok &= all(np.array_equal(ea[k], eb[k]) for k in ("sum_d", "sum_d2", "reach"))
+        if not ok:
+            bad += 1
+            print(json.dumps(dict(rows=rows, cols=cols, rects=rects, rmin=rmin, rmax=rmax, radius2=radius2,
+                                  seed=gseed, depth=depth, what="local/exact", n=g.n)), flush=True)
 print(json.dumps(dict(cases=n_cases, mismatches=bad)))

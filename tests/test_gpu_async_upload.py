@@ -206,6 +206,25 @@ def test_pipelined_interval_run_storage_overflow(p):
     _same_run(hb, ref)
 
 
+def test_async_run_index_growth_for_exact_and_local_metrics():
+    """The same uneven graph through the other users of the run index built
+    under an asynchronous upload (storage grown per chunk, no wavefront):
+    exact local metrics and the interval exact BFS equal the synchronous graph's."""
+    from paper_2604_08374_b200 import ExactBfs
+    g = _run_storage_overflow_graph()
+    ref_lm = DeviceGraph(g).local_metrics()
+    lm = DeviceGraph(g, async_upload=True).local_metrics()
+    for key in ref_lm:
+        assert np.array_equal(lm[key], ref_lm[key], equal_nan=lm[key].dtype.kind == "f"), key
+    ref = ExactBfs(DeviceGraph(g), 3)
+    ref.run()
+    x = ExactBfs(DeviceGraph(g, async_upload=True), 3, interval=True)
+    x.run()
+    ra, rb = x.result(), ref.result()
+    for key in ("sum_d", "sum_d2", "reach"):
+        assert np.array_equal(ra[key], rb[key]), key
+
+
 def test_pipelined_interval_fuzz_case_43x30():
     """The randomised campaign's case (seed 7) whose wavefront read past the
     estimated run storage (before it could grow)."""
