@@ -7,7 +7,8 @@ PKG      := paper_2604_08374_b200
 CSRC     := $(PKG)/csrc
 BUILD    := build
 CUDA_INC := $(dir $(shell which $(NVCC)))../include
-NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v --fmad=false
+NVEXTRA  ?=
+NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v --fmad=false $(NVEXTRA)
 CXXFLAGS := -O3 -std=c++17 -fPIC -Wall -ffp-contract=off -I$(CUDA_INC)
 LIB      := $(PKG)/libsieveball_cuda.so
 TOOL     := tools/sb_hyperball

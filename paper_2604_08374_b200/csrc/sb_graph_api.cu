@@ -449,8 +449,10 @@ static int graph_create(uint64_t n, const uint64_t* offsets, const uint32_t* deg
   if (rc) return bail(rc);
   GK(cudaStreamCreateWithFlags(&g->up_stream, cudaStreamNonBlocking));
   GK(cudaStreamCreateWithFlags(&g->val_stream, cudaStreamNonBlocking));
-  uint64_t kmax = 16;
-  if (const char* e = getenv("SB_UPLOAD_CHUNKS")) kmax = std::max(1, std::min(256, atoi(e)));  // A-B override
+  uint64_t kmax = 16;  // 16 / 24 / 32 / 48 / 64 measured: 16 is fastest at C3
+#ifdef SB_AB_UPLOAD_CHUNKS  // A-B builds only (make -B NVEXTRA=-DSB_AB_UPLOAD_CHUNKS): no switch in the product .so
+  if (const char* e = getenv("SB_UPLOAD_CHUNKS")) kmax = std::max(1, std::min(256, atoi(e)));
+#endif
   const int K = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(kmax, g->n_local / 64)));
   const uint64_t first = K > 1 ? g->stream_local / 64 : 0;
   g->chunk_node.assign(1, 0);

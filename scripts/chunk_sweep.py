@@ -1,6 +1,8 @@
 """A-B sweep of the asynchronous upload's chunk count (SB_UPLOAD_CHUNKS) at C3:
 end-to-end time of the wavefront first run (dense and interval), host CSR ->
-HBM -> run -> read-back, and the final registers' hash against a synchronous run."""
+HBM -> run -> read-back, and the final registers' hash against a synchronous run.
+Needs an A-B build (`make -B NVEXTRA=-DSB_AB_UPLOAD_CHUNKS`): the product library
+has no environment switch and always uses 16 chunks."""
 import hashlib
 import json
 import os

@@ -1,5 +1,5 @@
 """Run-to-run determinism at C3: R full HyperBall runs per mode (dense tile
-schedule, dense warp schedule, skip-unchanged, interval, async upload, wavefront first run dense/interval), SHA-256
+schedule, per-warp items and forced group schedules, skip-unchanged, interval, async upload, wavefront first run dense/interval), SHA-256
 of the final registers and of sum_d must be identical across all runs and modes."""
 import hashlib
 import json
@@ -25,12 +25,12 @@ for name, kw in modes.items():
                 hashlib.sha256(hb.state().sum_d.tobytes()).hexdigest()))
     hashes[name] = sorted(hs)
     del hb
-os.environ["SB_UNION_SCHEDULE"] = "warp"
-hb = HyperBall(dg, 10, None)
-hb.run()
-hashes["dense_warp_schedule"] = [(hashlib.sha256(hb.registers().tobytes()).hexdigest(),
-                                  hashlib.sha256(hb.state().sum_d.tobytes()).hexdigest())]
-del hb
+for sched in ("items", "group"):
+    hb = HyperBall(dg, 10, None, schedule=sched)
+    hb.run()
+    hashes[f"dense_{sched}_schedule"] = [(hashlib.sha256(hb.registers().tobytes()).hexdigest(),
+                                          hashlib.sha256(hb.state().sum_d.tobytes()).hexdigest())]
+    del hb
 hb = HyperBall(DeviceGraph(g, async_upload=True), 10, None)
 hb.run()
 hashes["async_upload"] = [(hashlib.sha256(hb.registers().tobytes()).hexdigest(),

@@ -188,6 +188,7 @@ fi
 done
 for what in "$@"; do
 if [[ $what == chunksweep ]]; then
+  # needs the A-B build: make -B NVEXTRA=-DSB_AB_UPLOAD_CHUNKS (the product .so always uses 16 chunks)
   run timeout 1200 python -u scripts/chunk_sweep.py ${CHUNKS:-16 24 32 48 64} > gpurun_out/chunk_sweep.jsonl 2> gpurun_out/chunk_sweep.log
 fi
 done
