@@ -230,3 +230,8 @@ if [[ $what == wave3 ]]; then
   run timeout 1500 python -u scripts/wave_fuzz.py 300 23 big > gpurun_out/wave_fuzz_big300.log 2>&1
 fi
 done
+for what in "$@"; do
+if [[ $what == fuzzbig ]]; then
+  run timeout 2400 python -u scripts/parity_fuzz.py 100 99 big > gpurun_out/parity_fuzz_big100_seed99.json 2> gpurun_out/parity_fuzz_big.log
+fi
+done

@@ -3,7 +3,9 @@ random p in [4, 16], random depth limit, random mode (dense / skip / interval /
 sharded / asynchronous upload with the wavefront first run) and schedule (auto /
 group / items), GPU vs the oracle after EVERY iteration (the wavefront run: its
 final state and every max increase); plus exact local metrics and the exact BFS
-on the same graph.  usage: python scripts/parity_fuzz.py [n_cases] [seed]
+on the same graph.  usage: python scripts/parity_fuzz.py [n_cases] [seed] [big]
+("big": 100-160 rows/cols, radius^2 20-400, p 8-12 -- graphs over the auto
+schedule's group-path threshold, so "auto" picks the 16-node group path)
 Prints one JSON summary (cases, failures with their parameters)."""
 import json
 import os
@@ -22,14 +24,24 @@ rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 12345)
 O = oracle.reference() if oracle.reference_available() else oracle.port()
 P = oracle.port()
 fails, done, t_start = [], 0, time.time()
+big = len(sys.argv) > 3 and sys.argv[3] == "big"
 for case in range(n_cases):
-    rows, cols = int(rng.integers(2, 60)), int(rng.integers(2, 60))
-    rects = int(rng.integers(0, rows * cols // 20 + 1))
-    rmin = int(rng.integers(1, 4))
-    rmax = rmin + int(rng.integers(0, 6))
-    radius2 = 0 if rng.random() < 0.4 else int(rng.integers(1, 200))
-    seed = int(rng.integers(1, 2**31))
-    p = int(rng.integers(4, 17)) if rng.random() < 0.5 else 10
+    if big:
+        rows, cols = int(rng.integers(100, 161)), int(rng.integers(100, 161))
+        rects = int(rng.integers(0, rows * cols // 40 + 1))
+        rmin = int(rng.integers(1, 4))
+        rmax = rmin + int(rng.integers(0, 8))
+        radius2 = int(rng.integers(20, 401))
+        seed = int(rng.integers(1, 2**31))
+        p = int(rng.integers(8, 13))
+    else:
+        rows, cols = int(rng.integers(2, 60)), int(rng.integers(2, 60))
+        rects = int(rng.integers(0, rows * cols // 20 + 1))
+        rmin = int(rng.integers(1, 4))
+        rmax = rmin + int(rng.integers(0, 6))
+        radius2 = 0 if rng.random() < 0.4 else int(rng.integers(1, 200))
+        seed = int(rng.integers(1, 2**31))
+        p = int(rng.integers(4, 17)) if rng.random() < 0.5 else 10
     depth = None if rng.random() < 0.5 else int(rng.integers(1, 6))
     mode = rng.choice(["dense", "skip", "interval", "shards", "async"])
     sched = str(rng.choice(["auto", "group", "items"])) if mode in ("dense", "skip") else "auto"
@@ -82,7 +94,7 @@ for case in range(n_cases):
                 break
             cur, nxt = nxt, cur
             c_prev, c_cur = c_cur, c_prev
-        if case % 4 == 0:  # widened passes on every 4th graph
+        if case % 4 == 0 and not big:  # widened passes on every 4th graph
             lm, ref = DeviceGraph(g).local_metrics(), P.local_metrics(g)
             for key in ref:
                 if not np.array_equal(lm[key], ref[key], equal_nan=lm[key].dtype.kind == "f"):
