@@ -232,6 +232,6 @@ fi
 done
 for what in "$@"; do
 if [[ $what == fuzzbig ]]; then
-  run timeout 2400 python -u scripts/parity_fuzz.py 100 99 big > gpurun_out/parity_fuzz_big100_seed99.json 2> gpurun_out/parity_fuzz_big.log
+  run timeout 2400 python -u scripts/parity_fuzz.py 1000 99 big > gpurun_out/parity_fuzz_big1000_seed99.json 2> gpurun_out/parity_fuzz_big.log
 fi
 done
