@@ -235,3 +235,8 @@ if [[ $what == fuzzbig ]]; then
   run timeout 2400 python -u scripts/parity_fuzz.py 1000 99 big > gpurun_out/parity_fuzz_big1000_seed99.json 2> gpurun_out/parity_fuzz_big.log
 fi
 done
+for what in "$@"; do
+if [[ $what == e2esmall ]]; then
+  run timeout 600 python -u scripts/e2e_small.py > gpurun_out/e2e_small.txt 2>&1
+fi
+done
