@@ -240,3 +240,9 @@ if [[ $what == e2esmall ]]; then
   run timeout 600 python -u scripts/e2e_small.py > gpurun_out/e2e_small.txt 2>&1
 fi
 done
+for what in "$@"; do
+if [[ $what == fuzzmore ]]; then
+  run timeout 1500 python -u scripts/parity_fuzz.py 2500 31337 > gpurun_out/parity_fuzz_2500_seed31337.json 2> gpurun_out/parity_fuzz31337.log
+  run timeout 1500 python -u scripts/parity_fuzz.py 1000 7 big > gpurun_out/parity_fuzz_big1000_seed7.json 2> gpurun_out/parity_fuzz_big7.log
+fi
+done
